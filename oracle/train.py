@@ -1,0 +1,110 @@
+"""Oracle-T: the small-MLP train step around the encoder -- TEST INFRASTRUCTURE.
+
+fp64 numpy, plain matrix products, no blocking or fusion.  Only tests/,
+smoke() and bench.py's CPU legs may import it.  Shares no code with the CUDA
+path.
+
+Readings:
+  R12  Adam, lr 0.01, beta = (0.9, 0.999), eps = 1e-8, bias
+       correction; loss = MSE over the GLOBAL batch,
+       dL/dy = 2 (y - target) / N_global.  Dense Adam: every parameter, every
+       step.
+  R13  precision points of the GPU train path, emulated here by rounding to
+       bf16 (round-to-nearest-even) exactly where the GPU rounds: the encoder
+       output x0, the bf16 shadow of every weight matrix, the hidden
+       activations h1, h2 after ReLU, and the back-propagated dz2, dz1 that
+       feed the tensor-core GEMMs.  Everything else is fp64 here (fp32 on the
+       GPU).
+  R15  ReLU hidden layers, identity output, biases present, widths e.g.
+       32 -> 64 -> 64 -> 1 (BASELINE.json configs[2]).
+
+Pins (tests/test_oracle_train.py): central finite differences of the fp64
+(unrounded) MLP, targets = forward -> zero loss and zero grads, zero
+weights -> bias-only output, Adam first-step closed form
+-lr * g / (|g| + eps), lr = 0 -> unchanged.
+"""
+from __future__ import annotations
+
+from typing import List, Sequence, Tuple
+
+import numpy as np
+
+
+def bf16_round(x: np.ndarray) -> np.ndarray:
+    """Round to the nearest bf16 (ties to even) via fp32, returned as fp64.
+    (fp32 -> bf16 is what the GPU's cvt.rn.bf16.f32 does.)"""
+    f = np.ascontiguousarray(np.asarray(x, dtype=np.float64).astype(np.float32))
+    b = f.view(np.uint32).astype(np.uint64)
+    b = (b + 0x7FFF + ((b >> 16) & 1)) & 0xFFFF0000
+    return b.astype(np.uint32).view(np.float32).astype(np.float64)
+
+
+def _id(x):
+    return np.asarray(x, dtype=np.float64)
+
+
+def mlp_forward(x0: np.ndarray, layers: Sequence[Tuple[np.ndarray, np.ndarray]], emulate_bf16: bool = True):
+    """Forward of the MLP: z_k = W_k a_{k-1} + b_k; a_k = ReLU(z_k) for
+    hidden layers, y = z_last.  Rows are samples; W is [out][in].
+    Returns (y [N], cache)."""
+    r = bf16_round if emulate_bf16 else _id
+    a = r(x0)
+    acts = [a]
+    zs = []
+    n_layers = len(layers)
+    for k, (W, b) in enumerate(layers):
+        Wk = r(W)
+        z = a @ Wk.T + _id(b)[None, :]
+        zs.append(z)
+        if k < n_layers - 1:
+            a = r(np.maximum(z, 0.0))
+            acts.append(a)
+    y = zs[-1][:, 0]
+    return y, (acts, zs)
+
+
+def mse_loss(y: np.ndarray, target: np.ndarray, n_global: int):
+    """MSE over the global batch (R12): loss = sum (y - t)^2 / N_global and
+    dL/dy = 2 (y - t) / N_global."""
+    d = _id(y) - _id(target)
+    return float(np.sum(d * d) / n_global), 2.0 * d / n_global
+
+
+def mlp_backward(dy: np.ndarray, layers, cache, emulate_bf16: bool = True):
+    """Analytic backward.  Returns (grads [(dW, db)...], dx0 [N][in]).
+    dz_k rounded to bf16 before it is used as a GEMM operand (R13) except
+    for the last layer's dy (the GPU keeps it in fp32 and uses CUDA cores
+    for the 64 -> 1 layer)."""
+    r = bf16_round if emulate_bf16 else _id
+    acts, zs = cache
+    n_layers = len(layers)
+    grads: List[Tuple[np.ndarray, np.ndarray]] = [None] * n_layers  # type: ignore
+    dz = _id(dy)[:, None]  # [N][1]
+    dx0 = None
+    for k in range(n_layers - 1, -1, -1):
+        W, _ = layers[k]
+        Wk = r(W)
+        a_prev = acts[k]
+        dz_op = dz if k == n_layers - 1 else r(dz)
+        dW = dz_op.T @ a_prev
+        db = dz.sum(axis=0)
+        grads[k] = (dW, db)
+        da = dz_op @ Wk
+        if k > 0:
+            dz = da * (zs[k - 1] > 0.0)
+        else:
+            dx0 = da
+    return grads, dx0
+
+
+def adam_step(p: np.ndarray, g: np.ndarray, m: np.ndarray, v: np.ndarray, step: int,
+              lr: float = 0.01, b1: float = 0.9, b2: float = 0.999, eps: float = 1e-8):
+    """Bias-corrected Adam (Kingma & Ba; P:489 lr; S:384 betas/eps), fp64.
+    step counts from 1.  Returns new (p, m, v)."""
+    p, g, m, v = _id(p), _id(g), _id(m), _id(v)
+    m = b1 * m + (1.0 - b1) * g
+    v = b2 * v + (1.0 - b2) * g * g
+    mhat = m / (1.0 - b1 ** step)
+    vhat = v / (1.0 - b2 ** step)
+    p = p - lr * mhat / (np.sqrt(vhat) + eps)
+    return p, m, v
