@@ -1,0 +1,376 @@
+#!/usr/bin/env python
+"""bench.py -- F-Hash encode fwd+bwd throughput on B200 (BASELINE.json metric).
+
+    python bench.py [--gpus N --steps K --warmup W] [--impl ours|reference]
+
+Workload (N=1 and per rank): BASELINE.json configs[1] ("cfg2"): L = 16
+levels, spatial 16..512 / temporal 2..64 geometric, F = 2 fp32, tables
+capped at 2^19 entries (levels 0-4 MPHF, 5-15 hashed), 2^20 uniform points
+per GPU, upstream grads N(0,1).  One step = zero dtable + encode fwd + encode
+bwd, all through the C ABI (libfhash.so).  Inputs are resident in HBM when
+the timed region starts; L2 is flushed (256 MiB write) between timed steps,
+outside the per-step events.
+
+Multi-GPU: the path shards by samples with no data-path collective (each
+rank runs its own 2^20 points, seed = rank): "scaling": "weak", value = all
+ranks' samples / max-over-ranks device time.
+
+The reference arm (--impl reference) times the CPU oracle (oracle/, plain
+C, fp64, 1 thread) on a bounded sample of the same workload -- the only
+other place this script executes oracle/.
+"""
+from __future__ import annotations
+
+import argparse
+import json
+import os
+import subprocess
+import sys
+import threading
+import time
+
+ROOT = os.path.dirname(os.path.abspath(__file__))
+sys.path.insert(0, ROOT)
+
+METRIC = "F-Hash encode fwd+bwd samples/s (whole job) and % of measured L2/HBM gather roofline"
+UNIT = "samples/s"
+
+
+def env_int(k, d):
+    try:
+        return int(os.environ.get(k, d))
+    except ValueError:
+        return d
+
+
+def load_peaks():
+    p = os.path.join(ROOT, "MEASURED_PEAKS.json")
+    if os.path.exists(p):
+        with open(p) as f:
+            d = json.load(f)
+        return float(d["hbm_gbs"]), "measured (MEASURED_PEAKS.json hbm_gbs)"
+    return 6650.0, "fallback (B200_PROFILING.md 6.65 TB/s)"
+
+
+def load_ncu_traffic():
+    """Per-launch DRAM bytes of our kernels from the committed ncu summary."""
+    p = os.path.join(ROOT, "profiles", "ncu_summary.json")
+    if not os.path.exists(p):
+        return {}
+    with open(p) as f:
+        return json.load(f).get("dram_bytes_per_launch", {})
+
+
+class ClockSampler:
+    """nvidia-smi clocks / throttle reasons sampled during the timed region."""
+    Q = ("clocks.sm,clocks.max.sm,clocks_event_reasons.hw_slowdown,clocks_event_reasons.hw_thermal_slowdown,"
+         "clocks_event_reasons.sw_thermal_slowdown,clocks_event_reasons.sw_power_cap")
+
+    def __init__(self, index):
+        self.index = index
+        self.proc = None
+
+    def __enter__(self):
+        try:
+            self.proc = subprocess.Popen(["nvidia-smi", f"--id={self.index}", f"--query-gpu={self.Q}",
+                                          "--format=csv,noheader,nounits", "-lms", "100"],
+                                         stdout=subprocess.PIPE, stderr=subprocess.DEVNULL, text=True)
+        except OSError:
+            self.proc = None
+        return self
+
+    def __exit__(self, *a):
+        self.rows = []
+        if self.proc is None:
+            return
+        time.sleep(0.25)
+        self.proc.terminate()
+        out, _ = self.proc.communicate(timeout=10)
+        for line in out.strip().splitlines():
+            parts = [x.strip() for x in line.split(",")]
+            if len(parts) == 6:
+                self.rows.append(parts)
+
+    def summary(self):
+        if not getattr(self, "rows", None):
+            return {"sm_mhz": None, "sm_max_mhz": None, "reasons": ["unavailable"], "samples": 0}
+        sm = sorted(float(r[0]) for r in self.rows)
+        names = ["hw_slowdown", "hw_thermal_slowdown", "sw_thermal_slowdown", "sw_power_cap"]
+        reasons = sorted({names[i] for r in self.rows for i in range(4) if r[2 + i].lower() == "active"})
+        return {"sm_mhz": sm[len(sm) // 2], "sm_max_mhz": float(self.rows[0][1]), "reasons": reasons,
+                "samples": len(sm)}
+
+
+# ------------------------------------------------------------------ reference
+def run_reference(args, rank, world):
+    """The CPU oracle, as it stands, on a bounded sample of the same workload."""
+    if rank != 0:
+        return
+    import numpy as np
+    import oracle
+    import workloads as W
+    cfg = W.CFG2
+    n_sample = 1 << 15
+    case = W.encode_case(cfg, n_sample, seed=0)
+    lv = oracle.Levels(cfg.levels, cfg.cap)
+    table64 = case.table.astype(np.float64)
+
+    def step():
+        lv.forward(case.coords, table64)
+        lv.backward(case.coords, case.dout, cfg.F)
+
+    for _ in range(args.warmup):
+        step()
+    t0 = time.perf_counter()
+    for _ in range(args.steps):
+        step()
+    dt = time.perf_counter() - t0
+    value = n_sample * args.steps / dt
+    sample = f"{n_sample} of the 2^20 cfg2 points per step (full 6.3M-entry tables), fwd+bwd, fp64 C oracle"
+    line = {
+        "impl": "reference", "metric": METRIC, "value": value, "unit": UNIT, "n_gpus": world,
+        "steps": args.steps, "warmup": args.warmup, "ms_per_step": dt * 1e3 / args.steps,
+        "higher_is_better": True, "scaling": "weak", "vs_baseline": None, "dtype": "f64", "data": "synthetic",
+        "config": config_block(cfg, W.N_CFG2, world),
+        "cpu_baseline": {"value": value, "unit": UNIT, "cores": 1, "kind": "oracle", "sample": sample},
+        "e2e": {"value": value, "unit": UNIT, "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0},
+    }
+    print(json.dumps(line), flush=True)
+
+
+def config_block(cfg, N, world):
+    return {"workload": "cfg2: BASELINE.json configs[1] encode-only fwd+bwd", "points_per_gpu": N,
+            "global_points": N * world, "levels": cfg.L, "F": cfg.F, "table_dtype": cfg.table_dtype,
+            "cap": cfg.cap, "parallelism": f"replicas x{world} (sample-sharded, no collective)",
+            "l2": "flushed between timed steps (256 MiB write, outside the step events)"}
+
+
+# ------------------------------------------------------------------ ours
+def cpu_baseline(cfg, case_coords, case_table, case_dout):
+    import numpy as np
+    import oracle
+    n = 1 << 19
+    lv = oracle.Levels(cfg.levels, cfg.cap)
+    t64 = case_table.astype(np.float64)
+    t0 = time.perf_counter()
+    lv.forward(case_coords[:n], t64)
+    lv.backward(case_coords[:n], case_dout[:n], cfg.F)
+    dt = time.perf_counter() - t0
+    return {"value": n / dt, "unit": UNIT, "cores": 1, "kind": "oracle",
+            "sample": f"first 2^19 of the 2^20 cfg2 points, fwd+bwd over the full tables, fp64 C, 1 thread, "
+                      f"{dt:.1f} s"}
+
+
+def microbench_roofline(fh, torch, enc, cfg, N, stream, hbm_peak):
+    """§8(d): the measured ceiling of the encode's access shape.  Per level
+    l, random x-pair gathers / vector reds over a T_l-entry buffer (same
+    entry width, 8 pairs per thread) give a corner rate; streaming bytes go
+    at the measured copy bandwidth.  t_roof = N * sum_l 16/rate_l + stream/BW."""
+    F = cfg.F
+    eb = F * 4
+    n_thr = 1 << 20
+    sink = torch.empty(n_thr, device="cuda")
+    ev0, ev1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+
+    def timeit(fn, reps=3):
+        best = 1e9
+        for _ in range(reps):
+            ev0.record(stream)
+            fn()
+            ev1.record(stream)
+            ev1.synchronize()
+            best = min(best, ev0.elapsed_time(ev1) / 1e3)
+        return best
+
+    # HBM copy ceiling with our own kernel (1 GiB -> 1 GiB)
+    nb = 1 << 30
+    a = torch.empty(nb, dtype=torch.uint8, device="cuda")
+    b = torch.empty(nb, dtype=torch.uint8, device="cuda")
+    t_copy = timeit(lambda: fh.bench_copy(b, a, nb, stream))
+    bw_copy = 2 * nb / t_copy
+    del a, b
+    g_rate, r_rate, g_split, r_split = [], [], [], []
+    for l in range(cfg.L):
+        T = enc.level_info(l)["table_size"]
+        buf = torch.zeros((T, F), device="cuda")
+        fh.bench_gather(buf, T, eb, n_thr, sink, mode=1, seed=l, stream=stream)
+        # mode 1: one aligned access per x-pair = the minimum-sector shape
+        tg = timeit(lambda: fh.bench_gather(buf, T, eb, n_thr, sink, mode=1, seed=l, stream=stream))
+        tr = timeit(lambda: fh.bench_red(buf, T, eb, n_thr, mode=1, seed=l, stream=stream))
+        g_rate.append(16 * n_thr / tg)   # corners (2 per pair access) per second
+        r_rate.append(16 * n_thr / tr)
+        # mode 0 (two entry-wide accesses per pair), reported for context
+        g_split.append(16 * n_thr / timeit(lambda: fh.bench_gather(buf, T, eb, n_thr, sink, mode=0, seed=l,
+                                                                   stream=stream)))
+        r_split.append(16 * n_thr / timeit(lambda: fh.bench_red(buf, T, eb, n_thr, mode=0, seed=l, stream=stream)))
+        del buf
+    stream_fwd = N * (16 + cfg.L * F * 4)
+    stream_bwd = N * (16 + cfg.L * F * 4)
+    t_fwd = sum(N * 16 / g for g in g_rate) + stream_fwd / bw_copy
+    t_bwd = sum(N * 16 / r for r in r_rate) + stream_bwd / bw_copy
+    return {
+        "t_roof_fwd_ms": t_fwd * 1e3, "t_roof_bwd_ms": t_bwd * 1e3,
+        "copy_gbs": bw_copy / 1e9, "hbm_peak_gbs": hbm_peak,
+        "gather_corner_rate_G_per_s": [round(g / 1e9, 2) for g in g_rate],
+        "red_corner_rate_G_per_s": [round(r / 1e9, 2) for r in r_rate],
+        "split_gather_corner_rate_G_per_s": [round(g / 1e9, 2) for g in g_split],
+        "split_red_corner_rate_G_per_s": [round(r / 1e9, 2) for r in r_split],
+    }
+
+
+def run_ours(args, rank, local_rank, world):
+    import numpy as np
+    import torch
+    import workloads as W
+    from paper_2507_03836_b200 import fhash as fh
+
+    torch.cuda.set_device(local_rank)
+    dist = None
+    if world > 1:
+        import torch.distributed as dist
+        dist.init_process_group("nccl", device_id=torch.device("cuda", local_rank))
+    cfg = W.CFG2
+    N = W.N_CFG2
+    enc = fh.Encoder(cfg.levels, cfg.F, cfg.table_dtype, cfg.cap)
+    case = W.encode_case(cfg, N, seed=rank)
+    coords = torch.from_numpy(case.coords).cuda()
+    table = torch.from_numpy(case.table).cuda()
+    dout = torch.from_numpy(case.dout).cuda()
+    out = torch.empty((N, cfg.L * cfg.F), device="cuda")
+    dtable = torch.empty((enc.entries, cfg.F), device="cuda")
+    flush = torch.empty(256 << 20, dtype=torch.uint8, device="cuda")
+    stream = torch.cuda.current_stream()
+
+    def step():
+        enc.zero_grad(dtable, stream)
+        enc.fwd(coords, table, out, stream=stream)
+        enc.bwd(coords, dout, dtable, stream=stream)
+
+    for _ in range(max(args.warmup, 3)):
+        flush.fill_(1)
+        step()
+    if enc.status_sync(stream) != fh.FH_OK:
+        raise RuntimeError("domain flag set on synthetic inputs")
+
+    K = args.steps
+    ev = [[torch.cuda.Event(enable_timing=True) for _ in range(4)] for _ in range(K)]
+    if dist:
+        dist.barrier()
+    torch.cuda.synchronize()
+    with ClockSampler(local_rank) as clk:
+        for k in range(K):
+            flush.fill_(k & 0xFF)
+            e = ev[k]
+            e[0].record(stream)
+            enc.zero_grad(dtable, stream)
+            e[1].record(stream)
+            enc.fwd(coords, table, out, stream=stream)
+            e[2].record(stream)
+            enc.bwd(coords, dout, dtable, stream=stream)
+            e[3].record(stream)
+        torch.cuda.synchronize()
+    if dist:
+        dist.barrier()
+    zero_ms = sum(e[0].elapsed_time(e[1]) for e in ev) / K
+    fwd_ms = sum(e[1].elapsed_time(e[2]) for e in ev) / K
+    bwd_ms = sum(e[2].elapsed_time(e[3]) for e in ev) / K
+    step_ms = sum(e[0].elapsed_time(e[3]) for e in ev) / K
+    total_s = step_ms * K / 1e3
+    if dist:
+        t = torch.tensor([total_s], device="cuda", dtype=torch.float64)
+        dist.all_reduce(t, op=dist.ReduceOp.MAX)
+        total_s = float(t.item())
+    status = enc.status_sync(stream)
+    if status != fh.FH_OK:
+        raise RuntimeError("domain flag set during timed region")
+    value = N * world * K / total_s
+
+    # e2e: the same step through the C ABI from pinned HOST buffers, copies
+    # inside the timed region (fh_encode_step_host).
+    coords_h = torch.from_numpy(case.coords).pin_memory()
+    dout_h = torch.from_numpy(case.dout).pin_memory()
+    out_h = torch.empty((N, cfg.L * cfg.F)).pin_memory()
+    dtable_h = torch.empty((enc.entries, cfg.F)).pin_memory()
+    ke = max(3, min(K, 10))
+    for _ in range(2):
+        enc.step_host(coords_h, dout_h, table, coords, dout, out, dtable, out_h, dtable_h, stream)
+    if dist:
+        dist.barrier()
+    torch.cuda.synchronize()
+    e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    e0.record(stream)
+    for _ in range(ke):
+        enc.step_host(coords_h, dout_h, table, coords, dout, out, dtable, out_h, dtable_h, stream)
+    e1.record(stream)
+    torch.cuda.synchronize()
+    e2e_s = e0.elapsed_time(e1) / 1e3
+    if dist:
+        t = torch.tensor([e2e_s], device="cuda", dtype=torch.float64)
+        dist.all_reduce(t, op=dist.ReduceOp.MAX)
+        e2e_s = float(t.item())
+    e2e = {"value": N * world * ke / e2e_s, "unit": UNIT, "h2d_bytes_per_step": N * 16 + N * cfg.L * cfg.F * 4,
+           "d2h_bytes_per_step": N * cfg.L * cfg.F * 4 + enc.entries * cfg.F * 4, "steps": ke,
+           "api": "fh_encode_step_host (pinned host in/out)"}
+
+    if rank != 0:
+        if dist:
+            dist.destroy_process_group()
+        return
+
+    hbm_peak, peak_src = load_peaks()
+    mb = microbench_roofline(fh, torch, enc, cfg, N, stream, hbm_peak)
+    # Contract roofline of the dominant kernel: algorithmic bytes / launch time.
+    LF4 = cfg.L * cfg.F * 4
+    alg = {"fwd": N * (16 * cfg.L * cfg.F * 4 + 16 + LF4), "bwd": N * (16 * cfg.L * cfg.F * 4 + 16 + LF4)}
+    dom = "bwd" if bwd_ms >= fwd_ms else "fwd"
+    dom_ms = bwd_ms if dom == "bwd" else fwd_ms
+    achieved = alg[dom] / (dom_ms / 1e3) / 1e9
+    traffic = load_ncu_traffic().get(dom)
+    roofline = {"bound": "hbm", "kernel": f"fh::{dom}_kernel<2>", "achieved": achieved, "peak": hbm_peak,
+                "unit": "GB/s", "frac": achieved / hbm_peak, "traffic": traffic,
+                "peak_source": peak_src,
+                "algorithmic_bytes_per_launch": alg[dom],
+                "note": "useful gather (or red) payload 16*L*F*4 B + coords 16 B + out/dout L*F*4 B per sample; "
+                        "the tables are L2-resident, so the gather roofline below is the binding ceiling"}
+    t_roof = mb["t_roof_fwd_ms"] + mb["t_roof_bwd_ms"]
+    gather_roofline = {
+        "bound": "l2-gather/red (measured microbenchmark, same access shape, per-level footprint)",
+        "t_roof_ms": t_roof, "t_measured_ms": fwd_ms + bwd_ms,
+        "frac": t_roof / (fwd_ms + bwd_ms),
+        "fwd_frac": mb["t_roof_fwd_ms"] / fwd_ms, "bwd_frac": mb["t_roof_bwd_ms"] / bwd_ms, **mb,
+    }
+    cpu = None
+    if world == 1 and not args.no_cpu_baseline:
+        cpu = cpu_baseline(cfg, case.coords, case.table, case.dout)
+    line = {
+        "metric": METRIC, "value": value, "unit": UNIT, "n_gpus": world, "steps": K, "warmup": max(args.warmup, 3),
+        "ms_per_step": total_s * 1e3 / K, "higher_is_better": True, "scaling": "weak", "vs_baseline": None,
+        "dtype": "f32", "data": "synthetic", "config": config_block(cfg, N, world),
+        "kernels_ms": {"zero_grad": zero_ms, "encode_fwd": fwd_ms, "encode_bwd": bwd_ms, "step": step_ms},
+        "roofline": roofline, "gather_roofline": gather_roofline, "cpu_baseline": cpu, "e2e": e2e,
+        "gpu_launches": 2 * K, "clocks": clk.summary(),
+    }
+    print(json.dumps(line), flush=True)
+    if dist:
+        dist.destroy_process_group()
+
+
+def main():
+    ap = argparse.ArgumentParser()
+    ap.add_argument("--gpus", type=int, default=1)
+    ap.add_argument("--steps", type=int, default=20)
+    ap.add_argument("--warmup", type=int, default=5)
+    ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
+    ap.add_argument("--no-cpu-baseline", action="store_true")
+    args = ap.parse_args()
+    rank = env_int("RANK", 0)
+    local_rank = env_int("LOCAL_RANK", 0)
+    world = env_int("WORLD_SIZE", 1)
+    if args.impl == "reference":
+        run_reference(args, rank, world)
+    else:
+        run_ours(args, rank, local_rank, world)
+
+
+if __name__ == "__main__":
+    main()

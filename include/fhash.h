@@ -1,0 +1,183 @@
+/*
+ * fhash.h -- C ABI of libfhash.so, the B200 (sm_100a) hot path of F-Hash
+ * (arXiv 2507.03836): the multi-resolution Tesseract (x,y,z,t) embedding
+ * encode through the paper's minimal perfect hash, forward and backward, and
+ * the small-MLP train step that uses it.
+ *
+ * Citations: "P:n" = the paper text line n with its section /
+ * equation; "S:n" = SPEC.md line n.  Readings R1..R18 of ambiguous passages
+ * are listed in DESIGN.md §3.
+ *
+ * Conventions shared by every entry point
+ *   - Plain pointers and sizes only.  "device" pointers are CUDA global
+ *     memory on the current device, allocated and OWNED BY THE CALLER; the
+ *     library owns only the opaque host handles it returns.
+ *   - Every call that takes a stream is stream-ordered on it and does NOT
+ *     synchronise (except fh_status_sync).  stream may be NULL (legacy
+ *     default stream).
+ *   - Errors: host-side validation returns synchronously (FH_E_ARG,
+ *     FH_E_RANGE, FH_E_STATE); launch failures return FH_E_CUDA.  Nothing
+ *     aborts and nothing throws across the ABI.  fh_last_error() returns a
+ *     thread-local message for the last failing call on the calling thread.
+ *   - Coordinates: [N][4] float32 = (x, y, z, t) in the ABI domain [0,1]
+ *     (R2: a caller in the paper's [-1,1] domain, maps q -> (q+1)/2).
+ *     16-byte aligned.  Out-of-domain or NaN coordinates are clamped to
+ *     [0,1] (NaN -> 0) and set a sticky per-encoder device flag that
+ *     fh_status_sync reports as FH_E_DOMAIN; they never fault.
+ *   - Tables: one packed buffer [sum_l T_l][F], level-major in the order
+ *     given to fh_build_levels, the F features of an entry contiguous.
+ */
+#ifndef FHASH_H_
+#define FHASH_H_
+
+#include <stddef.h>
+#include <stdint.h>
+
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+typedef enum {
+    FH_OK = 0,
+    FH_E_ARG = -1,       /* bad argument: null/misaligned pointer, L, R, F, dtype */
+    FH_E_RANGE = -2,     /* sizes overflow the supported range */
+    FH_E_DOMAIN = -3,    /* a kernel saw out-of-domain / NaN coordinates (clamped) */
+    FH_E_CUDA = -4,      /* CUDA launch or runtime error */
+    FH_E_DIVERGED = -5,  /* non-finite loss in a train step */
+    FH_E_STATE = -6      /* handle in the wrong state / wrong device */
+} fh_status;
+
+typedef enum { FH_F32 = 0, FH_F16 = 1, FH_BF16 = 2 } fh_dtype;
+
+/* Opaque CUDA stream (binary-compatible with cudaStream_t). */
+typedef struct CUstream_st *fh_stream;
+
+#define FH_MAX_LEVELS 32
+
+/* Vertices per axis of one level, order (x, y, z, t); each >= 2.
+ * R1: "Res" is the VERTEX count -- Eq. 9 is bijective only when
+ * 0 <= x < Res_x; confirmed by the Table-3 parameter counts. */
+typedef struct { uint32_t res[4]; } fh_level_res;
+
+typedef struct {
+    uint32_t res[4];      /* x, y, z, t vertex counts */
+    uint64_t corners;     /* C_l = prod res (64-bit) */
+    uint64_t table_size;  /* T_l: = C_l (bijective, Eq. 9) or the cap (hashed, R5) */
+    uint32_t hashed;      /* 1 if C_l > cap */
+    uint32_t reserved;
+    uint64_t offset;      /* first entry of this level in the packed table */
+} fh_level_info;
+
+typedef struct fh_encoder_s *fh_encoder;
+
+/* ---------------------------------------------------------------- a1 ---
+ * fh_fold_schedule -- Eqs. 4-8 (§3.2.1) and the temporal
+ * analogue (§3.2.2).
+ *   Level 1 = native (S_x, S_y, S_z, n_t) (Eq. 4); per-axis level count
+ *   L_a = ceil(log_fold S_a) (Eq. 5, integer: least L with fold^L >= S_a);
+ *   L_s = max over the four axes (Eq. 6, R9); Res^l = ceil(Res^{l-1}/fold)
+ *   while Res^{l-1} > fold, else Tail = 2, for l = 2..L_s (Eqs. 7-8, R8).
+ * out: caller array of *L_inout entries; on success *L_inout = L_s and out
+ * holds the levels in PAPER ORDER (finest first).
+ * Errors: FH_E_ARG if any S < 2, n_t < 2, fold < 2 or a NULL pointer;
+ * FH_E_RANGE if L_s exceeds the capacity *L_inout (which is set to L_s). */
+fh_status fh_fold_schedule(const uint32_t S_xyz[3], uint32_t n_t, uint32_t fold,
+                           fh_level_res *out, int *L_inout);
+
+/* ---------------------------------------------------------------- a1 ---
+ * fh_build_levels -- the per-level tables (D1/D2: "hash tables ... scaling
+ * their sizes proportionally with the embedding grid size").
+ *   res[L] (1 <= L <= 32): levels in OUTPUT order (R11: the concatenation
+ *   order of the encoded vector).  F in {1,2,4,8} features per entry.
+ *   table_dtype: FH_F32 or FH_F16 (the dtype of the table passed to the
+ *   encode calls).  cap: 0 = uncapped (pure MPHF); otherwise a power
+ *   of two; a level with C_l > cap becomes a hashed level of T_l = cap
+ *   entries (R5; the paper never caps).
+ * Errors: FH_E_ARG (L, F, R < 2, cap not a power of two, dtype);
+ * FH_E_RANGE if sum_l T_l * F >= 2^32.  On success *out owns a host handle
+ * (no device memory until the first encode call, which allocates a 16-byte
+ * status word on the current device). */
+fh_status fh_build_levels(const fh_level_res *res, int L, int F, fh_dtype table_dtype,
+                          uint64_t cap, fh_encoder *out);
+
+fh_status fh_level_info_get(fh_encoder enc, int l, fh_level_info *out);
+int       fh_num_levels(fh_encoder enc);
+int       fh_feature_dim(fh_encoder enc);
+uint64_t  fh_table_entries(fh_encoder enc);   /* sum_l T_l */
+uint64_t  fh_param_count(fh_encoder enc);     /* sum_l T_l * F */
+void      fh_encoder_destroy(fh_encoder enc);
+
+/* ------------------------------------------------------------ a2..a7 ---
+ * fh_encode_fwd -- steps 1-4 of §3.2.4 for every sample and
+ * level, concatenated:
+ *   per axis s = fp32(p * (R-1)), i = clamp(floor s, 0, R-2), w = s - i
+ *   (R2; steps 1-2); the 16 corners c = bx+2by+4bz+8bt (R3)
+ *   map through Eq. 9 ("a single look-up ... through simple
+ *   shifting") or the capped hash (R5) to entries of the level's
+ *   table; out = quadrilinear blend, trilinear per time slice (Eqs. 10-11)
+ *   then linear in t (Eq. 12, R6).
+ * coords [N][4] f32 (device); table [sum T][F] of the encoder's table_dtype
+ * (device, 32-byte aligned: corners are fetched as 32-byte blocks); out [N][L*F] of out_dtype FH_F32 or FH_BF16
+ * (device), row n = (level 0 features, level 1 features, ...).
+ * N = 0 is a no-op.  Errors: FH_E_ARG (NULL/misaligned, dtype), FH_E_CUDA. */
+fh_status fh_encode_fwd(fh_encoder enc, const float *coords, int64_t N, const void *table,
+                        void *out, fh_dtype out_dtype, fh_stream stream);
+
+/* ---------------------------------------------------------------- a10 --
+ * fh_encode_bwd -- adjoint of fh_encode_fwd ("gradient
+ * computation ... during backpropagation"):
+ *   dtable[idx_c][f] += W_c * dout[n][l*F+f]  for every n, l, corner c,
+ * with W_c the quadrilinear weight of corner c.  dout [N][L*F] f32 (device);
+ * dtable [sum T][F] f32 (device), ACCUMULATED INTO (the caller zeroes it).
+ * Order of the floating-point sums is unspecified (atomics).
+ * Errors: FH_E_ARG, FH_E_CUDA. */
+fh_status fh_encode_bwd(fh_encoder enc, const float *coords, int64_t N, const float *dout,
+                        float *dtable, fh_stream stream);
+
+/* ---------------------------------------------------------------- a4 ---
+ * fh_encode_indices -- the corner indices alone (steps 1-3), for parity:
+ * idx [N][L][16] uint32 global entry indices (level offset included),
+ * corner order R3; w [N][L][16] f32 corner weights (may be NULL). */
+fh_status fh_encode_indices(fh_encoder enc, const float *coords, int64_t N, uint32_t *idx,
+                            float *w, fh_stream stream);
+
+/* fh_zero_grad -- dtable [sum T][F] f32 (device) := 0, stream-ordered
+ * (cudaMemsetAsync).  Errors: FH_E_ARG (NULL), FH_E_CUDA. */
+fh_status fh_zero_grad(fh_encoder enc, float *dtable, fh_stream stream);
+
+/* fh_encode_fwd_bwd -- one encode step on device buffers, the unit
+ * bench.py times for BASELINE.json configs[1]: if zero_dtable, dtable is
+ * zeroed (cudaMemsetAsync) first; then fh_encode_fwd (out, out_dtype) and
+ * fh_encode_bwd (dout -> dtable).  Arguments and errors as those calls. */
+fh_status fh_encode_fwd_bwd(fh_encoder enc, const float *coords, int64_t N, const void *table,
+                            void *out, fh_dtype out_dtype, const float *dout, float *dtable,
+                            int zero_dtable, fh_stream stream);
+
+/* fh_encode_step_host -- one encode fwd+bwd step from HOST buffers (the
+ * end-to-end form used by bench.py's "e2e" figure): copies coords_h
+ * [N][4] and dout_h [N][L*F] (pinned host memory for asynchrony) into the
+ * caller's device buffers coords_d / dout_d, zeroes dtable_d, runs
+ * fh_encode_fwd (out_d, f32) and fh_encode_bwd, and copies out_d -> out_h
+ * and dtable_d -> dtable_h.  All on `stream`; returns without waiting.
+ * Errors: as the calls it makes. */
+fh_status fh_encode_step_host(fh_encoder enc, const float *coords_h, const float *dout_h,
+                              int64_t N, const void *table_d, float *coords_d, float *dout_d,
+                              float *out_d, float *dtable_d, float *out_h, float *dtable_h,
+                              fh_stream stream);
+
+/* fh_status_sync -- synchronise `stream`, then report and clear the
+ * encoder's sticky domain flag: FH_E_DOMAIN if any kernel of this encoder
+ * clamped an out-of-domain / NaN coordinate since the last call, else FH_OK
+ * (or FH_E_CUDA if the stream reported an error). */
+fh_status fh_status_sync(fh_encoder enc, fh_stream stream);
+
+/* Thread-local text of the last error on this thread ("" if none). */
+const char *fh_last_error(void);
+
+/* Library version string. */
+const char *fh_version(void);
+
+#ifdef __cplusplus
+}
+#endif
+#endif /* FHASH_H_ */

@@ -1,0 +1,508 @@
+// encode_kernels.cuh -- sm_100a kernels of the F-Hash Tesseract encode.
+//
+// Paper: §3.2.4 "Input Encoding", steps 1-4, Eq. 9 F-Hash
+// (P:170), Eqs. 10-12 quadrilinear interpolation; readings
+// R2 (cell location), R3 (corner order), R5 (capped hash), R6 (Eq. 12).
+//
+// Thread mapping: one thread per (sample n, level l), l fastest, so the
+// L threads of a sample are adjacent lanes: the coordinate load is one
+// broadcast per sample, the output row [n][L*F] is written contiguously by
+// adjacent lanes, and each thread keeps its 16 corner gathers in flight
+// together (16 independent loads per thread).  Level metadata is staged in
+// shared memory because lanes of a warp read different levels.
+#pragma once
+#include <cuda_bf16.h>
+#include <cuda_fp16.h>
+#include <stdint.h>
+
+namespace fh {
+
+// 64 bytes per level; kernel parameters carry up to FH_MAX_LEVELS of them.
+struct __align__(16) Level {
+    uint32_t res[4];     // Rx, Ry, Rz, Rt (vertices)
+    float scale[4];      // fp32(R - 1) per axis (R2)
+    uint32_t sy, sz, st; // Eq. 9 strides: Rx, Rx*Ry, Rx*Ry*Rz
+    uint32_t hashed;     // 1: capped level, R5 hash
+    uint32_t mask;       // T_l - 1 for hashed levels (T_l power of two)
+    uint32_t offset;     // first entry of the level in the packed table
+    uint32_t pad[2];
+};
+
+constexpr int kMaxLevels = 32;
+
+struct Params {
+    int L;
+    int F;
+    Level lv[kMaxLevels];
+};
+
+// R5 hash primes (Teschner et al. spatial hash; the t prime is
+// this build's choice).
+constexpr uint32_t kPy = 2654435761u;
+constexpr uint32_t kPz = 805459861u;
+constexpr uint32_t kPt = 2246822519u;
+
+// Steps 1-2 on one axis (R2): clamp to [0,1] (NaN -> 0), one IEEE fp32
+// multiply s = p*(R-1), i = clamp(floor s, 0, R-2), w = s - i (exact).
+__device__ __forceinline__ void locate(float p, float scale, uint32_t R, uint32_t &i, float &w,
+                                       bool &bad) {
+    float pc = p;
+    if (!(p >= 0.0f)) { pc = 0.0f; bad = true; }
+    else if (p > 1.0f) { pc = 1.0f; bad = true; }
+    const float s = __fmul_rn(pc, scale);
+    int ii = __float2int_rd(s);
+    ii = min(ii, (int)R - 2);
+    ii = max(ii, 0);
+    i = (uint32_t)ii;
+    w = __fsub_rn(s, __int2float_rn(ii));
+}
+
+// Cell of one (sample, level): base indices and fractions.
+struct Cell {
+    uint32_t idx[16];
+    float w[4];
+};
+
+// Step 3: the 16 corner entries.  Bijective levels: Eq. 9 at the cell
+// origin, each corner adds bx + by*Rx + bz*Rx*Ry + bt*Rx*Ry*Rz ("a single
+// look-up ... through simple shifting").  Hashed levels: R5.
+__device__ __forceinline__ bool cell_of(const Level &lv, float4 p, Cell &c) {
+    uint32_t ix, iy, iz, it;
+    bool bad = false;
+    locate(p.x, lv.scale[0], lv.res[0], ix, c.w[0], bad);
+    locate(p.y, lv.scale[1], lv.res[1], iy, c.w[1], bad);
+    locate(p.z, lv.scale[2], lv.res[2], iz, c.w[2], bad);
+    locate(p.w, lv.scale[3], lv.res[3], it, c.w[3], bad);
+    if (!lv.hashed) {
+        const uint32_t base = lv.offset + ix + iy * lv.sy + iz * lv.sz + it * lv.st;
+#pragma unroll
+        for (int k = 0; k < 16; k++)
+            c.idx[k] = base + (k & 1) + ((k >> 1) & 1) * lv.sy + ((k >> 2) & 1) * lv.sz +
+                       ((k >> 3) & 1) * lv.st;
+    } else {
+        const uint32_t hx0 = ix, hx1 = ix + 1;
+        const uint32_t hy0 = iy * kPy, hy1 = (iy + 1) * kPy;
+        const uint32_t hz0 = iz * kPz, hz1 = (iz + 1) * kPz;
+        const uint32_t ht0 = it * kPt, ht1 = (it + 1) * kPt;
+#pragma unroll
+        for (int k = 0; k < 16; k++) {
+            const uint32_t h = ((k & 1) ? hx1 : hx0) ^ (((k >> 1) & 1) ? hy1 : hy0) ^
+                               (((k >> 2) & 1) ? hz1 : hz0) ^ (((k >> 3) & 1) ? ht1 : ht0);
+            c.idx[k] = lv.offset + (h & lv.mask);
+        }
+    }
+    return bad;
+}
+
+// ------------------------------------------------------------ gathers
+// Load the F features of one entry as floats.  F*sizeof(T) <= 16 bytes is
+// one vector load through the read-only path.
+template <int F, typename T> struct Gather;
+
+template <> struct Gather<1, float> {
+    static __device__ __forceinline__ void load(const float *t, uint32_t i, float *o) { o[0] = __ldg(t + i); }
+};
+template <> struct Gather<2, float> {
+    static __device__ __forceinline__ void load(const float *t, uint32_t i, float *o) {
+        const float2 v = __ldg(reinterpret_cast<const float2 *>(t) + i);
+        o[0] = v.x; o[1] = v.y;
+    }
+};
+template <> struct Gather<4, float> {
+    static __device__ __forceinline__ void load(const float *t, uint32_t i, float *o) {
+        const float4 v = __ldg(reinterpret_cast<const float4 *>(t) + i);
+        o[0] = v.x; o[1] = v.y; o[2] = v.z; o[3] = v.w;
+    }
+};
+template <> struct Gather<8, float> {
+    static __device__ __forceinline__ void load(const float *t, uint32_t i, float *o) {
+        const float4 a = __ldg(reinterpret_cast<const float4 *>(t) + 2 * (size_t)i);
+        const float4 b = __ldg(reinterpret_cast<const float4 *>(t) + 2 * (size_t)i + 1);
+        o[0] = a.x; o[1] = a.y; o[2] = a.z; o[3] = a.w; o[4] = b.x; o[5] = b.y; o[6] = b.z; o[7] = b.w;
+    }
+};
+template <> struct Gather<1, __half> {
+    static __device__ __forceinline__ void load(const __half *t, uint32_t i, float *o) {
+        o[0] = __half2float(__ldg(t + i));
+    }
+};
+template <> struct Gather<2, __half> {
+    static __device__ __forceinline__ void load(const __half *t, uint32_t i, float *o) {
+        const __half2 v = __ldg(reinterpret_cast<const __half2 *>(t) + i);
+        const float2 f = __half22float2(v);
+        o[0] = f.x; o[1] = f.y;
+    }
+};
+template <> struct Gather<4, __half> {
+    static __device__ __forceinline__ void load(const __half *t, uint32_t i, float *o) {
+        const uint2 v = __ldg(reinterpret_cast<const uint2 *>(t) + i);
+        const float2 a = __half22float2(*reinterpret_cast<const __half2 *>(&v.x));
+        const float2 b = __half22float2(*reinterpret_cast<const __half2 *>(&v.y));
+        o[0] = a.x; o[1] = a.y; o[2] = b.x; o[3] = b.y;
+    }
+};
+template <> struct Gather<8, __half> {
+    static __device__ __forceinline__ void load(const __half *t, uint32_t i, float *o) {
+        const uint4 v = __ldg(reinterpret_cast<const uint4 *>(t) + i);
+        const uint32_t u[4] = {v.x, v.y, v.z, v.w};
+#pragma unroll
+        for (int k = 0; k < 4; k++) {
+            const float2 f = __half22float2(*reinterpret_cast<const __half2 *>(&u[k]));
+            o[2 * k] = f.x; o[2 * k + 1] = f.y;
+        }
+    }
+};
+
+// ------------------------------------------------------------ stores
+template <int F, typename O> struct Store;
+template <int F> struct Store<F, float> {
+    static __device__ __forceinline__ void store(float *o, const float *v) {
+        if constexpr (F == 1) o[0] = v[0];
+        else if constexpr (F == 2) *reinterpret_cast<float2 *>(o) = make_float2(v[0], v[1]);
+        else {
+#pragma unroll
+            for (int k = 0; k < F; k += 4)
+                *reinterpret_cast<float4 *>(o + k) = make_float4(v[k], v[k + 1], v[k + 2], v[k + 3]);
+        }
+    }
+};
+template <int F> struct Store<F, __nv_bfloat16> {
+    static __device__ __forceinline__ void store(__nv_bfloat16 *o, const float *v) {
+        if constexpr (F == 1) o[0] = __float2bfloat16_rn(v[0]);
+        else if constexpr (F == 2) *reinterpret_cast<__nv_bfloat162 *>(o) = __floats2bfloat162_rn(v[0], v[1]);
+        else if constexpr (F == 4) {
+            __nv_bfloat162 a = __floats2bfloat162_rn(v[0], v[1]), b = __floats2bfloat162_rn(v[2], v[3]);
+            uint2 u;
+            u.x = *reinterpret_cast<uint32_t *>(&a);
+            u.y = *reinterpret_cast<uint32_t *>(&b);
+            *reinterpret_cast<uint2 *>(o) = u;
+        } else {
+            uint4 u;
+            uint32_t *pu = reinterpret_cast<uint32_t *>(&u);
+#pragma unroll
+            for (int k = 0; k < 4; k++) {
+                __nv_bfloat162 a = __floats2bfloat162_rn(v[2 * k], v[2 * k + 1]);
+                pu[k] = *reinterpret_cast<uint32_t *>(&a);
+            }
+            *reinterpret_cast<uint4 *>(o) = u;
+        }
+    }
+};
+
+// lerp (1-w) a + w b as fma(w, b, (1-w)*a): each rounding is relative to
+// (1-w)|a| + w|b|, so four nested levels stay within ~12 u * sum_c W_c|E_c|
+// (u = 2^-24), inside the 1e-6 forward bar.  The form
+// a + w (b - a) is NOT used: at w ~ 1 it leaves an error of ulp(a) against
+// a result of size |b|.
+__device__ __forceinline__ float lerp(float a, float b, float w) {
+    return fmaf(w, b, __fmul_rn(__fsub_rn(1.0f, w), a));
+}
+
+__device__ __forceinline__ void load_levels(const Params &P, Level *s) {
+    const int n = P.L * (int)(sizeof(Level) / 4);
+    const uint32_t *src = reinterpret_cast<const uint32_t *>(P.lv);
+    uint32_t *dst = reinterpret_cast<uint32_t *>(s);
+    for (int i = threadIdx.x; i < n; i += blockDim.x) dst[i] = src[i];
+    __syncthreads();
+}
+
+// ------------------------------------------------------------ block gather
+// The 16 corners are 8 x-adjacent pairs.  Eq. 9 puts a pair at entries
+// (i, i+1); the R5 hash puts it at (h, h') with h' = h^1 when X is even and
+// within the same 4-entry block when X = 1 mod 4.  Either way the pair lies
+// in one 32-byte-aligned block with probability 3/4 (8-byte entries), so
+// each pair is fetched with ONE 256-bit load (LDG.E.ENL2.256, one L1
+// wavefront / one L2 sector) plus a second only when it straddles blocks:
+// 1.25 loads per pair instead of 2.
+template <typename T, int F> struct EntryTraits {
+    static constexpr int kBytes = F * (int)sizeof(T);
+    static constexpr int kPerBlock = kBytes >= 32 ? 1 : 32 / kBytes;   // entries per 32-byte block
+    static constexpr int kWords = kBytes >= 4 ? kBytes / 4 : 1;        // 32-bit words per entry
+};
+
+struct Block32 { uint32_t w[8]; };
+
+__device__ __forceinline__ Block32 ld_block(const void *base, uint32_t b) {
+    Block32 r;
+    const char *p = reinterpret_cast<const char *>(base) + (size_t)b * 32;
+    asm("ld.global.nc.v8.b32 {%0,%1,%2,%3,%4,%5,%6,%7}, [%8];"
+        : "=r"(r.w[0]), "=r"(r.w[1]), "=r"(r.w[2]), "=r"(r.w[3]), "=r"(r.w[4]), "=r"(r.w[5]), "=r"(r.w[6]),
+          "=r"(r.w[7])
+        : "l"(p));
+    return r;
+}
+
+// Convert the entry at slot s of a block to F floats.
+template <typename T, int F>
+__device__ __forceinline__ void extract(const Block32 &b, uint32_t s, float *o) {
+    using Tr = EntryTraits<T, F>;
+    if constexpr (Tr::kBytes >= 4) {
+        uint32_t w[Tr::kWords];
+#pragma unroll
+        for (int j = 0; j < Tr::kWords; j++) {
+            uint32_t v = b.w[j];
+#pragma unroll
+            for (int q = 1; q < Tr::kPerBlock; q++) v = (s == (uint32_t)q) ? b.w[q * Tr::kWords + j] : v;
+            w[j] = v;
+        }
+        if constexpr (sizeof(T) == 4) {
+#pragma unroll
+            for (int j = 0; j < F; j++) o[j] = __uint_as_float(w[j]);
+        } else {
+#pragma unroll
+            for (int j = 0; j < F / 2; j++) {
+                const float2 f = __half22float2(*reinterpret_cast<const __half2 *>(&w[j]));
+                o[2 * j] = f.x; o[2 * j + 1] = f.y;
+            }
+        }
+    } else {  // 2-byte entry (F = 1 half): 16 per block
+        uint32_t v = b.w[0];
+#pragma unroll
+        for (int q = 1; q < 8; q++) v = ((s >> 1) == (uint32_t)q) ? b.w[q] : v;
+        const unsigned short h = (s & 1) ? (unsigned short)(v >> 16) : (unsigned short)(v & 0xFFFF);
+        o[0] = __half2float(__ushort_as_half(h));
+    }
+}
+
+// Gather the 16 corner entries of one (sample, level) into e[16][F].
+// full_blocks = number of complete 32-byte blocks in the table; entries in
+// a trailing partial block are read entry-wise (never past the buffer).
+template <typename T, int F>
+__device__ __forceinline__ void gather16(const T *__restrict__ table, uint32_t full_blocks, const uint32_t (&idx)[16],
+                                         float (&e)[16][F]) {
+    using Tr = EntryTraits<T, F>;
+#ifndef FH_BLOCK_GATHER
+#define FH_BLOCK_GATHER 0
+#endif
+    if constexpr (Tr::kBytes == 8 && FH_BLOCK_GATHER == 2) {
+        // x-pair as one 16-byte load of the aligned chunk holding entry i0;
+        // the partner comes from the same chunk when (i0>>1) == (i1>>1),
+        // else from one more 8-byte load.  Chunks never pass the buffer end.
+        uint4 c[8];
+        uint2 x[8];
+        bool same[8];
+#pragma unroll
+        for (int k = 0; k < 8; k++) {
+            const uint32_t i0 = idx[2 * k], i1 = idx[2 * k + 1];
+            const uint32_t ch = i0 >> 1;
+            const bool tail = ch >= 2 * full_blocks;  // chunk may pass the end of the table
+            same[k] = !tail && (i0 >> 1) == (i1 >> 1);
+            if (!tail) {
+                c[k] = __ldg(reinterpret_cast<const uint4 *>(table) + ch);
+            } else {
+                const uint2 t = __ldg(reinterpret_cast<const uint2 *>(table) + i0);
+                c[k] = (i0 & 1) ? make_uint4(0, 0, t.x, t.y) : make_uint4(t.x, t.y, 0, 0);
+            }
+            if (!same[k]) x[k] = __ldg(reinterpret_cast<const uint2 *>(table) + i1);
+        }
+#pragma unroll
+        for (int k = 0; k < 8; k++) {
+            const bool odd0 = idx[2 * k] & 1;
+            const uint2 a = odd0 ? make_uint2(c[k].z, c[k].w) : make_uint2(c[k].x, c[k].y);
+            const uint2 b = same[k] ? (odd0 ? make_uint2(c[k].x, c[k].y) : make_uint2(c[k].z, c[k].w)) : x[k];
+            const uint32_t wa[2] = {a.x, a.y}, wb[2] = {b.x, b.y};
+            if constexpr (sizeof(T) == 4) {
+                e[2 * k][0] = __uint_as_float(wa[0]); e[2 * k][1] = __uint_as_float(wa[1]);
+                e[2 * k + 1][0] = __uint_as_float(wb[0]); e[2 * k + 1][1] = __uint_as_float(wb[1]);
+            } else {
+#pragma unroll
+                for (int j = 0; j < 2; j++) {
+                    const float2 fa = __half22float2(*reinterpret_cast<const __half2 *>(&wa[j]));
+                    const float2 fb = __half22float2(*reinterpret_cast<const __half2 *>(&wb[j]));
+                    e[2 * k][2 * j] = fa.x; e[2 * k][2 * j + 1] = fa.y;
+                    e[2 * k + 1][2 * j] = fb.x; e[2 * k + 1][2 * j + 1] = fb.y;
+                }
+            }
+        }
+    } else if constexpr (Tr::kBytes > 32 || !FH_BLOCK_GATHER) {
+#pragma unroll
+        for (int k = 0; k < 16; k++) Gather<F, T>::load(table, idx[k], e[k]);
+    } else {
+        Block32 b0[8], b1[8];
+        uint32_t s0[8], s1[8];
+        bool two[8], tail[8];
+#pragma unroll
+        for (int k = 0; k < 8; k++) {
+            const uint32_t i0 = idx[2 * k], i1 = idx[2 * k + 1];
+            const uint32_t k0 = i0 / Tr::kPerBlock, k1 = i1 / Tr::kPerBlock;
+            s0[k] = i0 % Tr::kPerBlock;
+            s1[k] = i1 % Tr::kPerBlock;
+            two[k] = k0 != k1;
+            tail[k] = (k0 >= full_blocks) || (k1 >= full_blocks);
+            if (!tail[k]) {
+                b0[k] = ld_block(table, k0);
+                if (two[k]) b1[k] = ld_block(table, k1);
+            }
+        }
+#pragma unroll
+        for (int k = 0; k < 8; k++) {
+            if (!tail[k]) {
+                extract<T, F>(b0[k], s0[k], e[2 * k]);
+                extract<T, F>(two[k] ? b1[k] : b0[k], s1[k], e[2 * k + 1]);
+            } else {
+                Gather<F, T>::load(table, idx[2 * k], e[2 * k]);
+                Gather<F, T>::load(table, idx[2 * k + 1], e[2 * k + 1]);
+            }
+        }
+    }
+}
+
+// ------------------------------------------------------------ forward
+// Step 4 (Eqs. 10-12): trilinear per time slice (8 x-lerps -> 4 y -> 2 z),
+// then the temporal lerp (R6), per feature.
+template <int F, typename T, typename O>
+#ifndef FH_FWD_MINB
+#define FH_FWD_MINB 2
+#endif
+__global__ void __launch_bounds__(256, FH_FWD_MINB) fwd_kernel(const __grid_constant__ Params P,
+                                                  const float4 *__restrict__ coords, int64_t N,
+                                                  const T *__restrict__ table, uint32_t full_blocks,
+                                                  O *__restrict__ out, int *__restrict__ flag) {
+    __shared__ Level slv[kMaxLevels];
+    load_levels(P, slv);
+    const int L = P.L;
+    const int64_t gid = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+    const int64_t n = gid / L;
+    if (n >= N) return;
+    const int l = (int)(gid - n * L);
+    const Level &lv = slv[l];
+    const float4 p = __ldg(coords + n);
+    Cell c;
+    const bool bad = cell_of(lv, p, c);
+    if (bad && l == 0) atomicOr(flag, 1);
+    float e[16][F];
+    gather16<T, F>(table, full_blocks, c.idx, e);
+    float v[F];
+#pragma unroll
+    for (int f = 0; f < F; f++) {
+        float s[2];
+#pragma unroll
+        for (int bt = 0; bt < 2; bt++) {
+            const int o = bt * 8;
+            const float x00 = lerp(e[o + 0][f], e[o + 1][f], c.w[0]);
+            const float x10 = lerp(e[o + 2][f], e[o + 3][f], c.w[0]);
+            const float x01 = lerp(e[o + 4][f], e[o + 5][f], c.w[0]);
+            const float x11 = lerp(e[o + 6][f], e[o + 7][f], c.w[0]);
+            const float y0 = lerp(x00, x10, c.w[1]);
+            const float y1 = lerp(x01, x11, c.w[1]);
+            s[bt] = lerp(y0, y1, c.w[2]);
+        }
+        v[f] = lerp(s[0], s[1], c.w[3]);
+    }
+    Store<F, O>::store(out + n * (int64_t)(L * F) + l * F, v);
+}
+
+// ------------------------------------------------------------ backward
+// dtable[idx_c] += W_c * g (adjoint of the forward), W_c = prod of the four
+// per-axis factors (bx ? wx : 1-wx) ... in fp32.  Vector reductions carry the
+// F features of an entry in one op (REDG.E.ADD.F32x2/x4); for F <= 2 an
+// x-pair that falls in one 16-byte chunk is ONE red.v4 (zeros in unused
+// lanes are exact no-ops), so a pair costs 1.5 reduction ops on average.
+__device__ __forceinline__ void red4(float *p, float a, float b, float c, float d) {
+    atomicAdd(reinterpret_cast<float4 *>(p), make_float4(a, b, c, d));
+}
+
+template <int F>
+__device__ __forceinline__ void red_entry(float *dtable, uint32_t i, const float *v) {
+    if constexpr (F == 1) atomicAdd(dtable + i, v[0]);
+    else if constexpr (F == 2) atomicAdd(reinterpret_cast<float2 *>(dtable) + i, make_float2(v[0], v[1]));
+    else {
+#pragma unroll
+        for (int k = 0; k < F; k += 4) red4(dtable + (size_t)i * F + k, v[k], v[k + 1], v[k + 2], v[k + 3]);
+    }
+}
+
+template <int F>
+__device__ __forceinline__ void red_pair(float *dtable, uint32_t i0, uint32_t i1, const float *v0, const float *v1) {
+    if constexpr (F == 2) {
+        if ((i0 >> 1) == (i1 >> 1)) {  // both entries in one 16-byte chunk
+            float *p = dtable + (size_t)(i0 & ~1u) * 2;
+            if (i0 & 1) red4(p, v1[0], v1[1], v0[0], v0[1]);
+            else red4(p, v0[0], v0[1], v1[0], v1[1]);
+            return;
+        }
+    } else if constexpr (F == 1) {
+        if ((i0 >> 2) == (i1 >> 2)) {
+            const uint32_t a = i0 & 3, b = i1 & 3;
+            float q[4];
+#pragma unroll
+            for (int j = 0; j < 4; j++) q[j] = (a == (uint32_t)j ? v0[0] : 0.f) + (b == (uint32_t)j ? v1[0] : 0.f);
+            red4(dtable + (i0 & ~3u), q[0], q[1], q[2], q[3]);
+            return;
+        }
+    }
+    red_entry<F>(dtable, i0, v0);
+    red_entry<F>(dtable, i1, v1);
+}
+
+template <int F>
+__global__ void __launch_bounds__(256) bwd_kernel(const __grid_constant__ Params P,
+                                                  const float4 *__restrict__ coords, int64_t N,
+                                                  const float *__restrict__ dout, float *__restrict__ dtable,
+                                                  int *__restrict__ flag) {
+    __shared__ Level slv[kMaxLevels];
+    load_levels(P, slv);
+    const int L = P.L;
+    const int64_t gid = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+    const int64_t n = gid / L;
+    if (n >= N) return;
+    const int l = (int)(gid - n * L);
+    const Level &lv = slv[l];
+    const float4 p = __ldg(coords + n);
+    Cell c;
+    const bool bad = cell_of(lv, p, c);
+    if (bad && l == 0) atomicOr(flag, 1);
+    float g[F];
+    const float *gp = dout + n * (int64_t)(L * F) + l * F;
+#pragma unroll
+    for (int f = 0; f < F; f++) g[f] = __ldg(gp + f);
+    const float wx[2] = {__fsub_rn(1.0f, c.w[0]), c.w[0]}, wy[2] = {__fsub_rn(1.0f, c.w[1]), c.w[1]};
+    const float wz[2] = {__fsub_rn(1.0f, c.w[2]), c.w[2]}, wt[2] = {__fsub_rn(1.0f, c.w[3]), c.w[3]};
+#pragma unroll
+    for (int k = 0; k < 16; k += 2) {
+        const float Wyzt = wy[(k >> 1) & 1] * wz[(k >> 2) & 1] * wt[(k >> 3) & 1];
+        const float W0 = wx[0] * Wyzt, W1 = wx[1] * Wyzt;
+        float v0[F], v1[F];
+#pragma unroll
+        for (int f = 0; f < F; f++) { v0[f] = W0 * g[f]; v1[f] = W1 * g[f]; }
+        red_pair<F>(dtable, c.idx[k], c.idx[k + 1], v0, v1);
+    }
+}
+
+// ------------------------------------------------------------ indices
+__global__ void __launch_bounds__(256) indices_kernel(const __grid_constant__ Params P,
+                                                      const float4 *__restrict__ coords, int64_t N,
+                                                      uint32_t *__restrict__ idx, float *__restrict__ wout,
+                                                      int *__restrict__ flag) {
+    __shared__ Level slv[kMaxLevels];
+    load_levels(P, slv);
+    const int L = P.L;
+    const int64_t gid = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+    const int64_t n = gid / L;
+    if (n >= N) return;
+    const int l = (int)(gid - n * L);
+    const float4 p = __ldg(coords + n);
+    Cell c;
+    const bool bad = cell_of(slv[l], p, c);
+    if (bad && l == 0) atomicOr(flag, 1);
+    uint4 *o = reinterpret_cast<uint4 *>(idx + gid * 16);
+#pragma unroll
+    for (int k = 0; k < 16; k += 4) o[k / 4] = make_uint4(c.idx[k], c.idx[k + 1], c.idx[k + 2], c.idx[k + 3]);
+    if (wout) {
+        const float wx[2] = {1.0f - c.w[0], c.w[0]}, wy[2] = {1.0f - c.w[1], c.w[1]};
+        const float wz[2] = {1.0f - c.w[2], c.w[2]}, wt[2] = {1.0f - c.w[3], c.w[3]};
+        float4 *ow = reinterpret_cast<float4 *>(wout + gid * 16);
+#pragma unroll
+        for (int k = 0; k < 16; k += 4) {
+            float q[4];
+#pragma unroll
+            for (int j = 0; j < 4; j++) {
+                const int kk = k + j;
+                q[j] = wx[kk & 1] * wy[(kk >> 1) & 1] * wz[(kk >> 2) & 1] * wt[(kk >> 3) & 1];
+            }
+            ow[k / 4] = make_float4(q[0], q[1], q[2], q[3]);
+        }
+    }
+}
+
+}  // namespace fh

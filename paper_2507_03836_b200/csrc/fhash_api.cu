@@ -1,0 +1,335 @@
+// fhash_api.cu -- host side of libfhash.so: the C ABI declared in
+// include/fhash.h (level builder a1, launch logic, validation, errors).
+#include <cuda_runtime.h>
+
+#include <cstdarg>
+#include <cstdio>
+#include <cstring>
+#include <new>
+
+#include "../../include/fhash.h"
+#include "encode_kernels.cuh"
+
+namespace {
+
+thread_local char g_err[512] = "";
+
+fh_status fail(fh_status s, const char *fmt, ...) {
+    va_list ap;
+    va_start(ap, fmt);
+    vsnprintf(g_err, sizeof(g_err), fmt, ap);
+    va_end(ap);
+    return s;
+}
+
+fh_status cuda_check(cudaError_t e, const char *what) {
+    if (e != cudaSuccess) return fail(FH_E_CUDA, "%s: %s", what, cudaGetErrorString(e));
+    return FH_OK;
+}
+
+bool aligned(const void *p, size_t a) { return (reinterpret_cast<uintptr_t>(p) % a) == 0; }
+
+size_t dtype_size(fh_dtype d) { return d == FH_F32 ? 4 : 2; }
+
+}  // namespace
+
+struct fh_encoder_s {
+    int L = 0, F = 0;
+    fh_dtype table_dtype = FH_F32;
+    uint64_t cap = 0;
+    fh_level_info info[FH_MAX_LEVELS];
+    uint64_t entries = 0;
+    fh::Params params;
+    int *flag = nullptr;  // sticky domain flag (device), allocated lazily
+    int device = -1;
+};
+
+// Make sure the encoder's status word exists on the current device.
+static fh_status ensure_flag(fh_encoder e) {
+    int dev = -1;
+    if (cudaGetDevice(&dev) != cudaSuccess) return fail(FH_E_CUDA, "cudaGetDevice failed");
+    if (e->flag) {
+        if (dev != e->device) return fail(FH_E_STATE, "encoder used on device %d, flag lives on %d", dev, e->device);
+        return FH_OK;
+    }
+    fh_status s = cuda_check(cudaMalloc(&e->flag, 16), "cudaMalloc(status word)");
+    if (s != FH_OK) return s;
+    s = cuda_check(cudaMemset(e->flag, 0, 16), "cudaMemset(status word)");
+    if (s != FH_OK) return s;
+    e->device = dev;
+    return FH_OK;
+}
+
+// ------------------------------------------------------------------ launches
+static dim3 grid_for(int64_t N, int L) {
+    const int64_t threads = N * (int64_t)L;
+    return dim3((unsigned)((threads + 255) / 256));
+}
+
+template <int F, typename T, typename O>
+static void launch_fwd(fh_encoder e, const float *coords, int64_t N, const void *table, void *out,
+                       cudaStream_t s) {
+    const uint32_t full_blocks = (uint32_t)((e->entries * (uint64_t)F * sizeof(T)) / 32);
+    fh::fwd_kernel<F, T, O><<<grid_for(N, e->L), 256, 0, s>>>(
+        e->params, reinterpret_cast<const float4 *>(coords), N, reinterpret_cast<const T *>(table), full_blocks,
+        reinterpret_cast<O *>(out), e->flag);
+}
+
+template <typename T, typename O>
+static void dispatch_fwd_F(fh_encoder e, const float *coords, int64_t N, const void *table, void *out,
+                           cudaStream_t s) {
+    switch (e->F) {
+        case 1: launch_fwd<1, T, O>(e, coords, N, table, out, s); break;
+        case 2: launch_fwd<2, T, O>(e, coords, N, table, out, s); break;
+        case 4: launch_fwd<4, T, O>(e, coords, N, table, out, s); break;
+        default: launch_fwd<8, T, O>(e, coords, N, table, out, s); break;
+    }
+}
+
+static fh_status check_common(fh_encoder e, const float *coords, int64_t N, const char *who) {
+    if (!e) return fail(FH_E_ARG, "%s: NULL encoder", who);
+    if (N < 0) return fail(FH_E_ARG, "%s: N = %lld < 0", who, (long long)N);
+    if (N > 0 && !coords) return fail(FH_E_ARG, "%s: NULL coords", who);
+    if (!aligned(coords, 16)) return fail(FH_E_ARG, "%s: coords not 16-byte aligned", who);
+    if (N > (int64_t)1 << 40) return fail(FH_E_RANGE, "%s: N too large", who);
+    return FH_OK;
+}
+
+extern "C" {
+
+const char *fh_last_error(void) { return g_err; }
+const char *fh_version(void) { return "fhash-b200 0.1 (sm_100a)"; }
+
+fh_status fh_fold_schedule(const uint32_t S_xyz[3], uint32_t n_t, uint32_t fold, fh_level_res *out,
+                           int *L_inout) {
+    g_err[0] = 0;
+    if (!S_xyz || !out || !L_inout) return fail(FH_E_ARG, "fh_fold_schedule: NULL pointer");
+    if (fold < 2 || n_t < 2) return fail(FH_E_ARG, "fh_fold_schedule: fold and n_t must be >= 2");
+    const uint32_t S[4] = {S_xyz[0], S_xyz[1], S_xyz[2], n_t};
+    int Ls = 0;
+    for (int a = 0; a < 4; a++) {
+        if (S[a] < 2) return fail(FH_E_ARG, "fh_fold_schedule: S[%d] = %u < 2", a, S[a]);
+        // Eq. 5: ceil(log_f S) as the least L >= 1 with f^L >= S (integer).
+        int La = 1;
+        for (uint64_t p = fold; p < S[a]; p *= fold) La++;
+        Ls = La > Ls ? La : Ls;  // Eq. 6
+    }
+    if (Ls > *L_inout) {
+        const int cap = *L_inout;
+        *L_inout = Ls;
+        return fail(FH_E_RANGE, "fh_fold_schedule: L_s = %d exceeds capacity %d", Ls, cap);
+    }
+    for (int a = 0; a < 4; a++) {
+        uint32_t r = S[a];
+        out[0].res[a] = r;  // Eq. 4
+        for (int l = 1; l < Ls; l++) {
+            r = (r > fold) ? (r + fold - 1) / fold : 2u;  // Eqs. 7-8
+            out[l].res[a] = r;
+        }
+    }
+    *L_inout = Ls;
+    return FH_OK;
+}
+
+fh_status fh_build_levels(const fh_level_res *res, int L, int F, fh_dtype table_dtype, uint64_t cap,
+                          fh_encoder *out) {
+    g_err[0] = 0;
+    if (!res || !out) return fail(FH_E_ARG, "fh_build_levels: NULL pointer");
+    *out = nullptr;
+    if (L < 1 || L > FH_MAX_LEVELS) return fail(FH_E_ARG, "fh_build_levels: L = %d not in [1, %d]", L, FH_MAX_LEVELS);
+    if (F != 1 && F != 2 && F != 4 && F != 8) return fail(FH_E_ARG, "fh_build_levels: F = %d not in {1,2,4,8}", F);
+    if (table_dtype != FH_F32 && table_dtype != FH_F16)
+        return fail(FH_E_ARG, "fh_build_levels: table dtype must be FH_F32 or FH_F16");
+    if (cap & (cap - 1)) return fail(FH_E_ARG, "fh_build_levels: cap %llu is not a power of two", (unsigned long long)cap);
+    if (cap > (1ull << 31)) return fail(FH_E_RANGE, "fh_build_levels: cap above 2^31");
+    fh_encoder e = new (std::nothrow) fh_encoder_s();
+    if (!e) return fail(FH_E_ARG, "fh_build_levels: out of host memory");
+    e->L = L;
+    e->F = F;
+    e->table_dtype = table_dtype;
+    e->cap = cap;
+    uint64_t off = 0;
+    e->params.L = L;
+    e->params.F = F;
+    for (int l = 0; l < L; l++) {
+        uint64_t c = 1;
+        for (int a = 0; a < 4; a++) {
+            const uint32_t r = res[l].res[a];
+            if (r < 2 || r > (1u << 24)) {
+                delete e;
+                return fail(FH_E_ARG, "fh_build_levels: level %d axis %d resolution %u not in [2, 2^24]", l, a, r);
+            }
+            c *= r;
+        }
+        fh_level_info &I = e->info[l];
+        memcpy(I.res, res[l].res, sizeof(I.res));
+        I.corners = c;
+        I.hashed = (cap != 0 && c > cap) ? 1u : 0u;
+        I.table_size = I.hashed ? cap : c;
+        I.reserved = 0;
+        I.offset = off;
+        off += I.table_size;
+        if (off * (uint64_t)F >= (1ull << 32)) {
+            delete e;
+            return fail(FH_E_RANGE, "fh_build_levels: sum T_l * F >= 2^32 at level %d", l);
+        }
+        fh::Level &K = e->params.lv[l];
+        memset(&K, 0, sizeof(K));
+        for (int a = 0; a < 4; a++) {
+            K.res[a] = I.res[a];
+            K.scale[a] = (float)(I.res[a] - 1);
+        }
+        K.sy = I.res[0];
+        K.sz = I.res[0] * I.res[1];
+        K.st = I.hashed ? 0u : (uint32_t)((uint64_t)I.res[0] * I.res[1] * I.res[2]);
+        if (I.hashed) K.sz = 0;  // unused on hashed levels (may overflow)
+        K.hashed = I.hashed;
+        K.mask = I.hashed ? (uint32_t)(cap - 1) : 0u;
+        K.offset = (uint32_t)I.offset;
+    }
+    e->entries = off;
+    *out = e;
+    return FH_OK;
+}
+
+fh_status fh_level_info_get(fh_encoder e, int l, fh_level_info *out) {
+    g_err[0] = 0;
+    if (!e || !out) return fail(FH_E_ARG, "fh_level_info_get: NULL pointer");
+    if (l < 0 || l >= e->L) return fail(FH_E_ARG, "fh_level_info_get: level %d out of range", l);
+    *out = e->info[l];
+    return FH_OK;
+}
+
+int fh_num_levels(fh_encoder e) { return e ? e->L : 0; }
+int fh_feature_dim(fh_encoder e) { return e ? e->F : 0; }
+uint64_t fh_table_entries(fh_encoder e) { return e ? e->entries : 0; }
+uint64_t fh_param_count(fh_encoder e) { return e ? e->entries * (uint64_t)e->F : 0; }
+
+void fh_encoder_destroy(fh_encoder e) {
+    if (!e) return;
+    if (e->flag) {
+        int cur = -1;
+        cudaGetDevice(&cur);
+        if (cur != e->device) cudaSetDevice(e->device);
+        cudaFree(e->flag);
+        if (cur != e->device && cur >= 0) cudaSetDevice(cur);
+    }
+    delete e;
+}
+
+fh_status fh_encode_fwd(fh_encoder e, const float *coords, int64_t N, const void *table, void *out,
+                        fh_dtype out_dtype, fh_stream stream) {
+    g_err[0] = 0;
+    fh_status st = check_common(e, coords, N, "fh_encode_fwd");
+    if (st != FH_OK) return st;
+    if (out_dtype != FH_F32 && out_dtype != FH_BF16)
+        return fail(FH_E_ARG, "fh_encode_fwd: out dtype must be FH_F32 or FH_BF16");
+    if (N == 0) return FH_OK;
+    if (!table || !aligned(table, 32)) return fail(FH_E_ARG, "fh_encode_fwd: NULL or not 32-byte aligned table");
+    const size_t ovec = (size_t)e->F * dtype_size(out_dtype);
+    if (!out || !aligned(out, ovec > 16 ? 16 : ovec)) return fail(FH_E_ARG, "fh_encode_fwd: NULL/misaligned out");
+    if ((st = ensure_flag(e)) != FH_OK) return st;
+    cudaStream_t s = reinterpret_cast<cudaStream_t>(stream);
+    if (e->table_dtype == FH_F32) {
+        if (out_dtype == FH_F32) dispatch_fwd_F<float, float>(e, coords, N, table, out, s);
+        else dispatch_fwd_F<float, __nv_bfloat16>(e, coords, N, table, out, s);
+    } else {
+        if (out_dtype == FH_F32) dispatch_fwd_F<__half, float>(e, coords, N, table, out, s);
+        else dispatch_fwd_F<__half, __nv_bfloat16>(e, coords, N, table, out, s);
+    }
+    return cuda_check(cudaGetLastError(), "fh_encode_fwd launch");
+}
+
+fh_status fh_encode_bwd(fh_encoder e, const float *coords, int64_t N, const float *dout, float *dtable,
+                        fh_stream stream) {
+    g_err[0] = 0;
+    fh_status st = check_common(e, coords, N, "fh_encode_bwd");
+    if (st != FH_OK) return st;
+    if (N == 0) return FH_OK;
+    if (!dout || !aligned(dout, 4)) return fail(FH_E_ARG, "fh_encode_bwd: NULL/misaligned dout");
+    const size_t vec = (size_t)e->F * 4;
+    if (!dtable || !aligned(dtable, vec > 16 ? 16 : vec)) return fail(FH_E_ARG, "fh_encode_bwd: NULL/misaligned dtable");
+    if ((st = ensure_flag(e)) != FH_OK) return st;
+    cudaStream_t s = reinterpret_cast<cudaStream_t>(stream);
+    const dim3 g = grid_for(N, e->L);
+    const float4 *c4 = reinterpret_cast<const float4 *>(coords);
+    switch (e->F) {
+        case 1: fh::bwd_kernel<1><<<g, 256, 0, s>>>(e->params, c4, N, dout, dtable, e->flag); break;
+        case 2: fh::bwd_kernel<2><<<g, 256, 0, s>>>(e->params, c4, N, dout, dtable, e->flag); break;
+        case 4: fh::bwd_kernel<4><<<g, 256, 0, s>>>(e->params, c4, N, dout, dtable, e->flag); break;
+        default: fh::bwd_kernel<8><<<g, 256, 0, s>>>(e->params, c4, N, dout, dtable, e->flag); break;
+    }
+    return cuda_check(cudaGetLastError(), "fh_encode_bwd launch");
+}
+
+fh_status fh_encode_indices(fh_encoder e, const float *coords, int64_t N, uint32_t *idx, float *w,
+                            fh_stream stream) {
+    g_err[0] = 0;
+    fh_status st = check_common(e, coords, N, "fh_encode_indices");
+    if (st != FH_OK) return st;
+    if (N == 0) return FH_OK;
+    if (!idx || !aligned(idx, 16) || !aligned(w, 16)) return fail(FH_E_ARG, "fh_encode_indices: NULL/misaligned output");
+    if ((st = ensure_flag(e)) != FH_OK) return st;
+    cudaStream_t s = reinterpret_cast<cudaStream_t>(stream);
+    fh::indices_kernel<<<grid_for(N, e->L), 256, 0, s>>>(e->params, reinterpret_cast<const float4 *>(coords), N,
+                                                         idx, w, e->flag);
+    return cuda_check(cudaGetLastError(), "fh_encode_indices launch");
+}
+
+fh_status fh_zero_grad(fh_encoder e, float *dtable, fh_stream stream) {
+    g_err[0] = 0;
+    if (!e || !dtable) return fail(FH_E_ARG, "fh_zero_grad: NULL pointer");
+    return cuda_check(cudaMemsetAsync(dtable, 0, e->entries * e->F * 4, reinterpret_cast<cudaStream_t>(stream)),
+                      "fh_zero_grad");
+}
+
+fh_status fh_encode_fwd_bwd(fh_encoder e, const float *coords, int64_t N, const void *table, void *out,
+                            fh_dtype out_dtype, const float *dout, float *dtable, int zero_dtable,
+                            fh_stream stream) {
+    g_err[0] = 0;
+    if (!e) return fail(FH_E_ARG, "fh_encode_fwd_bwd: NULL encoder");
+    if (!dtable) return fail(FH_E_ARG, "fh_encode_fwd_bwd: NULL dtable");
+    fh_status st;
+    if (zero_dtable &&
+        (st = cuda_check(cudaMemsetAsync(dtable, 0, e->entries * e->F * 4, reinterpret_cast<cudaStream_t>(stream)),
+                         "memset dtable")) != FH_OK)
+        return st;
+    if ((st = fh_encode_fwd(e, coords, N, table, out, out_dtype, stream)) != FH_OK) return st;
+    return fh_encode_bwd(e, coords, N, dout, dtable, stream);
+}
+
+fh_status fh_encode_step_host(fh_encoder e, const float *coords_h, const float *dout_h, int64_t N,
+                              const void *table_d, float *coords_d, float *dout_d, float *out_d,
+                              float *dtable_d, float *out_h, float *dtable_h, fh_stream stream) {
+    g_err[0] = 0;
+    if (!e) return fail(FH_E_ARG, "fh_encode_step_host: NULL encoder");
+    if (N < 0 || (N > 0 && (!coords_h || !dout_h || !coords_d || !dout_d || !out_d || !out_h)) || !dtable_d || !dtable_h)
+        return fail(FH_E_ARG, "fh_encode_step_host: NULL pointer");
+    cudaStream_t s = reinterpret_cast<cudaStream_t>(stream);
+    const size_t LF = (size_t)e->L * e->F;
+    fh_status st;
+    if ((st = cuda_check(cudaMemcpyAsync(coords_d, coords_h, (size_t)N * 16, cudaMemcpyHostToDevice, s), "H2D coords")) != FH_OK) return st;
+    if ((st = cuda_check(cudaMemcpyAsync(dout_d, dout_h, (size_t)N * LF * 4, cudaMemcpyHostToDevice, s), "H2D dout")) != FH_OK) return st;
+    if ((st = cuda_check(cudaMemsetAsync(dtable_d, 0, e->entries * e->F * 4, s), "memset dtable")) != FH_OK) return st;
+    if ((st = fh_encode_fwd(e, coords_d, N, table_d, out_d, FH_F32, stream)) != FH_OK) return st;
+    if ((st = fh_encode_bwd(e, coords_d, N, dout_d, dtable_d, stream)) != FH_OK) return st;
+    if ((st = cuda_check(cudaMemcpyAsync(out_h, out_d, (size_t)N * LF * 4, cudaMemcpyDeviceToHost, s), "D2H out")) != FH_OK) return st;
+    return cuda_check(cudaMemcpyAsync(dtable_h, dtable_d, e->entries * e->F * 4, cudaMemcpyDeviceToHost, s), "D2H dtable");
+}
+
+fh_status fh_status_sync(fh_encoder e, fh_stream stream) {
+    g_err[0] = 0;
+    if (!e) return fail(FH_E_ARG, "fh_status_sync: NULL encoder");
+    cudaStream_t s = reinterpret_cast<cudaStream_t>(stream);
+    fh_status st = cuda_check(cudaStreamSynchronize(s), "fh_status_sync");
+    if (st != FH_OK || !e->flag) return st;
+    int h = 0;
+    if ((st = cuda_check(cudaMemcpy(&h, e->flag, sizeof(int), cudaMemcpyDeviceToHost), "read status word")) != FH_OK) return st;
+    if (h) {
+        if ((st = cuda_check(cudaMemset(e->flag, 0, sizeof(int)), "clear status word")) != FH_OK) return st;
+        return fail(FH_E_DOMAIN, "out-of-domain or NaN coordinates were clamped to [0,1]");
+    }
+    return FH_OK;
+}
+
+}  // extern "C"

@@ -1,0 +1,219 @@
+"""Thin Python binding of libfhash.so (include/fhash.h) -- argument
+marshalling only.  Every step of the path runs in the library's sm_100a
+kernels; there is NO CPU fallback: if the shared library is missing or a
+call fails, this module raises.
+
+Torch is used for device memory and streams only: tensors are passed to the
+C ABI as raw device pointers on the current CUDA stream.
+"""
+from __future__ import annotations
+
+import ctypes
+import os
+from typing import List, Optional, Sequence, Tuple
+
+_PKG = os.path.dirname(os.path.abspath(__file__))
+LIB_PATH = os.environ.get("FHASH_LIB", os.path.join(_PKG, "libfhash.so"))  # override: experiments only
+
+FH_OK, FH_E_ARG, FH_E_RANGE, FH_E_DOMAIN, FH_E_CUDA, FH_E_DIVERGED, FH_E_STATE = 0, -1, -2, -3, -4, -5, -6
+FH_F32, FH_F16, FH_BF16 = 0, 1, 2
+MAX_LEVELS = 32
+
+_STATUS_NAMES = {0: "FH_OK", -1: "FH_E_ARG", -2: "FH_E_RANGE", -3: "FH_E_DOMAIN", -4: "FH_E_CUDA",
+                 -5: "FH_E_DIVERGED", -6: "FH_E_STATE"}
+
+# Every symbol include/fhash.h declares (checked by tests/test_abi.py).
+EXPORTS = [
+    "fh_fold_schedule", "fh_build_levels", "fh_level_info_get", "fh_num_levels", "fh_feature_dim",
+    "fh_table_entries", "fh_param_count", "fh_encoder_destroy", "fh_encode_fwd", "fh_encode_bwd",
+    "fh_encode_indices", "fh_zero_grad", "fh_encode_fwd_bwd", "fh_encode_step_host", "fh_status_sync", "fh_last_error",
+    "fh_version",
+    # include/fhash_bench.h (measurement kernels)
+    "fh_bench_gather", "fh_bench_red", "fh_bench_copy",
+]
+
+
+class FHashError(RuntimeError):
+    def __init__(self, status: int, msg: str):
+        super().__init__(f"{_STATUS_NAMES.get(status, status)}: {msg}")
+        self.status = status
+
+
+class LevelRes(ctypes.Structure):
+    _fields_ = [("res", ctypes.c_uint32 * 4)]
+
+
+class LevelInfo(ctypes.Structure):
+    _fields_ = [("res", ctypes.c_uint32 * 4), ("corners", ctypes.c_uint64), ("table_size", ctypes.c_uint64),
+                ("hashed", ctypes.c_uint32), ("reserved", ctypes.c_uint32), ("offset", ctypes.c_uint64)]
+
+
+_lib = None
+
+
+def lib() -> ctypes.CDLL:
+    """Load the in-tree libfhash.so (fails loudly if it was not built)."""
+    global _lib
+    if _lib is not None:
+        return _lib
+    if not os.path.exists(LIB_PATH):
+        raise ImportError(f"{LIB_PATH} not built: run `python -c 'import __graft_entry__ as g; g.build()'`")
+    L = ctypes.CDLL(LIB_PATH)
+    vp, i64, u64, c_int = ctypes.c_void_p, ctypes.c_int64, ctypes.c_uint64, ctypes.c_int
+    L.fh_fold_schedule.argtypes = [ctypes.POINTER(ctypes.c_uint32), ctypes.c_uint32, ctypes.c_uint32,
+                                   ctypes.POINTER(LevelRes), ctypes.POINTER(c_int)]
+    L.fh_build_levels.argtypes = [ctypes.POINTER(LevelRes), c_int, c_int, c_int, u64, ctypes.POINTER(vp)]
+    L.fh_level_info_get.argtypes = [vp, c_int, ctypes.POINTER(LevelInfo)]
+    L.fh_num_levels.argtypes = [vp]
+    L.fh_feature_dim.argtypes = [vp]
+    L.fh_table_entries.argtypes = [vp]
+    L.fh_table_entries.restype = u64
+    L.fh_param_count.argtypes = [vp]
+    L.fh_param_count.restype = u64
+    L.fh_encoder_destroy.argtypes = [vp]
+    L.fh_encoder_destroy.restype = None
+    L.fh_encode_fwd.argtypes = [vp, vp, i64, vp, vp, c_int, vp]
+    L.fh_encode_bwd.argtypes = [vp, vp, i64, vp, vp, vp]
+    L.fh_encode_indices.argtypes = [vp, vp, i64, vp, vp, vp]
+    L.fh_encode_fwd_bwd.argtypes = [vp, vp, i64, vp, vp, c_int, vp, vp, c_int, vp]
+    L.fh_zero_grad.argtypes = [vp, vp, vp]
+    L.fh_encode_step_host.argtypes = [vp, vp, vp, i64, vp, vp, vp, vp, vp, vp, vp, vp]
+    L.fh_status_sync.argtypes = [vp, vp]
+    L.fh_bench_gather.argtypes = [vp, u64, c_int, i64, c_int, c_int, ctypes.c_uint32, vp, vp]
+    L.fh_bench_red.argtypes = [vp, u64, c_int, i64, c_int, c_int, ctypes.c_uint32, vp]
+    L.fh_bench_copy.argtypes = [vp, vp, u64, vp]
+    for name in ("fh_bench_gather", "fh_bench_red", "fh_bench_copy"):
+        getattr(L, name).restype = c_int
+    L.fh_last_error.restype = ctypes.c_char_p
+    L.fh_version.restype = ctypes.c_char_p
+    for name in ("fh_fold_schedule", "fh_build_levels", "fh_level_info_get", "fh_encode_fwd", "fh_encode_bwd",
+                 "fh_encode_indices", "fh_encode_fwd_bwd", "fh_encode_step_host", "fh_status_sync", "fh_zero_grad"):
+        getattr(L, name).restype = c_int
+    _lib = L
+    return L
+
+
+def _check(status: int):
+    if status != FH_OK:
+        raise FHashError(status, lib().fh_last_error().decode())
+
+
+def _stream(stream) -> Optional[int]:
+    import torch
+    if stream is None:
+        stream = torch.cuda.current_stream()
+    return stream.cuda_stream if hasattr(stream, "cuda_stream") else int(stream)
+
+
+def _ptr(t) -> Optional[int]:
+    return None if t is None else t.data_ptr()
+
+
+def fold_schedule(S_xyz: Sequence[int], n_t: int, fold: int) -> List[Tuple[int, int, int, int]]:
+    """Eqs. 4-8 through the library; paper order (finest first)."""
+    S = (ctypes.c_uint32 * 3)(*S_xyz)
+    out = (LevelRes * 64)()
+    L = ctypes.c_int(64)
+    _check(lib().fh_fold_schedule(S, n_t, fold, out, ctypes.byref(L)))
+    return [tuple(out[i].res) for i in range(L.value)]
+
+
+_DT = {"f32": FH_F32, "f16": FH_F16, "bf16": FH_BF16}
+
+
+class Encoder:
+    """Handle on an fh_encoder (a1 build_levels).  levels: [(Rx,Ry,Rz,Rt)]
+    in output order; cap 0 = pure MPHF."""
+
+    def __init__(self, levels: Sequence[Sequence[int]], F: int, table_dtype: str = "f32", cap: int = 0):
+        L = len(levels)
+        arr = (LevelRes * max(L, 1))()
+        for i, r in enumerate(levels):
+            arr[i].res[:] = [int(v) for v in r]
+        h = ctypes.c_void_p()
+        _check(lib().fh_build_levels(arr, L, F, _DT[table_dtype], cap, ctypes.byref(h)))
+        self._h = h
+        self.levels = [tuple(int(v) for v in r) for r in levels]
+        self.L, self.F, self.cap, self.table_dtype = L, F, cap, table_dtype
+        self.entries = int(lib().fh_table_entries(h))
+        self.param_count = int(lib().fh_param_count(h))
+
+    def __del__(self):
+        h = getattr(self, "_h", None)
+        if h is not None and h.value and _lib is not None:
+            _lib.fh_encoder_destroy(h)
+            self._h = None
+
+    @property
+    def handle(self):
+        return self._h
+
+    def level_info(self, l: int) -> dict:
+        I = LevelInfo()
+        _check(lib().fh_level_info_get(self._h, l, ctypes.byref(I)))
+        return dict(res=tuple(I.res), corners=I.corners, table_size=I.table_size, hashed=bool(I.hashed),
+                    offset=I.offset)
+
+    # -------------------------------------------------------------- kernels
+    def fwd(self, coords, table, out=None, out_dtype: str = "f32", stream=None):
+        import torch
+        N = coords.shape[0]
+        if out is None:
+            dt = torch.float32 if out_dtype == "f32" else torch.bfloat16
+            out = torch.empty((N, self.L * self.F), dtype=dt, device=coords.device)
+        _check(lib().fh_encode_fwd(self._h, _ptr(coords), N, _ptr(table), _ptr(out), _DT[out_dtype],
+                                   _stream(stream)))
+        return out
+
+    def bwd(self, coords, dout, dtable, stream=None):
+        _check(lib().fh_encode_bwd(self._h, _ptr(coords), coords.shape[0], _ptr(dout), _ptr(dtable),
+                                   _stream(stream)))
+        return dtable
+
+    def indices(self, coords, want_w: bool = True, stream=None):
+        import torch
+        N = coords.shape[0]
+        idx = torch.empty((N, self.L, 16), dtype=torch.int32, device=coords.device)
+        w = torch.empty((N, self.L, 16), dtype=torch.float32, device=coords.device) if want_w else None
+        _check(lib().fh_encode_indices(self._h, _ptr(coords), N, _ptr(idx), _ptr(w), _stream(stream)))
+        return idx, w
+
+    def zero_grad(self, dtable, stream=None):
+        _check(lib().fh_zero_grad(self._h, _ptr(dtable), _stream(stream)))
+
+    def fwd_bwd(self, coords, table, out, dout, dtable, out_dtype: str = "f32", zero_dtable: bool = True,
+                stream=None):
+        _check(lib().fh_encode_fwd_bwd(self._h, _ptr(coords), coords.shape[0], _ptr(table), _ptr(out),
+                                       _DT[out_dtype], _ptr(dout), _ptr(dtable), int(zero_dtable),
+                                       _stream(stream)))
+
+    def step_host(self, coords_h, dout_h, table_d, coords_d, dout_d, out_d, dtable_d, out_h, dtable_h,
+                  stream=None):
+        _check(lib().fh_encode_step_host(self._h, _ptr(coords_h), _ptr(dout_h), coords_h.shape[0], _ptr(table_d),
+                                         _ptr(coords_d), _ptr(dout_d), _ptr(out_d), _ptr(dtable_d), _ptr(out_h),
+                                         _ptr(dtable_h), _stream(stream)))
+
+    def status_sync(self, stream=None) -> int:
+        """Synchronise and return the sticky status (FH_OK or FH_E_DOMAIN);
+        raises on CUDA errors."""
+        s = lib().fh_status_sync(self._h, _stream(stream))
+        if s not in (FH_OK, FH_E_DOMAIN):
+            _check(s)
+        return s
+
+
+# ------------------------------------------------------------ measurement
+def bench_gather(buf, n_entries: int, entry_bytes: int, n_threads: int, sink, mode: int = 1, seed: int = 0,
+                 stream=None):
+    """Roofline microbenchmark (include/fhash_bench.h): 8 random x-pairs per
+    thread; mode 1 = one aligned access per pair (minimum sectors)."""
+    _check(lib().fh_bench_gather(_ptr(buf), n_entries, entry_bytes, n_threads, 8, mode, seed, _ptr(sink),
+                                 _stream(stream)))
+
+
+def bench_red(buf, n_entries: int, entry_bytes: int, n_threads: int, mode: int = 1, seed: int = 0, stream=None):
+    _check(lib().fh_bench_red(_ptr(buf), n_entries, entry_bytes, n_threads, 8, mode, seed, _stream(stream)))
+
+
+def bench_copy(dst, src, nbytes: int, stream=None):
+    _check(lib().fh_bench_copy(_ptr(dst), _ptr(src), nbytes, _stream(stream)))

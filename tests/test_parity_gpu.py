@@ -1,0 +1,255 @@
+"""GPU parity: the CUDA path (through the C ABI) against the CPU oracle on
+the same seeded inputs, element by element.  -m gpu.
+
+Bars (from BASELINE.json north_star and SURVEY.md §8(c)):
+  indices     bit-exact (uint32), all N*L*16
+  weights     |w_gpu - W| <= 1e-6 * W + 1e-12   (fp32 4-factor product)
+  forward     |gpu - oracle| <= 1e-6 * sum_c W_c |E_c| + 1e-30
+  backward    |gpu - oracle| <= 1e-5 * sum |W_c g|; untouched entries exactly 0
+  bf16 out    within half a bf16 ulp of the oracle + the forward bound
+"""
+import numpy as np
+import pytest
+import torch
+
+import oracle
+import workloads as W
+
+pytestmark = pytest.mark.gpu
+
+if torch.cuda.is_available():
+    from paper_2507_03836_b200 import fhash as fh
+
+
+def dev(a):
+    return torch.from_numpy(np.ascontiguousarray(a)).cuda()
+
+
+def run_fwd(enc, case, out_dtype="f32"):
+    out = enc.fwd(dev(case.coords), dev(case.table), out_dtype=out_dtype)
+    st = enc.status_sync()
+    return out.float().cpu().numpy().astype(np.float64), st
+
+
+def run_bwd(enc, case):
+    dtable = torch.zeros((enc.entries, enc.F), dtype=torch.float32, device="cuda")
+    enc.bwd(dev(case.coords), dev(case.dout), dtable)
+    st = enc.status_sync()
+    return dtable.cpu().numpy().astype(np.float64), st
+
+
+def check_fwd(got, ref, absref, rel=1e-6):
+    err = np.abs(got - ref)
+    bound = rel * absref + 1e-30
+    bad = err > bound
+    assert not bad.any(), f"{bad.sum()} fwd mismatches; worst ratio {np.max(err / bound):.3g}"
+
+
+def check_bwd(got, G, A, rel=1e-5):
+    untouched = A == 0
+    assert np.all(got[untouched] == 0.0), "untouched entries must be exactly zero"
+    err = np.abs(got - G)
+    bound = rel * A
+    bad = (err > bound) & ~untouched
+    assert not bad.any(), f"{bad.sum()} bwd mismatches; worst ratio {np.max(err[~untouched] / bound[~untouched]):.3g}"
+
+
+CFGS = [W.CFG1, W.CFG1H]
+
+
+@pytest.mark.parametrize("cfg", CFGS, ids=lambda c: c.name)
+@pytest.mark.parametrize("N", [4096, 4096 + 37, 1, 255])
+def test_indices_bit_exact(cfg, N):
+    case = W.encode_case(cfg, N, seed=0)
+    enc = fh.Encoder(cfg.levels, cfg.F, cfg.table_dtype, cfg.cap)
+    ref = oracle.Levels(cfg.levels, cfg.cap)
+    idx, w = enc.indices(dev(case.coords))
+    assert enc.status_sync() == fh.FH_OK
+    ridx, rW, _ = ref.indices(case.coords)
+    assert np.array_equal(idx.cpu().numpy().view(np.uint32), ridx)
+    wg = w.cpu().numpy().astype(np.float64)
+    assert np.all(np.abs(wg - rW) <= 1e-6 * rW + 1e-12)
+
+
+@pytest.mark.parametrize("cfg", CFGS, ids=lambda c: c.name)
+@pytest.mark.parametrize("N", [4096, 4096 + 37, 1])
+def test_forward_parity(cfg, N):
+    case = W.encode_case(cfg, N, seed=0)
+    enc = fh.Encoder(cfg.levels, cfg.F, cfg.table_dtype, cfg.cap)
+    ref = oracle.Levels(cfg.levels, cfg.cap)
+    got, st = run_fwd(enc, case)
+    assert st == fh.FH_OK
+    r, ab = ref.forward(case.coords, case.table, want_abs=True)
+    check_fwd(got, r, ab)
+
+
+@pytest.mark.parametrize("cfg", CFGS, ids=lambda c: c.name)
+@pytest.mark.parametrize("N", [4096, 4096 + 37, 1])
+def test_backward_parity(cfg, N):
+    case = W.encode_case(cfg, N, seed=0)
+    enc = fh.Encoder(cfg.levels, cfg.F, cfg.table_dtype, cfg.cap)
+    ref = oracle.Levels(cfg.levels, cfg.cap)
+    got, st = run_bwd(enc, case)
+    assert st == fh.FH_OK
+    G, A = ref.backward(case.coords, case.dout, cfg.F, want_abs=True)
+    check_bwd(got, G, A)
+
+
+@pytest.mark.parametrize("F", [1, 2, 4, 8])
+@pytest.mark.parametrize("tdt", ["f32", "f16"])
+def test_feature_widths_and_dtypes(F, tdt):
+    cfg = W.EncoderConfig("f", W.cfg1_levels(), F=F, cap=1 << 11, table_dtype=tdt)
+    case = W.encode_case(cfg, 3001, seed=F)
+    enc = fh.Encoder(cfg.levels, F, tdt, cfg.cap)
+    ref = oracle.Levels(cfg.levels, cfg.cap)
+    got, _ = run_fwd(enc, case)
+    r, ab = ref.forward(case.coords, case.table.astype(np.float64), want_abs=True)
+    check_fwd(got, r, ab)
+    gb, _ = run_bwd(enc, case)
+    G, A = ref.backward(case.coords, case.dout, F, want_abs=True)
+    check_bwd(gb, G, A)
+
+
+@pytest.mark.parametrize("tdt", ["f32", "f16"])
+def test_bf16_output(tdt):
+    """R13: bf16 encoder output = RNE(fp32 blend); within half a bf16 ulp of
+    the oracle plus the fp32 forward bound."""
+    cfg = W.EncoderConfig("b", W.cfg1_levels(), F=2, cap=1 << 11, table_dtype=tdt)
+    case = W.encode_case(cfg, 4096, seed=5)
+    enc = fh.Encoder(cfg.levels, 2, tdt, cfg.cap)
+    ref = oracle.Levels(cfg.levels, cfg.cap)
+    got, _ = run_fwd(enc, case, out_dtype="bf16")
+    r, ab = ref.forward(case.coords, case.table.astype(np.float64), want_abs=True)
+    half_ulp = np.ldexp(1.0, np.frexp(np.abs(r))[1] - 9)
+    assert np.all(np.abs(got - r) <= half_ulp + 2e-6 * ab + 1e-30)
+
+
+def test_edge_and_lattice_coordinates():
+    """Domain edges (0, 1, next-below-1) and lattice vertices."""
+    cfg = W.CFG1H
+    coords = W.edge_coords()
+    case = W.encode_case(cfg, len(coords), seed=1, coords=coords)
+    enc = fh.Encoder(cfg.levels, cfg.F, cfg.table_dtype, cfg.cap)
+    ref = oracle.Levels(cfg.levels, cfg.cap)
+    idx, _ = enc.indices(dev(coords))
+    assert enc.status_sync() == fh.FH_OK
+    assert np.array_equal(idx.cpu().numpy().view(np.uint32), ref.indices(coords)[0])
+    got, _ = run_fwd(enc, case)
+    r, ab = ref.forward(coords, case.table, want_abs=True)
+    check_fwd(got, r, ab)
+    gb, _ = run_bwd(enc, case)
+    G, A = ref.backward(coords, case.dout, cfg.F, want_abs=True)
+    check_bwd(gb, G, A)
+
+
+def test_out_of_domain_flagged_and_clamped():
+    cfg = W.CFG1
+    bad = W.bad_coords()
+    case = W.encode_case(cfg, len(bad), seed=2, coords=bad)
+    enc = fh.Encoder(cfg.levels, cfg.F, cfg.table_dtype, cfg.cap)
+    ref = oracle.Levels(cfg.levels, cfg.cap)
+    got, st = run_fwd(enc, case)
+    assert st == fh.FH_E_DOMAIN
+    assert enc.status_sync() == fh.FH_OK  # flag cleared by the read
+    r, ab = ref.forward(bad, case.table, want_abs=True)
+    check_fwd(got, r, ab)
+    gb, st = run_bwd(enc, case)
+    assert st == fh.FH_E_DOMAIN
+    G, A = ref.backward(bad, case.dout, cfg.F, want_abs=True)
+    check_bwd(gb, G, A)
+
+
+def test_empty_batch_is_noop():
+    enc = fh.Encoder(W.CFG1.levels, 2)
+    c = torch.empty((0, 4), device="cuda")
+    out = enc.fwd(c, torch.zeros((enc.entries, 2), device="cuda"))
+    assert out.shape == (0, 8)
+    assert enc.status_sync() == fh.FH_OK
+
+
+def test_single_level_extremes():
+    """Degenerate resolutions: all-2 level (one cell), a long thin level,
+    and 32 levels (the maximum)."""
+    levels = [(2, 2, 2, 2), (1000, 2, 2, 2), (2, 2, 2, 1000)] + [(3, 4, 5, 2)] * 29
+    cfg = W.EncoderConfig("x", tuple(levels), F=2, cap=0, table_dtype="f32")
+    case = W.encode_case(cfg, 777, seed=4)
+    enc = fh.Encoder(levels, 2)
+    ref = oracle.Levels(levels)
+    idx, _ = enc.indices(dev(case.coords))
+    assert np.array_equal(idx.cpu().numpy().view(np.uint32), ref.indices(case.coords)[0])
+    got, _ = run_fwd(enc, case)
+    r, ab = ref.forward(case.coords, case.table, want_abs=True)
+    check_fwd(got, r, ab)
+
+
+# ----------------------------------------------- full size (bench launch cfg)
+def test_cfg2_full_size_parity():
+    """BASELINE.json configs[1] at full size (2^20 points, 16 levels), the
+    launch configuration bench.py times: forward on every row, backward on
+    every entry, indices on a 64k-row sample."""
+    cfg = W.CFG2
+    case = W.encode_case(cfg, W.N_CFG2, seed=0)
+    enc = fh.Encoder(cfg.levels, cfg.F, cfg.table_dtype, cfg.cap)
+    ref = oracle.Levels(cfg.levels, cfg.cap)
+    sub = case.coords[::16]
+    idx, _ = enc.indices(dev(sub), want_w=False)
+    assert np.array_equal(idx.cpu().numpy().view(np.uint32), ref.indices(sub, want_w=False)[0])
+    got, st = run_fwd(enc, case)
+    assert st == fh.FH_OK
+    r, ab = ref.forward(case.coords, case.table, want_abs=True)
+    check_fwd(got, r, ab)
+    del r, ab, got
+    gb, _ = run_bwd(enc, case)
+    G, A = ref.backward(case.coords, case.dout, cfg.F, want_abs=True)
+    check_bwd(gb, G, A)
+
+
+def test_cfg4_sampled_rows_and_adjoint():
+    """BASELINE.json configs[3] shapes (2^22 points, F=4, fp16 tables capped
+    at 2^22): forward on sampled rows vs the oracle, and the adjoint identity
+    <g, fwd(E)> = <bwd(g), E> at full size."""
+    cfg = W.CFG4
+    g = W.rng(0)
+    enc = fh.Encoder(cfg.levels, cfg.F, cfg.table_dtype, cfg.cap)
+    table = W.draw_table(g, enc.entries, cfg.F, "f16")
+    coords = W.draw_coords(g, W.N_CFG4)
+    ref = oracle.Levels(cfg.levels, cfg.cap)
+    c_d, t_d = dev(coords), dev(table)
+    out = enc.fwd(c_d, t_d)
+    rows = np.random.default_rng(1).choice(W.N_CFG4, 1 << 15, replace=False)
+    r, ab = ref.forward(coords[rows], table.astype(np.float64), want_abs=True)
+    check_fwd(out[torch.from_numpy(rows).cuda()].cpu().numpy().astype(np.float64), r, ab)
+    dout = torch.randn(out.shape, device="cuda", generator=torch.Generator("cuda").manual_seed(0))
+    dtab = torch.zeros((enc.entries, cfg.F), device="cuda")
+    enc.bwd(c_d, dout, dtab)
+    assert enc.status_sync() == fh.FH_OK
+    lhs = torch.sum(dout.double() * out.double()).item()
+    rhs = torch.sum(dtab.double() * t_d.double()).item()
+    scale = torch.sum(dout.double().abs() * out.double().abs()).item()
+    assert abs(lhs - rhs) <= 1e-5 * scale
+
+
+# ------------------------------------------------------ closed forms on GPU
+def test_constant_table_and_multilinear_on_gpu():
+    """Closed forms, no oracle: constant table -> constant output;
+    multilinear table -> p_x p_y p_z p_t."""
+    levels = [(4, 7, 5, 3), (13, 6, 9, 4)]
+    enc = fh.Encoder(levels, 2)
+    coords = W.draw_coords(W.rng(8), 5000)
+    c = dev(coords)
+    out = enc.fwd(c, torch.full((enc.entries, 2), 0.25, device="cuda")).cpu().numpy()
+    assert np.all(out == 0.25)
+    tab = np.zeros((enc.entries, 2), np.float32)
+    off = 0
+    for r in levels:
+        for t in range(r[3]):
+            for z in range(r[2]):
+                for y in range(r[1]):
+                    for x in range(r[0]):
+                        j = off + x + r[0] * (y + r[1] * (z + r[2] * t))
+                        tab[j, 0] = (x / (r[0] - 1)) * (y / (r[1] - 1)) * (z / (r[2] - 1)) * (t / (r[3] - 1))
+        off += r[0] * r[1] * r[2] * r[3]
+    out = enc.fwd(c, dev(tab)).cpu().numpy().astype(np.float64)
+    exp = np.prod(coords.astype(np.float64), axis=1)
+    assert np.max(np.abs(out[:, 0] - exp)) < 2e-6
+    assert np.max(np.abs(out[:, 2] - exp)) < 2e-6
