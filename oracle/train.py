@@ -87,7 +87,7 @@ def mlp_backward(dy: np.ndarray, layers, cache, emulate_bf16: bool = True):
         a_prev = acts[k]
         dz_op = dz if k == n_layers - 1 else r(dz)
         dW = dz_op.T @ a_prev
-        db = dz.sum(axis=0)
+        db = dz_op.sum(axis=0)   # R13: the bias gradient sums the same (rounded) dz the GEMMs use
         grads[k] = (dW, db)
         da = dz_op @ Wk
         if k > 0:

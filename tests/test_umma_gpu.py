@@ -1,0 +1,41 @@
+"""tcgen05 building blocks (tc_sm100.cuh) on the GPU: one-CTA bf16 GEMM
+D[128 x N] = A . B^T through shared-memory descriptors and TMEM, against a
+plain torch fp32 matmul of the same bf16 values.  Covers the K-major and
+MN-major operand layouts the fused MLP kernel uses.  -m gpu."""
+import ctypes
+import os
+import subprocess
+
+import pytest
+import torch
+
+pytestmark = pytest.mark.gpu
+
+HERE = os.path.dirname(os.path.abspath(__file__))
+SRC = os.path.join(HERE, "csrc", "umma_probe.cu")
+LIB = os.path.join(HERE, "csrc", "libumma_probe.so")
+
+
+def probe_lib():
+    if not os.path.exists(LIB) or os.path.getmtime(LIB) < os.path.getmtime(SRC):
+        subprocess.check_call(["/usr/local/cuda/bin/nvcc", "-gencode", "arch=compute_100a,code=sm_100a", "-O2",
+                               "-std=c++17", "-shared", "-Xcompiler", "-fPIC", SRC, "-o", LIB])
+    L = ctypes.CDLL(LIB)
+    L.umma_probe.argtypes = [ctypes.c_void_p] * 3 + [ctypes.c_int] * 4
+    return L
+
+
+@pytest.mark.parametrize("N,K,a_mn,b_mn", [(64, 64, 0, 0), (64, 32, 0, 0), (32, 64, 0, 0), (144, 128, 1, 1),
+                                           (112, 128, 1, 1), (64, 64, 0, 1), (64, 64, 1, 0)])
+def test_umma_gemm(N, K, a_mn, b_mn):
+    L = probe_lib()
+    g = torch.Generator("cuda").manual_seed(N * 1000 + K)
+    A = torch.randn(128, K, device="cuda", generator=g).bfloat16()
+    B = torch.randn(N, K, device="cuda", generator=g).bfloat16()
+    Ain = A.t().contiguous() if a_mn else A
+    Bin = B.t().contiguous() if b_mn else B
+    D = torch.empty(128, N, device="cuda")
+    assert L.umma_probe(Ain.data_ptr(), Bin.data_ptr(), D.data_ptr(), N, K, a_mn, b_mn) == 0
+    ref = A.float() @ B.float().t()
+    err = (D - ref).abs().max().item()
+    assert err <= 1e-3 * ref.abs().max().item(), err
