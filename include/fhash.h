@@ -171,6 +171,87 @@ fh_status fh_encode_step_host(fh_encoder enc, const float *coords_h, const float
  * (or FH_E_CUDA if the stream reported an error). */
 fh_status fh_status_sync(fh_encoder enc, fh_stream stream);
 
+/* ============================================================ train step
+ * The INR train step around the encoder (§3(4) of SURVEY; the paper trains
+ * "the INRs with input encoding ... Adam ... learning rate of 0.01", P:489,
+ * on the "shallow network" of P:233, "2 layers x 64 neurons"):
+ *   a2-a7 encode fwd (fp16 table shadow -> bf16 encoding, R13)
+ *   a8    MLP n_in -> 64 -> 64 -> 1, ReLU, biases (R15) on tcgen05 tensor
+ *         cores, forward and backward, bf16 operands / fp32 accumulation
+ *   a9    MSE over the GLOBAL batch: loss = sum (y - t)^2 / N_global,
+ *         dL/dy = 2 (y - t) / N_global (R12)
+ *   a10   encode bwd (fp32 dL/d(enc) scattered into fp32 table grads)
+ *   a11   dense bias-corrected Adam (lr, beta1, beta2, eps; R12) on fp32
+ *         masters of every parameter; rewrites the low-precision shadows and
+ *         zeroes the grads.
+ * Data parallel: fh_train_fwd_bwd leaves the complete local gradients in
+ * the caller's grad buffers; the caller all-reduces (SUM) them across ranks
+ * (e.g. torch.distributed over NCCL) and then calls fh_train_apply.  The
+ * loss is already scaled by 1/N_global, so summed gradients are exact. */
+typedef struct fh_trainer_s *fh_trainer;
+
+typedef struct {
+    int n_in;             /* MLP input width; must equal L*F; one of 16, 32, 48, 64 */
+    int n_hidden;         /* must be 64 */
+    int n_hidden_layers;  /* must be 2 */
+} fh_mlp_desc;
+
+/* Every buffer is caller-owned device memory (16-byte aligned).
+ * Table buffers have fh_table_entries(enc) * F elements; MLP buffers have
+ * fh_mlp_param_count() elements in the flat order
+ *   W1[64][n_in], b1[64], W2[64][64], b2[64], w3[64], b3
+ * (weights [out][in] row-major).  table_shadow has the encoder's table
+ * dtype (FH_F16: Adam writes it; FH_F32: pass NULL, the master is read
+ * directly); mlp_shadow is bf16.  Grad buffers must be zero before the
+ * first step (fh_train_apply re-zeroes them). */
+typedef struct {
+    float *table_master;
+    void *table_shadow;
+    float *table_grad;
+    float *table_m;
+    float *table_v;
+    float *mlp_master;
+    void *mlp_shadow;
+    float *mlp_grad;
+    float *mlp_m;
+    float *mlp_v;
+    void *workspace;          /* fh_train_workspace_size bytes */
+    size_t workspace_bytes;
+} fh_train_buffers;
+
+/* Adam hyper-parameters in double: 1 - beta is formed in double and rounded
+ * once to fp32 (fp32 1 - 0.999f is 1.3e-5 relative off 0.001). */
+typedef struct { double lr, beta1, beta2, eps; } fh_adam;
+
+uint64_t  fh_mlp_param_count(const fh_mlp_desc *mlp);
+size_t    fh_train_workspace_size(fh_encoder enc, const fh_mlp_desc *mlp, int64_t max_batch);
+
+/* Errors: FH_E_ARG (shape, NULL/misaligned buffer, small workspace),
+ * FH_E_CUDA.  The trainer keeps a reference to enc (caller keeps it alive). */
+fh_status fh_trainer_create(fh_encoder enc, const fh_mlp_desc *mlp, const fh_train_buffers *buf,
+                            const fh_adam *adam, int64_t max_batch, fh_trainer *out);
+
+/* Forward + loss + backward for N_local samples (coords [N][4] f32,
+ * target [N] f32, device).  loss_dev (device f32, may be NULL) receives
+ * sum_local (y - t)^2 / N_global.  Gradients are ADDED to the grad
+ * buffers.  N_local <= max_batch, N_global >= N_local. */
+fh_status fh_train_fwd_bwd(fh_trainer tr, const float *coords, const float *target, int64_t N_local,
+                           int64_t N_global, float *loss_dev, fh_stream stream);
+
+/* One Adam step on all parameters (step counter += 1). */
+fh_status fh_train_apply(fh_trainer tr, fh_stream stream);
+
+/* fh_train_fwd_bwd + fh_train_apply (single GPU). */
+fh_status fh_train_step(fh_trainer tr, const float *coords, const float *target, int64_t N_local,
+                        int64_t N_global, float *loss_dev, fh_stream stream);
+
+/* Synchronise `stream`; FH_E_DIVERGED if a non-finite loss was seen since
+ * the last call (sticky flag, cleared by the read), FH_E_DOMAIN if the
+ * encoder clamped coordinates, else FH_OK. */
+fh_status fh_trainer_status(fh_trainer tr, fh_stream stream);
+int64_t   fh_trainer_step_count(fh_trainer tr);
+void      fh_trainer_destroy(fh_trainer tr);
+
 /* Thread-local text of the last error on this thread ("" if none). */
 const char *fh_last_error(void);
 

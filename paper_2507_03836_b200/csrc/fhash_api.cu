@@ -7,42 +7,17 @@
 #include <cstring>
 #include <new>
 
-#include "../../include/fhash.h"
+#include "internal.h"
 #include "encode_kernels.cuh"
 
-namespace {
-
+namespace fh {
 thread_local char g_err[512] = "";
-
-fh_status fail(fh_status s, const char *fmt, ...) {
-    va_list ap;
-    va_start(ap, fmt);
-    vsnprintf(g_err, sizeof(g_err), fmt, ap);
-    va_end(ap);
-    return s;
 }
-
-fh_status cuda_check(cudaError_t e, const char *what) {
-    if (e != cudaSuccess) return fail(FH_E_CUDA, "%s: %s", what, cudaGetErrorString(e));
-    return FH_OK;
-}
-
-bool aligned(const void *p, size_t a) { return (reinterpret_cast<uintptr_t>(p) % a) == 0; }
-
-size_t dtype_size(fh_dtype d) { return d == FH_F32 ? 4 : 2; }
-
-}  // namespace
-
-struct fh_encoder_s {
-    int L = 0, F = 0;
-    fh_dtype table_dtype = FH_F32;
-    uint64_t cap = 0;
-    fh_level_info info[FH_MAX_LEVELS];
-    uint64_t entries = 0;
-    fh::Params params;
-    int *flag = nullptr;  // sticky domain flag (device), allocated lazily
-    int device = -1;
-};
+using fh::aligned;
+using fh::cuda_check;
+using fh::dtype_size;
+using fh::fail;
+using fh::g_err;
 
 // Make sure the encoder's status word exists on the current device.
 static fh_status ensure_flag(fh_encoder e) {

@@ -1,0 +1,44 @@
+// internal.h -- shared host-side internals of libfhash.so (not part of the ABI).
+#pragma once
+#include <cuda_runtime.h>
+
+#include <cstdarg>
+#include <cstdint>
+#include <cstdio>
+
+#include "../../include/fhash.h"
+#include "encode_params.h"
+
+namespace fh {
+
+// Thread-local last-error text (defined in fhash_api.cu).
+extern thread_local char g_err[512];
+
+inline fh_status fail(fh_status s, const char *fmt, ...) {
+    va_list ap;
+    va_start(ap, fmt);
+    vsnprintf(g_err, sizeof(g_err), fmt, ap);
+    va_end(ap);
+    return s;
+}
+
+inline fh_status cuda_check(cudaError_t e, const char *what) {
+    if (e != cudaSuccess) return fail(FH_E_CUDA, "%s: %s", what, cudaGetErrorString(e));
+    return FH_OK;
+}
+
+inline bool aligned(const void *p, size_t a) { return (reinterpret_cast<uintptr_t>(p) % a) == 0; }
+inline size_t dtype_size(fh_dtype d) { return d == FH_F32 ? 4 : 2; }
+
+}  // namespace fh
+
+struct fh_encoder_s {
+    int L = 0, F = 0;
+    fh_dtype table_dtype = FH_F32;
+    uint64_t cap = 0;
+    fh_level_info info[FH_MAX_LEVELS];
+    uint64_t entries = 0;
+    fh::Params params;
+    int *flag = nullptr;  // sticky domain flag (device), allocated lazily
+    int device = -1;
+};

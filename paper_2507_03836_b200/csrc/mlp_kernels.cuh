@@ -1,0 +1,439 @@
+// mlp_kernels.cuh -- the small MLP of the F-Hash INR on 5th-gen tensor
+// cores (tcgen05 + TMEM), fused forward + MSE loss + backward, and the fused
+// Adam optimiser.
+//
+// Paper: "a shallow network ... is used" on the concatenated encodings
+// (P:233); "number of MLP layers = 2, number of neurons per layer = 64"
+// (P:354); Adam, lr 0.01.  Readings R12 (Adam betas/eps,
+// MSE over the global batch), R13 (bf16 operand rounding points), R15
+// (ReLU hidden layers, identity output, biases) -- DESIGN.md §3.
+//
+// One persistent CTA per SM, 128 threads; each 128-sample tile is one
+// M = 128 tcgen05 GEMM chain with the accumulators in TMEM:
+//   MMA1  Z1  = X  . W1^T          (N = 64, K = K0)
+//   MMA2  Z2  = H1 . W2^T          (N = 64, K = 64)
+//   MMA3  dH1 = dZ2 . W2           (N = 64, K = 64)
+//   MMA4  dX  = dZ1 . W1           (N = K0, K = 64)
+//   MMA5  DW += [dZ2^T ; dZ1^T] . [H1 | X | 1]   (M = 128 hidden rows, K = 128 samples)
+// MMA5 accumulates dW2 (top-left), dW1 (bottom, X columns) and, through the
+// constant-one column, db2 / db1, in TMEM across all tiles of the CTA; the
+// transposed operands are the SAME shared-memory tiles read through
+// MN-major descriptors.  Thread t owns sample row t of every tile (TMEM
+// lane t), so every epilogue (bias, ReLU, bf16 rounding, the 64 -> 1 output
+// layer, the loss) runs in registers of one thread.
+#pragma once
+#include <cuda_bf16.h>
+#include <stdint.h>
+
+#include "tc_sm100.cuh"
+
+namespace fh {
+namespace mlp {
+
+constexpr int H = 64;          // hidden width
+constexpr int TILE = 128;      // samples per tile = TMEM lanes
+
+// Flat fp32 parameter layout (master, grads, Adam moments; the bf16 shadow
+// uses the same offsets): W1[H][K0], b1[H], W2[H][H], b2[H], w3[H], b3.
+__host__ __device__ constexpr int off_W1() { return 0; }
+__host__ __device__ constexpr int off_b1(int K0) { return H * K0; }
+__host__ __device__ constexpr int off_W2(int K0) { return H * K0 + H; }
+__host__ __device__ constexpr int off_b2(int K0) { return H * K0 + H + H * H; }
+__host__ __device__ constexpr int off_w3(int K0) { return H * K0 + 2 * H + H * H; }
+__host__ __device__ constexpr int off_b3(int K0) { return H * K0 + 3 * H + H * H; }
+__host__ __device__ constexpr int param_count(int K0) { return H * K0 + 3 * H + H * H + 1; }
+
+struct Smem {
+    // sizes for K0 <= 64
+    static constexpr int kHXMax = (H + 64 + 16);          // [H1 | X | 1 pad]
+};
+
+template <int K0>
+struct Layout {
+    static constexpr int WHX = H + K0 + 16;               // columns of the [H1 | X | 1..] tile
+    static constexpr uint32_t SBO_HX = (WHX / 8) * 128;   // bytes per 8-sample row group
+    static constexpr uint32_t SBO_DZ = (2 * H / 8) * 128; // [dZ2 | dZ1] tile: 2048
+    static constexpr uint32_t SBO_W1 = (K0 / 8) * 128;
+    static constexpr uint32_t SBO_W2 = (H / 8) * 128;
+    static constexpr uint32_t BYTES_HX = TILE * WHX * 2;
+    static constexpr uint32_t BYTES_DZ = TILE * 2 * H * 2;
+    static constexpr uint32_t BYTES_W1 = H * K0 * 2;
+    static constexpr uint32_t BYTES_W2 = H * H * 2;
+    static constexpr uint32_t BYTES_RED = TILE * (H + 1) * 4;  // dw3 transpose-reduce scratch
+    static constexpr uint32_t SMEM = BYTES_HX + BYTES_DZ + BYTES_W1 + BYTES_W2 + BYTES_RED;
+    // TMEM columns
+    static constexpr uint32_t T_Z1 = 0, T_Z2 = 64, T_DH1 = 128, T_DX = 192, T_DW = 256;
+    static constexpr uint32_t TMEM_COLS = 512;
+};
+
+__device__ __forceinline__ uint32_t pack_bf16(float a, float b) {
+    __nv_bfloat162 v = __floats2bfloat162_rn(a, b);
+    return *reinterpret_cast<uint32_t *>(&v);
+}
+__device__ __forceinline__ float bf16r(float a) { return __bfloat162float(__float2bfloat16_rn(a)); }
+
+struct TrainArgs {
+    const __nv_bfloat16 *x;      // [N][K0] encoder output
+    const float *target;         // [N]
+    const __nv_bfloat16 *wsh;    // bf16 shadow of the flat parameters
+    const float *wmaster;        // fp32 master (biases are read in fp32)
+    float *dx;                   // [N][K0] dL/d(enc), fp32
+    float *grad;                 // flat fp32 grads (+=)
+    float *loss;                 // += sum (y - t)^2 / N_global
+    int *flag;                   // bit 1: non-finite loss
+    int64_t N;
+    float inv_n_global;
+};
+
+// Write 8 bf16 (16 B) = one core-matrix row segment.
+__device__ __forceinline__ void st16(uint8_t *base, uint32_t off, uint4 v) {
+    *reinterpret_cast<uint4 *>(base + off) = v;
+}
+
+template <int K0>
+__global__ void __launch_bounds__(128, 1) mlp_train_kernel(const TrainArgs a) {
+    using Lo = Layout<K0>;
+    extern __shared__ __align__(1024) uint8_t smem[];
+    uint8_t *sHX = smem;
+    uint8_t *sDZ = sHX + Lo::BYTES_HX;
+    uint8_t *sW1 = sDZ + Lo::BYTES_DZ;
+    uint8_t *sW2 = sW1 + Lo::BYTES_W1;
+    float *sRed = reinterpret_cast<float *>(sW2 + Lo::BYTES_W2);
+    __shared__ uint64_t bar;
+    __shared__ uint32_t tbase;
+    __shared__ float s_db3[4], s_loss[4];
+
+    const int t = threadIdx.x, warp = t >> 5, lane = t & 31;
+    const int64_t n_tiles = (a.N + TILE - 1) / TILE;
+
+    // ---- weights -> shared memory (bf16 shadow), once per CTA
+    for (int i = t; i < H * K0; i += blockDim.x) {
+        const int r = i / K0, c = i % K0;
+        *reinterpret_cast<__nv_bfloat16 *>(sW1 + tc::core_off(r, c, Lo::SBO_W1)) = a.wsh[off_W1() + i];
+    }
+    for (int i = t; i < H * H; i += blockDim.x) {
+        const int r = i / H, c = i % H;
+        *reinterpret_cast<__nv_bfloat16 *>(sW2 + tc::core_off(r, c, Lo::SBO_W2)) = a.wsh[off_W2(K0) + i];
+    }
+    // constant columns [H + K0, H + K0 + 16) of the HX tile: 1, 0, ..., 0
+    {
+        const uint4 ones = make_uint4(pack_bf16(1.f, 0.f), 0u, 0u, 0u), zero = make_uint4(0u, 0u, 0u, 0u);
+        st16(sHX, tc::core_off(t, H + K0, Lo::SBO_HX), ones);
+        st16(sHX, tc::core_off(t, H + K0 + 8, Lo::SBO_HX), zero);
+    }
+    // constants in shared memory: biases (fp32 master), w3 (bf16 shadow values)
+    __shared__ float b1[H], b2[H], w3[H];
+    if (t < H) {
+        b1[t] = a.wmaster[off_b1(K0) + t];
+        b2[t] = a.wmaster[off_b2(K0) + t];
+        w3[t] = __bfloat162float(a.wsh[off_w3(K0) + t]);
+    }
+    const float b3 = a.wmaster[off_b3(K0)];
+
+    if (warp == 0) tc::tmem_alloc(&tbase, Lo::TMEM_COLS);
+    if (t == 0) { tc::mbar_init(&bar, 1); tc::fence_mbar_init(); }
+    tc::fence_smem_to_async();
+    tc::fence_before_sync();
+    __syncthreads();
+    tc::fence_after_sync();
+    const uint32_t tm = tbase;
+    const uint32_t lane_off = (uint32_t)(warp * 32) << 16;
+
+    const uint32_t aHX = tc::smem_u32(sHX), aDZ = tc::smem_u32(sDZ);
+    const uint32_t aW1 = tc::smem_u32(sW1), aW2 = tc::smem_u32(sW2);
+    constexpr uint32_t id_h = tc::idesc_bf16_f32(128, H, false, false);      // N = 64, K-major A,B
+    constexpr uint32_t id_dh = tc::idesc_bf16_f32(128, H, false, true);      // B = W2 MN-major
+    constexpr uint32_t id_dx = tc::idesc_bf16_f32(128, K0, false, true);     // B = W1 MN-major
+    constexpr uint32_t id_dw = tc::idesc_bf16_f32(128, Lo::WHX, true, true); // both MN-major
+
+    uint32_t phase = 0;
+    float dw3_acc = 0.f, db3_acc = 0.f, loss_acc = 0.f;
+    bool bad = false;
+    int my_tiles = 0;
+
+    for (int64_t tile = blockIdx.x; tile < n_tiles; tile += gridDim.x, my_tiles++) {
+        const int64_t row = tile * TILE + t;
+        const bool valid = row < a.N;
+        // ---- stage X row (bf16) into [H1 | X | 1] columns H.. H+K0
+        {
+            const uint4 *src = reinterpret_cast<const uint4 *>(a.x + row * K0);
+#pragma unroll
+            for (int q = 0; q < K0 / 8; q++) {
+                const uint4 v = valid ? __ldg(src + q) : make_uint4(0u, 0u, 0u, 0u);
+                st16(sHX, tc::core_off(t, H + 8 * q, Lo::SBO_HX), v);
+            }
+        }
+        const float tgt = valid ? __ldg(a.target + row) : 0.f;
+        tc::fence_smem_to_async();
+        tc::fence_before_sync();
+        __syncthreads();
+        tc::fence_after_sync();
+        // ---- MMA1: Z1 = X . W1^T
+        if (t == 0) {
+#pragma unroll
+            for (int s = 0; s < K0 / 16; s++)
+                tc::mma_bf16(tm + Lo::T_Z1, tc::sdesc(aHX + (H / 8) * 128 + s * 256, 128, Lo::SBO_HX),
+                             tc::sdesc(aW1 + s * 256, 128, Lo::SBO_W1), id_h, s > 0);
+            tc::commit(&bar);
+        }
+        tc::mbar_wait(&bar, phase); phase ^= 1;
+        tc::fence_after_sync();
+        // ---- epilogue 1: H1 = bf16(relu(Z1 + b1)), mask1
+        uint32_t m1[2] = {0u, 0u};
+#pragma unroll
+        for (int c = 0; c < H; c += 16) {
+            float v[16];
+            tc::tmem_ld16(tm + lane_off + Lo::T_Z1 + c, v);
+            tc::tmem_wait_ld();
+            uint32_t p[8];
+#pragma unroll
+            for (int j = 0; j < 16; j += 2) {
+                const float z0 = v[j] + b1[c + j], z1 = v[j + 1] + b1[c + j + 1];
+                m1[(c + j) >> 5] |= (z0 > 0.f ? 1u : 0u) << ((c + j) & 31);
+                m1[(c + j + 1) >> 5] |= (z1 > 0.f ? 1u : 0u) << ((c + j + 1) & 31);
+                p[j / 2] = pack_bf16(fmaxf(z0, 0.f), fmaxf(z1, 0.f));
+            }
+            st16(sHX, tc::core_off(t, c, Lo::SBO_HX), make_uint4(p[0], p[1], p[2], p[3]));
+            st16(sHX, tc::core_off(t, c + 8, Lo::SBO_HX), make_uint4(p[4], p[5], p[6], p[7]));
+        }
+        tc::fence_smem_to_async();
+        tc::fence_before_sync();
+        __syncthreads();
+        tc::fence_after_sync();
+        // ---- MMA2: Z2 = H1 . W2^T
+        if (t == 0) {
+#pragma unroll
+            for (int s = 0; s < H / 16; s++)
+                tc::mma_bf16(tm + Lo::T_Z2, tc::sdesc(aHX + s * 256, 128, Lo::SBO_HX),
+                             tc::sdesc(aW2 + s * 256, 128, Lo::SBO_W2), id_h, s > 0);
+            tc::commit(&bar);
+        }
+        tc::mbar_wait(&bar, phase); phase ^= 1;
+        tc::fence_after_sync();
+        // ---- epilogue 2: H2 = bf16(relu(Z2 + b2)); y = H2 . w3 + b3; MSE; dZ2
+        // h2 goes to this thread's row of sRed (fp32) to keep registers free
+        float *myred = sRed + t * (H + 1);
+        uint32_t m2[2] = {0u, 0u};
+        float y = 0.f;
+#pragma unroll
+        for (int c = 0; c < H; c += 16) {
+            float v[16];
+            tc::tmem_ld16(tm + lane_off + Lo::T_Z2 + c, v);
+            tc::tmem_wait_ld();
+#pragma unroll
+            for (int j = 0; j < 16; j++) {
+                const float z = v[j] + b2[c + j];
+                m2[(c + j) >> 5] |= (z > 0.f ? 1u : 0u) << ((c + j) & 31);
+                const float h = bf16r(fmaxf(z, 0.f));
+                y = fmaf(h, w3[c + j], y);   // output layer, j ascending (fp32)
+                myred[c + j] = h;
+            }
+        }
+        y += b3;
+        const float diff = valid ? (y - tgt) : 0.f;
+        if (!isfinite(diff)) bad = true;
+        loss_acc = fmaf(diff, diff, loss_acc);
+        const float dy = 2.f * diff * a.inv_n_global;
+        db3_acc += dy;
+        // dw3: transpose-reduce dy*h2 over the tile's 128 samples via smem
+#pragma unroll
+        for (int j = 0; j < H; j++) myred[j] *= dy;
+#pragma unroll
+        for (int c = 0; c < H; c += 8) {
+            uint32_t p[4];
+#pragma unroll
+            for (int j = 0; j < 8; j += 2) {
+                const float d0 = ((m2[(c + j) >> 5] >> ((c + j) & 31)) & 1u) ? dy * w3[c + j] : 0.f;
+                const float d1 = ((m2[(c + j + 1) >> 5] >> ((c + j + 1) & 31)) & 1u) ? dy * w3[c + j + 1] : 0.f;
+                p[j / 2] = pack_bf16(d0, d1);
+            }
+            st16(sDZ, tc::core_off(t, c, Lo::SBO_DZ), make_uint4(p[0], p[1], p[2], p[3]));
+        }
+        tc::fence_smem_to_async();
+        tc::fence_before_sync();
+        __syncthreads();
+        tc::fence_after_sync();
+        if (t < H) {
+            float s = 0.f;
+            for (int r = 0; r < TILE; r++) s += sRed[r * (H + 1) + t];
+            dw3_acc += s;
+        }
+        // ---- MMA3: dH1 = dZ2 . W2
+        if (t == 0) {
+#pragma unroll
+            for (int s = 0; s < H / 16; s++)
+                tc::mma_bf16(tm + Lo::T_DH1, tc::sdesc(aDZ + s * 256, 128, Lo::SBO_DZ),
+                             tc::sdesc(aW2 + s * 2 * Lo::SBO_W2, Lo::SBO_W2, 128), id_dh, s > 0);
+            tc::commit(&bar);
+        }
+        tc::mbar_wait(&bar, phase); phase ^= 1;
+        tc::fence_after_sync();
+        // ---- epilogue 3: dZ1 = bf16(dH1 * mask1)
+#pragma unroll
+        for (int c = 0; c < H; c += 16) {
+            float v[16];
+            tc::tmem_ld16(tm + lane_off + Lo::T_DH1 + c, v);
+            tc::tmem_wait_ld();
+            uint32_t p[8];
+#pragma unroll
+            for (int j = 0; j < 16; j += 2) {
+                const float d0 = ((m1[(c + j) >> 5] >> ((c + j) & 31)) & 1u) ? v[j] : 0.f;
+                const float d1 = ((m1[(c + j + 1) >> 5] >> ((c + j + 1) & 31)) & 1u) ? v[j + 1] : 0.f;
+                p[j / 2] = pack_bf16(d0, d1);
+            }
+            st16(sDZ, tc::core_off(t, H + c, Lo::SBO_DZ), make_uint4(p[0], p[1], p[2], p[3]));
+            st16(sDZ, tc::core_off(t, H + c + 8, Lo::SBO_DZ), make_uint4(p[4], p[5], p[6], p[7]));
+        }
+        tc::fence_smem_to_async();
+        tc::fence_before_sync();
+        __syncthreads();
+        tc::fence_after_sync();
+        // ---- MMA4: dX = dZ1 . W1 ; MMA5: DW += [dZ2^T; dZ1^T] . [H1 | X | 1]
+        if (t == 0) {
+#pragma unroll
+            for (int s = 0; s < H / 16; s++)
+                tc::mma_bf16(tm + Lo::T_DX, tc::sdesc(aDZ + (H / 8) * 128 + s * 256, 128, Lo::SBO_DZ),
+                             tc::sdesc(aW1 + s * 2 * Lo::SBO_W1, Lo::SBO_W1, 128), id_dx, s > 0);
+#pragma unroll
+            for (int s = 0; s < TILE / 16; s++)
+                tc::mma_bf16(tm + Lo::T_DW, tc::sdesc(aDZ + s * 2 * Lo::SBO_DZ, Lo::SBO_DZ, 128),
+                             tc::sdesc(aHX + s * 2 * Lo::SBO_HX, Lo::SBO_HX, 128), id_dw,
+                             (my_tiles > 0 || s > 0) ? 1u : 0u);
+            tc::commit(&bar);
+        }
+        tc::mbar_wait(&bar, phase); phase ^= 1;
+        tc::fence_after_sync();
+        // ---- epilogue 4: dX row -> global (fp32)
+#pragma unroll
+        for (int c = 0; c < K0; c += 16) {
+            float v[16];
+            tc::tmem_ld16(tm + lane_off + Lo::T_DX + c, v);
+            tc::tmem_wait_ld();
+            if (valid) {
+                float4 *dst = reinterpret_cast<float4 *>(a.dx + row * K0 + c);
+#pragma unroll
+                for (int j = 0; j < 16; j += 4) dst[j / 4] = make_float4(v[j], v[j + 1], v[j + 2], v[j + 3]);
+            }
+        }
+        tc::fence_before_sync();
+        __syncthreads();   // sRed / sDZ / sHX / TMEM reuse by the next tile
+        tc::fence_after_sync();
+    }
+
+    // ---- weight gradients out of TMEM: rows 0..63 -> dW2, db2; 64..127 -> dW1, db1
+    if (my_tiles > 0) {
+        const int r = t;  // TMEM lane = row of DW
+        float *g = a.grad;
+#pragma unroll 1
+        for (int c = 0; c < Lo::WHX; c += 16) {
+            float v[16];
+            tc::tmem_ld16(tm + lane_off + Lo::T_DW + c, v);
+            tc::tmem_wait_ld();
+#pragma unroll
+            for (int j = 0; j < 16; j++) {
+                const int col = c + j;
+                if (r < H) {
+                    if (col < H) atomicAdd(g + off_W2(K0) + r * H + col, v[j]);
+                    else if (col == H + K0) atomicAdd(g + off_b2(K0) + r, v[j]);
+                } else {
+                    if (col >= H && col < H + K0) atomicAdd(g + off_W1() + (r - H) * K0 + (col - H), v[j]);
+                    else if (col == H + K0) atomicAdd(g + off_b1(K0) + (r - H), v[j]);
+                }
+            }
+        }
+        if (t < H) atomicAdd(g + off_w3(K0) + t, dw3_acc);
+    }
+    // db3 and loss: warp reduce, then one atomic per CTA
+#pragma unroll
+    for (int o = 16; o > 0; o >>= 1) {
+        db3_acc += __shfl_xor_sync(0xffffffffu, db3_acc, o);
+        loss_acc += __shfl_xor_sync(0xffffffffu, loss_acc, o);
+    }
+    if (lane == 0) { s_db3[warp] = db3_acc; s_loss[warp] = loss_acc; }
+    if (bad) atomicOr(a.flag, 2);
+    tc::fence_before_sync();
+    __syncthreads();
+    if (t == 0 && my_tiles > 0) {
+        atomicAdd(a.grad + off_b3(K0), s_db3[0] + s_db3[1] + s_db3[2] + s_db3[3]);
+        atomicAdd(a.loss, (s_loss[0] + s_loss[1] + s_loss[2] + s_loss[3]) * a.inv_n_global);
+    }
+    if (warp == 0) tc::tmem_dealloc(tm, Lo::TMEM_COLS);
+}
+
+// ------------------------------------------------------------------ Adam
+// Bias-corrected Adam (R12), fp32 master/m/v, dense over every parameter:
+//   m = b1 m + (1-b1) g;  v = b2 v + (1-b2) g^2
+//   p -= lr * (m * c1) / (sqrt(v * c2) + eps),  c1 = 1/(1-b1^t), c2 = 1/(1-b2^t)
+// then writes the low-precision shadow (fp16 table / bf16 MLP) and zeroes g.
+struct AdamSeg {
+    float *p, *g, *m, *v;
+    void *shadow;        // __half* (kind 1) or __nv_bfloat16* (kind 2)
+    int64_t n;
+    int kind;
+};
+
+struct AdamArgs {
+    AdamSeg seg[2];
+    int64_t blocks0;     // blocks assigned to segment 0
+    float lr, b1, b2, eps, c1, c2;
+    float omb1, omb2;    // 1 - beta, rounded once from double (fp32 1.f - 0.999f is 5e-5 off)
+};
+
+template <typename S>
+__device__ __forceinline__ void adam_one(const AdamArgs &A, const AdamSeg &s, int64_t i) {
+    const float g = s.g[i];
+    const float m = fmaf(A.b1, s.m[i], A.omb1 * g);
+    const float v = fmaf(A.b2, s.v[i], A.omb2 * g * g);
+    const float p = s.p[i] - A.lr * (m * A.c1) / (sqrtf(v * A.c2) + A.eps);
+    s.m[i] = m; s.v[i] = v; s.p[i] = p; s.g[i] = 0.f;
+    if constexpr (sizeof(S) == 2) {
+        if (s.kind == 1) reinterpret_cast<__half *>(s.shadow)[i] = __float2half_rn(p);
+        else reinterpret_cast<__nv_bfloat16 *>(s.shadow)[i] = __float2bfloat16_rn(p);
+    }
+}
+
+__global__ void __launch_bounds__(256) adam_kernel(const AdamArgs A) {
+    const bool second = (int64_t)blockIdx.x >= A.blocks0;
+    const AdamSeg &s = second ? A.seg[1] : A.seg[0];
+    const int64_t b = second ? blockIdx.x - A.blocks0 : blockIdx.x;
+    const int64_t nb = second ? gridDim.x - A.blocks0 : A.blocks0;
+    // 4 elements per thread per iteration, vectorised when aligned
+    const int64_t n4 = s.n / 4;
+    for (int64_t q = b * blockDim.x + threadIdx.x; q < n4; q += nb * blockDim.x) {
+        float4 g = reinterpret_cast<const float4 *>(s.g)[q];
+        float4 m = reinterpret_cast<const float4 *>(s.m)[q];
+        float4 v = reinterpret_cast<const float4 *>(s.v)[q];
+        float4 p = reinterpret_cast<const float4 *>(s.p)[q];
+        float gg[4] = {g.x, g.y, g.z, g.w}, mm[4] = {m.x, m.y, m.z, m.w};
+        float vv[4] = {v.x, v.y, v.z, v.w}, pp[4] = {p.x, p.y, p.z, p.w};
+#pragma unroll
+        for (int k = 0; k < 4; k++) {
+            mm[k] = fmaf(A.b1, mm[k], A.omb1 * gg[k]);
+            vv[k] = fmaf(A.b2, vv[k], A.omb2 * gg[k] * gg[k]);
+            pp[k] = pp[k] - A.lr * (mm[k] * A.c1) / (sqrtf(vv[k] * A.c2) + A.eps);
+        }
+        reinterpret_cast<float4 *>(s.m)[q] = make_float4(mm[0], mm[1], mm[2], mm[3]);
+        reinterpret_cast<float4 *>(s.v)[q] = make_float4(vv[0], vv[1], vv[2], vv[3]);
+        reinterpret_cast<float4 *>(s.p)[q] = make_float4(pp[0], pp[1], pp[2], pp[3]);
+        reinterpret_cast<float4 *>(s.g)[q] = make_float4(0.f, 0.f, 0.f, 0.f);
+        if (s.kind == 1) {
+            __half2 h0 = __floats2half2_rn(pp[0], pp[1]), h1 = __floats2half2_rn(pp[2], pp[3]);
+            uint2 u;
+            u.x = *reinterpret_cast<uint32_t *>(&h0);
+            u.y = *reinterpret_cast<uint32_t *>(&h1);
+            reinterpret_cast<uint2 *>(s.shadow)[q] = u;
+        } else {
+            __nv_bfloat162 h0 = __floats2bfloat162_rn(pp[0], pp[1]), h1 = __floats2bfloat162_rn(pp[2], pp[3]);
+            uint2 u;
+            u.x = *reinterpret_cast<uint32_t *>(&h0);
+            u.y = *reinterpret_cast<uint32_t *>(&h1);
+            reinterpret_cast<uint2 *>(s.shadow)[q] = u;
+        }
+    }
+    // tail
+    if (b == 0)
+        for (int64_t i = n4 * 4 + threadIdx.x; i < s.n; i += blockDim.x) adam_one<__half>(A, s, i);
+}
+
+}  // namespace mlp
+}  // namespace fh

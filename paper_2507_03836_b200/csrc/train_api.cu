@@ -1,0 +1,224 @@
+// train_api.cu -- host side of the train step (include/fhash.h "train
+// step" section): trainer object, launch sequence, Adam bookkeeping.
+#include <cuda_runtime.h>
+
+#include <cmath>
+#include <cstring>
+#include <new>
+
+#include "internal.h"
+#include "mlp_kernels.cuh"
+
+using fh::aligned;
+using fh::cuda_check;
+using fh::fail;
+using fh::g_err;
+
+struct fh_trainer_s {
+    fh_encoder enc = nullptr;
+    int K0 = 0;
+    fh_train_buffers b{};
+    fh_adam adam{};
+    int64_t max_batch = 0;
+    int64_t step = 0;
+    int n_sm = 148;
+    // workspace carve-up
+    __nv_bfloat16 *enc_out = nullptr;  // [max_batch][K0]
+    float *dx = nullptr;               // [max_batch][K0]
+    int *flag = nullptr;               // bit 1: non-finite loss
+    float *loss_scratch = nullptr;
+};
+
+namespace {
+
+size_t align_up(size_t v, size_t a) { return (v + a - 1) / a * a; }
+
+fh_status check_mlp(fh_encoder enc, const fh_mlp_desc *m) {
+    if (!enc || !m) return fail(FH_E_ARG, "NULL encoder or MLP descriptor");
+    if (m->n_hidden != 64 || m->n_hidden_layers != 2)
+        return fail(FH_E_ARG, "MLP must be n_in -> 64 -> 64 -> 1 (n_hidden 64, 2 hidden layers)");
+    if (m->n_in != enc->L * enc->F) return fail(FH_E_ARG, "MLP n_in %d != L*F = %d", m->n_in, enc->L * enc->F);
+    if (m->n_in != 16 && m->n_in != 32 && m->n_in != 48 && m->n_in != 64)
+        return fail(FH_E_ARG, "MLP n_in must be 16, 32, 48 or 64 (got %d)", m->n_in);
+    return FH_OK;
+}
+
+template <int K0>
+fh_status launch_mlp(fh_trainer tr, const float *target, int64_t N, int64_t N_global, float *loss,
+                     cudaStream_t s) {
+    using Lo = fh::mlp::Layout<K0>;
+    // Request enough dynamic smem to keep ONE CTA per SM (the kernel owns all
+    // 512 TMEM columns of its SM).
+    const int smem = (int)(Lo::SMEM > 120 * 1024 ? Lo::SMEM : 120 * 1024);
+    fh_status st = cuda_check(cudaFuncSetAttribute(fh::mlp::mlp_train_kernel<K0>,
+                                                   cudaFuncAttributeMaxDynamicSharedMemorySize, smem),
+                              "cudaFuncSetAttribute(mlp)");
+    if (st != FH_OK) return st;
+    fh::mlp::TrainArgs a;
+    a.x = tr->enc_out;
+    a.target = target;
+    a.wsh = reinterpret_cast<const __nv_bfloat16 *>(tr->b.mlp_shadow);
+    a.wmaster = tr->b.mlp_master;
+    a.dx = tr->dx;
+    a.grad = tr->b.mlp_grad;
+    a.loss = loss;
+    a.flag = tr->flag;
+    a.N = N;
+    a.inv_n_global = (float)(1.0 / (double)N_global);
+    const int64_t tiles = (N + fh::mlp::TILE - 1) / fh::mlp::TILE;
+    const int grid = (int)(tiles < tr->n_sm ? tiles : tr->n_sm);
+    fh::mlp::mlp_train_kernel<K0><<<grid, 128, smem, s>>>(a);
+    return cuda_check(cudaGetLastError(), "mlp_train_kernel launch");
+}
+
+}  // namespace
+
+extern "C" {
+
+uint64_t fh_mlp_param_count(const fh_mlp_desc *m) {
+    return m ? (uint64_t)fh::mlp::param_count(m->n_in) : 0;
+}
+
+size_t fh_train_workspace_size(fh_encoder enc, const fh_mlp_desc *m, int64_t max_batch) {
+    if (!enc || !m || max_batch < 0) return 0;
+    const size_t K0 = (size_t)m->n_in;
+    return align_up((size_t)max_batch * K0 * 2, 256) + align_up((size_t)max_batch * K0 * 4, 256) + 256;
+}
+
+fh_status fh_trainer_create(fh_encoder enc, const fh_mlp_desc *m, const fh_train_buffers *b, const fh_adam *adam,
+                            int64_t max_batch, fh_trainer *out) {
+    g_err[0] = 0;
+    if (!out || !b || !adam) return fail(FH_E_ARG, "fh_trainer_create: NULL pointer");
+    *out = nullptr;
+    fh_status st = check_mlp(enc, m);
+    if (st != FH_OK) return st;
+    if (max_batch < 1) return fail(FH_E_ARG, "fh_trainer_create: max_batch < 1");
+    const void *need16[] = {b->table_master, b->table_grad, b->table_m, b->table_v, b->mlp_master,
+                            b->mlp_grad, b->mlp_m, b->mlp_v, b->mlp_shadow, b->workspace};
+    for (const void *p : need16)
+        if (!p || !aligned(p, 16)) return fail(FH_E_ARG, "fh_trainer_create: NULL or misaligned buffer");
+    if (enc->table_dtype == FH_F16 && (!b->table_shadow || !aligned(b->table_shadow, 32)))
+        return fail(FH_E_ARG, "fh_trainer_create: FH_F16 encoder needs a 32-byte aligned fp16 table_shadow");
+    if (enc->table_dtype == FH_F32 && b->table_shadow)
+        return fail(FH_E_ARG, "fh_trainer_create: FH_F32 encoder reads the master; pass table_shadow = NULL");
+    if (enc->table_dtype == FH_F32 && !aligned(b->table_master, 32))
+        return fail(FH_E_ARG, "fh_trainer_create: table_master must be 32-byte aligned");
+    if (b->workspace_bytes < fh_train_workspace_size(enc, m, max_batch))
+        return fail(FH_E_ARG, "fh_trainer_create: workspace too small");
+    fh_trainer tr = new (std::nothrow) fh_trainer_s();
+    if (!tr) return fail(FH_E_ARG, "fh_trainer_create: out of host memory");
+    tr->enc = enc;
+    tr->K0 = m->n_in;
+    tr->b = *b;
+    tr->adam = *adam;
+    tr->max_batch = max_batch;
+    int dev = 0;
+    cudaGetDevice(&dev);
+    cudaDeviceGetAttribute(&tr->n_sm, cudaDevAttrMultiProcessorCount, dev);
+    char *w = reinterpret_cast<char *>(b->workspace);
+    tr->enc_out = reinterpret_cast<__nv_bfloat16 *>(w);
+    w += align_up((size_t)max_batch * tr->K0 * 2, 256);
+    tr->dx = reinterpret_cast<float *>(w);
+    w += align_up((size_t)max_batch * tr->K0 * 4, 256);
+    tr->flag = reinterpret_cast<int *>(w);
+    tr->loss_scratch = reinterpret_cast<float *>(w + 16);
+    st = cuda_check(cudaMemset(tr->flag, 0, 32), "fh_trainer_create: clear flags");
+    if (st != FH_OK) { delete tr; return st; }
+    *out = tr;
+    return FH_OK;
+}
+
+fh_status fh_train_fwd_bwd(fh_trainer tr, const float *coords, const float *target, int64_t N, int64_t N_global,
+                           float *loss_dev, fh_stream stream) {
+    g_err[0] = 0;
+    if (!tr) return fail(FH_E_ARG, "fh_train_fwd_bwd: NULL trainer");
+    if (N < 0 || N > tr->max_batch || N_global < N || N_global < 1)
+        return fail(FH_E_ARG, "fh_train_fwd_bwd: need 0 <= N_local <= max_batch and N_global >= max(N_local, 1)");
+    if (N > 0 && (!coords || !target)) return fail(FH_E_ARG, "fh_train_fwd_bwd: NULL coords/target");
+    cudaStream_t s = reinterpret_cast<cudaStream_t>(stream);
+    float *loss = loss_dev ? loss_dev : tr->loss_scratch;
+    fh_status st = cuda_check(cudaMemsetAsync(loss, 0, sizeof(float), s), "zero loss");
+    if (st != FH_OK || N == 0) return st;
+    const void *table = tr->b.table_shadow ? tr->b.table_shadow : tr->b.table_master;
+    if ((st = fh_encode_fwd(tr->enc, coords, N, table, tr->enc_out, FH_BF16, stream)) != FH_OK) return st;
+    switch (tr->K0) {
+        case 16: st = launch_mlp<16>(tr, target, N, N_global, loss, s); break;
+        case 32: st = launch_mlp<32>(tr, target, N, N_global, loss, s); break;
+        case 48: st = launch_mlp<48>(tr, target, N, N_global, loss, s); break;
+        default: st = launch_mlp<64>(tr, target, N, N_global, loss, s); break;
+    }
+    if (st != FH_OK) return st;
+    return fh_encode_bwd(tr->enc, coords, N, tr->dx, tr->b.table_grad, stream);
+}
+
+fh_status fh_train_apply(fh_trainer tr, fh_stream stream) {
+    g_err[0] = 0;
+    if (!tr) return fail(FH_E_ARG, "fh_train_apply: NULL trainer");
+    tr->step += 1;
+    const double t = (double)tr->step;
+    fh::mlp::AdamArgs A;
+    A.lr = tr->adam.lr;
+    A.b1 = tr->adam.beta1;
+    A.b2 = tr->adam.beta2;
+    A.eps = tr->adam.eps;
+    A.omb1 = (float)(1.0 - (double)tr->adam.beta1);
+    A.omb2 = (float)(1.0 - (double)tr->adam.beta2);
+    A.c1 = (float)(1.0 / (1.0 - std::pow((double)tr->adam.beta1, t)));
+    A.c2 = (float)(1.0 / (1.0 - std::pow((double)tr->adam.beta2, t)));
+    fh::mlp::AdamSeg &T = A.seg[0];
+    T.p = tr->b.table_master;
+    T.g = tr->b.table_grad;
+    T.m = tr->b.table_m;
+    T.v = tr->b.table_v;
+    T.shadow = tr->b.table_shadow;
+    T.n = (int64_t)(tr->enc->entries * (uint64_t)tr->enc->F);
+    T.kind = tr->b.table_shadow ? 1 : 0;
+    fh::mlp::AdamSeg &M = A.seg[1];
+    M.p = tr->b.mlp_master;
+    M.g = tr->b.mlp_grad;
+    M.m = tr->b.mlp_m;
+    M.v = tr->b.mlp_v;
+    M.shadow = tr->b.mlp_shadow;
+    M.n = fh::mlp::param_count(tr->K0);
+    M.kind = 2;
+    // segment 0: enough blocks for ~4 float4 per thread; segment 1: a few blocks
+    const int64_t n4 = T.n / 4;
+    int64_t b0 = (n4 + 256 * 4 - 1) / (256 * 4);
+    const int64_t cap = (int64_t)tr->n_sm * 16;
+    if (b0 > cap) b0 = cap;
+    if (b0 < 1) b0 = 1;
+    A.blocks0 = b0;
+    const int64_t b1 = 4;
+    cudaStream_t s = reinterpret_cast<cudaStream_t>(stream);
+    fh::mlp::adam_kernel<<<(unsigned)(b0 + b1), 256, 0, s>>>(A);
+    return cuda_check(cudaGetLastError(), "adam_kernel launch");
+}
+
+fh_status fh_train_step(fh_trainer tr, const float *coords, const float *target, int64_t N, int64_t N_global,
+                        float *loss_dev, fh_stream stream) {
+    fh_status st = fh_train_fwd_bwd(tr, coords, target, N, N_global, loss_dev, stream);
+    if (st != FH_OK) return st;
+    return fh_train_apply(tr, stream);
+}
+
+fh_status fh_trainer_status(fh_trainer tr, fh_stream stream) {
+    g_err[0] = 0;
+    if (!tr) return fail(FH_E_ARG, "fh_trainer_status: NULL trainer");
+    fh_status st = fh_status_sync(tr->enc, stream);
+    if (st != FH_OK && st != FH_E_DOMAIN) return st;
+    int h = 0;
+    fh_status st2 = cuda_check(cudaMemcpy(&h, tr->flag, sizeof(int), cudaMemcpyDeviceToHost), "read trainer flag");
+    if (st2 != FH_OK) return st2;
+    if (h & 2) {
+        cudaMemset(tr->flag, 0, sizeof(int));
+        return fail(FH_E_DIVERGED, "non-finite loss in the train step");
+    }
+    if (st == FH_E_DOMAIN) return fail(FH_E_DOMAIN, "out-of-domain or NaN coordinates were clamped to [0,1]");
+    return FH_OK;
+}
+
+int64_t fh_trainer_step_count(fh_trainer tr) { return tr ? tr->step : -1; }
+
+void fh_trainer_destroy(fh_trainer tr) { delete tr; }
+
+}  // extern "C"

@@ -30,6 +30,9 @@ EXPORTS = [
     "fh_version",
     # include/fhash_bench.h (measurement kernels)
     "fh_bench_gather", "fh_bench_red", "fh_bench_copy",
+    # train step
+    "fh_mlp_param_count", "fh_train_workspace_size", "fh_trainer_create", "fh_train_fwd_bwd", "fh_train_apply",
+    "fh_train_step", "fh_trainer_status", "fh_trainer_step_count", "fh_trainer_destroy",
 ]
 
 
@@ -217,3 +220,139 @@ def bench_red(buf, n_entries: int, entry_bytes: int, n_threads: int, mode: int =
 
 def bench_copy(dst, src, nbytes: int, stream=None):
     _check(lib().fh_bench_copy(_ptr(dst), _ptr(src), nbytes, _stream(stream)))
+
+
+# ------------------------------------------------------------ train step
+class MLPDesc(ctypes.Structure):
+    _fields_ = [("n_in", ctypes.c_int), ("n_hidden", ctypes.c_int), ("n_hidden_layers", ctypes.c_int)]
+
+
+class TrainBuffers(ctypes.Structure):
+    _fields_ = [(n, ctypes.c_void_p) for n in ("table_master", "table_shadow", "table_grad", "table_m", "table_v",
+                                               "mlp_master", "mlp_shadow", "mlp_grad", "mlp_m", "mlp_v",
+                                               "workspace")] + [("workspace_bytes", ctypes.c_size_t)]
+
+
+class AdamCfg(ctypes.Structure):
+    _fields_ = [("lr", ctypes.c_double), ("beta1", ctypes.c_double), ("beta2", ctypes.c_double),
+                ("eps", ctypes.c_double)]
+
+
+def _train_lib():
+    L = lib()
+    if getattr(L, "_train_ready", False):
+        return L
+    vp, i64 = ctypes.c_void_p, ctypes.c_int64
+    L.fh_mlp_param_count.argtypes = [ctypes.POINTER(MLPDesc)]
+    L.fh_mlp_param_count.restype = ctypes.c_uint64
+    L.fh_train_workspace_size.argtypes = [vp, ctypes.POINTER(MLPDesc), i64]
+    L.fh_train_workspace_size.restype = ctypes.c_size_t
+    L.fh_trainer_create.argtypes = [vp, ctypes.POINTER(MLPDesc), ctypes.POINTER(TrainBuffers),
+                                    ctypes.POINTER(AdamCfg), i64, ctypes.POINTER(vp)]
+    L.fh_train_fwd_bwd.argtypes = [vp, vp, vp, i64, i64, vp, vp]
+    L.fh_train_step.argtypes = [vp, vp, vp, i64, i64, vp, vp]
+    L.fh_train_apply.argtypes = [vp, vp]
+    L.fh_trainer_status.argtypes = [vp, vp]
+    L.fh_trainer_step_count.argtypes = [vp]
+    L.fh_trainer_step_count.restype = i64
+    L.fh_trainer_destroy.argtypes = [vp]
+    L.fh_trainer_destroy.restype = None
+    for n in ("fh_trainer_create", "fh_train_fwd_bwd", "fh_train_step", "fh_train_apply", "fh_trainer_status"):
+        getattr(L, n).restype = ctypes.c_int
+    L._train_ready = True
+    return L
+
+
+class Trainer:
+    """Handle on an fh_trainer plus the device buffers it trains (torch
+    tensors on the current device; allocation only).
+
+    grads: ONE flat fp32 tensor [table (padded to 4) | mlp] so that a data
+    parallel caller all-reduces a single buffer between fwd_bwd() and
+    apply()."""
+
+    def __init__(self, enc: "Encoder", table_init, mlp_layers, max_batch: int, lr: float = 0.01,
+                 beta1: float = 0.9, beta2: float = 0.999, eps: float = 1e-8):
+        import numpy as np
+        import torch
+        L = _train_lib()
+        self.enc = enc
+        self.K0 = enc.L * enc.F
+        self.desc = MLPDesc(self.K0, 64, 2)
+        dev = torch.device("cuda", torch.cuda.current_device())
+        nt = enc.entries * enc.F
+        nt_pad = (nt + 3) // 4 * 4
+        P = int(L.fh_mlp_param_count(ctypes.byref(self.desc)))
+        self.n_table, self.n_mlp = nt, P
+        f32 = dict(dtype=torch.float32, device=dev)
+        self.table_master = torch.as_tensor(np.asarray(table_init, dtype=np.float32)).reshape(enc.entries, enc.F).to(dev)
+        self.table_shadow = self.table_master.half() if enc.table_dtype == "f16" else None
+        self.grads = torch.zeros(nt_pad + P, **f32)
+        self.table_grad = self.grads[:nt].view(enc.entries, enc.F)
+        self.mlp_grad = self.grads[nt_pad:]
+        self.table_m = torch.zeros(nt, **f32)
+        self.table_v = torch.zeros(nt, **f32)
+        flat = []
+        for W, b in mlp_layers:
+            flat += [np.asarray(W, np.float32).ravel(), np.asarray(b, np.float32).ravel()]
+        flat = np.concatenate(flat)
+        assert flat.size == P, (flat.size, P)
+        self.mlp_master = torch.from_numpy(flat).to(dev)
+        self.mlp_shadow = self.mlp_master.bfloat16()
+        self.mlp_m = torch.zeros(P, **f32)
+        self.mlp_v = torch.zeros(P, **f32)
+        ws = int(L.fh_train_workspace_size(enc.handle, ctypes.byref(self.desc), max_batch))
+        self.workspace = torch.zeros(ws, dtype=torch.uint8, device=dev)
+        self.max_batch = max_batch
+        b = TrainBuffers(self.table_master.data_ptr(), _ptr(self.table_shadow), self.table_grad.data_ptr(),
+                         self.table_m.data_ptr(), self.table_v.data_ptr(), self.mlp_master.data_ptr(),
+                         self.mlp_shadow.data_ptr(), self.mlp_grad.data_ptr(), self.mlp_m.data_ptr(),
+                         self.mlp_v.data_ptr(), self.workspace.data_ptr(), ws)
+        self._bufs = b
+        adam = AdamCfg(lr, beta1, beta2, eps)
+        h = ctypes.c_void_p()
+        _check(L.fh_trainer_create(enc.handle, ctypes.byref(self.desc), ctypes.byref(b), ctypes.byref(adam),
+                                   max_batch, ctypes.byref(h)))
+        self._h = h
+        self.loss = torch.zeros(1, **f32)
+
+    def __del__(self):
+        h = getattr(self, "_h", None)
+        if h is not None and h.value and _lib is not None:
+            _lib.fh_trainer_destroy(h)
+            self._h = None
+
+    # workspace views (read-only use in tests)
+    def enc_out(self, N):
+        import torch
+        return self.workspace[: N * self.K0 * 2].view(torch.bfloat16).view(N, self.K0)
+
+    def dx(self, N):
+        import torch
+        off = (self.max_batch * self.K0 * 2 + 255) // 256 * 256
+        return self.workspace[off: off + N * self.K0 * 4].view(torch.float32).view(N, self.K0)
+
+    def fwd_bwd(self, coords, target, n_global=None, stream=None):
+        N = coords.shape[0]
+        _check(_train_lib().fh_train_fwd_bwd(self._h, _ptr(coords), _ptr(target), N, n_global or N,
+                                             self.loss.data_ptr(), _stream(stream)))
+        return self.loss
+
+    def apply(self, stream=None):
+        _check(_train_lib().fh_train_apply(self._h, _stream(stream)))
+
+    def step(self, coords, target, n_global=None, stream=None):
+        N = coords.shape[0]
+        _check(_train_lib().fh_train_step(self._h, _ptr(coords), _ptr(target), N, n_global or N,
+                                          self.loss.data_ptr(), _stream(stream)))
+        return self.loss
+
+    def status(self, stream=None) -> int:
+        s = _train_lib().fh_trainer_status(self._h, _stream(stream))
+        if s not in (FH_OK, FH_E_DOMAIN, FH_E_DIVERGED):
+            _check(s)
+        return s
+
+    @property
+    def step_count(self) -> int:
+        return int(_train_lib().fh_trainer_step_count(self._h))

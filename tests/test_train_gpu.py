@@ -1,0 +1,160 @@
+"""GPU parity of the train step (a8 MLP fwd/bwd on tcgen05, a9 MSE, a10
+encode bwd of dL/d(enc), a11 Adam) against Oracle-T.  -m gpu.
+
+Following SURVEY.md §8(c), the MLP oracle is fed the GPU's own bf16 encoder
+output (so a bf16 rounding flip in the encode does not propagate), and the
+encode backward is checked with the GPU's own dL/d(enc) as upstream.
+Tolerances: loss 1e-3 relative; MLP grads and dL/d(enc)
+within 1e-2 of the tensor's max magnitude (bf16 operands, fp32 accumulation
+in a different order, occasional one-ulp bf16 flips of h / dz); table grads
+1e-5 * sum|W g|; Adam elementwise 1e-6 relative (+ lr-scaled floor).
+"""
+import numpy as np
+import pytest
+import torch
+
+import oracle
+from oracle import train as T
+import workloads as W
+
+pytestmark = pytest.mark.gpu
+
+if torch.cuda.is_available():
+    from paper_2507_03836_b200 import fhash as fh
+
+
+def small_cfg(F, L, tdt="f16", cap=1 << 12):
+    levels = tuple((s, s, s, t) for s, t in zip(W.geometric(4, 24, L), W.geometric(2, 6, L)))
+    return W.EncoderConfig(f"t{L}x{F}", levels, F=F, cap=cap, table_dtype=tdt)
+
+
+def make(cfg, N, seed=0, max_batch=None):
+    g = W.rng(seed)
+    enc = fh.Encoder(cfg.levels, cfg.F, cfg.table_dtype, cfg.cap)
+    table = W.draw_table(g, enc.entries, cfg.F, "f32")
+    layers = W.draw_mlp(g, W.MLPConfig((cfg.L * cfg.F, 64, 64, 1)))
+    coords = W.draw_coords(g, N)
+    target = g.random(N, dtype=np.float32)
+    tr = fh.Trainer(enc, table, layers, max_batch or N)
+    return enc, tr, coords, target
+
+
+@pytest.mark.parametrize("F,L,N", [(4, 4, 1000), (2, 16, 1000), (4, 16, 777), (2, 16, 128), (4, 12, 3000)])
+def test_mlp_fwd_bwd_parity(F, L, N):
+    cfg = small_cfg(F, L)
+    enc, tr, coords, target = make(cfg, N, seed=F * 100 + L)
+    c, t = torch.from_numpy(coords).cuda(), torch.from_numpy(target).cuda()
+    n_global = N + 17  # exercise the 1/N_global scaling
+    loss = tr.fwd_bwd(c, t, n_global)
+    assert tr.status() == fh.FH_OK
+    x0 = tr.enc_out(N).float().cpu().numpy().astype(np.float64)
+    master = tr.mlp_master.cpu().numpy().astype(np.float64)
+    K0 = cfg.L * cfg.F
+    o = 0
+    layers = []
+    for fi, fo in ((K0, 64), (64, 64), (64, 1)):
+        Wt = master[o:o + fi * fo].reshape(fo, fi); o += fi * fo
+        b = master[o:o + fo]; o += fo
+        layers.append((Wt, b))
+    y, cache = T.mlp_forward(x0, layers)
+    ref_loss, dy = T.mse_loss(y, target.astype(np.float64), n_global)
+    grads, dx0 = T.mlp_backward(dy, layers, cache)
+    assert abs(loss.item() - ref_loss) <= 1e-3 * abs(ref_loss)
+    g = tr.mlp_grad.cpu().numpy().astype(np.float64)
+    o = 0
+    for (dW, db) in grads:
+        for ref in (dW.ravel(), db.ravel()):
+            got = g[o:o + ref.size]; o += ref.size
+            tol = 1e-2 * np.max(np.abs(ref)) + 1e-12
+            assert np.max(np.abs(got - ref)) <= tol, (o, np.max(np.abs(got - ref)), tol)
+    dx = tr.dx(N).cpu().numpy().astype(np.float64)
+    assert np.max(np.abs(dx - dx0)) <= 1e-2 * np.max(np.abs(dx0))
+    # encode bwd of the GPU's own dL/d(enc), against Oracle-B (strict)
+    ref = oracle.Levels(cfg.levels, cfg.cap)
+    G, A = ref.backward(coords, dx, cfg.F, want_abs=True)
+    got = tr.table_grad.cpu().numpy().astype(np.float64)
+    assert np.all(got[A == 0] == 0)
+    assert np.all(np.abs(got - G) <= 1e-5 * A)
+
+
+def test_encoder_output_is_bf16_of_forward():
+    cfg = small_cfg(2, 16)
+    enc, tr, coords, target = make(cfg, 500, seed=3)
+    tr.fwd_bwd(torch.from_numpy(coords).cuda(), torch.from_numpy(target).cuda())
+    x0 = tr.enc_out(500).float().cpu().numpy().astype(np.float64)
+    ref = oracle.Levels(cfg.levels, cfg.cap)
+    r, ab = ref.forward(coords, tr.table_shadow.float().cpu().numpy().astype(np.float64), want_abs=True)
+    half_ulp = np.ldexp(1.0, np.frexp(np.abs(r))[1] - 9)
+    assert np.all(np.abs(x0 - r) <= half_ulp + 2e-6 * ab + 1e-30)
+
+
+def test_adam_parity_and_shadows():
+    cfg = small_cfg(4, 8)
+    enc, tr, coords, target = make(cfg, 256, seed=5)
+    g = torch.Generator("cuda").manual_seed(1)
+    p0 = (tr.table_master.clone(), tr.mlp_master.clone())
+    for step in (1, 2, 3):
+        gr = torch.randn(tr.grads.shape, device="cuda", generator=g) * 0.1
+        tr.grads.copy_(gr)
+        before = [x.clone().cpu().numpy().astype(np.float64) for x in
+                  (tr.table_master, tr.table_m, tr.table_v, tr.mlp_master, tr.mlp_m, tr.mlp_v)]
+        grn = gr.cpu().numpy().astype(np.float64)
+        tr.apply()
+        torch.cuda.synchronize()
+        assert tr.step_count == step
+        nt_pad = (tr.n_table + 3) // 4 * 4
+        for (p, m, v), gseg, (pg, mg, vg) in (
+                ((before[0].ravel(), before[1], before[2]), grn[:tr.n_table],
+                 (tr.table_master, tr.table_m, tr.table_v)),
+                ((before[3], before[4], before[5]), grn[nt_pad:], (tr.mlp_master, tr.mlp_m, tr.mlp_v))):
+            rp, rm, rv = T.adam_step(p, gseg, m, v, step)
+            gp = pg.cpu().numpy().ravel().astype(np.float64)
+            assert np.all(np.abs(gp - rp) <= 1e-6 * (np.abs(rp) + 0.01))
+            # m = b1 m + (1-b1) g cancels: bound by the magnitude of its terms
+            assert np.all(np.abs(mg.cpu().numpy() - rm) <= 1e-6 * (0.9 * np.abs(m) + 0.1 * np.abs(gseg)) + 1e-12)
+            assert np.allclose(vg.cpu().numpy(), rv, rtol=1e-6, atol=1e-15)
+        assert torch.all(tr.grads == 0)
+        assert torch.equal(tr.table_shadow, tr.table_master.half())
+        assert torch.equal(tr.mlp_shadow, tr.mlp_master.bfloat16())
+    assert not torch.equal(p0[0], tr.table_master)
+
+
+def test_zero_lr_leaves_parameters():
+    cfg = small_cfg(2, 8)
+    g = W.rng(0)
+    enc = fh.Encoder(cfg.levels, cfg.F, cfg.table_dtype, cfg.cap)
+    tr = fh.Trainer(enc, W.draw_table(g, enc.entries, 2), W.draw_mlp(g, W.MLPConfig((16, 64, 64, 1))), 512, lr=0.0)
+    p0 = tr.mlp_master.clone(), tr.table_master.clone()
+    c = torch.rand(512, 4, device="cuda")
+    tr.step(c, torch.rand(512, device="cuda"))
+    torch.cuda.synchronize()
+    assert torch.equal(p0[0], tr.mlp_master) and torch.equal(p0[1], tr.table_master)
+
+
+def test_training_reduces_loss_on_moving_gaussians():
+    """End-to-end sanity (not parity): the cfg3 field recipe at 32^3 x 8,
+    training on random voxels reduces the MSE by > 10x in 200 steps."""
+    field = torch.from_numpy(W.gaussian_blobs_field(W.rng(0), S=32, T=8)).cuda()
+    levels = tuple((s, s, s, t) for s, t in zip(W.geometric(4, 32, 8), W.geometric(2, 8, 8)))
+    enc = fh.Encoder(levels, 4, "f16", 1 << 14)
+    g = W.rng(1)
+    tr = fh.Trainer(enc, W.draw_table(g, enc.entries, 4), W.draw_mlp(g, W.MLPConfig((32, 64, 64, 1))), 1 << 14)
+    gen = torch.Generator("cuda").manual_seed(0)
+    losses = []
+    for it in range(200):
+        idx = torch.randint(0, field.numel(), (1 << 14,), device="cuda", generator=gen)
+        x = idx % 32; y = (idx // 32) % 32; z = (idx // 1024) % 32; t = idx // 32768
+        coords = torch.stack([x / 31.0, y / 31.0, z / 31.0, t / 7.0], 1).float().contiguous()
+        target = field.view(-1)[idx].contiguous()
+        losses.append(tr.step(coords, target).item())
+    assert tr.status() == fh.FH_OK
+    assert np.mean(losses[-10:]) < 0.1 * np.mean(losses[:5]), (losses[:5], losses[-10:])
+
+
+def test_divergence_flag():
+    cfg = small_cfg(2, 8)
+    enc, tr, coords, target = make(cfg, 300, seed=9)
+    target[5] = np.inf
+    tr.fwd_bwd(torch.from_numpy(coords).cuda(), torch.from_numpy(target).cuda())
+    assert tr.status() == fh.FH_E_DIVERGED
+    assert tr.status() == fh.FH_OK
