@@ -218,6 +218,79 @@ def microbench_roofline(fh, torch, enc, cfg, N, stream, hbm_peak):
     }
 
 
+def train_step_bench(fh, torch, W, which, rank, world, dist, steps, warmup):
+    """All §8(a) rows in one step: Philox voxel sampling from the synthetic
+    field, encode fwd (fp16 table -> bf16), tcgen05 MLP fwd + MSE + bwd,
+    encode bwd, [NCCL all-reduce of the flat fp32 grads over NVLink when
+    world > 1], fused Adam.
+      cfg3: BASELINE.json configs[2], 256^3 x 32 Gaussian blobs, batch 2^18 (N=1)
+      cfg5: BASELINE.json configs[4], configs[3] field + encoder, global
+            batch 2^24 split over the ranks (strong scaling)."""
+    import numpy as np
+    if which == "cfg3":
+        blobs = W.gaussian_blob_params(W.rng(0))
+        field = fh.field_gaussian_blobs(256, 32, blobs)
+        cfg, mlp, n_global = W.CFG3, W.MLP3, W.N_CFG3 * world
+    else:
+        field = fh.field_value_noise(640, 256, 256, 100, seed=0, band=0.02)
+        cfg, mlp, n_global = W.CFG4, W.MLP4, 1 << 24
+    n_local = n_global // world
+    enc = fh.Encoder(cfg.levels, cfg.F, cfg.table_dtype, cfg.cap)
+    gen = torch.Generator("cuda").manual_seed(0)           # identical init on every rank
+    table0 = (torch.rand((enc.entries, cfg.F), device="cuda", generator=gen) * 2 - 1) * 1e-4
+    tr = fh.Trainer(enc, table0, W.draw_mlp(W.rng(0), mlp), n_local)
+    del table0
+    coords = torch.empty((n_local, 4), device="cuda")
+    target = torch.empty((n_local,), device="cuda")
+    stream = torch.cuda.current_stream()
+
+    def one(k, ev=None):
+        if ev: ev[0].record(stream)
+        fh.sample_voxels(field, n_local, seed=1234, subsequence=rank, offset=k, coords=coords, target=target)
+        if ev: ev[1].record(stream)
+        loss = tr.fwd_bwd(coords, target, n_global)
+        if ev: ev[2].record(stream)
+        if world > 1:
+            dist.all_reduce(tr.grads)
+        if ev: ev[3].record(stream)
+        tr.apply()
+        if ev: ev[4].record(stream)
+        return loss
+
+    losses = []
+    for k in range(max(warmup, 3)):
+        losses.append(one(k).item())
+    ev = [[torch.cuda.Event(enable_timing=True) for _ in range(5)] for _ in range(steps)]
+    if dist:
+        dist.barrier()
+    torch.cuda.synchronize()
+    for k in range(steps):
+        one(1000 + k, ev[k])
+    torch.cuda.synchronize()
+    total = sum(e[0].elapsed_time(e[4]) for e in ev) / 1e3
+    phase = [sum(e[i].elapsed_time(e[i + 1]) for e in ev) / steps for i in range(4)]
+    if dist:
+        t = torch.tensor([total], device="cuda", dtype=torch.float64)
+        dist.all_reduce(t, op=dist.ReduceOp.MAX)
+        total = float(t.item())
+    last = tr.loss.clone()
+    if dist:
+        dist.all_reduce(last)
+    st = tr.status()
+    return {
+        "workload": f"{which}: " + ("BASELINE.json configs[2] train_step (256^3x32 Gaussian blobs, L=16 F=2 fp16, "
+                                    "MLP 32-64-64-1 bf16, batch 2^18)" if which == "cfg3" else
+                                    "BASELINE.json configs[4] DP train_step (configs[3] field 640x256x256x100, "
+                                    "L=16 F=4 fp16 cap 2^22, MLP 64-64-64-1, global batch 2^24)"),
+        "value": n_global * steps / total, "unit": "samples/s", "ms_per_step": total * 1e3 / steps,
+        "global_batch": n_global, "per_gpu_batch": n_local, "n_gpus": world,
+        "scaling": "strong" if which == "cfg5" else "weak",
+        "phase_ms": {"sample": phase[0], "fwd_bwd": phase[1], "allreduce": phase[2], "adam": phase[3]},
+        "loss_first_warmup": losses[0], "loss_last": float(last.item()), "status": int(st),
+        "params": enc.param_count + tr.n_mlp, "gpu_launches_per_step": 6,
+    }
+
+
 def run_ours(args, rank, local_rank, world):
     import numpy as np
     import torch
@@ -312,6 +385,18 @@ def run_ours(args, rank, local_rank, world):
            "d2h_bytes_per_step": N * cfg.L * cfg.F * 4 + enc.entries * cfg.F * 4, "steps": ke,
            "api": "fh_encode_step_host (pinned host in/out)"}
 
+    # Train step (all §8(a) rows): free the encode buffers first.
+    train = {}
+    if not args.no_train:
+        del coords_h, dout_h, out_h, dtable_h, out, dout, dtable, flush
+        torch.cuda.empty_cache()
+        kt = max(3, min(K, 10))
+        if world == 1:
+            train["cfg3"] = train_step_bench(fh, torch, W, "cfg3", rank, world, dist, kt, args.warmup)
+            torch.cuda.empty_cache()
+        train["cfg5"] = train_step_bench(fh, torch, W, "cfg5", rank, world, dist, kt, args.warmup)
+        torch.cuda.empty_cache()
+
     if rank != 0:
         if dist:
             dist.destroy_process_group()
@@ -348,7 +433,7 @@ def run_ours(args, rank, local_rank, world):
         "dtype": "f32", "data": "synthetic", "config": config_block(cfg, N, world),
         "kernels_ms": {"zero_grad": zero_ms, "encode_fwd": fwd_ms, "encode_bwd": bwd_ms, "step": step_ms},
         "roofline": roofline, "gather_roofline": gather_roofline, "cpu_baseline": cpu, "e2e": e2e,
-        "gpu_launches": 2 * K, "clocks": clk.summary(),
+        "gpu_launches": 2 * K, "clocks": clk.summary(), "train_step": train,
     }
     print(json.dumps(line), flush=True)
     if dist:
@@ -362,6 +447,7 @@ def main():
     ap.add_argument("--warmup", type=int, default=5)
     ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
     ap.add_argument("--no-cpu-baseline", action="store_true")
+    ap.add_argument("--no-train", action="store_true", help="skip the train_step (cfg3 / cfg5) sub-benchmarks")
     args = ap.parse_args()
     rank = env_int("RANK", 0)
     local_rank = env_int("LOCAL_RANK", 0)

@@ -33,6 +33,8 @@ EXPORTS = [
     # train step
     "fh_mlp_param_count", "fh_train_workspace_size", "fh_trainer_create", "fh_train_fwd_bwd", "fh_train_apply",
     "fh_train_step", "fh_trainer_status", "fh_trainer_step_count", "fh_trainer_destroy",
+    # include/fhash_data.h (synthetic data, harness)
+    "fh_data_gaussian_blobs", "fh_data_value_noise", "fh_data_normalize", "fh_data_sample_voxels",
 ]
 
 
@@ -285,7 +287,11 @@ class Trainer:
         P = int(L.fh_mlp_param_count(ctypes.byref(self.desc)))
         self.n_table, self.n_mlp = nt, P
         f32 = dict(dtype=torch.float32, device=dev)
-        self.table_master = torch.as_tensor(np.asarray(table_init, dtype=np.float32)).reshape(enc.entries, enc.F).to(dev)
+        if isinstance(table_init, torch.Tensor):
+            self.table_master = table_init.to(device=dev, dtype=torch.float32).reshape(enc.entries, enc.F).contiguous()
+        else:
+            self.table_master = torch.as_tensor(np.asarray(table_init, dtype=np.float32)).reshape(
+                enc.entries, enc.F).to(dev)
         self.table_shadow = self.table_master.half() if enc.table_dtype == "f16" else None
         self.grads = torch.zeros(nt_pad + P, **f32)
         self.table_grad = self.grads[:nt].view(enc.entries, enc.F)
@@ -356,3 +362,59 @@ class Trainer:
     @property
     def step_count(self) -> int:
         return int(_train_lib().fh_trainer_step_count(self._h))
+
+
+# ------------------------------------------------------------ synthetic data (harness)
+def _data_lib():
+    L = lib()
+    if getattr(L, "_data_ready", False):
+        return L
+    vp, c_int, i64 = ctypes.c_void_p, ctypes.c_int, ctypes.c_int64
+    L.fh_data_gaussian_blobs.argtypes = [vp, c_int, c_int, c_int, vp, vp]
+    L.fh_data_value_noise.argtypes = [vp, c_int, c_int, c_int, c_int, ctypes.c_uint32, vp]
+    L.fh_data_normalize.argtypes = [vp, i64, ctypes.c_float, vp, vp]
+    L.fh_data_sample_voxels.argtypes = [vp, c_int, c_int, c_int, c_int, i64, ctypes.c_uint64, ctypes.c_uint32,
+                                        ctypes.c_uint32, vp, vp, vp]
+    for n in ("fh_data_gaussian_blobs", "fh_data_value_noise", "fh_data_normalize", "fh_data_sample_voxels"):
+        getattr(L, n).restype = c_int
+    L._data_ready = True
+    return L
+
+
+def field_gaussian_blobs(S: int, T: int, blobs, stream=None):
+    """BASELINE.json configs[2] field on the device, normalised to [0,1].
+    blobs: [n][7] float32 host array (sigma, c0xyz, vxyz)."""
+    import numpy as np
+    import torch
+    b = np.ascontiguousarray(blobs, dtype=np.float32)
+    f = torch.empty((T, S, S, S), dtype=torch.float32, device="cuda")
+    scratch = torch.empty(16, dtype=torch.float32, device="cuda")
+    L = _data_lib()
+    _check(L.fh_data_gaussian_blobs(f.data_ptr(), S, T, b.shape[0], b.ctypes.data, _stream(stream)))
+    _check(L.fh_data_normalize(f.data_ptr(), f.numel(), 0.0, scratch.data_ptr(), _stream(stream)))
+    return f
+
+
+def field_value_noise(Sx: int, Sy: int, Sz: int, T: int, seed: int = 0, band: float = 0.02, stream=None):
+    """BASELINE.json configs[3] field on the device: 3-octave 4D value noise
+    with a sharp isosurface band, normalised to [0,1]."""
+    import torch
+    f = torch.empty((T, Sz, Sy, Sx), dtype=torch.float32, device="cuda")
+    scratch = torch.empty(16, dtype=torch.float32, device="cuda")
+    L = _data_lib()
+    _check(L.fh_data_value_noise(f.data_ptr(), Sx, Sy, Sz, T, seed, _stream(stream)))
+    _check(L.fh_data_normalize(f.data_ptr(), f.numel(), band, scratch.data_ptr(), _stream(stream)))
+    return f
+
+
+def sample_voxels(field, N: int, seed: int, subsequence: int, offset: int, coords=None, target=None, stream=None):
+    """Philox voxel sampler: returns (coords [N][4], target [N])."""
+    import torch
+    T, Sz, Sy, Sx = field.shape
+    if coords is None:
+        coords = torch.empty((N, 4), dtype=torch.float32, device=field.device)
+    if target is None:
+        target = torch.empty((N,), dtype=torch.float32, device=field.device)
+    _check(_data_lib().fh_data_sample_voxels(field.data_ptr(), Sx, Sy, Sz, T, N, seed, subsequence, offset,
+                                             coords.data_ptr(), target.data_ptr(), _stream(stream)))
+    return coords, target

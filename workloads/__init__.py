@@ -175,6 +175,15 @@ def draw_mlp(g: np.random.Generator, m: MLPConfig) -> List[Tuple[np.ndarray, np.
     return layers
 
 
+def gaussian_blob_params(g: np.random.Generator, blobs: int = 8) -> np.ndarray:
+    """[blobs][7] = (sigma, c0x, c0y, c0z, vx, vy, vz): sigma ~ U(0.05, 0.15),
+    c0 ~ U(0.2, 0.8)^3, v ~ U(-0.3, 0.3)^3."""
+    sig = g.uniform(0.05, 0.15, size=blobs)
+    c0 = g.uniform(0.2, 0.8, size=(blobs, 3))
+    v = g.uniform(-0.3, 0.3, size=(blobs, 3))
+    return np.concatenate([sig[:, None], c0, v], axis=1).astype(np.float32)
+
+
 def gaussian_blobs_field(g: np.random.Generator, S: int = 256, T: int = 32, blobs: int = 8,
                          dtype=np.float32) -> np.ndarray:
     """BASELINE.json configs[2] field: sum of 8 Gaussian blobs moving
