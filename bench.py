@@ -226,7 +226,7 @@ def train_step_bench(fh, torch, W, which, rank, world, dist, steps, warmup):
       cfg3: BASELINE.json configs[2], 256^3 x 32 Gaussian blobs, batch 2^18 (N=1)
       cfg5: BASELINE.json configs[4], configs[3] field + encoder, global
             batch 2^24 split over the ranks (strong scaling)."""
-    import numpy as np
+    from paper_2507_03836_b200 import dp
     if which == "cfg3":
         blobs = W.gaussian_blob_params(W.rng(0))
         field = fh.field_gaussian_blobs(256, 32, blobs)
@@ -251,7 +251,7 @@ def train_step_bench(fh, torch, W, which, rank, world, dist, steps, warmup):
         loss = tr.fwd_bwd(coords, target, n_global)
         if ev: ev[2].record(stream)
         if world > 1:
-            dist.all_reduce(tr.grads)
+            dp.allreduce_grads(tr.grads)      # NCCL SUM over NVLink/NVSwitch
         if ev: ev[3].record(stream)
         tr.apply()
         if ev: ev[4].record(stream)
@@ -273,6 +273,8 @@ def train_step_bench(fh, torch, W, which, rank, world, dist, steps, warmup):
         t = torch.tensor([total], device="cuda", dtype=torch.float64)
         dist.all_reduce(t, op=dist.ReduceOp.MAX)
         total = float(t.item())
+    # DP correctness: after the timed steps the replicas must be bit-identical
+    same = dp.replicas_identical(tr.table_master) and dp.replicas_identical(tr.mlp_master)
     last = tr.loss.clone()
     if dist:
         dist.all_reduce(last)
@@ -287,7 +289,7 @@ def train_step_bench(fh, torch, W, which, rank, world, dist, steps, warmup):
         "scaling": "strong" if which == "cfg5" else "weak",
         "phase_ms": {"sample": phase[0], "fwd_bwd": phase[1], "allreduce": phase[2], "adam": phase[3]},
         "loss_first_warmup": losses[0], "loss_last": float(last.item()), "status": int(st),
-        "params": enc.param_count + tr.n_mlp, "gpu_launches_per_step": 6,
+        "params": enc.param_count + tr.n_mlp, "gpu_launches_per_step": 6, "replicas_identical": bool(same),
     }
 
 

@@ -1,0 +1,90 @@
+"""Multi-process data-parallel host logic on CPU (gloo, world size 2).
+
+The GPU box in this run has one GPU, so the N>1 path is covered here: each
+rank computes its shard's gradients with the oracle (as a stand-in for the
+per-rank kernels), the product's all-reduce helper sums them, and the result
+must equal the single-process gradient of the global batch (the 1/N_global
+scaling of R12 makes the split exact).  Also: even sharding and the
+replica-identity check."""
+import os
+import socket
+
+import numpy as np
+import pytest
+import torch
+import torch.distributed as dist
+import torch.multiprocessing as mp
+
+from paper_2507_03836_b200 import dp
+
+
+def test_shard_even_split():
+    for n in (0, 1, 7, 1000, 2 ** 24):
+        for w in (1, 2, 3, 8):
+            parts = [dp.shard(n, r, w) for r in range(w)]
+            assert sum(c for _, c in parts) == n
+            assert parts[0][0] == 0
+            for (s0, c0), (s1, _) in zip(parts, parts[1:]):
+                assert s1 == s0 + c0
+            assert max(c for _, c in parts) - min(c for _, c in parts) <= 1
+    with pytest.raises(ValueError):
+        dp.shard(10, 2, 2)
+
+
+def _free_port():
+    s = socket.socket()
+    s.bind(("127.0.0.1", 0))
+    p = s.getsockname()[1]
+    s.close()
+    return p
+
+
+def _worker(rank, world, port, out):
+    os.environ["MASTER_ADDR"] = "127.0.0.1"
+    os.environ["MASTER_PORT"] = str(port)
+    dist.init_process_group("gloo", rank=rank, world_size=world)
+    try:
+        import workloads as W
+        from oracle import train as T
+        g = W.rng(0)
+        layers = W.draw_mlp(g, W.MLPConfig((16, 64, 64, 1)))
+        n_global = 1001
+        x = g.standard_normal((n_global, 16))
+        t = g.random(n_global)
+        s, c = dp.shard(n_global, rank, world)
+        y, cache = T.mlp_forward(x[s:s + c], layers, emulate_bf16=False)
+        _, dy = T.mse_loss(y, t[s:s + c], n_global)
+        grads, _ = T.mlp_backward(dy, layers, cache, emulate_bf16=False)
+        flat = torch.from_numpy(np.concatenate([np.concatenate([a.ravel(), b.ravel()]) for a, b in grads]))
+        dp.allreduce_grads(flat)
+        out[rank] = flat.numpy().copy()
+        # replicas: identical tensors compare equal, perturbed ones do not
+        same = torch.arange(10, dtype=torch.float32)
+        diff = same + (rank * 1e-3)
+        out[f"same{rank}"] = dp.replicas_identical(same)
+        out[f"diff{rank}"] = dp.replicas_identical(diff)
+    finally:
+        dist.destroy_process_group()
+
+
+def test_allreduce_of_shard_grads_equals_global_grad():
+    world = 2
+    with mp.Manager() as m:
+        out = m.dict()
+        mp.spawn(_worker, args=(world, _free_port(), out), nprocs=world, join=True)
+        res = dict(out)
+    import workloads as W
+    from oracle import train as T
+    g = W.rng(0)
+    layers = W.draw_mlp(g, W.MLPConfig((16, 64, 64, 1)))
+    x = g.standard_normal((1001, 16))
+    t = g.random(1001)
+    y, cache = T.mlp_forward(x, layers, emulate_bf16=False)
+    _, dy = T.mse_loss(y, t, 1001)
+    grads, _ = T.mlp_backward(dy, layers, cache, emulate_bf16=False)
+    ref = np.concatenate([np.concatenate([a.ravel(), b.ravel()]) for a, b in grads])
+    for r in range(world):
+        assert np.allclose(res[r], ref, rtol=1e-10, atol=1e-14)
+    assert np.array_equal(res[0], res[1])
+    assert res["same0"] and res["same1"]
+    assert not res["diff0"] and not res["diff1"]
