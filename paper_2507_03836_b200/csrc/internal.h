@@ -41,4 +41,9 @@ struct fh_encoder_s {
     fh::Params params;
     int *flag = nullptr;  // sticky domain flag (device), allocated lazily
     int device = -1;
+    // Level groups: consecutive levels whose table (fwd) or
+    // fp32 grad (bwd) footprint fits an L2 budget run as one pass, so the
+    // gathered / reduced region stays L2-resident.  g[i]..g[i+1] = group i.
+    int n_gf = 0, gf[FH_MAX_LEVELS + 1] = {0};
+    int n_gb = 0, gb[FH_MAX_LEVELS + 1] = {0};
 };
