@@ -43,11 +43,12 @@ __host__ __device__ constexpr int off_w3(int K0) { return H * K0 + 2 * H + H * H
 __host__ __device__ constexpr int off_b3(int K0) { return H * K0 + 3 * H + H * H; }
 __host__ __device__ constexpr int param_count(int K0) { return H * K0 + 3 * H + H * H + 1; }
 
-struct Smem {
-    // sizes for K0 <= 64
-    static constexpr int kHXMax = (H + 64 + 16);          // [H1 | X | 1 pad]
-};
-
+// Two independent tile "slots" per CTA (warps 0-3 and 4-7), each with its
+// own shared-memory tiles, TMEM columns, mbarrier and MMA-issuing thread, so
+// one slot's epilogue math overlaps the other slot's MMAs and loads.  Within
+// a slot the four per-tile accumulators Z1, Z2, dH1, dX share ONE 64-column
+// TMEM region (each is consumed before the next MMA of the chain is issued);
+// each slot accumulates its own DW block across all its tiles.
 template <int K0>
 struct Layout {
     static constexpr int WHX = H + K0 + 16;               // columns of the [H1 | X | 1..] tile
@@ -57,13 +58,16 @@ struct Layout {
     static constexpr uint32_t SBO_W2 = (H / 8) * 128;
     static constexpr uint32_t BYTES_HX = TILE * WHX * 2;
     static constexpr uint32_t BYTES_DZ = TILE * 2 * H * 2;
+    static constexpr uint32_t BYTES_H2 = TILE * H * 2;    // bf16 h2 rows (for dw3)
+    static constexpr uint32_t BYTES_SLOT = BYTES_HX + BYTES_DZ + BYTES_H2;
     static constexpr uint32_t BYTES_W1 = H * K0 * 2;
     static constexpr uint32_t BYTES_W2 = H * H * 2;
-    static constexpr uint32_t BYTES_RED = TILE * (H + 1) * 4;  // dw3 transpose-reduce scratch
-    static constexpr uint32_t SMEM = BYTES_HX + BYTES_DZ + BYTES_W1 + BYTES_W2 + BYTES_RED;
-    // TMEM columns
-    static constexpr uint32_t T_Z1 = 0, T_Z2 = 64, T_DH1 = 128, T_DX = 192, T_DW = 256;
+    static constexpr int SLOTS = 2;
+    static constexpr uint32_t SMEM = SLOTS * BYTES_SLOT + BYTES_W1 + BYTES_W2;
+    // TMEM columns (per slot, base = slot * 256)
+    static constexpr uint32_t T_ACC = 0, T_DW = 64;
     static constexpr uint32_t TMEM_COLS = 512;
+    static_assert(T_DW + WHX <= 256, "slot TMEM region overflow");
 };
 
 __device__ __forceinline__ uint32_t pack_bf16(float a, float b) {
@@ -71,6 +75,9 @@ __device__ __forceinline__ uint32_t pack_bf16(float a, float b) {
     return *reinterpret_cast<uint32_t *>(&v);
 }
 __device__ __forceinline__ float bf16r(float a) { return __bfloat162float(__float2bfloat16_rn(a)); }
+__device__ __forceinline__ float2 unpack_bf16(uint32_t u) {
+    return __bfloat1622float2(*reinterpret_cast<const __nv_bfloat162 *>(&u));
+}
 
 struct TrainArgs {
     const __nv_bfloat16 *x;      // [N][K0] encoder output
@@ -90,54 +97,82 @@ __device__ __forceinline__ void st16(uint8_t *base, uint32_t off, uint4 v) {
     *reinterpret_cast<uint4 *>(base + off) = v;
 }
 
+// Barrier over the 128 threads of one slot (named barrier 1 + slot).
+__device__ __forceinline__ void slot_sync(int slot) {
+    asm volatile("bar.sync %0, 128;" ::"r"(1 + slot) : "memory");
+}
+
+// Sum v[0..63] over the 32 lanes of a warp by recursive halving: 62
+// shuffles; afterwards lane holds the totals of columns col, col + 1 with
+// col = 32 b4 + 16 b3 + 8 b2 + 4 b1 + 2 b0 (b_k = bit k of the lane).
+__device__ __forceinline__ void warp_reduce64(float (&v)[64], int lane) {
+#pragma unroll
+    for (int st = 0; st < 5; st++) {
+        const int off = 16 >> st, half = 32 >> st;
+        const bool upper = (lane & off) != 0;
+#pragma unroll
+        for (int i = 0; i < half; i++) {
+            const float send = upper ? v[i] : v[i + half];
+            const float keep = upper ? v[i + half] : v[i];
+            v[i] = keep + __shfl_xor_sync(0xffffffffu, send, off);
+        }
+    }
+}
+__device__ __forceinline__ int reduce64_col(int lane) {
+    return 32 * ((lane >> 4) & 1) + 16 * ((lane >> 3) & 1) + 8 * ((lane >> 2) & 1) + 4 * ((lane >> 1) & 1) +
+           2 * (lane & 1);
+}
+
 template <int K0>
-__global__ void __launch_bounds__(128, 1) mlp_train_kernel(const TrainArgs a) {
+__global__ void __launch_bounds__(256, 1) mlp_train_kernel(const TrainArgs a) {
     using Lo = Layout<K0>;
     extern __shared__ __align__(1024) uint8_t smem[];
-    uint8_t *sHX = smem;
-    uint8_t *sDZ = sHX + Lo::BYTES_HX;
-    uint8_t *sW1 = sDZ + Lo::BYTES_DZ;
+    uint8_t *sW1 = smem;
     uint8_t *sW2 = sW1 + Lo::BYTES_W1;
-    float *sRed = reinterpret_cast<float *>(sW2 + Lo::BYTES_W2);
-    __shared__ uint64_t bar;
+    __shared__ uint64_t bar[2];
     __shared__ uint32_t tbase;
-    __shared__ float s_db3[4], s_loss[4];
+    __shared__ float b1[H], b2[H], w3[H];
+    __shared__ float s_db3[8], s_loss[8];
 
-    const int t = threadIdx.x, warp = t >> 5, lane = t & 31;
+    const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
+    const int slot = warp >> 2;          // 0: warps 0-3, 1: warps 4-7
+    const int t = tid & 127;             // sample row within the slot's tile = TMEM lane
+    uint8_t *sHX = smem + Lo::BYTES_W1 + Lo::BYTES_W2 + slot * Lo::BYTES_SLOT;
+    uint8_t *sDZ = sHX + Lo::BYTES_HX;
+    uint8_t *sH2 = sDZ + Lo::BYTES_DZ;
     const int64_t n_tiles = (a.N + TILE - 1) / TILE;
 
     // ---- weights -> shared memory (bf16 shadow), once per CTA
-    for (int i = t; i < H * K0; i += blockDim.x) {
+    for (int i = tid; i < H * K0; i += blockDim.x) {
         const int r = i / K0, c = i % K0;
         *reinterpret_cast<__nv_bfloat16 *>(sW1 + tc::core_off(r, c, Lo::SBO_W1)) = a.wsh[off_W1() + i];
     }
-    for (int i = t; i < H * H; i += blockDim.x) {
+    for (int i = tid; i < H * H; i += blockDim.x) {
         const int r = i / H, c = i % H;
         *reinterpret_cast<__nv_bfloat16 *>(sW2 + tc::core_off(r, c, Lo::SBO_W2)) = a.wsh[off_W2(K0) + i];
     }
-    // constant columns [H + K0, H + K0 + 16) of the HX tile: 1, 0, ..., 0
-    {
+    {   // constant columns [H + K0, H + K0 + 16) of each slot's HX tile: 1, 0, ..., 0
         const uint4 ones = make_uint4(pack_bf16(1.f, 0.f), 0u, 0u, 0u), zero = make_uint4(0u, 0u, 0u, 0u);
         st16(sHX, tc::core_off(t, H + K0, Lo::SBO_HX), ones);
         st16(sHX, tc::core_off(t, H + K0 + 8, Lo::SBO_HX), zero);
     }
-    // constants in shared memory: biases (fp32 master), w3 (bf16 shadow values)
-    __shared__ float b1[H], b2[H], w3[H];
-    if (t < H) {
-        b1[t] = a.wmaster[off_b1(K0) + t];
-        b2[t] = a.wmaster[off_b2(K0) + t];
-        w3[t] = __bfloat162float(a.wsh[off_w3(K0) + t]);
+    if (tid < H) {
+        b1[tid] = a.wmaster[off_b1(K0) + tid];
+        b2[tid] = a.wmaster[off_b2(K0) + tid];
+        w3[tid] = __bfloat162float(a.wsh[off_w3(K0) + tid]);
     }
     const float b3 = a.wmaster[off_b3(K0)];
 
     if (warp == 0) tc::tmem_alloc(&tbase, Lo::TMEM_COLS);
-    if (t == 0) { tc::mbar_init(&bar, 1); tc::fence_mbar_init(); }
+    if (tid == 0) { tc::mbar_init(&bar[0], 1); tc::mbar_init(&bar[1], 1); tc::fence_mbar_init(); }
     tc::fence_smem_to_async();
     tc::fence_before_sync();
     __syncthreads();
     tc::fence_after_sync();
-    const uint32_t tm = tbase;
-    const uint32_t lane_off = (uint32_t)(warp * 32) << 16;
+    const uint32_t tm = tbase + (uint32_t)slot * 256u;
+    const uint32_t lane_off = (uint32_t)((warp & 3) * 32) << 16;
+    uint64_t *mbar = &bar[slot];
+    const bool issuer = (t == 0);
 
     const uint32_t aHX = tc::smem_u32(sHX), aDZ = tc::smem_u32(sDZ);
     const uint32_t aW1 = tc::smem_u32(sW1), aW2 = tc::smem_u32(sW2);
@@ -147,43 +182,43 @@ __global__ void __launch_bounds__(128, 1) mlp_train_kernel(const TrainArgs a) {
     constexpr uint32_t id_dw = tc::idesc_bf16_f32(128, Lo::WHX, true, true); // both MN-major
 
     uint32_t phase = 0;
-    float dw3_acc = 0.f, db3_acc = 0.f, loss_acc = 0.f;
+    float dw3a = 0.f, dw3b = 0.f, db3_acc = 0.f, loss_acc = 0.f;
     bool bad = false;
     int my_tiles = 0;
 
-    for (int64_t tile = blockIdx.x; tile < n_tiles; tile += gridDim.x, my_tiles++) {
+    for (int64_t tile = 2 * (int64_t)blockIdx.x + slot; tile < n_tiles; tile += 2 * (int64_t)gridDim.x, my_tiles++) {
         const int64_t row = tile * TILE + t;
         const bool valid = row < a.N;
-        // ---- stage X row (bf16) into [H1 | X | 1] columns H.. H+K0
+        // ---- stage X row (bf16) into [H1 | X | 1] columns H .. H+K0
         {
             const uint4 *src = reinterpret_cast<const uint4 *>(a.x + row * K0);
+            uint4 xv[K0 / 8];
 #pragma unroll
-            for (int q = 0; q < K0 / 8; q++) {
-                const uint4 v = valid ? __ldg(src + q) : make_uint4(0u, 0u, 0u, 0u);
-                st16(sHX, tc::core_off(t, H + 8 * q, Lo::SBO_HX), v);
-            }
+            for (int q = 0; q < K0 / 8; q++) xv[q] = valid ? __ldg(src + q) : make_uint4(0u, 0u, 0u, 0u);
+#pragma unroll
+            for (int q = 0; q < K0 / 8; q++) st16(sHX, tc::core_off(t, H + 8 * q, Lo::SBO_HX), xv[q]);
         }
         const float tgt = valid ? __ldg(a.target + row) : 0.f;
         tc::fence_smem_to_async();
         tc::fence_before_sync();
-        __syncthreads();
+        slot_sync(slot);
         tc::fence_after_sync();
         // ---- MMA1: Z1 = X . W1^T
-        if (t == 0) {
+        if (issuer) {
 #pragma unroll
             for (int s = 0; s < K0 / 16; s++)
-                tc::mma_bf16(tm + Lo::T_Z1, tc::sdesc(aHX + (H / 8) * 128 + s * 256, 128, Lo::SBO_HX),
+                tc::mma_bf16(tm + Lo::T_ACC, tc::sdesc(aHX + (H / 8) * 128 + s * 256, 128, Lo::SBO_HX),
                              tc::sdesc(aW1 + s * 256, 128, Lo::SBO_W1), id_h, s > 0);
-            tc::commit(&bar);
+            tc::commit(mbar);
         }
-        tc::mbar_wait(&bar, phase); phase ^= 1;
+        tc::mbar_wait(mbar, phase); phase ^= 1;
         tc::fence_after_sync();
         // ---- epilogue 1: H1 = bf16(relu(Z1 + b1)), mask1
         uint32_t m1[2] = {0u, 0u};
 #pragma unroll
         for (int c = 0; c < H; c += 16) {
             float v[16];
-            tc::tmem_ld16(tm + lane_off + Lo::T_Z1 + c, v);
+            tc::tmem_ld16(tm + lane_off + Lo::T_ACC + c, v);
             tc::tmem_wait_ld();
             uint32_t p[8];
 #pragma unroll
@@ -198,46 +233,47 @@ __global__ void __launch_bounds__(128, 1) mlp_train_kernel(const TrainArgs a) {
         }
         tc::fence_smem_to_async();
         tc::fence_before_sync();
-        __syncthreads();
+        slot_sync(slot);
         tc::fence_after_sync();
         // ---- MMA2: Z2 = H1 . W2^T
-        if (t == 0) {
+        if (issuer) {
 #pragma unroll
             for (int s = 0; s < H / 16; s++)
-                tc::mma_bf16(tm + Lo::T_Z2, tc::sdesc(aHX + s * 256, 128, Lo::SBO_HX),
+                tc::mma_bf16(tm + Lo::T_ACC, tc::sdesc(aHX + s * 256, 128, Lo::SBO_HX),
                              tc::sdesc(aW2 + s * 256, 128, Lo::SBO_W2), id_h, s > 0);
-            tc::commit(&bar);
+            tc::commit(mbar);
         }
-        tc::mbar_wait(&bar, phase); phase ^= 1;
+        tc::mbar_wait(mbar, phase); phase ^= 1;
         tc::fence_after_sync();
-        // ---- epilogue 2: H2 = bf16(relu(Z2 + b2)); y = H2 . w3 + b3; MSE; dZ2
-        // h2 goes to this thread's row of sRed (fp32) to keep registers free
-        float *myred = sRed + t * (H + 1);
+        // ---- epilogue 2: H2 = bf16(relu(Z2 + b2)); y = H2 . w3 + b3; MSE; dZ2; dw3
         uint32_t m2[2] = {0u, 0u};
-        float y = 0.f;
+        float ya[4] = {0.f, 0.f, 0.f, 0.f};
+        uint4 *h2row = reinterpret_cast<uint4 *>(sH2 + t * H * 2);
 #pragma unroll
         for (int c = 0; c < H; c += 16) {
             float v[16];
-            tc::tmem_ld16(tm + lane_off + Lo::T_Z2 + c, v);
+            tc::tmem_ld16(tm + lane_off + Lo::T_ACC + c, v);
             tc::tmem_wait_ld();
+            uint32_t p[8];
 #pragma unroll
-            for (int j = 0; j < 16; j++) {
-                const float z = v[j] + b2[c + j];
-                m2[(c + j) >> 5] |= (z > 0.f ? 1u : 0u) << ((c + j) & 31);
-                const float h = bf16r(fmaxf(z, 0.f));
-                y = fmaf(h, w3[c + j], y);   // output layer, j ascending (fp32)
-                myred[c + j] = h;
+            for (int j = 0; j < 16; j += 2) {
+                const float z0 = v[j] + b2[c + j], z1 = v[j + 1] + b2[c + j + 1];
+                m2[(c + j) >> 5] |= (z0 > 0.f ? 1u : 0u) << ((c + j) & 31);
+                m2[(c + j + 1) >> 5] |= (z1 > 0.f ? 1u : 0u) << ((c + j + 1) & 31);
+                const float h0 = bf16r(fmaxf(z0, 0.f)), h1 = bf16r(fmaxf(z1, 0.f));
+                ya[(j >> 1) & 3] = fmaf(h0, w3[c + j], ya[(j >> 1) & 3]);
+                ya[(j >> 1) & 3] = fmaf(h1, w3[c + j + 1], ya[(j >> 1) & 3]);
+                p[j / 2] = pack_bf16(h0, h1);
             }
+            h2row[c / 8] = make_uint4(p[0], p[1], p[2], p[3]);
+            h2row[c / 8 + 1] = make_uint4(p[4], p[5], p[6], p[7]);
         }
-        y += b3;
+        const float y = ((ya[0] + ya[1]) + (ya[2] + ya[3])) + b3;
         const float diff = valid ? (y - tgt) : 0.f;
         if (!isfinite(diff)) bad = true;
         loss_acc = fmaf(diff, diff, loss_acc);
         const float dy = 2.f * diff * a.inv_n_global;
         db3_acc += dy;
-        // dw3: transpose-reduce dy*h2 over the tile's 128 samples via smem
-#pragma unroll
-        for (int j = 0; j < H; j++) myred[j] *= dy;
 #pragma unroll
         for (int c = 0; c < H; c += 8) {
             uint32_t p[4];
@@ -251,28 +287,40 @@ __global__ void __launch_bounds__(128, 1) mlp_train_kernel(const TrainArgs a) {
         }
         tc::fence_smem_to_async();
         tc::fence_before_sync();
-        __syncthreads();
+        slot_sync(slot);
         tc::fence_after_sync();
-        if (t < H) {
-            float s = 0.f;
-            for (int r = 0; r < TILE; r++) s += sRed[r * (H + 1) + t];
-            dw3_acc += s;
-        }
-        // ---- MMA3: dH1 = dZ2 . W2
-        if (t == 0) {
+        // ---- MMA3: dH1 = dZ2 . W2   (issued before the dw3 reduction below)
+        if (issuer) {
 #pragma unroll
             for (int s = 0; s < H / 16; s++)
-                tc::mma_bf16(tm + Lo::T_DH1, tc::sdesc(aDZ + s * 256, 128, Lo::SBO_DZ),
+                tc::mma_bf16(tm + Lo::T_ACC, tc::sdesc(aDZ + s * 256, 128, Lo::SBO_DZ),
                              tc::sdesc(aW2 + s * 2 * Lo::SBO_W2, Lo::SBO_W2, 128), id_dh, s > 0);
-            tc::commit(&bar);
+            tc::commit(mbar);
         }
-        tc::mbar_wait(&bar, phase); phase ^= 1;
+        {   // dw3 += sum over the warp's samples of dy * h2 (fp32), overlapping MMA3
+            float v[64];
+#pragma unroll
+            for (int q = 0; q < 8; q++) {
+                const uint4 u = h2row[q];
+                const uint32_t w[4] = {u.x, u.y, u.z, u.w};
+#pragma unroll
+                for (int k = 0; k < 4; k++) {
+                    const float2 f = unpack_bf16(w[k]);
+                    v[8 * q + 2 * k] = dy * f.x;
+                    v[8 * q + 2 * k + 1] = dy * f.y;
+                }
+            }
+            warp_reduce64(v, lane);
+            dw3a += v[0];
+            dw3b += v[1];
+        }
+        tc::mbar_wait(mbar, phase); phase ^= 1;
         tc::fence_after_sync();
         // ---- epilogue 3: dZ1 = bf16(dH1 * mask1)
 #pragma unroll
         for (int c = 0; c < H; c += 16) {
             float v[16];
-            tc::tmem_ld16(tm + lane_off + Lo::T_DH1 + c, v);
+            tc::tmem_ld16(tm + lane_off + Lo::T_ACC + c, v);
             tc::tmem_wait_ld();
             uint32_t p[8];
 #pragma unroll
@@ -286,28 +334,28 @@ __global__ void __launch_bounds__(128, 1) mlp_train_kernel(const TrainArgs a) {
         }
         tc::fence_smem_to_async();
         tc::fence_before_sync();
-        __syncthreads();
+        slot_sync(slot);
         tc::fence_after_sync();
         // ---- MMA4: dX = dZ1 . W1 ; MMA5: DW += [dZ2^T; dZ1^T] . [H1 | X | 1]
-        if (t == 0) {
+        if (issuer) {
 #pragma unroll
             for (int s = 0; s < H / 16; s++)
-                tc::mma_bf16(tm + Lo::T_DX, tc::sdesc(aDZ + (H / 8) * 128 + s * 256, 128, Lo::SBO_DZ),
+                tc::mma_bf16(tm + Lo::T_ACC, tc::sdesc(aDZ + (H / 8) * 128 + s * 256, 128, Lo::SBO_DZ),
                              tc::sdesc(aW1 + s * 2 * Lo::SBO_W1, Lo::SBO_W1, 128), id_dx, s > 0);
 #pragma unroll
             for (int s = 0; s < TILE / 16; s++)
                 tc::mma_bf16(tm + Lo::T_DW, tc::sdesc(aDZ + s * 2 * Lo::SBO_DZ, Lo::SBO_DZ, 128),
                              tc::sdesc(aHX + s * 2 * Lo::SBO_HX, Lo::SBO_HX, 128), id_dw,
                              (my_tiles > 0 || s > 0) ? 1u : 0u);
-            tc::commit(&bar);
+            tc::commit(mbar);
         }
-        tc::mbar_wait(&bar, phase); phase ^= 1;
+        tc::mbar_wait(mbar, phase); phase ^= 1;
         tc::fence_after_sync();
         // ---- epilogue 4: dX row -> global (fp32)
 #pragma unroll
         for (int c = 0; c < K0; c += 16) {
             float v[16];
-            tc::tmem_ld16(tm + lane_off + Lo::T_DX + c, v);
+            tc::tmem_ld16(tm + lane_off + Lo::T_ACC + c, v);
             tc::tmem_wait_ld();
             if (valid) {
                 float4 *dst = reinterpret_cast<float4 *>(a.dx + row * K0 + c);
@@ -316,7 +364,7 @@ __global__ void __launch_bounds__(128, 1) mlp_train_kernel(const TrainArgs a) {
             }
         }
         tc::fence_before_sync();
-        __syncthreads();   // sRed / sDZ / sHX / TMEM reuse by the next tile
+        slot_sync(slot);   // TMEM / smem reuse by this slot's next tile
         tc::fence_after_sync();
     }
 
@@ -341,7 +389,9 @@ __global__ void __launch_bounds__(128, 1) mlp_train_kernel(const TrainArgs a) {
                 }
             }
         }
-        if (t < H) atomicAdd(g + off_w3(K0) + t, dw3_acc);
+        const int col = reduce64_col(lane);
+        atomicAdd(g + off_w3(K0) + col, dw3a);
+        atomicAdd(g + off_w3(K0) + col + 1, dw3b);
     }
     // db3 and loss: warp reduce, then one atomic per CTA
 #pragma unroll
@@ -353,11 +403,15 @@ __global__ void __launch_bounds__(128, 1) mlp_train_kernel(const TrainArgs a) {
     if (bad) atomicOr(a.flag, 2);
     tc::fence_before_sync();
     __syncthreads();
-    if (t == 0 && my_tiles > 0) {
-        atomicAdd(a.grad + off_b3(K0), s_db3[0] + s_db3[1] + s_db3[2] + s_db3[3]);
-        atomicAdd(a.loss, (s_loss[0] + s_loss[1] + s_loss[2] + s_loss[3]) * a.inv_n_global);
+    if (tid == 0) {
+        float d = 0.f, l = 0.f;
+        for (int w = 0; w < 8; w++) { d += s_db3[w]; l += s_loss[w]; }
+        if (2 * (int64_t)blockIdx.x < n_tiles) {
+            atomicAdd(a.grad + off_b3(K0), d);
+            atomicAdd(a.loss, l * a.inv_n_global);
+        }
     }
-    if (warp == 0) tc::tmem_dealloc(tm, Lo::TMEM_COLS);
+    if (warp == 0) tc::tmem_dealloc(tbase, Lo::TMEM_COLS);
 }
 
 // ------------------------------------------------------------------ Adam

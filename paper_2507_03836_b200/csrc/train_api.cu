@@ -66,8 +66,9 @@ fh_status launch_mlp(fh_trainer tr, const float *target, int64_t N, int64_t N_gl
     a.N = N;
     a.inv_n_global = (float)(1.0 / (double)N_global);
     const int64_t tiles = (N + fh::mlp::TILE - 1) / fh::mlp::TILE;
-    const int grid = (int)(tiles < tr->n_sm ? tiles : tr->n_sm);
-    fh::mlp::mlp_train_kernel<K0><<<grid, 128, smem, s>>>(a);
+    const int64_t pairs = (tiles + 1) / 2;  // two tile slots per CTA
+    const int grid = (int)(pairs < tr->n_sm ? pairs : tr->n_sm);
+    fh::mlp::mlp_train_kernel<K0><<<grid, 256, smem, s>>>(a);
     return cuda_check(cudaGetLastError(), "mlp_train_kernel launch");
 }
 
