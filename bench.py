@@ -238,11 +238,15 @@ def train_step_bench(fh, torch, W, which, rank, world, dist, steps, warmup):
     enc = fh.Encoder(cfg.levels, cfg.F, cfg.table_dtype, cfg.cap)
     gen = torch.Generator("cuda").manual_seed(0)           # identical init on every rank
     table0 = (torch.rand((enc.entries, cfg.F), device="cuda", generator=gen) * 2 - 1) * 1e-4
-    tr = fh.Trainer(enc, table0, W.draw_mlp(W.rng(0), mlp), n_local)
+    tr = fh.Trainer(enc, table0, W.draw_mlp(W.rng(0), mlp), n_local, world=world)
     del table0
     coords = torch.empty((n_local, 4), device="cuda")
     target = torch.empty((n_local,), device="cuda")
     stream = torch.cuda.current_stream()
+    # world > 1: reduce-scatter of the table grads + all-reduce of the MLP
+    # grads (NCCL over NVLink/NVSwitch), Adam on this rank's 1/W shard,
+    # all-gather of the fp16 table shadow (dp.ShardedDP).
+    sdp = dp.ShardedDP(tr) if world > 1 else None
 
     def one(k, ev=None):
         if ev: ev[0].record(stream)
@@ -250,10 +254,14 @@ def train_step_bench(fh, torch, W, which, rank, world, dist, steps, warmup):
         if ev: ev[1].record(stream)
         loss = tr.fwd_bwd(coords, target, n_global)
         if ev: ev[2].record(stream)
-        if world > 1:
-            dp.allreduce_grads(tr.grads)      # NCCL SUM over NVLink/NVSwitch
+        if sdp:
+            sdp.reduce()
         if ev: ev[3].record(stream)
-        tr.apply()
+        if sdp:
+            sdp.apply()
+            sdp.gather()
+        else:
+            tr.apply()
         if ev: ev[4].record(stream)
         return loss
 
@@ -274,7 +282,7 @@ def train_step_bench(fh, torch, W, which, rank, world, dist, steps, warmup):
         dist.all_reduce(t, op=dist.ReduceOp.MAX)
         total = float(t.item())
     # DP correctness: after the timed steps the replicas must be bit-identical
-    same = dp.replicas_identical(tr.table_master) and dp.replicas_identical(tr.mlp_master)
+    same = dp.replicas_identical(tr.shadow_flat) and dp.replicas_identical(tr.mlp_master)
     last = tr.loss.clone()
     if dist:
         dist.all_reduce(last)
@@ -287,7 +295,9 @@ def train_step_bench(fh, torch, W, which, rank, world, dist, steps, warmup):
         "value": n_global * steps / total, "unit": "samples/s", "ms_per_step": total * 1e3 / steps,
         "global_batch": n_global, "per_gpu_batch": n_local, "n_gpus": world,
         "scaling": "strong" if which == "cfg5" else "weak",
-        "phase_ms": {"sample": phase[0], "fwd_bwd": phase[1], "allreduce": phase[2], "adam": phase[3]},
+        "phase_ms": {"sample": phase[0], "fwd_bwd": phase[1], "grad_reduce": phase[2],
+                     "adam_and_gather": phase[3]},
+        "dp": "reduce-scatter + sharded Adam + all-gather (NCCL)" if world > 1 else "single GPU",
         "loss_first_warmup": losses[0], "loss_last": float(last.item()), "status": int(st),
         "params": enc.param_count + tr.n_mlp, "gpu_launches_per_step": 6, "replicas_identical": bool(same),
     }

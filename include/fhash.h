@@ -241,6 +241,17 @@ fh_status fh_train_fwd_bwd(fh_trainer tr, const float *coords, const float *targ
 /* One Adam step on all parameters (step counter += 1). */
 fh_status fh_train_apply(fh_trainer tr, fh_stream stream);
 
+/* Sharded Adam (data parallel, ZeRO-1 style): Adam on the
+ * table parameters [begin, end) of the flat table space [0, entries*F),
+ * reading their (already reduce-scattered) gradients from grad_shard
+ * (device f32, end - begin values), plus the full MLP segment from the
+ * trainer's mlp_grad (already all-reduced).  Updates masters, moments and
+ * shadows in the range only; zeroes the trainer's table_grad and mlp_grad
+ * entirely for the next step.  begin must be a multiple of 4.  The caller
+ * then all-gathers the shadow (or, for FH_F32 tables, the master). */
+fh_status fh_train_apply_sharded(fh_trainer tr, int64_t begin, int64_t end, const float *grad_shard,
+                                 fh_stream stream);
+
 /* fh_train_fwd_bwd + fh_train_apply (single GPU). */
 fh_status fh_train_step(fh_trainer tr, const float *coords, const float *target, int64_t N_local,
                         int64_t N_global, float *loss_dev, fh_stream stream);

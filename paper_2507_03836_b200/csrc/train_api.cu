@@ -152,9 +152,11 @@ fh_status fh_train_fwd_bwd(fh_trainer tr, const float *coords, const float *targ
     return fh_encode_bwd(tr->enc, coords, N, tr->dx, tr->b.table_grad, stream);
 }
 
-fh_status fh_train_apply(fh_trainer tr, fh_stream stream) {
-    g_err[0] = 0;
-    if (!tr) return fail(FH_E_ARG, "fh_train_apply: NULL trainer");
+}  // extern "C"
+
+// Adam over table parameters [begin, end) with gradients tgrad (indexed from
+// begin), plus the whole MLP segment.
+static fh_status apply_impl(fh_trainer tr, int64_t begin, int64_t end, float *tgrad, cudaStream_t s) {
     tr->step += 1;
     const double t = (double)tr->step;
     fh::mlp::AdamArgs A;
@@ -167,12 +169,12 @@ fh_status fh_train_apply(fh_trainer tr, fh_stream stream) {
     A.c1 = (float)(1.0 / (1.0 - std::pow((double)tr->adam.beta1, t)));
     A.c2 = (float)(1.0 / (1.0 - std::pow((double)tr->adam.beta2, t)));
     fh::mlp::AdamSeg &T = A.seg[0];
-    T.p = tr->b.table_master;
-    T.g = tr->b.table_grad;
-    T.m = tr->b.table_m;
-    T.v = tr->b.table_v;
-    T.shadow = tr->b.table_shadow;
-    T.n = (int64_t)(tr->enc->entries * (uint64_t)tr->enc->F);
+    T.p = tr->b.table_master + begin;
+    T.g = tgrad;
+    T.m = tr->b.table_m + begin;
+    T.v = tr->b.table_v + begin;
+    T.shadow = tr->b.table_shadow ? reinterpret_cast<__half *>(tr->b.table_shadow) + begin : nullptr;
+    T.n = end - begin;
     T.kind = tr->b.table_shadow ? 1 : 0;
     fh::mlp::AdamSeg &M = A.seg[1];
     M.p = tr->b.mlp_master;
@@ -190,9 +192,33 @@ fh_status fh_train_apply(fh_trainer tr, fh_stream stream) {
     if (b0 < 1) b0 = 1;
     A.blocks0 = b0;
     const int64_t b1 = 4;
-    cudaStream_t s = reinterpret_cast<cudaStream_t>(stream);
     fh::mlp::adam_kernel<<<(unsigned)(b0 + b1), 256, 0, s>>>(A);
     return cuda_check(cudaGetLastError(), "adam_kernel launch");
+}
+
+extern "C" {
+
+fh_status fh_train_apply(fh_trainer tr, fh_stream stream) {
+    g_err[0] = 0;
+    if (!tr) return fail(FH_E_ARG, "fh_train_apply: NULL trainer");
+    const int64_t n = (int64_t)(tr->enc->entries * (uint64_t)tr->enc->F);
+    return apply_impl(tr, 0, n, tr->b.table_grad, reinterpret_cast<cudaStream_t>(stream));
+}
+
+fh_status fh_train_apply_sharded(fh_trainer tr, int64_t begin, int64_t end, const float *grad_shard,
+                                 fh_stream stream) {
+    g_err[0] = 0;
+    if (!tr) return fail(FH_E_ARG, "fh_train_apply_sharded: NULL trainer");
+    const int64_t n = (int64_t)(tr->enc->entries * (uint64_t)tr->enc->F);
+    if (begin < 0 || end < begin || end > n || (begin % 4) != 0)
+        return fail(FH_E_ARG, "fh_train_apply_sharded: need 0 <= begin <= end <= entries*F, begin %% 4 == 0");
+    if (end > begin && (!grad_shard || !aligned(grad_shard, 16)))
+        return fail(FH_E_ARG, "fh_train_apply_sharded: NULL or misaligned grad_shard");
+    cudaStream_t s = reinterpret_cast<cudaStream_t>(stream);
+    fh_status st = apply_impl(tr, begin, end, const_cast<float *>(grad_shard), s);
+    if (st != FH_OK) return st;
+    // the local (pre-reduction) table grads must start the next step at zero
+    return cuda_check(cudaMemsetAsync(tr->b.table_grad, 0, (size_t)n * sizeof(float), s), "zero table_grad");
 }
 
 fh_status fh_train_step(fh_trainer tr, const float *coords, const float *target, int64_t N, int64_t N_global,

@@ -32,7 +32,7 @@ EXPORTS = [
     "fh_bench_gather", "fh_bench_red", "fh_bench_copy",
     # train step
     "fh_mlp_param_count", "fh_train_workspace_size", "fh_trainer_create", "fh_train_fwd_bwd", "fh_train_apply",
-    "fh_train_step", "fh_trainer_status", "fh_trainer_step_count", "fh_trainer_destroy",
+    "fh_train_step", "fh_trainer_status", "fh_trainer_step_count", "fh_trainer_destroy", "fh_train_apply_sharded",
     # include/fhash_data.h (synthetic data, harness)
     "fh_data_gaussian_blobs", "fh_data_value_noise", "fh_data_normalize", "fh_data_sample_voxels",
 ]
@@ -254,6 +254,8 @@ def _train_lib():
     L.fh_train_fwd_bwd.argtypes = [vp, vp, vp, i64, i64, vp, vp]
     L.fh_train_step.argtypes = [vp, vp, vp, i64, i64, vp, vp]
     L.fh_train_apply.argtypes = [vp, vp]
+    L.fh_train_apply_sharded.argtypes = [vp, i64, i64, vp, vp]
+    L.fh_train_apply_sharded.restype = ctypes.c_int
     L.fh_trainer_status.argtypes = [vp, vp]
     L.fh_trainer_step_count.argtypes = [vp]
     L.fh_trainer_step_count.restype = i64
@@ -274,7 +276,10 @@ class Trainer:
     apply()."""
 
     def __init__(self, enc: "Encoder", table_init, mlp_layers, max_batch: int, lr: float = 0.01,
-                 beta1: float = 0.9, beta2: float = 0.999, eps: float = 1e-8):
+                 beta1: float = 0.9, beta2: float = 0.999, eps: float = 1e-8, world: int = 1):
+        # world > 1: the flat table region of grads and shadow is padded to a
+        # multiple of 4 * world so it splits into equal 16-byte-aligned shards
+        # (reduce-scatter / sharded Adam / all-gather, dp.sharded_step).
         import numpy as np
         import torch
         L = _train_lib()
@@ -283,7 +288,9 @@ class Trainer:
         self.desc = MLPDesc(self.K0, 64, 2)
         dev = torch.device("cuda", torch.cuda.current_device())
         nt = enc.entries * enc.F
-        nt_pad = (nt + 3) // 4 * 4
+        q = 4 * max(1, world)
+        nt_pad = (nt + q - 1) // q * q
+        self.world, self.nt_pad = max(1, world), nt_pad
         P = int(L.fh_mlp_param_count(ctypes.byref(self.desc)))
         self.n_table, self.n_mlp = nt, P
         f32 = dict(dtype=torch.float32, device=dev)
@@ -292,7 +299,11 @@ class Trainer:
         else:
             self.table_master = torch.as_tensor(np.asarray(table_init, dtype=np.float32)).reshape(
                 enc.entries, enc.F).to(dev)
-        self.table_shadow = self.table_master.half() if enc.table_dtype == "f16" else None
+        self.table_shadow, self.shadow_flat = None, None
+        if enc.table_dtype == "f16":
+            self.shadow_flat = torch.zeros(nt_pad, dtype=torch.float16, device=dev)
+            self.shadow_flat[:nt].copy_(self.table_master.view(-1))
+            self.table_shadow = self.shadow_flat[:nt].view(enc.entries, enc.F)
         self.grads = torch.zeros(nt_pad + P, **f32)
         self.table_grad = self.grads[:nt].view(enc.entries, enc.F)
         self.mlp_grad = self.grads[nt_pad:]
@@ -343,6 +354,9 @@ class Trainer:
         _check(_train_lib().fh_train_fwd_bwd(self._h, _ptr(coords), _ptr(target), N, n_global or N,
                                              self.loss.data_ptr(), _stream(stream)))
         return self.loss
+
+    def apply_sharded(self, begin: int, end: int, grad_shard, stream=None):
+        _check(_train_lib().fh_train_apply_sharded(self._h, begin, end, _ptr(grad_shard), _stream(stream)))
 
     def apply(self, stream=None):
         _check(_train_lib().fh_train_apply(self._h, _stream(stream)))

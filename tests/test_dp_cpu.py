@@ -67,6 +67,88 @@ def _worker(rank, world, port, out):
         dist.destroy_process_group()
 
 
+class _MockTrainer:
+    """CPU stand-in with the attributes dp.ShardedDP uses; fwd_bwd adds a
+    deterministic per-(rank, step) gradient, apply_sharded runs the oracle's
+    Adam on the given range (the GPU kernels are tested in test_train_gpu)."""
+
+    def __init__(self, n_table, n_mlp, world, rank):
+        from oracle import train as T
+        self.T = T
+        q = 4 * world
+        self.n_table, self.world, self.rank = n_table, world, rank
+        self.nt_pad = (n_table + q - 1) // q * q
+        self.grads = torch.zeros(self.nt_pad + n_mlp)
+        self.mlp_grad = self.grads[self.nt_pad:]
+        g = np.random.default_rng(99)
+        self.p = g.uniform(-1e-4, 1e-4, n_table)
+        self.pm = g.uniform(-0.1, 0.1, n_mlp)
+        self.m, self.v = np.zeros(n_table), np.zeros(n_table)
+        self.mm, self.mv = np.zeros(n_mlp), np.zeros(n_mlp)
+        self.shadow_flat = torch.zeros(self.nt_pad, dtype=torch.float16)
+        self.shadow_flat[:n_table] = torch.from_numpy(self.p).half()
+        self.step_no = 0
+
+    @staticmethod
+    def local_grad(rank, step, n):
+        return np.random.default_rng(1000 * step + rank).standard_normal(n).astype(np.float32)
+
+    def fwd_bwd(self, coords, target, n_global, stream=None):
+        nm = self.mlp_grad.numel()
+        g = torch.from_numpy(self.local_grad(self.rank, self.step_no, self.n_table + nm))
+        self.grads[:self.n_table] += g[:self.n_table]
+        self.mlp_grad += g[self.n_table:]
+
+    def apply_sharded(self, begin, end, shard, stream=None):
+        self.step_no += 1
+        s = self.step_no
+        g = shard.numpy()[:end - begin].astype(np.float64)
+        self.p[begin:end], self.m[begin:end], self.v[begin:end] = self.T.adam_step(
+            self.p[begin:end], g, self.m[begin:end], self.v[begin:end], s)
+        self.pm, self.mm, self.mv = self.T.adam_step(self.pm, self.mlp_grad.numpy().astype(np.float64),
+                                                     self.mm, self.mv, s)
+        self.shadow_flat[begin:end] = torch.from_numpy(self.p[begin:end]).half()
+        self.grads.zero_()
+
+
+def _sharded_worker(rank, world, port, out):
+    os.environ["MASTER_ADDR"] = "127.0.0.1"
+    os.environ["MASTER_PORT"] = str(port)
+    dist.init_process_group("gloo", rank=rank, world_size=world)
+    try:
+        tr = _MockTrainer(1001, 37, world, rank)
+        sdp = dp.ShardedDP(tr)
+        for _ in range(3):
+            sdp.step(None, None, 1)
+        out[f"shadow{rank}"] = tr.shadow_flat[:tr.n_table].float().numpy().copy()
+        out[f"mlp{rank}"] = tr.pm.copy()
+        out[f"same{rank}"] = dp.replicas_identical(tr.shadow_flat)
+    finally:
+        dist.destroy_process_group()
+
+
+def test_sharded_adam_equals_replicated_adam():
+    """Reduce-scatter + sharded Adam + all-gather gives every rank the same
+    fp16 shadow as a single process running Adam on the summed gradients."""
+    world = 2
+    with mp.Manager() as m:
+        out = m.dict()
+        mp.spawn(_sharded_worker, args=(world, _free_port(), out), nprocs=world, join=True)
+        res = dict(out)
+    ref = _MockTrainer(1001, 37, 1, 0)
+    from oracle import train as T
+    for s in range(1, 4):
+        g = sum(_MockTrainer.local_grad(r, s - 1, 1001 + 37).astype(np.float32)
+                for r in range(world)).astype(np.float64)
+        ref.p, ref.m, ref.v = T.adam_step(ref.p, g[:1001], ref.m, ref.v, s)
+        ref.pm, ref.mm, ref.mv = T.adam_step(ref.pm, g[1001:], ref.mm, ref.mv, s)
+    exp = torch.from_numpy(ref.p).half().float().numpy()
+    for r in range(world):
+        assert np.array_equal(res[f"shadow{r}"], exp)
+        assert np.allclose(res[f"mlp{r}"], ref.pm, rtol=0, atol=1e-12)
+        assert res[f"same{r}"]
+
+
 def test_allreduce_of_shard_grads_equals_global_grad():
     world = 2
     with mp.Manager() as m:

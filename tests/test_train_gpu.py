@@ -119,6 +119,44 @@ def test_adam_parity_and_shadows():
     assert not torch.equal(p0[0], tr.table_master)
 
 
+def test_sharded_apply_matches_full_apply():
+    """fh_train_apply_sharded over [0, n) equals fh_train_apply; over a
+    sub-range it touches only that range of the table state."""
+    from paper_2507_03836_b200 import dp
+    cfg = small_cfg(4, 8)
+    trs = []
+    for _ in range(2):
+        enc, tr, coords, target = make(cfg, 700, seed=11)
+        trs.append((enc, tr))
+    c, t = torch.from_numpy(coords).cuda(), torch.from_numpy(target).cuda()
+    (_, a), (_, b) = trs
+    sdp = dp.ShardedDP(b)   # no process group: world 1, shard = whole table
+    for _ in range(2):
+        # identical gradients on both (the encode bwd's atomics are unordered)
+        a.fwd_bwd(c, t, 700)
+        b.grads.copy_(a.grads)
+        a.apply()
+        sdp.reduce()
+        sdp.apply()
+        sdp.gather()
+    torch.cuda.synchronize()
+    assert torch.equal(a.table_master, b.table_master)
+    assert torch.equal(a.table_shadow, b.table_shadow)
+    assert torch.equal(a.mlp_master, b.mlp_master)
+    assert torch.all(b.grads == 0)
+    # partial range
+    b.fwd_bwd(c, t, 700)
+    before = b.table_master.clone().view(-1)
+    shard = b.grads[:b.n_table].clone()
+    lo, hi = 64, 64 + 400
+    b.apply_sharded(lo, hi, shard[lo:hi].contiguous())
+    torch.cuda.synchronize()
+    after = b.table_master.view(-1)
+    assert torch.equal(after[:lo], before[:lo]) and torch.equal(after[hi:], before[hi:])
+    assert not torch.equal(after[lo:hi], before[lo:hi])
+    assert torch.all(b.grads == 0)
+
+
 def test_zero_lr_leaves_parameters():
     cfg = small_cfg(2, 8)
     g = W.rng(0)
