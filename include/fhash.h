@@ -141,6 +141,29 @@ fh_status fh_encode_bwd(fh_encoder enc, const float *coords, int64_t N, const fl
 fh_status fh_encode_indices(fh_encoder enc, const float *coords, int64_t N, uint32_t *idx,
                             float *w, fh_stream stream);
 
+/* ------------------------------------------------- execution order ---
+ * fh_spatial_sort -- an ORDER in which to process a batch so that nearby
+ * samples run together (an execution-order optimisation, not part of the
+ * method: the encode results are unchanged up to fp summation order).
+ * Counting sort of the samples by the 16-bit Morton code of their cell on a
+ * 16^4 grid over [0,1]^4 (4 bits per axis, NaN -> 0).  order [N] uint32
+ * (device) receives a permutation of 0..N-1 (order inside a cell
+ * unspecified).  workspace (device, 16-byte aligned) of
+ * fh_spatial_sort_workspace_size(N) bytes.  N < 2^32.
+ * Errors: FH_E_ARG, FH_E_CUDA. */
+size_t    fh_spatial_sort_workspace_size(int64_t N);
+fh_status fh_spatial_sort(const float *coords, int64_t N, uint32_t *order, void *workspace,
+                          size_t workspace_bytes, fh_stream stream);
+
+/* fh_encode_fwd_ordered / fh_encode_bwd_ordered -- as fh_encode_fwd /
+ * fh_encode_bwd (same inputs, same outputs in the same [N][L*F] row order),
+ * but the kernels visit the samples in `order` (device [N] uint32, a
+ * permutation of 0..N-1, e.g. from fh_spatial_sort). */
+fh_status fh_encode_fwd_ordered(fh_encoder enc, const float *coords, int64_t N, const uint32_t *order,
+                                const void *table, void *out, fh_dtype out_dtype, fh_stream stream);
+fh_status fh_encode_bwd_ordered(fh_encoder enc, const float *coords, int64_t N, const uint32_t *order,
+                                const float *dout, float *dtable, fh_stream stream);
+
 /* fh_zero_grad -- dtable [sum T][F] f32 (device) := 0, stream-ordered
  * (cudaMemsetAsync).  Errors: FH_E_ARG (NULL), FH_E_CUDA. */
 fh_status fh_zero_grad(fh_encoder enc, float *dtable, fh_stream stream);

@@ -85,9 +85,22 @@ template <int F, typename T> struct Gather;
 template <> struct Gather<1, float> {
     static __device__ __forceinline__ void load(const float *t, uint32_t i, float *o) { o[0] = __ldg(t + i); }
 };
+#ifndef FH_GATHER_HINT
+#define FH_GATHER_HINT 0
+#endif
 template <> struct Gather<2, float> {
     static __device__ __forceinline__ void load(const float *t, uint32_t i, float *o) {
+#if FH_GATHER_HINT == 1
+        float2 v;
+        asm("ld.global.nc.L1::no_allocate.v2.f32 {%0,%1}, [%2];" : "=f"(v.x), "=f"(v.y)
+            : "l"(reinterpret_cast<const float2 *>(t) + i));
+#elif FH_GATHER_HINT == 2
+        float2 v;
+        asm("ld.global.nc.L2::evict_last.v2.f32 {%0,%1}, [%2];" : "=f"(v.x), "=f"(v.y)
+            : "l"(reinterpret_cast<const float2 *>(t) + i));
+#else
         const float2 v = __ldg(reinterpret_cast<const float2 *>(t) + i);
+#endif
         o[0] = v.x; o[1] = v.y;
     }
 };
@@ -340,15 +353,18 @@ template <int F, typename T, typename O>
 __global__ void __launch_bounds__(256, FH_FWD_MINB) fwd_kernel(const __grid_constant__ Params P,
                                                   const float4 *__restrict__ coords, int64_t N,
                                                   const T *__restrict__ table, uint32_t full_blocks,
-                                                  O *__restrict__ out, int *__restrict__ flag, int l0, int lc) {
-    // levels [l0, l0 + lc) of every sample (a level group: see DESIGN.md §8)
+                                                  O *__restrict__ out, int *__restrict__ flag, int l0, int lc,
+                                                  const uint32_t *__restrict__ perm) {
+    // levels [l0, l0 + lc) of every sample (a level group: see DESIGN.md §8);
+    // perm (optional): process samples in this (spatially sorted) order
     __shared__ Level slv[kMaxLevels];
     load_levels(P, slv);
     const int L = P.L;
     const int64_t gid = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
-    const int64_t n = gid / lc;
-    if (n >= N) return;
-    const int l = l0 + (int)(gid - n * lc);
+    const int64_t j = gid / lc;
+    if (j >= N) return;
+    const int l = l0 + (int)(gid - j * lc);
+    const int64_t n = perm ? (int64_t)__ldg(perm + j) : j;
     const Level &lv = slv[l];
     const float4 p = __ldg(coords + n);
     Cell c;
@@ -423,14 +439,16 @@ template <int F>
 __global__ void __launch_bounds__(256) bwd_kernel(const __grid_constant__ Params P,
                                                   const float4 *__restrict__ coords, int64_t N,
                                                   const float *__restrict__ dout, float *__restrict__ dtable,
-                                                  int *__restrict__ flag, int l0, int lc) {
+                                                  int *__restrict__ flag, int l0, int lc,
+                                                  const uint32_t *__restrict__ perm) {
     __shared__ Level slv[kMaxLevels];
     load_levels(P, slv);
     const int L = P.L;
     const int64_t gid = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
-    const int64_t n = gid / lc;
-    if (n >= N) return;
-    const int l = l0 + (int)(gid - n * lc);
+    const int64_t j = gid / lc;
+    if (j >= N) return;
+    const int l = l0 + (int)(gid - j * lc);
+    const int64_t n = perm ? (int64_t)__ldg(perm + j) : j;
     const Level &lv = slv[l];
     const float4 p = __ldg(coords + n);
     Cell c;

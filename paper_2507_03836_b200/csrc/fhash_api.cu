@@ -10,6 +10,7 @@
 
 #include "internal.h"
 #include "encode_kernels.cuh"
+#include "sort_kernels.cuh"
 
 namespace fh {
 thread_local char g_err[512] = "";
@@ -70,24 +71,24 @@ static dim3 grid_for(int64_t N, int L) {
 
 template <int F, typename T, typename O>
 static void launch_fwd(fh_encoder e, const float *coords, int64_t N, const void *table, void *out,
-                       cudaStream_t s) {
+                       cudaStream_t s, const uint32_t *perm) {
     const uint32_t full_blocks = (uint32_t)((e->entries * (uint64_t)F * sizeof(T)) / 32);
     for (int g = 0; g < e->n_gf; g++) {
         const int l0 = e->gf[g], lc = e->gf[g + 1] - e->gf[g];
         fh::fwd_kernel<F, T, O><<<grid_for(N, lc), 256, 0, s>>>(
             e->params, reinterpret_cast<const float4 *>(coords), N, reinterpret_cast<const T *>(table),
-            full_blocks, reinterpret_cast<O *>(out), e->flag, l0, lc);
+            full_blocks, reinterpret_cast<O *>(out), e->flag, l0, lc, perm);
     }
 }
 
 template <typename T, typename O>
 static void dispatch_fwd_F(fh_encoder e, const float *coords, int64_t N, const void *table, void *out,
-                           cudaStream_t s) {
+                           cudaStream_t s, const uint32_t *perm) {
     switch (e->F) {
-        case 1: launch_fwd<1, T, O>(e, coords, N, table, out, s); break;
-        case 2: launch_fwd<2, T, O>(e, coords, N, table, out, s); break;
-        case 4: launch_fwd<4, T, O>(e, coords, N, table, out, s); break;
-        default: launch_fwd<8, T, O>(e, coords, N, table, out, s); break;
+        case 1: launch_fwd<1, T, O>(e, coords, N, table, out, s, perm); break;
+        case 2: launch_fwd<2, T, O>(e, coords, N, table, out, s, perm); break;
+        case 4: launch_fwd<4, T, O>(e, coords, N, table, out, s, perm); break;
+        default: launch_fwd<8, T, O>(e, coords, N, table, out, s, perm); break;
     }
 }
 
@@ -222,8 +223,10 @@ void fh_encoder_destroy(fh_encoder e) {
     delete e;
 }
 
-fh_status fh_encode_fwd(fh_encoder e, const float *coords, int64_t N, const void *table, void *out,
-                        fh_dtype out_dtype, fh_stream stream) {
+}  // extern "C"
+
+static fh_status encode_fwd_impl(fh_encoder e, const float *coords, int64_t N, const uint32_t *perm,
+                                 const void *table, void *out, fh_dtype out_dtype, fh_stream stream) {
     g_err[0] = 0;
     fh_status st = check_common(e, coords, N, "fh_encode_fwd");
     if (st != FH_OK) return st;
@@ -236,17 +239,17 @@ fh_status fh_encode_fwd(fh_encoder e, const float *coords, int64_t N, const void
     if ((st = ensure_flag(e)) != FH_OK) return st;
     cudaStream_t s = reinterpret_cast<cudaStream_t>(stream);
     if (e->table_dtype == FH_F32) {
-        if (out_dtype == FH_F32) dispatch_fwd_F<float, float>(e, coords, N, table, out, s);
-        else dispatch_fwd_F<float, __nv_bfloat16>(e, coords, N, table, out, s);
+        if (out_dtype == FH_F32) dispatch_fwd_F<float, float>(e, coords, N, table, out, s, perm);
+        else dispatch_fwd_F<float, __nv_bfloat16>(e, coords, N, table, out, s, perm);
     } else {
-        if (out_dtype == FH_F32) dispatch_fwd_F<__half, float>(e, coords, N, table, out, s);
-        else dispatch_fwd_F<__half, __nv_bfloat16>(e, coords, N, table, out, s);
+        if (out_dtype == FH_F32) dispatch_fwd_F<__half, float>(e, coords, N, table, out, s, perm);
+        else dispatch_fwd_F<__half, __nv_bfloat16>(e, coords, N, table, out, s, perm);
     }
     return cuda_check(cudaGetLastError(), "fh_encode_fwd launch");
 }
 
-fh_status fh_encode_bwd(fh_encoder e, const float *coords, int64_t N, const float *dout, float *dtable,
-                        fh_stream stream) {
+static fh_status encode_bwd_impl(fh_encoder e, const float *coords, int64_t N, const uint32_t *perm,
+                                 const float *dout, float *dtable, fh_stream stream) {
     g_err[0] = 0;
     fh_status st = check_common(e, coords, N, "fh_encode_bwd");
     if (st != FH_OK) return st;
@@ -261,13 +264,62 @@ fh_status fh_encode_bwd(fh_encoder e, const float *coords, int64_t N, const floa
         const int l0 = e->gb[k], lc = e->gb[k + 1] - e->gb[k];
         const dim3 g = grid_for(N, lc);
         switch (e->F) {
-            case 1: fh::bwd_kernel<1><<<g, 256, 0, s>>>(e->params, c4, N, dout, dtable, e->flag, l0, lc); break;
-            case 2: fh::bwd_kernel<2><<<g, 256, 0, s>>>(e->params, c4, N, dout, dtable, e->flag, l0, lc); break;
-            case 4: fh::bwd_kernel<4><<<g, 256, 0, s>>>(e->params, c4, N, dout, dtable, e->flag, l0, lc); break;
-            default: fh::bwd_kernel<8><<<g, 256, 0, s>>>(e->params, c4, N, dout, dtable, e->flag, l0, lc); break;
+            case 1: fh::bwd_kernel<1><<<g, 256, 0, s>>>(e->params, c4, N, dout, dtable, e->flag, l0, lc, perm); break;
+            case 2: fh::bwd_kernel<2><<<g, 256, 0, s>>>(e->params, c4, N, dout, dtable, e->flag, l0, lc, perm); break;
+            case 4: fh::bwd_kernel<4><<<g, 256, 0, s>>>(e->params, c4, N, dout, dtable, e->flag, l0, lc, perm); break;
+            default: fh::bwd_kernel<8><<<g, 256, 0, s>>>(e->params, c4, N, dout, dtable, e->flag, l0, lc, perm); break;
         }
     }
     return cuda_check(cudaGetLastError(), "fh_encode_bwd launch");
+}
+
+extern "C" {
+
+fh_status fh_encode_fwd(fh_encoder e, const float *coords, int64_t N, const void *table, void *out,
+                        fh_dtype out_dtype, fh_stream stream) {
+    return encode_fwd_impl(e, coords, N, nullptr, table, out, out_dtype, stream);
+}
+
+fh_status fh_encode_bwd(fh_encoder e, const float *coords, int64_t N, const float *dout, float *dtable,
+                        fh_stream stream) {
+    return encode_bwd_impl(e, coords, N, nullptr, dout, dtable, stream);
+}
+
+fh_status fh_encode_fwd_ordered(fh_encoder e, const float *coords, int64_t N, const uint32_t *order,
+                                const void *table, void *out, fh_dtype out_dtype, fh_stream stream) {
+    if (!order && N > 0) return fail(FH_E_ARG, "fh_encode_fwd_ordered: NULL order");
+    return encode_fwd_impl(e, coords, N, order, table, out, out_dtype, stream);
+}
+
+fh_status fh_encode_bwd_ordered(fh_encoder e, const float *coords, int64_t N, const uint32_t *order,
+                                const float *dout, float *dtable, fh_stream stream) {
+    if (!order && N > 0) return fail(FH_E_ARG, "fh_encode_bwd_ordered: NULL order");
+    return encode_bwd_impl(e, coords, N, order, dout, dtable, stream);
+}
+
+size_t fh_spatial_sort_workspace_size(int64_t N) {
+    return (size_t)fh::sortk::kBins * 4 + ((size_t)(N < 0 ? 0 : N) * 2 + 255) / 256 * 256;
+}
+
+fh_status fh_spatial_sort(const float *coords, int64_t N, uint32_t *order, void *workspace, size_t ws_bytes,
+                          fh_stream stream) {
+    g_err[0] = 0;
+    if (N < 0 || N > 0xFFFFFFFFll) return fail(FH_E_ARG, "fh_spatial_sort: N out of range");
+    if (N == 0) return FH_OK;
+    if (!coords || !aligned(coords, 16) || !order || !workspace || !aligned(workspace, 16))
+        return fail(FH_E_ARG, "fh_spatial_sort: NULL or misaligned pointer");
+    if (ws_bytes < fh_spatial_sort_workspace_size(N)) return fail(FH_E_ARG, "fh_spatial_sort: workspace too small");
+    cudaStream_t s = reinterpret_cast<cudaStream_t>(stream);
+    uint32_t *hist = reinterpret_cast<uint32_t *>(workspace);
+    uint16_t *keys = reinterpret_cast<uint16_t *>(hist + fh::sortk::kBins);
+    fh_status st = cuda_check(cudaMemsetAsync(hist, 0, fh::sortk::kBins * 4, s), "fh_spatial_sort memset");
+    if (st != FH_OK) return st;
+    int64_t g = (N + 255) / 256;
+    if (g > 148 * 16) g = 148 * 16;
+    fh::sortk::key_hist_kernel<<<(unsigned)g, 256, 0, s>>>(reinterpret_cast<const float4 *>(coords), N, keys, hist);
+    fh::sortk::scan_kernel<<<1, 1024, 0, s>>>(hist);
+    fh::sortk::scatter_kernel<<<(unsigned)g, 256, 0, s>>>(keys, N, hist, order);
+    return cuda_check(cudaGetLastError(), "fh_spatial_sort launch");
 }
 
 fh_status fh_encode_indices(fh_encoder e, const float *coords, int64_t N, uint32_t *idx, float *w,

@@ -27,7 +27,8 @@ EXPORTS = [
     "fh_fold_schedule", "fh_build_levels", "fh_level_info_get", "fh_num_levels", "fh_feature_dim",
     "fh_table_entries", "fh_param_count", "fh_encoder_destroy", "fh_encode_fwd", "fh_encode_bwd",
     "fh_encode_indices", "fh_zero_grad", "fh_encode_fwd_bwd", "fh_encode_step_host", "fh_status_sync", "fh_last_error",
-    "fh_version",
+    "fh_version", "fh_spatial_sort_workspace_size", "fh_spatial_sort", "fh_encode_fwd_ordered",
+    "fh_encode_bwd_ordered",
     # include/fhash_bench.h (measurement kernels)
     "fh_bench_gather", "fh_bench_red", "fh_bench_copy",
     # train step
@@ -82,6 +83,13 @@ def lib() -> ctypes.CDLL:
     L.fh_encode_indices.argtypes = [vp, vp, i64, vp, vp, vp]
     L.fh_encode_fwd_bwd.argtypes = [vp, vp, i64, vp, vp, c_int, vp, vp, c_int, vp]
     L.fh_zero_grad.argtypes = [vp, vp, vp]
+    L.fh_spatial_sort_workspace_size.argtypes = [i64]
+    L.fh_spatial_sort_workspace_size.restype = ctypes.c_size_t
+    L.fh_spatial_sort.argtypes = [vp, i64, vp, vp, ctypes.c_size_t, vp]
+    L.fh_encode_fwd_ordered.argtypes = [vp, vp, i64, vp, vp, vp, c_int, vp]
+    L.fh_encode_bwd_ordered.argtypes = [vp, vp, i64, vp, vp, vp, vp]
+    for name in ("fh_spatial_sort", "fh_encode_fwd_ordered", "fh_encode_bwd_ordered"):
+        getattr(L, name).restype = c_int
     L.fh_encode_step_host.argtypes = [vp, vp, vp, i64, vp, vp, vp, vp, vp, vp, vp, vp]
     L.fh_status_sync.argtypes = [vp, vp]
     L.fh_bench_gather.argtypes = [vp, u64, c_int, i64, c_int, c_int, ctypes.c_uint32, vp, vp]
@@ -182,6 +190,16 @@ class Encoder:
         w = torch.empty((N, self.L, 16), dtype=torch.float32, device=coords.device) if want_w else None
         _check(lib().fh_encode_indices(self._h, _ptr(coords), N, _ptr(idx), _ptr(w), _stream(stream)))
         return idx, w
+
+    def fwd_ordered(self, coords, order, table, out, out_dtype: str = "f32", stream=None):
+        _check(lib().fh_encode_fwd_ordered(self._h, _ptr(coords), coords.shape[0], _ptr(order), _ptr(table),
+                                           _ptr(out), _DT[out_dtype], _stream(stream)))
+        return out
+
+    def bwd_ordered(self, coords, order, dout, dtable, stream=None):
+        _check(lib().fh_encode_bwd_ordered(self._h, _ptr(coords), coords.shape[0], _ptr(order), _ptr(dout),
+                                           _ptr(dtable), _stream(stream)))
+        return dtable
 
     def zero_grad(self, dtable, stream=None):
         _check(lib().fh_zero_grad(self._h, _ptr(dtable), _stream(stream)))
@@ -432,3 +450,22 @@ def sample_voxels(field, N: int, seed: int, subsequence: int, offset: int, coord
     _check(_data_lib().fh_data_sample_voxels(field.data_ptr(), Sx, Sy, Sz, T, N, seed, subsequence, offset,
                                              coords.data_ptr(), target.data_ptr(), _stream(stream)))
     return coords, target
+
+
+class SpatialOrder:
+    """Reusable device buffers for fh_spatial_sort (execution order of a batch)."""
+
+    def __init__(self, max_n: int, device=None):
+        import torch
+        dev = device or torch.device("cuda", torch.cuda.current_device())
+        self.max_n = max_n
+        self.order = torch.empty(max_n, dtype=torch.int32, device=dev)
+        nb = int(lib().fh_spatial_sort_workspace_size(max_n))
+        self.ws = torch.empty(nb, dtype=torch.uint8, device=dev)
+
+    def __call__(self, coords, stream=None):
+        N = coords.shape[0]
+        assert N <= self.max_n
+        _check(lib().fh_spatial_sort(_ptr(coords), N, _ptr(self.order), _ptr(self.ws), self.ws.numel(),
+                                     _stream(stream)))
+        return self.order[:N]

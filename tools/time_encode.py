@@ -32,22 +32,34 @@ def main():
     out = torch.empty((N, cfg.L * cfg.F), device="cuda")
     dtab = torch.zeros((enc.entries, cfg.F), device="cuda")
     flush = torch.empty(256 << 20, dtype=torch.uint8, device="cuda")
-    e = [torch.cuda.Event(enable_timing=True) for _ in range(3)]
-    tf = tb = 0.0
+    e = [torch.cuda.Event(enable_timing=True) for _ in range(4)]
+    sorted_mode = os.environ.get("FH_SORTED", "0") == "1"
+    so = fh.SpatialOrder(N) if sorted_mode else None
+    tf = tb = ts = 0.0
     for it in range(iters + 3):
         flush.fill_(it & 255)
         enc.zero_grad(dtab)
         e[0].record()
-        enc.fwd(coords, table, out)
+        order = so(coords) if so else None
         e[1].record()
-        enc.bwd(coords, dout, dtab)
+        if so:
+            enc.fwd_ordered(coords, order, table, out)
+        else:
+            enc.fwd(coords, table, out)
         e[2].record()
+        if so:
+            enc.bwd_ordered(coords, order, dout, dtab)
+        else:
+            enc.bwd(coords, dout, dtab)
+        e[3].record()
         torch.cuda.synchronize()
         if it >= 3:
-            tf += e[0].elapsed_time(e[1])
-            tb += e[1].elapsed_time(e[2])
-    print(f"{os.path.basename(fh.LIB_PATH)} {name}: fwd {tf / iters:.4f} ms  bwd {tb / iters:.4f} ms  "
-          f"({N / ((tf + tb) / iters / 1e3) / 1e6:.1f} M samples/s)")
+            ts += e[0].elapsed_time(e[1])
+            tf += e[1].elapsed_time(e[2])
+            tb += e[2].elapsed_time(e[3])
+    tot = (ts + tf + tb) / iters
+    print(f"{os.path.basename(fh.LIB_PATH)} {name}{' sorted' if so else ''}: sort {ts / iters:.4f} ms  "
+          f"fwd {tf / iters:.4f} ms  bwd {tb / iters:.4f} ms  ({N / (tot / 1e3) / 1e6:.1f} M samples/s)")
 
 
 if __name__ == "__main__":
