@@ -58,16 +58,19 @@ struct Layout {
     static constexpr uint32_t SBO_W2 = (H / 8) * 128;
     static constexpr uint32_t BYTES_HX = TILE * WHX * 2;
     static constexpr uint32_t BYTES_DZ = TILE * 2 * H * 2;
-    static constexpr uint32_t BYTES_H2 = TILE * H * 2;    // bf16 h2 rows (for dw3)
-    static constexpr uint32_t BYTES_SLOT = BYTES_HX + BYTES_DZ + BYTES_H2;
+    static constexpr uint32_t BYTES_H2 = TILE * H * 2;    // bf16 h2 tile (core-matrix layout, SBO 1024)
+    static constexpr uint32_t BYTES_DY = TILE * 16 * 2;   // [dy_hi, dy_lo, 0 x 14] per sample (SBO 256)
+    // the dw3 MMA reads A rows 64..127 past the h2 tile (results discarded):
+    // keep 1 KB of slack inside the slot so those reads stay in bounds
+    static constexpr uint32_t BYTES_SLOT = BYTES_HX + BYTES_DZ + BYTES_H2 + BYTES_DY + 1024;
     static constexpr uint32_t BYTES_W1 = H * K0 * 2;
     static constexpr uint32_t BYTES_W2 = H * H * 2;
     static constexpr int SLOTS = 2;
     static constexpr uint32_t SMEM = SLOTS * BYTES_SLOT + BYTES_W1 + BYTES_W2;
     // TMEM columns (per slot, base = slot * 256)
-    static constexpr uint32_t T_ACC = 0, T_DW = 64;
+    static constexpr uint32_t T_ACC = 0, T_DW = 64, T_D3 = 64 + WHX;  // T_D3: [dw3_hi, dw3_lo] accumulators
     static constexpr uint32_t TMEM_COLS = 512;
-    static_assert(T_DW + WHX <= 256, "slot TMEM region overflow");
+    static_assert(T_D3 + 16 <= 256, "slot TMEM region overflow");
 };
 
 __device__ __forceinline__ uint32_t pack_bf16(float a, float b) {
@@ -140,6 +143,7 @@ __global__ void __launch_bounds__(256, 1) mlp_train_kernel(const TrainArgs a) {
     uint8_t *sHX = smem + Lo::BYTES_W1 + Lo::BYTES_W2 + slot * Lo::BYTES_SLOT;
     uint8_t *sDZ = sHX + Lo::BYTES_HX;
     uint8_t *sH2 = sDZ + Lo::BYTES_DZ;
+    uint8_t *sDY = sH2 + Lo::BYTES_H2;
     const int64_t n_tiles = (a.N + TILE - 1) / TILE;
 
     // ---- weights -> shared memory (bf16 shadow), once per CTA
@@ -175,14 +179,16 @@ __global__ void __launch_bounds__(256, 1) mlp_train_kernel(const TrainArgs a) {
     const bool issuer = (t == 0);
 
     const uint32_t aHX = tc::smem_u32(sHX), aDZ = tc::smem_u32(sDZ);
+    const uint32_t aH2 = tc::smem_u32(sH2), aDY = tc::smem_u32(sDY);
     const uint32_t aW1 = tc::smem_u32(sW1), aW2 = tc::smem_u32(sW2);
     constexpr uint32_t id_h = tc::idesc_bf16_f32(128, H, false, false);      // N = 64, K-major A,B
     constexpr uint32_t id_dh = tc::idesc_bf16_f32(128, H, false, true);      // B = W2 MN-major
     constexpr uint32_t id_dx = tc::idesc_bf16_f32(128, K0, false, true);     // B = W1 MN-major
     constexpr uint32_t id_dw = tc::idesc_bf16_f32(128, Lo::WHX, true, true); // both MN-major
+    constexpr uint32_t id_d3 = tc::idesc_bf16_f32(128, 16, true, true);      // dw3: H2^T . [dy_hi dy_lo]
 
     uint32_t phase = 0;
-    float dw3a = 0.f, dw3b = 0.f, db3_acc = 0.f, loss_acc = 0.f;
+    float db3_acc = 0.f, loss_acc = 0.f;
     bool bad = false;
     int my_tiles = 0;
 
@@ -213,20 +219,19 @@ __global__ void __launch_bounds__(256, 1) mlp_train_kernel(const TrainArgs a) {
         }
         tc::mbar_wait(mbar, phase); phase ^= 1;
         tc::fence_after_sync();
-        // ---- epilogue 1: H1 = bf16(relu(Z1 + b1)), mask1
-        uint32_t m1[2] = {0u, 0u};
+        // ---- epilogue 1: H1 = bf16(relu(Z1 + b1)) (its sign is the ReLU mask later)
 #pragma unroll
         for (int c = 0; c < H; c += 16) {
             float v[16];
             tc::tmem_ld16(tm + lane_off + Lo::T_ACC + c, v);
             tc::tmem_wait_ld();
             uint32_t p[8];
+            const float4 *bb = reinterpret_cast<const float4 *>(b1 + c);
 #pragma unroll
-            for (int j = 0; j < 16; j += 2) {
-                const float z0 = v[j] + b1[c + j], z1 = v[j + 1] + b1[c + j + 1];
-                m1[(c + j) >> 5] |= (z0 > 0.f ? 1u : 0u) << ((c + j) & 31);
-                m1[(c + j + 1) >> 5] |= (z1 > 0.f ? 1u : 0u) << ((c + j + 1) & 31);
-                p[j / 2] = pack_bf16(fmaxf(z0, 0.f), fmaxf(z1, 0.f));
+            for (int j = 0; j < 16; j += 4) {
+                const float4 b = bb[j / 4];
+                p[j / 2] = pack_bf16(fmaxf(v[j] + b.x, 0.f), fmaxf(v[j + 1] + b.y, 0.f));
+                p[j / 2 + 1] = pack_bf16(fmaxf(v[j + 2] + b.z, 0.f), fmaxf(v[j + 3] + b.w, 0.f));
             }
             st16(sHX, tc::core_off(t, c, Lo::SBO_HX), make_uint4(p[0], p[1], p[2], p[3]));
             st16(sHX, tc::core_off(t, c + 8, Lo::SBO_HX), make_uint4(p[4], p[5], p[6], p[7]));
@@ -245,28 +250,31 @@ __global__ void __launch_bounds__(256, 1) mlp_train_kernel(const TrainArgs a) {
         }
         tc::mbar_wait(mbar, phase); phase ^= 1;
         tc::fence_after_sync();
-        // ---- epilogue 2: H2 = bf16(relu(Z2 + b2)); y = H2 . w3 + b3; MSE; dZ2; dw3
-        uint32_t m2[2] = {0u, 0u};
+        // ---- epilogue 2: H2 = bf16(relu(Z2 + b2)); y = H2 . w3 + b3; MSE; dZ2
+        // ReLU masks are read back as (h > 0): h = bf16(relu(z)) is > 0 iff z > 0.
         float ya[4] = {0.f, 0.f, 0.f, 0.f};
-        uint4 *h2row = reinterpret_cast<uint4 *>(sH2 + t * H * 2);
 #pragma unroll
         for (int c = 0; c < H; c += 16) {
             float v[16];
             tc::tmem_ld16(tm + lane_off + Lo::T_ACC + c, v);
             tc::tmem_wait_ld();
             uint32_t p[8];
+            const float4 *bb = reinterpret_cast<const float4 *>(b2 + c);
+            const float4 *ww = reinterpret_cast<const float4 *>(w3 + c);
 #pragma unroll
-            for (int j = 0; j < 16; j += 2) {
-                const float z0 = v[j] + b2[c + j], z1 = v[j + 1] + b2[c + j + 1];
-                m2[(c + j) >> 5] |= (z0 > 0.f ? 1u : 0u) << ((c + j) & 31);
-                m2[(c + j + 1) >> 5] |= (z1 > 0.f ? 1u : 0u) << ((c + j + 1) & 31);
-                const float h0 = bf16r(fmaxf(z0, 0.f)), h1 = bf16r(fmaxf(z1, 0.f));
-                ya[(j >> 1) & 3] = fmaf(h0, w3[c + j], ya[(j >> 1) & 3]);
-                ya[(j >> 1) & 3] = fmaf(h1, w3[c + j + 1], ya[(j >> 1) & 3]);
+            for (int j = 0; j < 16; j += 4) {
+                const float4 b = bb[j / 4], w = ww[j / 4];
+                const float h0 = bf16r(fmaxf(v[j] + b.x, 0.f)), h1 = bf16r(fmaxf(v[j + 1] + b.y, 0.f));
+                const float h2_ = bf16r(fmaxf(v[j + 2] + b.z, 0.f)), h3 = bf16r(fmaxf(v[j + 3] + b.w, 0.f));
+                ya[0] = fmaf(h0, w.x, ya[0]);
+                ya[1] = fmaf(h1, w.y, ya[1]);
+                ya[2] = fmaf(h2_, w.z, ya[2]);
+                ya[3] = fmaf(h3, w.w, ya[3]);
                 p[j / 2] = pack_bf16(h0, h1);
+                p[j / 2 + 1] = pack_bf16(h2_, h3);
             }
-            h2row[c / 8] = make_uint4(p[0], p[1], p[2], p[3]);
-            h2row[c / 8 + 1] = make_uint4(p[4], p[5], p[6], p[7]);
+            st16(sH2, tc::core_off(t, c, 1024), make_uint4(p[0], p[1], p[2], p[3]));
+            st16(sH2, tc::core_off(t, c + 8, 1024), make_uint4(p[4], p[5], p[6], p[7]));
         }
         const float y = ((ya[0] + ya[1]) + (ya[2] + ya[3])) + b3;
         const float diff = valid ? (y - tgt) : 0.f;
@@ -274,14 +282,23 @@ __global__ void __launch_bounds__(256, 1) mlp_train_kernel(const TrainArgs a) {
         loss_acc = fmaf(diff, diff, loss_acc);
         const float dy = 2.f * diff * a.inv_n_global;
         db3_acc += dy;
+        {   // dy as two bf16 (hi + lo: ~16 mantissa bits) for the dw3 GEMM below
+            const float hi = bf16r(dy);
+            st16(sDY, tc::core_off(t, 0, 256), make_uint4(pack_bf16(hi, dy - hi), 0u, 0u, 0u));
+            st16(sDY, tc::core_off(t, 8, 256), make_uint4(0u, 0u, 0u, 0u));
+        }
 #pragma unroll
         for (int c = 0; c < H; c += 8) {
+            const uint4 u = *reinterpret_cast<const uint4 *>(sH2 + tc::core_off(t, c, 1024));
+            const uint32_t hw[4] = {u.x, u.y, u.z, u.w};
+            const float4 w0 = reinterpret_cast<const float4 *>(w3 + c)[0];
+            const float4 w1 = reinterpret_cast<const float4 *>(w3 + c)[1];
+            const float ww[8] = {w0.x, w0.y, w0.z, w0.w, w1.x, w1.y, w1.z, w1.w};
             uint32_t p[4];
 #pragma unroll
-            for (int j = 0; j < 8; j += 2) {
-                const float d0 = ((m2[(c + j) >> 5] >> ((c + j) & 31)) & 1u) ? dy * w3[c + j] : 0.f;
-                const float d1 = ((m2[(c + j + 1) >> 5] >> ((c + j + 1) & 31)) & 1u) ? dy * w3[c + j + 1] : 0.f;
-                p[j / 2] = pack_bf16(d0, d1);
+            for (int k = 0; k < 4; k++) {
+                const float2 h = unpack_bf16(hw[k]);
+                p[k] = pack_bf16(h.x > 0.f ? dy * ww[2 * k] : 0.f, h.y > 0.f ? dy * ww[2 * k + 1] : 0.f);
             }
             st16(sDZ, tc::core_off(t, c, Lo::SBO_DZ), make_uint4(p[0], p[1], p[2], p[3]));
         }
@@ -289,45 +306,35 @@ __global__ void __launch_bounds__(256, 1) mlp_train_kernel(const TrainArgs a) {
         tc::fence_before_sync();
         slot_sync(slot);
         tc::fence_after_sync();
-        // ---- MMA3: dH1 = dZ2 . W2   (issued before the dw3 reduction below)
+        // ---- MMA3: dH1 = dZ2 . W2 ; MMA6: [dw3_hi dw3_lo] += H2^T . [dy_hi dy_lo]
+        // (MMA6: M = 128 with A rows 64..127 reading past the h2 tile -- discarded)
         if (issuer) {
 #pragma unroll
             for (int s = 0; s < H / 16; s++)
                 tc::mma_bf16(tm + Lo::T_ACC, tc::sdesc(aDZ + s * 256, 128, Lo::SBO_DZ),
                              tc::sdesc(aW2 + s * 2 * Lo::SBO_W2, Lo::SBO_W2, 128), id_dh, s > 0);
+#pragma unroll
+            for (int s = 0; s < TILE / 16; s++)
+                tc::mma_bf16(tm + Lo::T_D3, tc::sdesc(aH2 + s * 2 * 1024, 1024, 128),
+                             tc::sdesc(aDY + s * 2 * 256, 256, 128), id_d3, (my_tiles > 0 || s > 0) ? 1u : 0u);
             tc::commit(mbar);
-        }
-        {   // dw3 += sum over the warp's samples of dy * h2 (fp32), overlapping MMA3
-            float v[64];
-#pragma unroll
-            for (int q = 0; q < 8; q++) {
-                const uint4 u = h2row[q];
-                const uint32_t w[4] = {u.x, u.y, u.z, u.w};
-#pragma unroll
-                for (int k = 0; k < 4; k++) {
-                    const float2 f = unpack_bf16(w[k]);
-                    v[8 * q + 2 * k] = dy * f.x;
-                    v[8 * q + 2 * k + 1] = dy * f.y;
-                }
-            }
-            warp_reduce64(v, lane);
-            dw3a += v[0];
-            dw3b += v[1];
         }
         tc::mbar_wait(mbar, phase); phase ^= 1;
         tc::fence_after_sync();
-        // ---- epilogue 3: dZ1 = bf16(dH1 * mask1)
+        // ---- epilogue 3: dZ1 = bf16(dH1 * mask1), mask1 = (h1 > 0) from the H1 tile
 #pragma unroll
         for (int c = 0; c < H; c += 16) {
             float v[16];
             tc::tmem_ld16(tm + lane_off + Lo::T_ACC + c, v);
             tc::tmem_wait_ld();
+            const uint4 ha = *reinterpret_cast<const uint4 *>(sHX + tc::core_off(t, c, Lo::SBO_HX));
+            const uint4 hb = *reinterpret_cast<const uint4 *>(sHX + tc::core_off(t, c + 8, Lo::SBO_HX));
+            const uint32_t hw[8] = {ha.x, ha.y, ha.z, ha.w, hb.x, hb.y, hb.z, hb.w};
             uint32_t p[8];
 #pragma unroll
-            for (int j = 0; j < 16; j += 2) {
-                const float d0 = ((m1[(c + j) >> 5] >> ((c + j) & 31)) & 1u) ? v[j] : 0.f;
-                const float d1 = ((m1[(c + j + 1) >> 5] >> ((c + j + 1) & 31)) & 1u) ? v[j + 1] : 0.f;
-                p[j / 2] = pack_bf16(d0, d1);
+            for (int k = 0; k < 8; k++) {
+                const float2 h = unpack_bf16(hw[k]);
+                p[k] = pack_bf16(h.x > 0.f ? v[2 * k] : 0.f, h.y > 0.f ? v[2 * k + 1] : 0.f);
             }
             st16(sDZ, tc::core_off(t, H + c, Lo::SBO_DZ), make_uint4(p[0], p[1], p[2], p[3]));
             st16(sDZ, tc::core_off(t, H + c + 8, Lo::SBO_DZ), make_uint4(p[4], p[5], p[6], p[7]));
@@ -389,9 +396,11 @@ __global__ void __launch_bounds__(256, 1) mlp_train_kernel(const TrainArgs a) {
                 }
             }
         }
-        const int col = reduce64_col(lane);
-        atomicAdd(g + off_w3(K0) + col, dw3a);
-        atomicAdd(g + off_w3(K0) + col + 1, dw3b);
+        // dw3[r] = hi + lo columns of the D3 accumulator, rows 0..63
+        float d3[16];
+        tc::tmem_ld16(tm + lane_off + Lo::T_D3, d3);
+        tc::tmem_wait_ld();
+        if (r < H) atomicAdd(g + off_w3(K0) + r, d3[0] + d3[1]);
     }
     // db3 and loss: warp reduce, then one atomic per CTA
 #pragma unroll
