@@ -281,6 +281,18 @@ def train_step_bench(fh, torch, W, which, rank, world, dist, steps, warmup):
         t = torch.tensor([total], device="cuda", dtype=torch.float64)
         dist.all_reduce(t, op=dist.ReduceOp.MAX)
         total = float(t.item())
+    # NEXT-1: the renderer's model evaluation V = model(S) (fh_infer) on the
+    # same batch shape, after training
+    yb = torch.empty((n_local,), device="cuda")
+    for _ in range(3):
+        tr.infer(coords, yb)
+    ie0, ie1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    ie0.record(stream)
+    for _ in range(steps):
+        tr.infer(coords, yb)
+    ie1.record(stream)
+    torch.cuda.synchronize()
+    infer_ms = ie0.elapsed_time(ie1) / steps
     # DP correctness: after the timed steps the replicas must be bit-identical
     same = dp.replicas_identical(tr.shadow_flat) and dp.replicas_identical(tr.mlp_master)
     last = tr.loss.clone()
@@ -298,6 +310,8 @@ def train_step_bench(fh, torch, W, which, rank, world, dist, steps, warmup):
         "phase_ms": {"sample": phase[0], "fwd_bwd": phase[1], "grad_reduce": phase[2],
                      "adam_and_gather": phase[3]},
         "dp": "reduce-scatter + sharded Adam + all-gather (NCCL)" if world > 1 else "single GPU",
+        "infer": {"what": "fh_infer: encode fwd + tcgen05 MLP forward (Alg. 1 V = model(S))",
+                  "ms": infer_ms, "samples_per_s": n_local / (infer_ms / 1e3)},
         "loss_first_warmup": losses[0], "loss_last": float(last.item()), "status": int(st),
         "params": enc.param_count + tr.n_mlp, "gpu_launches_per_step": 6, "replicas_identical": bool(same),
     }

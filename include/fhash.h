@@ -286,6 +286,23 @@ fh_status fh_trainer_status(fh_trainer tr, fh_stream stream);
 int64_t   fh_trainer_step_count(fh_trainer tr);
 void      fh_trainer_destroy(fh_trainer tr);
 
+/* ============================================================ inference
+ * The renderer's model evaluation "V = model(S)" (Alg. 1):
+ * encode fwd (bf16 encoding into workspace) + the MLP forward on tcgen05,
+ * with exactly the forward numerics of the train step (R13).  table: the
+ * encoder's table dtype (fp16 shadow or fp32); mlp_shadow bf16 and
+ * mlp_master fp32 in the flat MLP layout; y [N] f32 (device).  workspace of
+ * fh_infer_workspace_size(enc, mlp, N) bytes.  Errors as fh_train_fwd_bwd. */
+size_t    fh_infer_workspace_size(fh_encoder enc, const fh_mlp_desc *mlp, int64_t max_batch);
+fh_status fh_infer(fh_encoder enc, const fh_mlp_desc *mlp, const void *table, const void *mlp_shadow,
+                   const float *mlp_master, const float *coords, int64_t N, float *y, void *workspace,
+                   size_t workspace_bytes, fh_stream stream);
+
+/* ARM marching pace, Alg. 1 line "N_s = max(min(N_r / N_a, 64), 1)"
+ * (P:255): N_r read as the total number of rays (the symbol is undefined in
+ * the paper; R19), integer division.  0 when no ray is alive. */
+int64_t   fh_arm_pace(int64_t n_rays, int64_t n_alive);
+
 /* Thread-local text of the last error on this thread ("" if none). */
 const char *fh_last_error(void);
 

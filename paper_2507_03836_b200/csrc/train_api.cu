@@ -246,6 +246,53 @@ fh_status fh_trainer_status(fh_trainer tr, fh_stream stream) {
 
 int64_t fh_trainer_step_count(fh_trainer tr) { return tr ? tr->step : -1; }
 
+size_t fh_infer_workspace_size(fh_encoder enc, const fh_mlp_desc *m, int64_t max_batch) {
+    if (!enc || !m || max_batch < 0) return 0;
+    return align_up((size_t)max_batch * (size_t)m->n_in * 2, 256);
+}
+
+fh_status fh_infer(fh_encoder enc, const fh_mlp_desc *m, const void *table, const void *mlp_shadow,
+                   const float *mlp_master, const float *coords, int64_t N, float *y, void *workspace,
+                   size_t workspace_bytes, fh_stream stream) {
+    g_err[0] = 0;
+    fh_status st = check_mlp(enc, m);
+    if (st != FH_OK) return st;
+    if (N < 0) return fail(FH_E_ARG, "fh_infer: N < 0");
+    if (N == 0) return FH_OK;
+    if (!mlp_shadow || !mlp_master || !y || !workspace || !aligned(workspace, 16))
+        return fail(FH_E_ARG, "fh_infer: NULL or misaligned pointer");
+    if (workspace_bytes < fh_infer_workspace_size(enc, m, N)) return fail(FH_E_ARG, "fh_infer: workspace too small");
+    __nv_bfloat16 *x = reinterpret_cast<__nv_bfloat16 *>(workspace);
+    if ((st = fh_encode_fwd(enc, coords, N, table, x, FH_BF16, stream)) != FH_OK) return st;
+    cudaStream_t s = reinterpret_cast<cudaStream_t>(stream);
+    fh::mlp::InferArgs a{x, reinterpret_cast<const __nv_bfloat16 *>(mlp_shadow), mlp_master, y, N};
+    int n_sm = 148, dev = 0;
+    cudaGetDevice(&dev);
+    cudaDeviceGetAttribute(&n_sm, cudaDevAttrMultiProcessorCount, dev);
+    const int64_t pairs = ((N + fh::mlp::TILE - 1) / fh::mlp::TILE + 1) / 2;
+    const int grid = (int)(pairs < 2 * n_sm ? pairs : 2 * n_sm);
+    auto go = [&](auto kern, int smem) -> fh_status {
+        fh_status q = cuda_check(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, smem),
+                                 "cudaFuncSetAttribute(mlp_infer)");
+        if (q != FH_OK) return q;
+        kern<<<grid, 256, smem, s>>>(a);
+        return cuda_check(cudaGetLastError(), "mlp_infer_kernel launch");
+    };
+    switch (m->n_in) {
+        case 16: return go(fh::mlp::mlp_infer_kernel<16>, (int)fh::mlp::InferLayout<16>::SMEM);
+        case 32: return go(fh::mlp::mlp_infer_kernel<32>, (int)fh::mlp::InferLayout<32>::SMEM);
+        case 48: return go(fh::mlp::mlp_infer_kernel<48>, (int)fh::mlp::InferLayout<48>::SMEM);
+        default: return go(fh::mlp::mlp_infer_kernel<64>, (int)fh::mlp::InferLayout<64>::SMEM);
+    }
+}
+
+int64_t fh_arm_pace(int64_t n_rays, int64_t n_alive) {
+    if (n_alive <= 0 || n_rays <= 0) return 0;
+    int64_t p = n_rays / n_alive;
+    if (p > 64) p = 64;
+    return p < 1 ? 1 : p;
+}
+
 void fh_trainer_destroy(fh_trainer tr) { delete tr; }
 
 }  // extern "C"

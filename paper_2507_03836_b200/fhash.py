@@ -34,6 +34,8 @@ EXPORTS = [
     # train step
     "fh_mlp_param_count", "fh_train_workspace_size", "fh_trainer_create", "fh_train_fwd_bwd", "fh_train_apply",
     "fh_train_step", "fh_trainer_status", "fh_trainer_step_count", "fh_trainer_destroy", "fh_train_apply_sharded",
+    # inference (renderer's model evaluation) and the ARM pace rule
+    "fh_infer_workspace_size", "fh_infer", "fh_arm_pace",
     # include/fhash_data.h (synthetic data, harness)
     "fh_data_gaussian_blobs", "fh_data_value_noise", "fh_data_normalize", "fh_data_sample_voxels",
 ]
@@ -274,6 +276,12 @@ def _train_lib():
     L.fh_train_apply.argtypes = [vp, vp]
     L.fh_train_apply_sharded.argtypes = [vp, i64, i64, vp, vp]
     L.fh_train_apply_sharded.restype = ctypes.c_int
+    L.fh_infer_workspace_size.argtypes = [vp, ctypes.POINTER(MLPDesc), i64]
+    L.fh_infer_workspace_size.restype = ctypes.c_size_t
+    L.fh_infer.argtypes = [vp, ctypes.POINTER(MLPDesc), vp, vp, vp, vp, i64, vp, vp, ctypes.c_size_t, vp]
+    L.fh_infer.restype = ctypes.c_int
+    L.fh_arm_pace.argtypes = [i64, i64]
+    L.fh_arm_pace.restype = i64
     L.fh_trainer_status.argtypes = [vp, vp]
     L.fh_trainer_step_count.argtypes = [vp]
     L.fh_trainer_step_count.restype = i64
@@ -373,6 +381,22 @@ class Trainer:
                                              self.loss.data_ptr(), _stream(stream)))
         return self.loss
 
+    def infer(self, coords, y=None, stream=None):
+        """Model evaluation V = model(S) (fh_infer) with this trainer's
+        current parameters; reuses the trainer workspace's encoder buffer."""
+        import torch
+        N = coords.shape[0]
+        assert N <= self.max_batch
+        if y is None:
+            y = torch.empty(N, dtype=torch.float32, device=coords.device)
+        table = self.table_shadow if self.table_shadow is not None else self.table_master
+        L = _train_lib()
+        ws = int(L.fh_infer_workspace_size(self.enc.handle, ctypes.byref(self.desc), N))
+        _check(L.fh_infer(self.enc.handle, ctypes.byref(self.desc), _ptr(table), _ptr(self.mlp_shadow),
+                          _ptr(self.mlp_master), _ptr(coords), N, _ptr(y), _ptr(self.workspace), ws,
+                          _stream(stream)))
+        return y
+
     def apply_sharded(self, begin: int, end: int, grad_shard, stream=None):
         _check(_train_lib().fh_train_apply_sharded(self._h, begin, end, _ptr(grad_shard), _stream(stream)))
 
@@ -394,6 +418,11 @@ class Trainer:
     @property
     def step_count(self) -> int:
         return int(_train_lib().fh_trainer_step_count(self._h))
+
+
+def arm_pace(n_rays: int, n_alive: int) -> int:
+    """Alg. 1 marching pace N_s = max(min(N_r / N_a, 64), 1) (fh_arm_pace)."""
+    return int(_train_lib().fh_arm_pace(n_rays, n_alive))
 
 
 # ------------------------------------------------------------ synthetic data (harness)

@@ -99,6 +99,15 @@ def test_fold_schedule_errors():
         fh.fold_schedule((4, 4, 4), 2, 1)
 
 
+def test_arm_pace_alg1():
+    """Alg. 1: N_s = max(min(N_r / N_a, 64), 1); 0 when no ray alive."""
+    assert fh.arm_pace(1000, 1000) == 1
+    assert fh.arm_pace(1000, 1) == 64
+    assert fh.arm_pace(100, 3) == 33
+    assert fh.arm_pace(100, 200) == 1
+    assert fh.arm_pace(100, 0) == 0
+
+
 def test_encode_argument_errors_are_host_side():
     """Argument validation happens before any device work: NULL/misaligned
     pointers and bad dtypes are rejected synchronously (no GPU needed)."""

@@ -157,6 +157,27 @@ def test_sharded_apply_matches_full_apply():
     assert torch.all(b.grads == 0)
 
 
+@pytest.mark.parametrize("F,L,N", [(2, 16, 1000), (4, 16, 3001), (4, 4, 130)])
+def test_infer_forward_parity(F, L, N):
+    """NEXT-1: fh_infer (encode fwd + tcgen05 MLP forward) equals Oracle-T's
+    forward on the GPU's own bf16 encoding, and reproduces the train step's
+    loss."""
+    cfg = small_cfg(F, L)
+    enc, tr, coords, target = make(cfg, N, seed=21 + F + L)
+    c, t = torch.from_numpy(coords).cuda(), torch.from_numpy(target).cuda()
+    loss = tr.fwd_bwd(c, t, N).item()
+    x0 = tr.enc_out(N).float().cpu().numpy().astype(np.float64)
+    y = tr.infer(c).cpu().numpy().astype(np.float64)
+    master = tr.mlp_master.cpu().numpy().astype(np.float64)
+    K0, o, layers = cfg.L * cfg.F, 0, []
+    for fi, fo in ((K0, 64), (64, 64), (64, 1)):
+        Wt = master[o:o + fi * fo].reshape(fo, fi); o += fi * fo
+        layers.append((Wt, master[o:o + fo])); o += fo
+    yr, _ = T.mlp_forward(x0, layers)
+    assert np.max(np.abs(y - yr)) <= 1e-3 * max(1.0, np.max(np.abs(yr)))
+    assert abs(np.mean((y - target) ** 2) - loss) <= 1e-4 * loss
+
+
 def test_zero_lr_leaves_parameters():
     cfg = small_cfg(2, 8)
     g = W.rng(0)
