@@ -66,6 +66,15 @@ def lib():
         L.fho_encode_bwd.restype = None
         L.fho_level_stats.argtypes = [u32p, ctypes.c_int, ctypes.c_uint64, ctypes.c_uint64, u64p, u64p]
         L.fho_level_stats.restype = ctypes.c_int
+        mcommon = [u32p, ctypes.c_int, ctypes.c_uint32, ctypes.c_uint64]
+        L.fho_mhe_indices.argtypes = mcommon + [f32p, ctypes.c_int64, u32p, f64p]
+        L.fho_mhe_indices.restype = ctypes.c_int64
+        L.fho_mhe_fwd.argtypes = mcommon + [ctypes.c_int, f32p, ctypes.c_int64, f64p, f64p, f64p]
+        L.fho_mhe_fwd.restype = None
+        L.fho_mhe_bwd.argtypes = mcommon + [ctypes.c_int, f32p, ctypes.c_int64, f64p, f64p, f64p]
+        L.fho_mhe_bwd.restype = None
+        L.fho_mhe_level_stats.argtypes = [ctypes.c_uint32, ctypes.c_uint64, ctypes.c_uint64, u64p, u64p]
+        L.fho_mhe_level_stats.restype = ctypes.c_int
         _lib = L
     return _lib
 
@@ -160,6 +169,63 @@ class Levels:
         if rc != 0:
             raise ValueError(f"level_stats rc={rc}")
         return int(d[0]), int(col[0]), float(d[0]) / float(self.tsize[l])
+
+
+class MHELevels:
+    """NEXT-3 oracle: the MHE baseline (one 3D hash encoder per key frame,
+    fixed T per level; Fig. 4).  res: vertices per
+    spatial axis per level."""
+
+    def __init__(self, res: Sequence[int], n_frames: int, T: int):
+        self.res = _c(res, np.uint32)
+        self.L, self.n_frames, self.T = len(self.res), int(n_frames), int(T)
+        self.total = self.L * self.n_frames * self.T
+
+    def param_count(self, F: int) -> int:
+        return self.total * F
+
+    def _common(self):
+        return (_p(self.res, ctypes.c_uint32), self.L, self.n_frames, self.T)
+
+    def indices(self, coords, want_w=True):
+        c = _c(coords, np.float32).reshape(-1, 4)
+        N = c.shape[0]
+        idx = np.zeros((N, self.L, 8), np.uint32)
+        W = np.zeros((N, self.L, 8), np.float64) if want_w else None
+        nb = lib().fho_mhe_indices(*self._common(), _p(c, ctypes.c_float), N, _p(idx, ctypes.c_uint32),
+                                   _p(W, ctypes.c_double) if want_w else None)
+        return idx, W, int(nb)
+
+    def forward(self, coords, table, want_abs=False):
+        c = _c(coords, np.float32).reshape(-1, 4)
+        t = _c(np.asarray(table).astype(np.float64), np.float64)
+        F = t.shape[1]
+        assert t.shape[0] == self.total
+        N = c.shape[0]
+        out = np.zeros((N, self.L * F))
+        ab = np.zeros_like(out) if want_abs else None
+        lib().fho_mhe_fwd(*self._common(), F, _p(c, ctypes.c_float), N, _p(t, ctypes.c_double),
+                          _p(out, ctypes.c_double), _p(ab, ctypes.c_double) if want_abs else None)
+        return (out, ab) if want_abs else out
+
+    def backward(self, coords, dout, F, want_abs=False):
+        c = _c(coords, np.float32).reshape(-1, 4)
+        g = _c(np.asarray(dout).astype(np.float64), np.float64)
+        N = c.shape[0]
+        G = np.zeros((self.total, F))
+        A = np.zeros_like(G) if want_abs else None
+        lib().fho_mhe_bwd(*self._common(), F, _p(c, ctypes.c_float), N, _p(g, ctypes.c_double),
+                          _p(G, ctypes.c_double), _p(A, ctypes.c_double) if want_abs else None)
+        return (G, A) if want_abs else G
+
+    def level_stats(self, l: int, max_vertices: int = 1 << 27):
+        d = np.zeros(1, np.uint64)
+        col = np.zeros(1, np.uint64)
+        rc = lib().fho_mhe_level_stats(int(self.res[l]), self.T, max_vertices, _p(d, ctypes.c_uint64),
+                                       _p(col, ctypes.c_uint64))
+        if rc != 0:
+            raise ValueError(f"mhe level_stats rc={rc}")
+        return int(d[0]), int(col[0]), float(d[0]) / float(self.T)
 
 
 def fhash(res4: Sequence[int], x: int, y: int, z: int, t: int) -> int:

@@ -240,6 +240,136 @@ void fho_encode_bwd(const uint32_t *res, const int32_t *hashed, const uint64_t *
     }
 }
 
+/* ------------------------------------------------------------ NEXT-3 --
+ * MHE baseline encoder (the comparison system of P:378 / Fig. 4, P:177-182;
+ * SPEC baseline_encode S:321-329): one 3D multi-resolution hash encoder per
+ * key frame, a FIXED table size T per level (bucket waste on small levels,
+ * S:354), index = direct x + y R + z R^2 when R^3 <= T, else the spatial hash
+ * (x*1 xor y*2654435761 xor z*805459861) mod T (uint32); trilinear blend of 8
+ * corners.  Frame k of a sample: nearest key frame of its t (reading R20):
+ * s = fp32(t * (n-1)), k = clamp(floor(s + 0.5), 0, n-1) with t clamped as
+ * R2.  Level l of frame k occupies entries offset_l + k*T + [0, T).
+ * Corner order c = bx + 2 by + 4 bz.  W_c in fp64 from the fp32 fractions. */
+static int mhe_corners_one(const float *p, uint32_t R, uint32_t n_frames, uint64_t T, uint64_t offset,
+                           uint64_t idx[8], double W[8])
+{
+    uint32_t i[3];
+    float w[3];
+    int bad = 0;
+    for (int a = 0; a < 3; a++) locate_axis(p[a], R, &i[a], &w[a], &bad);
+    uint32_t k_i;
+    float k_w;
+    /* frame: nearest vertex of an n_frames-vertex time axis */
+    {
+        float pc;
+        if (p[3] >= 0.0f) { if (p[3] <= 1.0f) pc = p[3]; else { pc = 1.0f; bad = 1; } }
+        else { pc = 0.0f; bad = 1; }
+        volatile float nm1 = (float)(n_frames - 1);
+        volatile float s = pc * nm1;
+        float fl = floorf(s);
+        int64_t k = (int64_t)fl + ((s - fl) >= 0.5f ? 1 : 0);
+        if (k < 0) k = 0;
+        if (k > (int64_t)n_frames - 1) k = (int64_t)n_frames - 1;
+        k_i = (uint32_t)k;
+        k_w = 0.0f;
+        (void)k_w;
+    }
+    const uint64_t cube = (uint64_t)R * R * R;
+    for (int c = 0; c < 8; c++) {
+        uint32_t b[3] = { (uint32_t)(c & 1), (uint32_t)((c >> 1) & 1), (uint32_t)((c >> 2) & 1) };
+        uint32_t X = i[0] + b[0], Y = i[1] + b[1], Z = i[2] + b[2];
+        uint64_t local;
+        if (cube <= T) local = (uint64_t)X + (uint64_t)Y * R + (uint64_t)Z * R * R;
+        else local = (uint64_t)((X * 1u) ^ (Y * 2654435761u) ^ (Z * 805459861u)) % T;
+        idx[c] = offset + (uint64_t)k_i * T + local;
+        double Wc = 1.0;
+        for (int a = 0; a < 3; a++) Wc *= b[a] ? (double)w[a] : 1.0 - (double)w[a];
+        W[c] = Wc;
+    }
+    return bad;
+}
+
+/* res[L]: vertices per spatial axis; every level has T entries per frame. */
+int64_t fho_mhe_indices(const uint32_t *res, int L, uint32_t n_frames, uint64_t T, const float *coords,
+                        int64_t N, uint32_t *idx, double *W)
+{
+    int64_t nbad = 0;
+    for (int64_t n = 0; n < N; n++) {
+        int bad = 0;
+        for (int l = 0; l < L; l++) {
+            uint64_t id[8];
+            double w[8];
+            bad |= mhe_corners_one(coords + 4 * n, res[l], n_frames, T, (uint64_t)l * n_frames * T, id, w);
+            for (int c = 0; c < 8; c++) {
+                idx[(n * L + l) * 8 + c] = (uint32_t)id[c];
+                if (W) W[(n * L + l) * 8 + c] = w[c];
+            }
+        }
+        nbad += bad;
+    }
+    return nbad;
+}
+
+void fho_mhe_fwd(const uint32_t *res, int L, uint32_t n_frames, uint64_t T, int F, const float *coords,
+                 int64_t N, const double *table, double *out, double *absout)
+{
+    for (int64_t n = 0; n < N; n++)
+        for (int l = 0; l < L; l++) {
+            uint64_t id[8];
+            double w[8];
+            mhe_corners_one(coords + 4 * n, res[l], n_frames, T, (uint64_t)l * n_frames * T, id, w);
+            for (int f = 0; f < F; f++) {
+                double acc = 0.0, aacc = 0.0;
+                for (int c = 0; c < 8; c++) {
+                    double e = table[id[c] * (uint64_t)F + f];
+                    acc += w[c] * e;
+                    aacc += w[c] * fabs(e);
+                }
+                out[n * (int64_t)L * F + l * F + f] = acc;
+                if (absout) absout[n * (int64_t)L * F + l * F + f] = aacc;
+            }
+        }
+}
+
+void fho_mhe_bwd(const uint32_t *res, int L, uint32_t n_frames, uint64_t T, int F, const float *coords,
+                 int64_t N, const double *dout, double *G, double *A)
+{
+    for (int64_t n = 0; n < N; n++)
+        for (int l = 0; l < L; l++) {
+            uint64_t id[8];
+            double w[8];
+            mhe_corners_one(coords + 4 * n, res[l], n_frames, T, (uint64_t)l * n_frames * T, id, w);
+            for (int c = 0; c < 8; c++)
+                for (int f = 0; f < F; f++) {
+                    double g = dout[n * (int64_t)L * F + l * F + f];
+                    G[id[c] * (uint64_t)F + f] += w[c] * g;
+                    if (A) A[id[c] * (uint64_t)F + f] += fabs(w[c] * g);
+                }
+        }
+}
+
+/* MHE level statistics over one frame: distinct buckets hit by the R^3
+ * vertices, collisions = R^3 - distinct, utilisation = distinct / T. */
+int fho_mhe_level_stats(uint32_t R, uint64_t T, uint64_t max_vertices, uint64_t *distinct, uint64_t *collisions)
+{
+    uint64_t C = (uint64_t)R * R * R;
+    if (C > max_vertices) return -1;
+    uint8_t *hit = calloc(T, 1);
+    if (!hit) return -2;
+    uint64_t d = 0;
+    for (uint32_t z = 0; z < R; z++)
+        for (uint32_t y = 0; y < R; y++)
+            for (uint32_t x = 0; x < R; x++) {
+                uint64_t b = (C <= T) ? (uint64_t)x + (uint64_t)y * R + (uint64_t)z * R * R
+                                      : (uint64_t)((x * 1u) ^ (y * 2654435761u) ^ (z * 805459861u)) % T;
+                if (!hit[b]) { hit[b] = 1; d++; }
+            }
+    free(hit);
+    *distinct = d;
+    *collisions = C - d;
+    return 0;
+}
+
 /* Oracle-S, encoding_stats: brute force over every lattice
  * vertex of level l: buckets hit, collisions = vertices - distinct buckets,
  * utilisation = distinct / T_l.  Returns -1 if the level has more than
