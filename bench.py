@@ -317,6 +317,50 @@ def train_step_bench(fh, torch, W, which, rank, world, dist, steps, warmup):
     }
 
 
+def paper_encoder_compare(fh, torch, W, steps):
+    """NEXT-3: F-Hash vs the MHE baseline on a paper-shaped workload
+    (Combustion-Seg FBB 200x110x54, 10 key frames, fold 2, F = 2; MHE with
+    T = 2^20, 6 levels, one encoder per key frame -- PAPER.md Table 3 column
+    P:619), batch 2^21 of voxel-aligned samples on key frames.
+    Encode fwd + bwd, fp32 tables, L2 flushed before each step."""
+    S, n, B = (200, 110, 54), 10, 1 << 21
+    gen = torch.Generator("cuda").manual_seed(7)
+    vox = [torch.randint(0, s, (B,), device="cuda", generator=gen) for s in S]
+    k = torch.randint(0, n, (B,), device="cuda", generator=gen)
+    coords = torch.stack([vox[0] / (S[0] - 1), vox[1] / (S[1] - 1), vox[2] / (S[2] - 1), k / (n - 1)],
+                         1).float().contiguous()
+    flush = torch.empty(256 << 20, dtype=torch.uint8, device="cuda")
+    res = {}
+    encs = {
+        "fhash": fh.Encoder(fh.fold_schedule(S, n, 2), 2),
+        "mhe": fh.MHEEncoder(W.geometric(16, 200, 6), 2, 1 << 20, n),
+    }
+    for name, enc in encs.items():
+        table = (torch.rand((enc.entries, 2), device="cuda", generator=gen) - 0.5) * 2e-4
+        out = torch.empty((B, enc.L * 2), device="cuda")
+        g = torch.randn((B, enc.L * 2), device="cuda", generator=gen)
+        dt = torch.zeros_like(table)
+        e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        tot = 0.0
+        for it in range(steps + 3):
+            flush.fill_(it & 255)
+            enc.zero_grad(dt)
+            e0.record()
+            enc.fwd(coords, table, out)
+            enc.bwd(coords, g, dt)
+            e1.record()
+            torch.cuda.synchronize()
+            if it >= 3:
+                tot += e0.elapsed_time(e1)
+        ms = tot / steps
+        res[name] = {"levels": enc.L, "params": enc.param_count, "params_Mi": round(enc.param_count / 2 ** 20, 2),
+                     "fwd_bwd_ms": ms, "samples_per_s": B / (ms / 1e3)}
+        del table, out, g, dt
+    res["workload"] = ("Combustion-Seg shape: FBB 200x110x54, 10 key frames, batch 2^21 voxel samples; "
+                       "F-Hash fold 2 (Eqs. 4-8) vs MHE T=2^20 x 6 levels x 10 frames; F=2 fp32")
+    return res
+
+
 def run_ours(args, rank, local_rank, world):
     import numpy as np
     import torch
@@ -422,6 +466,8 @@ def run_ours(args, rank, local_rank, world):
             torch.cuda.empty_cache()
         train["cfg5"] = train_step_bench(fh, torch, W, "cfg5", rank, world, dist, kt, args.warmup)
         torch.cuda.empty_cache()
+    encoders = paper_encoder_compare(fh, torch, W, max(3, min(K, 10))) if not args.no_train else None
+    torch.cuda.empty_cache()
 
     if rank != 0:
         if dist:
@@ -460,6 +506,7 @@ def run_ours(args, rank, local_rank, world):
         "kernels_ms": {"zero_grad": zero_ms, "encode_fwd": fwd_ms, "encode_bwd": bwd_ms, "step": step_ms},
         "roofline": roofline, "gather_roofline": gather_roofline, "cpu_baseline": cpu, "e2e": e2e,
         "gpu_launches": 2 * K, "clocks": clk.summary(), "train_step": train,
+        "paper_encoders": encoders,
     }
     print(json.dumps(line), flush=True)
     if dist:

@@ -100,6 +100,25 @@ fh_status fh_fold_schedule(const uint32_t S_xyz[3], uint32_t n_t, uint32_t fold,
 fh_status fh_build_levels(const fh_level_res *res, int L, int F, fh_dtype table_dtype,
                           uint64_t cap, fh_encoder *out);
 
+/* ---------------------------------------------------------- NEXT-3 ---
+ * fh_build_mhe -- the MHE baseline the paper compares against (
+ * Fig. 4; SPEC baseline_encode S:321-329), on the same kernels:
+ * one 3D multi-resolution hash encoder per key frame.  res[L]: vertices per
+ * spatial axis per level; every level and frame has a FIXED table of T
+ * entries (power of two): direct index x + y R + z R^2 when R^3 <= T (the
+ * rest of the T buckets are wasted), else (x*1 ^ y*2654435761 ^ z*805459861)
+ * mod T (uint32).  A sample's frame is the key frame nearest to its t:
+ * s = fp32(t (n_frames-1)), k = floor(s) + (s - floor(s) >= 0.5) (R20);
+ * trilinear blend of the 8 corners of its (x,y,z) cell.  Table: level l,
+ * frame k at entries offset_l + k T + [0, T); params = L n_frames T F.
+ * The fh_encode_* calls accept the returned handle (fh_encode_indices then
+ * writes [N][L][8]); the ordered variants and the trainer do not.
+ * Errors: FH_E_ARG, FH_E_RANGE. */
+fh_status fh_build_mhe(const uint32_t *res, int L, int F, fh_dtype table_dtype, uint64_t T,
+                       uint32_t n_frames, fh_encoder *out);
+/* 0 = F-Hash Tesseract encoder, 1 = MHE baseline. */
+int       fh_encoder_kind(fh_encoder enc);
+
 fh_status fh_level_info_get(fh_encoder enc, int l, fh_level_info *out);
 int       fh_num_levels(fh_encoder enc);
 int       fh_feature_dim(fh_encoder enc);

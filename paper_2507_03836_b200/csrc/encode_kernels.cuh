@@ -471,6 +471,64 @@ __global__ void __launch_bounds__(256) bwd_kernel(const __grid_constant__ Params
     }
 }
 
+// ------------------------------------------------------------ small levels
+// The fold schedule (Eqs. 4-8) ends in tiny levels (down to 2x2x2x2 = 16
+// entries) that receive ~16 N contributions: global reductions to the same
+// few addresses serialise in the L2 atomic units.  Levels whose grads fit in
+// shared memory are instead accumulated per CTA in shared memory (CTA-private
+// copies) and flushed with one global reduction per entry per CTA.
+template <int F>
+__global__ void __launch_bounds__(256) bwd_small_kernel(const __grid_constant__ Params P,
+                                                        const __grid_constant__ SmallSet S,
+                                                        const float4 *__restrict__ coords, int64_t N,
+                                                        const float *__restrict__ dout, float *__restrict__ dtable,
+                                                        int *__restrict__ flag, const uint32_t *__restrict__ perm) {
+    extern __shared__ float acc[];
+    __shared__ Level slv[kMaxLevels];
+    load_levels(P, slv);
+    for (int i = threadIdx.x; i < S.total; i += blockDim.x) acc[i] = 0.f;
+    __syncthreads();
+    const int L = P.L;
+    const int64_t items = N * S.n;
+    for (int64_t gid = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; gid < items;
+         gid += (int64_t)gridDim.x * blockDim.x) {
+        const int64_t j = gid / S.n;
+        const int li = (int)(gid - j * S.n);
+        const int l = S.id[li];
+        const int64_t n = perm ? (int64_t)__ldg(perm + j) : j;
+        const Level &lv = slv[l];
+        Cell c;
+        if (cell_of(lv, __ldg(coords + n), c) && li == 0) atomicOr(flag, 1);
+        float g[F];
+#pragma unroll
+        for (int f = 0; f < F; f++) g[f] = __ldg(dout + n * (int64_t)(L * F) + l * F + f);
+        const float wx[2] = {__fsub_rn(1.0f, c.w[0]), c.w[0]}, wy[2] = {__fsub_rn(1.0f, c.w[1]), c.w[1]};
+        const float wz[2] = {__fsub_rn(1.0f, c.w[2]), c.w[2]}, wt[2] = {__fsub_rn(1.0f, c.w[3]), c.w[3]};
+        float *a = acc + S.soff[li] - (int)lv.offset * F;
+#pragma unroll
+        for (int k = 0; k < 16; k += 2) {
+            const float Wyzt = wy[(k >> 1) & 1] * wz[(k >> 2) & 1] * wt[(k >> 3) & 1];
+            const float W0 = wx[0] * Wyzt, W1 = wx[1] * Wyzt;
+#pragma unroll
+            for (int f = 0; f < F; f++) {
+                atomicAdd(a + c.idx[k] * F + f, W0 * g[f]);
+                atomicAdd(a + c.idx[k + 1] * F + f, W1 * g[f]);
+            }
+        }
+    }
+    __syncthreads();
+    // flush this CTA's partial sums
+    for (int li = 0; li < S.n; li++) {
+        const Level &lv = slv[S.id[li]];
+        const int cnt = (li + 1 < S.n ? S.soff[li + 1] : S.total) - S.soff[li];
+        float *dst = dtable + (size_t)lv.offset * F;
+        for (int i = threadIdx.x; i < cnt; i += blockDim.x) {
+            const float v = acc[S.soff[li] + i];
+            if (v != 0.f) atomicAdd(dst + i, v);
+        }
+    }
+}
+
 // ------------------------------------------------------------ indices
 __global__ void __launch_bounds__(256) indices_kernel(const __grid_constant__ Params P,
                                                       const float4 *__restrict__ coords, int64_t N,

@@ -23,4 +23,13 @@ struct Params {
     Level lv[kMaxLevels];
 };
 
+// Levels whose fp32 grads are accumulated in shared memory in the backward
+// (see bwd_small_kernel).
+struct SmallSet {
+    int n;                    // number of small levels
+    int id[kMaxLevels];       // level ids
+    int soff[kMaxLevels];     // float offset of each level's block in shared memory
+    int total;                // floats in shared memory
+};
+
 }  // namespace fh

@@ -11,6 +11,7 @@
 #include "internal.h"
 #include "encode_kernels.cuh"
 #include "sort_kernels.cuh"
+#include "mhe_kernels.cuh"
 
 namespace fh {
 thread_local char g_err[512] = "";
@@ -59,7 +60,55 @@ static fh_status ensure_flag(fh_encoder e) {
     // Measured on B200 (cfg4, 305 MiB fp16 tables / 609 MiB grads): one pass
     // 6.06 / 19.95 ms fwd / bwd; groups of <= 0.55 L2: 2.98 / 6.34 ms.
     make_groups(budget("FH_FWD_GROUP_MB", 0.55), (size_t)e->F * dtype_size(e->table_dtype), e->gf, e->n_gf);
-    make_groups(budget("FH_BWD_GROUP_MB", 0.55), (size_t)e->F * 4, e->gb, e->n_gb);
+    // Backward: levels whose fp32 grads fit a shared-memory budget are
+    // privatised per CTA (bwd_small_kernel), smallest first; the others form
+    // contiguous runs split by the L2 budget.
+    {
+        const double lim = budget("FH_BWD_GROUP_MB", 0.55);
+        const char *sv = getenv("FH_SMALL_KB");
+        const int per_level_max = 48 * 1024, total_max = sv ? atoi(sv) * 1024 : 96 * 1024;
+        bool small[FH_MAX_LEVELS] = {false};
+        int order[FH_MAX_LEVELS];
+        for (int l = 0; l < e->L; l++) order[l] = l;
+        for (int a = 0; a < e->L; a++)   // sort level ids by table size (tiny L: insertion sort)
+            for (int b = a + 1; b < e->L; b++)
+                if (e->info[order[b]].table_size < e->info[order[a]].table_size) {
+                    const int t = order[a]; order[a] = order[b]; order[b] = t;
+                }
+        int used = 0;
+        for (int a = 0; a < e->L && e->kind == 0; a++) {
+            const int l = order[a];
+            const uint64_t bytes = e->info[l].table_size * (uint64_t)e->F * 4;
+            if (bytes > (uint64_t)per_level_max || used + (int)bytes > total_max) break;
+            small[l] = true;
+            used += (int)bytes;
+        }
+        e->small.n = 0;
+        e->small.total = 0;
+        for (int l = 0; l < e->L; l++)
+            if (small[l]) {
+                e->small.id[e->small.n] = l;
+                e->small.soff[e->small.n] = e->small.total;
+                e->small.total += (int)(e->info[l].table_size * (uint64_t)e->F);
+                e->small.n++;
+            }
+        e->n_gb = 0;
+        int l = 0;
+        while (l < e->L) {
+            if (small[l]) { l++; continue; }
+            const int b = l;
+            double acc = 0.0;
+            while (l < e->L && !small[l]) {
+                const double sz = (double)e->info[l].table_size * e->F * 4.0;
+                if (lim > 0.0 && l > b && acc + sz > lim) break;
+                acc += sz;
+                l++;
+            }
+            e->gb[2 * e->n_gb] = b;
+            e->gb[2 * e->n_gb + 1] = l;
+            e->n_gb++;
+        }
+    }
     return FH_OK;
 }
 
@@ -223,7 +272,77 @@ void fh_encoder_destroy(fh_encoder e) {
     delete e;
 }
 
+fh_status fh_build_mhe(const uint32_t *res, int L, int F, fh_dtype table_dtype, uint64_t T, uint32_t n_frames,
+                       fh_encoder *out) {
+    g_err[0] = 0;
+    if (!res || !out) return fail(FH_E_ARG, "fh_build_mhe: NULL pointer");
+    *out = nullptr;
+    if (L < 1 || L > FH_MAX_LEVELS) return fail(FH_E_ARG, "fh_build_mhe: L = %d not in [1, %d]", L, FH_MAX_LEVELS);
+    if (F != 1 && F != 2 && F != 4 && F != 8) return fail(FH_E_ARG, "fh_build_mhe: F not in {1,2,4,8}");
+    if (table_dtype != FH_F32 && table_dtype != FH_F16) return fail(FH_E_ARG, "fh_build_mhe: bad table dtype");
+    if (T < 2 || (T & (T - 1)) || T > (1ull << 31)) return fail(FH_E_ARG, "fh_build_mhe: T must be a power of two");
+    if (n_frames < 1 || n_frames > (1u << 20)) return fail(FH_E_ARG, "fh_build_mhe: bad n_frames");
+    fh_encoder e = new (std::nothrow) fh_encoder_s();
+    if (!e) return fail(FH_E_ARG, "fh_build_mhe: out of host memory");
+    e->kind = 1;
+    e->L = L;
+    e->F = F;
+    e->table_dtype = table_dtype;
+    e->cap = T;
+    e->params.L = L;
+    e->params.F = F;
+    uint64_t off = 0;
+    for (int l = 0; l < L; l++) {
+        const uint32_t R = res[l];
+        if (R < 2 || R > (1u << 20)) { delete e; return fail(FH_E_ARG, "fh_build_mhe: level %d R = %u", l, R); }
+        const uint64_t cube = (uint64_t)R * R * R;
+        fh_level_info &I = e->info[l];
+        I.res[0] = I.res[1] = I.res[2] = R;
+        I.res[3] = n_frames;
+        I.corners = cube * n_frames;
+        I.hashed = cube > T ? 1u : 0u;
+        I.table_size = T * n_frames;   // fixed T per level and frame (bucket waste when cube < T)
+        I.reserved = 0;
+        I.offset = off;
+        off += I.table_size;
+        if (off * (uint64_t)F >= (1ull << 32)) { delete e; return fail(FH_E_RANGE, "fh_build_mhe: too many parameters"); }
+        fh::Level &K = e->params.lv[l];
+        memset(&K, 0, sizeof(K));
+        for (int a = 0; a < 3; a++) { K.res[a] = R; K.scale[a] = (float)(R - 1); }
+        K.res[3] = n_frames;
+        K.scale[3] = (float)(n_frames > 1 ? n_frames - 1 : 0);
+        K.sy = R;
+        K.sz = I.hashed ? 0u : R * R;
+        K.st = (uint32_t)T;
+        K.hashed = I.hashed;
+        K.mask = (uint32_t)(T - 1);
+        K.offset = (uint32_t)I.offset;
+    }
+    e->entries = off;
+    *out = e;
+    return FH_OK;
+}
+
+int fh_encoder_kind(fh_encoder e) { return e ? e->kind : -1; }
+
 }  // extern "C"
+
+template <typename T, typename O>
+static void dispatch_mhe_fwd(fh_encoder e, const float *coords, int64_t N, const void *table, void *out,
+                             cudaStream_t s) {
+    for (int g = 0; g < e->n_gf; g++) {
+        const int l0 = e->gf[g], lc = e->gf[g + 1] - e->gf[g];
+        const float4 *c4 = reinterpret_cast<const float4 *>(coords);
+        const T *tb = reinterpret_cast<const T *>(table);
+        O *o = reinterpret_cast<O *>(out);
+        switch (e->F) {
+            case 1: fh::mhe::fwd_kernel<1, T, O><<<grid_for(N, lc), 256, 0, s>>>(e->params, c4, N, tb, o, e->flag, l0, lc); break;
+            case 2: fh::mhe::fwd_kernel<2, T, O><<<grid_for(N, lc), 256, 0, s>>>(e->params, c4, N, tb, o, e->flag, l0, lc); break;
+            case 4: fh::mhe::fwd_kernel<4, T, O><<<grid_for(N, lc), 256, 0, s>>>(e->params, c4, N, tb, o, e->flag, l0, lc); break;
+            default: fh::mhe::fwd_kernel<8, T, O><<<grid_for(N, lc), 256, 0, s>>>(e->params, c4, N, tb, o, e->flag, l0, lc); break;
+        }
+    }
+}
 
 static fh_status encode_fwd_impl(fh_encoder e, const float *coords, int64_t N, const uint32_t *perm,
                                  const void *table, void *out, fh_dtype out_dtype, fh_stream stream) {
@@ -238,6 +357,17 @@ static fh_status encode_fwd_impl(fh_encoder e, const float *coords, int64_t N, c
     if (!out || !aligned(out, ovec > 16 ? 16 : ovec)) return fail(FH_E_ARG, "fh_encode_fwd: NULL/misaligned out");
     if ((st = ensure_flag(e)) != FH_OK) return st;
     cudaStream_t s = reinterpret_cast<cudaStream_t>(stream);
+    if (e->kind == 1) {
+        if (perm) return fail(FH_E_ARG, "fh_encode_fwd_ordered: not supported for MHE encoders");
+        if (e->table_dtype == FH_F32) {
+            if (out_dtype == FH_F32) dispatch_mhe_fwd<float, float>(e, coords, N, table, out, s);
+            else dispatch_mhe_fwd<float, __nv_bfloat16>(e, coords, N, table, out, s);
+        } else {
+            if (out_dtype == FH_F32) dispatch_mhe_fwd<__half, float>(e, coords, N, table, out, s);
+            else dispatch_mhe_fwd<__half, __nv_bfloat16>(e, coords, N, table, out, s);
+        }
+        return cuda_check(cudaGetLastError(), "fh_encode_fwd (MHE) launch");
+    }
     if (e->table_dtype == FH_F32) {
         if (out_dtype == FH_F32) dispatch_fwd_F<float, float>(e, coords, N, table, out, s, perm);
         else dispatch_fwd_F<float, __nv_bfloat16>(e, coords, N, table, out, s, perm);
@@ -260,9 +390,39 @@ static fh_status encode_bwd_impl(fh_encoder e, const float *coords, int64_t N, c
     if ((st = ensure_flag(e)) != FH_OK) return st;
     cudaStream_t s = reinterpret_cast<cudaStream_t>(stream);
     const float4 *c4 = reinterpret_cast<const float4 *>(coords);
+    if (e->kind == 1 && perm) return fail(FH_E_ARG, "fh_encode_bwd_ordered: not supported for MHE encoders");
+    if (e->small.n > 0) {
+        const int smem = e->small.total * 4;
+        int64_t blocks = (N * e->small.n + 255) / 256;
+        if (blocks > 2 * 148) blocks = 2 * 148;
+        const dim3 g((unsigned)blocks);
+        fh_status q = FH_OK;
+        switch (e->F) {
+#define FH_SMALL(FF)                                                                                          \
+    q = cuda_check(cudaFuncSetAttribute(fh::bwd_small_kernel<FF>, cudaFuncAttributeMaxDynamicSharedMemorySize, \
+                                        smem), "cudaFuncSetAttribute(bwd_small)");                           \
+    if (q != FH_OK) return q;                                                                                 \
+    fh::bwd_small_kernel<FF><<<g, 256, smem, s>>>(e->params, e->small, c4, N, dout, dtable, e->flag, perm);   \
+    break;
+            case 1: FH_SMALL(1)
+            case 2: FH_SMALL(2)
+            case 4: FH_SMALL(4)
+            default: FH_SMALL(8)
+#undef FH_SMALL
+        }
+    }
     for (int k = 0; k < e->n_gb; k++) {
-        const int l0 = e->gb[k], lc = e->gb[k + 1] - e->gb[k];
+        const int l0 = e->gb[2 * k], lc = e->gb[2 * k + 1] - e->gb[2 * k];
         const dim3 g = grid_for(N, lc);
+        if (e->kind == 1) {
+            switch (e->F) {
+                case 1: fh::mhe::bwd_kernel<1><<<g, 256, 0, s>>>(e->params, c4, N, dout, dtable, e->flag, l0, lc); break;
+                case 2: fh::mhe::bwd_kernel<2><<<g, 256, 0, s>>>(e->params, c4, N, dout, dtable, e->flag, l0, lc); break;
+                case 4: fh::mhe::bwd_kernel<4><<<g, 256, 0, s>>>(e->params, c4, N, dout, dtable, e->flag, l0, lc); break;
+                default: fh::mhe::bwd_kernel<8><<<g, 256, 0, s>>>(e->params, c4, N, dout, dtable, e->flag, l0, lc); break;
+            }
+            continue;
+        }
         switch (e->F) {
             case 1: fh::bwd_kernel<1><<<g, 256, 0, s>>>(e->params, c4, N, dout, dtable, e->flag, l0, lc, perm); break;
             case 2: fh::bwd_kernel<2><<<g, 256, 0, s>>>(e->params, c4, N, dout, dtable, e->flag, l0, lc, perm); break;
@@ -331,8 +491,12 @@ fh_status fh_encode_indices(fh_encoder e, const float *coords, int64_t N, uint32
     if (!idx || !aligned(idx, 16) || !aligned(w, 16)) return fail(FH_E_ARG, "fh_encode_indices: NULL/misaligned output");
     if ((st = ensure_flag(e)) != FH_OK) return st;
     cudaStream_t s = reinterpret_cast<cudaStream_t>(stream);
-    fh::indices_kernel<<<grid_for(N, e->L), 256, 0, s>>>(e->params, reinterpret_cast<const float4 *>(coords), N,
-                                                         idx, w, e->flag);
+    if (e->kind == 1)
+        fh::mhe::indices_kernel<<<grid_for(N, e->L), 256, 0, s>>>(
+            e->params, reinterpret_cast<const float4 *>(coords), N, idx, w, e->flag);
+    else
+        fh::indices_kernel<<<grid_for(N, e->L), 256, 0, s>>>(e->params, reinterpret_cast<const float4 *>(coords),
+                                                             N, idx, w, e->flag);
     return cuda_check(cudaGetLastError(), "fh_encode_indices launch");
 }
 

@@ -33,6 +33,7 @@ inline size_t dtype_size(fh_dtype d) { return d == FH_F32 ? 4 : 2; }
 }  // namespace fh
 
 struct fh_encoder_s {
+    int kind = 0;  // 0: F-Hash Tesseract encoder; 1: MHE baseline (NEXT-3)
     int L = 0, F = 0;
     fh_dtype table_dtype = FH_F32;
     uint64_t cap = 0;
@@ -45,5 +46,6 @@ struct fh_encoder_s {
     // fp32 grad (bwd) footprint fits an L2 budget run as one pass, so the
     // gathered / reduced region stays L2-resident.  g[i]..g[i+1] = group i.
     int n_gf = 0, gf[FH_MAX_LEVELS + 1] = {0};
-    int n_gb = 0, gb[FH_MAX_LEVELS + 1] = {0};
+    int n_gb = 0, gb[2 * FH_MAX_LEVELS + 2] = {0};  // bwd: pairs (begin, end) of non-small runs
+    fh::SmallSet small{};                            // bwd: levels privatised in shared memory
 };

@@ -28,7 +28,7 @@ EXPORTS = [
     "fh_table_entries", "fh_param_count", "fh_encoder_destroy", "fh_encode_fwd", "fh_encode_bwd",
     "fh_encode_indices", "fh_zero_grad", "fh_encode_fwd_bwd", "fh_encode_step_host", "fh_status_sync", "fh_last_error",
     "fh_version", "fh_spatial_sort_workspace_size", "fh_spatial_sort", "fh_encode_fwd_ordered",
-    "fh_encode_bwd_ordered",
+    "fh_encode_bwd_ordered", "fh_build_mhe", "fh_encoder_kind",
     # include/fhash_bench.h (measurement kernels)
     "fh_bench_gather", "fh_bench_red", "fh_bench_copy",
     # train step
@@ -85,6 +85,10 @@ def lib() -> ctypes.CDLL:
     L.fh_encode_indices.argtypes = [vp, vp, i64, vp, vp, vp]
     L.fh_encode_fwd_bwd.argtypes = [vp, vp, i64, vp, vp, c_int, vp, vp, c_int, vp]
     L.fh_zero_grad.argtypes = [vp, vp, vp]
+    L.fh_build_mhe.argtypes = [ctypes.POINTER(ctypes.c_uint32), c_int, c_int, c_int, u64, ctypes.c_uint32,
+                               ctypes.POINTER(vp)]
+    L.fh_build_mhe.restype = c_int
+    L.fh_encoder_kind.argtypes = [vp]
     L.fh_spatial_sort_workspace_size.argtypes = [i64]
     L.fh_spatial_sort_workspace_size.restype = ctypes.c_size_t
     L.fh_spatial_sort.argtypes = [vp, i64, vp, vp, ctypes.c_size_t, vp]
@@ -479,6 +483,31 @@ def sample_voxels(field, N: int, seed: int, subsequence: int, offset: int, coord
     _check(_data_lib().fh_data_sample_voxels(field.data_ptr(), Sx, Sy, Sz, T, N, seed, subsequence, offset,
                                              coords.data_ptr(), target.data_ptr(), _stream(stream)))
     return coords, target
+
+
+class MHEEncoder(Encoder):
+    """NEXT-3: the MHE baseline encoder (fh_build_mhe) behind the same
+    fwd / bwd / indices calls.  res: vertices per spatial axis per level."""
+
+    def __init__(self, res: Sequence[int], F: int, T: int, n_frames: int, table_dtype: str = "f32"):
+        L = len(res)
+        arr = (ctypes.c_uint32 * max(L, 1))(*[int(r) for r in res])
+        h = ctypes.c_void_p()
+        _check(lib().fh_build_mhe(arr, L, F, _DT[table_dtype], T, n_frames, ctypes.byref(h)))
+        self._h = h
+        self.levels = [(int(r), int(r), int(r), int(n_frames)) for r in res]
+        self.L, self.F, self.cap, self.table_dtype = L, F, T, table_dtype
+        self.T, self.n_frames = T, n_frames
+        self.entries = int(lib().fh_table_entries(h))
+        self.param_count = int(lib().fh_param_count(h))
+
+    def indices(self, coords, want_w: bool = True, stream=None):
+        import torch
+        N = coords.shape[0]
+        idx = torch.empty((N, self.L, 8), dtype=torch.int32, device=coords.device)
+        w = torch.empty((N, self.L, 8), dtype=torch.float32, device=coords.device) if want_w else None
+        _check(lib().fh_encode_indices(self._h, _ptr(coords), N, _ptr(idx), _ptr(w), _stream(stream)))
+        return idx, w
 
 
 class SpatialOrder:
