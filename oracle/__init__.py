@@ -55,6 +55,8 @@ def lib():
         L.fho_build_levels.restype = ctypes.c_uint64
         L.fho_fhash.argtypes = [u32p] + [ctypes.c_uint64] * 4
         L.fho_fhash.restype = ctypes.c_uint64
+        L.fho_brick_index.argtypes = [u32p] + [ctypes.c_uint64] * 4
+        L.fho_brick_index.restype = ctypes.c_uint64
         L.fho_spatial_hash.argtypes = [ctypes.c_uint32] * 4 + [ctypes.c_uint64]
         L.fho_spatial_hash.restype = ctypes.c_uint64
         common = [u32p, i32p, u64p, u64p, ctypes.c_int]
@@ -101,7 +103,9 @@ def fold_schedule(S_xyz: Sequence[int], n_t: int, fold: int, max_L: int = 64):
 class Levels:
     """Oracle level table (a1).  res: [L][4] (x,y,z,t) vertex counts."""
 
-    def __init__(self, res: Sequence[Sequence[int]], cap: int = 0):
+    def __init__(self, res: Sequence[Sequence[int]], cap: int = 0, lin: int = 0):
+        """lin: 0 = Eq. 9 row-major; 1 = brick (tiled Z-order) order
+        of the bijective levels (NEXT-2, reading R21)."""
         self.res = _c(res, np.uint32).reshape(-1, 4)
         self.L = self.res.shape[0]
         self.cap = int(cap)
@@ -115,6 +119,8 @@ class Levels:
         if tot == 0:
             raise ValueError("build_levels: bad arguments")
         self.total = int(tot)
+        if lin == 1:   # mode code 2 in the C oracle = brick order on bijective levels
+            self.hashed[self.hashed == 0] = 2
 
     def param_count(self, F: int) -> int:
         return self.total * F
@@ -232,6 +238,12 @@ def fhash(res4: Sequence[int], x: int, y: int, z: int, t: int) -> int:
     """Eq. 9 for one corner; res4 = (Rx, Ry, Rz, Rt)."""
     r = _c(res4, np.uint32)
     return int(lib().fho_fhash(_p(r, ctypes.c_uint32), x, y, z, t))
+
+
+def brick_index(res4: Sequence[int], x: int, y: int, z: int, t: int) -> int:
+    """NEXT-2 brick (tiled Z-order) linearization of one vertex (R21)."""
+    r = _c(res4, np.uint32)
+    return int(lib().fho_brick_index(_p(r, ctypes.c_uint32), x, y, z, t))
 
 
 def spatial_hash(X: int, Y: int, Z: int, T: int, tsize: int) -> int:

@@ -106,6 +106,35 @@ uint64_t fho_fhash(const uint32_t r[4], uint64_t x, uint64_t y, uint64_t z, uint
     return t * Rx * Ry * Rz + z * Rx * Ry + y * Rx + x;
 }
 
+/* NEXT-2: a locality-preserving bijective linearization ("Other
+ * linearizations like Morton and Z-order can also be used to construct F-Hash
+ * with preserved locality"): tiled (one-level Z-order) order -- the
+ * grid is cut into bricks of 2 x 2 x 2 x 2 vertices (clipped at the grid
+ * edge), bricks are enumerated in row-major (x fastest) order and vertices
+ * in row-major order inside a brick (reading R21):
+ *   b_a = v_a / B_a, i_a = v_a % B_a, e_a = min(B_a, R_a - b_a B_a)
+ *   idx = b_t B_t Rz Ry Rx + b_z B_z Ry Rx e_t + b_y B_y Rx e_z e_t
+ *       + b_x B_x e_y e_z e_t + ((i_t e_z + i_z) e_y + i_y) e_x + i_x
+ * Bijective onto [0, Rx Ry Rz Rt) (brute-force pinned in the tests). */
+static const uint64_t kBrick[4] = { 2, 2, 2, 2 };
+
+uint64_t fho_brick_index(const uint32_t r[4], uint64_t x, uint64_t y, uint64_t z, uint64_t t)
+{
+    uint64_t v[4] = { x, y, z, t }, b[4], i[4], e[4];
+    for (int a = 0; a < 4; a++) {
+        b[a] = v[a] / kBrick[a];
+        i[a] = v[a] % kBrick[a];
+        uint64_t rem = (uint64_t)r[a] - b[a] * kBrick[a];
+        e[a] = rem < kBrick[a] ? rem : kBrick[a];
+    }
+    uint64_t Rx = r[0], Ry = r[1], Rz = r[2];
+    return b[3] * kBrick[3] * Rz * Ry * Rx
+         + b[2] * kBrick[2] * Ry * Rx * e[3]
+         + b[1] * kBrick[1] * Rx * e[2] * e[3]
+         + b[0] * kBrick[0] * e[1] * e[2] * e[3]
+         + ((i[3] * e[2] + i[2]) * e[1] + i[1]) * e[0] + i[0];
+}
+
 /* Capped levels (R5; the paper never caps).  MHE spatial hash
  * (Teschner et al., cited at P:174) extended to 4D:
  *   (X*1 xor Y*2654435761 xor Z*805459861 xor T*2246822519) mod 2^32 mod T_l
@@ -154,8 +183,10 @@ static int corners_one(const float *p /*x,y,z,t*/, const uint32_t r[4], int hash
         uint32_t b[4] = { (uint32_t)(c & 1), (uint32_t)((c >> 1) & 1),
                           (uint32_t)((c >> 2) & 1), (uint32_t)((c >> 3) & 1) };
         uint32_t X = i[0] + b[0], Y = i[1] + b[1], Z = i[2] + b[2], T = i[3] + b[3];
-        uint64_t local = hashed ? fho_spatial_hash(X, Y, Z, T, tsize)
-                                : fho_fhash(r, X, Y, Z, T);
+        /* hashed: 0 = Eq. 9, 1 = capped hash (R5), 2 = brick order (NEXT-2, R21) */
+        uint64_t local = hashed == 1 ? fho_spatial_hash(X, Y, Z, T, tsize)
+                       : hashed == 2 ? fho_brick_index(r, X, Y, Z, T)
+                                     : fho_fhash(r, X, Y, Z, T);
         idx[c] = offset + local;
         double Wc = 1.0;
         for (int a = 0; a < 4; a++) Wc *= b[a] ? (double)w[a] : 1.0 - (double)w[a];
@@ -386,7 +417,8 @@ int fho_level_stats(const uint32_t r[4], int hashed, uint64_t tsize, uint64_t ma
         for (uint32_t z = 0; z < r[2]; z++)
             for (uint32_t y = 0; y < r[1]; y++)
                 for (uint32_t x = 0; x < r[0]; x++) {
-                    uint64_t b = hashed ? fho_spatial_hash(x, y, z, t, tsize) : fho_fhash(r, x, y, z, t);
+                    uint64_t b = hashed == 1 ? fho_spatial_hash(x, y, z, t, tsize)
+                               : hashed == 2 ? fho_brick_index(r, x, y, z, t) : fho_fhash(r, x, y, z, t);
                     if (b >= tsize) { out_of_range++; continue; }
                     if (!hit[b]) { hit[b] = 1; d++; }
                 }

@@ -117,6 +117,41 @@ def test_bijectivity_random_fold_schedules():
             assert col == 0 and util == 1.0
 
 
+def test_brick_linearization_bijective_and_local():
+    """NEXT-2 (P:174 'Morton and Z-order ... with preserved locality'):
+    the brick order is a bijection onto [0, C) on every cfg1 level and on
+    ragged shapes (brute force), equals Eq. 9 when every axis fits one brick,
+    and keeps the 16 corners of a cell closer than Eq. 9 does."""
+    for r in [(4, 8, 12, 2), (8, 8, 8, 3), (12, 12, 12, 4), (16, 16, 16, 5), (5, 7, 9, 3), (2, 2, 2, 2),
+              (13, 3, 6, 7), (17, 1 + 1, 11, 5)]:
+        got = sorted(oracle.brick_index(r, x, y, z, t) for t in range(r[3]) for z in range(r[2])
+                     for y in range(r[1]) for x in range(r[0]))
+        assert got == list(range(r[0] * r[1] * r[2] * r[3])), r
+        lv = oracle.Levels([r], lin=1)
+        d, col, util = lv.level_stats(0)
+        assert col == 0 and util == 1.0
+    r = (2, 2, 2, 2)   # one brick: identical to Eq. 9
+    for t in range(2):
+        for z in range(2):
+            for y in range(2):
+                for x in range(2):
+                    assert oracle.brick_index(r, x, y, z, t) == oracle.fhash(r, x, y, z, t)
+    # the brick of a cell at even coordinates holds exactly its 16 corners, in
+    # Morton (Z-order) bit order x, y, z, t of the lowest bit
+    r = (6, 4, 4, 4)
+    base = oracle.brick_index(r, 2, 2, 2, 2)
+    assert [oracle.brick_index(r, 2 + (c & 1), 2 + (c >> 1 & 1), 2 + (c >> 2 & 1), 2 + (c >> 3 & 1)) - base
+            for c in range(16)] == list(range(16))
+    r = (64, 64, 64, 8)
+    lines = []
+    for lin in (0, 1):
+        lv = oracle.Levels([r], lin=lin)
+        idx, _, _ = lv.indices(W.draw_coords(W.rng(3), 2000), want_w=False)
+        # distinct 128-byte lines (16 entries of 8 B) touched by a cell's 16 corners
+        lines.append(np.mean([len(set((row // 16).tolist())) for row in idx[:, 0, :]]))
+    assert lines[1] < 0.65 * lines[0], lines
+
+
 def test_capped_levels_hash_stats():
     """R5 capped levels: T_l = cap, every bucket index < T_l, pigeonhole
     collisions and utilisation < 1 possible; the bijective levels
