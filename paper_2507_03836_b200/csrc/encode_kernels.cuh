@@ -353,23 +353,26 @@ template <int F, typename T, typename O>
 __global__ void __launch_bounds__(256, FH_FWD_MINB) fwd_kernel(const __grid_constant__ Params P,
                                                   const float4 *__restrict__ coords, int64_t N,
                                                   const T *__restrict__ table, uint32_t full_blocks,
-                                                  O *__restrict__ out, int *__restrict__ flag, int l0, int lc,
+                                                  O *__restrict__ out, int *__restrict__ flag,
+                                                  const __grid_constant__ LevelList LL,
                                                   const uint32_t *__restrict__ perm) {
-    // levels [l0, l0 + lc) of every sample (a level group: see DESIGN.md §8);
+    // the levels LL.id[0..LL.n) of every sample (a level group: see DESIGN.md §8);
     // perm (optional): process samples in this (spatially sorted) order
     __shared__ Level slv[kMaxLevels];
     load_levels(P, slv);
     const int L = P.L;
+    const int lc = LL.n;
     const int64_t gid = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
     const int64_t j = gid / lc;
     if (j >= N) return;
-    const int l = l0 + (int)(gid - j * lc);
+    const int li = (int)(gid - j * lc);
+    const int l = LL.id[li];
     const int64_t n = perm ? (int64_t)__ldg(perm + j) : j;
     const Level &lv = slv[l];
     const float4 p = __ldg(coords + n);
     Cell c;
     const bool bad = cell_of(lv, p, c);
-    if (bad && l == l0) atomicOr(flag, 1);
+    if (bad && li == 0) atomicOr(flag, 1);
     float e[16][F];
     gather16<T, F>(table, full_blocks, c.idx, e);
     float v[F];
@@ -439,21 +442,23 @@ template <int F>
 __global__ void __launch_bounds__(256) bwd_kernel(const __grid_constant__ Params P,
                                                   const float4 *__restrict__ coords, int64_t N,
                                                   const float *__restrict__ dout, float *__restrict__ dtable,
-                                                  int *__restrict__ flag, int l0, int lc,
+                                                  int *__restrict__ flag, const __grid_constant__ LevelList LL,
                                                   const uint32_t *__restrict__ perm) {
     __shared__ Level slv[kMaxLevels];
     load_levels(P, slv);
     const int L = P.L;
+    const int lc = LL.n;
     const int64_t gid = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
     const int64_t j = gid / lc;
     if (j >= N) return;
-    const int l = l0 + (int)(gid - j * lc);
+    const int li = (int)(gid - j * lc);
+    const int l = LL.id[li];
     const int64_t n = perm ? (int64_t)__ldg(perm + j) : j;
     const Level &lv = slv[l];
     const float4 p = __ldg(coords + n);
     Cell c;
     const bool bad = cell_of(lv, p, c);
-    if (bad && l == l0) atomicOr(flag, 1);
+    if (bad && li == 0) atomicOr(flag, 1);
     float g[F];
     const float *gp = dout + n * (int64_t)(L * F) + l * F;
 #pragma unroll

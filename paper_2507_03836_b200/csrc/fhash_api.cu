@@ -5,12 +5,14 @@
 #include <cstdarg>
 #include <cstdio>
 #include <cstdlib>
+#include <cmath>
 #include <cstring>
 #include <new>
 
 #include "internal.h"
 #include "encode_kernels.cuh"
 #include "sort_kernels.cuh"
+#include "tiled_kernels.cuh"
 #include "mhe_kernels.cuh"
 
 namespace fh {
@@ -38,6 +40,8 @@ static fh_status ensure_flag(fh_encoder e) {
     // Level groups from the device's L2 size.
     int l2 = 0;
     cudaDeviceGetAttribute(&l2, cudaDevAttrL2CacheSize, dev);
+    cudaDeviceGetAttribute(&e->n_sm, cudaDevAttrMultiProcessorCount, dev);
+    cudaDeviceGetAttribute(&e->smem_optin, cudaDevAttrMaxSharedMemoryPerBlockOptin, dev);
     auto budget = [&](const char *env, double frac) -> double {
         const char *v = getenv(env);
         if (v) return atof(v) * 1048576.0;  // MiB; 0 = one group
@@ -59,7 +63,9 @@ static fh_status ensure_flag(fh_encoder e) {
     };
     // Measured on B200 (cfg4, 305 MiB fp16 tables / 609 MiB grads): one pass
     // 6.06 / 19.95 ms fwd / bwd; groups of <= 0.55 L2: 2.98 / 6.34 ms.
-    make_groups(budget("FH_FWD_GROUP_MB", 0.55), (size_t)e->F * dtype_size(e->table_dtype), e->gf, e->n_gf);
+    e->fwd_limit = budget("FH_FWD_GROUP_MB", 0.55);
+    e->bwd_limit = budget("FH_BWD_GROUP_MB", 0.55);
+    make_groups(e->fwd_limit, (size_t)e->F * dtype_size(e->table_dtype), e->gf, e->n_gf);
     // Backward: levels whose fp32 grads fit a shared-memory budget are
     // privatised per CTA (bwd_small_kernel), smallest first; the others form
     // contiguous runs split by the L2 budget.
@@ -118,16 +124,103 @@ static dim3 grid_for(int64_t N, int L) {
     return dim3((unsigned)((threads + 255) / 256));
 }
 
+// Split the levels with include[l] into direct-pass lists whose footprint
+// (T_l * bytes_per_entry) fits `limit` bytes (0 = one list), in level order.
+static int split_lists(fh_encoder e, const bool *include, double bytes_per_entry, double limit, fh::LevelList *out) {
+    int n = 0;
+    double acc = 0.0;
+    for (int l = 0; l < e->L; l++) {
+        if (!include[l]) continue;
+        const double b = (double)e->info[l].table_size * bytes_per_entry;
+        if (n == 0 || (limit > 0.0 && out[n - 1].n > 0 && acc + b > limit)) {
+            out[n].n = 0;
+            n++;
+            acc = 0.0;
+        }
+        out[n - 1].id[out[n - 1].n++] = l;
+        acc += b;
+    }
+    return n;
+}
+
+// ---------------------------------------------------------------- tiling
+// Tile plan of an ordered (spatially sorted) pass: samples per tile and the
+// levels whose per-tile vertex box is expected to fit box_bytes at
+// bytes_per_vertex (tiled_kernels.cuh).  The estimate follows the Morton key:
+// a tile of S of N sorted samples spans about S/N of the 2^16 key bins, i.e.
+// the lowest log2(2^16 S/N) key bits; counting those bits per axis gives its
+// extent in bins, hence in cells of level l.  A margin (default 1.5) covers
+// tiles that straddle two key blocks.  The kernel re-checks every (tile,
+// level) box and falls back to the direct global path when one does not fit.
+static void plan_tiles(fh_encoder e, int64_t N, double max_vertices, double per_sample, int box_bytes,
+                       fh::tiled::TileSet &ts, bool *tiled) {
+    using namespace fh::tiled;
+    const int64_t per_wave = (int64_t)e->n_sm * kMaxTile;
+    const int64_t waves = (N + per_wave - 1) / per_wave;
+    int64_t S = (N + (int64_t)e->n_sm * waves - 1) / ((int64_t)e->n_sm * waves);
+    if (S < 256) S = 256;
+    if (S > kMaxTile) S = kMaxTile;
+    const char *sv = getenv("FH_TILE_S");
+    if (sv && atoi(sv) > 0 && atoi(sv) <= kMaxTile) S = atoi(sv);
+    ts.S = (int)S;
+    ts.box_bytes = box_bytes;
+    ts.n = 0;
+    double kbits = 16.0 + std::log2((double)S / (double)(N > 0 ? N : 1));
+    if (kbits > 16.0) kbits = 16.0;
+    if (kbits < 0.0) kbits = 0.0;
+    int low[4] = {0, 0, 0, 0};
+    const int kb = (int)std::ceil(kbits);
+    for (int k = 0; k < kb && k < 16; k++) low[e->key.axis[k]]++;
+    const char *mv = getenv("FH_TILE_MARGIN");
+    const double margin = mv ? atof(mv) : 1.25;
+    // staged boxes pay off up to per_sample vertices per sample (the kernels
+    // allow a larger bound for tiles that straddle key blocks)
+    const double cap = std::min(max_vertices, per_sample * (double)S);
+    for (int l = 0; l < e->L; l++) {
+        double V = 1.0;
+        for (int a = 0; a < 4; a++) {
+            const double frac = std::ldexp(1.0, low[a] - (int)e->key.bits[a]);
+            const double cells = (double)(e->info[l].res[a] - 1) * (frac < 1.0 ? frac : 1.0);
+            double verts = std::ceil(cells) + 2.0;
+            if (verts > e->info[l].res[a]) verts = e->info[l].res[a];
+            V *= verts;
+        }
+        tiled[l] = V * margin <= cap;
+        if (tiled[l]) ts.id[ts.n++] = l;
+    }
+}
+
 template <int F, typename T, typename O>
 static void launch_fwd(fh_encoder e, const float *coords, int64_t N, const void *table, void *out,
                        cudaStream_t s, const uint32_t *perm) {
     const uint32_t full_blocks = (uint32_t)((e->entries * (uint64_t)F * sizeof(T)) / 32);
-    for (int g = 0; g < e->n_gf; g++) {
-        const int l0 = e->gf[g], lc = e->gf[g + 1] - e->gf[g];
-        fh::fwd_kernel<F, T, O><<<grid_for(N, lc), 256, 0, s>>>(
-            e->params, reinterpret_cast<const float4 *>(coords), N, reinterpret_cast<const T *>(table),
-            full_blocks, reinterpret_cast<O *>(out), e->flag, l0, lc, perm);
+    const float4 *c4 = reinterpret_cast<const float4 *>(coords);
+    bool include[FH_MAX_LEVELS];
+    for (int l = 0; l < e->L; l++) include[l] = true;
+    const uint32_t *dperm = perm;
+    if (perm) {
+        // ordered pass: coarse / mid levels tiled through shared memory
+        fh::tiled::TileSet ts;
+        const int box_bytes = e->smem_optin - 4096;
+        plan_tiles(e, N, (double)box_bytes / 2.0 / (F * sizeof(T)), 4.0, box_bytes, ts, include);  // two box buffers
+        for (int l = 0; l < e->L; l++) include[l] = !include[l];
+        if (ts.n > 0) {
+            cudaFuncSetAttribute(fh::tiled::fwd_tiled_kernel<F, T, O>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                 box_bytes);
+            const unsigned grid = (unsigned)((N + ts.S - 1) / ts.S);
+            fh::tiled::fwd_tiled_kernel<F, T, O><<<grid, fh::tiled::kThreads, box_bytes, s>>>(
+                e->params, ts, c4, N, perm, reinterpret_cast<const T *>(table), full_blocks,
+                reinterpret_cast<O *>(out), e->flag);
+        }
+        const char *fo = getenv("FH_FINE_ORDER");
+        if (!(fo && atoi(fo) == 1)) dperm = nullptr;  // direct levels: natural order (coalesced rows)
     }
+    fh::LevelList lists[FH_MAX_LEVELS];
+    const int n = split_lists(e, include, (double)F * sizeof(T), e->fwd_limit, lists);
+    for (int g = 0; g < n; g++)
+        fh::fwd_kernel<F, T, O><<<grid_for(N, lists[g].n), 256, 0, s>>>(
+            e->params, c4, N, reinterpret_cast<const T *>(table), full_blocks, reinterpret_cast<O *>(out), e->flag,
+            lists[g], dperm);
 }
 
 template <typename T, typename O>
@@ -141,6 +234,51 @@ static void dispatch_fwd_F(fh_encoder e, const float *coords, int64_t N, const v
     }
 }
 
+template <int F>
+static void launch_bwd_direct(fh_encoder e, const float4 *c4, int64_t N, const float *dout, float *dtable,
+                              cudaStream_t s, const uint32_t *perm, const bool *include) {
+    fh::LevelList lists[FH_MAX_LEVELS];
+    const int n = split_lists(e, include, (double)F * 4.0, e->bwd_limit, lists);
+    for (int g = 0; g < n; g++)
+        fh::bwd_kernel<F><<<grid_for(N, lists[g].n), 256, 0, s>>>(e->params, c4, N, dout, dtable, e->flag, lists[g],
+                                                                   perm);
+}
+
+// Ordered backward: levels where a sorted warp's samples nearly always share
+// a cell -- expected samples per cell >= FH_AGG_MIN_DENSITY, default 128 F --
+// run the warp-aggregated kernel in `order`; the others run the direct
+// kernel in natural order (FH_FINE_ORDER=1: in `order`).  Measured on B200
+// (tools/time_levels.py): aggregation wins only on the most contended
+// levels (cfg2 level 0: 163 -> 76 us, cfg4 level 0: 697 -> 496 us); at
+// lower densities its extra instructions cost more than the reductions it
+// saves.
+template <int F>
+static void launch_bwd_ordered(fh_encoder e, const float4 *c4, int64_t N, const float *dout, float *dtable,
+                               cudaStream_t s, const uint32_t *perm) {
+    const char *dv = getenv("FH_AGG_MIN_DENSITY");
+    const double dmin = dv ? atof(dv) : 128.0 * F;
+    bool agg[FH_MAX_LEVELS], rest[FH_MAX_LEVELS];
+    for (int l = 0; l < e->L; l++) {
+        double cells = 1.0;
+        for (int a = 0; a < 4; a++) cells *= (double)(e->info[l].res[a] - 1);
+        agg[l] = (double)N / cells >= dmin;
+        rest[l] = !agg[l];
+    }
+    fh::LevelList lists[FH_MAX_LEVELS];
+    const int n = split_lists(e, agg, (double)F * 4.0, e->bwd_limit, lists);
+    const int smem = fh::tiled::kAggWarps * fh::tiled::AggLayout<F>::kWarpFloats * 4;
+    if (n > 0 && smem > 48 * 1024)
+        cudaFuncSetAttribute(fh::tiled::bwd_agg_kernel<F>, cudaFuncAttributeMaxDynamicSharedMemorySize, smem);
+    for (int g = 0; g < n; g++) {
+        const int64_t warps = (N + 31) / 32 * lists[g].n;
+        const unsigned grid = (unsigned)((warps + fh::tiled::kAggWarps - 1) / fh::tiled::kAggWarps);
+        fh::tiled::bwd_agg_kernel<F><<<grid, fh::tiled::kAggThreads, smem, s>>>(e->params, lists[g], c4, N, perm, dout,
+                                                                           dtable, e->flag);
+    }
+    const char *fo = getenv("FH_FINE_ORDER");
+    launch_bwd_direct<F>(e, c4, N, dout, dtable, s, (fo && atoi(fo) == 1) ? perm : nullptr, rest);
+}
+
 static fh_status check_common(fh_encoder e, const float *coords, int64_t N, const char *who) {
     if (!e) return fail(FH_E_ARG, "%s: NULL encoder", who);
     if (N < 0) return fail(FH_E_ARG, "%s: N = %lld < 0", who, (long long)N);
@@ -148,6 +286,39 @@ static fh_status check_common(fh_encoder e, const float *coords, int64_t N, cons
     if (!aligned(coords, 16)) return fail(FH_E_ARG, "%s: coords not 16-byte aligned", who);
     if (N > (int64_t)1 << 40) return fail(FH_E_RANGE, "%s: N too large", who);
     return FH_OK;
+}
+
+// Morton key of fh_spatial_sort for this encoder (sort_kernels.cuh): 16
+// bits shared greedily among the axes, each next bit to the axis whose bins
+// are widest in cells of the finest level (most corners), so bins are about
+// cubic in cells; bits are interleaved from the least significant end
+// (position j of every axis that has more than j bits), so an aligned block
+// of 2^k consecutive keys is also about cubic in cells.
+static void make_key_spec(fh_encoder e) {
+    int fin = 0;
+    for (int l = 1; l < e->L; l++)
+        if (e->info[l].corners > e->info[fin].corners) fin = l;
+    double ext[4];
+    for (int a = 0; a < 4; a++) {
+        ext[a] = (double)(e->info[fin].res[a] - 1);
+        e->key.bits[a] = 0;
+    }
+    for (int k = 0; k < 16; k++) {
+        int best = 0;
+        for (int a = 1; a < 4; a++)
+            if (ext[a] > ext[best]) best = a;
+        e->key.bits[best]++;
+        ext[best] *= 0.5;
+    }
+    int pos = 0;
+    for (uint32_t j = 0; pos < 16; j++)
+        for (int a = 0; a < 4 && pos < 16; a++)
+            if (e->key.bits[a] > j) {
+                e->key.axis[pos] = (uint8_t)a;
+                e->key.bit[pos] = (uint8_t)j;
+                e->key.pos[a][j] = (uint8_t)pos;
+                pos++;
+            }
 }
 
 extern "C" {
@@ -243,6 +414,7 @@ fh_status fh_build_levels(const fh_level_res *res, int L, int F, fh_dtype table_
         K.offset = (uint32_t)I.offset;
     }
     e->entries = off;
+    make_key_spec(e);
     *out = e;
     return FH_OK;
 }
@@ -391,6 +563,15 @@ static fh_status encode_bwd_impl(fh_encoder e, const float *coords, int64_t N, c
     cudaStream_t s = reinterpret_cast<cudaStream_t>(stream);
     const float4 *c4 = reinterpret_cast<const float4 *>(coords);
     if (e->kind == 1 && perm) return fail(FH_E_ARG, "fh_encode_bwd_ordered: not supported for MHE encoders");
+    if (perm) {
+        switch (e->F) {
+            case 1: launch_bwd_ordered<1>(e, c4, N, dout, dtable, s, perm); break;
+            case 2: launch_bwd_ordered<2>(e, c4, N, dout, dtable, s, perm); break;
+            case 4: launch_bwd_ordered<4>(e, c4, N, dout, dtable, s, perm); break;
+            default: launch_bwd_ordered<8>(e, c4, N, dout, dtable, s, perm); break;
+        }
+        return cuda_check(cudaGetLastError(), "fh_encode_bwd_ordered launch");
+    }
     if (e->small.n > 0) {
         const int smem = e->small.total * 4;
         int64_t blocks = (N * e->small.n + 255) / 256;
@@ -423,11 +604,14 @@ static fh_status encode_bwd_impl(fh_encoder e, const float *coords, int64_t N, c
             }
             continue;
         }
+        fh::LevelList ll;
+        ll.n = lc;
+        for (int i = 0; i < lc; i++) ll.id[i] = l0 + i;
         switch (e->F) {
-            case 1: fh::bwd_kernel<1><<<g, 256, 0, s>>>(e->params, c4, N, dout, dtable, e->flag, l0, lc, perm); break;
-            case 2: fh::bwd_kernel<2><<<g, 256, 0, s>>>(e->params, c4, N, dout, dtable, e->flag, l0, lc, perm); break;
-            case 4: fh::bwd_kernel<4><<<g, 256, 0, s>>>(e->params, c4, N, dout, dtable, e->flag, l0, lc, perm); break;
-            default: fh::bwd_kernel<8><<<g, 256, 0, s>>>(e->params, c4, N, dout, dtable, e->flag, l0, lc, perm); break;
+            case 1: fh::bwd_kernel<1><<<g, 256, 0, s>>>(e->params, c4, N, dout, dtable, e->flag, ll, nullptr); break;
+            case 2: fh::bwd_kernel<2><<<g, 256, 0, s>>>(e->params, c4, N, dout, dtable, e->flag, ll, nullptr); break;
+            case 4: fh::bwd_kernel<4><<<g, 256, 0, s>>>(e->params, c4, N, dout, dtable, e->flag, ll, nullptr); break;
+            default: fh::bwd_kernel<8><<<g, 256, 0, s>>>(e->params, c4, N, dout, dtable, e->flag, ll, nullptr); break;
         }
     }
     return cuda_check(cudaGetLastError(), "fh_encode_bwd launch");
@@ -457,13 +641,23 @@ fh_status fh_encode_bwd_ordered(fh_encoder e, const float *coords, int64_t N, co
     return encode_bwd_impl(e, coords, N, order, dout, dtable, stream);
 }
 
-size_t fh_spatial_sort_workspace_size(int64_t N) {
-    return (size_t)fh::sortk::kBins * 4 + ((size_t)(N < 0 ? 0 : N) * 2 + 255) / 256 * 256;
+fh_status fh_spatial_sort_bits(fh_encoder e, uint32_t bits[4], uint8_t axis_of_key_bit[16]) {
+    g_err[0] = 0;
+    if (!e || !bits) return fail(FH_E_ARG, "fh_spatial_sort_bits: NULL pointer");
+    for (int a = 0; a < 4; a++) bits[a] = e->key.bits[a];
+    if (axis_of_key_bit)
+        for (int k = 0; k < 16; k++) axis_of_key_bit[k] = e->key.axis[k];
+    return FH_OK;
 }
 
-fh_status fh_spatial_sort(const float *coords, int64_t N, uint32_t *order, void *workspace, size_t ws_bytes,
-                          fh_stream stream) {
+size_t fh_spatial_sort_workspace_size(int64_t N) {
+    return (size_t)(fh::sortk::kBins + fh::sortk::kScanBlocks) * 4 + ((size_t)(N < 0 ? 0 : N) * 2 + 255) / 256 * 256;
+}
+
+fh_status fh_spatial_sort(fh_encoder e, const float *coords, int64_t N, uint32_t *order, void *workspace,
+                          size_t ws_bytes, fh_stream stream) {
     g_err[0] = 0;
+    if (!e) return fail(FH_E_ARG, "fh_spatial_sort: NULL encoder");
     if (N < 0 || N > 0xFFFFFFFFll) return fail(FH_E_ARG, "fh_spatial_sort: N out of range");
     if (N == 0) return FH_OK;
     if (!coords || !aligned(coords, 16) || !order || !workspace || !aligned(workspace, 16))
@@ -471,14 +665,15 @@ fh_status fh_spatial_sort(const float *coords, int64_t N, uint32_t *order, void 
     if (ws_bytes < fh_spatial_sort_workspace_size(N)) return fail(FH_E_ARG, "fh_spatial_sort: workspace too small");
     cudaStream_t s = reinterpret_cast<cudaStream_t>(stream);
     uint32_t *hist = reinterpret_cast<uint32_t *>(workspace);
-    uint16_t *keys = reinterpret_cast<uint16_t *>(hist + fh::sortk::kBins);
+    uint32_t *sums = hist + fh::sortk::kBins;
+    uint16_t *keys = reinterpret_cast<uint16_t *>(sums + fh::sortk::kScanBlocks);
     fh_status st = cuda_check(cudaMemsetAsync(hist, 0, fh::sortk::kBins * 4, s), "fh_spatial_sort memset");
     if (st != FH_OK) return st;
     int64_t g = (N + 255) / 256;
     if (g > 148 * 16) g = 148 * 16;
-    fh::sortk::key_hist_kernel<<<(unsigned)g, 256, 0, s>>>(reinterpret_cast<const float4 *>(coords), N, keys, hist);
-    fh::sortk::scan_kernel<<<1, 1024, 0, s>>>(hist);
-    fh::sortk::scatter_kernel<<<(unsigned)g, 256, 0, s>>>(keys, N, hist, order);
+    fh::sortk::key_hist_kernel<<<(unsigned)g, 256, 0, s>>>(e->key, reinterpret_cast<const float4 *>(coords), N, keys, hist);
+    fh::sortk::scan_blocks_kernel<<<fh::sortk::kScanBlocks, 1024, 0, s>>>(hist, sums);
+    fh::sortk::scatter_kernel<<<(unsigned)g, 256, 0, s>>>(keys, N, hist, sums, order);
     return cuda_check(cudaGetLastError(), "fh_spatial_sort launch");
 }
 

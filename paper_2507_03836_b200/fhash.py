@@ -28,7 +28,7 @@ EXPORTS = [
     "fh_table_entries", "fh_param_count", "fh_encoder_destroy", "fh_encode_fwd", "fh_encode_bwd",
     "fh_encode_indices", "fh_zero_grad", "fh_encode_fwd_bwd", "fh_encode_step_host", "fh_status_sync", "fh_last_error",
     "fh_version", "fh_spatial_sort_workspace_size", "fh_spatial_sort", "fh_encode_fwd_ordered",
-    "fh_encode_bwd_ordered", "fh_build_mhe", "fh_encoder_kind",
+    "fh_encode_bwd_ordered", "fh_build_mhe", "fh_encoder_kind", "fh_spatial_sort_bits",
     # include/fhash_bench.h (measurement kernels)
     "fh_bench_gather", "fh_bench_red", "fh_bench_copy",
     # train step
@@ -91,7 +91,9 @@ def lib() -> ctypes.CDLL:
     L.fh_encoder_kind.argtypes = [vp]
     L.fh_spatial_sort_workspace_size.argtypes = [i64]
     L.fh_spatial_sort_workspace_size.restype = ctypes.c_size_t
-    L.fh_spatial_sort.argtypes = [vp, i64, vp, vp, ctypes.c_size_t, vp]
+    L.fh_spatial_sort.argtypes = [vp, vp, i64, vp, vp, ctypes.c_size_t, vp]
+    L.fh_spatial_sort_bits.argtypes = [vp, ctypes.POINTER(ctypes.c_uint32), ctypes.POINTER(ctypes.c_uint8)]
+    L.fh_spatial_sort_bits.restype = c_int
     L.fh_encode_fwd_ordered.argtypes = [vp, vp, i64, vp, vp, vp, c_int, vp]
     L.fh_encode_bwd_ordered.argtypes = [vp, vp, i64, vp, vp, vp, vp]
     for name in ("fh_spatial_sort", "fh_encode_fwd_ordered", "fh_encode_bwd_ordered"):
@@ -206,6 +208,13 @@ class Encoder:
         _check(lib().fh_encode_bwd_ordered(self._h, _ptr(coords), coords.shape[0], _ptr(order), _ptr(dout),
                                            _ptr(dtable), _stream(stream)))
         return dtable
+
+    def sort_bits(self):
+        """(bits per axis [4], axis of each of the 16 key bits, LSB first)."""
+        b = (ctypes.c_uint32 * 4)()
+        ax = (ctypes.c_uint8 * 16)()
+        _check(lib().fh_spatial_sort_bits(self._h, b, ax))
+        return list(b), list(ax)
 
     def zero_grad(self, dtable, stream=None):
         _check(lib().fh_zero_grad(self._h, _ptr(dtable), _stream(stream)))
@@ -511,11 +520,13 @@ class MHEEncoder(Encoder):
 
 
 class SpatialOrder:
-    """Reusable device buffers for fh_spatial_sort (execution order of a batch)."""
+    """Reusable device buffers for fh_spatial_sort (execution order of a
+    batch, keyed by the encoder's Morton bit allocation)."""
 
-    def __init__(self, max_n: int, device=None):
+    def __init__(self, enc: "Encoder", max_n: int, device=None):
         import torch
         dev = device or torch.device("cuda", torch.cuda.current_device())
+        self.enc = enc
         self.max_n = max_n
         self.order = torch.empty(max_n, dtype=torch.int32, device=dev)
         nb = int(lib().fh_spatial_sort_workspace_size(max_n))
@@ -524,6 +535,6 @@ class SpatialOrder:
     def __call__(self, coords, stream=None):
         N = coords.shape[0]
         assert N <= self.max_n
-        _check(lib().fh_spatial_sort(_ptr(coords), N, _ptr(self.order), _ptr(self.ws), self.ws.numel(),
+        _check(lib().fh_spatial_sort(self.enc.handle, _ptr(coords), N, _ptr(self.order), _ptr(self.ws), self.ws.numel(),
                                      _stream(stream)))
         return self.order[:N]

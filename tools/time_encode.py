@@ -34,7 +34,7 @@ def main():
     flush = torch.empty(256 << 20, dtype=torch.uint8, device="cuda")
     e = [torch.cuda.Event(enable_timing=True) for _ in range(4)]
     sorted_mode = os.environ.get("FH_SORTED", "0") == "1"
-    so = fh.SpatialOrder(N) if sorted_mode else None
+    so = fh.SpatialOrder(enc, N) if sorted_mode else None
     tf = tb = ts = 0.0
     for it in range(iters + 3):
         flush.fill_(it & 255)
