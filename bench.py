@@ -333,6 +333,8 @@ def paper_encoder_compare(fh, torch, W, steps):
     res = {}
     encs = {
         "fhash": fh.Encoder(fh.fold_schedule(S, n, 2), 2),
+        # NEXT-2: the same encoder with the brick (tiled Z-order) linearization, P:174 / R21
+        "fhash_brick": fh.Encoder(fh.fold_schedule(S, n, 2), 2, lin=fh.FH_LIN_BRICK),
         "mhe": fh.MHEEncoder(W.geometric(16, 200, 6), 2, 1 << 20, n),
     }
     for name, enc in encs.items():
@@ -357,7 +359,8 @@ def paper_encoder_compare(fh, torch, W, steps):
                      "fwd_bwd_ms": ms, "samples_per_s": B / (ms / 1e3)}
         del table, out, g, dt
     res["workload"] = ("Combustion-Seg shape: FBB 200x110x54, 10 key frames, batch 2^21 voxel samples; "
-                       "F-Hash fold 2 (Eqs. 4-8) vs MHE T=2^20 x 6 levels x 10 frames; F=2 fp32")
+                       "F-Hash fold 2 (Eqs. 4-8; Eq. 9 and brick linearization) vs MHE T=2^20 x 6 levels "
+                       "x 10 frames; F=2 fp32")
     return res
 
 

@@ -64,7 +64,7 @@ typedef struct {
     uint64_t corners;     /* C_l = prod res (64-bit) */
     uint64_t table_size;  /* T_l: = C_l (bijective, Eq. 9) or the cap (hashed, R5) */
     uint32_t hashed;      /* 1 if C_l > cap */
-    uint32_t reserved;
+    uint32_t reserved;    /* linearization of a bijective level: FH_LIN_EQ9 or FH_LIN_BRICK (0 if hashed) */
     uint64_t offset;      /* first entry of this level in the packed table */
 } fh_level_info;
 
@@ -99,6 +99,25 @@ fh_status fh_fold_schedule(const uint32_t S_xyz[3], uint32_t n_t, uint32_t fold,
  * status word on the current device). */
 fh_status fh_build_levels(const fh_level_res *res, int L, int F, fh_dtype table_dtype,
                           uint64_t cap, fh_encoder *out);
+
+/* ---------------------------------------------------------- NEXT-2 ---
+ * fh_build_levels_lin -- fh_build_levels with a choice of the bijective
+ * linearization ("Other linearizations like Morton and Z-order can also be
+ * used to construct F-Hash with preserved locality", §3.2.3):
+ *   FH_LIN_EQ9    Eq. 9 row-major, x fastest -- fh_build_levels;
+ *   FH_LIN_BRICK  brick order (reading R21): 2x2x2x2-vertex bricks (clipped
+ *                 at odd grid edges) in row-major order, vertices row-major
+ *                 inside a brick; with b = v>>1, i = v&1, e = min(2, R-2b):
+ *                 idx = 2 b_t RxRyRz + 2 b_z RxRy e_t + 2 b_y Rx e_z e_t
+ *                     + 2 b_x e_y e_z e_t + ((i_t e_z + i_z) e_y + i_y) e_x + i_x.
+ *                 Still a bijection onto [0, C_l) (minimal perfect hash); the
+ *                 16 corners of a cell at even coordinates are 16 consecutive
+ *                 entries.  Hashed (capped) levels are unaffected.
+ * Table size, packing and every encode call are as for fh_build_levels.
+ * Errors: as fh_build_levels, FH_E_ARG for another linearization value. */
+enum { FH_LIN_EQ9 = 0, FH_LIN_BRICK = 1 };
+fh_status fh_build_levels_lin(const fh_level_res *res, int L, int F, fh_dtype table_dtype,
+                              uint64_t cap, int linearization, fh_encoder *out);
 
 /* ---------------------------------------------------------- NEXT-3 ---
  * fh_build_mhe -- the MHE baseline the paper compares against (

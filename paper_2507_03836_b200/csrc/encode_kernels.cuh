@@ -40,6 +40,23 @@ __device__ __forceinline__ void locate(float p, float scale, uint32_t R, uint32_
     w = __fsub_rn(s, __int2float_rn(ii));
 }
 
+// NEXT-2 ("Other linearizations like Morton and Z-order can also be
+// used to construct F-Hash with preserved locality"; reading R21): brick
+// order of a bijective level -- 2x2x2x2-vertex bricks (clipped to e_a = 1 at
+// an odd grid edge) enumerated row-major, vertices row-major inside a brick.
+// With b = v >> 1, i = v & 1, e = min(2, R - 2b) per axis:
+//   idx = 2 b_t RxRyRz + 2 b_z RxRy e_t + 2 b_y Rx e_z e_t + 2 b_x e_y e_z e_t
+//       + ((i_t e_z + i_z) e_y + i_y) e_x + i_x
+// The 16 corners of a cell at even coordinates are one brick, i.e. 16
+// consecutive entries (one 128-byte line at 8-byte entries).
+__device__ __forceinline__ uint32_t brick_index(const Level &lv, uint32_t X, uint32_t Y, uint32_t Z, uint32_t T) {
+    const uint32_t bx = X >> 1, by = Y >> 1, bz = Z >> 1, bt = T >> 1;
+    const uint32_t ex = min(2u, lv.res[0] - 2u * bx), ey = min(2u, lv.res[1] - 2u * by);
+    const uint32_t ez = min(2u, lv.res[2] - 2u * bz), et = min(2u, lv.res[3] - 2u * bt);
+    return 2u * bt * lv.st + 2u * bz * lv.sz * et + 2u * by * lv.sy * ez * et + 2u * bx * ey * ez * et +
+           (((T & 1u) * ez + (Z & 1u)) * ey + (Y & 1u)) * ex + (X & 1u);
+}
+
 // Cell of one (sample, level): base indices and fractions.
 struct Cell {
     uint32_t idx[16];
@@ -56,12 +73,17 @@ __device__ __forceinline__ bool cell_of(const Level &lv, float4 p, Cell &c) {
     locate(p.y, lv.scale[1], lv.res[1], iy, c.w[1], bad);
     locate(p.z, lv.scale[2], lv.res[2], iz, c.w[2], bad);
     locate(p.w, lv.scale[3], lv.res[3], it, c.w[3], bad);
-    if (!lv.hashed) {
+    if (lv.hashed == 0) {
         const uint32_t base = lv.offset + ix + iy * lv.sy + iz * lv.sz + it * lv.st;
 #pragma unroll
         for (int k = 0; k < 16; k++)
             c.idx[k] = base + (k & 1) + ((k >> 1) & 1) * lv.sy + ((k >> 2) & 1) * lv.sz +
                        ((k >> 3) & 1) * lv.st;
+    } else if (lv.hashed == 2) {
+#pragma unroll
+        for (int k = 0; k < 16; k++)
+            c.idx[k] = lv.offset + brick_index(lv, ix + (k & 1), iy + ((k >> 1) & 1), iz + ((k >> 2) & 1),
+                                               it + ((k >> 3) & 1));
     } else {
         const uint32_t hx0 = ix, hx1 = ix + 1;
         const uint32_t hy0 = iy * kPy, hy1 = (iy + 1) * kPy;

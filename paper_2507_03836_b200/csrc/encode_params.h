@@ -9,7 +9,7 @@ struct __align__(16) Level {
     uint32_t res[4];     // Rx, Ry, Rz, Rt (vertices)
     float scale[4];      // fp32(R - 1) per axis (R2)
     uint32_t sy, sz, st; // Eq. 9 strides: Rx, Rx*Ry, Rx*Ry*Rz
-    uint32_t hashed;     // 1: capped level, R5 hash
+    uint32_t hashed;     // 0: Eq. 9 (row-major); 1: capped level, R5 hash; 2: brick order (NEXT-2, R21)
     uint32_t mask;       // T_l - 1 for hashed levels (T_l power of two)
     uint32_t offset;     // first entry of the level in the packed table
     uint32_t pad[2];

@@ -359,7 +359,14 @@ fh_status fh_fold_schedule(const uint32_t S_xyz[3], uint32_t n_t, uint32_t fold,
 
 fh_status fh_build_levels(const fh_level_res *res, int L, int F, fh_dtype table_dtype, uint64_t cap,
                           fh_encoder *out) {
+    return fh_build_levels_lin(res, L, F, table_dtype, cap, FH_LIN_EQ9, out);
+}
+
+fh_status fh_build_levels_lin(const fh_level_res *res, int L, int F, fh_dtype table_dtype, uint64_t cap,
+                              int linearization, fh_encoder *out) {
     g_err[0] = 0;
+    if (linearization != FH_LIN_EQ9 && linearization != FH_LIN_BRICK)
+        return fail(FH_E_ARG, "fh_build_levels: linearization %d not FH_LIN_EQ9 or FH_LIN_BRICK", linearization);
     if (!res || !out) return fail(FH_E_ARG, "fh_build_levels: NULL pointer");
     *out = nullptr;
     if (L < 1 || L > FH_MAX_LEVELS) return fail(FH_E_ARG, "fh_build_levels: L = %d not in [1, %d]", L, FH_MAX_LEVELS);
@@ -392,7 +399,7 @@ fh_status fh_build_levels(const fh_level_res *res, int L, int F, fh_dtype table_
         I.corners = c;
         I.hashed = (cap != 0 && c > cap) ? 1u : 0u;
         I.table_size = I.hashed ? cap : c;
-        I.reserved = 0;
+        I.reserved = I.hashed ? 0u : (uint32_t)linearization;
         I.offset = off;
         off += I.table_size;
         if (off * (uint64_t)F >= (1ull << 32)) {
@@ -409,7 +416,7 @@ fh_status fh_build_levels(const fh_level_res *res, int L, int F, fh_dtype table_
         K.sz = I.res[0] * I.res[1];
         K.st = I.hashed ? 0u : (uint32_t)((uint64_t)I.res[0] * I.res[1] * I.res[2]);
         if (I.hashed) K.sz = 0;  // unused on hashed levels (may overflow)
-        K.hashed = I.hashed;
+        K.hashed = I.hashed ? 1u : (linearization == FH_LIN_BRICK ? 2u : 0u);
         K.mask = I.hashed ? (uint32_t)(cap - 1) : 0u;
         K.offset = (uint32_t)I.offset;
     }

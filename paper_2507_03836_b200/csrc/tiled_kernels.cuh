@@ -125,10 +125,11 @@ __device__ __forceinline__ Box box_of(const Level &lv, const Tile &tl, uint32_t 
     return b;
 }
 
-// Global entry of vertex (X, Y, Z, Tt) of a level: Eq. 9 or the R5 hash
+// Global entry of vertex (X, Y, Z, Tt) of a level: Eq. 9, the brick order (R21) or the R5 hash
 // (the same arithmetic as cell_of's corner loop).
 __device__ __forceinline__ uint32_t vertex_entry(const Level &lv, uint32_t X, uint32_t Y, uint32_t Z, uint32_t Tt) {
-    if (!lv.hashed) return lv.offset + X + Y * lv.sy + Z * lv.sz + Tt * lv.st;
+    if (lv.hashed == 0) return lv.offset + X + Y * lv.sy + Z * lv.sz + Tt * lv.st;
+    if (lv.hashed == 2) return lv.offset + brick_index(lv, X, Y, Z, Tt);
     return lv.offset + ((X ^ (Y * kPy) ^ (Z * kPz) ^ (Tt * kPt)) & lv.mask);
 }
 

@@ -28,7 +28,7 @@ EXPORTS = [
     "fh_table_entries", "fh_param_count", "fh_encoder_destroy", "fh_encode_fwd", "fh_encode_bwd",
     "fh_encode_indices", "fh_zero_grad", "fh_encode_fwd_bwd", "fh_encode_step_host", "fh_status_sync", "fh_last_error",
     "fh_version", "fh_spatial_sort_workspace_size", "fh_spatial_sort", "fh_encode_fwd_ordered",
-    "fh_encode_bwd_ordered", "fh_build_mhe", "fh_encoder_kind", "fh_spatial_sort_bits",
+    "fh_encode_bwd_ordered", "fh_build_mhe", "fh_encoder_kind", "fh_spatial_sort_bits", "fh_build_levels_lin",
     # include/fhash_bench.h (measurement kernels)
     "fh_bench_gather", "fh_bench_red", "fh_bench_copy",
     # train step
@@ -53,7 +53,7 @@ class LevelRes(ctypes.Structure):
 
 class LevelInfo(ctypes.Structure):
     _fields_ = [("res", ctypes.c_uint32 * 4), ("corners", ctypes.c_uint64), ("table_size", ctypes.c_uint64),
-                ("hashed", ctypes.c_uint32), ("reserved", ctypes.c_uint32), ("offset", ctypes.c_uint64)]
+                ("hashed", ctypes.c_uint32), ("lin", ctypes.c_uint32), ("offset", ctypes.c_uint64)]
 
 
 _lib = None
@@ -71,6 +71,8 @@ def lib() -> ctypes.CDLL:
     L.fh_fold_schedule.argtypes = [ctypes.POINTER(ctypes.c_uint32), ctypes.c_uint32, ctypes.c_uint32,
                                    ctypes.POINTER(LevelRes), ctypes.POINTER(c_int)]
     L.fh_build_levels.argtypes = [ctypes.POINTER(LevelRes), c_int, c_int, c_int, u64, ctypes.POINTER(vp)]
+    L.fh_build_levels_lin.argtypes = [ctypes.POINTER(LevelRes), c_int, c_int, c_int, u64, c_int, ctypes.POINTER(vp)]
+    L.fh_build_levels_lin.restype = c_int
     L.fh_level_info_get.argtypes = [vp, c_int, ctypes.POINTER(LevelInfo)]
     L.fh_num_levels.argtypes = [vp]
     L.fh_feature_dim.argtypes = [vp]
@@ -142,18 +144,24 @@ def fold_schedule(S_xyz: Sequence[int], n_t: int, fold: int) -> List[Tuple[int, 
 _DT = {"f32": FH_F32, "f16": FH_F16, "bf16": FH_BF16}
 
 
+FH_LIN_EQ9, FH_LIN_BRICK = 0, 1
+
+
 class Encoder:
     """Handle on an fh_encoder (a1 build_levels).  levels: [(Rx,Ry,Rz,Rt)]
-    in output order; cap 0 = pure MPHF."""
+    in output order; cap 0 = pure MPHF; lin: FH_LIN_EQ9 (Eq. 9) or
+    FH_LIN_BRICK (NEXT-2 brick order of the bijective levels, R21)."""
 
-    def __init__(self, levels: Sequence[Sequence[int]], F: int, table_dtype: str = "f32", cap: int = 0):
+    def __init__(self, levels: Sequence[Sequence[int]], F: int, table_dtype: str = "f32", cap: int = 0,
+                 lin: int = FH_LIN_EQ9):
         L = len(levels)
         arr = (LevelRes * max(L, 1))()
         for i, r in enumerate(levels):
             arr[i].res[:] = [int(v) for v in r]
         h = ctypes.c_void_p()
-        _check(lib().fh_build_levels(arr, L, F, _DT[table_dtype], cap, ctypes.byref(h)))
+        _check(lib().fh_build_levels_lin(arr, L, F, _DT[table_dtype], cap, lin, ctypes.byref(h)))
         self._h = h
+        self.lin = lin
         self.levels = [tuple(int(v) for v in r) for r in levels]
         self.L, self.F, self.cap, self.table_dtype = L, F, cap, table_dtype
         self.entries = int(lib().fh_table_entries(h))
@@ -173,7 +181,7 @@ class Encoder:
         I = LevelInfo()
         _check(lib().fh_level_info_get(self._h, l, ctypes.byref(I)))
         return dict(res=tuple(I.res), corners=I.corners, table_size=I.table_size, hashed=bool(I.hashed),
-                    offset=I.offset)
+                    offset=I.offset, lin=int(I.lin))
 
     # -------------------------------------------------------------- kernels
     def fwd(self, coords, table, out=None, out_dtype: str = "f32", stream=None):

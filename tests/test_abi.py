@@ -121,3 +121,21 @@ def test_encode_argument_errors_are_host_side():
     assert b"NULL" in L.fh_last_error()
     # N = 0 is a no-op
     assert L.fh_encode_fwd(enc.handle, 16, 0, 16, 16, 0, None) == fh.FH_OK
+
+
+def test_build_levels_lin_brick_info_and_errors():
+    """NEXT-2 through the ABI: the brick linearization keeps the table sizes
+    and packing of Eq. 9 (a bijection onto [0, C_l)), is reported per level,
+    leaves hashed levels alone, and rejects unknown values."""
+    cfg = W.CFG1H
+    a = fh.Encoder(cfg.levels, 2, cap=cfg.cap)
+    b = fh.Encoder(cfg.levels, 2, cap=cfg.cap, lin=fh.FH_LIN_BRICK)
+    assert a.entries == b.entries
+    for l in range(cfg.L):
+        ia, ib = a.level_info(l), b.level_info(l)
+        assert ia["table_size"] == ib["table_size"] and ia["offset"] == ib["offset"]
+        assert ia["lin"] == 0
+        assert ib["lin"] == (0 if ib["hashed"] else fh.FH_LIN_BRICK)
+    with pytest.raises(fh.FHashError) as e:
+        fh.Encoder(cfg.levels, 2, lin=7)
+    assert e.value.status == fh.FH_E_ARG

@@ -267,6 +267,72 @@ def test_tiled_out_of_domain_flagged():
     assert ordered_check(cfg, case) == fh.FH_E_DOMAIN
 
 
+# ------------------------------------------ NEXT-2: brick linearization (R21)
+BRICK_LEVELS = [W.cfg1_levels(), ((5, 7, 9, 3), (13, 3, 6, 7), (2, 2, 2, 2), (17, 2, 11, 5)),
+                tuple(oracle.fold_schedule((200, 110, 54), 10, 2)[3:])]
+
+
+@pytest.mark.parametrize("levels", BRICK_LEVELS, ids=["cfg1", "ragged", "fold2-tail"])
+@pytest.mark.parametrize("cap", [0, 1 << 11])
+def test_brick_indices_forward_backward(levels, cap):
+    """FH_LIN_BRICK: indices bit-exact against the oracle's brick order
+    (Levels(lin=1)) on even, odd and degenerate shapes with and without
+    capped levels; forward and backward within the bars."""
+    cfg = W.EncoderConfig("brick", tuple(levels), F=2, cap=cap, table_dtype="f32")
+    case = W.encode_case(cfg, 4096 + 37, seed=11)
+    enc = fh.Encoder(cfg.levels, 2, "f32", cap, lin=fh.FH_LIN_BRICK)
+    ref = oracle.Levels(cfg.levels, cap, lin=1)
+    idx, w = enc.indices(dev(case.coords))
+    assert enc.status_sync() == fh.FH_OK
+    ridx, rW, _ = ref.indices(case.coords)
+    assert np.array_equal(idx.cpu().numpy().view(np.uint32), ridx)
+    got, _ = run_fwd(enc, case)
+    r, ab = ref.forward(case.coords, case.table, want_abs=True)
+    check_fwd(got, r, ab)
+    gb, _ = run_bwd(enc, case)
+    G, A = ref.backward(case.coords, case.dout, 2, want_abs=True)
+    check_bwd(gb, G, A)
+
+
+def test_brick_edges_and_ordered_path():
+    """Brick order at the domain edges / lattice points, and through the
+    ordered (tiled forward, aggregated backward) path."""
+    cfg = W.EncoderConfig("brick", W.cfg1_levels(), F=2, cap=0, table_dtype="f32")
+    coords = np.concatenate([W.edge_coords(), W.draw_coords(W.rng(12), 6000)])
+    case = W.encode_case(cfg, len(coords), seed=12, coords=coords)
+    enc = fh.Encoder(cfg.levels, 2, lin=fh.FH_LIN_BRICK)
+    ref = oracle.Levels(cfg.levels, 0, lin=1)
+    idx, _ = enc.indices(dev(coords))
+    assert np.array_equal(idx.cpu().numpy().view(np.uint32), ref.indices(coords)[0])
+    c, t, g = dev(case.coords), dev(case.table), dev(case.dout)
+    a = enc.fwd(c, t)
+    order = fh.SpatialOrder(enc, len(coords))(c)
+    assert torch.equal(a, enc.fwd_ordered(c, order, t, torch.empty_like(a)))
+    r, ab = ref.forward(coords, case.table, want_abs=True)
+    check_fwd(a.cpu().numpy().astype(np.float64), r, ab)
+    dt = torch.zeros((enc.entries, 2), device="cuda")
+    enc.bwd_ordered(c, order, g, dt)
+    G, A = ref.backward(coords, case.dout, 2, want_abs=True)
+    check_bwd(dt.cpu().numpy().astype(np.float64), G, A)
+
+
+def test_brick_cfg2_full_size():
+    """cfg2 (levels 0-4 bijective -> brick order, 5-15 hashed) at the bench
+    size: forward on every row and backward on every entry vs the oracle."""
+    cfg = W.CFG2
+    case = W.encode_case(cfg, W.N_CFG2, seed=3)
+    enc = fh.Encoder(cfg.levels, cfg.F, cfg.table_dtype, cfg.cap, lin=fh.FH_LIN_BRICK)
+    ref = oracle.Levels(cfg.levels, cfg.cap, lin=1)
+    got, st = run_fwd(enc, case)
+    assert st == fh.FH_OK
+    r, ab = ref.forward(case.coords, case.table, want_abs=True)
+    check_fwd(got, r, ab)
+    del r, ab, got
+    gb, _ = run_bwd(enc, case)
+    G, A = ref.backward(case.coords, case.dout, cfg.F, want_abs=True)
+    check_bwd(gb, G, A)
+
+
 # ----------------------------------------------- full size (bench launch cfg)
 def test_cfg2_full_size_parity():
     """BASELINE.json configs[1] at full size (2^20 points, 16 levels), the

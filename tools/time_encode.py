@@ -21,9 +21,10 @@ from paper_2507_03836_b200 import fhash as fh  # noqa: E402
 def main():
     name = sys.argv[1] if len(sys.argv) > 1 else "cfg2"
     iters = int(sys.argv[2]) if len(sys.argv) > 2 else 20
-    cfg = {"cfg2": W.CFG2, "cfg3": W.CFG3, "cfg4": W.CFG4}[name]
-    N = {"cfg2": W.N_CFG2, "cfg3": W.N_CFG3, "cfg4": W.N_CFG4}[name]
-    enc = fh.Encoder(cfg.levels, cfg.F, cfg.table_dtype, cfg.cap)
+    pc = W.EncoderConfig("pc", tuple(fh.fold_schedule((200, 110, 54), 10, 2)), F=2, cap=0, table_dtype="f32")
+    cfg = {"cfg2": W.CFG2, "cfg3": W.CFG3, "cfg4": W.CFG4, "pc": pc}[name]
+    N = {"cfg2": W.N_CFG2, "cfg3": W.N_CFG3, "cfg4": W.N_CFG4, "pc": 1 << 21}[name]
+    enc = fh.Encoder(cfg.levels, cfg.F, cfg.table_dtype, cfg.cap, lin=int(os.environ.get("FH_LIN", "0")))
     g = torch.Generator("cuda").manual_seed(0)
     coords = torch.rand((N, 4), device="cuda", generator=g)
     tdt = torch.float32 if cfg.table_dtype == "f32" else torch.float16
@@ -58,7 +59,7 @@ def main():
             tf += e[1].elapsed_time(e[2])
             tb += e[2].elapsed_time(e[3])
     tot = (ts + tf + tb) / iters
-    print(f"{os.path.basename(fh.LIB_PATH)} {name}{' sorted' if so else ''}: sort {ts / iters:.4f} ms  "
+    print(f"{os.path.basename(fh.LIB_PATH)} {name}{' sorted' if so else ''} lin={enc.lin}: sort {ts / iters:.4f} ms  "
           f"fwd {tf / iters:.4f} ms  bwd {tb / iters:.4f} ms  ({N / (tot / 1e3) / 1e6:.1f} M samples/s)")
 
 
