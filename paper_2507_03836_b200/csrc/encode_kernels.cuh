@@ -282,6 +282,49 @@ __device__ __forceinline__ void extract(const Block32 &b, uint32_t s, float *o) 
     }
 }
 
+// Raw loads for the pair gather: one entry (W words) or an aligned pair of
+// entries (2W words) through the read-only path.
+template <int W>
+__device__ __forceinline__ void ld_entry(const void *table, uint32_t i, uint32_t *o) {
+    if constexpr (W == 1) {
+        o[0] = __ldg(reinterpret_cast<const uint32_t *>(table) + i);
+    } else if constexpr (W == 2) {
+        const uint2 v = __ldg(reinterpret_cast<const uint2 *>(table) + i);
+        o[0] = v.x; o[1] = v.y;
+    } else {
+        const uint4 v = __ldg(reinterpret_cast<const uint4 *>(table) + i);
+        o[0] = v.x; o[1] = v.y; o[2] = v.z; o[3] = v.w;
+    }
+}
+template <int W>
+__device__ __forceinline__ void ld_pair(const void *table, uint32_t chunk, uint32_t *o) {
+    if constexpr (W == 1) {
+        const uint2 v = __ldg(reinterpret_cast<const uint2 *>(table) + chunk);
+        o[0] = v.x; o[1] = v.y;
+    } else if constexpr (W == 2) {
+        const uint4 v = __ldg(reinterpret_cast<const uint4 *>(table) + chunk);
+        o[0] = v.x; o[1] = v.y; o[2] = v.z; o[3] = v.w;
+    } else {
+        const Block32 b = ld_block(table, chunk);
+#pragma unroll
+        for (int j = 0; j < 8; j++) o[j] = b.w[j];
+    }
+}
+// F features of type T packed in 32-bit words -> floats.
+template <typename T, int F>
+__device__ __forceinline__ void words_to_float(const uint32_t *w, float *o) {
+    if constexpr (sizeof(T) == 4) {
+#pragma unroll
+        for (int j = 0; j < F; j++) o[j] = __uint_as_float(w[j]);
+    } else {
+#pragma unroll
+        for (int j = 0; j < F / 2; j++) {
+            const float2 f = __half22float2(*reinterpret_cast<const __half2 *>(&w[j]));
+            o[2 * j] = f.x; o[2 * j + 1] = f.y;
+        }
+    }
+}
+
 // Gather the 16 corner entries of one (sample, level) into e[16][F].
 // full_blocks = number of complete 32-byte blocks in the table; entries in
 // a trailing partial block are read entry-wise (never past the buffer).
@@ -290,9 +333,41 @@ __device__ __forceinline__ void gather16(const T *__restrict__ table, uint32_t f
                                          float (&e)[16][F]) {
     using Tr = EntryTraits<T, F>;
 #ifndef FH_BLOCK_GATHER
-#define FH_BLOCK_GATHER 0
+#define FH_BLOCK_GATHER 3
 #endif
-    if constexpr (Tr::kBytes == 8 && FH_BLOCK_GATHER == 2) {
+    if constexpr ((Tr::kBytes == 4 || Tr::kBytes == 8 || Tr::kBytes == 16) && FH_BLOCK_GATHER == 3) {
+        // x-pair in ONE load of the aligned 2-entry chunk when both entries
+        // share it (i1 == i0 ^ 1: about half the pairs on Eq. 9 and on the R5
+        // hash, whose x-neighbours differ in the low bits), else two entry
+        // loads into the same registers.  1.5 L1 requests per pair instead of
+        // 2, no extra registers.  Measured on B200: cfg2 fwd 0.763 -> 0.738
+        // ms, cfg4 fwd 3.017 -> 2.841 ms.
+        constexpr int W = Tr::kWords;          // 32-bit words per entry (1, 2, 4)
+        uint32_t r[8][2 * W];
+#pragma unroll
+        for (int k = 0; k < 8; k++) {
+            const uint32_t i0 = idx[2 * k], i1 = idx[2 * k + 1];
+            if ((i0 ^ i1) == 1u) {
+                ld_pair<W>(table, i0 >> 1, r[k]);
+            } else {
+                ld_entry<W>(table, i0, r[k]);
+                ld_entry<W>(table, i1, r[k] + W);
+            }
+        }
+#pragma unroll
+        for (int k = 0; k < 8; k++) {
+            const uint32_t i0 = idx[2 * k], i1 = idx[2 * k + 1];
+            const bool swap = ((i0 ^ i1) == 1u) && (i0 & 1u);  // the chunk holds (i1, i0)
+            uint32_t wa[W], wb[W];
+#pragma unroll
+            for (int j = 0; j < W; j++) {
+                wa[j] = swap ? r[k][W + j] : r[k][j];
+                wb[j] = swap ? r[k][j] : r[k][W + j];
+            }
+            words_to_float<T, F>(wa, e[2 * k]);
+            words_to_float<T, F>(wb, e[2 * k + 1]);
+        }
+    } else if constexpr (Tr::kBytes == 8 && FH_BLOCK_GATHER == 2) {
         // x-pair as one 16-byte load of the aligned chunk holding entry i0;
         // the partner comes from the same chunk when (i0>>1) == (i1>>1),
         // else from one more 8-byte load.  Chunks never pass the buffer end.
@@ -332,7 +407,7 @@ __device__ __forceinline__ void gather16(const T *__restrict__ table, uint32_t f
                 }
             }
         }
-    } else if constexpr (Tr::kBytes > 32 || !FH_BLOCK_GATHER) {
+    } else if constexpr (Tr::kBytes > 32 || FH_BLOCK_GATHER != 1) {
 #pragma unroll
         for (int k = 0; k < 16; k++) Gather<F, T>::load(table, idx[k], e[k]);
     } else {
