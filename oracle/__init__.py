@@ -7,6 +7,9 @@ CUDA path (`paper_2507_03836_b200/`) and never imports it.
   * fhash_oracle.c  -- level builder (Eqs. 4-9), cell location, the 16
                        corner indices, fp64 forward / backward, stats.
   * train.py        -- MLP forward/backward, MSE, Adam in fp64 numpy.
+  * coreset.py      -- NEXT-4 feature-based coreset selection (§3.1, Eqs.
+                       1-3): extraction, dilation, occupancy bits, FBB,
+                       Eqs. 1-2 coordinates, the Eq. 3 union.
 
 Parity-pin status of each function is listed in DESIGN.md §4; the capped
 (hashed) level index is "parity unpinned" by the paper (pinned only by its
