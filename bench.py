@@ -364,6 +364,55 @@ def paper_encoder_compare(fh, torch, W, steps):
     return res
 
 
+def coreset_bench(fh, torch, W, steps, hbm_peak, with_cpu):
+    """NEXT-4: GPU coreset selection (fh_coreset_build + fh_coreset_emit,
+    PAPER §3.1, Eqs. 1-3) on 8 key frames of the cfg3 field (256^3 moving
+    Gaussian blobs), segmentation feature at 0.5.  HBM-streaming: algorithmic
+    bytes = 4 B/vertex volume read + 20 B/sample written + the occupancy bits."""
+    import numpy as np
+    blobs = W.gaussian_blob_params(W.rng(0))
+    field = fh.field_gaussian_blobs(256, 32, blobs)
+    keys = field[::4].contiguous()
+    del field
+    n = keys.shape[0]
+    V = keys[0].numel()
+    flush = torch.empty(256 << 20, dtype=torch.uint8, device="cuda")
+    cs = fh.Coreset(keys, fh.FH_FEAT_SEGMENTATION, 0.5)
+    M = cs.count
+    coords = torch.empty((M, 4), device="cuda")
+    vals = torch.empty((M,), device="cuda")
+    e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    tot = 0.0
+    for it in range(steps + 2):
+        flush.fill_(it & 255)
+        e0.record()
+        c2 = fh.Coreset(keys, fh.FH_FEAT_SEGMENTATION, 0.5)
+        c2.emit(coords, vals)
+        e1.record()
+        torch.cuda.synchronize()
+        if it >= 2:
+            tot += e0.elapsed_time(e1)
+    ms = tot / steps
+    alg = n * V * 4 + M * 20 + n * cs.words * 4
+    out = {"workload": "8 key frames of the cfg3 field (256^3 Gaussian blobs), segmentation >= 0.5; "
+                       "build (feature, dilation, occupancy, FBB, counts) + emit (Eqs. 1-3 samples)",
+           "vertices": n * V, "coreset_samples": M, "coreset_fraction": M / (n * V),
+           "fbb": cs.fbb, "ms": ms, "vertices_per_s": n * V / (ms / 1e3),
+           "roofline": {"bound": "hbm", "achieved_gbs": alg / (ms / 1e3) / 1e9, "peak_gbs": hbm_peak,
+                        "frac": alg / (ms / 1e3) / 1e9 / hbm_peak, "algorithmic_bytes": alg},
+           "gpu_launches": 11}
+    if with_cpu:
+        from oracle import coreset as C
+        small = keys[:2, 96:128, 96:128, 96:128].cpu().numpy()
+        t0 = time.perf_counter()
+        C.build_coreset(small, C.SEGMENTATION, 0.5)
+        dt = time.perf_counter() - t0
+        out["cpu_baseline"] = {"value": small.size / dt, "unit": "vertices/s", "cores": 1, "kind": "oracle",
+                               "sample": f"2 frames x 32^3 crop of the same volume, {dt:.1f} s"}
+    del keys, cs, coords, vals, flush
+    return out
+
+
 def run_ours(args, rank, local_rank, world):
     import numpy as np
     import torch
@@ -471,13 +520,16 @@ def run_ours(args, rank, local_rank, world):
         torch.cuda.empty_cache()
     encoders = paper_encoder_compare(fh, torch, W, max(3, min(K, 10))) if not args.no_train else None
     torch.cuda.empty_cache()
+    hbm_peak, peak_src = load_peaks()
+    coreset = coreset_bench(fh, torch, W, max(3, min(K, 10)), hbm_peak,
+                            with_cpu=(rank == 0 and not args.no_cpu_baseline)) if not args.no_train else None
+    torch.cuda.empty_cache()
 
     if rank != 0:
         if dist:
             dist.destroy_process_group()
         return
 
-    hbm_peak, peak_src = load_peaks()
     mb = microbench_roofline(fh, torch, enc, cfg, N, stream, hbm_peak)
     # Contract roofline of the dominant kernel: algorithmic bytes / launch time.
     LF4 = cfg.L * cfg.F * 4
@@ -509,7 +561,7 @@ def run_ours(args, rank, local_rank, world):
         "kernels_ms": {"zero_grad": zero_ms, "encode_fwd": fwd_ms, "encode_bwd": bwd_ms, "step": step_ms},
         "roofline": roofline, "gather_roofline": gather_roofline, "cpu_baseline": cpu, "e2e": e2e,
         "gpu_launches": 2 * K, "clocks": clk.summary(), "train_step": train,
-        "paper_encoders": encoders,
+        "paper_encoders": encoders, "coreset": coreset,
     }
     print(json.dumps(line), flush=True)
     if dist:

@@ -36,6 +36,8 @@ EXPORTS = [
     "fh_train_step", "fh_trainer_status", "fh_trainer_step_count", "fh_trainer_destroy", "fh_train_apply_sharded",
     # inference (renderer's model evaluation) and the ARM pace rule
     "fh_infer_workspace_size", "fh_infer", "fh_arm_pace",
+    # include/fhash_coreset.h (NEXT-4 coreset selection)
+    "fh_coreset_workspace_size", "fh_occupancy_words", "fh_morton_cell", "fh_coreset_build", "fh_coreset_emit",
     # include/fhash_data.h (synthetic data, harness)
     "fh_data_gaussian_blobs", "fh_data_value_noise", "fh_data_normalize", "fh_data_sample_voxels",
 ]
@@ -546,3 +548,86 @@ class SpatialOrder:
         _check(lib().fh_spatial_sort(self.enc.handle, _ptr(coords), N, _ptr(self.order), _ptr(self.ws), self.ws.numel(),
                                      _stream(stream)))
         return self.order[:N]
+
+
+# ------------------------------------------------------------ NEXT-4 coreset
+FH_FEAT_INTERVAL, FH_FEAT_ISOSURFACE, FH_FEAT_SEGMENTATION = 0, 1, 2
+
+
+class FeatureSpec(ctypes.Structure):
+    _fields_ = [("kind", ctypes.c_int), ("p0", ctypes.c_float), ("p1", ctypes.c_float)]
+
+
+def _coreset_lib():
+    L = lib()
+    if getattr(L, "_coreset_ready", False):
+        return L
+    vp, u32p, i64 = ctypes.c_void_p, ctypes.POINTER(ctypes.c_uint32), ctypes.c_int64
+    L.fh_coreset_workspace_size.argtypes = [u32p, ctypes.c_int]
+    L.fh_coreset_workspace_size.restype = ctypes.c_size_t
+    L.fh_occupancy_words.argtypes = [u32p]
+    L.fh_occupancy_words.restype = ctypes.c_uint64
+    L.fh_morton_cell.argtypes = [u32p, ctypes.c_uint32, ctypes.c_uint32, ctypes.c_uint32]
+    L.fh_morton_cell.restype = ctypes.c_uint64
+    L.fh_coreset_build.argtypes = [vp, u32p, ctypes.c_int, ctypes.POINTER(FeatureSpec), vp, ctypes.c_size_t, vp,
+                                   vp, vp, vp]
+    L.fh_coreset_build.restype = ctypes.c_int
+    L.fh_coreset_emit.argtypes = [vp, u32p, ctypes.c_int, vp, ctypes.c_size_t, vp, vp, ctypes.c_uint64, vp]
+    L.fh_coreset_emit.restype = ctypes.c_int
+    L._coreset_ready = True
+    return L
+
+
+def occupancy_words(dims_xyz) -> int:
+    return int(_coreset_lib().fh_occupancy_words((ctypes.c_uint32 * 3)(*dims_xyz)))
+
+
+def morton_cell(dims_xyz, x: int, y: int, z: int) -> int:
+    return int(_coreset_lib().fh_morton_cell((ctypes.c_uint32 * 3)(*dims_xyz), x, y, z))
+
+
+class Coreset:
+    """NEXT-4: feature-based coreset selection (fh_coreset_build / _emit) on
+    the key frames vol [n][Z][Y][X] float32 (a CUDA tensor).  build() is
+    stream-ordered; .count / .fbb synchronise to read the results."""
+
+    def __init__(self, vol, kind: int, p0: float, p1: float = 0.0, occupancy: bool = True, stream=None):
+        import torch
+        n, Z, Y, X = vol.shape
+        self.vol, self.n = vol, n
+        self.dims = (ctypes.c_uint32 * 3)(X, Y, Z)
+        L = _coreset_lib()
+        ws = int(L.fh_coreset_workspace_size(self.dims, n))
+        if ws == 0:
+            raise FHashError(FH_E_RANGE, "coreset: volume too large or degenerate")
+        dev = vol.device
+        self.workspace = torch.empty(ws, dtype=torch.uint8, device=dev)
+        self.fbb_dev = torch.empty(6, dtype=torch.int32, device=dev)
+        self.count_dev = torch.zeros(1, dtype=torch.int64, device=dev)
+        self.words = int(L.fh_occupancy_words(self.dims))
+        self.occupancy = torch.empty((n, self.words), dtype=torch.int32, device=dev) if occupancy else None
+        self.spec = FeatureSpec(kind, p0, p1)
+        _check(L.fh_coreset_build(_ptr(vol), self.dims, n, ctypes.byref(self.spec), _ptr(self.workspace), ws,
+                                  _ptr(self.occupancy), _ptr(self.fbb_dev), _ptr(self.count_dev), _stream(stream)))
+
+    @property
+    def count(self) -> int:
+        return int(self.count_dev.item())
+
+    @property
+    def fbb(self):
+        f = self.fbb_dev.cpu().tolist()
+        return None if f[0] == 2 ** 31 - 1 else (tuple(f[:3]), tuple(f[3:]))
+
+    def emit(self, coords=None, values=None, stream=None):
+        import torch
+        M = self.count
+        if coords is None:
+            coords = torch.empty((max(M, 1), 4), dtype=torch.float32, device=self.vol.device)
+        if values is None:
+            values = torch.empty((max(M, 1),), dtype=torch.float32, device=self.vol.device)
+        cap = min(coords.shape[0], values.shape[0])
+        _check(_coreset_lib().fh_coreset_emit(_ptr(self.vol), self.dims, self.n, _ptr(self.workspace),
+                                              self.workspace.numel(), _ptr(coords), _ptr(values), cap,
+                                              _stream(stream)))
+        return coords[:M], values[:M]

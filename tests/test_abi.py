@@ -5,6 +5,7 @@ import ctypes
 import os
 import re
 
+import numpy as np
 import pytest
 
 import oracle
@@ -139,3 +140,24 @@ def test_build_levels_lin_brick_info_and_errors():
     with pytest.raises(fh.FHashError) as e:
         fh.Encoder(cfg.levels, 2, lin=7)
     assert e.value.status == fh.FH_E_ARG
+
+
+def test_coreset_host_helpers_match_oracle():
+    """NEXT-4 host helpers: fh_morton_cell equals the oracle's R24 interleave
+    on cubic and rectangular grids; fh_occupancy_words = 2^(sum b_a) bits in
+    words; workspace sizing rejects degenerate / oversized volumes."""
+    from oracle import coreset as C
+    for dims in [(33, 33, 33), (6, 4, 3), (641, 257, 257), (2, 2, 2), (9, 130, 5)]:
+        cells = [d - 1 for d in dims]
+        bits = C.morton_bits(cells)
+        g = np.random.default_rng(sum(dims))
+        for _ in range(200):
+            x, y, z = (int(g.integers(0, c)) for c in cells)
+            assert fh.morton_cell(dims, x, y, z) == C.morton_encode(x, y, z, bits)
+        assert fh.occupancy_words(dims) == ((1 << sum(bits)) + 31) // 32
+        assert fh.morton_cell(dims, cells[0], 0, 0) == 2 ** 64 - 1
+    L = fh._coreset_lib()
+    dims = (ctypes.c_uint32 * 3)(1, 4, 4)
+    assert L.fh_coreset_workspace_size(dims, 2) == 0
+    dims = (ctypes.c_uint32 * 3)(2048, 2048, 1024)
+    assert L.fh_coreset_workspace_size(dims, 1) == 0
