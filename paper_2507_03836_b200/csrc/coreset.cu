@@ -54,6 +54,7 @@ struct Morton {
     uint8_t bit[64];
     uint8_t lo_off[32][3];   // cell offsets of the 32 codes of one word (low 5 code bits)
     int nrows;               // distinct (dy, dz) among them
+    bool std5;               // low 5 code bits are x0 y0 z0 x1 y1 (every axis has >= 2 bits)
     uint8_t row_dy[32], row_dz[32], row_of[32];
 };
 
@@ -76,6 +77,7 @@ static Morton make_morton(uint32_t X, uint32_t Y, uint32_t Z) {
                 pos++;
             }
     m.nbits = pos;
+    m.std5 = m.bits[0] >= 2 && m.bits[1] >= 2 && m.bits[2] >= 2;
     m.nrows = 0;
     for (int i = 0; i < 32; i++) {
         m.lo_off[i][0] = m.lo_off[i][1] = m.lo_off[i][2] = 0;
@@ -146,49 +148,50 @@ __device__ __forceinline__ bool feature_test(float v, const fh_feature_spec &s) 
     return fabs((double)v - (double)s.p0) <= (double)s.p1;  // exact: fp32 operands
 }
 
-constexpr int kFeatUnroll = 4;   // words (independent 128-byte loads) in flight per warp
+constexpr int kFeatUnroll = 8;   // words (independent 128-byte loads) in flight per warp
 
+// Warp per vertex ROW (grid-stride over the n Z Y rows): the row's
+// (frame, z, y) is derived once, then lane i tests vertex 32 w + i of each
+// word w of the row, kFeatUnroll loads in flight; the ballot is the word.
 __global__ void __launch_bounds__(kThreads) feature_kernel(const float *__restrict__ vol, Dims d, fh_feature_spec s,
                                                           const uint32_t *__restrict__ sbits,
                                                           uint32_t *__restrict__ f) {
-    const uint32_t total = (uint32_t)d.n * d.Z * d.Y * d.Wx;   // < 2^32 (make_dims)
+    const uint32_t rows = (uint32_t)d.n * d.Z * d.Y;   // < 2^32 (make_dims)
     const int lane = threadIdx.x & 31;
     const uint32_t G = (gridDim.x * kThreads) >> 5;   // warps in the grid
-    for (uint32_t g0 = (blockIdx.x * kThreads + threadIdx.x) >> 5; g0 < total; g0 += G * kFeatUnroll) {
-        float v[kFeatUnroll];
-        bool ok[kFeatUnroll];
+    for (uint32_t row = (blockIdx.x * kThreads + threadIdx.x) >> 5; row < rows; row += G) {
+        const float *r = vol + (uint64_t)row * d.X;   // rows of [n][Z][Y][X] are contiguous
+        uint32_t *frow = f + (uint64_t)row * d.Wx;
+        const uint32_t y = row % d.Y, z = (row / d.Y) % d.Z, k = row / (d.Y * d.Z);
+        for (uint32_t w0 = 0; w0 < d.Wx; w0 += kFeatUnroll) {
+            float v[kFeatUnroll];
 #pragma unroll
-        for (int u = 0; u < kFeatUnroll; u++) {
-            const uint32_t g = g0 + u * G;
-            const uint32_t row = g / d.Wx;
-            const uint32_t x = (g - row * d.Wx) * 32 + lane;
-            ok[u] = g < total && x < d.X;
-            v[u] = ok[u] ? __ldg(vol + (uint64_t)row * d.X + x) : 0.f;   // rows of [n][Z][Y][X] are contiguous
-        }
+            for (int u = 0; u < kFeatUnroll; u++) {
+                const uint32_t x = (w0 + u) * 32 + lane;
+                v[u] = x < d.X ? __ldg(r + x) : 0.f;
+            }
 #pragma unroll
-        for (int u = 0; u < kFeatUnroll; u++) {
-            const uint32_t g = g0 + u * G;
-            uint32_t bits = __ballot_sync(0xffffffffu, ok[u] && feature_test(v[u], s));
-            if (lane == 0 && g < total) {
-                const uint32_t row = g / d.Wx;
-                const uint32_t w = g - row * d.Wx;
-                if (s.kind == FH_FEAT_ISOSURFACE) {
-                    // corners of straddling cells: vertex (x, y, z) is a corner of
-                    // the cells (x-1..x, y-1..y, z-1..z); cell x -> vertices x, x+1
-                    const uint32_t y = row % d.Y, z = (row / d.Y) % d.Z;
-                    const uint32_t k = row / (d.Y * d.Z);
-                    for (int dz = 0; dz < 2; dz++)
-                        for (int dy = 0; dy < 2; dy++) {
-                            const int cy = (int)y - dy, cz = (int)z - dz;
-                            if (cy < 0 || cz < 0 || cy >= (int)d.Y - 1 || cz >= (int)d.Z - 1) continue;
-                            const uint32_t *sr = sbits + ((k * (d.Z - 1) + cz) * (d.Y - 1) + cy) * d.Wc;
-                            const uint32_t cw = w < d.Wc ? sr[w] : 0u;
-                            const uint32_t cprev = w > 0 ? sr[w - 1] : 0u;
-                            bits |= cw | (cw << 1) | (cprev >> 31);
-                        }
-                    bits &= last_word_mask(d.X, w, d.Wx);
+            for (int u = 0; u < kFeatUnroll; u++) {
+                const uint32_t w = w0 + u;
+                if (w >= d.Wx) break;   // warp-uniform
+                uint32_t bits = __ballot_sync(0xffffffffu, (w * 32 + lane < d.X) && feature_test(v[u], s));
+                if (lane == 0) {
+                    if (s.kind == FH_FEAT_ISOSURFACE) {
+                        // corners of straddling cells: vertex (x, y, z) is a corner of
+                        // the cells (x-1..x, y-1..y, z-1..z); cell x -> vertices x, x+1
+                        for (int dz = 0; dz < 2; dz++)
+                            for (int dy = 0; dy < 2; dy++) {
+                                const int cy = (int)y - dy, cz = (int)z - dz;
+                                if (cy < 0 || cz < 0 || cy >= (int)d.Y - 1 || cz >= (int)d.Z - 1) continue;
+                                const uint32_t *sr = sbits + ((k * (d.Z - 1) + cz) * (d.Y - 1) + cy) * d.Wc;
+                                const uint32_t cw = w < d.Wc ? sr[w] : 0u;
+                                const uint32_t cprev = w > 0 ? sr[w - 1] : 0u;
+                                bits |= cw | (cw << 1) | (cprev >> 31);
+                            }
+                        bits &= last_word_mask(d.X, w, d.Wx);
+                    }
+                    frow[w] = bits;
                 }
-                f[g] = bits;
             }
         }
     }
@@ -321,7 +324,21 @@ __global__ void __launch_bounds__(kThreads) occupancy_kernel(const uint32_t *__r
         const uint32_t *fr = cm + k * (uint64_t)(d.Z - 1) * (d.Y - 1) * d.Wc;
         const int ncodes = 1 << (m.nbits < 5 ? m.nbits : 5);
         uint32_t word = 0;
-        if (m.nrows <= 8) {
+        if (m.std5) {
+            // low code bits (x0, y0, z0, x1, y1): row (y, z) contributes the 4 x
+            // bits (base x .. base x + 3) at code positions off(y, z) + {0, 1, 8, 9}
+#pragma unroll
+            for (int zz = 0; zz < 2; zz++)
+#pragma unroll
+                for (int yy = 0; yy < 4; yy++) {
+                    const uint32_t cy = base[1] + yy, cz = base[2] + zz;
+                    if (cy >= d.Y - 1 || cz >= d.Z - 1 || base[0] >= d.X - 1) continue;
+                    const uint32_t rw = __ldg(fr + ((uint64_t)cz * (d.Y - 1) + cy) * d.Wc + (base[0] >> 5));
+                    const uint32_t nib = (rw >> (base[0] & 31)) & 0xFu;   // bits past the grid are 0
+                    const uint32_t spread = (nib & 3u) | ((nib & 12u) << 6);
+                    word |= spread << ((yy & 1) * 2 + zz * 4 + (yy >> 1) * 16);
+                }
+        } else if (m.nrows <= 8) {
             uint32_t rows[8];
 #pragma unroll
             for (int r = 0; r < 8; r++) {
@@ -574,7 +591,7 @@ fh_status fh_coreset_build(const float *vol, const uint32_t dims_xyz[3], int n_f
     uint32_t *offs = reinterpret_cast<uint32_t *>(w + L.offs);
     if (spec->kind == FH_FEAT_ISOSURFACE)
         straddle_kernel<<<grid_for(32 * L.swords), kThreads, 0, s>>>(vol, d, spec->p0, sb);
-    feature_kernel<<<grid_for(32 * L.words), kThreads, 0, s>>>(vol, d, *spec, sb, f);
+    feature_kernel<<<grid_for(32ull * d.n * d.Z * d.Y), kThreads, 0, s>>>(vol, d, *spec, sb, f);
     init_boxes_kernel<<<(6 * n_frames + 255) / 256, 256, 0, s>>>(boxes, n_frames);
     dilate_kernel<<<(unsigned)L.nchunks, kThreads, 0, s>>>(f, d, dm, boxes, counts);
     if (occupancy) {
