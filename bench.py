@@ -481,21 +481,41 @@ def run_ours(args, rank, local_rank, world):
     value = N * world * K / total_s
 
     # e2e: the same step through the C ABI from pinned HOST buffers, copies
-    # inside the timed region (fh_encode_step_host).
+    # inside the timed region (fh_encode_step_host: H2D of the step's coords and
+    # dout, zero dtable, fwd, bwd, D2H of out and dtable).  Steps alternate
+    # between two streams with two device / host-output buffer sets, so step
+    # k+1's H2D overlaps step k's kernels and D2H (PCIe is full duplex); every
+    # step's copies stay inside the timed region.
     coords_h = torch.from_numpy(case.coords).pin_memory()
     dout_h = torch.from_numpy(case.dout).pin_memory()
-    out_h = torch.empty((N, cfg.L * cfg.F)).pin_memory()
-    dtable_h = torch.empty((enc.entries, cfg.F)).pin_memory()
-    ke = max(3, min(K, 10))
-    for _ in range(2):
-        enc.step_host(coords_h, dout_h, table, coords, dout, out, dtable, out_h, dtable_h, stream)
+    streams = [torch.cuda.Stream(), torch.cuda.Stream()]
+    sets = [dict(c=coords, g=dout, o=out, dt=dtable)]
+    sets.append(dict(c=torch.empty_like(coords), g=torch.empty_like(dout), o=torch.empty_like(out),
+                     dt=torch.empty_like(dtable)))
+    for b in sets:
+        b["oh"] = torch.empty((N, cfg.L * cfg.F)).pin_memory()
+        b["dth"] = torch.empty((enc.entries, cfg.F)).pin_memory()
+
+    def e2e_step(k):
+        b, st = sets[k % 2], streams[k % 2]
+        enc.step_host(coords_h, dout_h, table, b["c"], b["g"], b["o"], b["dt"], b["oh"], b["dth"], st)
+
+    ke = max(4, min(K, 10))
+    for k in range(4):
+        e2e_step(k)
     if dist:
         dist.barrier()
     torch.cuda.synchronize()
     e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
     e0.record(stream)
-    for _ in range(ke):
-        enc.step_host(coords_h, dout_h, table, coords, dout, out, dtable, out_h, dtable_h, stream)
+    for st in streams:
+        st.wait_event(e0)
+    for k in range(ke):
+        e2e_step(k)
+    for st in streams:
+        j = torch.cuda.Event()
+        j.record(st)
+        stream.wait_event(j)
     e1.record(stream)
     torch.cuda.synchronize()
     e2e_s = e0.elapsed_time(e1) / 1e3
@@ -503,14 +523,16 @@ def run_ours(args, rank, local_rank, world):
         t = torch.tensor([e2e_s], device="cuda", dtype=torch.float64)
         dist.all_reduce(t, op=dist.ReduceOp.MAX)
         e2e_s = float(t.item())
+    if not torch.equal(sets[0]["oh"], sets[1]["oh"]):   # same inputs -> identical forward output
+        raise RuntimeError("e2e: the two pipelined buffer sets disagree")
     e2e = {"value": N * world * ke / e2e_s, "unit": UNIT, "h2d_bytes_per_step": N * 16 + N * cfg.L * cfg.F * 4,
            "d2h_bytes_per_step": N * cfg.L * cfg.F * 4 + enc.entries * cfg.F * 4, "steps": ke,
-           "api": "fh_encode_step_host (pinned host in/out)"}
+           "api": "fh_encode_step_host (pinned host in/out), steps alternating over two streams / buffer sets"}
 
     # Train step (all §8(a) rows): free the encode buffers first.
     train = {}
     if not args.no_train:
-        del coords_h, dout_h, out_h, dtable_h, out, dout, dtable, flush
+        del coords_h, dout_h, sets, out, dout, dtable, flush
         torch.cuda.empty_cache()
         kt = max(3, min(K, 10))
         if world == 1:

@@ -238,6 +238,9 @@ fh_status fh_encode_fwd_bwd(fh_encoder enc, const float *coords, int64_t N, cons
  * caller's device buffers coords_d / dout_d, zeroes dtable_d, runs
  * fh_encode_fwd (out_d, f32) and fh_encode_bwd, and copies out_d -> out_h
  * and dtable_d -> dtable_h.  All on `stream`; returns without waiting.
+ * Stream-ordered, so a caller pipelines consecutive steps by alternating two
+ * streams with two sets of device buffers and host outputs: step k+1's H2D
+ * then overlaps step k's kernels and D2H (bench.py's e2e does this).
  * Errors: as the calls it makes. */
 fh_status fh_encode_step_host(fh_encoder enc, const float *coords_h, const float *dout_h,
                               int64_t N, const void *table_d, float *coords_d, float *dout_d,
