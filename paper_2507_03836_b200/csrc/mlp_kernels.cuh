@@ -579,8 +579,8 @@ __device__ __forceinline__ void adam_one(const AdamArgs &A, const AdamSeg &s, in
     s.m[i] = m; s.v[i] = v; s.p[i] = p; s.g[i] = 0.f;
     if constexpr (sizeof(S) == 2) {
         if (s.kind == 1) reinterpret_cast<__half *>(s.shadow)[i] = __float2half_rn(p);
-        else reinterpret_cast<__nv_bfloat16 *>(s.shadow)[i] = __float2bfloat16_rn(p);
-    }
+        else if (s.kind == 2) reinterpret_cast<__nv_bfloat16 *>(s.shadow)[i] = __float2bfloat16_rn(p);
+    }   // kind 0: fp32 master only (FH_F32 tables are read directly), no shadow
 }
 
 __global__ void __launch_bounds__(256) adam_kernel(const AdamArgs A) {
@@ -613,7 +613,7 @@ __global__ void __launch_bounds__(256) adam_kernel(const AdamArgs A) {
             u.x = *reinterpret_cast<uint32_t *>(&h0);
             u.y = *reinterpret_cast<uint32_t *>(&h1);
             reinterpret_cast<uint2 *>(s.shadow)[q] = u;
-        } else {
+        } else if (s.kind == 2) {
             __nv_bfloat162 h0 = __floats2bfloat162_rn(pp[0], pp[1]), h1 = __floats2bfloat162_rn(pp[2], pp[3]);
             uint2 u;
             u.x = *reinterpret_cast<uint32_t *>(&h0);

@@ -119,6 +119,28 @@ def test_adam_parity_and_shadows():
     assert not torch.equal(p0[0], tr.table_master)
 
 
+def test_fp32_table_training_adam():
+    """FH_F32 tables (no fp16 shadow: the kernels read the fp32 master
+    directly): a full train step runs, Adam matches the oracle on every table
+    parameter and writes no shadow."""
+    cfg = small_cfg(2, 8, tdt="f32")
+    enc, tr, coords, target = make(cfg, 900, seed=21)
+    assert tr.table_shadow is None
+    c, t = torch.from_numpy(coords).cuda(), torch.from_numpy(target).cuda()
+    loss = tr.fwd_bwd(c, t)
+    assert tr.status() == fh.FH_OK and torch.isfinite(loss).all()
+    g = tr.grads.clone().cpu().numpy().astype(np.float64)
+    before = [x.clone().cpu().numpy().astype(np.float64) for x in (tr.table_master, tr.table_m, tr.table_v)]
+    tr.apply()
+    torch.cuda.synchronize()
+    rp, _, _ = T.adam_step(before[0].ravel(), g[:tr.n_table], before[1], before[2], 1)
+    gp = tr.table_master.cpu().numpy().ravel().astype(np.float64)
+    assert np.all(np.abs(gp - rp) <= 1e-6 * (np.abs(rp) + 0.01))
+    assert torch.all(tr.grads == 0)
+    loss2 = tr.step(c, t)   # the next step reads the updated fp32 master
+    assert tr.status() == fh.FH_OK and torch.isfinite(loss2).all()
+
+
 def test_sharded_apply_matches_full_apply():
     """fh_train_apply_sharded over [0, n) equals fh_train_apply; over a
     sub-range it touches only that range of the table state."""
