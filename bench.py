@@ -243,10 +243,18 @@ def train_step_bench(fh, torch, W, which, rank, world, dist, steps, warmup):
     coords = torch.empty((n_local, 4), device="cuda")
     target = torch.empty((n_local,), device="cuda")
     stream = torch.cuda.current_stream()
-    # world > 1: reduce-scatter of the table grads + all-reduce of the MLP
-    # grads (NCCL over NVLink/NVSwitch), Adam on this rank's 1/W shard,
-    # all-gather of the fp16 table shadow (dp.ShardedDP).
-    sdp = dp.ShardedDP(tr) if world > 1 else None
+    # world > 1: per-backward-launch reduce-scatter of the table grads on a
+    # communication stream, overlapped with the rest of the backward
+    # (dp.OverlappedShardedDP; NCCL over NVLink/NVSwitch), all-reduce of the
+    # tails + MLP grads, Adam on this rank's chunks, all-gather of the fp16
+    # table shadow.  Falls back to dp.ShardedDP (no overlap) if the plan
+    # needs more than 63 Adam ranges.
+    sdp = None
+    if world > 1:
+        try:
+            sdp = dp.OverlappedShardedDP(tr)
+        except ValueError:
+            sdp = dp.ShardedDP(tr)
 
     def one(k, ev=None):
         if ev: ev[0].record(stream)
@@ -254,13 +262,16 @@ def train_step_bench(fh, torch, W, which, rank, world, dist, steps, warmup):
         if ev: ev[1].record(stream)
         loss = tr.fwd_bwd(coords, target, n_global)
         if ev: ev[2].record(stream)
-        if sdp:
+        if isinstance(sdp, dp.OverlappedShardedDP):
+            if ev: ev[3].record(stream)   # the reduction already overlaps the backward
+            sdp.reduce_and_apply()
+        elif sdp:
             sdp.reduce()
-        if ev: ev[3].record(stream)
-        if sdp:
+            if ev: ev[3].record(stream)
             sdp.apply()
             sdp.gather()
         else:
+            if ev: ev[3].record(stream)
             tr.apply()
         if ev: ev[4].record(stream)
         return loss
@@ -309,7 +320,9 @@ def train_step_bench(fh, torch, W, which, rank, world, dist, steps, warmup):
         "scaling": "strong" if which == "cfg5" else "weak",
         "phase_ms": {"sample": phase[0], "fwd_bwd": phase[1], "grad_reduce": phase[2],
                      "adam_and_gather": phase[3]},
-        "dp": "reduce-scatter + sharded Adam + all-gather (NCCL)" if world > 1 else "single GPU",
+        "dp": ("per-backward-launch reduce-scatter overlapped with the backward + sharded Adam + all-gather (NCCL)"
+               if isinstance(sdp, dp.OverlappedShardedDP) else
+               "reduce-scatter + sharded Adam + all-gather (NCCL)" if world > 1 else "single GPU"),
         "infer": {"what": "fh_infer: encode fwd + tcgen05 MLP forward (Alg. 1 V = model(S))",
                   "ms": infer_ms, "samples_per_s": n_local / (infer_ms / 1e3)},
         "loss_first_warmup": losses[0], "loss_last": float(last.item()), "status": int(st),

@@ -334,6 +334,30 @@ fh_status fh_train_apply(fh_trainer tr, fh_stream stream);
 fh_status fh_train_apply_sharded(fh_trainer tr, int64_t begin, int64_t end, const float *grad_shard,
                                  fh_stream stream);
 
+/* ---- overlapping the gradient reduction with the backward
+ * The encode backward of fh_train_fwd_bwd runs as a few launches (the
+ * shared-memory pass over the tiny levels, then level groups sized to the
+ * L2); once launch i has run, the table gradients of its ranges are final,
+ * so a data-parallel caller can reduce them while later launches run.
+ * fh_train_bwd_launches: number of backward launches (-1 on error).
+ * fh_train_bwd_ranges: the flat table element ranges [r[2k], r[2k+1]) that
+ *   launch i finalises (k < *n_ranges); FH_E_RANGE if more than max_ranges.
+ * fh_train_set_bwd_events: from now on fh_train_fwd_bwd records events[i]
+ *   (caller-owned cudaEvent_t, created by the caller) on its stream right
+ *   after backward launch i; n = fh_train_bwd_launches, or 0 to stop.
+ * fh_train_apply_ranges: one Adam step (step counter += 1) over the table
+ *   element ranges [begin_i, end_i) (disjoint) reading grad_i[0 .. end_i -
+ *   begin_i) (device f32, e.g. this rank's reduce-scattered chunks), plus the
+ *   whole MLP segment from the trainer's mlp_grad; rewrites the shadows of
+ *   those ranges and zeroes the trainer's table_grad and mlp_grad.  At most
+ *   63 ranges; ranges whose pointers are not 16-byte aligned take a scalar
+ *   path.  Errors: FH_E_ARG. */
+int       fh_train_bwd_launches(fh_trainer tr);
+fh_status fh_train_bwd_ranges(fh_trainer tr, int launch, int64_t *ranges, int max_ranges, int *n_ranges);
+fh_status fh_train_set_bwd_events(fh_trainer tr, void *const *events, int n);
+fh_status fh_train_apply_ranges(fh_trainer tr, int n, const int64_t *begin, const int64_t *end,
+                                const float *const *grad, fh_stream stream);
+
 /* fh_train_fwd_bwd + fh_train_apply (single GPU). */
 fh_status fh_train_step(fh_trainer tr, const float *coords, const float *target, int64_t N_local,
                         int64_t N_global, float *loss_dev, fh_stream stream);

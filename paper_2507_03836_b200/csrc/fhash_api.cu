@@ -558,7 +558,8 @@ static fh_status encode_fwd_impl(fh_encoder e, const float *coords, int64_t N, c
 }
 
 static fh_status encode_bwd_impl(fh_encoder e, const float *coords, int64_t N, const uint32_t *perm,
-                                 const float *dout, float *dtable, fh_stream stream) {
+                                 const float *dout, float *dtable, fh_stream stream,
+                                 cudaEvent_t *ev = nullptr, int n_ev = 0) {
     g_err[0] = 0;
     fh_status st = check_common(e, coords, N, "fh_encode_bwd");
     if (st != FH_OK) return st;
@@ -598,7 +599,9 @@ static fh_status encode_bwd_impl(fh_encoder e, const float *coords, int64_t N, c
             default: FH_SMALL(8)
 #undef FH_SMALL
         }
+        if (ev && n_ev > 0) cudaEventRecord(ev[0], s);
     }
+    const int ev0 = e->small.n > 0 ? 1 : 0;
     for (int k = 0; k < e->n_gb; k++) {
         const int l0 = e->gb[2 * k], lc = e->gb[2 * k + 1] - e->gb[2 * k];
         const dim3 g = grid_for(N, lc);
@@ -620,9 +623,44 @@ static fh_status encode_bwd_impl(fh_encoder e, const float *coords, int64_t N, c
             case 4: fh::bwd_kernel<4><<<g, 256, 0, s>>>(e->params, c4, N, dout, dtable, e->flag, ll, nullptr); break;
             default: fh::bwd_kernel<8><<<g, 256, 0, s>>>(e->params, c4, N, dout, dtable, e->flag, ll, nullptr); break;
         }
+        if (ev && ev0 + k < n_ev) cudaEventRecord(ev[ev0 + k], s);
     }
     return cuda_check(cudaGetLastError(), "fh_encode_bwd launch");
 }
+
+namespace fh {
+// Backward launches of fh_encode_bwd (natural order) and the table element
+// ranges each one finalises -- for callers that overlap the gradient
+// reduction with the rest of the backward (train_api.cu).
+int bwd_launch_count(fh_encoder e) {
+    if (!e || ensure_flag(e) != FH_OK) return -1;
+    return (e->small.n > 0 ? 1 : 0) + e->n_gb;
+}
+int bwd_launch_ranges(fh_encoder e, int i, int64_t *r, int max) {
+    const int cnt = bwd_launch_count(e);
+    if (i < 0 || i >= cnt) return -1;
+    const int64_t F = e->F;
+    int k = 0;
+    if (e->small.n > 0) {
+        if (i == 0) {
+            for (int j = 0; j < e->small.n; j++) {
+                const fh_level_info &I = e->info[e->small.id[j]];
+                if (k < max) { r[2 * k] = (int64_t)I.offset * F; r[2 * k + 1] = (int64_t)(I.offset + I.table_size) * F; }
+                k++;
+            }
+            return k;
+        }
+        i -= 1;
+    }
+    const fh_level_info &a = e->info[e->gb[2 * i]], &b = e->info[e->gb[2 * i + 1] - 1];
+    if (max > 0) { r[0] = (int64_t)a.offset * F; r[1] = (int64_t)(b.offset + b.table_size) * F; }
+    return 1;
+}
+fh_status encode_bwd_events(fh_encoder e, const float *coords, int64_t N, const float *dout, float *dtable,
+                            fh_stream stream, cudaEvent_t *ev, int n_ev) {
+    return encode_bwd_impl(e, coords, N, nullptr, dout, dtable, stream, ev, n_ev);
+}
+}  // namespace fh
 
 extern "C" {
 

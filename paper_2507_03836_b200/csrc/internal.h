@@ -30,6 +30,12 @@ inline fh_status cuda_check(cudaError_t e, const char *what) {
 inline bool aligned(const void *p, size_t a) { return (reinterpret_cast<uintptr_t>(p) % a) == 0; }
 inline size_t dtype_size(fh_dtype d) { return d == FH_F32 ? 4 : 2; }
 
+// fhash_api.cu: backward launches and the gradient ranges they finalise.
+int bwd_launch_count(fh_encoder e);
+int bwd_launch_ranges(fh_encoder e, int launch, int64_t *ranges, int max);
+fh_status encode_bwd_events(fh_encoder e, const float *coords, int64_t N, const float *dout, float *dtable,
+                            fh_stream stream, cudaEvent_t *ev, int n_ev);
+
 }  // namespace fh
 
 struct fh_encoder_s {

@@ -558,37 +558,46 @@ __global__ void __launch_bounds__(256, 1) mlp_infer_kernel(const InferArgs a) {
 // then writes the low-precision shadow (fp16 table / bf16 MLP) and zeroes g.
 struct AdamSeg {
     float *p, *g, *m, *v;
-    void *shadow;        // __half* (kind 1) or __nv_bfloat16* (kind 2)
+    void *shadow;        // __half* (kind 1), __nv_bfloat16* (kind 2), unused (kind 0)
     int64_t n;
     int kind;
+    int vec;             // 1: p, g, m, v 16-byte and shadow 8-byte aligned -> float4 path
 };
 
+// Up to kMaxAdamSeg segments per launch (table ranges + the MLP); segment i
+// owns blocks [block0[i], block0[i+1]).
+constexpr int kMaxAdamSeg = 64;
+
 struct AdamArgs {
-    AdamSeg seg[2];
-    int64_t blocks0;     // blocks assigned to segment 0
+    AdamSeg seg[kMaxAdamSeg];
+    int64_t block0[kMaxAdamSeg + 1];
+    int nseg;
     float lr, b1, b2, eps, c1, c2;
     float omb1, omb2;    // 1 - beta, rounded once from double (fp32 1.f - 0.999f is 5e-5 off)
 };
 
-template <typename S>
 __device__ __forceinline__ void adam_one(const AdamArgs &A, const AdamSeg &s, int64_t i) {
     const float g = s.g[i];
     const float m = fmaf(A.b1, s.m[i], A.omb1 * g);
     const float v = fmaf(A.b2, s.v[i], A.omb2 * g * g);
     const float p = s.p[i] - A.lr * (m * A.c1) / (sqrtf(v * A.c2) + A.eps);
     s.m[i] = m; s.v[i] = v; s.p[i] = p; s.g[i] = 0.f;
-    if constexpr (sizeof(S) == 2) {
-        if (s.kind == 1) reinterpret_cast<__half *>(s.shadow)[i] = __float2half_rn(p);
-        else if (s.kind == 2) reinterpret_cast<__nv_bfloat16 *>(s.shadow)[i] = __float2bfloat16_rn(p);
-    }   // kind 0: fp32 master only (FH_F32 tables are read directly), no shadow
+    if (s.kind == 1) reinterpret_cast<__half *>(s.shadow)[i] = __float2half_rn(p);
+    else if (s.kind == 2) reinterpret_cast<__nv_bfloat16 *>(s.shadow)[i] = __float2bfloat16_rn(p);
+    // kind 0: fp32 master only (FH_F32 tables are read directly), no shadow
 }
 
-__global__ void __launch_bounds__(256) adam_kernel(const AdamArgs A) {
-    const bool second = (int64_t)blockIdx.x >= A.blocks0;
-    const AdamSeg &s = second ? A.seg[1] : A.seg[0];
-    const int64_t b = second ? blockIdx.x - A.blocks0 : blockIdx.x;
-    const int64_t nb = second ? gridDim.x - A.blocks0 : A.blocks0;
-    // 4 elements per thread per iteration, vectorised when aligned
+__global__ void __launch_bounds__(256) adam_kernel(const __grid_constant__ AdamArgs A) {
+    int si = 0;
+    while (si + 1 < A.nseg && (int64_t)blockIdx.x >= A.block0[si + 1]) si++;
+    const AdamSeg &s = A.seg[si];
+    const int64_t b = (int64_t)blockIdx.x - A.block0[si];
+    const int64_t nb = A.block0[si + 1] - A.block0[si];
+    if (!s.vec) {   // unaligned segment (a tail range): scalar
+        for (int64_t i = b * blockDim.x + threadIdx.x; i < s.n; i += nb * blockDim.x) adam_one(A, s, i);
+        return;
+    }
+    // 4 elements per thread per iteration
     const int64_t n4 = s.n / 4;
     for (int64_t q = b * blockDim.x + threadIdx.x; q < n4; q += nb * blockDim.x) {
         float4 g = reinterpret_cast<const float4 *>(s.g)[q];
@@ -623,7 +632,7 @@ __global__ void __launch_bounds__(256) adam_kernel(const AdamArgs A) {
     }
     // tail
     if (b == 0)
-        for (int64_t i = n4 * 4 + threadIdx.x; i < s.n; i += blockDim.x) adam_one<__half>(A, s, i);
+        for (int64_t i = n4 * 4 + threadIdx.x; i < s.n; i += blockDim.x) adam_one(A, s, i);
 }
 
 }  // namespace mlp

@@ -27,6 +27,8 @@ struct fh_trainer_s {
     float *dx = nullptr;               // [max_batch][K0]
     int *flag = nullptr;               // bit 1: non-finite loss
     float *loss_scratch = nullptr;
+    cudaEvent_t bwd_ev[FH_MAX_LEVELS + 1] = {};  // caller's events, recorded after each backward launch
+    int n_bwd_ev = 0;
 };
 
 namespace {
@@ -149,17 +151,48 @@ fh_status fh_train_fwd_bwd(fh_trainer tr, const float *coords, const float *targ
         default: st = launch_mlp<64>(tr, target, N, N_global, loss, s); break;
     }
     if (st != FH_OK) return st;
-    return fh_encode_bwd(tr->enc, coords, N, tr->dx, tr->b.table_grad, stream);
+    return fh::encode_bwd_events(tr->enc, coords, N, tr->dx, tr->b.table_grad, stream, tr->bwd_ev, tr->n_bwd_ev);
+}
+
+int fh_train_bwd_launches(fh_trainer tr) { return tr ? fh::bwd_launch_count(tr->enc) : -1; }
+
+fh_status fh_train_bwd_ranges(fh_trainer tr, int launch, int64_t *ranges, int max_ranges, int *n_ranges) {
+    g_err[0] = 0;
+    if (!tr || !ranges || !n_ranges || max_ranges < 0) return fail(FH_E_ARG, "fh_train_bwd_ranges: NULL argument");
+    const int k = fh::bwd_launch_ranges(tr->enc, launch, ranges, max_ranges);
+    if (k < 0) return fail(FH_E_ARG, "fh_train_bwd_ranges: launch %d out of range", launch);
+    *n_ranges = k;
+    if (k > max_ranges) return fail(FH_E_RANGE, "fh_train_bwd_ranges: %d ranges, capacity %d", k, max_ranges);
+    return FH_OK;
+}
+
+fh_status fh_train_set_bwd_events(fh_trainer tr, void *const *events, int n) {
+    g_err[0] = 0;
+    if (!tr) return fail(FH_E_ARG, "fh_train_set_bwd_events: NULL trainer");
+    const int cnt = fh::bwd_launch_count(tr->enc);
+    if (n != 0 && n != cnt)
+        return fail(FH_E_ARG, "fh_train_set_bwd_events: %d events for %d backward launches", n, cnt);
+    if (n > 0 && !events) return fail(FH_E_ARG, "fh_train_set_bwd_events: NULL events");
+    for (int i = 0; i < n; i++) tr->bwd_ev[i] = reinterpret_cast<cudaEvent_t>(events[i]);
+    tr->n_bwd_ev = n;
+    return FH_OK;
 }
 
 }  // extern "C"
 
-// Adam over table parameters [begin, end) with gradients tgrad (indexed from
-// begin), plus the whole MLP segment.
-static fh_status apply_impl(fh_trainer tr, int64_t begin, int64_t end, float *tgrad, cudaStream_t s) {
+// Adam over the table element ranges [begin_i, end_i) with gradients
+// grad_i (indexed from begin_i), plus the whole MLP segment: ONE launch, one
+// step of the bias-correction counter.
+static fh_status apply_ranges_impl(fh_trainer tr, int n, const int64_t *begin, const int64_t *end,
+                                   float *const *grad, cudaStream_t s) {
+    using fh::mlp::AdamArgs;
+    using fh::mlp::AdamSeg;
+    if (n < 0 || n + 1 > fh::mlp::kMaxAdamSeg)
+        return fail(FH_E_ARG, "Adam: %d table ranges (max %d)", n, fh::mlp::kMaxAdamSeg - 1);
     tr->step += 1;
     const double t = (double)tr->step;
-    fh::mlp::AdamArgs A;
+    AdamArgs A;
+    memset(&A, 0, sizeof(A));
     A.lr = tr->adam.lr;
     A.b1 = tr->adam.beta1;
     A.b2 = tr->adam.beta2;
@@ -168,15 +201,36 @@ static fh_status apply_impl(fh_trainer tr, int64_t begin, int64_t end, float *tg
     A.omb2 = (float)(1.0 - (double)tr->adam.beta2);
     A.c1 = (float)(1.0 / (1.0 - std::pow((double)tr->adam.beta1, t)));
     A.c2 = (float)(1.0 / (1.0 - std::pow((double)tr->adam.beta2, t)));
-    fh::mlp::AdamSeg &T = A.seg[0];
-    T.p = tr->b.table_master + begin;
-    T.g = tgrad;
-    T.m = tr->b.table_m + begin;
-    T.v = tr->b.table_v + begin;
-    T.shadow = tr->b.table_shadow ? reinterpret_cast<__half *>(tr->b.table_shadow) + begin : nullptr;
-    T.n = end - begin;
-    T.kind = tr->b.table_shadow ? 1 : 0;
-    fh::mlp::AdamSeg &M = A.seg[1];
+    const int64_t cap = (int64_t)tr->n_sm * 16;
+    int64_t total_n = 0;
+    for (int i = 0; i < n; i++) total_n += end[i] - begin[i];
+    int64_t blocks = 0;
+    int k = 0;
+    auto add = [&](AdamSeg g, int64_t want) {
+        if (g.n <= 0) return;
+        g.vec = (aligned(g.p, 16) && aligned(g.g, 16) && aligned(g.m, 16) && aligned(g.v, 16) &&
+                 (g.kind == 0 || aligned(g.shadow, 8))) ? 1 : 0;
+        if (want < 1) want = 1;
+        A.seg[k] = g;
+        A.block0[k] = blocks;
+        blocks += want;
+        k++;
+    };
+    for (int i = 0; i < n; i++) {
+        AdamSeg T{};
+        T.p = tr->b.table_master + begin[i];
+        T.g = grad[i];
+        T.m = tr->b.table_m + begin[i];
+        T.v = tr->b.table_v + begin[i];
+        T.shadow = tr->b.table_shadow ? reinterpret_cast<__half *>(tr->b.table_shadow) + begin[i] : nullptr;
+        T.n = end[i] - begin[i];
+        T.kind = tr->b.table_shadow ? 1 : 0;
+        // blocks for ~4 float4 per thread, shared out of the cap in proportion to size
+        int64_t want = (T.n / 4 + 256 * 4 - 1) / (256 * 4);
+        if (total_n > 0 && want > cap * T.n / total_n + 1) want = cap * T.n / total_n + 1;
+        add(T, want);
+    }
+    AdamSeg M{};
     M.p = tr->b.mlp_master;
     M.g = tr->b.mlp_grad;
     M.m = tr->b.mlp_m;
@@ -184,16 +238,16 @@ static fh_status apply_impl(fh_trainer tr, int64_t begin, int64_t end, float *tg
     M.shadow = tr->b.mlp_shadow;
     M.n = fh::mlp::param_count(tr->K0);
     M.kind = 2;
-    // segment 0: enough blocks for ~4 float4 per thread; segment 1: a few blocks
-    const int64_t n4 = T.n / 4;
-    int64_t b0 = (n4 + 256 * 4 - 1) / (256 * 4);
-    const int64_t cap = (int64_t)tr->n_sm * 16;
-    if (b0 > cap) b0 = cap;
-    if (b0 < 1) b0 = 1;
-    A.blocks0 = b0;
-    const int64_t b1 = 4;
-    fh::mlp::adam_kernel<<<(unsigned)(b0 + b1), 256, 0, s>>>(A);
+    add(M, 4);
+    A.nseg = k;
+    A.block0[k] = blocks;
+    fh::mlp::adam_kernel<<<(unsigned)blocks, 256, 0, s>>>(A);
     return cuda_check(cudaGetLastError(), "adam_kernel launch");
+}
+
+static fh_status apply_impl(fh_trainer tr, int64_t begin, int64_t end, float *tgrad, cudaStream_t s) {
+    float *g[1] = {tgrad};
+    return apply_ranges_impl(tr, end > begin ? 1 : 0, &begin, &end, g, s);
 }
 
 extern "C" {
@@ -203,6 +257,32 @@ fh_status fh_train_apply(fh_trainer tr, fh_stream stream) {
     if (!tr) return fail(FH_E_ARG, "fh_train_apply: NULL trainer");
     const int64_t n = (int64_t)(tr->enc->entries * (uint64_t)tr->enc->F);
     return apply_impl(tr, 0, n, tr->b.table_grad, reinterpret_cast<cudaStream_t>(stream));
+}
+
+fh_status fh_train_apply_ranges(fh_trainer tr, int n, const int64_t *begin, const int64_t *end,
+                                const float *const *grad, fh_stream stream) {
+    g_err[0] = 0;
+    if (!tr) return fail(FH_E_ARG, "fh_train_apply_ranges: NULL trainer");
+    if (n < 0 || n >= fh::mlp::kMaxAdamSeg || (n > 0 && (!begin || !end || !grad)))
+        return fail(FH_E_ARG, "fh_train_apply_ranges: bad range list (n = %d, max %d)", n, fh::mlp::kMaxAdamSeg - 1);
+    const int64_t nt = (int64_t)(tr->enc->entries * (uint64_t)tr->enc->F);
+    for (int i = 0; i < n; i++) {
+        if (begin[i] < 0 || end[i] < begin[i] || end[i] > nt)
+            return fail(FH_E_ARG, "fh_train_apply_ranges: range %d [%lld, %lld) outside [0, %lld)", i,
+                        (long long)begin[i], (long long)end[i], (long long)nt);
+        if (end[i] > begin[i] && !grad[i]) return fail(FH_E_ARG, "fh_train_apply_ranges: NULL grad %d", i);
+        for (int j = 0; j < i; j++)
+            if (begin[i] < end[j] && begin[j] < end[i])
+                return fail(FH_E_ARG, "fh_train_apply_ranges: ranges %d and %d overlap", j, i);
+    }
+    cudaStream_t s = reinterpret_cast<cudaStream_t>(stream);
+    fh_status st = apply_ranges_impl(tr, n, begin, end, const_cast<float *const *>(grad), s);
+    if (st != FH_OK) return st;
+    // the local (pre-reduction) grads must start the next step at zero
+    st = cuda_check(cudaMemsetAsync(tr->b.table_grad, 0, (size_t)nt * sizeof(float), s), "zero table_grad");
+    if (st != FH_OK) return st;
+    return cuda_check(cudaMemsetAsync(tr->b.mlp_grad, 0, (size_t)fh::mlp::param_count(tr->K0) * sizeof(float), s),
+                      "zero mlp_grad");
 }
 
 fh_status fh_train_apply_sharded(fh_trainer tr, int64_t begin, int64_t end, const float *grad_shard,

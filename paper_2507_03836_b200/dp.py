@@ -100,6 +100,138 @@ class ShardedDP:
         return loss
 
 
+def overlap_plan(launch_ranges, world: int, rank: int):
+    """Partition of the table gradient for OverlappedShardedDP.
+
+    launch_ranges: per backward launch, the flat element ranges it finalises
+    (Trainer.bwd_launch_ranges).  Each range [b, e) splits into a MAIN part
+    [a, a + m) -- a = b rounded up to 4, m the largest multiple of 4 W that
+    fits -- reduce-scattered in W equal chunks of m / W (a multiple of 4, so
+    every chunk is 16-byte aligned for the vectorised Adam), and at most
+    3 + 4 W - 1 TAIL elements, all-reduced and updated on every rank.
+    Returns (mains, tails): mains = [(launch, a, m)], tails = [(b, e)]."""
+    mains, tails = [], []
+    q = 4 * world
+    for li, rngs in enumerate(launch_ranges):
+        for b, e in rngs:
+            a = min((b + 3) // 4 * 4, e)
+            m = (e - a) // q * q
+            if a > b:
+                tails.append((b, a))
+            if m > 0:
+                mains.append((li, a, m))
+            if a + m < e:
+                tails.append((a + m, e))
+    return mains, tails
+
+
+class OverlappedShardedDP:
+    """ShardedDP with the reduction overlapped with the backward (SURVEY.md
+    §8(e) item 2).  fh_train_fwd_bwd records one CUDA event after each
+    backward launch (a level group whose gradients are then final); a
+    communication stream waits for each event and reduce-scatters that
+    group's gradients while the later groups' backward still runs.  Each
+    rank then runs ONE Adam launch over its chunks of every group plus the
+    (tiny, replicated) tails (fh_train_apply_ranges) and all-gathers the
+    fp16 shadow of its chunks.  Same mathematics as ShardedDP / the
+    single-process step: every table element is in exactly one main chunk
+    or tail, see overlap_plan.  Works on CPU tensors too (gloo, no streams),
+    which is how the CPU tests exercise the partition."""
+
+    def __init__(self, trainer, group=None):
+        import torch
+        import torch.distributed as dist
+        self.tr = trainer
+        self.group = group
+        self.world = dist.get_world_size(group) if dist.is_initialized() else 1
+        self.rank = dist.get_rank(group) if dist.is_initialized() else 0
+        if trainer.shadow_flat is None:
+            raise ValueError("sharded DP needs an fp16 table shadow (the replicated state)")
+        self.launches = trainer.bwd_launch_ranges()
+        self.mains, self.tails = overlap_plan(self.launches, self.world, self.rank)
+        dev = trainer.grads.device
+        self.cuda = dev.type == "cuda"
+        self.chunks = [m // self.world for (_, _, m) in self.mains]
+        self.shard = torch.empty(max(1, sum(self.chunks)), dtype=torch.float32, device=dev)
+        self.shard_views, off = [], 0
+        for c in self.chunks:
+            self.shard_views.append(self.shard[off:off + c])
+            off += c
+        idx = [i for (b, e) in self.tails for i in range(b, e)]
+        self.n_tail = len(idx)
+        self.tail_idx = torch.tensor(idx, dtype=torch.int64, device=dev)
+        n_mlp = trainer.mlp_grad.numel()
+        self.tail_buf = torch.empty(self.n_tail + n_mlp, dtype=torch.float32, device=dev)
+        self.tail_views, off = [], 0
+        for b, e in self.tails:
+            self.tail_views.append(self.tail_buf[off:off + e - b])
+            off += e - b
+        # Adam ranges: this rank's chunk of every main part, then the tails
+        self.ranges = [(a + self.rank * c, a + (self.rank + 1) * c) for (_, a, m), c in zip(self.mains, self.chunks)]
+        self.ranges += list(self.tails)
+        if len(self.ranges) > 63:
+            raise ValueError(f"{len(self.ranges)} Adam ranges (max 63)")
+        self._inplace_ok = (not dist.is_initialized()) or dist.get_backend(group) == "nccl"
+        self.events = []
+        if self.cuda:
+            self.comm = torch.cuda.Stream(device=dev)
+            self.events = [torch.cuda.Event() for _ in self.launches]
+            for ev in self.events:   # create the CUDA events before handing them over
+                ev.record()
+            trainer.set_bwd_events(self.events)
+
+    def _by_launch(self):
+        out = [[] for _ in self.launches]
+        for k, (li, a, m) in enumerate(self.mains):
+            out[li].append(k)
+        return out
+
+    def step(self, coords, target, n_global: int, stream=None):
+        loss = self.tr.fwd_bwd(coords, target, n_global, stream=stream)
+        self.reduce_and_apply(stream=stream)
+        return loss
+
+    def reduce_and_apply(self, stream=None):
+        """Everything after fwd_bwd: the per-launch reduce-scatters (queued
+        behind the backward launches' events), the tails + MLP all-reduce,
+        one Adam over the owned ranges, the shadow all-gathers."""
+        import contextlib
+        import torch
+        import torch.distributed as dist
+        tr = self.tr
+        grads = tr.grads
+        if self.world == 1:
+            grad_views = [grads[a:a + m] for (_, a, m) in self.mains] + [grads[b:e] for b, e in self.tails]
+            tr.apply_ranges(self.ranges, grad_views, stream=stream)
+            return
+        cur = torch.cuda.current_stream() if self.cuda else None
+        ctx = torch.cuda.stream(self.comm) if self.cuda else contextlib.nullcontext()
+        with ctx:
+            for li, ks in enumerate(self._by_launch()):
+                if self.cuda:
+                    self.comm.wait_event(self.events[li])   # launch li's gradients are final
+                for k in ks:
+                    _, a, m = self.mains[k]
+                    dist.reduce_scatter_tensor(self.shard_views[k], grads[a:a + m], op=dist.ReduceOp.SUM,
+                                               group=self.group)
+            if self.cuda:
+                self.comm.wait_stream(cur)                  # MLP grads and tails: whole step done
+            if self.n_tail:
+                torch.index_select(grads, 0, self.tail_idx, out=self.tail_buf[:self.n_tail])
+            self.tail_buf[self.n_tail:].copy_(tr.mlp_grad)
+            dist.all_reduce(self.tail_buf, op=dist.ReduceOp.SUM, group=self.group)
+            tr.mlp_grad.copy_(self.tail_buf[self.n_tail:])
+        if self.cuda:
+            cur.wait_stream(self.comm)
+        tr.apply_ranges(self.ranges, self.shard_views + self.tail_views, stream=stream)
+        flat = tr.shadow_flat
+        for (_, a, m), c in zip(self.mains, self.chunks):
+            mine = flat[a + self.rank * c: a + (self.rank + 1) * c]
+            if not self._inplace_ok:
+                mine = mine.clone()          # gloo: no aliasing of input and output
+            dist.all_gather_into_tensor(flat[a:a + m], mine, group=self.group)
+
+
 def replicas_identical(tensor, group=None) -> bool:
     """True when `tensor` is bit-identical on every rank (compares a 64-bit
     checksum of its bytes gathered from all ranks)."""

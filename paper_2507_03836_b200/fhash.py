@@ -34,6 +34,7 @@ EXPORTS = [
     # train step
     "fh_mlp_param_count", "fh_train_workspace_size", "fh_trainer_create", "fh_train_fwd_bwd", "fh_train_apply",
     "fh_train_step", "fh_trainer_status", "fh_trainer_step_count", "fh_trainer_destroy", "fh_train_apply_sharded",
+    "fh_train_bwd_launches", "fh_train_bwd_ranges", "fh_train_set_bwd_events", "fh_train_apply_ranges",
     # inference (renderer's model evaluation) and the ARM pace rule
     "fh_infer_workspace_size", "fh_infer", "fh_arm_pace",
     # include/fhash_coreset.h (NEXT-4 coreset selection)
@@ -299,6 +300,15 @@ def _train_lib():
     L.fh_train_apply.argtypes = [vp, vp]
     L.fh_train_apply_sharded.argtypes = [vp, i64, i64, vp, vp]
     L.fh_train_apply_sharded.restype = ctypes.c_int
+    L.fh_train_bwd_launches.argtypes = [vp]
+    L.fh_train_bwd_launches.restype = ctypes.c_int
+    L.fh_train_bwd_ranges.argtypes = [vp, ctypes.c_int, ctypes.POINTER(i64), ctypes.c_int, ctypes.POINTER(ctypes.c_int)]
+    L.fh_train_bwd_ranges.restype = ctypes.c_int
+    L.fh_train_set_bwd_events.argtypes = [vp, ctypes.POINTER(vp), ctypes.c_int]
+    L.fh_train_set_bwd_events.restype = ctypes.c_int
+    L.fh_train_apply_ranges.argtypes = [vp, ctypes.c_int, ctypes.POINTER(i64), ctypes.POINTER(i64),
+                                        ctypes.POINTER(vp), vp]
+    L.fh_train_apply_ranges.restype = ctypes.c_int
     L.fh_infer_workspace_size.argtypes = [vp, ctypes.POINTER(MLPDesc), i64]
     L.fh_infer_workspace_size.restype = ctypes.c_size_t
     L.fh_infer.argtypes = [vp, ctypes.POINTER(MLPDesc), vp, vp, vp, vp, i64, vp, vp, ctypes.c_size_t, vp]
@@ -425,6 +435,36 @@ class Trainer:
 
     def apply(self, stream=None):
         _check(_train_lib().fh_train_apply(self._h, _stream(stream)))
+
+    # -- overlap of the gradient reduction with the backward (dp.OverlappedShardedDP)
+    def bwd_launch_ranges(self):
+        """[[(begin, end), ...] per backward launch] in flat table elements."""
+        L = _train_lib()
+        n = int(L.fh_train_bwd_launches(self._h))
+        if n < 0:
+            raise FHashError(FH_E_STATE, "fh_train_bwd_launches failed")
+        out = []
+        for i in range(n):
+            buf = (ctypes.c_int64 * 64)()
+            k = ctypes.c_int()
+            _check(L.fh_train_bwd_ranges(self._h, i, buf, 32, ctypes.byref(k)))
+            out.append([(int(buf[2 * j]), int(buf[2 * j + 1])) for j in range(k.value)])
+        return out
+
+    def set_bwd_events(self, events):
+        """events: torch.cuda.Event list (one per backward launch) or []."""
+        arr = (ctypes.c_void_p * max(1, len(events)))(*[e.cuda_event for e in events])
+        self._events = list(events)   # keep alive
+        _check(_train_lib().fh_train_set_bwd_events(self._h, arr, len(events)))
+
+    def apply_ranges(self, ranges, grads, stream=None):
+        """One Adam step over table element ranges [(b, e)] with grads (f32
+        CUDA tensors of e-b values each) + the MLP segment."""
+        n = len(ranges)
+        b = (ctypes.c_int64 * max(1, n))(*[r[0] for r in ranges])
+        e = (ctypes.c_int64 * max(1, n))(*[r[1] for r in ranges])
+        g = (ctypes.c_void_p * max(1, n))(*[t.data_ptr() for t in grads])
+        _check(_train_lib().fh_train_apply_ranges(self._h, n, b, e, g, _stream(stream)))
 
     def step(self, coords, target, n_global=None, stream=None):
         N = coords.shape[0]

@@ -170,3 +170,92 @@ def test_allreduce_of_shard_grads_equals_global_grad():
     assert np.array_equal(res[0], res[1])
     assert res["same0"] and res["same1"]
     assert not res["diff0"] and not res["diff1"]
+
+
+# ---------------------------------------------- overlapped reduction (§8(e) 2)
+def test_overlap_plan_partitions_the_table():
+    """Every table element is in exactly one rank's main chunk or in a tail
+    (replicated); chunks are 4-aligned and equal across ranks."""
+    g = np.random.default_rng(3)
+    for trial in range(40):
+        n = int(g.integers(1, 5000))
+        cuts = sorted(set(int(c) for c in g.integers(0, n, int(g.integers(0, 8))))) + [n]
+        rngs, b = [], 0
+        for c in cuts:
+            if c > b:
+                rngs.append((b, c))
+            b = c
+        launches = [rngs[i::2] for i in range(2)]   # ranges spread over two launches
+        for W in (1, 2, 3, 8):
+            cover = np.zeros(n, np.int64)
+            for r in range(W):
+                mains, tails = dp.overlap_plan(launches, W, r)
+                for (_, a, m) in mains:
+                    assert a % 4 == 0 and m % (4 * W) == 0
+                    c = m // W
+                    cover[a + r * c:a + (r + 1) * c] += 1
+            for (b, e) in tails:
+                assert e - b < 4 * W + 4
+                cover[b:e] += 1
+            assert np.all(cover == 1), (trial, W)
+
+
+class _MockOverlapTrainer(_MockTrainer):
+    """Adds the overlap interface: two backward launches covering the table,
+    and apply_ranges running the oracle's Adam on each range."""
+
+    def bwd_launch_ranges(self):
+        n = self.n_table
+        return [[(0, 301)], [(301, 702), (702, n)]]
+
+    def set_bwd_events(self, events):
+        pass
+
+    def apply_ranges(self, ranges, grads, stream=None):
+        self.step_no += 1
+        s = self.step_no
+        for (b, e), g in zip(ranges, grads):
+            gg = g.numpy()[:e - b].astype(np.float64)
+            self.p[b:e], self.m[b:e], self.v[b:e] = self.T.adam_step(self.p[b:e], gg, self.m[b:e], self.v[b:e], s)
+            self.shadow_flat[b:e] = torch.from_numpy(self.p[b:e]).half()
+        self.pm, self.mm, self.mv = self.T.adam_step(self.pm, self.mlp_grad.numpy().astype(np.float64),
+                                                     self.mm, self.mv, s)
+        self.grads.zero_()
+
+
+def _overlap_worker(rank, world, port, out):
+    os.environ["MASTER_ADDR"] = "127.0.0.1"
+    os.environ["MASTER_PORT"] = str(port)
+    dist.init_process_group("gloo", rank=rank, world_size=world)
+    try:
+        tr = _MockOverlapTrainer(1001, 37, world, rank)
+        odp = dp.OverlappedShardedDP(tr)
+        for _ in range(3):
+            odp.step(None, None, 1)
+        out[f"shadow{rank}"] = tr.shadow_flat[:tr.n_table].float().numpy().copy()
+        out[f"mlp{rank}"] = tr.pm.copy()
+        out[f"same{rank}"] = dp.replicas_identical(tr.shadow_flat)
+    finally:
+        dist.destroy_process_group()
+
+
+def test_overlapped_sharded_adam_equals_replicated_adam():
+    """Per-launch reduce-scatter + all-reduced tails + one Adam over the
+    owned ranges + all-gather gives every rank the single-process result."""
+    world = 2
+    with mp.Manager() as m:
+        out = m.dict()
+        mp.spawn(_overlap_worker, args=(world, _free_port(), out), nprocs=world, join=True)
+        res = dict(out)
+    ref = _MockTrainer(1001, 37, 1, 0)
+    from oracle import train as T
+    for s in range(1, 4):
+        g = sum(_MockTrainer.local_grad(r, s - 1, 1001 + 37).astype(np.float32)
+                for r in range(world)).astype(np.float64)
+        ref.p, ref.m, ref.v = T.adam_step(ref.p, g[:1001], ref.m, ref.v, s)
+        ref.pm, ref.mm, ref.mv = T.adam_step(ref.pm, g[1001:], ref.mm, ref.mv, s)
+    exp = torch.from_numpy(ref.p).half().float().numpy()
+    for r in range(world):
+        assert np.array_equal(res[f"shadow{r}"], exp)
+        assert np.allclose(res[f"mlp{r}"], ref.pm, rtol=0, atol=1e-12)
+        assert res[f"same{r}"]

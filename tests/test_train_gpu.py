@@ -239,3 +239,62 @@ def test_divergence_flag():
     tr.fwd_bwd(torch.from_numpy(coords).cuda(), torch.from_numpy(target).cuda())
     assert tr.status() == fh.FH_E_DIVERGED
     assert tr.status() == fh.FH_OK
+
+
+def test_bwd_launch_ranges_events_and_apply_ranges():
+    """The backward launches' ranges partition the table; the caller's
+    events are recorded by fh_train_fwd_bwd; fh_train_apply_ranges over
+    ranges covering the table (aligned chunks + unaligned tails, in any
+    order) is bit-identical to fh_train_apply."""
+    from paper_2507_03836_b200 import dp
+    cfg = small_cfg(2, 16, cap=1 << 10)
+    trs = [make(cfg, 1500, seed=31) for _ in range(2)]
+    (_, ta, coords, target), (_, tb, _, _) = trs
+    launches = ta.bwd_launch_ranges()
+    cover = np.zeros(ta.n_table, np.int64)
+    for rngs in launches:
+        for b, e in rngs:
+            cover[b:e] += 1
+    assert np.all(cover == 1) and len(launches) >= 1
+    evs = [torch.cuda.Event() for _ in launches]
+    for ev in evs:
+        ev.record()
+    ta.set_bwd_events(evs)
+    c, t = torch.from_numpy(coords).cuda(), torch.from_numpy(target).cuda()
+    mains, tails = dp.overlap_plan(launches, 3, 0)
+    for step in range(3):
+        ta.fwd_bwd(c, t)
+        tb.grads.copy_(ta.grads)      # same gradients (atomics make two runs differ in fp32 order)
+        torch.cuda.synchronize()
+        assert all(ev.query() for ev in evs)
+        ranges = [(a, a + m) for (_, a, m) in mains][::-1] + tails   # any order
+        ta.apply_ranges(ranges, [ta.grads[b:e] for b, e in ranges])
+        tb.apply()
+        torch.cuda.synchronize()
+        assert torch.equal(ta.table_master, tb.table_master)
+        assert torch.equal(ta.table_shadow, tb.table_shadow)
+        assert torch.equal(ta.mlp_master, tb.mlp_master)
+        assert torch.all(ta.grads == 0)
+    assert ta.step_count == tb.step_count == 3
+    ta.set_bwd_events([])
+
+
+def test_overlapped_dp_single_rank_equals_plain_step():
+    """OverlappedShardedDP without a process group (one rank) takes exactly
+    the plain train step."""
+    from paper_2507_03836_b200 import dp
+    cfg = small_cfg(4, 16, cap=1 << 11)
+    (_, ta, coords, target), (_, tb, _, _) = [make(cfg, 2000, seed=41) for _ in range(2)]
+    odp = dp.OverlappedShardedDP(ta)
+    c, t = torch.from_numpy(coords).cuda(), torch.from_numpy(target).cuda()
+    for _ in range(3):
+        ta.fwd_bwd(c, t, 2000)
+        tb.grads.copy_(ta.grads)      # same gradients (atomics make two runs differ in fp32 order)
+        odp.reduce_and_apply()
+        tb.apply()
+        torch.cuda.synchronize()
+        assert torch.equal(ta.table_master, tb.table_master)
+        assert torch.equal(ta.table_shadow, tb.table_shadow)
+        assert torch.equal(ta.mlp_master, tb.mlp_master)
+    loss = odp.step(c, t, 2000)        # the composed step runs too
+    assert ta.status() == fh.FH_OK and torch.isfinite(loss).all()
