@@ -304,6 +304,33 @@ def train_step_bench(fh, torch, W, which, rank, world, dist, steps, warmup):
     ie1.record(stream)
     torch.cuda.synchronize()
     infer_ms = ie0.elapsed_time(ie1) / steps
+    # renderer-sized batches (Alg. 1 marches <= 64 samples per ray): latency of
+    # one fh_infer call, eager vs replayed from a CUDA graph
+    small = {}
+    for nb in (1 << 10, 1 << 12, 1 << 16):
+        cs, ys = coords[:nb], yb[:nb]
+        reps = 100
+        ie0.record(stream)
+        for _ in range(reps):
+            tr.infer(cs, ys)
+        ie1.record(stream)
+        torch.cuda.synchronize()
+        eager_us = ie0.elapsed_time(ie1) / reps * 1e3
+        gs = torch.cuda.Stream()
+        gs.wait_stream(stream)
+        graph = torch.cuda.CUDAGraph()
+        with torch.cuda.stream(gs):
+            tr.infer(cs, ys, stream=gs)
+            with torch.cuda.graph(graph, stream=gs):
+                tr.infer(cs, ys, stream=gs)
+        torch.cuda.synchronize()
+        ie0.record(stream)
+        for _ in range(reps):
+            graph.replay()
+        ie1.record(stream)
+        torch.cuda.synchronize()
+        small[str(nb)] = {"eager_us": eager_us, "graph_us": ie0.elapsed_time(ie1) / reps * 1e3}
+        del graph
     # DP correctness: after the timed steps the replicas must be bit-identical
     same = dp.replicas_identical(tr.shadow_flat) and dp.replicas_identical(tr.mlp_master)
     last = tr.loss.clone()
@@ -324,7 +351,8 @@ def train_step_bench(fh, torch, W, which, rank, world, dist, steps, warmup):
                if isinstance(sdp, dp.OverlappedShardedDP) else
                "reduce-scatter + sharded Adam + all-gather (NCCL)" if world > 1 else "single GPU"),
         "infer": {"what": "fh_infer: encode fwd + tcgen05 MLP forward (Alg. 1 V = model(S))",
-                  "ms": infer_ms, "samples_per_s": n_local / (infer_ms / 1e3)},
+                  "ms": infer_ms, "samples_per_s": n_local / (infer_ms / 1e3),
+                  "small_batch_latency": small},
         "loss_first_warmup": losses[0], "loss_last": float(last.item()), "status": int(st),
         "params": enc.param_count + tr.n_mlp, "gpu_launches_per_step": 6, "replicas_identical": bool(same),
     }

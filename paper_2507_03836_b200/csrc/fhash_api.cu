@@ -216,7 +216,10 @@ static void launch_fwd(fh_encoder e, const float *coords, int64_t N, const void 
         if (!(fo && atoi(fo) == 1)) dperm = nullptr;  // direct levels: natural order (coalesced rows)
     }
     fh::LevelList lists[FH_MAX_LEVELS];
-    const int n = split_lists(e, include, (double)F * sizeof(T), e->fwd_limit, lists);
+    // small batches (e.g. the renderer's ray batches) touch few entries: one
+    // pass, fewer launches; large batches: L2-sized level groups
+    const double limit = N < (1 << 15) ? 0.0 : e->fwd_limit;
+    const int n = split_lists(e, include, (double)F * sizeof(T), limit, lists);
     for (int g = 0; g < n; g++)
         fh::fwd_kernel<F, T, O><<<grid_for(N, lists[g].n), 256, 0, s>>>(
             e->params, c4, N, reinterpret_cast<const T *>(table), full_blocks, reinterpret_cast<O *>(out), e->flag,
