@@ -218,6 +218,82 @@ def microbench_roofline(fh, torch, enc, cfg, N, stream, hbm_peak):
     }
 
 
+def hbm_regime_bench(fh, torch, W, steps, copy_gbs):
+    """The metric's HBM regime: BASELINE.json configs[3] encoder (L=16, F=4
+    fp16 tables capped at 2^22: 305 MiB of tables, 609 MiB of fp32 grads),
+    2^22 uniform points, encode fwd (bf16 out, as in the train step) + bwd,
+    L2 flushed.  Roofline: the kernels run L2-sized level-group passes, so per
+    level the measured random-gather / red rate at that level's table size
+    and entry width (8 B fp16x4 rows; 16 B fp32x4 grads, no pair merge) bounds
+    the corner traffic, and the compulsory HBM bytes -- tables read once,
+    grads read + written once, coordinates, encodings and upstream grads
+    streamed -- go at the measured copy bandwidth:
+        t_roof = N sum_l 16 / rate_l + HBM bytes / BW_copy."""
+    cfg, N = W.CFG4, W.N_CFG4
+    enc = fh.Encoder(cfg.levels, cfg.F, cfg.table_dtype, cfg.cap)
+    g = torch.Generator("cuda").manual_seed(4)
+    coords = torch.rand((N, 4), device="cuda", generator=g)
+    table = ((torch.rand((enc.entries, cfg.F), device="cuda", generator=g) - 0.5) * 2e-4).half()
+    out = torch.empty((N, cfg.L * cfg.F), device="cuda", dtype=torch.bfloat16)
+    dout = torch.randn((N, cfg.L * cfg.F), device="cuda", generator=g)
+    dt = torch.zeros((enc.entries, cfg.F), device="cuda")
+    flush = torch.empty(256 << 20, dtype=torch.uint8, device="cuda")
+    e = [torch.cuda.Event(enable_timing=True) for _ in range(3)]
+    tf = tb = 0.0
+    for it in range(steps + 2):
+        flush.fill_(it & 255)
+        enc.zero_grad(dt)
+        e[0].record()
+        enc.fwd(coords, table, out, out_dtype="bf16")
+        e[1].record()
+        enc.bwd(coords, dout, dt)
+        e[2].record()
+        torch.cuda.synchronize()
+        if it >= 2:
+            tf += e[0].elapsed_time(e[1])
+            tb += e[1].elapsed_time(e[2])
+    fwd_ms, bwd_ms = tf / steps, tb / steps
+    del out, dout, flush
+    n_thr = 1 << 20
+    sink = torch.empty(n_thr, device="cuda")
+    ev0, ev1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+
+    def timeit(fn, reps=3):
+        best = 1e9
+        for _ in range(reps):
+            ev0.record()
+            fn()
+            ev1.record()
+            ev1.synchronize()
+            best = min(best, ev0.elapsed_time(ev1) / 1e3)
+        return best
+
+    t_g = t_r = 0.0
+    for l in range(cfg.L):
+        T = enc.level_info(l)["table_size"]
+        gb = torch.zeros((T, 2), device="cuda")                 # 8-byte rows (fp16 x 4)
+        rb = torch.zeros((T, 4), device="cuda")                 # 16-byte rows (fp32 x 4)
+        fh.bench_gather(gb, T, 8, n_thr, sink, mode=1, seed=l)
+        rg = 16 * n_thr / timeit(lambda: fh.bench_gather(gb, T, 8, n_thr, sink, mode=1, seed=l))
+        rr = 16 * n_thr / timeit(lambda: fh.bench_red(rb, T, 16, n_thr, mode=1, seed=l))
+        t_g += N * 16 / rg
+        t_r += N * 16 / rr
+        del gb, rb
+    LF = cfg.L * cfg.F
+    hbm_fwd = enc.entries * cfg.F * 2 + N * (16 + LF * 2)           # tables + coords + bf16 out
+    hbm_bwd = enc.entries * cfg.F * 4 * 2 + N * (16 + LF * 4)       # grads RMW + coords + fp32 dout
+    bw = copy_gbs * 1e9
+    roof_f = t_g + hbm_fwd / bw
+    roof_b = t_r + hbm_bwd / bw
+    return {"workload": "cfg4 encoder (BASELINE.json configs[3]): 2^22 points, L=16, F=4 fp16 tables cap 2^22 "
+                        "(305 MiB) + fp32 grads (609 MiB); fwd (bf16 out) + bwd, L2 flushed",
+            "fwd_ms": fwd_ms, "bwd_ms": bwd_ms, "samples_per_s": N / ((fwd_ms + bwd_ms) / 1e3),
+            "t_roof_fwd_ms": roof_f * 1e3, "t_roof_bwd_ms": roof_b * 1e3,
+            "fwd_frac": roof_f * 1e3 / fwd_ms, "bwd_frac": roof_b * 1e3 / bwd_ms,
+            "frac": (roof_f + roof_b) * 1e3 / (fwd_ms + bwd_ms),
+            "hbm_bytes_per_step": hbm_fwd + hbm_bwd}
+
+
 def train_step_bench(fh, torch, W, which, rank, world, dist, steps, warmup):
     """All §8(a) rows in one step: Philox voxel sampling from the synthetic
     field, encode fwd (fp16 table -> bf16), tcgen05 MLP fwd + MSE + bwd,
@@ -594,6 +670,7 @@ def run_ours(args, rank, local_rank, world):
         return
 
     mb = microbench_roofline(fh, torch, enc, cfg, N, stream, hbm_peak)
+    hbm_regime = hbm_regime_bench(fh, torch, W, max(3, min(K, 10)), mb["copy_gbs"]) if not args.no_train else None
     # Contract roofline of the dominant kernel: algorithmic bytes / launch time.
     LF4 = cfg.L * cfg.F * 4
     alg = {"fwd": N * (16 * cfg.L * cfg.F * 4 + 16 + LF4), "bwd": N * (16 * cfg.L * cfg.F * 4 + 16 + LF4)}
@@ -624,7 +701,7 @@ def run_ours(args, rank, local_rank, world):
         "kernels_ms": {"zero_grad": zero_ms, "encode_fwd": fwd_ms, "encode_bwd": bwd_ms, "step": step_ms},
         "roofline": roofline, "gather_roofline": gather_roofline, "cpu_baseline": cpu, "e2e": e2e,
         "gpu_launches": 2 * K, "clocks": clk.summary(), "train_step": train,
-        "paper_encoders": encoders, "coreset": coreset,
+        "paper_encoders": encoders, "coreset": coreset, "hbm_regime": hbm_regime,
     }
     print(json.dumps(line), flush=True)
     if dist:
