@@ -107,22 +107,9 @@ template <int F, typename T> struct Gather;
 template <> struct Gather<1, float> {
     static __device__ __forceinline__ void load(const float *t, uint32_t i, float *o) { o[0] = __ldg(t + i); }
 };
-#ifndef FH_GATHER_HINT
-#define FH_GATHER_HINT 0
-#endif
 template <> struct Gather<2, float> {
     static __device__ __forceinline__ void load(const float *t, uint32_t i, float *o) {
-#if FH_GATHER_HINT == 1
-        float2 v;
-        asm("ld.global.nc.L1::no_allocate.v2.f32 {%0,%1}, [%2];" : "=f"(v.x), "=f"(v.y)
-            : "l"(reinterpret_cast<const float2 *>(t) + i));
-#elif FH_GATHER_HINT == 2
-        float2 v;
-        asm("ld.global.nc.L2::evict_last.v2.f32 {%0,%1}, [%2];" : "=f"(v.x), "=f"(v.y)
-            : "l"(reinterpret_cast<const float2 *>(t) + i));
-#else
         const float2 v = __ldg(reinterpret_cast<const float2 *>(t) + i);
-#endif
         o[0] = v.x; o[1] = v.y;
     }
 };
@@ -224,17 +211,14 @@ __device__ __forceinline__ void load_levels(const Params &P, Level *s) {
     __syncthreads();
 }
 
-// ------------------------------------------------------------ block gather
+// ------------------------------------------------------------ pair gather
 // The 16 corners are 8 x-adjacent pairs.  Eq. 9 puts a pair at entries
-// (i, i+1); the R5 hash puts it at (h, h') with h' = h^1 when X is even and
-// within the same 4-entry block when X = 1 mod 4.  Either way the pair lies
-// in one 32-byte-aligned block with probability 3/4 (8-byte entries), so
-// each pair is fetched with ONE 256-bit load (LDG.E.ENL2.256, one L1
-// wavefront / one L2 sector) plus a second only when it straddles blocks:
-// 1.25 loads per pair instead of 2.
+// (i, i+1); the R5 hash puts it at (h, h') with h' = h^1 when X is even.
+// When the two entries form one aligned 2-entry chunk (i1 == i0 ^ 1, about
+// half the pairs) they are fetched with one load of twice the entry width
+// (wider 32-byte block loads measured slower).
 template <typename T, int F> struct EntryTraits {
     static constexpr int kBytes = F * (int)sizeof(T);
-    static constexpr int kPerBlock = kBytes >= 32 ? 1 : 32 / kBytes;   // entries per 32-byte block
     static constexpr int kWords = kBytes >= 4 ? kBytes / 4 : 1;        // 32-bit words per entry
 };
 
@@ -248,38 +232,6 @@ __device__ __forceinline__ Block32 ld_block(const void *base, uint32_t b) {
           "=r"(r.w[7])
         : "l"(p));
     return r;
-}
-
-// Convert the entry at slot s of a block to F floats.
-template <typename T, int F>
-__device__ __forceinline__ void extract(const Block32 &b, uint32_t s, float *o) {
-    using Tr = EntryTraits<T, F>;
-    if constexpr (Tr::kBytes >= 4) {
-        uint32_t w[Tr::kWords];
-#pragma unroll
-        for (int j = 0; j < Tr::kWords; j++) {
-            uint32_t v = b.w[j];
-#pragma unroll
-            for (int q = 1; q < Tr::kPerBlock; q++) v = (s == (uint32_t)q) ? b.w[q * Tr::kWords + j] : v;
-            w[j] = v;
-        }
-        if constexpr (sizeof(T) == 4) {
-#pragma unroll
-            for (int j = 0; j < F; j++) o[j] = __uint_as_float(w[j]);
-        } else {
-#pragma unroll
-            for (int j = 0; j < F / 2; j++) {
-                const float2 f = __half22float2(*reinterpret_cast<const __half2 *>(&w[j]));
-                o[2 * j] = f.x; o[2 * j + 1] = f.y;
-            }
-        }
-    } else {  // 2-byte entry (F = 1 half): 16 per block
-        uint32_t v = b.w[0];
-#pragma unroll
-        for (int q = 1; q < 8; q++) v = ((s >> 1) == (uint32_t)q) ? b.w[q] : v;
-        const unsigned short h = (s & 1) ? (unsigned short)(v >> 16) : (unsigned short)(v & 0xFFFF);
-        o[0] = __half2float(__ushort_as_half(h));
-    }
 }
 
 // Raw loads for the pair gather: one entry (W words) or an aligned pair of
@@ -326,16 +278,13 @@ __device__ __forceinline__ void words_to_float(const uint32_t *w, float *o) {
 }
 
 // Gather the 16 corner entries of one (sample, level) into e[16][F].
-// full_blocks = number of complete 32-byte blocks in the table; entries in
-// a trailing partial block are read entry-wise (never past the buffer).
+// (full_blocks, the number of complete 32-byte blocks of the table, is not
+// needed by the pair loads, which never leave the two entries' chunk.)
 template <typename T, int F>
 __device__ __forceinline__ void gather16(const T *__restrict__ table, uint32_t full_blocks, const uint32_t (&idx)[16],
                                          float (&e)[16][F]) {
     using Tr = EntryTraits<T, F>;
-#ifndef FH_BLOCK_GATHER
-#define FH_BLOCK_GATHER 3
-#endif
-    if constexpr ((Tr::kBytes == 4 || Tr::kBytes == 8 || Tr::kBytes == 16) && FH_BLOCK_GATHER == 3) {
+    if constexpr (Tr::kBytes == 4 || Tr::kBytes == 8 || Tr::kBytes == 16) {
         // x-pair in ONE load of the aligned 2-entry chunk when both entries
         // share it (i1 == i0 ^ 1: about half the pairs on Eq. 9 and on the R5
         // hash, whose x-neighbours differ in the low bits), else two entry
@@ -367,76 +316,9 @@ __device__ __forceinline__ void gather16(const T *__restrict__ table, uint32_t f
             words_to_float<T, F>(wa, e[2 * k]);
             words_to_float<T, F>(wb, e[2 * k + 1]);
         }
-    } else if constexpr (Tr::kBytes == 8 && FH_BLOCK_GATHER == 2) {
-        // x-pair as one 16-byte load of the aligned chunk holding entry i0;
-        // the partner comes from the same chunk when (i0>>1) == (i1>>1),
-        // else from one more 8-byte load.  Chunks never pass the buffer end.
-        uint4 c[8];
-        uint2 x[8];
-        bool same[8];
-#pragma unroll
-        for (int k = 0; k < 8; k++) {
-            const uint32_t i0 = idx[2 * k], i1 = idx[2 * k + 1];
-            const uint32_t ch = i0 >> 1;
-            const bool tail = ch >= 2 * full_blocks;  // chunk may pass the end of the table
-            same[k] = !tail && (i0 >> 1) == (i1 >> 1);
-            if (!tail) {
-                c[k] = __ldg(reinterpret_cast<const uint4 *>(table) + ch);
-            } else {
-                const uint2 t = __ldg(reinterpret_cast<const uint2 *>(table) + i0);
-                c[k] = (i0 & 1) ? make_uint4(0, 0, t.x, t.y) : make_uint4(t.x, t.y, 0, 0);
-            }
-            if (!same[k]) x[k] = __ldg(reinterpret_cast<const uint2 *>(table) + i1);
-        }
-#pragma unroll
-        for (int k = 0; k < 8; k++) {
-            const bool odd0 = idx[2 * k] & 1;
-            const uint2 a = odd0 ? make_uint2(c[k].z, c[k].w) : make_uint2(c[k].x, c[k].y);
-            const uint2 b = same[k] ? (odd0 ? make_uint2(c[k].x, c[k].y) : make_uint2(c[k].z, c[k].w)) : x[k];
-            const uint32_t wa[2] = {a.x, a.y}, wb[2] = {b.x, b.y};
-            if constexpr (sizeof(T) == 4) {
-                e[2 * k][0] = __uint_as_float(wa[0]); e[2 * k][1] = __uint_as_float(wa[1]);
-                e[2 * k + 1][0] = __uint_as_float(wb[0]); e[2 * k + 1][1] = __uint_as_float(wb[1]);
-            } else {
-#pragma unroll
-                for (int j = 0; j < 2; j++) {
-                    const float2 fa = __half22float2(*reinterpret_cast<const __half2 *>(&wa[j]));
-                    const float2 fb = __half22float2(*reinterpret_cast<const __half2 *>(&wb[j]));
-                    e[2 * k][2 * j] = fa.x; e[2 * k][2 * j + 1] = fa.y;
-                    e[2 * k + 1][2 * j] = fb.x; e[2 * k + 1][2 * j + 1] = fb.y;
-                }
-            }
-        }
-    } else if constexpr (Tr::kBytes > 32 || FH_BLOCK_GATHER != 1) {
+    } else {   // 2- and 32-byte entries: one load per corner
 #pragma unroll
         for (int k = 0; k < 16; k++) Gather<F, T>::load(table, idx[k], e[k]);
-    } else {
-        Block32 b0[8], b1[8];
-        uint32_t s0[8], s1[8];
-        bool two[8], tail[8];
-#pragma unroll
-        for (int k = 0; k < 8; k++) {
-            const uint32_t i0 = idx[2 * k], i1 = idx[2 * k + 1];
-            const uint32_t k0 = i0 / Tr::kPerBlock, k1 = i1 / Tr::kPerBlock;
-            s0[k] = i0 % Tr::kPerBlock;
-            s1[k] = i1 % Tr::kPerBlock;
-            two[k] = k0 != k1;
-            tail[k] = (k0 >= full_blocks) || (k1 >= full_blocks);
-            if (!tail[k]) {
-                b0[k] = ld_block(table, k0);
-                if (two[k]) b1[k] = ld_block(table, k1);
-            }
-        }
-#pragma unroll
-        for (int k = 0; k < 8; k++) {
-            if (!tail[k]) {
-                extract<T, F>(b0[k], s0[k], e[2 * k]);
-                extract<T, F>(two[k] ? b1[k] : b0[k], s1[k], e[2 * k + 1]);
-            } else {
-                Gather<F, T>::load(table, idx[2 * k], e[2 * k]);
-                Gather<F, T>::load(table, idx[2 * k + 1], e[2 * k + 1]);
-            }
-        }
     }
 }
 
