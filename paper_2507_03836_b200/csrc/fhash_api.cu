@@ -63,6 +63,10 @@ static fh_status ensure_flag(fh_encoder e) {
     };
     // Measured on B200 (cfg4, 305 MiB fp16 tables / 609 MiB grads): one pass
     // 6.06 / 19.95 ms fwd / bwd; groups of <= 0.55 L2: 2.98 / 6.34 ms.
+    if (const char *v = getenv("FH_TILE_S")) e->tile_s = atoi(v);
+    if (const char *v = getenv("FH_TILE_MARGIN")) e->tile_margin = atof(v);
+    if (const char *v = getenv("FH_FINE_ORDER")) e->fine_order = atoi(v) == 1;
+    if (const char *v = getenv("FH_AGG_MIN_DENSITY")) e->agg_density = atof(v);
     e->fwd_limit = budget("FH_FWD_GROUP_MB", 0.55);
     e->bwd_limit = budget("FH_BWD_GROUP_MB", 0.55);
     make_groups(e->fwd_limit, (size_t)e->F * dtype_size(e->table_dtype), e->gf, e->n_gf);
@@ -160,8 +164,7 @@ static void plan_tiles(fh_encoder e, int64_t N, double max_vertices, double per_
     int64_t S = (N + (int64_t)e->n_sm * waves - 1) / ((int64_t)e->n_sm * waves);
     if (S < 256) S = 256;
     if (S > kMaxTile) S = kMaxTile;
-    const char *sv = getenv("FH_TILE_S");
-    if (sv && atoi(sv) > 0 && atoi(sv) <= kMaxTile) S = atoi(sv);
+    if (e->tile_s > 0 && e->tile_s <= kMaxTile) S = e->tile_s;
     ts.S = (int)S;
     ts.box_bytes = box_bytes;
     ts.n = 0;
@@ -171,8 +174,7 @@ static void plan_tiles(fh_encoder e, int64_t N, double max_vertices, double per_
     int low[4] = {0, 0, 0, 0};
     const int kb = (int)std::ceil(kbits);
     for (int k = 0; k < kb && k < 16; k++) low[e->key.axis[k]]++;
-    const char *mv = getenv("FH_TILE_MARGIN");
-    const double margin = mv ? atof(mv) : 1.25;
+    const double margin = e->tile_margin;
     // staged boxes pay off up to per_sample vertices per sample (the kernels
     // allow a larger bound for tiles that straddle key blocks)
     const double cap = std::min(max_vertices, per_sample * (double)S);
@@ -212,8 +214,7 @@ static void launch_fwd(fh_encoder e, const float *coords, int64_t N, const void 
                 e->params, ts, c4, N, perm, reinterpret_cast<const T *>(table), full_blocks,
                 reinterpret_cast<O *>(out), e->flag);
         }
-        const char *fo = getenv("FH_FINE_ORDER");
-        if (!(fo && atoi(fo) == 1)) dperm = nullptr;  // direct levels: natural order (coalesced rows)
+        if (!e->fine_order) dperm = nullptr;  // direct levels: natural order (coalesced rows)
     }
     fh::LevelList lists[FH_MAX_LEVELS];
     // small batches (e.g. the renderer's ray batches) touch few entries: one
@@ -258,8 +259,7 @@ static void launch_bwd_direct(fh_encoder e, const float4 *c4, int64_t N, const f
 template <int F>
 static void launch_bwd_ordered(fh_encoder e, const float4 *c4, int64_t N, const float *dout, float *dtable,
                                cudaStream_t s, const uint32_t *perm) {
-    const char *dv = getenv("FH_AGG_MIN_DENSITY");
-    const double dmin = dv ? atof(dv) : 128.0 * F;
+    const double dmin = e->agg_density >= 0.0 ? e->agg_density : 128.0 * F;
     bool agg[FH_MAX_LEVELS], rest[FH_MAX_LEVELS];
     for (int l = 0; l < e->L; l++) {
         double cells = 1.0;
@@ -278,8 +278,7 @@ static void launch_bwd_ordered(fh_encoder e, const float4 *c4, int64_t N, const 
         fh::tiled::bwd_agg_kernel<F><<<grid, fh::tiled::kAggThreads, smem, s>>>(e->params, lists[g], c4, N, perm, dout,
                                                                            dtable, e->flag);
     }
-    const char *fo = getenv("FH_FINE_ORDER");
-    launch_bwd_direct<F>(e, c4, N, dout, dtable, s, (fo && atoi(fo) == 1) ? perm : nullptr, rest);
+    launch_bwd_direct<F>(e, c4, N, dout, dtable, s, e->fine_order ? perm : nullptr, rest);
 }
 
 static fh_status check_common(fh_encoder e, const float *coords, int64_t N, const char *who) {

@@ -58,4 +58,10 @@ struct fh_encoder_s {
     fh::KeySpec key{};                               // Morton key of fh_spatial_sort (set by the builder)
     int n_sm = 148;                                  // SMs of the device (set with the status word)
     int smem_optin = 0;                              // max dynamic shared memory per CTA (opt-in)
+    // ordered-path knobs, read once from the environment when the encoder
+    // binds to its device (experiments; defaults in fhash_api.cu)
+    int tile_s = 0;                                  // FH_TILE_S: samples per tile (0 = auto)
+    double tile_margin = 1.25;                       // FH_TILE_MARGIN
+    bool fine_order = false;                         // FH_FINE_ORDER=1: direct levels in `order`
+    double agg_density = -1.0;                       // FH_AGG_MIN_DENSITY (< 0: 128 F)
 };
