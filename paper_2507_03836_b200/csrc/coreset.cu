@@ -163,7 +163,40 @@ __global__ void __launch_bounds__(kThreads) feature_kernel(const float *__restri
         const float *r = vol + (uint64_t)row * d.X;   // rows of [n][Z][Y][X] are contiguous
         uint32_t *frow = f + (uint64_t)row * d.Wx;
         const uint32_t y = row % d.Y, z = (row / d.Y) % d.Z, k = row / (d.Y * d.Z);
-        for (uint32_t w0 = 0; w0 < d.Wx; w0 += kFeatUnroll) {
+        uint32_t w_begin = 0;
+        if (s.kind != FH_FEAT_ISOSURFACE && (d.X & 3u) == 0 && (reinterpret_cast<uintptr_t>(vol) & 15u) == 0) {
+            // 128 vertices (4 words) per step: lane l loads vertices 4l .. 4l+3
+            // as one float4; ballot j has bit l = vertex 4l + j, so word w
+            // takes byte w of the four ballots, spread to bits 4i + j.
+            const uint32_t groups = d.X / 128;
+            const float4 *r4 = reinterpret_cast<const float4 *>(r);
+            for (uint32_t q0 = 0; q0 < groups; q0 += 2) {
+                float4 v[2];
+#pragma unroll
+                for (int u = 0; u < 2; u++)
+                    v[u] = q0 + u < groups ? __ldg(r4 + (q0 + u) * 32 + lane) : make_float4(0.f, 0.f, 0.f, 0.f);
+#pragma unroll
+                for (int u = 0; u < 2; u++) {
+                    if (q0 + u >= groups) break;   // warp-uniform
+                    const uint32_t b0 = __ballot_sync(0xffffffffu, feature_test(v[u].x, s));
+                    const uint32_t b1 = __ballot_sync(0xffffffffu, feature_test(v[u].y, s));
+                    const uint32_t b2 = __ballot_sync(0xffffffffu, feature_test(v[u].z, s));
+                    const uint32_t b3 = __ballot_sync(0xffffffffu, feature_test(v[u].w, s));
+                    if (lane < 4) {
+                        auto spread = [](uint32_t x) {   // bit i -> bit 4 i (i < 8)
+                            x = (x | (x << 12)) & 0x000F000Fu;
+                            x = (x | (x << 6)) & 0x03030303u;
+                            return (x | (x << 3)) & 0x11111111u;
+                        };
+                        const uint32_t sh = 8u * lane;
+                        frow[(q0 + u) * 4 + lane] = spread((b0 >> sh) & 0xFFu) | (spread((b1 >> sh) & 0xFFu) << 1) |
+                                                    (spread((b2 >> sh) & 0xFFu) << 2) | (spread((b3 >> sh) & 0xFFu) << 3);
+                    }
+                }
+            }
+            w_begin = groups * 4;
+        }
+        for (uint32_t w0 = w_begin; w0 < d.Wx; w0 += kFeatUnroll) {
             float v[kFeatUnroll];
 #pragma unroll
             for (int u = 0; u < kFeatUnroll; u++) {
