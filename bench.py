@@ -294,7 +294,7 @@ def hbm_regime_bench(fh, torch, W, steps, copy_gbs):
             "hbm_bytes_per_step": hbm_fwd + hbm_bwd}
 
 
-def train_step_bench(fh, torch, W, which, rank, world, dist, steps, warmup):
+def train_step_bench(fh, torch, W, which, rank, world, dist, steps, warmup, dp_mode="nccl"):
     """All §8(a) rows in one step: Philox voxel sampling from the synthetic
     field, encode fwd (fp16 table -> bf16), tcgen05 MLP fwd + MSE + bwd,
     encode bwd, [NCCL all-reduce of the flat fp32 grads over NVLink when
@@ -314,7 +314,9 @@ def train_step_bench(fh, torch, W, which, rank, world, dist, steps, warmup):
     enc = fh.Encoder(cfg.levels, cfg.F, cfg.table_dtype, cfg.cap)
     gen = torch.Generator("cuda").manual_seed(0)           # identical init on every rank
     table0 = (torch.rand((enc.entries, cfg.F), device="cuda", generator=gen) * 2 - 1) * 1e-4
-    tr = fh.Trainer(enc, table0, W.draw_mlp(W.rng(0), mlp), n_local, world=world)
+    peer = world > 1 and dp_mode == "peer"
+    tr = fh.Trainer(enc, table0, W.draw_mlp(W.rng(0), mlp), n_local, world=world,
+                    alloc=dp.symm_alloc if peer else None)
     del table0
     coords = torch.empty((n_local, 4), device="cuda")
     target = torch.empty((n_local,), device="cuda")
@@ -326,7 +328,9 @@ def train_step_bench(fh, torch, W, which, rank, world, dist, steps, warmup):
     # table shadow.  Falls back to dp.ShardedDP (no overlap) if the plan
     # needs more than 63 Adam ranges.
     sdp = None
-    if world > 1:
+    if peer:
+        sdp = dp.PeerShardedDP(tr)     # --dp peer: fused reduce + Adam + all-gather over NVLink peer memory
+    elif world > 1:
         try:
             sdp = dp.OverlappedShardedDP(tr)
         except ValueError:
@@ -338,7 +342,7 @@ def train_step_bench(fh, torch, W, which, rank, world, dist, steps, warmup):
         if ev: ev[1].record(stream)
         loss = tr.fwd_bwd(coords, target, n_global)
         if ev: ev[2].record(stream)
-        if isinstance(sdp, dp.OverlappedShardedDP):
+        if isinstance(sdp, (dp.OverlappedShardedDP, dp.PeerShardedDP)):
             if ev: ev[3].record(stream)   # the reduction already overlaps the backward
             sdp.reduce_and_apply()
         elif sdp:
@@ -423,7 +427,9 @@ def train_step_bench(fh, torch, W, which, rank, world, dist, steps, warmup):
         "scaling": "strong" if which == "cfg5" else "weak",
         "phase_ms": {"sample": phase[0], "fwd_bwd": phase[1], "grad_reduce": phase[2],
                      "adam_and_gather": phase[3]},
-        "dp": ("per-backward-launch reduce-scatter overlapped with the backward + sharded Adam + all-gather (NCCL)"
+        "dp": ("per-level-group fused reduce + Adam + shadow broadcast over NVLink peer memory (fh_train_apply_peers)"
+               if isinstance(sdp, dp.PeerShardedDP) else
+               "per-backward-launch reduce-scatter overlapped with the backward + sharded Adam + all-gather (NCCL)"
                if isinstance(sdp, dp.OverlappedShardedDP) else
                "reduce-scatter + sharded Adam + all-gather (NCCL)" if world > 1 else "single GPU"),
         "infer": {"what": "fh_infer: encode fwd + tcgen05 MLP forward (Alg. 1 V = model(S))",
@@ -653,9 +659,9 @@ def run_ours(args, rank, local_rank, world):
         torch.cuda.empty_cache()
         kt = max(3, min(K, 10))
         if world == 1:
-            train["cfg3"] = train_step_bench(fh, torch, W, "cfg3", rank, world, dist, kt, args.warmup)
+            train["cfg3"] = train_step_bench(fh, torch, W, "cfg3", rank, world, dist, kt, args.warmup, args.dp)
             torch.cuda.empty_cache()
-        train["cfg5"] = train_step_bench(fh, torch, W, "cfg5", rank, world, dist, kt, args.warmup)
+        train["cfg5"] = train_step_bench(fh, torch, W, "cfg5", rank, world, dist, kt, args.warmup, args.dp)
         torch.cuda.empty_cache()
     encoders = paper_encoder_compare(fh, torch, W, max(3, min(K, 10))) if not args.no_train else None
     torch.cuda.empty_cache()
@@ -716,6 +722,9 @@ def main():
     ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--no-train", action="store_true", help="skip the train_step (cfg3 / cfg5) sub-benchmarks")
+    ap.add_argument("--dp", default="nccl", choices=["nccl", "peer"],
+                    help="N>1 gradient path: NCCL reduce-scatter overlapped with the backward (default), or the "
+                         "fused peer-memory reduce + Adam + all-gather kernel (torch symmetric memory)")
     args = ap.parse_args()
     rank = env_int("RANK", 0)
     local_rank = env_int("LOCAL_RANK", 0)

@@ -358,6 +358,28 @@ fh_status fh_train_set_bwd_events(fh_trainer tr, void *const *events, int n);
 fh_status fh_train_apply_ranges(fh_trainer tr, int n, const int64_t *begin, const int64_t *end,
                                 const float *const *grad, fh_stream stream);
 
+/* ---- fused reduce-scatter + Adam + all-gather over peer memory (§8(e) 3)
+ * fh_train_apply_peers: ONE kernel per call, for a data-parallel group of W
+ * ranks (1 <= W <= 8) whose gradient and shadow buffers are mapped into
+ * this process (e.g. torch symmetric memory over NVLink / NVSwitch).  For
+ * every table element range [begin_i, end_i) it reads the gradient as the
+ * SUM over ranks r = 0..W-1 (in that order) of peer_table_grad[r][e], runs
+ * Adam on this trainer's fp32 master / moments, and stores the fp16 value
+ * into peer_table_shadow[r][e] of EVERY rank (broadcast[i] = 1: this rank's
+ * chunk) or only into its own shadow (broadcast[i] = 0: a range every rank
+ * updates identically).  with_mlp = 1 also updates the MLP from the sum of
+ * peer_mlp_grad[r].  new_step = 1 on the first call of a step (step
+ * counter += 1; later calls of the same step pass 0).  Does NOT zero any
+ * gradient (peers may still be reading them): the caller zeroes its local
+ * grads once every rank is done, and orders the call after every rank's
+ * backward (e.g. a symmetric-memory barrier).  Pointers: device-accessible
+ * (peer) addresses of each rank's flat table grad [entries*F] f32, fp16
+ * shadow, and MLP grad.  Errors: FH_E_ARG, FH_E_STATE (no fp16 shadow). */
+fh_status fh_train_apply_peers(fh_trainer tr, int W, const float *const *peer_table_grad,
+                               void *const *peer_table_shadow, const float *const *peer_mlp_grad, int n,
+                               const int64_t *begin, const int64_t *end, const int *broadcast, int with_mlp,
+                               int new_step, fh_stream stream);
+
 /* fh_train_fwd_bwd + fh_train_apply (single GPU). */
 fh_status fh_train_step(fh_trainer tr, const float *coords, const float *target, int64_t N_local,
                         int64_t N_global, float *loss_dev, fh_stream stream);

@@ -635,5 +635,60 @@ __global__ void __launch_bounds__(256) adam_kernel(const __grid_constant__ AdamA
         for (int64_t i = n4 * 4 + threadIdx.x; i < s.n; i += blockDim.x) adam_one(A, s, i);
 }
 
+// ------------------------------------------------------------ fused DP step
+// Reduce-scatter + Adam + all-gather in ONE kernel over peer memory
+// (on NVLink peer pointers instead of an NVLS
+// multicast object): segment i is a range of the flat table (or the MLP)
+// that this rank updates; its gradient is the SUM over the W ranks' grad
+// buffers read through peer pointers, Adam runs in registers on the local
+// master / moments, and the fp16 shadow is stored into every rank's shadow
+// buffer (broadcast segments: this rank's chunk) or only the local one
+// (replicated segments every rank computes identically).  The caller orders
+// it against the other ranks (all of them finished the gradients it reads;
+// nobody reuses them before every rank is done).
+constexpr int kMaxPeers = 8;
+
+struct PeerArgs {
+    const float *pg[kMaxPeers];    // each rank's flat table grad buffer
+    __half *psh[kMaxPeers];        // each rank's fp16 table shadow
+    const float *pmg[kMaxPeers];   // each rank's MLP grad buffer
+    int W;
+    int64_t off[kMaxAdamSeg];      // element offset of segment i in the peer buffers
+    int src[kMaxAdamSeg];          // 0: table grads, 1: MLP grads
+    int bcast[kMaxAdamSeg];        // 1: store the fp16 shadow into every rank's buffer
+};
+
+__global__ void __launch_bounds__(256) adam_peers_kernel(const __grid_constant__ AdamArgs A,
+                                                         const __grid_constant__ PeerArgs P) {
+    int si = 0;
+    while (si + 1 < A.nseg && (int64_t)blockIdx.x >= A.block0[si + 1]) si++;
+    const AdamSeg &s = A.seg[si];
+    const int64_t b = (int64_t)blockIdx.x - A.block0[si];
+    const int64_t nb = A.block0[si + 1] - A.block0[si];
+    const float *const *G = P.src[si] ? P.pmg : P.pg;
+    const int64_t off = P.off[si];
+    auto update = [&](int64_t i, float g) {
+        const float m = fmaf(A.b1, s.m[i], A.omb1 * g);
+        const float v = fmaf(A.b2, s.v[i], A.omb2 * g * g);
+        const float p = s.p[i] - A.lr * (m * A.c1) / (sqrtf(v * A.c2) + A.eps);
+        s.m[i] = m; s.v[i] = v; s.p[i] = p;
+        if (s.kind == 2) {
+            reinterpret_cast<__nv_bfloat16 *>(s.shadow)[i] = __float2bfloat16_rn(p);
+        } else if (s.kind == 1) {
+            const __half h = __float2half_rn(p);
+            if (P.bcast[si]) {
+                for (int r = 0; r < P.W; r++) P.psh[r][off + i] = h;
+            } else {
+                reinterpret_cast<__half *>(s.shadow)[i] = h;
+            }
+        }
+    };
+    for (int64_t i = b * blockDim.x + threadIdx.x; i < s.n; i += nb * blockDim.x) {
+        float g = 0.f;
+        for (int r = 0; r < P.W; r++) g += G[r][off + i];   // ranks in order: same sum on every rank
+        update(i, g);
+    }
+}
+
 }  // namespace mlp
 }  // namespace fh

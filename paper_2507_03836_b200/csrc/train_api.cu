@@ -285,6 +285,92 @@ fh_status fh_train_apply_ranges(fh_trainer tr, int n, const int64_t *begin, cons
                       "zero mlp_grad");
 }
 
+fh_status fh_train_apply_peers(fh_trainer tr, int W, const float *const *peer_table_grad,
+                               void *const *peer_table_shadow, const float *const *peer_mlp_grad, int n,
+                               const int64_t *begin, const int64_t *end, const int *broadcast, int with_mlp,
+                               int new_step, fh_stream stream) {
+    using fh::mlp::AdamArgs;
+    using fh::mlp::AdamSeg;
+    using fh::mlp::PeerArgs;
+    g_err[0] = 0;
+    if (!tr) return fail(FH_E_ARG, "fh_train_apply_peers: NULL trainer");
+    if (W < 1 || W > fh::mlp::kMaxPeers) return fail(FH_E_ARG, "fh_train_apply_peers: W = %d not in [1, 8]", W);
+    if (!tr->b.table_shadow) return fail(FH_E_STATE, "fh_train_apply_peers: needs an fp16 table shadow");
+    if (n < 0 || n + (with_mlp ? 1 : 0) > fh::mlp::kMaxAdamSeg || (n > 0 && (!begin || !end || !broadcast)))
+        return fail(FH_E_ARG, "fh_train_apply_peers: bad range list (n = %d)", n);
+    if (!peer_table_grad || !peer_table_shadow || (with_mlp && !peer_mlp_grad))
+        return fail(FH_E_ARG, "fh_train_apply_peers: NULL peer pointer table");
+    for (int r = 0; r < W; r++)
+        if (!peer_table_grad[r] || !peer_table_shadow[r] || (with_mlp && !peer_mlp_grad[r]))
+            return fail(FH_E_ARG, "fh_train_apply_peers: NULL pointer for rank %d", r);
+    const int64_t nt = (int64_t)(tr->enc->entries * (uint64_t)tr->enc->F);
+    for (int i = 0; i < n; i++)
+        if (begin[i] < 0 || end[i] < begin[i] || end[i] > nt)
+            return fail(FH_E_ARG, "fh_train_apply_peers: range %d outside the table", i);
+    if (new_step) tr->step += 1;
+    if (tr->step < 1) return fail(FH_E_STATE, "fh_train_apply_peers: first call of a step must set new_step");
+    const double t = (double)tr->step;
+    AdamArgs A;
+    PeerArgs P;
+    memset(&A, 0, sizeof(A));
+    memset(&P, 0, sizeof(P));
+    A.lr = tr->adam.lr;
+    A.b1 = tr->adam.beta1;
+    A.b2 = tr->adam.beta2;
+    A.eps = tr->adam.eps;
+    A.omb1 = (float)(1.0 - (double)tr->adam.beta1);
+    A.omb2 = (float)(1.0 - (double)tr->adam.beta2);
+    A.c1 = (float)(1.0 / (1.0 - std::pow((double)tr->adam.beta1, t)));
+    A.c2 = (float)(1.0 / (1.0 - std::pow((double)tr->adam.beta2, t)));
+    P.W = W;
+    for (int r = 0; r < W; r++) {
+        P.pg[r] = peer_table_grad[r];
+        P.psh[r] = reinterpret_cast<__half *>(peer_table_shadow[r]);
+        P.pmg[r] = with_mlp ? peer_mlp_grad[r] : nullptr;
+    }
+    const int64_t cap = (int64_t)tr->n_sm * 16;
+    int64_t blocks = 0;
+    int k = 0;
+    auto add = [&](AdamSeg g, int64_t off, int src, int bc) {
+        if (g.n <= 0) return;
+        int64_t want = (g.n + 256 * 4 - 1) / (256 * 4);
+        if (want > cap) want = cap;
+        if (want < 1) want = 1;
+        A.seg[k] = g;
+        P.off[k] = off;
+        P.src[k] = src;
+        P.bcast[k] = bc;
+        A.block0[k] = blocks;
+        blocks += want;
+        k++;
+    };
+    for (int i = 0; i < n; i++) {
+        AdamSeg T{};
+        T.p = tr->b.table_master + begin[i];
+        T.m = tr->b.table_m + begin[i];
+        T.v = tr->b.table_v + begin[i];
+        T.shadow = reinterpret_cast<__half *>(tr->b.table_shadow) + begin[i];
+        T.n = end[i] - begin[i];
+        T.kind = 1;
+        add(T, begin[i], 0, broadcast[i] ? 1 : 0);
+    }
+    if (with_mlp) {
+        AdamSeg M{};
+        M.p = tr->b.mlp_master;
+        M.m = tr->b.mlp_m;
+        M.v = tr->b.mlp_v;
+        M.shadow = tr->b.mlp_shadow;
+        M.n = fh::mlp::param_count(tr->K0);
+        M.kind = 2;
+        add(M, 0, 1, 0);
+    }
+    if (k == 0) return FH_OK;
+    A.nseg = k;
+    A.block0[k] = blocks;
+    fh::mlp::adam_peers_kernel<<<(unsigned)blocks, 256, 0, reinterpret_cast<cudaStream_t>(stream)>>>(A, P);
+    return cuda_check(cudaGetLastError(), "adam_peers_kernel launch");
+}
+
 fh_status fh_train_apply_sharded(fh_trainer tr, int64_t begin, int64_t end, const float *grad_shard,
                                  fh_stream stream) {
     g_err[0] = 0;

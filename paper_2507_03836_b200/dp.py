@@ -232,6 +232,84 @@ class OverlappedShardedDP:
             dist.all_gather_into_tensor(flat[a:a + m], mine, group=self.group)
 
 
+def symm_alloc(n: int, dtype, device):
+    """Trainer(alloc=...) hook: grads / shadow in torch symmetric memory, so
+    every rank can map every other rank's buffers (PeerShardedDP)."""
+    import torch.distributed._symmetric_memory as sm
+    return sm.empty(n, dtype=dtype, device=device)
+
+
+class PeerShardedDP:
+    """The reduction fused with the optimiser over peer memory (SURVEY.md
+    §8(e) item 3, with NVLink peer pointers of torch symmetric memory in
+    place of an NVLS multicast object).  Per backward level group, once
+    every rank has finished it (a symmetric-memory barrier on the
+    communication stream, queued behind the group's event), ONE kernel
+    (fh_train_apply_peers) sums this rank's chunk of the group over all
+    ranks' gradient buffers, runs Adam, and stores the fp16 shadow into every
+    rank's shadow buffer -- reduce-scatter, Adam and all-gather in one pass,
+    overlapped with the later groups' backward.  The tails of overlap_plan
+    and the MLP are summed and updated redundantly on every rank at the end;
+    a last barrier precedes zeroing the local gradients.  The trainer must
+    be built with alloc=dp.symm_alloc."""
+
+    def __init__(self, trainer, group=None):
+        import torch
+        import torch.distributed as dist
+        import torch.distributed._symmetric_memory as sm
+        self.tr = trainer
+        if trainer.shadow_flat is None:
+            raise ValueError("PeerShardedDP needs an fp16 table shadow")
+        grp = group or dist.group.WORLD
+        name = grp.group_name
+        self.hg = sm.rendezvous(trainer.grads, name)
+        self.hs = sm.rendezvous(trainer.shadow_flat, name)
+        self.world, self.rank = self.hg.world_size, self.hg.rank
+        if self.world > 8:
+            raise ValueError("PeerShardedDP supports up to 8 ranks")
+        og, osh = int(getattr(self.hg, "offset", 0)), int(getattr(self.hs, "offset", 0))
+        self.pg = [int(p) + og for p in self.hg.buffer_ptrs]
+        self.ps = [int(p) + osh for p in self.hs.buffer_ptrs]
+        self.pm = [p + trainer.nt_pad * 4 for p in self.pg]
+        self.launches = trainer.bwd_launch_ranges()
+        self.mains, self.tails = overlap_plan(self.launches, self.world, self.rank)
+        self.by_launch = [[] for _ in self.launches]
+        for (li, a, m) in self.mains:
+            c = m // self.world
+            self.by_launch[li].append((a + self.rank * c, a + (self.rank + 1) * c))
+        self.comm = torch.cuda.Stream(device=trainer.grads.device)
+        self.events = [torch.cuda.Event() for _ in self.launches]
+        for ev in self.events:
+            ev.record()
+        trainer.set_bwd_events(self.events)
+
+    def step(self, coords, target, n_global: int, stream=None):
+        loss = self.tr.fwd_bwd(coords, target, n_global, stream=stream)
+        self.reduce_and_apply(stream=stream)
+        return loss
+
+    def reduce_and_apply(self, stream=None):
+        import torch
+        tr = self.tr
+        cur = torch.cuda.current_stream() if stream is None else stream
+        first = True
+        with torch.cuda.stream(self.comm):
+            for li, ranges in enumerate(self.by_launch):
+                self.comm.wait_event(self.events[li])   # this rank's group li is final
+                self.hg.barrier(channel=0)              # ... and every other rank's
+                if ranges:
+                    tr.apply_peers(self.pg, self.ps, self.pm, ranges, [1] * len(ranges), False, first,
+                                   stream=self.comm)
+                    first = False
+            self.comm.wait_stream(cur)                  # the whole local step (tails, MLP grads)
+            self.hg.barrier(channel=0)
+            tr.apply_peers(self.pg, self.ps, self.pm, self.tails, [0] * len(self.tails), True, first,
+                           stream=self.comm)
+            self.hg.barrier(channel=0)                  # every rank done reading gradients
+            tr.grads.zero_()
+        cur.wait_stream(self.comm)
+
+
 def replicas_identical(tensor, group=None) -> bool:
     """True when `tensor` is bit-identical on every rank (compares a 64-bit
     checksum of its bytes gathered from all ranks)."""

@@ -35,6 +35,7 @@ EXPORTS = [
     "fh_mlp_param_count", "fh_train_workspace_size", "fh_trainer_create", "fh_train_fwd_bwd", "fh_train_apply",
     "fh_train_step", "fh_trainer_status", "fh_trainer_step_count", "fh_trainer_destroy", "fh_train_apply_sharded",
     "fh_train_bwd_launches", "fh_train_bwd_ranges", "fh_train_set_bwd_events", "fh_train_apply_ranges",
+    "fh_train_apply_peers",
     # inference (renderer's model evaluation) and the ARM pace rule
     "fh_infer_workspace_size", "fh_infer", "fh_arm_pace",
     # include/fhash_coreset.h (NEXT-4 coreset selection)
@@ -309,6 +310,10 @@ def _train_lib():
     L.fh_train_apply_ranges.argtypes = [vp, ctypes.c_int, ctypes.POINTER(i64), ctypes.POINTER(i64),
                                         ctypes.POINTER(vp), vp]
     L.fh_train_apply_ranges.restype = ctypes.c_int
+    L.fh_train_apply_peers.argtypes = [vp, ctypes.c_int, ctypes.POINTER(vp), ctypes.POINTER(vp), ctypes.POINTER(vp),
+                                       ctypes.c_int, ctypes.POINTER(i64), ctypes.POINTER(i64),
+                                       ctypes.POINTER(ctypes.c_int), ctypes.c_int, ctypes.c_int, vp]
+    L.fh_train_apply_peers.restype = ctypes.c_int
     L.fh_infer_workspace_size.argtypes = [vp, ctypes.POINTER(MLPDesc), i64]
     L.fh_infer_workspace_size.restype = ctypes.c_size_t
     L.fh_infer.argtypes = [vp, ctypes.POINTER(MLPDesc), vp, vp, vp, vp, i64, vp, vp, ctypes.c_size_t, vp]
@@ -335,10 +340,12 @@ class Trainer:
     apply()."""
 
     def __init__(self, enc: "Encoder", table_init, mlp_layers, max_batch: int, lr: float = 0.01,
-                 beta1: float = 0.9, beta2: float = 0.999, eps: float = 1e-8, world: int = 1):
+                 beta1: float = 0.9, beta2: float = 0.999, eps: float = 1e-8, world: int = 1, alloc=None):
         # world > 1: the flat table region of grads and shadow is padded to a
         # multiple of 4 * world so it splits into equal 16-byte-aligned shards
         # (reduce-scatter / sharded Adam / all-gather, dp.sharded_step).
+        # alloc(numel, dtype, device): allocator of the grads and shadow
+        # buffers (e.g. torch symmetric memory for dp.PeerShardedDP).
         import numpy as np
         import torch
         L = _train_lib()
@@ -359,11 +366,17 @@ class Trainer:
             self.table_master = torch.as_tensor(np.asarray(table_init, dtype=np.float32)).reshape(
                 enc.entries, enc.F).to(dev)
         self.table_shadow, self.shadow_flat = None, None
+        def zeros(n, dtype):
+            if alloc is None:
+                return torch.zeros(n, dtype=dtype, device=dev)
+            t = alloc(n, dtype, dev)
+            t.zero_()
+            return t
         if enc.table_dtype == "f16":
-            self.shadow_flat = torch.zeros(nt_pad, dtype=torch.float16, device=dev)
+            self.shadow_flat = zeros(nt_pad, torch.float16)
             self.shadow_flat[:nt].copy_(self.table_master.view(-1))
             self.table_shadow = self.shadow_flat[:nt].view(enc.entries, enc.F)
-        self.grads = torch.zeros(nt_pad + P, **f32)
+        self.grads = zeros(nt_pad + P, torch.float32)
         self.table_grad = self.grads[:nt].view(enc.entries, enc.F)
         self.mlp_grad = self.grads[nt_pad:]
         self.table_m = torch.zeros(nt, **f32)
@@ -456,6 +469,19 @@ class Trainer:
         arr = (ctypes.c_void_p * max(1, len(events)))(*[e.cuda_event for e in events])
         self._events = list(events)   # keep alive
         _check(_train_lib().fh_train_set_bwd_events(self._h, arr, len(events)))
+
+    def apply_peers(self, peer_grads, peer_shadows, peer_mlp_grads, ranges, broadcast, with_mlp, new_step,
+                    stream=None):
+        """fh_train_apply_peers: peer_* are lists of W device addresses (int)."""
+        W, n = len(peer_grads), len(ranges)
+        pg = (ctypes.c_void_p * W)(*peer_grads)
+        ps = (ctypes.c_void_p * W)(*peer_shadows)
+        pm = (ctypes.c_void_p * W)(*peer_mlp_grads)
+        b = (ctypes.c_int64 * max(1, n))(*[r[0] for r in ranges])
+        e = (ctypes.c_int64 * max(1, n))(*[r[1] for r in ranges])
+        bc = (ctypes.c_int * max(1, n))(*[int(x) for x in broadcast])
+        _check(_train_lib().fh_train_apply_peers(self._h, W, pg, ps, pm, n, b, e, bc, int(with_mlp), int(new_step),
+                                                 _stream(stream)))
 
     def apply_ranges(self, ranges, grads, stream=None):
         """One Adam step over table element ranges [(b, e)] with grads (f32

@@ -298,3 +298,71 @@ def test_overlapped_dp_single_rank_equals_plain_step():
         assert torch.equal(ta.mlp_master, tb.mlp_master)
     loss = odp.step(c, t, 2000)        # the composed step runs too
     assert ta.status() == fh.FH_OK and torch.isfinite(loss).all()
+
+
+def test_apply_peers_sums_ranks_and_broadcasts():
+    """fh_train_apply_peers with W = 3 'ranks' simulated by local buffers:
+    the update uses the rank-ordered SUM of the three gradient buffers
+    (bit-identical to Adam on the summed gradient), broadcast ranges land in
+    all three shadow buffers, replicated ranges only in the local one, and
+    the MLP uses the summed MLP gradients."""
+    cfg = small_cfg(2, 16, cap=1 << 10)
+    (_, ta, coords, target), (_, tb, _, _) = [make(cfg, 1500, seed=51) for _ in range(2)]
+    c, t = torch.from_numpy(coords).cuda(), torch.from_numpy(target).cuda()
+    ta.fwd_bwd(c, t)
+    g = torch.Generator("cuda").manual_seed(5)
+    peers = [ta.grads] + [torch.randn(ta.grads.shape, device="cuda", generator=g) * 0.01 for _ in range(2)]
+    shadows = [ta.shadow_flat] + [torch.zeros_like(ta.shadow_flat) for _ in range(2)]
+    total = (peers[0] + peers[1]) + peers[2]
+    nt = ta.n_table
+    half = (nt // 2) // 4 * 4
+    bcast_rng, local_rng = [(0, half)], [(half, nt)]
+    ta.apply_peers([p.data_ptr() for p in peers], [s.data_ptr() for s in shadows],
+                   [p[ta.nt_pad:].data_ptr() for p in peers], bcast_rng + local_rng, [1, 0], True, True)
+    tb.grads.copy_(total)
+    tb.apply()
+    torch.cuda.synchronize()
+    assert torch.equal(ta.table_master, tb.table_master)
+    assert torch.equal(ta.mlp_master, tb.mlp_master)
+    assert torch.equal(ta.table_shadow, tb.table_shadow)
+    for s in shadows[1:]:
+        assert torch.equal(s[:half], ta.shadow_flat[:half])
+        assert torch.all(s[half:nt] == 0)
+    assert ta.step_count == 1
+
+
+def test_peer_sharded_dp_single_rank():
+    """dp.PeerShardedDP on a 1-rank NCCL group with torch symmetric memory:
+    the fused kernel path equals the plain step (same gradients)."""
+    import os
+    import torch.distributed as dist
+    from paper_2507_03836_b200 import dp
+    os.environ.setdefault("MASTER_ADDR", "127.0.0.1")
+    os.environ["MASTER_PORT"] = "29561"
+    dist.init_process_group("nccl", rank=0, world_size=1, device_id=torch.device("cuda", 0))
+    try:
+        cfg = small_cfg(4, 16, cap=1 << 11)
+        g = W.rng(61)
+        enc = fh.Encoder(cfg.levels, cfg.F, cfg.table_dtype, cfg.cap)
+        table = W.draw_table(g, enc.entries, cfg.F, "f32")
+        layers = W.draw_mlp(g, W.MLPConfig((cfg.L * cfg.F, 64, 64, 1)))
+        coords = W.draw_coords(g, 2000)
+        target = g.random(2000, dtype=np.float32)
+        ta = fh.Trainer(enc, table, layers, 2000, alloc=dp.symm_alloc)
+        tb = fh.Trainer(enc, table, layers, 2000)
+        pdp = dp.PeerShardedDP(ta)
+        c, t = torch.from_numpy(coords).cuda(), torch.from_numpy(target).cuda()
+        for _ in range(3):
+            ta.fwd_bwd(c, t)
+            tb.grads.copy_(ta.grads)
+            pdp.reduce_and_apply()
+            tb.apply()
+            torch.cuda.synchronize()
+            assert torch.equal(ta.table_master, tb.table_master)
+            assert torch.equal(ta.table_shadow, tb.table_shadow)
+            assert torch.equal(ta.mlp_master, tb.mlp_master)
+            assert torch.all(ta.grads == 0)
+        loss = pdp.step(c, t, 2000)
+        assert ta.status() == fh.FH_OK and torch.isfinite(loss).all()
+    finally:
+        dist.destroy_process_group()
