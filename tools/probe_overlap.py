@@ -28,7 +28,7 @@ def run(name, iters=10):
     od = "f32" if name == "cfg2" else "bf16"
     e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
     res = {}
-    for mode in ("serial", "concurrent", "serial"):
+    for mode in ("serial", "concurrent"):
         tot = 0.0
         for it in range(iters + 2):
             flush.fill_(it & 255)
