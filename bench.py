@@ -478,8 +478,12 @@ def paper_encoder_compare(fh, torch, W, steps):
             if it >= 3:
                 tot += e0.elapsed_time(e1)
         ms = tot / steps
+        # encoding_stats (fh_level_stats, S:330-338 / Fig. 4): collisions and bucket utilisation
+        st = [enc.level_stats(l) for l in range(enc.L)]
         res[name] = {"levels": enc.L, "params": enc.param_count, "params_Mi": round(enc.param_count / 2 ** 20, 2),
-                     "fwd_bwd_ms": ms, "samples_per_s": B / (ms / 1e3)}
+                     "fwd_bwd_ms": ms, "samples_per_s": B / (ms / 1e3),
+                     "collisions": sum(c for _, c, _ in st),
+                     "utilisation_per_level": [round(u, 4) for _, _, u in st]}
         del table, out, g, dt
     res["workload"] = ("Combustion-Seg shape: FBB 200x110x54, 10 key frames, batch 2^21 voxel samples; "
                        "F-Hash fold 2 (Eqs. 4-8; Eq. 9 and brick linearization) vs MHE T=2^20 x 6 levels "

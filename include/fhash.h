@@ -408,6 +408,22 @@ fh_status fh_infer(fh_encoder enc, const fh_mlp_desc *mlp, const void *table, co
  * the paper; R19), integer division.  0 when no ray is alive. */
 int64_t   fh_arm_pace(int64_t n_rays, int64_t n_alive);
 
+/* ============================================================ encoding stats
+ * fh_level_stats -- encoding_stats of one level (the
+ * collision / bucket-waste contrast of Fig. 4): every lattice
+ * vertex of the level (for an MHE encoder: of one key frame's R^3 grid) is
+ * mapped to its bucket exactly as the encode maps corners, and *out (device,
+ * uint64) receives the number of DISTINCT buckets hit.  With C vertices
+ * (fh_level_info corners; R^3 for MHE) and T buckets (table_size; the MHE
+ * T): collisions = C - distinct, utilisation = distinct / T.  F-Hash levels
+ * (Eq. 9 / brick) give distinct = C = T.  Exhaustive -- a diagnostic, not on
+ * the train path.  workspace (device, 16-byte aligned) of
+ * fh_level_stats_workspace_size(enc, level) bytes (a T-bit bitmap).
+ * Errors: FH_E_ARG, FH_E_CUDA. */
+size_t    fh_level_stats_workspace_size(fh_encoder enc, int level);
+fh_status fh_level_stats(fh_encoder enc, int level, void *workspace, size_t workspace_bytes, uint64_t *out,
+                         fh_stream stream);
+
 /* Thread-local text of the last error on this thread ("" if none). */
 const char *fh_last_error(void);
 

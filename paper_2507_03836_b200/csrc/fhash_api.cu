@@ -799,3 +799,5 @@ fh_status fh_status_sync(fh_encoder e, fh_stream stream) {
 }
 
 }  // extern "C"
+
+#include "stats.cuh"

@@ -35,7 +35,7 @@ EXPORTS = [
     "fh_mlp_param_count", "fh_train_workspace_size", "fh_trainer_create", "fh_train_fwd_bwd", "fh_train_apply",
     "fh_train_step", "fh_trainer_status", "fh_trainer_step_count", "fh_trainer_destroy", "fh_train_apply_sharded",
     "fh_train_bwd_launches", "fh_train_bwd_ranges", "fh_train_set_bwd_events", "fh_train_apply_ranges",
-    "fh_train_apply_peers",
+    "fh_train_apply_peers", "fh_level_stats_workspace_size", "fh_level_stats",
     # inference (renderer's model evaluation) and the ARM pace rule
     "fh_infer_workspace_size", "fh_infer", "fh_arm_pace",
     # include/fhash_coreset.h (NEXT-4 coreset selection)
@@ -95,6 +95,10 @@ def lib() -> ctypes.CDLL:
                                ctypes.POINTER(vp)]
     L.fh_build_mhe.restype = c_int
     L.fh_encoder_kind.argtypes = [vp]
+    L.fh_level_stats_workspace_size.argtypes = [vp, c_int]
+    L.fh_level_stats_workspace_size.restype = ctypes.c_size_t
+    L.fh_level_stats.argtypes = [vp, c_int, vp, ctypes.c_size_t, vp, vp]
+    L.fh_level_stats.restype = c_int
     L.fh_spatial_sort_workspace_size.argtypes = [i64]
     L.fh_spatial_sort_workspace_size.restype = ctypes.c_size_t
     L.fh_spatial_sort.argtypes = [vp, vp, i64, vp, vp, ctypes.c_size_t, vp]
@@ -220,6 +224,23 @@ class Encoder:
         _check(lib().fh_encode_bwd_ordered(self._h, _ptr(coords), coords.shape[0], _ptr(order), _ptr(dout),
                                            _ptr(dtable), _stream(stream)))
         return dtable
+
+    def level_stats(self, l: int, stream=None):
+        """encoding_stats of level l on the GPU (fh_level_stats): (distinct
+        buckets, collisions, utilisation) -- same tuple as the oracle's."""
+        import torch
+        L = lib()
+        ws = int(L.fh_level_stats_workspace_size(self._h, l))
+        w = torch.empty(ws, dtype=torch.uint8, device="cuda")
+        out = torch.zeros(1, dtype=torch.int64, device="cuda")
+        _check(L.fh_level_stats(self._h, l, _ptr(w), ws, _ptr(out), _stream(stream)))
+        d = int(out.item())
+        info = self.level_info(l)
+        if isinstance(self, MHEEncoder):
+            C, T = info["res"][0] ** 3, self.T
+        else:
+            C, T = info["corners"], info["table_size"]
+        return d, C - d, d / T
 
     def sort_bits(self):
         """(bits per axis [4], axis of each of the 16 key bits, LSB first)."""
