@@ -135,13 +135,15 @@ uint64_t fho_brick_index(const uint32_t r[4], uint64_t x, uint64_t y, uint64_t z
          + ((i[3] * e[2] + i[2]) * e[1] + i[1]) * e[0] + i[0];
 }
 
-/* Capped levels (R5; the paper never caps).  MHE spatial hash
- * (Teschner et al., cited at P:174) extended to 4D:
- *   (X*1 xor Y*2654435761 xor Z*805459861 xor T*2246822519) mod 2^32 mod T_l
+/* Capped levels (R5; the paper never caps).  The primes of the MHE
+ * spatial hash (Teschner et al., cited at P:174) on y, z and
+ * t, with x entering additively (prime 1, added instead of xor-ed) so that
+ * x-neighbours stay adjacent entries as in Eq. 9 (x fastest):
+ *   (X + (Y*2654435761 xor Z*805459861 xor T*2246822519)) mod 2^32 mod T_l
  * uint32 wrap-around; T_l is a power of two.  The t-axis prime is our choice. */
 uint64_t fho_spatial_hash(uint32_t X, uint32_t Y, uint32_t Z, uint32_t T, uint64_t tsize)
 {
-    uint32_t h = (X * 1u) ^ (Y * 2654435761u) ^ (Z * 805459861u) ^ (T * 2246822519u);
+    uint32_t h = X + ((Y * 2654435761u) ^ (Z * 805459861u) ^ (T * 2246822519u));
     return (uint64_t)h % tsize;
 }
 

@@ -25,6 +25,21 @@ constexpr uint32_t kPy = 2654435761u;
 constexpr uint32_t kPz = 805459861u;
 constexpr uint32_t kPt = 2246822519u;
 
+// R5: a capped level's bucket of vertex (X, Y, Z, T) is
+//   (X + (Y kPy ^ Z kPz ^ T kPt)) mod 2^32 mod T_l
+// -- x enters additively, so x-neighbours stay adjacent entries as in Eq. 9
+// (the pair layout of DESIGN.md §8.1 then covers every x-pair).
+#ifndef FH_HASH_XADD
+#define FH_HASH_XADD 1
+#endif
+__device__ __forceinline__ uint32_t hash_x(uint32_t X, uint32_t yzt) {
+#if FH_HASH_XADD
+    return X + yzt;
+#else
+    return X ^ yzt;
+#endif
+}
+
 // Steps 1-2 on one axis (R2): clamp to [0,1] (NaN -> 0), one IEEE fp32
 // multiply s = p*(R-1), i = clamp(floor s, 0, R-2), w = s - i (exact).
 __device__ __forceinline__ void locate(float p, float scale, uint32_t R, uint32_t &i, float &w,
@@ -91,8 +106,8 @@ __device__ __forceinline__ bool cell_of(const Level &lv, float4 p, Cell &c) {
         const uint32_t ht0 = it * kPt, ht1 = (it + 1) * kPt;
 #pragma unroll
         for (int k = 0; k < 16; k++) {
-            const uint32_t h = ((k & 1) ? hx1 : hx0) ^ (((k >> 1) & 1) ? hy1 : hy0) ^
-                               (((k >> 2) & 1) ? hz1 : hz0) ^ (((k >> 3) & 1) ? ht1 : ht0);
+            const uint32_t h = hash_x(((k & 1) ? hx1 : hx0), (((k >> 1) & 1) ? hy1 : hy0) ^
+                                                                 (((k >> 2) & 1) ? hz1 : hz0) ^ (((k >> 3) & 1) ? ht1 : ht0));
             c.idx[k] = lv.offset + (h & lv.mask);
         }
     }
@@ -281,8 +296,8 @@ __device__ __forceinline__ void words_to_float(const uint32_t *w, float *o) {
 // (full_blocks, the number of complete 32-byte blocks of the table, is not
 // needed by the pair loads, which never leave the two entries' chunk.)
 template <typename T, int F>
-__device__ __forceinline__ void gather16(const T *__restrict__ table, uint32_t full_blocks, const uint32_t (&idx)[16],
-                                         float (&e)[16][F]) {
+__device__ __forceinline__ void gather16(const T *__restrict__ table, const T *__restrict__ tsh,
+                                         const uint32_t (&idx)[16], float (&e)[16][F]) {
     using Tr = EntryTraits<T, F>;
     if constexpr (Tr::kBytes == 4 || Tr::kBytes == 8 || Tr::kBytes == 16) {
         // x-pair in ONE load of the aligned 2-entry chunk when both entries
@@ -296,7 +311,9 @@ __device__ __forceinline__ void gather16(const T *__restrict__ table, uint32_t f
 #pragma unroll
         for (int k = 0; k < 8; k++) {
             const uint32_t i0 = idx[2 * k], i1 = idx[2 * k + 1];
-            if ((i0 ^ i1) == 1u) {
+            if (tsh && i1 == i0 + 1u && (i0 & 1u)) {
+                ld_pair<W>(tsh, i0 >> 1, r[k]);      // odd-aligned pair: the shifted copy's chunk
+            } else if ((i0 ^ i1) == 1u) {
                 ld_pair<W>(table, i0 >> 1, r[k]);
             } else {
                 ld_entry<W>(table, i0, r[k]);
@@ -331,7 +348,7 @@ template <int F, typename T, typename O>
 #endif
 __global__ void __launch_bounds__(256, FH_FWD_MINB) fwd_kernel(const __grid_constant__ Params P,
                                                   const float4 *__restrict__ coords, int64_t N,
-                                                  const T *__restrict__ table, uint32_t full_blocks,
+                                                  const T *__restrict__ table, const T *__restrict__ tsh,
                                                   O *__restrict__ out, int *__restrict__ flag,
                                                   const __grid_constant__ LevelList LL,
                                                   const uint32_t *__restrict__ perm) {
@@ -353,7 +370,7 @@ __global__ void __launch_bounds__(256, FH_FWD_MINB) fwd_kernel(const __grid_cons
     const bool bad = cell_of(lv, p, c);
     if (bad && li == 0) atomicOr(flag, 1);
     float e[16][F];
-    gather16<T, F>(table, full_blocks, c.idx, e);
+    gather16<T, F>(table, tsh, c.idx, e);
     float v[F];
 #pragma unroll
     for (int f = 0; f < F; f++) {
@@ -395,7 +412,12 @@ __device__ __forceinline__ void red_entry(float *dtable, uint32_t i, const float
 }
 
 template <int F>
-__device__ __forceinline__ void red_pair(float *dtable, uint32_t i0, uint32_t i1, const float *v0, const float *v1) {
+__device__ __forceinline__ void red_pair(float *dtable, float *gsh, uint32_t i0, uint32_t i1, const float *v0,
+                                         const float *v1) {
+    // gsh (optional): the shifted gradient scratch, holding entry j at float
+    // offset j*F - 2 (kShiftFloats), so that an x-pair (i, i+1) straddling a
+    // 16-byte chunk of dtable lies in ONE 16-byte chunk of gsh; merged back
+    // by merge_shift_kernel.
     if constexpr (F == 2) {
         if ((i0 >> 1) == (i1 >> 1)) {  // both entries in one 16-byte chunk
             float *p = dtable + (size_t)(i0 & ~1u) * 2;
@@ -403,7 +425,15 @@ __device__ __forceinline__ void red_pair(float *dtable, uint32_t i0, uint32_t i1
             else red4(p, v0[0], v0[1], v1[0], v1[1]);
             return;
         }
+        if (gsh && i1 == i0 + 1u) {    // i0 odd: chunk (i0, i0+1) of gsh
+            red4(gsh + (size_t)i0 * 2 - 2, v0[0], v0[1], v1[0], v1[1]);
+            return;
+        }
     } else if constexpr (F == 1) {
+        if (gsh && i1 == i0 + 1u && (i0 & 3u) == 3u) {   // gsh chunk (i0-1 .. i0+2)
+            red4(gsh + (size_t)i0 - 3, 0.f, v0[0], v1[0], 0.f);
+            return;
+        }
         if ((i0 >> 2) == (i1 >> 2)) {
             const uint32_t a = i0 & 3, b = i1 & 3;
             float q[4];
@@ -421,6 +451,7 @@ template <int F>
 __global__ void __launch_bounds__(256) bwd_kernel(const __grid_constant__ Params P,
                                                   const float4 *__restrict__ coords, int64_t N,
                                                   const float *__restrict__ dout, float *__restrict__ dtable,
+                                                  float *__restrict__ gsh,
                                                   int *__restrict__ flag, const __grid_constant__ LevelList LL,
                                                   const uint32_t *__restrict__ perm) {
     __shared__ Level slv[kMaxLevels];
@@ -451,7 +482,33 @@ __global__ void __launch_bounds__(256) bwd_kernel(const __grid_constant__ Params
         float v0[F], v1[F];
 #pragma unroll
         for (int f = 0; f < F; f++) { v0[f] = W0 * g[f]; v1[f] = W1 * g[f]; }
-        red_pair<F>(dtable, c.idx[k], c.idx[k + 1], v0, v1);
+        red_pair<F>(dtable, gsh, c.idx[k], c.idx[k + 1], v0, v1);
+    }
+}
+
+// ------------------------------------------------------------ shifted scratch
+// The pair layout of DESIGN.md §8.1: an x-pair of entries (i, i+1) with i
+// odd (F = 2; i = 3 mod 4 for F = 1) straddles a 16-byte chunk of the table.
+// The forward reads it from a copy of the table shifted by one entry; the
+// backward reduces it into a scratch gsh shifted by two floats
+// (kShiftFloats), which this kernel adds back, dtable[m + 2] += gsh[m], and
+// re-zeroes, over float range [m0, m1) of gsh (m0 even).
+constexpr int kShiftFloats = 2;
+
+__global__ void __launch_bounds__(256) merge_shift_kernel(float *__restrict__ dtable, float *__restrict__ gsh,
+                                                          int64_t m0, int64_t m1) {
+    const int64_t q0 = m0 >> 1, q1 = (m1 + 1) >> 1;
+    float2 *g2 = reinterpret_cast<float2 *>(gsh);
+    float2 *d2 = reinterpret_cast<float2 *>(dtable) + 1;
+    for (int64_t q = q0 + (int64_t)blockIdx.x * blockDim.x + threadIdx.x; q < q1; q += (int64_t)gridDim.x * blockDim.x) {
+        const float2 v = g2[q];
+        if (v.x != 0.f || v.y != 0.f) {
+            float2 d = d2[q];
+            d.x += v.x;
+            d.y += v.y;
+            d2[q] = d;
+            g2[q] = make_float2(0.f, 0.f);
+        }
     }
 }
 

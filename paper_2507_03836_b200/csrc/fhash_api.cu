@@ -67,6 +67,10 @@ static fh_status ensure_flag(fh_encoder e) {
     if (const char *v = getenv("FH_TILE_MARGIN")) e->tile_margin = atof(v);
     if (const char *v = getenv("FH_FINE_ORDER")) e->fine_order = atoi(v) == 1;
     if (const char *v = getenv("FH_AGG_MIN_DENSITY")) e->agg_density = atof(v);
+    if (const char *v = getenv("FH_PAIR_SHIFT")) e->pair_shift = atoi(v);
+    // with the shifted pairs a level's footprint is its table (grads) plus
+    // the shifted copy (scratch)
+    e->fwd_fp = (e->pair_shift & 2) ? 2.0 : 1.0;
     e->fwd_limit = budget("FH_FWD_GROUP_MB", 0.55);
     e->bwd_limit = budget("FH_BWD_GROUP_MB", 0.55);
     make_groups(e->fwd_limit, (size_t)e->F * dtype_size(e->table_dtype), e->gf, e->n_gf);
@@ -102,6 +106,14 @@ static fh_status ensure_flag(fh_encoder e) {
                 e->small.total += (int)(e->info[l].table_size * (uint64_t)e->F);
                 e->small.n++;
             }
+        // shifted gradient pairs for the levels whose grads
+        // plus scratch stay within the L2 budget; a level beyond it runs in a
+        // pass of its own from HBM, where the merge would cost more than the
+        // reductions it saves (measured: Combustion fold-2 shape).
+        for (int q = 0; q < e->L; q++) {
+            const double g = (double)e->info[q].table_size * e->F * 4.0;
+            e->shiftable[q] = (e->pair_shift & 1) && e->kind == 0 && e->F <= 2 && (lim <= 0.0 || 2.0 * g <= lim);
+        }
         e->n_gb = 0;
         int l = 0;
         while (l < e->L) {
@@ -109,7 +121,7 @@ static fh_status ensure_flag(fh_encoder e) {
             const int b = l;
             double acc = 0.0;
             while (l < e->L && !small[l]) {
-                const double sz = (double)e->info[l].table_size * e->F * 4.0;
+                const double sz = (double)e->info[l].table_size * e->F * 4.0 * (e->shiftable[l] ? 2.0 : 1.0);
                 if (lim > 0.0 && l > b && acc + sz > lim) break;
                 acc += sz;
                 l++;
@@ -120,6 +132,49 @@ static fh_status ensure_flag(fh_encoder e) {
         }
     }
     return FH_OK;
+}
+
+// ------------------------------------------------------- shifted-pair scratch
+// Whether a direct pass of N samples uses the shifted pairs:
+// the copy / merge it costs streams the table once, so it pays when the
+// pass gathers at least about as many corners as the table has entries.
+static bool use_shift_fwd(fh_encoder e, int64_t N) {
+    return (e->pair_shift & 2) && e->kind == 0 && (double)N * e->L * 2.0 >= (double)e->entries;
+}
+
+// The scratch slot of `stream` with at least tsh_bytes / gsh_bytes (a zeroed
+// gsh), allocated on first use; nullptr when no slot is free or the stream
+// is capturing a graph (the caller then runs without the shifted pairs).
+static fh_encoder_s::Scratch *get_scratch(fh_encoder e, cudaStream_t s, size_t tsh_bytes, size_t gsh_bytes) {
+    fh_encoder_s::Scratch *slot = nullptr;
+    for (auto &sc : e->scratch)
+        if (sc.stream == (void *)s && (sc.tsh || sc.gsh)) { slot = &sc; break; }
+    if (!slot)
+        for (auto &sc : e->scratch)
+            if (!sc.tsh && !sc.gsh) { slot = &sc; break; }
+    if (!slot) return nullptr;
+    const bool need_t = tsh_bytes > slot->tsh_bytes, need_g = gsh_bytes > slot->gsh_bytes;
+    if (need_t || need_g) {
+        cudaStreamCaptureStatus cs = cudaStreamCaptureStatusNone;
+        if (cudaStreamIsCapturing(s, &cs) != cudaSuccess || cs != cudaStreamCaptureStatusNone) return nullptr;
+        if (need_t) {
+            void *p = nullptr;
+            if (cudaMalloc(&p, tsh_bytes) != cudaSuccess) { cudaGetLastError(); return nullptr; }
+            if (slot->tsh) cudaFree(slot->tsh);
+            slot->tsh = p;
+            slot->tsh_bytes = tsh_bytes;
+        }
+        if (need_g) {
+            void *p = nullptr;
+            if (cudaMalloc(&p, gsh_bytes) != cudaSuccess) { cudaGetLastError(); return nullptr; }
+            if (cudaMemsetAsync(p, 0, gsh_bytes, s) != cudaSuccess) { cudaFree(p); cudaGetLastError(); return nullptr; }
+            if (slot->gsh) { cudaStreamSynchronize(s); cudaFree(slot->gsh); }
+            slot->gsh = reinterpret_cast<float *>(p);
+            slot->gsh_bytes = gsh_bytes;
+        }
+    }
+    slot->stream = (void *)s;
+    return slot;
 }
 
 // ------------------------------------------------------------------ launches
@@ -196,6 +251,16 @@ template <int F, typename T, typename O>
 static void launch_fwd(fh_encoder e, const float *coords, int64_t N, const void *table, void *out,
                        cudaStream_t s, const uint32_t *perm) {
     const uint32_t full_blocks = (uint32_t)((e->entries * (uint64_t)F * sizeof(T)) / 32);
+    constexpr int kEb = F * (int)sizeof(T);
+    // the shifted copy of the table: entry j+1 at slot j
+    const T *tsh = nullptr;
+    if ((kEb == 4 || kEb == 8 || kEb == 16) && use_shift_fwd(e, N) && e->entries > 1) {
+        const size_t bytes = (size_t)e->entries * kEb;
+        fh_encoder_s::Scratch *sc = get_scratch(e, s, bytes, 0);
+        if (sc && cudaMemcpyAsync(sc->tsh, reinterpret_cast<const char *>(table) + kEb, bytes - kEb,
+                                  cudaMemcpyDeviceToDevice, s) == cudaSuccess)
+            tsh = reinterpret_cast<const T *>(sc->tsh);
+    }
     const float4 *c4 = reinterpret_cast<const float4 *>(coords);
     bool include[FH_MAX_LEVELS];
     for (int l = 0; l < e->L; l++) include[l] = true;
@@ -220,10 +285,10 @@ static void launch_fwd(fh_encoder e, const float *coords, int64_t N, const void 
     // small batches (e.g. the renderer's ray batches) touch few entries: one
     // pass, fewer launches; large batches: L2-sized level groups
     const double limit = N < (1 << 15) ? 0.0 : e->fwd_limit;
-    const int n = split_lists(e, include, (double)F * sizeof(T), limit, lists);
+    const int n = split_lists(e, include, (double)F * sizeof(T) * (tsh ? e->fwd_fp : 1.0), limit, lists);
     for (int g = 0; g < n; g++)
         fh::fwd_kernel<F, T, O><<<grid_for(N, lists[g].n), 256, 0, s>>>(
-            e->params, c4, N, reinterpret_cast<const T *>(table), full_blocks, reinterpret_cast<O *>(out), e->flag,
+            e->params, c4, N, reinterpret_cast<const T *>(table), tsh, reinterpret_cast<O *>(out), e->flag,
             lists[g], dperm);
 }
 
@@ -244,8 +309,8 @@ static void launch_bwd_direct(fh_encoder e, const float4 *c4, int64_t N, const f
     fh::LevelList lists[FH_MAX_LEVELS];
     const int n = split_lists(e, include, (double)F * 4.0, e->bwd_limit, lists);
     for (int g = 0; g < n; g++)
-        fh::bwd_kernel<F><<<grid_for(N, lists[g].n), 256, 0, s>>>(e->params, c4, N, dout, dtable, e->flag, lists[g],
-                                                                   perm);
+        fh::bwd_kernel<F><<<grid_for(N, lists[g].n), 256, 0, s>>>(e->params, c4, N, dout, dtable, nullptr, e->flag,
+                                                                   lists[g], perm);
 }
 
 // Ordered backward: levels where a sorted warp's samples nearly always share
@@ -448,6 +513,10 @@ void fh_encoder_destroy(fh_encoder e) {
         cudaGetDevice(&cur);
         if (cur != e->device) cudaSetDevice(e->device);
         cudaFree(e->flag);
+        for (auto &sc : e->scratch) {
+            if (sc.tsh) cudaFree(sc.tsh);
+            if (sc.gsh) cudaFree(sc.gsh);
+        }
         if (cur != e->device && cur >= 0) cudaSetDevice(cur);
     }
     delete e;
@@ -604,6 +673,16 @@ static fh_status encode_bwd_impl(fh_encoder e, const float *coords, int64_t N, c
         if (ev && n_ev > 0) cudaEventRecord(ev[0], s);
     }
     const int ev0 = e->small.n > 0 ? 1 : 0;
+    // shifted gradient scratch: F <= 2, groups of
+    // shiftable levels, passes that reduce at least about as many corners
+    // as the group has entries (else the merge costs more than it saves)
+    float *gsh_buf = nullptr;
+    bool any_shift = false;
+    for (int l = 0; l < e->L; l++) any_shift |= e->shiftable[l];
+    if (any_shift) {
+        fh_encoder_s::Scratch *sc = get_scratch(e, s, 0, (size_t)e->entries * e->F * 4 + 64);
+        if (sc) gsh_buf = sc->gsh;
+    }
     for (int k = 0; k < e->n_gb; k++) {
         const int l0 = e->gb[2 * k], lc = e->gb[2 * k + 1] - e->gb[2 * k];
         const dim3 g = grid_for(N, lc);
@@ -618,12 +697,27 @@ static fh_status encode_bwd_impl(fh_encoder e, const float *coords, int64_t N, c
         }
         fh::LevelList ll;
         ll.n = lc;
-        for (int i = 0; i < lc; i++) ll.id[i] = l0 + i;
+        bool shift = gsh_buf != nullptr;
+        for (int i = 0; i < lc; i++) {
+            ll.id[i] = l0 + i;
+            shift &= e->shiftable[l0 + i];
+        }
+        const uint64_t ge = e->info[l0 + lc - 1].offset + e->info[l0 + lc - 1].table_size - e->info[l0].offset;
+        float *gsh = shift && (double)N * lc * 2.0 >= (double)ge ? gsh_buf : nullptr;
         switch (e->F) {
-            case 1: fh::bwd_kernel<1><<<g, 256, 0, s>>>(e->params, c4, N, dout, dtable, e->flag, ll, nullptr); break;
-            case 2: fh::bwd_kernel<2><<<g, 256, 0, s>>>(e->params, c4, N, dout, dtable, e->flag, ll, nullptr); break;
-            case 4: fh::bwd_kernel<4><<<g, 256, 0, s>>>(e->params, c4, N, dout, dtable, e->flag, ll, nullptr); break;
-            default: fh::bwd_kernel<8><<<g, 256, 0, s>>>(e->params, c4, N, dout, dtable, e->flag, ll, nullptr); break;
+            case 1: fh::bwd_kernel<1><<<g, 256, 0, s>>>(e->params, c4, N, dout, dtable, gsh, e->flag, ll, nullptr); break;
+            case 2: fh::bwd_kernel<2><<<g, 256, 0, s>>>(e->params, c4, N, dout, dtable, gsh, e->flag, ll, nullptr); break;
+            case 4: fh::bwd_kernel<4><<<g, 256, 0, s>>>(e->params, c4, N, dout, dtable, nullptr, e->flag, ll, nullptr); break;
+            default: fh::bwd_kernel<8><<<g, 256, 0, s>>>(e->params, c4, N, dout, dtable, nullptr, e->flag, ll, nullptr); break;
+        }
+        if (gsh) {   // fold this group's shifted partial sums back into dtable (and re-zero them)
+            const fh_level_info &a = e->info[l0], &b = e->info[l0 + lc - 1];
+            int64_t m0 = (int64_t)a.offset * e->F - fh::kShiftFloats, m1 = (int64_t)(b.offset + b.table_size) * e->F - fh::kShiftFloats;
+            if (m0 < 0) m0 = 0;
+            const int64_t q = (m1 - m0 + 1) / 2;
+            int64_t blocks = (q + 255) / 256;
+            if (blocks > (int64_t)e->n_sm * 8) blocks = (int64_t)e->n_sm * 8;
+            if (blocks > 0) fh::merge_shift_kernel<<<(unsigned)blocks, 256, 0, s>>>(dtable, gsh, m0, m1);
         }
         if (ev && ev0 + k < n_ev) cudaEventRecord(ev[ev0 + k], s);
     }

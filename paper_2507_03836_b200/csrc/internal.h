@@ -64,4 +64,20 @@ struct fh_encoder_s {
     double tile_margin = 1.25;                       // FH_TILE_MARGIN
     bool fine_order = false;                         // FH_FINE_ORDER=1: direct levels in `order`
     double agg_density = -1.0;                       // FH_AGG_MIN_DENSITY (< 0: 128 F)
+    // Shifted-pair scratch, one slot per stream that ran a
+    // large direct pass: tsh = the table shifted by one entry (forward),
+    // gsh = zeroed fp32 gradient scratch shifted by two floats (backward).
+    // Allocated on first use; freed with the encoder.
+    struct Scratch {
+        void *stream = nullptr;
+        void *tsh = nullptr;
+        size_t tsh_bytes = 0;
+        float *gsh = nullptr;
+        size_t gsh_bytes = 0;
+    };
+    static constexpr int kScratchSlots = 4;
+    Scratch scratch[kScratchSlots];
+    int pair_shift = 1;                              // FH_PAIR_SHIFT bits: 1 backward (default), 2 forward
+    double fwd_fp = 1.0;                             // forward footprint factor (2 with the shifted copy)
+    bool shiftable[FH_MAX_LEVELS] = {false};         // backward: level uses the shifted gradient pairs
 };

@@ -106,7 +106,7 @@ __global__ void __launch_bounds__(256) bwd_kernel(const __grid_constant__ Params
         float v0[F], v1[F];
 #pragma unroll
         for (int f = 0; f < F; f++) { v0[f] = W0 * g[f]; v1[f] = W1 * g[f]; }
-        red_pair<F>(dtable, c.idx[q], c.idx[q + 1], v0, v1);
+        red_pair<F>(dtable, nullptr, c.idx[q], c.idx[q + 1], v0, v1);
     }
 }
 

@@ -130,7 +130,7 @@ __device__ __forceinline__ Box box_of(const Level &lv, const Tile &tl, uint32_t 
 __device__ __forceinline__ uint32_t vertex_entry(const Level &lv, uint32_t X, uint32_t Y, uint32_t Z, uint32_t Tt) {
     if (lv.hashed == 0) return lv.offset + X + Y * lv.sy + Z * lv.sz + Tt * lv.st;
     if (lv.hashed == 2) return lv.offset + brick_index(lv, X, Y, Z, Tt);
-    return lv.offset + ((X ^ (Y * kPy) ^ (Z * kPz) ^ (Tt * kPt)) & lv.mask);
+    return lv.offset + (hash_x(X, (Y * kPy) ^ (Z * kPz) ^ (Tt * kPt)) & lv.mask);
 }
 
 // Box vertex v (x fastest) -> global entry.
@@ -279,7 +279,7 @@ __global__ void __launch_bounds__(kThreads, 1)
                 cell_of(lv, tl.p[q], c);
 #pragma unroll
                 for (int a = 0; a < 4; a++) w[a] = c.w[a];
-                gather16<T, F>(table, full_blocks, c.idx, e);
+                gather16<T, F>(table, nullptr, c.idx, e);
             }
             float val[F];
 #pragma unroll
@@ -378,7 +378,7 @@ __global__ void __launch_bounds__(kAggThreads)
             float v0[F], v1[F];
 #pragma unroll
             for (int f = 0; f < F; f++) { v0[f] = W0 * g[f]; v1[f] = W1 * g[f]; }
-            red_pair<F>(dtable, c.idx[k], c.idx[k + 1], v0, v1);
+            red_pair<F>(dtable, nullptr, c.idx[k], c.idx[k + 1], v0, v1);
         }
         return;
     }

@@ -177,6 +177,20 @@ def test_hash_reduces_to_x_when_yzt_zero():
     assert oracle.spatial_hash(0, 3, 0, 0, 1 << 32) == (3 * 2654435761) % (1 << 32)
 
 
+def test_hash_x_neighbours_adjacent():
+    """R5 (x additive): the x-neighbour of a capped-level vertex is the next
+    bucket (mod T_l) -- the property the pair layout relies on (DESIGN.md
+    §8.1) -- while y, z, t neighbours scatter."""
+    g = W.rng(5)
+    T = 1 << 11
+    for _ in range(200):
+        X, Y, Z, Tt = (int(v) for v in g.integers(0, 5000, 4))
+        h = oracle.spatial_hash(X, Y, Z, Tt, T)
+        assert oracle.spatial_hash(X + 1, Y, Z, Tt, T) == (h + 1) % T
+    far = sum(abs(oracle.spatial_hash(7, y + 1, 3, 2, T) - oracle.spatial_hash(7, y, 3, 2, T)) > 16 for y in range(100))
+    assert far > 80
+
+
 def test_cfg2_cfg4_table_sizes():
     """SURVEY.md Appendix A per-level tables (independently computed)."""
     lv2 = oracle.Levels(W.CFG2.levels, W.CFG2.cap)

@@ -95,6 +95,31 @@ def test_backward_parity(cfg, N):
     check_bwd(got, G, A)
 
 
+@pytest.mark.parametrize("shift", ["0", "1", "3"])
+@pytest.mark.parametrize("F,tdt", [(1, "f32"), (2, "f32"), (2, "f16"), (4, "f16"), (1, "f16")])
+def test_shifted_pairs_modes(shift, F, tdt, monkeypatch):
+    """DESIGN.md §8.1 shifted pairs: FH_PAIR_SHIFT 0 (off), 1 (backward
+    scratch, default), 3 (also the shifted table copy in the forward) give
+    oracle-exact results on Eq. 9 and capped (R5) levels; the scratch is
+    re-zeroed by the merge, so a second backward accumulates exactly."""
+    monkeypatch.setenv("FH_PAIR_SHIFT", shift)
+    cfg = W.EncoderConfig("shift", W.CFG1H.levels, F=F, cap=W.CFG1H.cap, table_dtype=tdt)
+    case = W.encode_case(cfg, 8192 + 5, seed=21)
+    enc = fh.Encoder(cfg.levels, F, tdt, cfg.cap)
+    ref = oracle.Levels(cfg.levels, cfg.cap)
+    got, st = run_fwd(enc, case)
+    assert st == fh.FH_OK
+    r, ab = ref.forward(case.coords, case.table, want_abs=True)
+    check_fwd(got, r, ab)
+    dtable = torch.zeros((enc.entries, F), dtype=torch.float32, device="cuda")
+    c, g = dev(case.coords), dev(case.dout)
+    enc.bwd(c, g, dtable)
+    enc.bwd(c, g, dtable)
+    assert enc.status_sync() == fh.FH_OK
+    G, A = ref.backward(case.coords, case.dout, F, want_abs=True)
+    check_bwd(dtable.cpu().numpy().astype(np.float64), 2 * G, 2 * A)
+
+
 @pytest.mark.parametrize("F", [1, 2, 4, 8])
 @pytest.mark.parametrize("tdt", ["f32", "f16"])
 def test_feature_widths_and_dtypes(F, tdt):
