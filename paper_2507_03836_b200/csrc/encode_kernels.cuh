@@ -226,6 +226,30 @@ __device__ __forceinline__ void load_levels(const Params &P, Level *s) {
     __syncthreads();
 }
 
+// Level table in shared memory, transposed in 16-byte quarters: quarter q of
+// level l at g[q][l].  The lanes of a warp read up to 16 different levels
+// (l fastest in the thread mapping); with the 64-byte Level stride an
+// LDS.128 of 16 levels hit only two bank groups (8 wavefronts; ncu showed
+// 34 M shared wavefronts, 30 % of the forward's LSU data pipe), transposed
+// it is 256 contiguous bytes (2 wavefronts).
+struct LevelSmem {
+    uint4 g[4][kMaxLevels];
+    __device__ __forceinline__ Level get(int l) const {
+        Level v;
+        uint4 *d = reinterpret_cast<uint4 *>(&v);
+#pragma unroll
+        for (int q = 0; q < 4; q++) d[q] = g[q][l];
+        return v;
+    }
+};
+static_assert(sizeof(Level) == 64, "Level is four 16-byte quarters");
+
+__device__ __forceinline__ void load_levels(const Params &P, LevelSmem &s) {
+    const uint4 *src = reinterpret_cast<const uint4 *>(P.lv);
+    for (int i = threadIdx.x; i < 4 * P.L; i += blockDim.x) s.g[i & 3][i >> 2] = src[i];
+    __syncthreads();
+}
+
 // ------------------------------------------------------------ pair gather
 // The 16 corners are 8 x-adjacent pairs.  Eq. 9 puts a pair at entries
 // (i, i+1); the R5 hash puts it at (h, h') with h' = h^1 when X is even.
@@ -354,7 +378,7 @@ __global__ void __launch_bounds__(256, FH_FWD_MINB) fwd_kernel(const __grid_cons
                                                   const uint32_t *__restrict__ perm) {
     // the levels LL.id[0..LL.n) of every sample (a level group: see DESIGN.md §8);
     // perm (optional): process samples in this (spatially sorted) order
-    __shared__ Level slv[kMaxLevels];
+    __shared__ LevelSmem slv;
     load_levels(P, slv);
     const int L = P.L;
     const int lc = LL.n;
@@ -364,13 +388,13 @@ __global__ void __launch_bounds__(256, FH_FWD_MINB) fwd_kernel(const __grid_cons
     const int li = (int)(gid - j * lc);
     const int l = LL.id[li];
     const int64_t n = perm ? (int64_t)__ldg(perm + j) : j;
-    const Level &lv = slv[l];
+    const Level lv = slv.get(l);
     const float4 p = __ldg(coords + n);
     Cell c;
     const bool bad = cell_of(lv, p, c);
     if (bad && li == 0) atomicOr(flag, 1);
     float e[16][F];
-    gather16<T, F>(table, tsh, c.idx, e);
+    gather16<T, F>(table, lv.tshift ? tsh : nullptr, c.idx, e);
     float v[F];
 #pragma unroll
     for (int f = 0; f < F; f++) {
@@ -454,7 +478,7 @@ __global__ void __launch_bounds__(256) bwd_kernel(const __grid_constant__ Params
                                                   float *__restrict__ gsh,
                                                   int *__restrict__ flag, const __grid_constant__ LevelList LL,
                                                   const uint32_t *__restrict__ perm) {
-    __shared__ Level slv[kMaxLevels];
+    __shared__ LevelSmem slv;
     load_levels(P, slv);
     const int L = P.L;
     const int lc = LL.n;
@@ -464,7 +488,7 @@ __global__ void __launch_bounds__(256) bwd_kernel(const __grid_constant__ Params
     const int li = (int)(gid - j * lc);
     const int l = LL.id[li];
     const int64_t n = perm ? (int64_t)__ldg(perm + j) : j;
-    const Level &lv = slv[l];
+    const Level lv = slv.get(l);
     const float4 p = __ldg(coords + n);
     Cell c;
     const bool bad = cell_of(lv, p, c);
@@ -525,7 +549,7 @@ __global__ void __launch_bounds__(256) bwd_small_kernel(const __grid_constant__ 
                                                         const float *__restrict__ dout, float *__restrict__ dtable,
                                                         int *__restrict__ flag, const uint32_t *__restrict__ perm) {
     extern __shared__ float acc[];
-    __shared__ Level slv[kMaxLevels];
+    __shared__ LevelSmem slv;
     load_levels(P, slv);
     for (int i = threadIdx.x; i < S.total; i += blockDim.x) acc[i] = 0.f;
     __syncthreads();
@@ -537,7 +561,7 @@ __global__ void __launch_bounds__(256) bwd_small_kernel(const __grid_constant__ 
         const int li = (int)(gid - j * S.n);
         const int l = S.id[li];
         const int64_t n = perm ? (int64_t)__ldg(perm + j) : j;
-        const Level &lv = slv[l];
+        const Level lv = slv.get(l);
         Cell c;
         if (cell_of(lv, __ldg(coords + n), c) && li == 0) atomicOr(flag, 1);
         float g[F];
@@ -560,7 +584,7 @@ __global__ void __launch_bounds__(256) bwd_small_kernel(const __grid_constant__ 
     __syncthreads();
     // flush this CTA's partial sums
     for (int li = 0; li < S.n; li++) {
-        const Level &lv = slv[S.id[li]];
+        const Level lv = slv.get(S.id[li]);
         const int cnt = (li + 1 < S.n ? S.soff[li + 1] : S.total) - S.soff[li];
         float *dst = dtable + (size_t)lv.offset * F;
         for (int i = threadIdx.x; i < cnt; i += blockDim.x) {
@@ -575,7 +599,7 @@ __global__ void __launch_bounds__(256) indices_kernel(const __grid_constant__ Pa
                                                       const float4 *__restrict__ coords, int64_t N,
                                                       uint32_t *__restrict__ idx, float *__restrict__ wout,
                                                       int *__restrict__ flag) {
-    __shared__ Level slv[kMaxLevels];
+    __shared__ LevelSmem slv;
     load_levels(P, slv);
     const int L = P.L;
     const int64_t gid = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
@@ -584,7 +608,7 @@ __global__ void __launch_bounds__(256) indices_kernel(const __grid_constant__ Pa
     const int l = (int)(gid - n * L);
     const float4 p = __ldg(coords + n);
     Cell c;
-    const bool bad = cell_of(slv[l], p, c);
+    const bool bad = cell_of(slv.get(l), p, c);
     if (bad && l == 0) atomicOr(flag, 1);
     uint4 *o = reinterpret_cast<uint4 *>(idx + gid * 16);
 #pragma unroll

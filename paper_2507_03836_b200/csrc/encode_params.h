@@ -12,7 +12,8 @@ struct __align__(16) Level {
     uint32_t hashed;     // 0: Eq. 9 (row-major); 1: capped level, R5 hash; 2: brick order (NEXT-2, R21)
     uint32_t mask;       // T_l - 1 for hashed levels (T_l power of two)
     uint32_t offset;     // first entry of the level in the packed table
-    uint32_t pad[2];
+    uint32_t tshift;     // forward: x-pairs at odd entries read the shifted table copy (set per launch)
+    uint32_t pad;
 };
 
 constexpr int kMaxLevels = 32;

@@ -68,9 +68,6 @@ static fh_status ensure_flag(fh_encoder e) {
     if (const char *v = getenv("FH_FINE_ORDER")) e->fine_order = atoi(v) == 1;
     if (const char *v = getenv("FH_AGG_MIN_DENSITY")) e->agg_density = atof(v);
     if (const char *v = getenv("FH_PAIR_SHIFT")) e->pair_shift = atoi(v);
-    // with the shifted pairs a level's footprint is its table (grads) plus
-    // the shifted copy (scratch)
-    e->fwd_fp = (e->pair_shift & 2) ? 2.0 : 1.0;
     e->fwd_limit = budget("FH_FWD_GROUP_MB", 0.55);
     e->bwd_limit = budget("FH_BWD_GROUP_MB", 0.55);
     make_groups(e->fwd_limit, (size_t)e->F * dtype_size(e->table_dtype), e->gf, e->n_gf);
@@ -138,10 +135,6 @@ static fh_status ensure_flag(fh_encoder e) {
 // Whether a direct pass of N samples uses the shifted pairs:
 // the copy / merge it costs streams the table once, so it pays when the
 // pass gathers at least about as many corners as the table has entries.
-static bool use_shift_fwd(fh_encoder e, int64_t N) {
-    return (e->pair_shift & 2) && e->kind == 0 && (double)N * e->L * 2.0 >= (double)e->entries;
-}
-
 // The scratch slot of `stream` with at least tsh_bytes / gsh_bytes (a zeroed
 // gsh), allocated on first use; nullptr when no slot is free or the stream
 // is capturing a graph (the caller then runs without the shifted pairs).
@@ -185,12 +178,13 @@ static dim3 grid_for(int64_t N, int L) {
 
 // Split the levels with include[l] into direct-pass lists whose footprint
 // (T_l * bytes_per_entry) fits `limit` bytes (0 = one list), in level order.
-static int split_lists(fh_encoder e, const bool *include, double bytes_per_entry, double limit, fh::LevelList *out) {
+static int split_lists(fh_encoder e, const bool *include, double bytes_per_entry, double limit, fh::LevelList *out,
+                       const bool *doubled = nullptr) {
     int n = 0;
     double acc = 0.0;
     for (int l = 0; l < e->L; l++) {
         if (!include[l]) continue;
-        const double b = (double)e->info[l].table_size * bytes_per_entry;
+        const double b = (double)e->info[l].table_size * bytes_per_entry * (doubled && doubled[l] ? 2.0 : 1.0);
         if (n == 0 || (limit > 0.0 && out[n - 1].n > 0 && acc + b > limit)) {
             out[n].n = 0;
             n++;
@@ -252,14 +246,42 @@ static void launch_fwd(fh_encoder e, const float *coords, int64_t N, const void 
                        cudaStream_t s, const uint32_t *perm) {
     const uint32_t full_blocks = (uint32_t)((e->entries * (uint64_t)F * sizeof(T)) / 32);
     constexpr int kEb = F * (int)sizeof(T);
-    // the shifted copy of the table: entry j+1 at slot j
+    // The shifted copy of the table: slot j holds entry j+1,
+    // so an x-pair at (i, i+1), i odd, is ONE aligned load.  Per level: only
+    // where table + copy stay within the L2 budget (else the doubled
+    // footprint misses to HBM; measured Combustion fold-2 shape 0.60 ->
+    // 0.74 ms) and the pass gathers enough corners to pay for the copy.
     const T *tsh = nullptr;
-    if ((kEb == 4 || kEb == 8 || kEb == 16) && use_shift_fwd(e, N) && e->entries > 1) {
-        const size_t bytes = (size_t)e->entries * kEb;
-        fh_encoder_s::Scratch *sc = get_scratch(e, s, bytes, 0);
-        if (sc && cudaMemcpyAsync(sc->tsh, reinterpret_cast<const char *>(table) + kEb, bytes - kEb,
-                                  cudaMemcpyDeviceToDevice, s) == cudaSuccess)
+    bool sh[FH_MAX_LEVELS] = {false};
+    fh::Params prm = e->params;
+    if ((kEb == 4 || kEb == 8 || kEb == 16) && (e->pair_shift & 2) && e->kind == 0 && !perm && N >= (1 << 15)) {
+        bool any = false;
+        for (int l = 0; l < e->L; l++) {
+            const double t = (double)e->info[l].table_size;
+            // table + copy within half the group budget (cfg4's 32 MiB
+            // levels doubled to 64 MiB ran 2.94 -> 3.32 ms)
+            sh[l] = (e->fwd_limit <= 0.0 || 4.0 * t * kEb <= e->fwd_limit) && 8.0 * (double)N >= t;
+            any |= sh[l];
+        }
+        fh_encoder_s::Scratch *sc = any ? get_scratch(e, s, (size_t)e->entries * kEb, 0) : nullptr;
+        if (sc) {
+            // one copy per run of consecutive shifted levels
+            for (int l = 0; l < e->L;) {
+                if (!sh[l]) { l++; continue; }
+                int r = l;
+                while (r + 1 < e->L && sh[r + 1]) r++;
+                const uint64_t b = e->info[l].offset, en = e->info[r].offset + e->info[r].table_size;
+                if (en - b > 1)
+                    cudaMemcpyAsync(reinterpret_cast<char *>(sc->tsh) + b * kEb,
+                                    reinterpret_cast<const char *>(table) + (b + 1) * kEb, (en - b - 1) * kEb,
+                                    cudaMemcpyDeviceToDevice, s);
+                l = r + 1;
+            }
             tsh = reinterpret_cast<const T *>(sc->tsh);
+            for (int l = 0; l < e->L; l++) prm.lv[l].tshift = sh[l] ? 1u : 0u;
+        } else {
+            for (int l = 0; l < e->L; l++) sh[l] = false;
+        }
     }
     const float4 *c4 = reinterpret_cast<const float4 *>(coords);
     bool include[FH_MAX_LEVELS];
@@ -285,10 +307,10 @@ static void launch_fwd(fh_encoder e, const float *coords, int64_t N, const void 
     // small batches (e.g. the renderer's ray batches) touch few entries: one
     // pass, fewer launches; large batches: L2-sized level groups
     const double limit = N < (1 << 15) ? 0.0 : e->fwd_limit;
-    const int n = split_lists(e, include, (double)F * sizeof(T) * (tsh ? e->fwd_fp : 1.0), limit, lists);
+    const int n = split_lists(e, include, (double)F * sizeof(T), limit, lists, sh);
     for (int g = 0; g < n; g++)
         fh::fwd_kernel<F, T, O><<<grid_for(N, lists[g].n), 256, 0, s>>>(
-            e->params, c4, N, reinterpret_cast<const T *>(table), tsh, reinterpret_cast<O *>(out), e->flag,
+            prm, c4, N, reinterpret_cast<const T *>(table), tsh, reinterpret_cast<O *>(out), e->flag,
             lists[g], dperm);
 }
 

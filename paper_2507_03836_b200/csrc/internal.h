@@ -77,7 +77,6 @@ struct fh_encoder_s {
     };
     static constexpr int kScratchSlots = 4;
     Scratch scratch[kScratchSlots];
-    int pair_shift = 1;                              // FH_PAIR_SHIFT bits: 1 backward (default), 2 forward
-    double fwd_fp = 1.0;                             // forward footprint factor (2 with the shifted copy)
+    int pair_shift = 3;                              // FH_PAIR_SHIFT bits: 1 backward, 2 forward (default both)
     bool shiftable[FH_MAX_LEVELS] = {false};         // backward: level uses the shifted gradient pairs
 };

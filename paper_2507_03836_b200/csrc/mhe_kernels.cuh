@@ -54,7 +54,7 @@ template <int F, typename T, typename O>
 __global__ void __launch_bounds__(256) fwd_kernel(const __grid_constant__ Params P, const float4 *__restrict__ coords,
                                                   int64_t N, const T *__restrict__ table, O *__restrict__ out,
                                                   int *__restrict__ flag, int l0, int lc) {
-    __shared__ Level slv[kMaxLevels];
+    __shared__ LevelSmem slv;
     load_levels(P, slv);
     const int L = P.L;
     const int64_t gid = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
@@ -62,7 +62,7 @@ __global__ void __launch_bounds__(256) fwd_kernel(const __grid_constant__ Params
     if (n >= N) return;
     const int l = l0 + (int)(gid - n * lc);
     Cell8 c;
-    const bool bad = cell_of(slv[l], __ldg(coords + n), c);
+    const bool bad = cell_of(slv.get(l), __ldg(coords + n), c);
     if (bad && l == l0) atomicOr(flag, 1);
     float e[8][F];
 #pragma unroll
@@ -83,7 +83,7 @@ template <int F>
 __global__ void __launch_bounds__(256) bwd_kernel(const __grid_constant__ Params P, const float4 *__restrict__ coords,
                                                   int64_t N, const float *__restrict__ dout,
                                                   float *__restrict__ dtable, int *__restrict__ flag, int l0, int lc) {
-    __shared__ Level slv[kMaxLevels];
+    __shared__ LevelSmem slv;
     load_levels(P, slv);
     const int L = P.L;
     const int64_t gid = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
@@ -91,7 +91,7 @@ __global__ void __launch_bounds__(256) bwd_kernel(const __grid_constant__ Params
     if (n >= N) return;
     const int l = l0 + (int)(gid - n * lc);
     Cell8 c;
-    const bool bad = cell_of(slv[l], __ldg(coords + n), c);
+    const bool bad = cell_of(slv.get(l), __ldg(coords + n), c);
     if (bad && l == l0) atomicOr(flag, 1);
     float g[F];
     const float *gp = dout + n * (int64_t)(L * F) + l * F;
@@ -114,7 +114,7 @@ __global__ void __launch_bounds__(256) indices_kernel(const __grid_constant__ Pa
                                                       const float4 *__restrict__ coords, int64_t N,
                                                       uint32_t *__restrict__ idx, float *__restrict__ wout,
                                                       int *__restrict__ flag) {
-    __shared__ Level slv[kMaxLevels];
+    __shared__ LevelSmem slv;
     load_levels(P, slv);
     const int L = P.L;
     const int64_t gid = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
@@ -122,7 +122,7 @@ __global__ void __launch_bounds__(256) indices_kernel(const __grid_constant__ Pa
     if (n >= N) return;
     const int l = (int)(gid - n * L);
     Cell8 c;
-    const bool bad = cell_of(slv[l], __ldg(coords + n), c);
+    const bool bad = cell_of(slv.get(l), __ldg(coords + n), c);
     if (bad && l == 0) atomicOr(flag, 1);
 #pragma unroll
     for (int q = 0; q < 8; q++) idx[gid * 8 + q] = c.idx[q];

@@ -95,12 +95,13 @@ def test_backward_parity(cfg, N):
     check_bwd(got, G, A)
 
 
-@pytest.mark.parametrize("shift", ["0", "1", "3"])
+@pytest.mark.parametrize("shift", ["0", "1", "2", "3"])
 @pytest.mark.parametrize("F,tdt", [(1, "f32"), (2, "f32"), (2, "f16"), (4, "f16"), (1, "f16")])
 def test_shifted_pairs_modes(shift, F, tdt, monkeypatch):
     """DESIGN.md §8.1 shifted pairs: FH_PAIR_SHIFT 0 (off), 1 (backward
     scratch, default), 3 (also the shifted table copy in the forward) give
-    oracle-exact results on Eq. 9 and capped (R5) levels; the scratch is
+    oracle-exact results on Eq. 9 and capped (R5) levels (2: forward only);
+    the scratch is
     re-zeroed by the merge, so a second backward accumulates exactly."""
     monkeypatch.setenv("FH_PAIR_SHIFT", shift)
     cfg = W.EncoderConfig("shift", W.CFG1H.levels, F=F, cap=W.CFG1H.cap, table_dtype=tdt)
