@@ -206,10 +206,29 @@ def microbench_roofline(fh, torch, enc, cfg, N, stream, hbm_peak):
         del buf
     stream_fwd = N * (16 + cfg.L * F * 4)
     stream_bwd = N * (16 + cfg.L * F * 4)
-    t_fwd = sum(N * 16 / g for g in g_rate) + stream_fwd / bw_copy
-    t_bwd = sum(N * 16 / r for r in r_rate) + stream_bwd / bw_copy
+    t_fwd_lv = sum(N * 16 / g for g in g_rate) + stream_fwd / bw_copy
+    t_bwd_lv = sum(N * 16 / r for r in r_rate) + stream_bwd / bw_copy
+    # the encode's own shape: all levels in one launch, (sample, level)
+    # threads level-fastest, 8 ideal x-pairs per thread inside each level's
+    # range of the packed table (fh_bench_*_levels) -- the per-level runs
+    # above overstate the coarse levels' contention, which the kernel's
+    # level mix dilutes
+    full = torch.zeros((enc.entries, F), device="cuda")
+    msink = torch.empty(N * cfg.L, device="cuda")
+    fh.bench_gather_levels(full, enc, eb, N, msink, stream=stream)
+    tg_mix = timeit(lambda: fh.bench_gather_levels(full, enc, eb, N, msink, stream=stream))
+    fh.bench_red_levels(full, enc, eb, N, stream=stream)
+    tr_mix = timeit(lambda: fh.bench_red_levels(full, enc, eb, N, stream=stream))
+    del full, msink
+    t_fwd = tg_mix + stream_fwd / bw_copy
+    t_bwd = tr_mix + stream_bwd / bw_copy
     return {
         "t_roof_fwd_ms": t_fwd * 1e3, "t_roof_bwd_ms": t_bwd * 1e3,
+        "model": "level-mix microbenchmark (fh_bench_gather_levels / fh_bench_red_levels) + streamed bytes at the "
+                 "measured copy bandwidth",
+        "t_roof_per_level_sum_fwd_ms": t_fwd_lv * 1e3, "t_roof_per_level_sum_bwd_ms": t_bwd_lv * 1e3,
+        "mix_gather_corner_rate_G_per_s": round(N * cfg.L * 16 / tg_mix / 1e9, 2),
+        "mix_red_corner_rate_G_per_s": round(N * cfg.L * 16 / tr_mix / 1e9, 2),
         "copy_gbs": bw_copy / 1e9, "hbm_peak_gbs": hbm_peak,
         "gather_corner_rate_G_per_s": [round(g / 1e9, 2) for g in g_rate],
         "red_corner_rate_G_per_s": [round(r / 1e9, 2) for r in r_rate],

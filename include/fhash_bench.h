@@ -35,6 +35,18 @@ fh_status fh_bench_gather(const void *buf, uint64_t n_entries, int entry_bytes, 
 fh_status fh_bench_red(float *buf, uint64_t n_entries, int entry_bytes, int64_t n_threads, int pairs,
                        int mode, uint32_t seed, fh_stream stream);
 
+/* Level-mix variants (the encode's own shape): thread t is
+ * (sample t / L, level t % L) as in the encode kernels, and issues 8 x-pairs,
+ * each ONE aligned access of two entries (the ideal pair of mode 1) at a
+ * uniform position inside level l's range [level_off[l], level_off[l] +
+ * level_size[l]) of the packed buffer (host arrays, L <= 32, sizes >= 4).
+ * n_samples * L threads; sink [n_samples * L].  gather: entry_bytes 4 or 8;
+ * red: 4, 8 or 16 (16-byte entries: two reductions per pair). */
+fh_status fh_bench_gather_levels(const void *buf, const uint64_t *level_off, const uint64_t *level_size, int L,
+                                 int entry_bytes, int64_t n_samples, uint32_t seed, float *sink, fh_stream stream);
+fh_status fh_bench_red_levels(float *buf, const uint64_t *level_off, const uint64_t *level_size, int L,
+                              int entry_bytes, int64_t n_samples, uint32_t seed, fh_stream stream);
+
 /* Streaming copy dst[i] = src[i] over `bytes` (16-byte aligned): the HBM
  * ceiling measured with the library's own kernel. */
 fh_status fh_bench_copy(void *dst, const void *src, uint64_t bytes, fh_stream stream);

@@ -366,11 +366,15 @@ __device__ __forceinline__ void gather16(const T *__restrict__ table, const T *_
 // ------------------------------------------------------------ forward
 // Step 4 (Eqs. 10-12): trilinear per time slice (8 x-lerps -> 4 y -> 2 z),
 // then the temporal lerp (R6), per feature.
+// Occupancy: the gathers are latency-bound at the L1->L2 request port, so
+// resident warps matter.  F <= 2 fits 64 registers (4 CTAs of 256 per SM;
+// cfg2 fwd 0.633 -> 0.605 ms); wider entries keep 2 (their 16 corners need
+// the registers: cfg4 2.97 -> 3.17 ms when capped at 64).
+template <int F>
+struct FwdMinBlocks { static constexpr int value = F <= 2 ? 4 : 2; };
+
 template <int F, typename T, typename O>
-#ifndef FH_FWD_MINB
-#define FH_FWD_MINB 2
-#endif
-__global__ void __launch_bounds__(256, FH_FWD_MINB) fwd_kernel(const __grid_constant__ Params P,
+__global__ void __launch_bounds__(256, FwdMinBlocks<F>::value) fwd_kernel(const __grid_constant__ Params P,
                                                   const float4 *__restrict__ coords, int64_t N,
                                                   const T *__restrict__ table, const T *__restrict__ tsh,
                                                   O *__restrict__ out, int *__restrict__ flag,

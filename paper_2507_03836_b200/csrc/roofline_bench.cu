@@ -80,6 +80,58 @@ __global__ void __launch_bounds__(256) red_kernel(float *__restrict__ buf, uint3
     }
 }
 
+// Level-mix shape of the encode: thread t = (sample t / L, level t % L),
+// level fastest as in fwd_kernel / bwd_kernel; its 8 x-pairs are ONE aligned
+// access of two entries each at uniform positions inside the level's range
+// of the packed table (the "ideal" pair of mode 1).  16-byte entries: two
+// entry accesses per pair (no 32-byte red exists).
+struct LevelRanges {
+    int L;
+    uint32_t off[32];    // first entry of level l
+    uint32_t pairs[32];  // floor(T_l / 2) aligned pairs inside the level
+};
+
+__device__ __forceinline__ uint32_t level_pair(const LevelRanges &R, int l, uint64_t t, int k, uint32_t seed) {
+    // chunk of two entries (global index) fully inside level l
+    const uint32_t o = R.off[l];
+    const uint32_t j = rand_index(t, k, seed, R.pairs[l]);
+    return ((o + 1u) >> 1) + j;   // first whole chunk at or after o
+}
+
+template <typename V2>
+__global__ void __launch_bounds__(256) gather_levels_kernel(const V2 *__restrict__ buf, const __grid_constant__ LevelRanges R,
+                                                            int64_t n, uint32_t seed, float *__restrict__ sink) {
+    const int64_t t = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+    if (t >= n) return;
+    const int l = (int)(t % R.L);
+    V2 a[8];
+#pragma unroll
+    for (int k = 0; k < 8; k++) a[k] = __ldg(buf + level_pair(R, l, t, k, seed));
+    float s = 0.f;
+#pragma unroll
+    for (int k = 0; k < 8; k++) s += vsum(a[k]);
+    sink[t] = s;
+}
+
+template <int W>
+__global__ void __launch_bounds__(256) red_levels_kernel(float *__restrict__ buf, const __grid_constant__ LevelRanges R,
+                                                         int64_t n, uint32_t seed) {
+    const int64_t t = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+    if (t >= n) return;
+    const int l = (int)(t % R.L);
+    const float v = 1e-7f * (float)(t & 7);
+#pragma unroll
+    for (int k = 0; k < 8; k++) {
+        const uint32_t c = level_pair(R, l, t, k, seed);
+        if constexpr (W >= 4) {
+            red_w<W>(buf + (size_t)c * 2 * W, v);
+            red_w<W>(buf + (size_t)c * 2 * W + W, v);
+        } else {
+            red_w<2 * W>(buf + (size_t)c * 2 * W, v);
+        }
+    }
+}
+
 __global__ void __launch_bounds__(256) copy_kernel(const int4 *__restrict__ src, int4 *__restrict__ dst, int64_t n) {
     const int64_t stride = (int64_t)gridDim.x * blockDim.x;
     for (int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; i < n; i += stride) dst[i] = __ldcs(src + i);
@@ -141,6 +193,48 @@ fh_status fh_bench_red(float *buf, uint64_t n_entries, int entry_bytes, int64_t 
     }
 #undef FH_R
     return launch_ok("fh_bench_red");
+}
+
+static fh_status make_ranges(const uint64_t *off, const uint64_t *size, int L, LevelRanges &R) {
+    if (!off || !size || L < 1 || L > 32) return FH_E_ARG;
+    R.L = L;
+    for (int l = 0; l < L; l++) {
+        if (off[l] + size[l] > 0xFFFFFFFFull || size[l] < 4) return FH_E_ARG;
+        R.off[l] = (uint32_t)off[l];
+        R.pairs[l] = (uint32_t)((size[l] - (off[l] & 1)) / 2);
+    }
+    return FH_OK;
+}
+
+fh_status fh_bench_gather_levels(const void *buf, const uint64_t *level_off, const uint64_t *level_size, int L,
+                                 int entry_bytes, int64_t n_samples, uint32_t seed, float *sink, fh_stream stream) {
+    LevelRanges R;
+    if (!buf || !sink || n_samples <= 0 || make_ranges(level_off, level_size, L, R) != FH_OK) return FH_E_ARG;
+    cudaStream_t s = reinterpret_cast<cudaStream_t>(stream);
+    const int64_t n = n_samples * L;
+    const dim3 g((unsigned)((n + 255) / 256));
+    switch (entry_bytes) {
+        case 4: gather_levels_kernel<float2><<<g, 256, 0, s>>>((const float2 *)buf, R, n, seed, sink); break;
+        case 8: gather_levels_kernel<float4><<<g, 256, 0, s>>>((const float4 *)buf, R, n, seed, sink); break;
+        default: return FH_E_ARG;
+    }
+    return launch_ok("fh_bench_gather_levels");
+}
+
+fh_status fh_bench_red_levels(float *buf, const uint64_t *level_off, const uint64_t *level_size, int L,
+                              int entry_bytes, int64_t n_samples, uint32_t seed, fh_stream stream) {
+    LevelRanges R;
+    if (!buf || n_samples <= 0 || make_ranges(level_off, level_size, L, R) != FH_OK) return FH_E_ARG;
+    cudaStream_t s = reinterpret_cast<cudaStream_t>(stream);
+    const int64_t n = n_samples * L;
+    const dim3 g((unsigned)((n + 255) / 256));
+    switch (entry_bytes) {
+        case 4: red_levels_kernel<1><<<g, 256, 0, s>>>(buf, R, n, seed); break;
+        case 8: red_levels_kernel<2><<<g, 256, 0, s>>>(buf, R, n, seed); break;
+        case 16: red_levels_kernel<4><<<g, 256, 0, s>>>(buf, R, n, seed); break;
+        default: return FH_E_ARG;
+    }
+    return launch_ok("fh_bench_red_levels");
 }
 
 fh_status fh_bench_copy(void *dst, const void *src, uint64_t bytes, fh_stream stream) {

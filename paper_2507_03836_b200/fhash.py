@@ -30,7 +30,7 @@ EXPORTS = [
     "fh_version", "fh_spatial_sort_workspace_size", "fh_spatial_sort", "fh_encode_fwd_ordered",
     "fh_encode_bwd_ordered", "fh_build_mhe", "fh_encoder_kind", "fh_spatial_sort_bits", "fh_build_levels_lin",
     # include/fhash_bench.h (measurement kernels)
-    "fh_bench_gather", "fh_bench_red", "fh_bench_copy",
+    "fh_bench_gather", "fh_bench_red", "fh_bench_copy", "fh_bench_gather_levels", "fh_bench_red_levels",
     # train step
     "fh_mlp_param_count", "fh_train_workspace_size", "fh_trainer_create", "fh_train_fwd_bwd", "fh_train_apply",
     "fh_train_step", "fh_trainer_status", "fh_trainer_step_count", "fh_trainer_destroy", "fh_train_apply_sharded",
@@ -113,7 +113,9 @@ def lib() -> ctypes.CDLL:
     L.fh_bench_gather.argtypes = [vp, u64, c_int, i64, c_int, c_int, ctypes.c_uint32, vp, vp]
     L.fh_bench_red.argtypes = [vp, u64, c_int, i64, c_int, c_int, ctypes.c_uint32, vp]
     L.fh_bench_copy.argtypes = [vp, vp, u64, vp]
-    for name in ("fh_bench_gather", "fh_bench_red", "fh_bench_copy"):
+    L.fh_bench_gather_levels.argtypes = [vp, vp, vp, c_int, c_int, i64, ctypes.c_uint32, vp, vp]
+    L.fh_bench_red_levels.argtypes = [vp, vp, vp, c_int, c_int, i64, ctypes.c_uint32, vp]
+    for name in ("fh_bench_gather", "fh_bench_red", "fh_bench_copy", "fh_bench_gather_levels", "fh_bench_red_levels"):
         getattr(L, name).restype = c_int
     L.fh_last_error.restype = ctypes.c_char_p
     L.fh_version.restype = ctypes.c_char_p
@@ -284,6 +286,25 @@ def bench_gather(buf, n_entries: int, entry_bytes: int, n_threads: int, sink, mo
 
 def bench_red(buf, n_entries: int, entry_bytes: int, n_threads: int, mode: int = 1, seed: int = 0, stream=None):
     _check(lib().fh_bench_red(_ptr(buf), n_entries, entry_bytes, n_threads, 8, mode, seed, _stream(stream)))
+
+
+def _level_arrays(enc):
+    off = (ctypes.c_uint64 * enc.L)(*[enc.level_info(l)["offset"] for l in range(enc.L)])
+    size = (ctypes.c_uint64 * enc.L)(*[enc.level_info(l)["table_size"] for l in range(enc.L)])
+    return off, size
+
+
+def bench_gather_levels(buf, enc, entry_bytes: int, n_samples: int, sink, seed: int = 0, stream=None):
+    """Level-mix roofline microbenchmark: the encode's thread shape (sample,
+    level), 8 ideal x-pairs per thread inside each level's table range."""
+    off, size = _level_arrays(enc)
+    _check(lib().fh_bench_gather_levels(_ptr(buf), off, size, enc.L, entry_bytes, n_samples, seed, _ptr(sink),
+                                        _stream(stream)))
+
+
+def bench_red_levels(buf, enc, entry_bytes: int, n_samples: int, seed: int = 0, stream=None):
+    off, size = _level_arrays(enc)
+    _check(lib().fh_bench_red_levels(_ptr(buf), off, size, enc.L, entry_bytes, n_samples, seed, _stream(stream)))
 
 
 def bench_copy(dst, src, nbytes: int, stream=None):
