@@ -69,13 +69,16 @@ static fh_status ensure_flag(fh_encoder e) {
     if (const char *v = getenv("FH_AGG_MIN_DENSITY")) e->agg_density = atof(v);
     if (const char *v = getenv("FH_PAIR_SHIFT")) e->pair_shift = atoi(v);
     e->fwd_limit = budget("FH_FWD_GROUP_MB", 0.55);
-    e->bwd_limit = budget("FH_BWD_GROUP_MB", 0.55);
+    // backward: 0.45 L2 (measured with the shifted gradient scratch, whose
+    // grads + scratch double a level's footprint: cfg2 bwd 0.737 -> 0.711
+    // ms, cfg3 0.248 -> 0.231 ms; cfg4's 64 MiB levels group alike)
+    e->bwd_limit = budget("FH_BWD_GROUP_MB", 0.45);
     make_groups(e->fwd_limit, (size_t)e->F * dtype_size(e->table_dtype), e->gf, e->n_gf);
     // Backward: levels whose fp32 grads fit a shared-memory budget are
     // privatised per CTA (bwd_small_kernel), smallest first; the others form
     // contiguous runs split by the L2 budget.
     {
-        const double lim = budget("FH_BWD_GROUP_MB", 0.55);
+        const double lim = e->bwd_limit;
         const char *sv = getenv("FH_SMALL_KB");
         const int per_level_max = 48 * 1024, total_max = sv ? atoi(sv) * 1024 : 96 * 1024;
         bool small[FH_MAX_LEVELS] = {false};
