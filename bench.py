@@ -261,11 +261,10 @@ def hbm_regime_bench(fh, torch, W, steps, copy_gbs):
     tf = tb = 0.0
     for it in range(steps + 2):
         flush.fill_(it & 255)
-        enc.zero_grad(dt)
         e[0].record()
         enc.fwd(coords, table, out, out_dtype="bf16")
         e[1].record()
-        enc.bwd(coords, dout, dt)
+        enc.bwd(coords, dout, dt, overwrite=True)
         e[2].record()
         torch.cuda.synchronize()
         if it >= 2:
@@ -382,9 +381,11 @@ def train_step_bench(fh, torch, W, which, rank, world, dist, steps, warmup, dp_m
     if dist:
         dist.barrier()
     torch.cuda.synchronize()
+    l0 = fh.kernel_launches()
     for k in range(steps):
         one(1000 + k, ev[k])
     torch.cuda.synchronize()
+    launches = (fh.kernel_launches() - l0) / steps
     total = sum(e[0].elapsed_time(e[4]) for e in ev) / 1e3
     phase = [sum(e[i].elapsed_time(e[i + 1]) for e in ev) / steps for i in range(4)]
     if dist:
@@ -455,7 +456,7 @@ def train_step_bench(fh, torch, W, which, rank, world, dist, steps, warmup, dp_m
                   "ms": infer_ms, "samples_per_s": n_local / (infer_ms / 1e3),
                   "small_batch_latency": small},
         "loss_first_warmup": losses[0], "loss_last": float(last.item()), "status": int(st),
-        "params": enc.param_count + tr.n_mlp, "gpu_launches_per_step": 6, "replicas_identical": bool(same),
+        "params": enc.param_count + tr.n_mlp, "gpu_launches_per_step": launches, "replicas_identical": bool(same),
     }
 
 
@@ -488,10 +489,9 @@ def paper_encoder_compare(fh, torch, W, steps):
         tot = 0.0
         for it in range(steps + 3):
             flush.fill_(it & 255)
-            enc.zero_grad(dt)
             e0.record()
             enc.fwd(coords, table, out)
-            enc.bwd(coords, g, dt)
+            enc.bwd(coords, g, dt, overwrite=True)
             e1.record()
             torch.cuda.synchronize()
             if it >= 3:
@@ -529,13 +529,16 @@ def coreset_bench(fh, torch, W, steps, hbm_peak, with_cpu):
     vals = torch.empty((M,), device="cuda")
     e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
     tot = 0.0
+    launches = 0
     for it in range(steps + 2):
         flush.fill_(it & 255)
+        l0 = fh.kernel_launches()
         e0.record()
         c2 = fh.Coreset(keys, fh.FH_FEAT_SEGMENTATION, 0.5)
         c2.emit(coords, vals)
         e1.record()
         torch.cuda.synchronize()
+        launches = fh.kernel_launches() - l0
         if it >= 2:
             tot += e0.elapsed_time(e1)
     ms = tot / steps
@@ -546,7 +549,7 @@ def coreset_bench(fh, torch, W, steps, hbm_peak, with_cpu):
            "fbb": cs.fbb, "ms": ms, "vertices_per_s": n * V / (ms / 1e3),
            "roofline": {"bound": "hbm", "achieved_gbs": alg / (ms / 1e3) / 1e9, "peak_gbs": hbm_peak,
                         "frac": alg / (ms / 1e3) / 1e9 / hbm_peak, "algorithmic_bytes": alg},
-           "gpu_launches": 11}
+           "gpu_launches": launches}
     if with_cpu:
         from oracle import coreset as C
         small = keys[:2, 96:128, 96:128, 96:128].cpu().numpy()
@@ -583,9 +586,10 @@ def run_ours(args, rank, local_rank, world):
     stream = torch.cuda.current_stream()
 
     def step():
-        enc.zero_grad(dtable, stream)
+        # dtable = the gradient: fh_encode_bwd_ex(FH_BWD_OVERWRITE) zeroes each
+        # level group right before its reductions (include/fhash.h)
         enc.fwd(coords, table, out, stream=stream)
-        enc.bwd(coords, dout, dtable, stream=stream)
+        enc.bwd(coords, dout, dtable, stream=stream, overwrite=True)
 
     for _ in range(max(args.warmup, 3)):
         flush.fill_(1)
@@ -598,21 +602,21 @@ def run_ours(args, rank, local_rank, world):
     if dist:
         dist.barrier()
     torch.cuda.synchronize()
+    l0 = fh.kernel_launches()
     with ClockSampler(local_rank) as clk:
         for k in range(K):
             flush.fill_(k & 0xFF)
             e = ev[k]
             e[0].record(stream)
-            enc.zero_grad(dtable, stream)
             e[1].record(stream)
             enc.fwd(coords, table, out, stream=stream)
             e[2].record(stream)
-            enc.bwd(coords, dout, dtable, stream=stream)
+            enc.bwd(coords, dout, dtable, stream=stream, overwrite=True)
             e[3].record(stream)
         torch.cuda.synchronize()
+    launches = fh.kernel_launches() - l0
     if dist:
         dist.barrier()
-    zero_ms = sum(e[0].elapsed_time(e[1]) for e in ev) / K
     fwd_ms = sum(e[1].elapsed_time(e[2]) for e in ev) / K
     bwd_ms = sum(e[2].elapsed_time(e[3]) for e in ev) / K
     step_ms = sum(e[0].elapsed_time(e[3]) for e in ev) / K
@@ -628,22 +632,25 @@ def run_ours(args, rank, local_rank, world):
 
     # e2e: the same step through the C ABI from pinned HOST buffers, copies
     # inside the timed region (fh_encode_step_host: H2D of the step's coords and
-    # dout, zero dtable, fwd, bwd, D2H of out and dtable).  Steps alternate
-    # between two streams with two device / host-output buffer sets, so step
-    # k+1's H2D overlaps step k's kernels and D2H (PCIe is full duplex); every
-    # step's copies stay inside the timed region.
+    # dout, fwd, bwd (dtable overwritten), D2H of out and dtable).  Steps
+    # rotate over three streams with three device / host-output buffer sets,
+    # so step k+1's H2D overlaps step k's kernels and step k-1's D2H (PCIe is
+    # full duplex; with two sets the next H2D on a stream waits for that
+    # stream's D2H); every step's copies stay inside the timed region.
     coords_h = torch.from_numpy(case.coords).pin_memory()
     dout_h = torch.from_numpy(case.dout).pin_memory()
-    streams = [torch.cuda.Stream(), torch.cuda.Stream()]
+    NS = 3
+    streams = [torch.cuda.Stream() for _ in range(NS)]
     sets = [dict(c=coords, g=dout, o=out, dt=dtable)]
-    sets.append(dict(c=torch.empty_like(coords), g=torch.empty_like(dout), o=torch.empty_like(out),
-                     dt=torch.empty_like(dtable)))
+    for _ in range(NS - 1):
+        sets.append(dict(c=torch.empty_like(coords), g=torch.empty_like(dout), o=torch.empty_like(out),
+                         dt=torch.empty_like(dtable)))
     for b in sets:
         b["oh"] = torch.empty((N, cfg.L * cfg.F)).pin_memory()
         b["dth"] = torch.empty((enc.entries, cfg.F)).pin_memory()
 
     def e2e_step(k):
-        b, st = sets[k % 2], streams[k % 2]
+        b, st = sets[k % NS], streams[k % NS]
         enc.step_host(coords_h, dout_h, table, b["c"], b["g"], b["o"], b["dt"], b["oh"], b["dth"], st)
 
     ke = max(4, min(K, 10))
@@ -673,7 +680,7 @@ def run_ours(args, rank, local_rank, world):
         raise RuntimeError("e2e: the two pipelined buffer sets disagree")
     e2e = {"value": N * world * ke / e2e_s, "unit": UNIT, "h2d_bytes_per_step": N * 16 + N * cfg.L * cfg.F * 4,
            "d2h_bytes_per_step": N * cfg.L * cfg.F * 4 + enc.entries * cfg.F * 4, "steps": ke,
-           "api": "fh_encode_step_host (pinned host in/out), steps alternating over two streams / buffer sets"}
+           "api": "fh_encode_step_host (pinned host in/out), steps rotating over three streams / buffer sets"}
 
     # Train step (all §8(a) rows): free the encode buffers first.
     train = {}
@@ -727,9 +734,9 @@ def run_ours(args, rank, local_rank, world):
         "metric": METRIC, "value": value, "unit": UNIT, "n_gpus": world, "steps": K, "warmup": max(args.warmup, 3),
         "ms_per_step": total_s * 1e3 / K, "higher_is_better": True, "scaling": "weak", "vs_baseline": None,
         "dtype": "f32", "data": "synthetic", "config": config_block(cfg, N, world),
-        "kernels_ms": {"zero_grad": zero_ms, "encode_fwd": fwd_ms, "encode_bwd": bwd_ms, "step": step_ms},
+        "kernels_ms": {"zero_grad": "inside encode_bwd (FH_BWD_OVERWRITE)", "encode_fwd": fwd_ms, "encode_bwd": bwd_ms, "step": step_ms},
         "roofline": roofline, "gather_roofline": gather_roofline, "cpu_baseline": cpu, "e2e": e2e,
-        "gpu_launches": 2 * K, "clocks": clk.summary(), "train_step": train,
+        "gpu_launches": launches, "clocks": clk.summary(), "train_step": train,
         "paper_encoders": encoders, "coreset": coreset, "hbm_regime": hbm_regime,
     }
     print(json.dumps(line), flush=True)

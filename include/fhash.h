@@ -172,6 +172,16 @@ fh_status fh_encode_fwd(fh_encoder enc, const float *coords, int64_t N, const vo
 fh_status fh_encode_bwd(fh_encoder enc, const float *coords, int64_t N, const float *dout,
                         float *dtable, fh_stream stream);
 
+/* fh_encode_bwd_ex -- fh_encode_bwd with flags.  FH_BWD_OVERWRITE: dtable
+ * is OVERWRITTEN with the gradient instead of accumulated into; the library
+ * zeroes it level group by level group right before the launch that
+ * reduces into that group (so the zeroed lines are still L2-resident when
+ * the reductions arrive; a separate fh_zero_grad before the forward has
+ * them evicted by the forward's traffic).  Unknown flags: FH_E_ARG. */
+#define FH_BWD_OVERWRITE 1u
+fh_status fh_encode_bwd_ex(fh_encoder enc, const float *coords, int64_t N, const float *dout,
+                           float *dtable, unsigned flags, fh_stream stream);
+
 /* ---------------------------------------------------------------- a4 ---
  * fh_encode_indices -- the corner indices alone (steps 1-3), for parity:
  * idx [N][L][16] uint32 global entry indices (level offset included),
@@ -225,9 +235,10 @@ fh_status fh_encode_bwd_ordered(fh_encoder enc, const float *coords, int64_t N, 
 fh_status fh_zero_grad(fh_encoder enc, float *dtable, fh_stream stream);
 
 /* fh_encode_fwd_bwd -- one encode step on device buffers, the unit
- * bench.py times for BASELINE.json configs[1]: if zero_dtable, dtable is
- * zeroed (cudaMemsetAsync) first; then fh_encode_fwd (out, out_dtype) and
- * fh_encode_bwd (dout -> dtable).  Arguments and errors as those calls. */
+ * bench.py times for BASELINE.json configs[1]: fh_encode_fwd (out,
+ * out_dtype), then fh_encode_bwd_ex (dout -> dtable; FH_BWD_OVERWRITE when
+ * zero_dtable, i.e. dtable = the gradient, else dtable += it).  Arguments
+ * and errors as those calls. */
 fh_status fh_encode_fwd_bwd(fh_encoder enc, const float *coords, int64_t N, const void *table,
                             void *out, fh_dtype out_dtype, const float *dout, float *dtable,
                             int zero_dtable, fh_stream stream);
@@ -235,12 +246,14 @@ fh_status fh_encode_fwd_bwd(fh_encoder enc, const float *coords, int64_t N, cons
 /* fh_encode_step_host -- one encode fwd+bwd step from HOST buffers (the
  * end-to-end form used by bench.py's "e2e" figure): copies coords_h
  * [N][4] and dout_h [N][L*F] (pinned host memory for asynchrony) into the
- * caller's device buffers coords_d / dout_d, zeroes dtable_d, runs
- * fh_encode_fwd (out_d, f32) and fh_encode_bwd, and copies out_d -> out_h
- * and dtable_d -> dtable_h.  All on `stream`; returns without waiting.
- * Stream-ordered, so a caller pipelines consecutive steps by alternating two
- * streams with two sets of device buffers and host outputs: step k+1's H2D
- * then overlaps step k's kernels and D2H (bench.py's e2e does this).
+ * caller's device buffers coords_d / dout_d, runs fh_encode_fwd (out_d,
+ * f32) and fh_encode_bwd_ex (FH_BWD_OVERWRITE: dtable_d = the gradient), and
+ * copies out_d -> out_h and dtable_d -> dtable_h.  All on `stream`; returns
+ * without waiting.  Stream-ordered, so a caller pipelines consecutive steps
+ * by rotating over several streams with their own device buffers and host
+ * outputs: step k+1's H2D then overlaps step k's kernels and step k-1's D2H
+ * (bench.py's e2e uses three).  The encoder keeps its shifted-pair scratch
+ * per stream, so concurrent steps on different streams do not share it.
  * Errors: as the calls it makes. */
 fh_status fh_encode_step_host(fh_encoder enc, const float *coords_h, const float *dout_h,
                               int64_t N, const void *table_d, float *coords_d, float *dout_d,
@@ -423,6 +436,12 @@ int64_t   fh_arm_pace(int64_t n_rays, int64_t n_alive);
 size_t    fh_level_stats_workspace_size(fh_encoder enc, int level);
 fh_status fh_level_stats(fh_encoder enc, int level, void *workspace, size_t workspace_bytes, uint64_t *out,
                          fh_stream stream);
+
+/* fh_kernel_launches -- number of CUDA kernels this library has launched
+ * so far (all threads, all encoders / trainers; the method's kernels, not
+ * the fhash_bench.h / fhash_data.h harness kernels, not memset / memcpy).
+ * Read before and after a region to count its launches. */
+unsigned long long fh_kernel_launches(void);
 
 /* Thread-local text of the last error on this thread ("" if none). */
 const char *fh_last_error(void);

@@ -558,10 +558,10 @@ static Layout layout(const Dims &d) {
 static void scan_u32(uint32_t *a, uint64_t n, uint32_t *scratch, cudaStream_t s) {
     if (n == 0) return;
     const uint64_t blocks = (n + 1023) / 1024;
-    scan_block_kernel<<<(unsigned)blocks, 1024, 0, s>>>(a, n, blocks > 1 ? scratch : nullptr);
+    { scan_block_kernel<<<(unsigned)blocks, 1024, 0, s>>>(a, n, blocks > 1 ? scratch : nullptr); fh::count_launch(); }
     if (blocks > 1) {
         scan_u32(scratch, blocks, scratch + up(4 * blocks) / 4, s);
-        add_block_offsets_kernel<<<(unsigned)blocks, 1024, 0, s>>>(a, n, scratch);
+        { add_block_offsets_kernel<<<(unsigned)blocks, 1024, 0, s>>>(a, n, scratch); fh::count_launch(); }
     }
 }
 
@@ -623,21 +623,21 @@ fh_status fh_coreset_build(const float *vol, const uint32_t dims_xyz[3], int n_f
     uint32_t *counts = reinterpret_cast<uint32_t *>(w + L.counts);
     uint32_t *offs = reinterpret_cast<uint32_t *>(w + L.offs);
     if (spec->kind == FH_FEAT_ISOSURFACE)
-        straddle_kernel<<<grid_for(32 * L.swords), kThreads, 0, s>>>(vol, d, spec->p0, sb);
-    feature_kernel<<<grid_for(32ull * d.n * d.Z * d.Y), kThreads, 0, s>>>(vol, d, *spec, sb, f);
-    init_boxes_kernel<<<(6 * n_frames + 255) / 256, 256, 0, s>>>(boxes, n_frames);
-    dilate_kernel<<<(unsigned)L.nchunks, kThreads, 0, s>>>(f, d, dm, boxes, counts);
+        { straddle_kernel<<<grid_for(32 * L.swords), kThreads, 0, s>>>(vol, d, spec->p0, sb); fh::count_launch(); }
+    { feature_kernel<<<grid_for(32ull * d.n * d.Z * d.Y), kThreads, 0, s>>>(vol, d, *spec, sb, f); fh::count_launch(); }
+    { init_boxes_kernel<<<(6 * n_frames + 255) / 256, 256, 0, s>>>(boxes, n_frames); fh::count_launch(); }
+    { dilate_kernel<<<(unsigned)L.nchunks, kThreads, 0, s>>>(f, d, dm, boxes, counts); fh::count_launch(); }
     if (occupancy) {
         // the cell-row mask reuses the straddle bit buffer (same shape)
-        cellrow_kernel<<<grid_for(L.swords), kThreads, 0, s>>>(dm, d, sb);
+        { cellrow_kernel<<<grid_for(L.swords), kThreads, 0, s>>>(dm, d, sb); fh::count_launch(); }
         const uint64_t words = fh_occupancy_words(dims_xyz);
         const dim3 og(grid_for(words), (unsigned)d.n);
-        occupancy_kernel<<<og, kThreads, 0, s>>>(sb, d, make_morton(d.X, d.Y, d.Z), words, occupancy);
+        { occupancy_kernel<<<og, kThreads, 0, s>>>(sb, d, make_morton(d.X, d.Y, d.Z), words, occupancy); fh::count_launch(); }
     }
     cudaMemcpyAsync(offs, counts, 4 * L.nchunks, cudaMemcpyDeviceToDevice, s);
     scan_u32(offs, L.nchunks, reinterpret_cast<uint32_t *>(w + L.scratch), s);
-    fbb_kernel<<<1, 1, 0, s>>>(boxes, n_frames, d, offs, counts, L.nchunks, fbb, reinterpret_cast<int *>(w + L.fbb),
-                               count);
+    { fbb_kernel<<<1, 1, 0, s>>>(boxes, n_frames, d, offs, counts, L.nchunks, fbb, reinterpret_cast<int *>(w + L.fbb),
+                               count); fh::count_launch(); }
     return cuda_check(cudaGetLastError(), "fh_coreset_build launch");
 }
 
@@ -655,9 +655,9 @@ fh_status fh_coreset_emit(const float *vol, const uint32_t dims_xyz[3], int n_fr
     if (capacity == 0) return FH_OK;
     cudaStream_t s = reinterpret_cast<cudaStream_t>(stream);
     const char *w = reinterpret_cast<const char *>(workspace);
-    emit_kernel<<<(unsigned)L.nchunks, kThreads, 0, s>>>(
+    { emit_kernel<<<(unsigned)L.nchunks, kThreads, 0, s>>>(
         reinterpret_cast<const uint32_t *>(w + L.dm), vol, d, reinterpret_cast<const uint32_t *>(w + L.offs),
-        reinterpret_cast<const int *>(w + L.fbb), reinterpret_cast<float4 *>(coords), values, capacity);
+        reinterpret_cast<const int *>(w + L.fbb), reinterpret_cast<float4 *>(coords), values, capacity); fh::count_launch(); }
     return cuda_check(cudaGetLastError(), "fh_coreset_emit launch");
 }
 

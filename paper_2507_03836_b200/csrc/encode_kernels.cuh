@@ -519,8 +519,9 @@ __global__ void __launch_bounds__(256) bwd_kernel(const __grid_constant__ Params
 // odd (F = 2; i = 3 mod 4 for F = 1) straddles a 16-byte chunk of the table.
 // The forward reads it from a copy of the table shifted by one entry; the
 // backward reduces it into a scratch gsh shifted by two floats
-// (kShiftFloats), which this kernel adds back, dtable[m + 2] += gsh[m], and
-// re-zeroes, over float range [m0, m1) of gsh (m0 even).
+// (kShiftFloats), which this kernel adds back, dtable[m + 2] += gsh[m], over
+// float range [m0, m1) of gsh (m0 even; the host zeroes that range right
+// before the group's backward launch).
 constexpr int kShiftFloats = 2;
 
 __global__ void __launch_bounds__(256) merge_shift_kernel(float *__restrict__ dtable, float *__restrict__ gsh,
@@ -535,7 +536,6 @@ __global__ void __launch_bounds__(256) merge_shift_kernel(float *__restrict__ dt
             d.x += v.x;
             d.y += v.y;
             d2[q] = d;
-            g2[q] = make_float2(0.f, 0.f);
         }
     }
 }

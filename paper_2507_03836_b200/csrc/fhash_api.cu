@@ -17,6 +17,7 @@
 
 namespace fh {
 thread_local char g_err[512] = "";
+std::atomic<unsigned long long> g_launches{0};
 }
 using fh::aligned;
 using fh::cuda_check;
@@ -300,9 +301,9 @@ static void launch_fwd(fh_encoder e, const float *coords, int64_t N, const void 
             cudaFuncSetAttribute(fh::tiled::fwd_tiled_kernel<F, T, O>, cudaFuncAttributeMaxDynamicSharedMemorySize,
                                  box_bytes);
             const unsigned grid = (unsigned)((N + ts.S - 1) / ts.S);
-            fh::tiled::fwd_tiled_kernel<F, T, O><<<grid, fh::tiled::kThreads, box_bytes, s>>>(
+            { fh::tiled::fwd_tiled_kernel<F, T, O><<<grid, fh::tiled::kThreads, box_bytes, s>>>(
                 e->params, ts, c4, N, perm, reinterpret_cast<const T *>(table), full_blocks,
-                reinterpret_cast<O *>(out), e->flag);
+                reinterpret_cast<O *>(out), e->flag); fh::count_launch(); }
         }
         if (!e->fine_order) dperm = nullptr;  // direct levels: natural order (coalesced rows)
     }
@@ -312,9 +313,9 @@ static void launch_fwd(fh_encoder e, const float *coords, int64_t N, const void 
     const double limit = N < (1 << 15) ? 0.0 : e->fwd_limit;
     const int n = split_lists(e, include, (double)F * sizeof(T), limit, lists, sh);
     for (int g = 0; g < n; g++)
-        fh::fwd_kernel<F, T, O><<<grid_for(N, lists[g].n), 256, 0, s>>>(
+        { fh::fwd_kernel<F, T, O><<<grid_for(N, lists[g].n), 256, 0, s>>>(
             prm, c4, N, reinterpret_cast<const T *>(table), tsh, reinterpret_cast<O *>(out), e->flag,
-            lists[g], dperm);
+            lists[g], dperm); fh::count_launch(); }
 }
 
 template <typename T, typename O>
@@ -334,8 +335,8 @@ static void launch_bwd_direct(fh_encoder e, const float4 *c4, int64_t N, const f
     fh::LevelList lists[FH_MAX_LEVELS];
     const int n = split_lists(e, include, (double)F * 4.0, e->bwd_limit, lists);
     for (int g = 0; g < n; g++)
-        fh::bwd_kernel<F><<<grid_for(N, lists[g].n), 256, 0, s>>>(e->params, c4, N, dout, dtable, nullptr, e->flag,
-                                                                   lists[g], perm);
+        { fh::bwd_kernel<F><<<grid_for(N, lists[g].n), 256, 0, s>>>(e->params, c4, N, dout, dtable, nullptr, e->flag,
+                                                                   lists[g], perm); fh::count_launch(); }
 }
 
 // Ordered backward: levels where a sorted warp's samples nearly always share
@@ -365,8 +366,8 @@ static void launch_bwd_ordered(fh_encoder e, const float4 *c4, int64_t N, const 
     for (int g = 0; g < n; g++) {
         const int64_t warps = (N + 31) / 32 * lists[g].n;
         const unsigned grid = (unsigned)((warps + fh::tiled::kAggWarps - 1) / fh::tiled::kAggWarps);
-        fh::tiled::bwd_agg_kernel<F><<<grid, fh::tiled::kAggThreads, smem, s>>>(e->params, lists[g], c4, N, perm, dout,
-                                                                           dtable, e->flag);
+        { fh::tiled::bwd_agg_kernel<F><<<grid, fh::tiled::kAggThreads, smem, s>>>(e->params, lists[g], c4, N, perm, dout,
+                                                                           dtable, e->flag); fh::count_launch(); }
     }
     launch_bwd_direct<F>(e, c4, N, dout, dtable, s, e->fine_order ? perm : nullptr, rest);
 }
@@ -600,6 +601,8 @@ fh_status fh_build_mhe(const uint32_t *res, int L, int F, fh_dtype table_dtype, 
 
 int fh_encoder_kind(fh_encoder e) { return e ? e->kind : -1; }
 
+unsigned long long fh_kernel_launches(void) { return fh::g_launches.load(std::memory_order_relaxed); }
+
 }  // extern "C"
 
 template <typename T, typename O>
@@ -611,10 +614,10 @@ static void dispatch_mhe_fwd(fh_encoder e, const float *coords, int64_t N, const
         const T *tb = reinterpret_cast<const T *>(table);
         O *o = reinterpret_cast<O *>(out);
         switch (e->F) {
-            case 1: fh::mhe::fwd_kernel<1, T, O><<<grid_for(N, lc), 256, 0, s>>>(e->params, c4, N, tb, o, e->flag, l0, lc); break;
-            case 2: fh::mhe::fwd_kernel<2, T, O><<<grid_for(N, lc), 256, 0, s>>>(e->params, c4, N, tb, o, e->flag, l0, lc); break;
-            case 4: fh::mhe::fwd_kernel<4, T, O><<<grid_for(N, lc), 256, 0, s>>>(e->params, c4, N, tb, o, e->flag, l0, lc); break;
-            default: fh::mhe::fwd_kernel<8, T, O><<<grid_for(N, lc), 256, 0, s>>>(e->params, c4, N, tb, o, e->flag, l0, lc); break;
+            case 1: { fh::mhe::fwd_kernel<1, T, O><<<grid_for(N, lc), 256, 0, s>>>(e->params, c4, N, tb, o, e->flag, l0, lc); fh::count_launch(); } break;
+            case 2: { fh::mhe::fwd_kernel<2, T, O><<<grid_for(N, lc), 256, 0, s>>>(e->params, c4, N, tb, o, e->flag, l0, lc); fh::count_launch(); } break;
+            case 4: { fh::mhe::fwd_kernel<4, T, O><<<grid_for(N, lc), 256, 0, s>>>(e->params, c4, N, tb, o, e->flag, l0, lc); fh::count_launch(); } break;
+            default: { fh::mhe::fwd_kernel<8, T, O><<<grid_for(N, lc), 256, 0, s>>>(e->params, c4, N, tb, o, e->flag, l0, lc); fh::count_launch(); } break;
         }
     }
 }
@@ -655,18 +658,26 @@ static fh_status encode_fwd_impl(fh_encoder e, const float *coords, int64_t N, c
 
 static fh_status encode_bwd_impl(fh_encoder e, const float *coords, int64_t N, const uint32_t *perm,
                                  const float *dout, float *dtable, fh_stream stream,
-                                 cudaEvent_t *ev = nullptr, int n_ev = 0) {
+                                 cudaEvent_t *ev = nullptr, int n_ev = 0, bool zero = false) {
     g_err[0] = 0;
     fh_status st = check_common(e, coords, N, "fh_encode_bwd");
     if (st != FH_OK) return st;
-    if (N == 0) return FH_OK;
-    if (!dout || !aligned(dout, 4)) return fail(FH_E_ARG, "fh_encode_bwd: NULL/misaligned dout");
     const size_t vec = (size_t)e->F * 4;
     if (!dtable || !aligned(dtable, vec > 16 ? 16 : vec)) return fail(FH_E_ARG, "fh_encode_bwd: NULL/misaligned dtable");
-    if ((st = ensure_flag(e)) != FH_OK) return st;
     cudaStream_t s = reinterpret_cast<cudaStream_t>(stream);
+    // zero: dtable is overwritten -- zeroed range by range right before the
+    // launch that reduces into it, so the zero lines are still in L2 when the
+    // reductions arrive (no DRAM read of a zeroed gradient)
+    auto zero_levels = [&](int l0, int l1) -> fh_status {
+        const uint64_t a = e->info[l0].offset, b = e->info[l1 - 1].offset + e->info[l1 - 1].table_size;
+        return cuda_check(cudaMemsetAsync(dtable + a * e->F, 0, (b - a) * e->F * 4, s), "fh_encode_bwd: zero dtable");
+    };
+    if (N == 0) return zero ? zero_levels(0, e->L) : FH_OK;
+    if (!dout || !aligned(dout, 4)) return fail(FH_E_ARG, "fh_encode_bwd: NULL/misaligned dout");
+    if ((st = ensure_flag(e)) != FH_OK) return st;
     const float4 *c4 = reinterpret_cast<const float4 *>(coords);
     if (e->kind == 1 && perm) return fail(FH_E_ARG, "fh_encode_bwd_ordered: not supported for MHE encoders");
+    if (perm && zero && (st = zero_levels(0, e->L)) != FH_OK) return st;
     if (perm) {
         switch (e->F) {
             case 1: launch_bwd_ordered<1>(e, c4, N, dout, dtable, s, perm); break;
@@ -677,6 +688,9 @@ static fh_status encode_bwd_impl(fh_encoder e, const float *coords, int64_t N, c
         return cuda_check(cudaGetLastError(), "fh_encode_bwd_ordered launch");
     }
     if (e->small.n > 0) {
+        if (zero)
+            for (int j = 0; j < e->small.n; j++)
+                if ((st = zero_levels(e->small.id[j], e->small.id[j] + 1)) != FH_OK) return st;
         const int smem = e->small.total * 4;
         int64_t blocks = (N * e->small.n + 255) / 256;
         if (blocks > 2 * 148) blocks = 2 * 148;
@@ -687,7 +701,7 @@ static fh_status encode_bwd_impl(fh_encoder e, const float *coords, int64_t N, c
     q = cuda_check(cudaFuncSetAttribute(fh::bwd_small_kernel<FF>, cudaFuncAttributeMaxDynamicSharedMemorySize, \
                                         smem), "cudaFuncSetAttribute(bwd_small)");                           \
     if (q != FH_OK) return q;                                                                                 \
-    fh::bwd_small_kernel<FF><<<g, 256, smem, s>>>(e->params, e->small, c4, N, dout, dtable, e->flag, perm);   \
+    { fh::bwd_small_kernel<FF><<<g, 256, smem, s>>>(e->params, e->small, c4, N, dout, dtable, e->flag, perm); fh::count_launch(); }   \
     break;
             case 1: FH_SMALL(1)
             case 2: FH_SMALL(2)
@@ -711,12 +725,13 @@ static fh_status encode_bwd_impl(fh_encoder e, const float *coords, int64_t N, c
     for (int k = 0; k < e->n_gb; k++) {
         const int l0 = e->gb[2 * k], lc = e->gb[2 * k + 1] - e->gb[2 * k];
         const dim3 g = grid_for(N, lc);
+        if (zero && (st = zero_levels(l0, l0 + lc)) != FH_OK) return st;
         if (e->kind == 1) {
             switch (e->F) {
-                case 1: fh::mhe::bwd_kernel<1><<<g, 256, 0, s>>>(e->params, c4, N, dout, dtable, e->flag, l0, lc); break;
-                case 2: fh::mhe::bwd_kernel<2><<<g, 256, 0, s>>>(e->params, c4, N, dout, dtable, e->flag, l0, lc); break;
-                case 4: fh::mhe::bwd_kernel<4><<<g, 256, 0, s>>>(e->params, c4, N, dout, dtable, e->flag, l0, lc); break;
-                default: fh::mhe::bwd_kernel<8><<<g, 256, 0, s>>>(e->params, c4, N, dout, dtable, e->flag, l0, lc); break;
+                case 1: { fh::mhe::bwd_kernel<1><<<g, 256, 0, s>>>(e->params, c4, N, dout, dtable, e->flag, l0, lc); fh::count_launch(); } break;
+                case 2: { fh::mhe::bwd_kernel<2><<<g, 256, 0, s>>>(e->params, c4, N, dout, dtable, e->flag, l0, lc); fh::count_launch(); } break;
+                case 4: { fh::mhe::bwd_kernel<4><<<g, 256, 0, s>>>(e->params, c4, N, dout, dtable, e->flag, l0, lc); fh::count_launch(); } break;
+                default: { fh::mhe::bwd_kernel<8><<<g, 256, 0, s>>>(e->params, c4, N, dout, dtable, e->flag, l0, lc); fh::count_launch(); } break;
             }
             continue;
         }
@@ -729,20 +744,23 @@ static fh_status encode_bwd_impl(fh_encoder e, const float *coords, int64_t N, c
         }
         const uint64_t ge = e->info[l0 + lc - 1].offset + e->info[l0 + lc - 1].table_size - e->info[l0].offset;
         float *gsh = shift && (double)N * lc * 2.0 >= (double)ge ? gsh_buf : nullptr;
+        // this group's range of the shifted scratch, zeroed right before use
+        int64_t m0 = (int64_t)e->info[l0].offset * e->F - fh::kShiftFloats;
+        const int64_t m1 = (int64_t)(e->info[l0 + lc - 1].offset + e->info[l0 + lc - 1].table_size) * e->F - fh::kShiftFloats;
+        if (m0 < 0) m0 = 0;
+        if (gsh && (st = cuda_check(cudaMemsetAsync(gsh + m0, 0, (size_t)(m1 - m0) * 4, s), "zero gsh")) != FH_OK)
+            return st;
         switch (e->F) {
-            case 1: fh::bwd_kernel<1><<<g, 256, 0, s>>>(e->params, c4, N, dout, dtable, gsh, e->flag, ll, nullptr); break;
-            case 2: fh::bwd_kernel<2><<<g, 256, 0, s>>>(e->params, c4, N, dout, dtable, gsh, e->flag, ll, nullptr); break;
-            case 4: fh::bwd_kernel<4><<<g, 256, 0, s>>>(e->params, c4, N, dout, dtable, nullptr, e->flag, ll, nullptr); break;
-            default: fh::bwd_kernel<8><<<g, 256, 0, s>>>(e->params, c4, N, dout, dtable, nullptr, e->flag, ll, nullptr); break;
+            case 1: { fh::bwd_kernel<1><<<g, 256, 0, s>>>(e->params, c4, N, dout, dtable, gsh, e->flag, ll, nullptr); fh::count_launch(); } break;
+            case 2: { fh::bwd_kernel<2><<<g, 256, 0, s>>>(e->params, c4, N, dout, dtable, gsh, e->flag, ll, nullptr); fh::count_launch(); } break;
+            case 4: { fh::bwd_kernel<4><<<g, 256, 0, s>>>(e->params, c4, N, dout, dtable, nullptr, e->flag, ll, nullptr); fh::count_launch(); } break;
+            default: { fh::bwd_kernel<8><<<g, 256, 0, s>>>(e->params, c4, N, dout, dtable, nullptr, e->flag, ll, nullptr); fh::count_launch(); } break;
         }
-        if (gsh) {   // fold this group's shifted partial sums back into dtable (and re-zero them)
-            const fh_level_info &a = e->info[l0], &b = e->info[l0 + lc - 1];
-            int64_t m0 = (int64_t)a.offset * e->F - fh::kShiftFloats, m1 = (int64_t)(b.offset + b.table_size) * e->F - fh::kShiftFloats;
-            if (m0 < 0) m0 = 0;
+        if (gsh) {   // fold this group's shifted partial sums back into dtable
             const int64_t q = (m1 - m0 + 1) / 2;
             int64_t blocks = (q + 255) / 256;
             if (blocks > (int64_t)e->n_sm * 8) blocks = (int64_t)e->n_sm * 8;
-            if (blocks > 0) fh::merge_shift_kernel<<<(unsigned)blocks, 256, 0, s>>>(dtable, gsh, m0, m1);
+            if (blocks > 0) { fh::merge_shift_kernel<<<(unsigned)blocks, 256, 0, s>>>(dtable, gsh, m0, m1); fh::count_launch(); }
         }
         if (ev && ev0 + k < n_ev) cudaEventRecord(ev[ev0 + k], s);
     }
@@ -788,6 +806,12 @@ extern "C" {
 fh_status fh_encode_fwd(fh_encoder e, const float *coords, int64_t N, const void *table, void *out,
                         fh_dtype out_dtype, fh_stream stream) {
     return encode_fwd_impl(e, coords, N, nullptr, table, out, out_dtype, stream);
+}
+
+fh_status fh_encode_bwd_ex(fh_encoder e, const float *coords, int64_t N, const float *dout, float *dtable,
+                           unsigned flags, fh_stream stream) {
+    if (flags & ~(unsigned)FH_BWD_OVERWRITE) return fail(FH_E_ARG, "fh_encode_bwd_ex: unknown flags 0x%x", flags);
+    return encode_bwd_impl(e, coords, N, nullptr, dout, dtable, stream, nullptr, 0, (flags & FH_BWD_OVERWRITE) != 0);
 }
 
 fh_status fh_encode_bwd(fh_encoder e, const float *coords, int64_t N, const float *dout, float *dtable,
@@ -837,9 +861,9 @@ fh_status fh_spatial_sort(fh_encoder e, const float *coords, int64_t N, uint32_t
     if (st != FH_OK) return st;
     int64_t g = (N + 255) / 256;
     if (g > 148 * 16) g = 148 * 16;
-    fh::sortk::key_hist_kernel<<<(unsigned)g, 256, 0, s>>>(e->key, reinterpret_cast<const float4 *>(coords), N, keys, hist);
-    fh::sortk::scan_blocks_kernel<<<fh::sortk::kScanBlocks, 1024, 0, s>>>(hist, sums);
-    fh::sortk::scatter_kernel<<<(unsigned)g, 256, 0, s>>>(keys, N, hist, sums, order);
+    { fh::sortk::key_hist_kernel<<<(unsigned)g, 256, 0, s>>>(e->key, reinterpret_cast<const float4 *>(coords), N, keys, hist); fh::count_launch(); }
+    { fh::sortk::scan_blocks_kernel<<<fh::sortk::kScanBlocks, 1024, 0, s>>>(hist, sums); fh::count_launch(); }
+    { fh::sortk::scatter_kernel<<<(unsigned)g, 256, 0, s>>>(keys, N, hist, sums, order); fh::count_launch(); }
     return cuda_check(cudaGetLastError(), "fh_spatial_sort launch");
 }
 
@@ -853,11 +877,11 @@ fh_status fh_encode_indices(fh_encoder e, const float *coords, int64_t N, uint32
     if ((st = ensure_flag(e)) != FH_OK) return st;
     cudaStream_t s = reinterpret_cast<cudaStream_t>(stream);
     if (e->kind == 1)
-        fh::mhe::indices_kernel<<<grid_for(N, e->L), 256, 0, s>>>(
-            e->params, reinterpret_cast<const float4 *>(coords), N, idx, w, e->flag);
+        { fh::mhe::indices_kernel<<<grid_for(N, e->L), 256, 0, s>>>(
+            e->params, reinterpret_cast<const float4 *>(coords), N, idx, w, e->flag); fh::count_launch(); }
     else
-        fh::indices_kernel<<<grid_for(N, e->L), 256, 0, s>>>(e->params, reinterpret_cast<const float4 *>(coords),
-                                                             N, idx, w, e->flag);
+        { fh::indices_kernel<<<grid_for(N, e->L), 256, 0, s>>>(e->params, reinterpret_cast<const float4 *>(coords),
+                                                             N, idx, w, e->flag); fh::count_launch(); }
     return cuda_check(cudaGetLastError(), "fh_encode_indices launch");
 }
 
@@ -875,12 +899,8 @@ fh_status fh_encode_fwd_bwd(fh_encoder e, const float *coords, int64_t N, const 
     if (!e) return fail(FH_E_ARG, "fh_encode_fwd_bwd: NULL encoder");
     if (!dtable) return fail(FH_E_ARG, "fh_encode_fwd_bwd: NULL dtable");
     fh_status st;
-    if (zero_dtable &&
-        (st = cuda_check(cudaMemsetAsync(dtable, 0, e->entries * e->F * 4, reinterpret_cast<cudaStream_t>(stream)),
-                         "memset dtable")) != FH_OK)
-        return st;
     if ((st = fh_encode_fwd(e, coords, N, table, out, out_dtype, stream)) != FH_OK) return st;
-    return fh_encode_bwd(e, coords, N, dout, dtable, stream);
+    return fh_encode_bwd_ex(e, coords, N, dout, dtable, zero_dtable ? FH_BWD_OVERWRITE : 0, stream);
 }
 
 fh_status fh_encode_step_host(fh_encoder e, const float *coords_h, const float *dout_h, int64_t N,
@@ -895,9 +915,8 @@ fh_status fh_encode_step_host(fh_encoder e, const float *coords_h, const float *
     fh_status st;
     if ((st = cuda_check(cudaMemcpyAsync(coords_d, coords_h, (size_t)N * 16, cudaMemcpyHostToDevice, s), "H2D coords")) != FH_OK) return st;
     if ((st = cuda_check(cudaMemcpyAsync(dout_d, dout_h, (size_t)N * LF * 4, cudaMemcpyHostToDevice, s), "H2D dout")) != FH_OK) return st;
-    if ((st = cuda_check(cudaMemsetAsync(dtable_d, 0, e->entries * e->F * 4, s), "memset dtable")) != FH_OK) return st;
     if ((st = fh_encode_fwd(e, coords_d, N, table_d, out_d, FH_F32, stream)) != FH_OK) return st;
-    if ((st = fh_encode_bwd(e, coords_d, N, dout_d, dtable_d, stream)) != FH_OK) return st;
+    if ((st = fh_encode_bwd_ex(e, coords_d, N, dout_d, dtable_d, FH_BWD_OVERWRITE, stream)) != FH_OK) return st;
     if ((st = cuda_check(cudaMemcpyAsync(out_h, out_d, (size_t)N * LF * 4, cudaMemcpyDeviceToHost, s), "D2H out")) != FH_OK) return st;
     return cuda_check(cudaMemcpyAsync(dtable_h, dtable_d, e->entries * e->F * 4, cudaMemcpyDeviceToHost, s), "D2H dtable");
 }

@@ -1,5 +1,6 @@
 // internal.h -- shared host-side internals of libfhash.so (not part of the ABI).
 #pragma once
+#include <atomic>
 #include <cuda_runtime.h>
 
 #include <cstdarg>
@@ -29,6 +30,11 @@ inline fh_status cuda_check(cudaError_t e, const char *what) {
 
 inline bool aligned(const void *p, size_t a) { return (reinterpret_cast<uintptr_t>(p) % a) == 0; }
 inline size_t dtype_size(fh_dtype d) { return d == FH_F32 ? 4 : 2; }
+
+// Kernel launches issued by the library (fh_kernel_launches): incremented
+// at every launch site of the method's kernels.
+extern std::atomic<unsigned long long> g_launches;
+inline void count_launch() { g_launches.fetch_add(1, std::memory_order_relaxed); }
 
 // fhash_api.cu: backward launches and the gradient ranges they finalise.
 int bwd_launch_count(fh_encoder e);
@@ -75,7 +81,7 @@ struct fh_encoder_s {
         float *gsh = nullptr;
         size_t gsh_bytes = 0;
     };
-    static constexpr int kScratchSlots = 4;
+    static constexpr int kScratchSlots = 8;
     Scratch scratch[kScratchSlots];
     int pair_shift = 3;                              // FH_PAIR_SHIFT bits: 1 backward, 2 forward (default both)
     bool shiftable[FH_MAX_LEVELS] = {false};         // backward: level uses the shifted gradient pairs

@@ -88,11 +88,11 @@ fh_status fh_level_stats(fh_encoder e, int level, void *workspace, size_t worksp
     if (st != FH_OK) return st;
     uint64_t g = (C + 255) / 256;
     if (g > 148ull * 64) g = 148ull * 64;
-    fh_stats::stats_mark_kernel<<<(unsigned)(g ? g : 1), 256, 0, s>>>(e->params.lv[level], e->kind, C, T, bits);
+    { fh_stats::stats_mark_kernel<<<(unsigned)(g ? g : 1), 256, 0, s>>>(e->params.lv[level], e->kind, C, T, bits); fh::count_launch(); }
     uint64_t g2 = (words + 255) / 256;
     if (g2 > 148ull * 16) g2 = 148ull * 16;
-    fh_stats::stats_count_kernel<<<(unsigned)(g2 ? g2 : 1), 256, 0, s>>>(bits, words,
-                                                                reinterpret_cast<unsigned long long *>(out));
+    { fh_stats::stats_count_kernel<<<(unsigned)(g2 ? g2 : 1), 256, 0, s>>>(bits, words,
+                                                                reinterpret_cast<unsigned long long *>(out)); fh::count_launch(); }
     return fh::cuda_check(cudaGetLastError(), "fh_level_stats launch");
 }
 

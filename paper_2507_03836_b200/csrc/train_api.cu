@@ -70,7 +70,7 @@ fh_status launch_mlp(fh_trainer tr, const float *target, int64_t N, int64_t N_gl
     const int64_t tiles = (N + fh::mlp::TILE - 1) / fh::mlp::TILE;
     const int64_t pairs = (tiles + 1) / 2;  // two tile slots per CTA
     const int grid = (int)(pairs < tr->n_sm ? pairs : tr->n_sm);
-    fh::mlp::mlp_train_kernel<K0><<<grid, 256, smem, s>>>(a);
+    { fh::mlp::mlp_train_kernel<K0><<<grid, 256, smem, s>>>(a); fh::count_launch(); }
     return cuda_check(cudaGetLastError(), "mlp_train_kernel launch");
 }
 
@@ -241,7 +241,7 @@ static fh_status apply_ranges_impl(fh_trainer tr, int n, const int64_t *begin, c
     add(M, 4);
     A.nseg = k;
     A.block0[k] = blocks;
-    fh::mlp::adam_kernel<<<(unsigned)blocks, 256, 0, s>>>(A);
+    { fh::mlp::adam_kernel<<<(unsigned)blocks, 256, 0, s>>>(A); fh::count_launch(); }
     return cuda_check(cudaGetLastError(), "adam_kernel launch");
 }
 
@@ -367,7 +367,7 @@ fh_status fh_train_apply_peers(fh_trainer tr, int W, const float *const *peer_ta
     if (k == 0) return FH_OK;
     A.nseg = k;
     A.block0[k] = blocks;
-    fh::mlp::adam_peers_kernel<<<(unsigned)blocks, 256, 0, reinterpret_cast<cudaStream_t>(stream)>>>(A, P);
+    { fh::mlp::adam_peers_kernel<<<(unsigned)blocks, 256, 0, reinterpret_cast<cudaStream_t>(stream)>>>(A, P); fh::count_launch(); }
     return cuda_check(cudaGetLastError(), "adam_peers_kernel launch");
 }
 
@@ -441,7 +441,7 @@ fh_status fh_infer(fh_encoder enc, const fh_mlp_desc *m, const void *table, cons
         fh_status q = cuda_check(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, smem),
                                  "cudaFuncSetAttribute(mlp_infer)");
         if (q != FH_OK) return q;
-        kern<<<grid, 256, smem, s>>>(a);
+        { kern<<<grid, 256, smem, s>>>(a); fh::count_launch(); }
         return cuda_check(cudaGetLastError(), "mlp_infer_kernel launch");
     };
     switch (m->n_in) {

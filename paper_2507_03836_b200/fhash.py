@@ -25,7 +25,7 @@ _STATUS_NAMES = {0: "FH_OK", -1: "FH_E_ARG", -2: "FH_E_RANGE", -3: "FH_E_DOMAIN"
 # Every symbol include/fhash.h declares (checked by tests/test_abi.py).
 EXPORTS = [
     "fh_fold_schedule", "fh_build_levels", "fh_level_info_get", "fh_num_levels", "fh_feature_dim",
-    "fh_table_entries", "fh_param_count", "fh_encoder_destroy", "fh_encode_fwd", "fh_encode_bwd",
+    "fh_table_entries", "fh_param_count", "fh_encoder_destroy", "fh_encode_fwd", "fh_encode_bwd", "fh_encode_bwd_ex",
     "fh_encode_indices", "fh_zero_grad", "fh_encode_fwd_bwd", "fh_encode_step_host", "fh_status_sync", "fh_last_error",
     "fh_version", "fh_spatial_sort_workspace_size", "fh_spatial_sort", "fh_encode_fwd_ordered",
     "fh_encode_bwd_ordered", "fh_build_mhe", "fh_encoder_kind", "fh_spatial_sort_bits", "fh_build_levels_lin",
@@ -35,7 +35,7 @@ EXPORTS = [
     "fh_mlp_param_count", "fh_train_workspace_size", "fh_trainer_create", "fh_train_fwd_bwd", "fh_train_apply",
     "fh_train_step", "fh_trainer_status", "fh_trainer_step_count", "fh_trainer_destroy", "fh_train_apply_sharded",
     "fh_train_bwd_launches", "fh_train_bwd_ranges", "fh_train_set_bwd_events", "fh_train_apply_ranges",
-    "fh_train_apply_peers", "fh_level_stats_workspace_size", "fh_level_stats",
+    "fh_train_apply_peers", "fh_level_stats_workspace_size", "fh_level_stats", "fh_kernel_launches",
     # inference (renderer's model evaluation) and the ARM pace rule
     "fh_infer_workspace_size", "fh_infer", "fh_arm_pace",
     # include/fhash_coreset.h (NEXT-4 coreset selection)
@@ -90,6 +90,8 @@ def lib() -> ctypes.CDLL:
     L.fh_encode_bwd.argtypes = [vp, vp, i64, vp, vp, vp]
     L.fh_encode_indices.argtypes = [vp, vp, i64, vp, vp, vp]
     L.fh_encode_fwd_bwd.argtypes = [vp, vp, i64, vp, vp, c_int, vp, vp, c_int, vp]
+    L.fh_encode_bwd_ex.argtypes = [vp, vp, i64, vp, vp, ctypes.c_uint, vp]
+    L.fh_encode_bwd_ex.restype = c_int
     L.fh_zero_grad.argtypes = [vp, vp, vp]
     L.fh_build_mhe.argtypes = [ctypes.POINTER(ctypes.c_uint32), c_int, c_int, c_int, u64, ctypes.c_uint32,
                                ctypes.POINTER(vp)]
@@ -99,6 +101,8 @@ def lib() -> ctypes.CDLL:
     L.fh_level_stats_workspace_size.restype = ctypes.c_size_t
     L.fh_level_stats.argtypes = [vp, c_int, vp, ctypes.c_size_t, vp, vp]
     L.fh_level_stats.restype = c_int
+    L.fh_kernel_launches.argtypes = []
+    L.fh_kernel_launches.restype = ctypes.c_ulonglong
     L.fh_spatial_sort_workspace_size.argtypes = [i64]
     L.fh_spatial_sort_workspace_size.restype = ctypes.c_size_t
     L.fh_spatial_sort.argtypes = [vp, vp, i64, vp, vp, ctypes.c_size_t, vp]
@@ -204,9 +208,16 @@ class Encoder:
                                    _stream(stream)))
         return out
 
-    def bwd(self, coords, dout, dtable, stream=None):
-        _check(lib().fh_encode_bwd(self._h, _ptr(coords), coords.shape[0], _ptr(dout), _ptr(dtable),
-                                   _stream(stream)))
+    def bwd(self, coords, dout, dtable, stream=None, overwrite: bool = False):
+        """dtable += gradient (fh_encode_bwd), or dtable = gradient with
+        overwrite=True (fh_encode_bwd_ex FH_BWD_OVERWRITE: zeroed per level
+        group right before its reductions)."""
+        if overwrite:
+            _check(lib().fh_encode_bwd_ex(self._h, _ptr(coords), coords.shape[0], _ptr(dout), _ptr(dtable), 1,
+                                          _stream(stream)))
+        else:
+            _check(lib().fh_encode_bwd(self._h, _ptr(coords), coords.shape[0], _ptr(dout), _ptr(dtable),
+                                       _stream(stream)))
         return dtable
 
     def indices(self, coords, want_w: bool = True, stream=None):
@@ -305,6 +316,11 @@ def bench_gather_levels(buf, enc, entry_bytes: int, n_samples: int, sink, seed: 
 def bench_red_levels(buf, enc, entry_bytes: int, n_samples: int, seed: int = 0, stream=None):
     off, size = _level_arrays(enc)
     _check(lib().fh_bench_red_levels(_ptr(buf), off, size, enc.L, entry_bytes, n_samples, seed, _stream(stream)))
+
+
+def kernel_launches() -> int:
+    """Kernels the library has launched so far (fh_kernel_launches)."""
+    return int(lib().fh_kernel_launches())
 
 
 def bench_copy(dst, src, nbytes: int, stream=None):

@@ -121,6 +121,32 @@ def test_shifted_pairs_modes(shift, F, tdt, monkeypatch):
     check_bwd(dtable.cpu().numpy().astype(np.float64), 2 * G, 2 * A)
 
 
+@pytest.mark.parametrize("cfg", [W.CFG1, W.CFG1H], ids=lambda c: c.name)
+@pytest.mark.parametrize("N", [0, 1, 4096 + 37])
+def test_backward_overwrite(cfg, N):
+    """fh_encode_bwd_ex(FH_BWD_OVERWRITE): dtable = the gradient whatever it
+    held before (every level group, the shared-memory small levels and the
+    shifted scratch included); N = 0 leaves it all zero."""
+    case = W.encode_case(cfg, max(N, 1), seed=3)
+    enc = fh.Encoder(cfg.levels, cfg.F, cfg.table_dtype, cfg.cap)
+    ref = oracle.Levels(cfg.levels, cfg.cap)
+    dtable = torch.full((enc.entries, cfg.F), 7.0, device="cuda")
+    c, g = dev(case.coords[:N]), dev(case.dout[:N])
+    enc.bwd(c, g, dtable, overwrite=True)
+    assert enc.status_sync() == fh.FH_OK
+    if N == 0:
+        assert torch.count_nonzero(dtable).item() == 0
+        return
+    G, A = ref.backward(case.coords[:N], case.dout[:N], cfg.F, want_abs=True)
+    check_bwd(dtable.cpu().numpy().astype(np.float64), G, A)
+    # fh_encode_fwd_bwd(zero_dtable=1) is the same overwrite
+    dtable.fill_(-3.0)
+    out = torch.empty((N, enc.L * cfg.F), device="cuda")
+    enc.fwd_bwd(c, dev(case.table), out, g, dtable, zero_dtable=True)
+    assert enc.status_sync() == fh.FH_OK
+    check_bwd(dtable.cpu().numpy().astype(np.float64), G, A)
+
+
 @pytest.mark.parametrize("F", [1, 2, 4, 8])
 @pytest.mark.parametrize("tdt", ["f32", "f16"])
 def test_feature_widths_and_dtypes(F, tdt):

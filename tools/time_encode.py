@@ -37,9 +37,11 @@ def main():
     sorted_mode = os.environ.get("FH_SORTED", "0") == "1"
     so = fh.SpatialOrder(enc, N) if sorted_mode else None
     tf = tb = ts = 0.0
+    overwrite = os.environ.get("FH_OVERWRITE", "0") == "1"   # bwd overwrites dtable (no separate zero_grad)
     for it in range(iters + 3):
         flush.fill_(it & 255)
-        enc.zero_grad(dtab)
+        if not overwrite:
+            enc.zero_grad(dtab)
         e[0].record()
         order = so(coords) if so else None
         e[1].record()
@@ -51,7 +53,7 @@ def main():
         if so:
             enc.bwd_ordered(coords, order, dout, dtab)
         else:
-            enc.bwd(coords, dout, dtab)
+            enc.bwd(coords, dout, dtab, overwrite=overwrite)
         e[3].record()
         torch.cuda.synchronize()
         if it >= 3:
