@@ -174,28 +174,33 @@ template <> struct Gather<8, __half> {
 };
 
 // ------------------------------------------------------------ stores
+// The output rows and the coords / dout rows are streamed once per pass:
+// evict-first (st.global.cs / ld.global.cs) so they do not push the level
+// group's tables (forward) or gradients (backward) out of the L2.
 template <int F, typename O> struct Store;
 template <int F> struct Store<F, float> {
     static __device__ __forceinline__ void store(float *o, const float *v) {
-        if constexpr (F == 1) o[0] = v[0];
-        else if constexpr (F == 2) *reinterpret_cast<float2 *>(o) = make_float2(v[0], v[1]);
+        if constexpr (F == 1) __stcs(o, v[0]);
+        else if constexpr (F == 2) __stcs(reinterpret_cast<float2 *>(o), make_float2(v[0], v[1]));
         else {
 #pragma unroll
             for (int k = 0; k < F; k += 4)
-                *reinterpret_cast<float4 *>(o + k) = make_float4(v[k], v[k + 1], v[k + 2], v[k + 3]);
+                __stcs(reinterpret_cast<float4 *>(o + k), make_float4(v[k], v[k + 1], v[k + 2], v[k + 3]));
         }
     }
 };
 template <int F> struct Store<F, __nv_bfloat16> {
     static __device__ __forceinline__ void store(__nv_bfloat16 *o, const float *v) {
         if constexpr (F == 1) o[0] = __float2bfloat16_rn(v[0]);
-        else if constexpr (F == 2) *reinterpret_cast<__nv_bfloat162 *>(o) = __floats2bfloat162_rn(v[0], v[1]);
-        else if constexpr (F == 4) {
+        else if constexpr (F == 2) {
+            __nv_bfloat162 a = __floats2bfloat162_rn(v[0], v[1]);
+            __stcs(reinterpret_cast<unsigned int *>(o), *reinterpret_cast<unsigned int *>(&a));
+        } else if constexpr (F == 4) {
             __nv_bfloat162 a = __floats2bfloat162_rn(v[0], v[1]), b = __floats2bfloat162_rn(v[2], v[3]);
             uint2 u;
             u.x = *reinterpret_cast<uint32_t *>(&a);
             u.y = *reinterpret_cast<uint32_t *>(&b);
-            *reinterpret_cast<uint2 *>(o) = u;
+            __stcs(reinterpret_cast<uint2 *>(o), u);
         } else {
             uint4 u;
             uint32_t *pu = reinterpret_cast<uint32_t *>(&u);
@@ -204,7 +209,7 @@ template <int F> struct Store<F, __nv_bfloat16> {
                 __nv_bfloat162 a = __floats2bfloat162_rn(v[2 * k], v[2 * k + 1]);
                 pu[k] = *reinterpret_cast<uint32_t *>(&a);
             }
-            *reinterpret_cast<uint4 *>(o) = u;
+            __stcs(reinterpret_cast<uint4 *>(o), u);
         }
     }
 };
@@ -393,7 +398,7 @@ __global__ void __launch_bounds__(256, FwdMinBlocks<F>::value) fwd_kernel(const 
     const int l = LL.id[li];
     const int64_t n = perm ? (int64_t)__ldg(perm + j) : j;
     const Level lv = slv.get(l);
-    const float4 p = __ldg(coords + n);
+    const float4 p = __ldcs(coords + n);
     Cell c;
     const bool bad = cell_of(lv, p, c);
     if (bad && li == 0) atomicOr(flag, 1);
@@ -493,14 +498,25 @@ __global__ void __launch_bounds__(256) bwd_kernel(const __grid_constant__ Params
     const int l = LL.id[li];
     const int64_t n = perm ? (int64_t)__ldg(perm + j) : j;
     const Level lv = slv.get(l);
-    const float4 p = __ldg(coords + n);
+    const float4 p = __ldcs(coords + n);
     Cell c;
     const bool bad = cell_of(lv, p, c);
     if (bad && li == 0) atomicOr(flag, 1);
     float g[F];
     const float *gp = dout + n * (int64_t)(L * F) + l * F;
+    if constexpr (F == 2) {
+        const float2 q = __ldcs(reinterpret_cast<const float2 *>(gp));
+        g[0] = q.x; g[1] = q.y;
+    } else if constexpr (F % 4 == 0) {
 #pragma unroll
-    for (int f = 0; f < F; f++) g[f] = __ldg(gp + f);
+        for (int f = 0; f < F; f += 4) {
+            const float4 q = __ldcs(reinterpret_cast<const float4 *>(gp + f));
+            g[f] = q.x; g[f + 1] = q.y; g[f + 2] = q.z; g[f + 3] = q.w;
+        }
+    } else {
+#pragma unroll
+        for (int f = 0; f < F; f++) g[f] = __ldcs(gp + f);
+    }
     const float wx[2] = {__fsub_rn(1.0f, c.w[0]), c.w[0]}, wy[2] = {__fsub_rn(1.0f, c.w[1]), c.w[1]};
     const float wz[2] = {__fsub_rn(1.0f, c.w[2]), c.w[2]}, wt[2] = {__fsub_rn(1.0f, c.w[3]), c.w[3]};
 #pragma unroll

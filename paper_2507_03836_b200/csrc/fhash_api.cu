@@ -182,8 +182,15 @@ static dim3 grid_for(int64_t N, int L) {
 
 // Split the levels with include[l] into direct-pass lists whose footprint
 // (T_l * bytes_per_entry) fits `limit` bytes (0 = one list), in level order.
+//
+// align (levels per 32-byte sector of an output / dout row, 1 = off): when
+// every level is included, each group boundary is moved down to a multiple
+// of `align` where that leaves the previous group non-empty, so a pass
+// writes (reads) whole sectors of the [N][L*F] rows -- a group ending
+// mid-sector leaves partially written sectors that the L2 must merge with
+// DRAM on eviction.
 static int split_lists(fh_encoder e, const bool *include, double bytes_per_entry, double limit, fh::LevelList *out,
-                       const bool *doubled = nullptr) {
+                       const bool *doubled = nullptr, int align = 1) {
     int n = 0;
     double acc = 0.0;
     for (int l = 0; l < e->L; l++) {
@@ -196,6 +203,21 @@ static int split_lists(fh_encoder e, const bool *include, double bytes_per_entry
         }
         out[n - 1].id[out[n - 1].n++] = l;
         acc += b;
+    }
+    bool all = true;
+    for (int l = 0; l < e->L; l++) all &= include[l];
+    if (align > 1 && all && n > 1) {
+        int start[FH_MAX_LEVELS + 1];
+        for (int g = 0; g < n; g++) start[g] = out[g].id[0];
+        start[n] = e->L;
+        for (int g = 1; g < n; g++) {
+            const int a = start[g] / align * align;
+            if (a > start[g - 1]) start[g] = a;
+        }
+        for (int g = 0; g < n; g++) {
+            out[g].n = 0;
+            for (int l = start[g]; l < start[g + 1]; l++) out[g].id[out[g].n++] = l;
+        }
     }
     return n;
 }
@@ -311,7 +333,8 @@ static void launch_fwd(fh_encoder e, const float *coords, int64_t N, const void 
     // small batches (e.g. the renderer's ray batches) touch few entries: one
     // pass, fewer launches; large batches: L2-sized level groups
     const double limit = N < (1 << 15) ? 0.0 : e->fwd_limit;
-    const int n = split_lists(e, include, (double)F * sizeof(T), limit, lists, sh);
+    const int n = split_lists(e, include, (double)F * sizeof(T), limit, lists, sh,
+                              (int)(32 / (F * sizeof(O))) > 1 ? (int)(32 / (F * sizeof(O))) : 1);
     for (int g = 0; g < n; g++)
         { fh::fwd_kernel<F, T, O><<<grid_for(N, lists[g].n), 256, 0, s>>>(
             prm, c4, N, reinterpret_cast<const T *>(table), tsh, reinterpret_cast<O *>(out), e->flag,
@@ -673,7 +696,7 @@ static fh_status encode_bwd_impl(fh_encoder e, const float *coords, int64_t N, c
         return cuda_check(cudaMemsetAsync(dtable + a * e->F, 0, (b - a) * e->F * 4, s), "fh_encode_bwd: zero dtable");
     };
     if (N == 0) return zero ? zero_levels(0, e->L) : FH_OK;
-    if (!dout || !aligned(dout, 4)) return fail(FH_E_ARG, "fh_encode_bwd: NULL/misaligned dout");
+    if (!dout || !aligned(dout, vec > 16 ? 16 : vec)) return fail(FH_E_ARG, "fh_encode_bwd: NULL/misaligned dout");
     if ((st = ensure_flag(e)) != FH_OK) return st;
     const float4 *c4 = reinterpret_cast<const float4 *>(coords);
     if (e->kind == 1 && perm) return fail(FH_E_ARG, "fh_encode_bwd_ordered: not supported for MHE encoders");

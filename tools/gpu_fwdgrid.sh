@@ -1,5 +1,5 @@
 cd /root/repo
-for cfg in cfg2 pc cfg3; do
-for sh in 1 3; do for mb in 16 24 32 48 69; do
-  echo -n "shift=$sh mb=$mb "; FH_PAIR_SHIFT=$sh FH_FWD_GROUP_MB=$mb python tools/time_encode.py $cfg 20
-done; done; done
+python -m pytest tests/test_parity_gpu.py -x -q 2>&1 | tail -1
+for cfg in cfg2 cfg3 pc cfg4; do for mb in 24 32 40 48 56 69; do
+  echo -n "mb=$mb "; FH_OVERWRITE=1 FH_FWD_GROUP_MB=$mb python tools/time_encode.py $cfg 20
+done; done
