@@ -714,10 +714,11 @@ def run_ours(args, rank, local_rank, world):
     dom_ms = bwd_ms if dom == "bwd" else fwd_ms
     achieved = alg[dom] / (dom_ms / 1e3) / 1e9
     traffic = load_ncu_traffic().get(dom)
-    roofline = {"bound": "hbm", "kernel": f"fh::{dom}_kernel<2>", "achieved": achieved, "peak": hbm_peak,
+    roofline = {"bound": "hbm", "kernel": f"encode {dom} pass (fh::{dom}_kernel<2> level groups"
+                + (" + merge_shift_kernel)" if dom == "bwd" else ")"), "achieved": achieved, "peak": hbm_peak,
                 "unit": "GB/s", "frac": achieved / hbm_peak, "traffic": traffic,
                 "peak_source": peak_src,
-                "algorithmic_bytes_per_launch": alg[dom],
+                "algorithmic_bytes_per_launch": alg[dom], "launch_unit": "one encode pass (all its launches)",
                 "note": "useful gather (or red) payload 16*L*F*4 B + coords 16 B + out/dout L*F*4 B per sample; "
                         "the tables are L2-resident, so the gather roofline below is the binding ceiling"}
     t_roof = mb["t_roof_fwd_ms"] + mb["t_roof_bwd_ms"]
