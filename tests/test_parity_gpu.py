@@ -465,3 +465,84 @@ def test_constant_table_and_multilinear_on_gpu():
     exp = np.prod(coords.astype(np.float64), axis=1)
     assert np.max(np.abs(out[:, 0] - exp)) < 2e-6
     assert np.max(np.abs(out[:, 2] - exp)) < 2e-6
+
+
+def test_concurrent_streams_share_one_encoder():
+    """The shifted-pair scratch is per (encoder, stream): two
+    full-size passes of ONE encoder on two streams at once, different data,
+    each equal to the oracle on its own inputs (sampled rows / adjoint at
+    cfg2 size would not see a scratch race between the streams; an exact
+    check needs oracle-sized inputs, so cfg1h at a batch large enough to use
+    the scratch on every level)."""
+    cfg = W.CFG1H
+    enc = fh.Encoder(cfg.levels, cfg.F, cfg.table_dtype, cfg.cap)
+    ref = oracle.Levels(cfg.levels, cfg.cap)
+    cases = [W.encode_case(cfg, 40000 + k, seed=40 + k) for k in range(2)]
+    streams = [torch.cuda.Stream(), torch.cuda.Stream()]
+    outs, dts = [], []
+    torch.cuda.synchronize()
+    for case, st in zip(cases, streams):
+        with torch.cuda.stream(st):
+            c, t, g = dev(case.coords), dev(case.table), dev(case.dout)
+            o = torch.empty((c.shape[0], enc.L * cfg.F), device="cuda")
+            d = torch.full((enc.entries, cfg.F), 5.0, device="cuda")
+            for _ in range(3):   # repeated passes keep both streams busy together
+                enc.fwd(c, t, o, stream=st)
+                enc.bwd(c, g, d, stream=st, overwrite=True)
+            outs.append(o)
+            dts.append(d)
+    torch.cuda.synchronize()
+    assert enc.status_sync() == fh.FH_OK
+    for case, o, d in zip(cases, outs, dts):
+        r, ab = ref.forward(case.coords, case.table, want_abs=True)
+        check_fwd(o.cpu().numpy().astype(np.float64), r, ab)
+        G, A = ref.backward(case.coords, case.dout, cfg.F, want_abs=True)
+        check_bwd(d.cpu().numpy().astype(np.float64), G, A)
+
+
+def test_kernel_launch_counter():
+    """fh_kernel_launches counts the library's kernels: a cfg1h fwd + bwd
+    issues at least one forward and one backward launch, and nothing is
+    counted for an empty batch."""
+    cfg = W.CFG1H
+    enc = fh.Encoder(cfg.levels, cfg.F, cfg.table_dtype, cfg.cap)
+    case = W.encode_case(cfg, 5000, seed=2)
+    c, t, g = dev(case.coords), dev(case.table), dev(case.dout)
+    d = torch.zeros((enc.entries, cfg.F), device="cuda")
+    n0 = fh.kernel_launches()
+    enc.fwd(c[:0], t, torch.empty((0, enc.L * cfg.F), device="cuda"))
+    enc.bwd(c[:0], g[:0], d)
+    assert fh.kernel_launches() == n0
+    enc.fwd(c, t)
+    n1 = fh.kernel_launches()
+    enc.bwd(c, g, d)
+    n2 = fh.kernel_launches()
+    torch.cuda.synchronize()
+    assert n1 - n0 >= 1 and n2 - n1 >= 1
+
+
+def test_step_host_end_to_end():
+    """fh_encode_step_host (the bench's e2e path): H2D of coords / dout from
+    pinned host buffers, fwd, bwd overwriting a dtable that held garbage,
+    D2H of out and dtable -- host results equal the oracle."""
+    cfg = W.CFG1H
+    enc = fh.Encoder(cfg.levels, cfg.F, cfg.table_dtype, cfg.cap)
+    ref = oracle.Levels(cfg.levels, cfg.cap)
+    case = W.encode_case(cfg, 3000 + 7, seed=9)
+    N, LF = case.coords.shape[0], enc.L * cfg.F
+    coords_h = torch.from_numpy(np.ascontiguousarray(case.coords)).pin_memory()
+    dout_h = torch.from_numpy(np.ascontiguousarray(case.dout)).pin_memory()
+    out_h = torch.empty((N, LF)).pin_memory()
+    dt_h = torch.empty((enc.entries, cfg.F)).pin_memory()
+    table = dev(case.table)
+    cd, gd = torch.empty((N, 4), device="cuda"), torch.empty((N, LF), device="cuda")
+    od = torch.empty((N, LF), device="cuda")
+    dd = torch.full((enc.entries, cfg.F), float("nan"), device="cuda")
+    st = torch.cuda.Stream()
+    enc.step_host(coords_h, dout_h, table, cd, gd, od, dd, out_h, dt_h, st)
+    st.synchronize()
+    assert enc.status_sync(st) == fh.FH_OK
+    r, ab = ref.forward(case.coords, case.table, want_abs=True)
+    check_fwd(out_h.numpy().astype(np.float64), r, ab)
+    G, A = ref.backward(case.coords, case.dout, cfg.F, want_abs=True)
+    check_bwd(dt_h.numpy().astype(np.float64), G, A)
