@@ -138,13 +138,16 @@ class OverlappedShardedDP:
     or tail, see overlap_plan.  Works on CPU tensors too (gloo, no streams),
     which is how the CPU tests exercise the partition."""
 
-    def __init__(self, trainer, group=None):
+    def __init__(self, trainer, group=None, force_collectives: bool = False):
         import torch
         import torch.distributed as dist
         self.tr = trainer
         self.group = group
         self.world = dist.get_world_size(group) if dist.is_initialized() else 1
         self.rank = dist.get_rank(group) if dist.is_initialized() else 0
+        # force_collectives: run the collective path even on a 1-rank group
+        # (tests the stream / event plumbing with NCCL on one GPU)
+        self.force = force_collectives and dist.is_initialized()
         if trainer.shadow_flat is None:
             raise ValueError("sharded DP needs an fp16 table shadow (the replicated state)")
         self.launches = trainer.bwd_launch_ranges()
@@ -200,7 +203,7 @@ class OverlappedShardedDP:
         import torch.distributed as dist
         tr = self.tr
         grads = tr.grads
-        if self.world == 1:
+        if self.world == 1 and not self.force:
             grad_views = [grads[a:a + m] for (_, a, m) in self.mains] + [grads[b:e] for b, e in self.tails]
             tr.apply_ranges(self.ranges, grad_views, stream=stream)
             return

@@ -366,3 +366,45 @@ def test_peer_sharded_dp_single_rank():
         assert ta.status() == fh.FH_OK and torch.isfinite(loss).all()
     finally:
         dist.destroy_process_group()
+
+
+def test_overlapped_dp_nccl_single_rank_collective_path():
+    """dp.OverlappedShardedDP with its collective path forced on a 1-rank
+    NCCL group: reduce-scatters queued on the communication stream behind
+    the backward launches' events, the tails + MLP all-reduce, Adam over the
+    owned ranges and the shadow all-gathers -- bit-identical to the plain
+    step (same gradients; NCCL over one rank is a copy).  Exercises the
+    stream / event plumbing the multi-GPU bench uses."""
+    import os
+    import torch.distributed as dist
+    from paper_2507_03836_b200 import dp
+    os.environ.setdefault("MASTER_ADDR", "127.0.0.1")
+    os.environ["MASTER_PORT"] = "29563"
+    dist.init_process_group("nccl", rank=0, world_size=1, device_id=torch.device("cuda", 0))
+    try:
+        cfg = small_cfg(4, 16, cap=1 << 11)
+        g = W.rng(62)
+        enc = fh.Encoder(cfg.levels, cfg.F, cfg.table_dtype, cfg.cap)
+        table = W.draw_table(g, enc.entries, cfg.F, "f32")
+        layers = W.draw_mlp(g, W.MLPConfig((cfg.L * cfg.F, 64, 64, 1)))
+        coords = W.draw_coords(g, 3000)
+        target = g.random(3000, dtype=np.float32)
+        ta = fh.Trainer(enc, table, layers, 3000)
+        tb = fh.Trainer(enc, table, layers, 3000)
+        odp = dp.OverlappedShardedDP(ta, force_collectives=True)
+        assert odp.force
+        c, t = torch.from_numpy(coords).cuda(), torch.from_numpy(target).cuda()
+        for _ in range(3):
+            ta.fwd_bwd(c, t)
+            tb.grads.copy_(ta.grads)
+            odp.reduce_and_apply()
+            tb.apply()
+            torch.cuda.synchronize()
+            assert torch.equal(ta.table_master, tb.table_master)
+            assert torch.equal(ta.table_shadow, tb.table_shadow)
+            assert torch.equal(ta.mlp_master, tb.mlp_master)
+        loss = odp.step(c, t, 3000)
+        torch.cuda.synchronize()
+        assert ta.status() == fh.FH_OK and torch.isfinite(loss).all()
+    finally:
+        dist.destroy_process_group()
