@@ -145,6 +145,80 @@ def config_block(cfg, N, world):
             "l2": "flushed between timed steps (256 MiB write, outside the step events)"}
 
 
+def cpu_model() -> str:
+    try:
+        with open("/proc/cpuinfo") as f:
+            for line in f:
+                if line.startswith("model name"):
+                    return line.split(":", 1)[1].strip()
+    except OSError:
+        pass
+    return "unknown"
+
+
+_PAR = {}
+
+
+def _par_worker(args):
+    """One process of the all-cores oracle run: forward of its sample range
+    (output discarded) and backward into its own private shared-memory
+    gradient table."""
+    from multiprocessing import shared_memory
+    import numpy as np
+    import oracle
+    k, a, b, shm_name, total, F = args
+    d = _PAR
+    lv = oracle.Levels(d["levels"], d["cap"])
+    lv.forward(d["coords"][a:b], d["t64"])
+    G = lv.backward(d["coords"][a:b], d["dout"][a:b], F)
+    shm = shared_memory.SharedMemory(name=shm_name)
+    dst = np.ndarray((total, F), dtype=np.float64, buffer=shm.buf)
+    dst[:] = G
+    del dst
+    shm.close()
+    return k
+
+
+def cpu_baseline_all_cores(cfg, case_coords, case_table, case_dout, max_procs=16):
+    """the same oracle on all host cores -- the
+    forward split over samples, the backward into per-process private
+    gradient tables summed in a fixed (process) order.  Process-level
+    parallelism around the unmodified oracle (fork + shared memory); capped
+    at max_procs processes (each private table is 100 MB at cfg2)."""
+    import multiprocessing as mp
+    from multiprocessing import shared_memory
+    import numpy as np
+    P = max(1, min(len(os.sched_getaffinity(0)), max_procs))
+    n = len(case_coords)
+    total = int(sum(W_table_sizes(cfg)))
+    _PAR.update(levels=cfg.levels, cap=cfg.cap, coords=case_coords, t64=case_table.astype(np.float64),
+                dout=case_dout)
+    shms = [shared_memory.SharedMemory(create=True, size=total * cfg.F * 8) for _ in range(P)]
+    try:
+        bounds = [(i * n // P, (i + 1) * n // P) for i in range(P)]
+        ctx = mp.get_context("fork")
+        with ctx.Pool(P) as pool:
+            pool.map(_par_worker, [(0, 0, 1, shms[0].name, total, cfg.F)] * P)   # warm the workers
+            t0 = time.perf_counter()
+            pool.map(_par_worker, [(i, a, b, shms[i].name, total, cfg.F) for i, (a, b) in enumerate(bounds)])
+            G = np.zeros((total, cfg.F))
+            for sh in shms:   # fixed merge order
+                G += np.ndarray((total, cfg.F), dtype=np.float64, buffer=sh.buf)
+            dt = time.perf_counter() - t0
+    finally:
+        for sh in shms:
+            sh.close()
+            sh.unlink()
+    return {"value": n / dt, "unit": UNIT, "cores": P, "kind": "oracle", "cpu_model": cpu_model(),
+            "sample": f"all {n} cfg2 points, fwd+bwd, fp64 C oracle in {P} processes (samples split; private "
+                      f"grad tables summed in process order), {dt:.2f} s"}
+
+
+def W_table_sizes(cfg):
+    import workloads as W
+    return W.table_sizes(cfg.levels, cfg.cap)
+
+
 # ------------------------------------------------------------------ ours
 def cpu_baseline(cfg, case_coords, case_table, case_dout):
     import numpy as np
@@ -156,7 +230,7 @@ def cpu_baseline(cfg, case_coords, case_table, case_dout):
     lv.forward(case_coords[:n], t64)
     lv.backward(case_coords[:n], case_dout[:n], cfg.F)
     dt = time.perf_counter() - t0
-    return {"value": n / dt, "unit": UNIT, "cores": 1, "kind": "oracle",
+    return {"value": n / dt, "unit": UNIT, "cores": 1, "kind": "oracle", "cpu_model": cpu_model(),
             "sample": f"all {n} cfg2 points, fwd+bwd over the full tables, fp64 C, 1 thread, "
                       f"{dt:.1f} s"}
 
@@ -729,14 +803,19 @@ def run_ours(args, rank, local_rank, world):
         "fwd_frac": mb["t_roof_fwd_ms"] / fwd_ms, "bwd_frac": mb["t_roof_bwd_ms"] / bwd_ms, **mb,
     }
     cpu = None
+    cpu_all = None
     if world == 1 and not args.no_cpu_baseline:
         cpu = cpu_baseline(cfg, case.coords, case.table, case.dout)
+        try:
+            cpu_all = cpu_baseline_all_cores(cfg, case.coords, case.table, case.dout)
+        except Exception as ex:   # the all-cores run is context; never fail the bench on it
+            cpu_all = {"unavailable": f"{type(ex).__name__}: {ex}"}
     line = {
         "metric": METRIC, "value": value, "unit": UNIT, "n_gpus": world, "steps": K, "warmup": max(args.warmup, 3),
         "ms_per_step": total_s * 1e3 / K, "higher_is_better": True, "scaling": "weak", "vs_baseline": None,
         "dtype": "f32", "data": "synthetic", "config": config_block(cfg, N, world),
         "kernels_ms": {"zero_grad": "inside encode_bwd (FH_BWD_OVERWRITE)", "encode_fwd": fwd_ms, "encode_bwd": bwd_ms, "step": step_ms},
-        "roofline": roofline, "gather_roofline": gather_roofline, "cpu_baseline": cpu, "e2e": e2e,
+        "roofline": roofline, "gather_roofline": gather_roofline, "cpu_baseline": cpu, "cpu_baseline_all_cores": cpu_all, "e2e": e2e,
         "gpu_launches": launches, "clocks": clk.summary(), "train_step": train,
         "paper_encoders": encoders, "coreset": coreset, "hbm_regime": hbm_regime,
     }
