@@ -713,7 +713,7 @@ def run_ours(args, rank, local_rank, world):
     # stream's D2H); every step's copies stay inside the timed region.
     coords_h = torch.from_numpy(case.coords).pin_memory()
     dout_h = torch.from_numpy(case.dout).pin_memory()
-    NS = 3
+    NS = int(os.environ.get("FH_E2E_STREAMS", "3"))   # streams / buffer sets the e2e steps rotate over
     streams = [torch.cuda.Stream() for _ in range(NS)]
     sets = [dict(c=coords, g=dout, o=out, dt=dtable)]
     for _ in range(NS - 1):
