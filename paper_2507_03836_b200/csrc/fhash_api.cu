@@ -183,41 +183,44 @@ static dim3 grid_for(int64_t N, int L) {
 // Split the levels with include[l] into direct-pass lists whose footprint
 // (T_l * bytes_per_entry) fits `limit` bytes (0 = one list), in level order.
 //
-// align (levels per 32-byte sector of an output / dout row, 1 = off): when
-// every level is included, each group boundary is moved down to a multiple
-// of `align` where that leaves the previous group non-empty, so a pass
-// writes (reads) whole sectors of the [N][L*F] rows -- a group ending
-// mid-sector leaves partially written sectors that the L2 must merge with
-// DRAM on eviction.
+// align (levels per 32-byte sector of an output row, 1 = off): when every
+// level is included, a cut that would end a group mid-sector is moved down
+// to the last sector boundary inside the group if the levels it moves still
+// fit the next group's budget, so a pass writes whole sectors of the
+// [N][L*F] rows -- a group ending mid-sector leaves partially written
+// sectors that the L2 must merge with DRAM on eviction.
 static int split_lists(fh_encoder e, const bool *include, double bytes_per_entry, double limit, fh::LevelList *out,
                        const bool *doubled = nullptr, int align = 1) {
+    bool all = true;
+    for (int l = 0; l < e->L; l++) all &= include[l];
+    if (!all) align = 1;
+    double sz[FH_MAX_LEVELS];
+    for (int l = 0; l < e->L; l++)
+        sz[l] = (double)e->info[l].table_size * bytes_per_entry * (doubled && doubled[l] ? 2.0 : 1.0);
     int n = 0;
     double acc = 0.0;
     for (int l = 0; l < e->L; l++) {
         if (!include[l]) continue;
-        const double b = (double)e->info[l].table_size * bytes_per_entry * (doubled && doubled[l] ? 2.0 : 1.0);
-        if (n == 0 || (limit > 0.0 && out[n - 1].n > 0 && acc + b > limit)) {
-            out[n].n = 0;
-            n++;
+        if (n == 0) {
+            out[n++].n = 0;
             acc = 0.0;
+        } else if (limit > 0.0 && out[n - 1].n > 0 && acc + sz[l] > limit) {
+            fh::LevelList &cur = out[n - 1];
+            const int g0 = cur.id[0];
+            const int a = l / align * align;   // last sector boundary at or before l
+            double moved = sz[l];
+            for (int m = a; m < l; m++) moved += sz[m];
+            out[n].n = 0;
+            acc = 0.0;
+            if (align > 1 && a > g0 && a < l && moved <= limit) {
+                for (int m = a; m < l; m++) out[n].id[out[n].n++] = m;
+                cur.n -= l - a;
+                acc = moved - sz[l];
+            }
+            n++;
         }
         out[n - 1].id[out[n - 1].n++] = l;
-        acc += b;
-    }
-    bool all = true;
-    for (int l = 0; l < e->L; l++) all &= include[l];
-    if (align > 1 && all && n > 1) {
-        int start[FH_MAX_LEVELS + 1];
-        for (int g = 0; g < n; g++) start[g] = out[g].id[0];
-        start[n] = e->L;
-        for (int g = 1; g < n; g++) {
-            const int a = start[g] / align * align;
-            if (a > start[g - 1]) start[g] = a;
-        }
-        for (int g = 0; g < n; g++) {
-            out[g].n = 0;
-            for (int l = start[g]; l < start[g + 1]; l++) out[g].id[out[g].n++] = l;
-        }
+        acc += sz[l];
     }
     return n;
 }
