@@ -292,7 +292,10 @@ static void launch_fwd(fh_encoder e, const float *coords, int64_t N, const void 
             sh[l] = (e->fwd_limit <= 0.0 || 4.0 * t * kEb <= e->fwd_limit) && 8.0 * (double)N >= t;
             any |= sh[l];
         }
-        fh_encoder_s::Scratch *sc = any ? get_scratch(e, s, (size_t)e->entries * kEb, 0) : nullptr;
+        uint64_t end = 0;   // the copy only spans up to the last shifted level
+        for (int l = 0; l < e->L; l++)
+            if (sh[l] && e->info[l].offset + e->info[l].table_size > end) end = e->info[l].offset + e->info[l].table_size;
+        fh_encoder_s::Scratch *sc = any ? get_scratch(e, s, (size_t)end * kEb, 0) : nullptr;
         if (sc) {
             // one copy per run of consecutive shifted levels
             for (int l = 0; l < e->L;) {
@@ -745,7 +748,11 @@ static fh_status encode_bwd_impl(fh_encoder e, const float *coords, int64_t N, c
     bool any_shift = false;
     for (int l = 0; l < e->L; l++) any_shift |= e->shiftable[l];
     if (any_shift) {
-        fh_encoder_s::Scratch *sc = get_scratch(e, s, 0, (size_t)e->entries * e->F * 4 + 64);
+        uint64_t end = 0;   // the scratch only spans up to the last shiftable level
+        for (int l = 0; l < e->L; l++)
+            if (e->shiftable[l] && e->info[l].offset + e->info[l].table_size > end)
+                end = e->info[l].offset + e->info[l].table_size;
+        fh_encoder_s::Scratch *sc = get_scratch(e, s, 0, (size_t)end * e->F * 4 + 64);
         if (sc) gsh_buf = sc->gsh;
     }
     for (int k = 0; k < e->n_gb; k++) {
