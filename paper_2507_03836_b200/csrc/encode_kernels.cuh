@@ -480,13 +480,18 @@ __device__ __forceinline__ void red_pair(float *dtable, float *gsh, uint32_t i0,
     red_entry<F>(dtable, i1, v1);
 }
 
-template <int F>
+// RANGED: only corners whose entry lies in [lo, lo + span) are reduced --
+// one of several passes over a level whose gradients exceed the L2 budget,
+// each pass's range staying L2-resident (the index math and dout are
+// repeated per pass, the reductions are not).
+template <int F, bool RANGED = false>
 __global__ void __launch_bounds__(256) bwd_kernel(const __grid_constant__ Params P,
                                                   const float4 *__restrict__ coords, int64_t N,
                                                   const float *__restrict__ dout, float *__restrict__ dtable,
                                                   float *__restrict__ gsh,
                                                   int *__restrict__ flag, const __grid_constant__ LevelList LL,
-                                                  const uint32_t *__restrict__ perm) {
+                                                  const uint32_t *__restrict__ perm, uint32_t lo = 0,
+                                                  uint32_t span = 0) {
     __shared__ LevelSmem slv;
     load_levels(P, slv);
     const int L = P.L;
@@ -526,7 +531,17 @@ __global__ void __launch_bounds__(256) bwd_kernel(const __grid_constant__ Params
         float v0[F], v1[F];
 #pragma unroll
         for (int f = 0; f < F; f++) { v0[f] = W0 * g[f]; v1[f] = W1 * g[f]; }
-        red_pair<F>(dtable, gsh, c.idx[k], c.idx[k + 1], v0, v1);
+        if constexpr (RANGED) {
+            const bool in0 = c.idx[k] - lo < span, in1 = c.idx[k + 1] - lo < span;
+            if (in0 && in1) {
+                red_pair<F>(dtable, gsh, c.idx[k], c.idx[k + 1], v0, v1);
+            } else {
+                if (in0) red_entry<F>(dtable, c.idx[k], v0);
+                if (in1) red_entry<F>(dtable, c.idx[k + 1], v1);
+            }
+        } else {
+            red_pair<F>(dtable, gsh, c.idx[k], c.idx[k + 1], v0, v1);
+        }
     }
 }
 

@@ -69,6 +69,7 @@ static fh_status ensure_flag(fh_encoder e) {
     if (const char *v = getenv("FH_FINE_ORDER")) e->fine_order = atoi(v) == 1;
     if (const char *v = getenv("FH_AGG_MIN_DENSITY")) e->agg_density = atof(v);
     if (const char *v = getenv("FH_PAIR_SHIFT")) e->pair_shift = atoi(v);
+    if (const char *v = getenv("FH_BWD_SPLIT")) e->bwd_split = atoi(v) != 0;
     e->fwd_limit = budget("FH_FWD_GROUP_MB", 0.55);
     // backward: 0.45 L2 (measured with the shifted gradient scratch, whose
     // grads + scratch double a level's footprint: cfg2 bwd 0.737 -> 0.711
@@ -783,6 +784,28 @@ static fh_status encode_bwd_impl(fh_encoder e, const float *coords, int64_t N, c
         if (m0 < 0) m0 = 0;
         if (gsh && (st = cuda_check(cudaMemsetAsync(gsh + m0, 0, (size_t)(m1 - m0) * 4, s), "zero gsh")) != FH_OK)
             return st;
+        // a single level whose gradients exceed the L2 budget: P passes over
+        // entry ranges of it, each L2-resident.  Measured: Combustion fold-2
+        // shape (F = 2, one 95 MB level) bwd 2.24 -> 2.14 ms; cfg4 (F = 4,
+        // 64 MB levels) 6.05 -> 6.34 ms (the repeated index math and dout
+        // reads cost more than the L2 hits gain at 16 B per corner), so F <= 2.
+        const double gbytes = (double)e->info[l0].table_size * e->F * 4.0;
+        if (lc == 1 && !gsh && e->F <= 2 && e->bwd_split && e->bwd_limit > 0.0 && gbytes > e->bwd_limit) {
+            const int P = (int)std::ceil(gbytes / e->bwd_limit);
+            const uint64_t T = e->info[l0].table_size, off = e->info[l0].offset;
+            for (int q = 0; q < P; q++) {
+                const uint64_t a = off + T * q / P, b = off + T * (q + 1) / P;
+                const uint32_t lo = (uint32_t)a, span = (uint32_t)(b - a);
+                switch (e->F) {
+                    case 1: { fh::bwd_kernel<1, true><<<g, 256, 0, s>>>(e->params, c4, N, dout, dtable, nullptr, e->flag, ll, nullptr, lo, span); fh::count_launch(); } break;
+                    case 2: { fh::bwd_kernel<2, true><<<g, 256, 0, s>>>(e->params, c4, N, dout, dtable, nullptr, e->flag, ll, nullptr, lo, span); fh::count_launch(); } break;
+                    case 4: { fh::bwd_kernel<4, true><<<g, 256, 0, s>>>(e->params, c4, N, dout, dtable, nullptr, e->flag, ll, nullptr, lo, span); fh::count_launch(); } break;
+                    default: { fh::bwd_kernel<8, true><<<g, 256, 0, s>>>(e->params, c4, N, dout, dtable, nullptr, e->flag, ll, nullptr, lo, span); fh::count_launch(); } break;
+                }
+            }
+            if (ev && ev0 + k < n_ev) cudaEventRecord(ev[ev0 + k], s);
+            continue;
+        }
         switch (e->F) {
             case 1: { fh::bwd_kernel<1><<<g, 256, 0, s>>>(e->params, c4, N, dout, dtable, gsh, e->flag, ll, nullptr); fh::count_launch(); } break;
             case 2: { fh::bwd_kernel<2><<<g, 256, 0, s>>>(e->params, c4, N, dout, dtable, gsh, e->flag, ll, nullptr); fh::count_launch(); } break;

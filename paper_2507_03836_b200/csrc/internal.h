@@ -85,4 +85,5 @@ struct fh_encoder_s {
     Scratch scratch[kScratchSlots];
     int pair_shift = 3;                              // FH_PAIR_SHIFT bits: 1 backward, 2 forward (default both)
     bool shiftable[FH_MAX_LEVELS] = {false};         // backward: level uses the shifted gradient pairs
+    bool bwd_split = true;                           // FH_BWD_SPLIT=0: no entry-range passes for big levels
 };

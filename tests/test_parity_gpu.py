@@ -546,3 +546,20 @@ def test_step_host_end_to_end():
     check_fwd(out_h.numpy().astype(np.float64), r, ab)
     G, A = ref.backward(case.coords, case.dout, cfg.F, want_abs=True)
     check_bwd(dt_h.numpy().astype(np.float64), G, A)
+
+
+@pytest.mark.parametrize("split", ["0", "1"])
+def test_backward_entry_range_passes(split, monkeypatch):
+    """A level whose gradients exceed the backward group budget is reduced
+    in entry-range passes (FH_BWD_SPLIT, default on for F <= 2): forced with
+    a tiny budget (FH_BWD_GROUP_MB) on cfg1h, results equal the oracle."""
+    monkeypatch.setenv("FH_BWD_SPLIT", split)
+    monkeypatch.setenv("FH_BWD_GROUP_MB", "0.02")   # 20 KB: every level alone, the big ones split
+    cfg = W.CFG1H
+    case = W.encode_case(cfg, 6000 + 3, seed=17)
+    enc = fh.Encoder(cfg.levels, cfg.F, cfg.table_dtype, cfg.cap)
+    ref = oracle.Levels(cfg.levels, cfg.cap)
+    got, st = run_bwd(enc, case)
+    assert st == fh.FH_OK
+    G, A = ref.backward(case.coords, case.dout, cfg.F, want_abs=True)
+    check_bwd(got, G, A)
