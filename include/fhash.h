@@ -155,8 +155,16 @@ void      fh_encoder_destroy(fh_encoder enc);
  *   table; out = quadrilinear blend, trilinear per time slice (Eqs. 10-11)
  *   then linear in t (Eq. 12, R6).
  * coords [N][4] f32 (device); table [sum T][F] of the encoder's table_dtype
- * (device, 32-byte aligned: corners are fetched as 32-byte blocks); out [N][L*F] of out_dtype FH_F32 or FH_BF16
- * (device), row n = (level 0 features, level 1 features, ...).
+ * (device, 32-byte aligned: x-pairs of corners are fetched as aligned
+ * 2-entry chunks); out [N][L*F] of out_dtype FH_F32 or FH_BF16 (device),
+ * row n = (level 0 features, level 1 features, ...).
+ * Scratch: large passes use encoder-owned scratch of the calling stream
+ * (the table shifted by one entry, and in fh_encode_bwd a
+ * shifted gradient scratch), allocated on the stream's first large pass
+ * (never while the stream is capturing a graph: such a pass runs without
+ * it).  Calls of one encoder are therefore safe concurrently on different
+ * streams; a graph captured on stream s reuses s's scratch, so do not
+ * replay it concurrently with other passes of the same encoder on s.
  * N = 0 is a no-op.  Errors: FH_E_ARG (NULL/misaligned, dtype), FH_E_CUDA. */
 fh_status fh_encode_fwd(fh_encoder enc, const float *coords, int64_t N, const void *table,
                         void *out, fh_dtype out_dtype, fh_stream stream);
