@@ -84,6 +84,9 @@ def test_table3_param_count_through_abi():
     (dict(levels=[(4, 4, 4, 2)], F=2, cap=1000), fh.FH_E_ARG),
     (dict(levels=[(4, 4, 4, 2)] * 33, F=2), fh.FH_E_ARG),
     (dict(levels=[(4096, 4096, 4096, 16)], F=2), fh.FH_E_RANGE),
+    (dict(levels=[(1024, 1024, 1024, 2)], F=2), fh.FH_E_RANGE),             # sum T F = 2^32 exactly
+    (dict(levels=[(1024, 1024, 1023, 2), (128, 128, 128, 2)], F=2), fh.FH_E_RANGE),   # crosses 2^32 at level 1
+    (dict(levels=[(4, 4, 4, 2)], F=2, cap=1 << 32), fh.FH_E_RANGE),           # cap above 2^31
     (dict(levels=[(1 << 25, 2, 2, 2)], F=1), fh.FH_E_ARG),
 ])
 def test_build_levels_errors(kw, status):

@@ -563,3 +563,44 @@ def test_backward_entry_range_passes(split, monkeypatch):
     assert st == fh.FH_OK
     G, A = ref.backward(case.coords, case.dout, cfg.F, want_abs=True)
     check_bwd(got, G, A)
+
+
+@pytest.mark.parametrize("levels,cap,F", [([(1024, 1024, 1023, 2), (4, 4, 4, 2)], 0, 2),
+                                          ([(2048, 2048, 1024, 2), (5, 3, 4, 2)], 1 << 31, 1)],
+                         ids=["eq9-2^31-entries", "hash-cap-2^31"])
+def test_maximum_table_size(levels, cap, F):
+    """Maximum sizes (sum T_l * F just below 2^32, the uint32 index range of
+    the ABI): a bijective level of 2^31 - 2^21 entries at F = 2, and a level
+    capped at 2^31 (R5 hash) at F = 1, each followed by a small level whose
+    offset is near the top of the range.  Indices bit-exact against the
+    oracle; partition of unity (constant table -> output 1); backward by the
+    adjoint identity <g, fwd(t)> = <bwd(g), t> (the oracle cannot hold the
+    17 GB tables in fp64)."""
+    enc = fh.Encoder(levels, F, "f32", cap)
+    ref = oracle.Levels(levels, cap)
+    assert enc.entries == ref.total and enc.entries * F < (1 << 32)
+    g = W.rng(77)
+    coords = np.concatenate([W.draw_coords(g, 4000), W.edge_coords()]).astype(np.float32)
+    c = dev(coords)
+    idx, _ = enc.indices(c)
+    assert enc.status_sync() == fh.FH_OK
+    assert np.array_equal(idx.cpu().numpy().view(np.uint32), ref.indices(coords, want_w=False)[0])
+    gen = torch.Generator("cuda").manual_seed(5)
+    table = torch.ones((enc.entries, F), device="cuda")
+    out = enc.fwd(c, table)
+    assert torch.allclose(out, torch.ones_like(out), rtol=0, atol=1e-6)
+    table.uniform_(-1.0, 1.0, generator=gen)
+    out = enc.fwd(c, table)
+    dout = torch.randn(out.shape, device="cuda", generator=gen)
+    dt = torch.zeros_like(table)
+    enc.bwd(c, dout, dt)
+    assert enc.status_sync() == fh.FH_OK
+    lhs = torch.sum(dout.double() * out.double()).item()
+    rhs = 0.0
+    step = 1 << 26
+    for a in range(0, enc.entries, step):
+        rhs += torch.sum(dt[a:a + step].double() * table[a:a + step].double()).item()
+    scale = torch.sum(dout.abs().double()).item()
+    assert abs(lhs - rhs) <= 1e-5 * scale, (lhs, rhs, scale)
+    del table, dt
+    torch.cuda.empty_cache()
