@@ -574,9 +574,11 @@ __global__ void __launch_bounds__(256) merge_shift_kernel(float *__restrict__ dt
 // ------------------------------------------------------------ small levels
 // The fold schedule (Eqs. 4-8) ends in tiny levels (down to 2x2x2x2 = 16
 // entries) that receive ~16 N contributions: global reductions to the same
-// few addresses serialise in the L2 atomic units.  Levels whose grads fit in
-// shared memory are instead accumulated per CTA in shared memory (CTA-private
-// copies) and flushed with one global reduction per entry per CTA.
+// few addresses serialise in the L2 atomic units.  These levels are
+// accumulated per CTA in shared memory instead (CTA-private copies; the
+// shared-memory fp32 atomics are CAS loops on sm_100a), the tiniest (<= 64
+// floats) in one private copy per LANE updated with plain read-add-write,
+// and flushed with one global reduction per entry per CTA.
 template <int F>
 __global__ void __launch_bounds__(256) bwd_small_kernel(const __grid_constant__ Params P,
                                                         const __grid_constant__ SmallSet S,
@@ -586,7 +588,10 @@ __global__ void __launch_bounds__(256) bwd_small_kernel(const __grid_constant__ 
     extern __shared__ float acc[];
     __shared__ LevelSmem slv;
     load_levels(P, slv);
-    for (int i = threadIdx.x; i < S.total; i += blockDim.x) acc[i] = 0.f;
+    // lane-private blocks of the tiny levels: [warp][slot][lane] after acc
+    const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+    float *lp = acc + S.total + warp * S.ttotal * 32 + lane;
+    for (int i = threadIdx.x; i < S.total + (int)(blockDim.x >> 5) * S.ttotal * 32; i += blockDim.x) acc[i] = 0.f;
     __syncthreads();
     const int L = P.L;
     const int64_t items = N * S.n;
@@ -604,6 +609,22 @@ __global__ void __launch_bounds__(256) bwd_small_kernel(const __grid_constant__ 
         for (int f = 0; f < F; f++) g[f] = __ldg(dout + n * (int64_t)(L * F) + l * F + f);
         const float wx[2] = {__fsub_rn(1.0f, c.w[0]), c.w[0]}, wy[2] = {__fsub_rn(1.0f, c.w[1]), c.w[1]};
         const float wz[2] = {__fsub_rn(1.0f, c.w[2]), c.w[2]}, wt[2] = {__fsub_rn(1.0f, c.w[3]), c.w[3]};
+        if (S.toff[li] >= 0) {
+            // tiny level: every lane owns a private copy (column `lane` of its
+            // warp's block, conflict-free): plain read-add-write, no atomics
+            float *t = lp + (S.toff[li] - (int)lv.offset * F) * 32;
+#pragma unroll
+            for (int k = 0; k < 16; k += 2) {
+                const float Wyzt = wy[(k >> 1) & 1] * wz[(k >> 2) & 1] * wt[(k >> 3) & 1];
+                const float W0 = wx[0] * Wyzt, W1 = wx[1] * Wyzt;
+#pragma unroll
+                for (int f = 0; f < F; f++) {
+                    t[(c.idx[k] * F + f) * 32] += W0 * g[f];
+                    t[(c.idx[k + 1] * F + f) * 32] += W1 * g[f];
+                }
+            }
+            continue;
+        }
         float *a = acc + S.soff[li] - (int)lv.offset * F;
 #pragma unroll
         for (int k = 0; k < 16; k += 2) {
@@ -614,6 +635,17 @@ __global__ void __launch_bounds__(256) bwd_small_kernel(const __grid_constant__ 
                 atomicAdd(a + c.idx[k] * F + f, W0 * g[f]);
                 atomicAdd(a + c.idx[k + 1] * F + f, W1 * g[f]);
             }
+        }
+    }
+    __syncwarp();
+    // fold the lane-private blocks into the CTA copy: lane l sums slot s over
+    // the warp's 32 lanes (rotated start: conflict-free), then one CTA atomic
+    if (S.ttotal > 0) {
+        const float *wb = acc + S.total + warp * S.ttotal * 32;
+        for (int slot = lane; slot < S.ttotal; slot += 32) {
+            float v = 0.f;
+            for (int m = 0; m < 32; m++) v += wb[slot * 32 + ((m + lane) & 31)];
+            if (v != 0.f) atomicAdd(acc + S.tmap[slot], v);
         }
     }
     __syncthreads();

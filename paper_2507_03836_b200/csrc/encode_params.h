@@ -31,7 +31,14 @@ struct SmallSet {
     int id[kMaxLevels];       // level ids
     int soff[kMaxLevels];     // float offset of each level's block in shared memory
     int total;                // floats in shared memory
+    // tiny levels (T_l F <= 64, e.g. the 2x2x2x2 end of a fold schedule):
+    // lane-private accumulators, toff[i] = float offset of small level i in
+    // every lane's private block (-1: not tiny); ttotal floats per lane
+    int toff[kMaxLevels];
+    int ttotal;
+    int tmap[96];             // tiny slot -> float offset of the same element in the CTA block
 };
+constexpr int kMaxTinyFloats = 96;
 
 // A set of levels one direct encode launch processes (thread = (sample,
 // list entry), list entry fastest).

@@ -76,13 +76,21 @@ static fh_status ensure_flag(fh_encoder e) {
     // ms, cfg3 0.248 -> 0.231 ms; cfg4's 64 MiB levels group alike)
     e->bwd_limit = budget("FH_BWD_GROUP_MB", 0.45);
     make_groups(e->fwd_limit, (size_t)e->F * dtype_size(e->table_dtype), e->gf, e->n_gf);
-    // Backward: levels whose fp32 grads fit a shared-memory budget are
-    // privatised per CTA (bwd_small_kernel), smallest first; the others form
-    // contiguous runs split by the L2 budget.
+    // Backward: the coarse, contended levels (at most FH_SMALL_MAX_T = 2048
+    // entries: the few-cell end of a fold schedule) are privatised in shared
+    // memory (bwd_small_kernel: one copy per CTA, lane-private copies for the
+    // tiniest), smallest first, within 96 KB; the others form contiguous runs
+    // split by the L2 budget.  Measured on the Combustion fold-2 shape: its
+    // 728-entry level is faster privatised, its 4900-entry level faster
+    // through the L2 reductions (bwd 1.79 -> 1.28 ms moving it out); copies
+    // per warp instead of per CTA were slower (1.80 ms: twice the shared
+    // memory, one CTA per SM).
     {
         const double lim = e->bwd_limit;
         const char *sv = getenv("FH_SMALL_KB");
-        const int per_level_max = 48 * 1024, total_max = sv ? atoi(sv) * 1024 : 96 * 1024;
+        const char *tv = getenv("FH_SMALL_MAX_T");
+        const uint64_t max_t = tv ? (uint64_t)atoll(tv) : 2048;
+        const int per_level_max = 1 << 30, total_max = sv ? atoi(sv) * 1024 : 96 * 1024;
         bool small[FH_MAX_LEVELS] = {false};
         int order[FH_MAX_LEVELS];
         for (int l = 0; l < e->L; l++) order[l] = l;
@@ -95,17 +103,29 @@ static fh_status ensure_flag(fh_encoder e) {
         for (int a = 0; a < e->L && e->kind == 0; a++) {
             const int l = order[a];
             const uint64_t bytes = e->info[l].table_size * (uint64_t)e->F * 4;
-            if (bytes > (uint64_t)per_level_max || used + (int)bytes > total_max) break;
+            if (e->info[l].table_size > max_t || bytes > (uint64_t)per_level_max || used + (int)bytes > total_max) break;
             small[l] = true;
             used += (int)bytes;
         }
         e->small.n = 0;
         e->small.total = 0;
+        e->small.ttotal = 0;
+        const bool tiny_on = !getenv("FH_TINY") || atoi(getenv("FH_TINY")) != 0;
         for (int l = 0; l < e->L; l++)
             if (small[l]) {
-                e->small.id[e->small.n] = l;
-                e->small.soff[e->small.n] = e->small.total;
-                e->small.total += (int)(e->info[l].table_size * (uint64_t)e->F);
+                const int tf = (int)(e->info[l].table_size * (uint64_t)e->F);
+                const int i = e->small.n;
+                e->small.id[i] = l;
+                e->small.soff[i] = e->small.total;
+                e->small.toff[i] = -1;
+                // tiny: lane-private accumulation (bwd_small_kernel); 8 warps x
+                // 96 floats x 32 lanes = 96 KB of shared memory at most
+                if (tiny_on && tf <= 64 && e->small.ttotal + tf <= fh::kMaxTinyFloats) {
+                    e->small.toff[i] = e->small.ttotal;
+                    for (int q = 0; q < tf; q++) e->small.tmap[e->small.ttotal + q] = e->small.total + q;
+                    e->small.ttotal += tf;
+                }
+                e->small.total += tf;
                 e->small.n++;
             }
         // shifted gradient pairs for the levels whose grads
@@ -721,9 +741,11 @@ static fh_status encode_bwd_impl(fh_encoder e, const float *coords, int64_t N, c
         if (zero)
             for (int j = 0; j < e->small.n; j++)
                 if ((st = zero_levels(e->small.id[j], e->small.id[j] + 1)) != FH_OK) return st;
-        const int smem = e->small.total * 4;
+        const int smem = (e->small.total + 8 * e->small.ttotal * 32) * 4;   // CTA block + lane-private blocks
         int64_t blocks = (N * e->small.n + 255) / 256;
-        if (blocks > 2 * 148) blocks = 2 * 148;
+        const int per_sm = smem > 0 ? (e->smem_optin > 0 ? e->smem_optin : 232448) / (smem + 2048) : 2;
+        const int64_t cap = (int64_t)e->n_sm * (per_sm < 1 ? 1 : per_sm > 2 ? 2 : per_sm);
+        if (blocks > cap) blocks = cap;
         const dim3 g((unsigned)blocks);
         fh_status q = FH_OK;
         switch (e->F) {
