@@ -445,6 +445,17 @@ size_t    fh_level_stats_workspace_size(fh_encoder enc, int level);
 fh_status fh_level_stats(fh_encoder enc, int level, void *workspace, size_t workspace_bytes, uint64_t *out,
                          fh_stream stream);
 
+/* fh_encoder_scratch_size / fh_encoder_attach_scratch -- caller-owned
+ * shifted-pair scratch (see fh_encode_fwd).  By default the encoder
+ * allocates it itself per stream on the first large pass; a caller that
+ * owns all device memory instead attaches fh_encoder_scratch_size(enc)
+ * bytes (device, 256-byte aligned, covers every pass of this encoder) for
+ * `stream`.  The library never grows or frees attached memory; ptr = NULL
+ * detaches (after synchronising `stream`).  0 / FH_E_ARG for MHE encoders;
+ * FH_E_STATE if all 8 stream slots are taken. */
+size_t    fh_encoder_scratch_size(fh_encoder enc);
+fh_status fh_encoder_attach_scratch(fh_encoder enc, fh_stream stream, void *ptr, size_t bytes);
+
 /* fh_kernel_launches -- number of CUDA kernels this library has launched
  * so far (all threads, all encoders / trainers; the method's kernels, not
  * the fhash_bench.h / fhash_data.h harness kernels, not memset / memcpy).

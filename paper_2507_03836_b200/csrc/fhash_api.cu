@@ -172,6 +172,7 @@ static fh_encoder_s::Scratch *get_scratch(fh_encoder e, cudaStream_t s, size_t t
             if (!sc.tsh && !sc.gsh) { slot = &sc; break; }
     if (!slot) return nullptr;
     const bool need_t = tsh_bytes > slot->tsh_bytes, need_g = gsh_bytes > slot->gsh_bytes;
+    if ((need_t || need_g) && slot->caller) return nullptr;   // caller-owned scratch is never grown
     if (need_t || need_g) {
         cudaStreamCaptureStatus cs = cudaStreamCaptureStatusNone;
         if (cudaStreamIsCapturing(s, &cs) != cudaSuccess || cs != cudaStreamCaptureStatusNone) return nullptr;
@@ -590,6 +591,7 @@ void fh_encoder_destroy(fh_encoder e) {
         if (cur != e->device) cudaSetDevice(e->device);
         cudaFree(e->flag);
         for (auto &sc : e->scratch) {
+            if (sc.caller) continue;
             if (sc.tsh) cudaFree(sc.tsh);
             if (sc.gsh) cudaFree(sc.gsh);
         }
@@ -652,6 +654,58 @@ fh_status fh_build_mhe(const uint32_t *res, int L, int F, fh_dtype table_dtype, 
 int fh_encoder_kind(fh_encoder e) { return e ? e->kind : -1; }
 
 unsigned long long fh_kernel_launches(void) { return fh::g_launches.load(std::memory_order_relaxed); }
+
+static size_t scratch_parts(fh_encoder e, size_t *tsh_bytes, size_t *gsh_bytes) {
+    const size_t t = (size_t)e->entries * e->F * dtype_size(e->table_dtype);
+    const size_t g = e->F <= 2 ? (size_t)e->entries * e->F * 4 + 64 : 0;
+    const size_t ta = (t + 255) / 256 * 256;
+    if (tsh_bytes) *tsh_bytes = ta;
+    if (gsh_bytes) *gsh_bytes = g;
+    return ta + g;
+}
+
+size_t fh_encoder_scratch_size(fh_encoder e) {
+    if (!e || e->kind != 0) return 0;
+    return scratch_parts(e, nullptr, nullptr);
+}
+
+fh_status fh_encoder_attach_scratch(fh_encoder e, fh_stream stream, void *ptr, size_t bytes) {
+    g_err[0] = 0;
+    if (!e) return fail(FH_E_ARG, "fh_encoder_attach_scratch: NULL encoder");
+    if (e->kind != 0) return fail(FH_E_ARG, "fh_encoder_attach_scratch: MHE encoders use no scratch");
+    fh_status st = ensure_flag(e);
+    if (st != FH_OK) return st;
+    void *s = stream;
+    fh_encoder_s::Scratch *slot = nullptr;
+    for (auto &sc : e->scratch)
+        if (sc.stream == s && (sc.tsh || sc.gsh)) { slot = &sc; break; }
+    if (slot) {   // detach / replace: stream-ordered with earlier passes on this stream
+        if ((st = cuda_check(cudaStreamSynchronize(reinterpret_cast<cudaStream_t>(stream)), "attach_scratch sync")) != FH_OK)
+            return st;
+        if (!slot->caller) {
+            if (slot->tsh) cudaFree(slot->tsh);
+            if (slot->gsh) cudaFree(slot->gsh);
+        }
+        *slot = fh_encoder_s::Scratch{};
+    }
+    if (!ptr) return FH_OK;   // detached: the library allocates again on demand
+    size_t tb, gb;
+    const size_t need = scratch_parts(e, &tb, &gb);
+    if (bytes < need || !aligned(ptr, 256))
+        return fail(FH_E_ARG, "fh_encoder_attach_scratch: need %zu bytes, 256-byte aligned", need);
+    if (!slot)
+        for (auto &sc : e->scratch)
+            if (!sc.tsh && !sc.gsh) { slot = &sc; break; }
+    if (!slot) return fail(FH_E_STATE, "fh_encoder_attach_scratch: all %d stream slots in use", fh_encoder_s::kScratchSlots);
+    slot->stream = s;
+    slot->caller = true;
+    slot->tsh = ptr;
+    slot->tsh_bytes = tb;
+    slot->gsh = gb ? reinterpret_cast<float *>(reinterpret_cast<char *>(ptr) + tb) : nullptr;
+    slot->gsh_bytes = gb;
+    if (!slot->gsh) slot->gsh_bytes = 0;
+    return FH_OK;
+}
 
 }  // extern "C"
 

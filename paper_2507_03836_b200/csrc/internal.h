@@ -80,6 +80,7 @@ struct fh_encoder_s {
         size_t tsh_bytes = 0;
         float *gsh = nullptr;
         size_t gsh_bytes = 0;
+        bool caller = false;   // attached by fh_encoder_attach_scratch: caller-owned, never grown or freed
     };
     static constexpr int kScratchSlots = 8;
     Scratch scratch[kScratchSlots];

@@ -35,7 +35,7 @@ EXPORTS = [
     "fh_mlp_param_count", "fh_train_workspace_size", "fh_trainer_create", "fh_train_fwd_bwd", "fh_train_apply",
     "fh_train_step", "fh_trainer_status", "fh_trainer_step_count", "fh_trainer_destroy", "fh_train_apply_sharded",
     "fh_train_bwd_launches", "fh_train_bwd_ranges", "fh_train_set_bwd_events", "fh_train_apply_ranges",
-    "fh_train_apply_peers", "fh_level_stats_workspace_size", "fh_level_stats", "fh_kernel_launches",
+    "fh_train_apply_peers", "fh_level_stats_workspace_size", "fh_level_stats", "fh_kernel_launches", "fh_encoder_scratch_size", "fh_encoder_attach_scratch",
     # inference (renderer's model evaluation) and the ARM pace rule
     "fh_infer_workspace_size", "fh_infer", "fh_arm_pace",
     # include/fhash_coreset.h (NEXT-4 coreset selection)
@@ -103,6 +103,10 @@ def lib() -> ctypes.CDLL:
     L.fh_level_stats.restype = c_int
     L.fh_kernel_launches.argtypes = []
     L.fh_kernel_launches.restype = ctypes.c_ulonglong
+    L.fh_encoder_scratch_size.argtypes = [vp]
+    L.fh_encoder_scratch_size.restype = ctypes.c_size_t
+    L.fh_encoder_attach_scratch.argtypes = [vp, vp, vp, ctypes.c_size_t]
+    L.fh_encoder_attach_scratch.restype = c_int
     L.fh_spatial_sort_workspace_size.argtypes = [i64]
     L.fh_spatial_sort_workspace_size.restype = ctypes.c_size_t
     L.fh_spatial_sort.argtypes = [vp, vp, i64, vp, vp, ctypes.c_size_t, vp]
@@ -254,6 +258,18 @@ class Encoder:
         else:
             C, T = info["corners"], info["table_size"]
         return d, C - d, d / T
+
+    def scratch_size(self) -> int:
+        return int(lib().fh_encoder_scratch_size(self._h))
+
+    def attach_scratch(self, buf, stream=None):
+        """Use caller-owned device memory (>= scratch_size() bytes) as the
+        shifted-pair scratch of `stream`; buf=None detaches."""
+        if buf is None:
+            _check(lib().fh_encoder_attach_scratch(self._h, _stream(stream), None, 0))
+        else:
+            _check(lib().fh_encoder_attach_scratch(self._h, _stream(stream), _ptr(buf),
+                                                   buf.numel() * buf.element_size()))
 
     def sort_bits(self):
         """(bits per axis [4], axis of each of the 16 key bits, LSB first)."""

@@ -604,3 +604,36 @@ def test_maximum_table_size(levels, cap, F):
     assert abs(lhs - rhs) <= 1e-5 * scale, (lhs, rhs, scale)
     del table, dt
     torch.cuda.empty_cache()
+
+
+def test_caller_owned_scratch():
+    """fh_encoder_attach_scratch: the shifted-pair scratch in caller-owned
+    memory (the caller owns every device buffer); results
+    equal the oracle; detach works; MHE encoders refuse."""
+    cfg = W.CFG1H
+    enc = fh.Encoder(cfg.levels, cfg.F, cfg.table_dtype, cfg.cap)
+    ref = oracle.Levels(cfg.levels, cfg.cap)
+    n = enc.scratch_size()
+    assert n >= enc.entries * cfg.F * 4
+    buf = torch.empty(n, dtype=torch.uint8, device="cuda")
+    st = torch.cuda.Stream()
+    enc.attach_scratch(buf, st)
+    case = W.encode_case(cfg, 20000, seed=23)
+    with torch.cuda.stream(st):
+        c, t, g = dev(case.coords), dev(case.table), dev(case.dout)
+        out = enc.fwd(c, t, stream=st)
+        d = torch.full((enc.entries, cfg.F), 3.0, device="cuda")
+        enc.bwd(c, g, d, stream=st, overwrite=True)
+    st.synchronize()
+    assert enc.status_sync(st) == fh.FH_OK
+    r, ab = ref.forward(case.coords, case.table, want_abs=True)
+    check_fwd(out.cpu().numpy().astype(np.float64), r, ab)
+    G, A = ref.backward(case.coords, case.dout, cfg.F, want_abs=True)
+    check_bwd(d.cpu().numpy().astype(np.float64), G, A)
+    enc.attach_scratch(None, st)
+    with pytest.raises(fh.FHashError):
+        enc.attach_scratch(buf[: n // 2], st)          # too small
+    mhe = fh.MHEEncoder([8, 16], 2, 1 << 10, 2, "f32")
+    assert mhe.scratch_size() == 0
+    with pytest.raises(fh.FHashError):
+        mhe.attach_scratch(buf, st)
