@@ -159,6 +159,42 @@ __global__ void __launch_bounds__(kThreads) feature_kernel(const float *__restri
     const uint32_t rows = (uint32_t)d.n * d.Z * d.Y;   // < 2^32 (make_dims)
     const int lane = threadIdx.x & 31;
     const uint32_t G = (gridDim.x * kThreads) >> 5;   // warps in the grid
+    if (s.kind != FH_FEAT_ISOSURFACE && (d.X & 127u) == 0 && (reinterpret_cast<uintptr_t>(vol) & 15u) == 0) {
+        // rows of whole 128-vertex groups: the (row, group) units of the
+        // volume flattened, kUnits per warp in flight (memory-level
+        // parallelism: one unit is only 512 B per warp)
+        constexpr int kUnits = 4;
+        const uint32_t groups = d.X / 128;
+        const uint64_t units = (uint64_t)rows * groups;
+        const float4 *v4 = reinterpret_cast<const float4 *>(vol);
+        const uint64_t warp0 = (blockIdx.x * kThreads + threadIdx.x) >> 5;
+        for (uint64_t u0 = warp0 * kUnits; u0 < units; u0 += (uint64_t)G * kUnits) {
+            float4 v[kUnits];
+#pragma unroll
+            for (int u = 0; u < kUnits; u++)
+                v[u] = u0 + u < units ? __ldcs(v4 + (u0 + u) * 32 + lane) : make_float4(0.f, 0.f, 0.f, 0.f);
+#pragma unroll
+            for (int u = 0; u < kUnits; u++) {
+                if (u0 + u >= units) break;   // warp-uniform
+                const uint32_t b0 = __ballot_sync(0xffffffffu, feature_test(v[u].x, s));
+                const uint32_t b1 = __ballot_sync(0xffffffffu, feature_test(v[u].y, s));
+                const uint32_t b2 = __ballot_sync(0xffffffffu, feature_test(v[u].z, s));
+                const uint32_t b3 = __ballot_sync(0xffffffffu, feature_test(v[u].w, s));
+                if (lane < 4) {
+                    auto spread = [](uint32_t x) {   // bit i -> bit 4 i (i < 8)
+                        x = (x | (x << 12)) & 0x000F000Fu;
+                        x = (x | (x << 6)) & 0x03030303u;
+                        return (x | (x << 3)) & 0x11111111u;
+                    };
+                    const uint32_t sh = 8u * lane;
+                    // unit (row, q) -> words 4 q .. 4 q + 3 of the row; rows hold Wx = 4 groups words
+                    f[(u0 + u) * 4 + lane] = spread((b0 >> sh) & 0xFFu) | (spread((b1 >> sh) & 0xFFu) << 1) |
+                                             (spread((b2 >> sh) & 0xFFu) << 2) | (spread((b3 >> sh) & 0xFFu) << 3);
+                }
+            }
+        }
+        return;
+    }
     for (uint32_t row = (blockIdx.x * kThreads + threadIdx.x) >> 5; row < rows; row += G) {
         const float *r = vol + (uint64_t)row * d.X;   // rows of [n][Z][Y][X] are contiguous
         uint32_t *frow = f + (uint64_t)row * d.Wx;
