@@ -36,9 +36,10 @@ struct SmallSet {
     // every lane's private block (-1: not tiny); ttotal floats per lane
     int toff[kMaxLevels];
     int ttotal;
-    int tmap[96];             // tiny slot -> float offset of the same element in the CTA block
+    int tmap[320];            // tiny slot -> float offset of the same element in the CTA block
 };
-constexpr int kMaxTinyFloats = 96;
+constexpr int kMaxTinyFloats = 320;   // lane-private floats per lane (all tiny levels together)
+constexpr int kMaxTinyLevel = 256;    // a level of at most this many floats (T_l F) is tiny
 
 // A set of levels one direct encode launch processes (thread = (sample,
 // list entry), list entry fastest).

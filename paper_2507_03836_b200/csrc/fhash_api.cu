@@ -118,9 +118,9 @@ static fh_status ensure_flag(fh_encoder e) {
                 e->small.id[i] = l;
                 e->small.soff[i] = e->small.total;
                 e->small.toff[i] = -1;
-                // tiny: lane-private accumulation (bwd_small_kernel); 8 warps x
-                // 96 floats x 32 lanes = 96 KB of shared memory at most
-                if (tiny_on && tf <= 64 && e->small.ttotal + tf <= fh::kMaxTinyFloats) {
+                // tiny: lane-private accumulation (bwd_small_kernel, its own
+                // launch sized so every lane's copy fits shared memory)
+                if (tiny_on && tf <= fh::kMaxTinyLevel && e->small.ttotal + tf <= fh::kMaxTinyFloats) {
                     e->small.toff[i] = e->small.ttotal;
                     for (int q = 0; q < tf; q++) e->small.tmap[e->small.ttotal + q] = e->small.total + q;
                     e->small.ttotal += tf;
@@ -128,6 +128,26 @@ static fh_status ensure_flag(fh_encoder e) {
                 e->small.total += tf;
                 e->small.n++;
             }
+        // the launches: CTA copies (non-tiny levels), then one lane-private
+        // launch per tiny level (each lane's copy is then only that level,
+        // so more warps fit per SM: 2x2x2x2 -> ~55 warps, 7x4x2x2 -> ~8)
+        e->small_cta = fh::SmallSet{};
+        e->n_tiny = 0;
+        for (int i = 0; i < e->small.n; i++) {
+            const int l = e->small.id[i];
+            const int tf = (int)(e->info[l].table_size * (uint64_t)e->F);
+            if (e->small.toff[i] >= 0) e->small_tiny[e->n_tiny++] = fh::SmallSet{};
+            fh::SmallSet &D = e->small.toff[i] >= 0 ? e->small_tiny[e->n_tiny - 1] : e->small_cta;
+            D.id[D.n] = l;
+            D.soff[D.n] = D.total;
+            D.toff[D.n] = e->small.toff[i] >= 0 ? D.total : -1;
+            if (e->small.toff[i] >= 0) {
+                for (int q = 0; q < tf; q++) D.tmap[D.total + q] = D.total + q;
+                D.ttotal += tf;
+            }
+            D.total += tf;
+            D.n++;
+        }
         // shifted gradient pairs for the levels whose grads
         // plus scratch stay within the L2 budget; a level beyond it runs in a
         // pass of its own from HBM, where the merge would cost more than the
@@ -795,25 +815,39 @@ static fh_status encode_bwd_impl(fh_encoder e, const float *coords, int64_t N, c
         if (zero)
             for (int j = 0; j < e->small.n; j++)
                 if ((st = zero_levels(e->small.id[j], e->small.id[j] + 1)) != FH_OK) return st;
-        const int smem = (e->small.total + 8 * e->small.ttotal * 32) * 4;   // CTA block + lane-private blocks
-        int64_t blocks = (N * e->small.n + 255) / 256;
-        const int per_sm = smem > 0 ? (e->smem_optin > 0 ? e->smem_optin : 232448) / (smem + 2048) : 2;
-        const int64_t cap = (int64_t)e->n_sm * (per_sm < 1 ? 1 : per_sm > 2 ? 2 : per_sm);
-        if (blocks > cap) blocks = cap;
-        const dim3 g((unsigned)blocks);
-        fh_status q = FH_OK;
-        switch (e->F) {
+        const int optin = e->smem_optin > 0 ? e->smem_optin : 232448;
+        for (int part = 0; part <= e->n_tiny; part++) {
+            const fh::SmallSet &S = part == 0 ? e->small_cta : e->small_tiny[part - 1];
+            if (S.n == 0) continue;
+            int threads = 256, smem = S.total * 4;
+            int64_t cap;
+            if (part == 0) {   // CTA copies: up to 2 CTAs of 256 per SM
+                const int per_sm = optin / (smem + 2048);
+                cap = (int64_t)e->n_sm * (per_sm < 1 ? 1 : per_sm > 2 ? 2 : per_sm);
+            } else {           // lane-private copies: whole warps per CTA, as many CTAs per SM as fit
+                const int w = (optin - 4096 - smem) / (S.ttotal * 4 * 32);
+                threads = (w > 8 ? 8 : w < 1 ? 1 : w) * 32;
+                smem += threads * S.ttotal * 4;
+                const int per_sm = 232448 / (smem + 2048);   // the SM's shared memory, not the per-CTA opt-in
+                cap = (int64_t)e->n_sm * (per_sm < 1 ? 1 : per_sm > 8 ? 8 : per_sm);
+            }
+            int64_t blocks = (N * S.n + threads - 1) / threads;
+            if (blocks > cap) blocks = cap;
+            const dim3 g((unsigned)blocks);
+            fh_status q = FH_OK;
+            switch (e->F) {
 #define FH_SMALL(FF)                                                                                          \
     q = cuda_check(cudaFuncSetAttribute(fh::bwd_small_kernel<FF>, cudaFuncAttributeMaxDynamicSharedMemorySize, \
                                         smem), "cudaFuncSetAttribute(bwd_small)");                           \
     if (q != FH_OK) return q;                                                                                 \
-    { fh::bwd_small_kernel<FF><<<g, 256, smem, s>>>(e->params, e->small, c4, N, dout, dtable, e->flag, perm); fh::count_launch(); }   \
+    { fh::bwd_small_kernel<FF><<<g, threads, smem, s>>>(e->params, S, c4, N, dout, dtable, e->flag, perm); fh::count_launch(); }   \
     break;
-            case 1: FH_SMALL(1)
-            case 2: FH_SMALL(2)
-            case 4: FH_SMALL(4)
-            default: FH_SMALL(8)
+                case 1: FH_SMALL(1)
+                case 2: FH_SMALL(2)
+                case 4: FH_SMALL(4)
+                default: FH_SMALL(8)
 #undef FH_SMALL
+            }
         }
         if (ev && n_ev > 0) cudaEventRecord(ev[0], s);
     }

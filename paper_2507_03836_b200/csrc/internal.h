@@ -60,6 +60,9 @@ struct fh_encoder_s {
     int n_gf = 0, gf[FH_MAX_LEVELS + 1] = {0};
     int n_gb = 0, gb[2 * FH_MAX_LEVELS + 2] = {0};  // bwd: pairs (begin, end) of non-small runs
     fh::SmallSet small{};                            // bwd: levels privatised in shared memory
+    fh::SmallSet small_cta{};                        // ... launch with CTA copies (non-tiny levels)
+    fh::SmallSet small_tiny[FH_MAX_LEVELS];          // ... one launch per tiny level (lane-private copies)
+    int n_tiny = 0;
     double fwd_limit = 0.0, bwd_limit = 0.0;         // L2 budgets of one direct pass (bytes; 0 = one pass)
     fh::KeySpec key{};                               // Morton key of fh_spatial_sort (set by the builder)
     int n_sm = 148;                                  // SMs of the device (set with the status word)
