@@ -595,18 +595,34 @@ __global__ void __launch_bounds__(256) bwd_small_kernel(const __grid_constant__ 
     __syncthreads();
     const int L = P.L;
     const int64_t items = N * S.n;
-    for (int64_t gid = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; gid < items;
-         gid += (int64_t)gridDim.x * blockDim.x) {
+    const int64_t stride = (int64_t)gridDim.x * blockDim.x;
+    // one item ahead: the next item's coordinates and upstream gradient are
+    // in flight while this one accumulates (the lane-private launches run
+    // few warps per SM, so the loads' latency is not hidden by occupancy)
+    auto fetch = [&](int64_t gid, float4 &pc, float (&gg)[F]) {
+        const int64_t j = gid / S.n;
+        const int li = (int)(gid - j * S.n);
+        const int64_t n = perm ? (int64_t)__ldg(perm + j) : j;
+        pc = __ldg(coords + n);
+#pragma unroll
+        for (int f = 0; f < F; f++) gg[f] = __ldg(dout + n * (int64_t)(L * F) + S.id[li] * F + f);
+    };
+    float4 p_nxt = make_float4(0.f, 0.f, 0.f, 0.f);
+    float g_nxt[F];
+    int64_t gid = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+    if (gid < items) fetch(gid, p_nxt, g_nxt);
+    for (; gid < items; gid += stride) {
         const int64_t j = gid / S.n;
         const int li = (int)(gid - j * S.n);
         const int l = S.id[li];
-        const int64_t n = perm ? (int64_t)__ldg(perm + j) : j;
         const Level lv = slv.get(l);
-        Cell c;
-        if (cell_of(lv, __ldg(coords + n), c) && li == 0) atomicOr(flag, 1);
+        const float4 pcur = p_nxt;
         float g[F];
 #pragma unroll
-        for (int f = 0; f < F; f++) g[f] = __ldg(dout + n * (int64_t)(L * F) + l * F + f);
+        for (int f = 0; f < F; f++) g[f] = g_nxt[f];
+        if (gid + stride < items) fetch(gid + stride, p_nxt, g_nxt);
+        Cell c;
+        if (cell_of(lv, pcur, c) && li == 0) atomicOr(flag, 1);
         const float wx[2] = {__fsub_rn(1.0f, c.w[0]), c.w[0]}, wy[2] = {__fsub_rn(1.0f, c.w[1]), c.w[1]};
         const float wz[2] = {__fsub_rn(1.0f, c.w[2]), c.w[2]}, wt[2] = {__fsub_rn(1.0f, c.w[3]), c.w[3]};
         if (S.toff[li] >= 0) {
