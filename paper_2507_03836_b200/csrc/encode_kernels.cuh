@@ -590,8 +590,11 @@ __global__ void __launch_bounds__(256) bwd_small_kernel(const __grid_constant__ 
     load_levels(P, slv);
     // lane-private blocks of the tiny levels: [warp][slot][lane] after acc
     const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
-    float *lp = acc + S.total + warp * S.ttotal * 32 + lane;
-    for (int i = threadIdx.x; i < S.total + (int)(blockDim.x >> 5) * S.ttotal * 32; i += blockDim.x) acc[i] = 0.f;
+    // S.copies = 1: one block per CTA; = warps: one block per warp
+    const int ncopy = S.copies > 1 ? S.copies : 1;
+    float *blk = acc + (ncopy > 1 ? warp * S.total : 0);
+    float *lp = acc + ncopy * S.total + warp * S.ttotal * 32 + lane;
+    for (int i = threadIdx.x; i < ncopy * S.total + (int)(blockDim.x >> 5) * S.ttotal * 32; i += blockDim.x) acc[i] = 0.f;
     __syncthreads();
     const int L = P.L;
     const int64_t items = N * S.n;
@@ -641,7 +644,7 @@ __global__ void __launch_bounds__(256) bwd_small_kernel(const __grid_constant__ 
             }
             continue;
         }
-        float *a = acc + S.soff[li] - (int)lv.offset * F;
+        float *a = blk + S.soff[li] - (int)lv.offset * F;
 #pragma unroll
         for (int k = 0; k < 16; k += 2) {
             const float Wyzt = wy[(k >> 1) & 1] * wz[(k >> 2) & 1] * wt[(k >> 3) & 1];
@@ -657,7 +660,7 @@ __global__ void __launch_bounds__(256) bwd_small_kernel(const __grid_constant__ 
     // fold the lane-private blocks into the CTA copy: lane l sums slot s over
     // the warp's 32 lanes (rotated start: conflict-free), then one CTA atomic
     if (S.ttotal > 0) {
-        const float *wb = acc + S.total + warp * S.ttotal * 32;
+        const float *wb = acc + ncopy * S.total + warp * S.ttotal * 32;
         for (int slot = lane; slot < S.ttotal; slot += 32) {
             float v = 0.f;
             for (int m = 0; m < 32; m++) v += wb[slot * 32 + ((m + lane) & 31)];
@@ -671,7 +674,8 @@ __global__ void __launch_bounds__(256) bwd_small_kernel(const __grid_constant__ 
         const int cnt = (li + 1 < S.n ? S.soff[li + 1] : S.total) - S.soff[li];
         float *dst = dtable + (size_t)lv.offset * F;
         for (int i = threadIdx.x; i < cnt; i += blockDim.x) {
-            const float v = acc[S.soff[li] + i];
+            float v = 0.f;
+            for (int w = 0; w < ncopy; w++) v += acc[w * S.total + S.soff[li] + i];
             if (v != 0.f) atomicAdd(dst + i, v);
         }
     }

@@ -37,6 +37,7 @@ struct SmallSet {
     int toff[kMaxLevels];
     int ttotal;
     int tmap[320];            // tiny slot -> float offset of the same element in the CTA block
+    int copies;               // blocks of `total` floats: 1 per CTA, or one per warp (= warps per CTA)
 };
 constexpr int kMaxTinyFloats = 320;   // lane-private floats per lane (all tiny levels together)
 constexpr int kMaxTinyLevel = 256;    // a level of at most this many floats (T_l F) is tiny

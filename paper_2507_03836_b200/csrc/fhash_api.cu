@@ -70,6 +70,7 @@ static fh_status ensure_flag(fh_encoder e) {
     if (const char *v = getenv("FH_AGG_MIN_DENSITY")) e->agg_density = atof(v);
     if (const char *v = getenv("FH_PAIR_SHIFT")) e->pair_shift = atoi(v);
     if (const char *v = getenv("FH_BWD_SPLIT")) e->bwd_split = atoi(v) != 0;
+    if (const char *v = getenv("FH_SMALL_WARP")) e->small_warp_copies = atoi(v) != 0;
     e->fwd_limit = budget("FH_FWD_GROUP_MB", 0.55);
     // backward: 0.45 L2 (measured with the shifted gradient scratch, whose
     // grads + scratch double a level's footprint: cfg2 bwd 0.737 -> 0.711
@@ -821,9 +822,15 @@ static fh_status encode_bwd_impl(fh_encoder e, const float *coords, int64_t N, c
             if (S.n == 0) continue;
             int threads = 256, smem = S.total * 4;
             int64_t cap;
-            if (part == 0) {   // CTA copies: up to 2 CTAs of 256 per SM
-                const int per_sm = optin / (smem + 2048);
-                cap = (int64_t)e->n_sm * (per_sm < 1 ? 1 : per_sm > 2 ? 2 : per_sm);
+            fh::SmallSet Sx = S;
+            if (part == 0) {   // one copy per warp when 8 fit in 64 KB (fewer CAS retries between warps:
+                               // Combustion's 728-entry level 161 -> 144 us), else one per CTA
+                const bool pw = e->small_warp_copies && 8 * S.total * 4 <= 64 * 1024;
+                Sx.copies = pw ? 8 : 1;
+                smem = Sx.copies * S.total * 4;
+                const int per_sm = 232448 / (smem + 2048);
+                const int mx = pw ? 4 : 2;
+                cap = (int64_t)e->n_sm * (per_sm < 1 ? 1 : per_sm > mx ? mx : per_sm);
             } else {           // lane-private copies: whole warps per CTA, as many CTAs per SM as fit
                 const int w = (optin - 4096 - smem) / (S.ttotal * 4 * 32);
                 threads = (w > 8 ? 8 : w < 1 ? 1 : w) * 32;
@@ -840,7 +847,7 @@ static fh_status encode_bwd_impl(fh_encoder e, const float *coords, int64_t N, c
     q = cuda_check(cudaFuncSetAttribute(fh::bwd_small_kernel<FF>, cudaFuncAttributeMaxDynamicSharedMemorySize, \
                                         smem), "cudaFuncSetAttribute(bwd_small)");                           \
     if (q != FH_OK) return q;                                                                                 \
-    { fh::bwd_small_kernel<FF><<<g, threads, smem, s>>>(e->params, S, c4, N, dout, dtable, e->flag, perm); fh::count_launch(); }   \
+    { fh::bwd_small_kernel<FF><<<g, threads, smem, s>>>(e->params, Sx, c4, N, dout, dtable, e->flag, perm); fh::count_launch(); }   \
     break;
                 case 1: FH_SMALL(1)
                 case 2: FH_SMALL(2)
