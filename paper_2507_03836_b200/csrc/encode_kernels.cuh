@@ -491,12 +491,14 @@ __global__ void __launch_bounds__(256) bwd_kernel(const __grid_constant__ Params
                                                   float *__restrict__ gsh,
                                                   int *__restrict__ flag, const __grid_constant__ LevelList LL,
                                                   const uint32_t *__restrict__ perm, uint32_t lo = 0,
-                                                  uint32_t span = 0) {
+                                                  uint32_t span = 0, uint32_t rep_n = 0, int64_t rep_stride = 0) {
     __shared__ LevelSmem slv;
     load_levels(P, slv);
     const int L = P.L;
     const int lc = LL.n;
     const int64_t gid = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+    // replicated pass (one contended level): CTA b reduces into copy b % rep_n
+    if (rep_n > 1) dtable += (int64_t)(blockIdx.x % rep_n) * rep_stride;
     const int64_t j = gid / lc;
     if (j >= N) return;
     const int li = (int)(gid - j * lc);
@@ -568,6 +570,17 @@ __global__ void __launch_bounds__(256) merge_shift_kernel(float *__restrict__ dt
             d.y += v.y;
             d2[q] = d;
         }
+    }
+}
+
+// Sum of the replicated copies of one level into dtable (the replicated
+// backward pass): dst[i] += sum_r src[r * stride + i], i < count.
+__global__ void __launch_bounds__(256) rep_reduce_kernel(float *__restrict__ dst, const float *__restrict__ src,
+                                                         int R, int64_t stride, int64_t count) {
+    for (int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; i < count; i += (int64_t)gridDim.x * blockDim.x) {
+        float v = 0.f;
+        for (int r = 0; r < R; r++) v += src[r * stride + i];
+        if (v != 0.f) dst[i] += v;
     }
 }
 

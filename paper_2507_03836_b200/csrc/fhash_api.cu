@@ -157,6 +157,18 @@ static fh_status ensure_flag(fh_encoder e) {
             const double g = (double)e->info[q].table_size * e->F * 4.0;
             e->shiftable[q] = (e->pair_shift & 1) && e->kind == 0 && e->F <= 2 && (lim <= 0.0 || 2.0 * g <= lim);
         }
+        // contended mid-size levels (not small, at most FH_REP_MAX_T entries):
+        // a pass of their own into replicated gradient copies (see the
+        // backward launch loop), F <= 2 (the copies live in the shifted scratch)
+        // Measured: the Combustion fold-2 shape's 4900-entry level 223 ->
+        // ~150 us replicated; cfg2's 8192-entry level slower in a pass of its
+        // own than mixed with the other levels (bwd 0.713 -> 0.758 ms), so
+        // strictly below 8192 entries by default.
+        const char *rv = getenv("FH_REP_MAX_T");
+        const uint64_t rep_max = rv ? (uint64_t)atoll(rv) : 8191;
+        for (int q = 0; q < e->L; q++)
+            e->rep[q] = e->kind == 0 && e->F <= 2 && (e->pair_shift & 1) && !small[q] &&
+                        e->info[q].table_size <= rep_max;
         e->n_gb = 0;
         int l = 0;
         while (l < e->L) {
@@ -166,6 +178,7 @@ static fh_status ensure_flag(fh_encoder e) {
             while (l < e->L && !small[l]) {
                 const double sz = (double)e->info[l].table_size * e->F * 4.0 * (e->shiftable[l] ? 2.0 : 1.0);
                 if (lim > 0.0 && l > b && acc + sz > lim) break;
+                if (l > b && (e->rep[l] || e->rep[l - 1])) break;   // replicated levels run alone
                 acc += sz;
                 l++;
             }
@@ -678,7 +691,12 @@ unsigned long long fh_kernel_launches(void) { return fh::g_launches.load(std::me
 
 static size_t scratch_parts(fh_encoder e, size_t *tsh_bytes, size_t *gsh_bytes) {
     const size_t t = (size_t)e->entries * e->F * dtype_size(e->table_dtype);
-    const size_t g = e->F <= 2 ? (size_t)e->entries * e->F * 4 + 64 : 0;
+    size_t g = e->F <= 2 ? (size_t)e->entries * e->F * 4 + 64 : 0;
+    for (int l = 0; l < e->L; l++)   // 64 replicated copies of a replicated level (set by ensure_flag)
+        if (e->rep[l]) {
+            const size_t stride = (size_t)((e->info[l].table_size + 2) * e->F + 3) / 4 * 4;
+            if (64 * stride * 4 > g) g = 64 * stride * 4;
+        }
     const size_t ta = (t + 255) / 256 * 256;
     if (tsh_bytes) *tsh_bytes = ta;
     if (gsh_bytes) *gsh_bytes = g;
@@ -686,7 +704,7 @@ static size_t scratch_parts(fh_encoder e, size_t *tsh_bytes, size_t *gsh_bytes) 
 }
 
 size_t fh_encoder_scratch_size(fh_encoder e) {
-    if (!e || e->kind != 0) return 0;
+    if (!e || e->kind != 0 || ensure_flag(e) != FH_OK) return 0;
     return scratch_parts(e, nullptr, nullptr);
 }
 
@@ -864,13 +882,20 @@ static fh_status encode_bwd_impl(fh_encoder e, const float *coords, int64_t N, c
     // as the group has entries (else the merge costs more than it saves)
     float *gsh_buf = nullptr;
     bool any_shift = false;
-    for (int l = 0; l < e->L; l++) any_shift |= e->shiftable[l];
+    for (int l = 0; l < e->L; l++) any_shift |= e->shiftable[l] || e->rep[l];
     if (any_shift) {
         uint64_t end = 0;   // the scratch only spans up to the last shiftable level
-        for (int l = 0; l < e->L; l++)
+        size_t need = 64;   // ... and holds 64 replicated copies of any replicated level
+        for (int l = 0; l < e->L; l++) {
             if (e->shiftable[l] && e->info[l].offset + e->info[l].table_size > end)
                 end = e->info[l].offset + e->info[l].table_size;
-        fh_encoder_s::Scratch *sc = get_scratch(e, s, 0, (size_t)end * e->F * 4 + 64);
+            if (e->rep[l]) {
+                const size_t stride = (size_t)((e->info[l].table_size + 2) * e->F + 3) / 4 * 4;
+                if (64 * stride * 4 > need) need = 64 * stride * 4;
+            }
+        }
+        if ((size_t)end * e->F * 4 + 64 > need) need = (size_t)end * e->F * 4 + 64;
+        fh_encoder_s::Scratch *sc = get_scratch(e, s, 0, need);
         if (sc) gsh_buf = sc->gsh;
     }
     for (int k = 0; k < e->n_gb; k++) {
@@ -895,6 +920,35 @@ static fh_status encode_bwd_impl(fh_encoder e, const float *coords, int64_t N, c
         }
         const uint64_t ge = e->info[l0 + lc - 1].offset + e->info[l0 + lc - 1].table_size - e->info[l0].offset;
         float *gsh = shift && (double)N * lc * 2.0 >= (double)ge ? gsh_buf : nullptr;
+        // a contended mid-size level (e->rep): a pass of its own into R
+        // replicated copies in the shifted scratch (CTA b -> copy b % R), so
+        // same-address reductions spread over R addresses, then one summing
+        // kernel.  The copies start at the even entry at or below the level's
+        // offset, so the pairs keep their 16-byte alignment.
+        if (lc == 1 && e->rep[l0] && gsh_buf && (double)N * 16.0 >= 4096.0 * (double)e->info[l0].table_size) {
+            const uint64_t T = e->info[l0].table_size, off = e->info[l0].offset, off_al = off & ~1ull;
+            const int64_t stride = (int64_t)((T + (off - off_al) + 1) * e->F + 3) / 4 * 4;   // floats
+            size_t cap = 0;
+            for (auto &sc : e->scratch) if (sc.gsh == gsh_buf) cap = sc.gsh_bytes;
+            int R = (int)(cap / ((size_t)stride * 4));
+            if (R > 64) R = 64;
+            if (R >= 2) {
+                if ((st = cuda_check(cudaMemsetAsync(gsh_buf, 0, (size_t)R * stride * 4, s), "zero replicas")) != FH_OK)
+                    return st;
+                float *base = gsh_buf - (int64_t)off_al * e->F;
+                switch (e->F) {
+                    case 1: { fh::bwd_kernel<1><<<g, 256, 0, s>>>(e->params, c4, N, dout, base, nullptr, e->flag, ll, nullptr, 0, 0, (uint32_t)R, stride); fh::count_launch(); } break;
+                    default: { fh::bwd_kernel<2><<<g, 256, 0, s>>>(e->params, c4, N, dout, base, nullptr, e->flag, ll, nullptr, 0, 0, (uint32_t)R, stride); fh::count_launch(); } break;
+                }
+                const int64_t cnt = (int64_t)T * e->F;
+                int64_t blocks = (cnt + 255) / 256;
+                if (blocks > (int64_t)e->n_sm * 4) blocks = (int64_t)e->n_sm * 4;
+                { fh::rep_reduce_kernel<<<(unsigned)blocks, 256, 0, s>>>(dtable + off * e->F, gsh_buf + (off - off_al) * e->F,
+                                                                         R, stride, cnt); fh::count_launch(); }
+                if (ev && ev0 + k < n_ev) cudaEventRecord(ev[ev0 + k], s);
+                continue;
+            }
+        }
         // this group's range of the shifted scratch, zeroed right before use
         int64_t m0 = (int64_t)e->info[l0].offset * e->F - fh::kShiftFloats;
         const int64_t m1 = (int64_t)(e->info[l0 + lc - 1].offset + e->info[l0 + lc - 1].table_size) * e->F - fh::kShiftFloats;

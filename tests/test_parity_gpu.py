@@ -637,3 +637,21 @@ def test_caller_owned_scratch():
     assert mhe.scratch_size() == 0
     with pytest.raises(fh.FHashError):
         mhe.attach_scratch(buf, st)
+
+
+@pytest.mark.parametrize("rep", ["0", "8191"])
+def test_backward_replicated_pass(rep, monkeypatch):
+    """A contended mid-size level (< 8192 entries, >= 4096 updates per entry)
+    is reduced in a pass of its own into 64 replicated copies summed
+    afterwards (FH_REP_MAX_T; 0 disables): equal to the oracle, odd level
+    offset included (the copies keep the pairs' 16-byte alignment)."""
+    monkeypatch.setenv("FH_REP_MAX_T", rep)
+    levels = [(3, 3, 3, 3), (9, 8, 5, 3)]           # offset of level 1 = 81 (odd), T = 1080
+    cfg = W.EncoderConfig("rep", tuple(levels), F=2, cap=0, table_dtype="f32")
+    case = W.encode_case(cfg, 300000, seed=31)
+    enc = fh.Encoder(levels, 2)
+    ref = oracle.Levels(levels)
+    got, st = run_bwd(enc, case)
+    assert st == fh.FH_OK
+    G, A = ref.backward(case.coords, case.dout, 2, want_abs=True)
+    check_bwd(got, G, A)

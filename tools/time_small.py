@@ -15,9 +15,12 @@ from paper_2507_03836_b200 import fhash as fh  # noqa: E402
 
 
 def main():
-    iters = int(sys.argv[1]) if len(sys.argv) > 1 else 10
+    iters = int(sys.argv[1]) if len(sys.argv) > 1 and sys.argv[1].isdigit() else 10
     full = fh.fold_schedule((200, 110, 54), 10, 2)
-    for name, lv in [("l4-7", full[4:]), ("l4", full[4:5]), ("l5", full[5:6]), ("l6-7", full[6:])]:
+    sets = [("l4-7", full[4:]), ("l4", full[4:5]), ("l5", full[5:6]), ("l6-7", full[6:])]
+    if "--all" in sys.argv:
+        sets += [("l1-3", full[1:4]), ("l1", full[1:2]), ("l2", full[2:3]), ("l3", full[3:4]), ("l0", full[0:1])]
+    for name, lv in sets:
         enc = fh.Encoder(lv, 2)
         N = 1 << 21
         g = torch.Generator("cuda").manual_seed(0)
