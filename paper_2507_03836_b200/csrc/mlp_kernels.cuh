@@ -88,7 +88,9 @@ struct TrainArgs {
     const __nv_bfloat16 *wsh;    // bf16 shadow of the flat parameters
     const float *wmaster;        // fp32 master (biases are read in fp32)
     float *dx;                   // [N][K0] dL/d(enc), fp32
-    float *grad;                 // flat fp32 grads (+=)
+    float *grad;                 // flat fp32 grads (+=, through partial + mlp_grad_reduce_kernel)
+    float *partial;              // [2 gridDim.x][P] per-slot partial gradients (every element written)
+    int P;                       // param_count(K0)
     float *loss;                 // += sum (y - t)^2 / N_global
     int *flag;                   // bit 1: non-finite loss
     int64_t N;
@@ -375,32 +377,42 @@ __global__ void __launch_bounds__(256, 1) mlp_train_kernel(const TrainArgs a) {
         tc::fence_after_sync();
     }
 
-    // ---- weight gradients out of TMEM: rows 0..63 -> dW2, db2; 64..127 -> dW1, db1
-    if (my_tiles > 0) {
+    // ---- weight gradients out of TMEM: rows 0..63 -> dW2, db2; 64..127 -> dW1, db1,
+    // written (not atomically added) into this slot's row of the partial
+    // buffer; mlp_grad_reduce_kernel sums the rows.  (Per-slot atomics on
+    // the same 6-8 k addresses from ~300 slots cost ~38 us per call at cfg3.)
+    {
         const int r = t;  // TMEM lane = row of DW
-        float *g = a.grad;
+        float *g = a.partial + (int64_t)(2 * blockIdx.x + slot) * a.P;
 #pragma unroll 1
         for (int c = 0; c < Lo::WHX; c += 16) {
             float v[16];
-            tc::tmem_ld16(tm + lane_off + Lo::T_DW + c, v);
-            tc::tmem_wait_ld();
+            if (my_tiles > 0) {   // slot-uniform
+                tc::tmem_ld16(tm + lane_off + Lo::T_DW + c, v);
+                tc::tmem_wait_ld();
+            } else {
+#pragma unroll
+                for (int j = 0; j < 16; j++) v[j] = 0.f;
+            }
 #pragma unroll
             for (int j = 0; j < 16; j++) {
                 const int col = c + j;
                 if (r < H) {
-                    if (col < H) atomicAdd(g + off_W2(K0) + r * H + col, v[j]);
-                    else if (col == H + K0) atomicAdd(g + off_b2(K0) + r, v[j]);
+                    if (col < H) g[off_W2(K0) + r * H + col] = v[j];
+                    else if (col == H + K0) g[off_b2(K0) + r] = v[j];
                 } else {
-                    if (col >= H && col < H + K0) atomicAdd(g + off_W1() + (r - H) * K0 + (col - H), v[j]);
-                    else if (col == H + K0) atomicAdd(g + off_b1(K0) + (r - H), v[j]);
+                    if (col >= H && col < H + K0) g[off_W1() + (r - H) * K0 + (col - H)] = v[j];
+                    else if (col == H + K0) g[off_b1(K0) + (r - H)] = v[j];
                 }
             }
         }
         // dw3[r] = hi + lo columns of the D3 accumulator, rows 0..63
-        float d3[16];
-        tc::tmem_ld16(tm + lane_off + Lo::T_D3, d3);
-        tc::tmem_wait_ld();
-        if (r < H) atomicAdd(g + off_w3(K0) + r, d3[0] + d3[1]);
+        float d3[16] = {0.f};
+        if (my_tiles > 0) {
+            tc::tmem_ld16(tm + lane_off + Lo::T_D3, d3);
+            tc::tmem_wait_ld();
+        }
+        if (r < H) g[off_w3(K0) + r] = d3[0] + d3[1];
     }
     // db3 and loss: warp reduce, then one atomic per CTA
 #pragma unroll
@@ -415,12 +427,24 @@ __global__ void __launch_bounds__(256, 1) mlp_train_kernel(const TrainArgs a) {
     if (tid == 0) {
         float d = 0.f, l = 0.f;
         for (int w = 0; w < 8; w++) { d += s_db3[w]; l += s_loss[w]; }
-        if (2 * (int64_t)blockIdx.x < n_tiles) {
-            atomicAdd(a.grad + off_b3(K0), d);
-            atomicAdd(a.loss, l * a.inv_n_global);
-        }
+        a.partial[(int64_t)(2 * blockIdx.x) * a.P + off_b3(K0)] = d;
+        a.partial[(int64_t)(2 * blockIdx.x + 1) * a.P + off_b3(K0)] = 0.f;
+        if (2 * (int64_t)blockIdx.x < n_tiles) atomicAdd(a.loss, l * a.inv_n_global);
     }
     if (warp == 0) tc::tmem_dealloc(tbase, Lo::TMEM_COLS);
+}
+
+// grad[p] += sum over the partial rows [0, rows) of partial[row][p]: block
+// (x) = 256 parameters, block (y) = a chunk of 16 rows, one atomic per
+// parameter per chunk.
+__global__ void __launch_bounds__(256) mlp_grad_reduce_kernel(float *__restrict__ grad,
+                                                              const float *__restrict__ partial, int rows, int P) {
+    const int p = blockIdx.x * blockDim.x + threadIdx.x;
+    if (p >= P) return;
+    const int r0 = blockIdx.y * 16, r1 = min(rows, r0 + 16);
+    float v = 0.f;
+    for (int r = r0; r < r1; r++) v += partial[(int64_t)r * P + p];
+    atomicAdd(grad + p, v);
 }
 
 // ------------------------------------------------------------ inference

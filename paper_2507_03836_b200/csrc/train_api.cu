@@ -26,6 +26,7 @@ struct fh_trainer_s {
     __nv_bfloat16 *enc_out = nullptr;  // [max_batch][K0]
     float *dx = nullptr;               // [max_batch][K0]
     int *flag = nullptr;               // bit 1: non-finite loss
+    float *partial = nullptr;          // [2 n_sm][P] per-slot MLP gradient partials
     float *loss_scratch = nullptr;
     cudaEvent_t bwd_ev[FH_MAX_LEVELS + 1] = {};  // caller's events, recorded after each backward launch
     int n_bwd_ev = 0;
@@ -34,6 +35,15 @@ struct fh_trainer_s {
 namespace {
 
 size_t align_up(size_t v, size_t a) { return (v + a - 1) / a * a; }
+
+// The MLP kernel's per-slot gradient partials: 2 slots x (at most) one CTA
+// per SM of the current device.
+int device_sms() {
+    int dev = 0, n = 148;
+    if (cudaGetDevice(&dev) == cudaSuccess) cudaDeviceGetAttribute(&n, cudaDevAttrMultiProcessorCount, dev);
+    return n > 0 ? n : 148;
+}
+size_t partial_bytes(int K0) { return align_up((size_t)2 * device_sms() * fh::mlp::param_count(K0) * 4, 256); }
 
 fh_status check_mlp(fh_encoder enc, const fh_mlp_desc *m) {
     if (!enc || !m) return fail(FH_E_ARG, "NULL encoder or MLP descriptor");
@@ -63,6 +73,8 @@ fh_status launch_mlp(fh_trainer tr, const float *target, int64_t N, int64_t N_gl
     a.wmaster = tr->b.mlp_master;
     a.dx = tr->dx;
     a.grad = tr->b.mlp_grad;
+    a.partial = tr->partial;
+    a.P = fh::mlp::param_count(K0);
     a.loss = loss;
     a.flag = tr->flag;
     a.N = N;
@@ -71,6 +83,9 @@ fh_status launch_mlp(fh_trainer tr, const float *target, int64_t N, int64_t N_gl
     const int64_t pairs = (tiles + 1) / 2;  // two tile slots per CTA
     const int grid = (int)(pairs < tr->n_sm ? pairs : tr->n_sm);
     { fh::mlp::mlp_train_kernel<K0><<<grid, 256, smem, s>>>(a); fh::count_launch(); }
+    const int rows = 2 * grid;
+    const dim3 rg((unsigned)((a.P + 255) / 256), (unsigned)((rows + 15) / 16));
+    { fh::mlp::mlp_grad_reduce_kernel<<<rg, 256, 0, s>>>(tr->b.mlp_grad, tr->partial, rows, a.P); fh::count_launch(); }
     return cuda_check(cudaGetLastError(), "mlp_train_kernel launch");
 }
 
@@ -85,7 +100,8 @@ uint64_t fh_mlp_param_count(const fh_mlp_desc *m) {
 size_t fh_train_workspace_size(fh_encoder enc, const fh_mlp_desc *m, int64_t max_batch) {
     if (!enc || !m || max_batch < 0) return 0;
     const size_t K0 = (size_t)m->n_in;
-    return align_up((size_t)max_batch * K0 * 2, 256) + align_up((size_t)max_batch * K0 * 4, 256) + 256;
+    return align_up((size_t)max_batch * K0 * 2, 256) + align_up((size_t)max_batch * K0 * 4, 256) + 256 +
+           partial_bytes(m->n_in);
 }
 
 fh_status fh_trainer_create(fh_encoder enc, const fh_mlp_desc *m, const fh_train_buffers *b, const fh_adam *adam,
@@ -125,6 +141,7 @@ fh_status fh_trainer_create(fh_encoder enc, const fh_mlp_desc *m, const fh_train
     w += align_up((size_t)max_batch * tr->K0 * 4, 256);
     tr->flag = reinterpret_cast<int *>(w);
     tr->loss_scratch = reinterpret_cast<float *>(w + 16);
+    tr->partial = reinterpret_cast<float *>(w + 256);
     st = cuda_check(cudaMemset(tr->flag, 0, 32), "fh_trainer_create: clear flags");
     if (st != FH_OK) { delete tr; return st; }
     *out = tr;
