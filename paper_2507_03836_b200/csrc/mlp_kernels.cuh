@@ -394,16 +394,17 @@ __global__ void __launch_bounds__(256, 1) mlp_train_kernel(const TrainArgs a) {
 #pragma unroll
                 for (int j = 0; j < 16; j++) v[j] = 0.f;
             }
+            // 16-column chunks lie entirely in one block: W2 (c < H), W1 (H <= c < H + K0) or the
+            // bias chunk (c = H + K0); the two weight blocks as float4 stores (rows padded to 4)
+            float4 *dst = nullptr;
+            if (r < H && c < H) dst = reinterpret_cast<float4 *>(g + off_W2(K0) + r * H + c);
+            else if (r >= H && c >= H && c < H + K0) dst = reinterpret_cast<float4 *>(g + off_W1() + (r - H) * K0 + (c - H));
+            if (dst) {
 #pragma unroll
-            for (int j = 0; j < 16; j++) {
-                const int col = c + j;
-                if (r < H) {
-                    if (col < H) g[off_W2(K0) + r * H + col] = v[j];
-                    else if (col == H + K0) g[off_b2(K0) + r] = v[j];
-                } else {
-                    if (col >= H && col < H + K0) g[off_W1() + (r - H) * K0 + (col - H)] = v[j];
-                    else if (col == H + K0) g[off_b1(K0) + (r - H)] = v[j];
-                }
+                for (int j = 0; j < 16; j += 4) dst[j / 4] = make_float4(v[j], v[j + 1], v[j + 2], v[j + 3]);
+            } else if (c == H + K0) {
+                if (r < H) g[off_b2(K0) + r] = v[0];
+                else g[off_b1(K0) + (r - H)] = v[0];
             }
         }
         // dw3[r] = hi + lo columns of the D3 accumulator, rows 0..63
@@ -438,9 +439,10 @@ __global__ void __launch_bounds__(256, 1) mlp_train_kernel(const TrainArgs a) {
 // (x) = 256 parameters, block (y) = a chunk of 16 rows, one atomic per
 // parameter per chunk.
 __global__ void __launch_bounds__(256) mlp_grad_reduce_kernel(float *__restrict__ grad,
-                                                              const float *__restrict__ partial, int rows, int P) {
+                                                              const float *__restrict__ partial, int rows, int P,
+                                                              int n_params) {
     const int p = blockIdx.x * blockDim.x + threadIdx.x;
-    if (p >= P) return;
+    if (p >= n_params) return;
     const int r0 = blockIdx.y * 16, r1 = min(rows, r0 + 16);
     float v = 0.f;
     for (int r = r0; r < r1; r++) v += partial[(int64_t)r * P + p];

@@ -43,7 +43,9 @@ int device_sms() {
     if (cudaGetDevice(&dev) == cudaSuccess) cudaDeviceGetAttribute(&n, cudaDevAttrMultiProcessorCount, dev);
     return n > 0 ? n : 148;
 }
-size_t partial_bytes(int K0) { return align_up((size_t)2 * device_sms() * fh::mlp::param_count(K0) * 4, 256); }
+size_t partial_bytes(int K0) {
+    return align_up((size_t)2 * device_sms() * ((fh::mlp::param_count(K0) + 3) / 4 * 4) * 4, 256);
+}
 
 fh_status check_mlp(fh_encoder enc, const fh_mlp_desc *m) {
     if (!enc || !m) return fail(FH_E_ARG, "NULL encoder or MLP descriptor");
@@ -74,7 +76,7 @@ fh_status launch_mlp(fh_trainer tr, const float *target, int64_t N, int64_t N_gl
     a.dx = tr->dx;
     a.grad = tr->b.mlp_grad;
     a.partial = tr->partial;
-    a.P = fh::mlp::param_count(K0);
+    a.P = (fh::mlp::param_count(K0) + 3) / 4 * 4;   // partial row stride (16-byte rows)
     a.loss = loss;
     a.flag = tr->flag;
     a.N = N;
@@ -85,7 +87,8 @@ fh_status launch_mlp(fh_trainer tr, const float *target, int64_t N, int64_t N_gl
     { fh::mlp::mlp_train_kernel<K0><<<grid, 256, smem, s>>>(a); fh::count_launch(); }
     const int rows = 2 * grid;
     const dim3 rg((unsigned)((a.P + 255) / 256), (unsigned)((rows + 15) / 16));
-    { fh::mlp::mlp_grad_reduce_kernel<<<rg, 256, 0, s>>>(tr->b.mlp_grad, tr->partial, rows, a.P); fh::count_launch(); }
+    { fh::mlp::mlp_grad_reduce_kernel<<<rg, 256, 0, s>>>(tr->b.mlp_grad, tr->partial, rows, a.P,
+                                                          fh::mlp::param_count(K0)); fh::count_launch(); }
     return cuda_check(cudaGetLastError(), "mlp_train_kernel launch");
 }
 
