@@ -305,8 +305,8 @@ typedef struct {
  *   W1[64][n_in], b1[64], W2[64][64], b2[64], w3[64], b3
  * (weights [out][in] row-major).  table_shadow has the encoder's table
  * dtype (FH_F16: Adam writes it; FH_F32: pass NULL, the master is read
- * directly); mlp_shadow is bf16.  Grad buffers must be zero before the
- * first step (fh_train_apply re-zeroes them). */
+ * directly); mlp_shadow is bf16.  The grad buffers need no initialisation:
+ * every fh_train_fwd_bwd overwrites them with the step's gradient. */
 typedef struct {
     float *table_master;
     void *table_shadow;
@@ -336,8 +336,11 @@ fh_status fh_trainer_create(fh_encoder enc, const fh_mlp_desc *mlp, const fh_tra
 
 /* Forward + loss + backward for N_local samples (coords [N][4] f32,
  * target [N] f32, device).  loss_dev (device f32, may be NULL) receives
- * sum_local (y - t)^2 / N_global.  Gradients are ADDED to the grad
- * buffers.  N_local <= max_batch, N_global >= N_local. */
+ * sum_local (y - t)^2 / N_global.  The grad buffers are OVERWRITTEN with
+ * this call's gradient (table grads zeroed level group by level group right
+ * before the reductions, FH_BWD_OVERWRITE; MLP grads zeroed first), so the
+ * optimiser never has to clear them.  N_local <= max_batch, N_global >=
+ * N_local. */
 fh_status fh_train_fwd_bwd(fh_trainer tr, const float *coords, const float *target, int64_t N_local,
                            int64_t N_global, float *loss_dev, fh_stream stream);
 
@@ -349,8 +352,7 @@ fh_status fh_train_apply(fh_trainer tr, fh_stream stream);
  * reading their (already reduce-scattered) gradients from grad_shard
  * (device f32, end - begin values), plus the full MLP segment from the
  * trainer's mlp_grad (already all-reduced).  Updates masters, moments and
- * shadows in the range only; zeroes the trainer's table_grad and mlp_grad
- * entirely for the next step.  begin must be a multiple of 4.  The caller
+ * shadows in the range only.  begin must be a multiple of 4.  The caller
  * then all-gathers the shadow (or, for FH_F32 tables, the master). */
 fh_status fh_train_apply_sharded(fh_trainer tr, int64_t begin, int64_t end, const float *grad_shard,
                                  fh_stream stream);
@@ -370,7 +372,7 @@ fh_status fh_train_apply_sharded(fh_trainer tr, int64_t begin, int64_t end, cons
  *   element ranges [begin_i, end_i) (disjoint) reading grad_i[0 .. end_i -
  *   begin_i) (device f32, e.g. this rank's reduce-scattered chunks), plus the
  *   whole MLP segment from the trainer's mlp_grad; rewrites the shadows of
- *   those ranges and zeroes the trainer's table_grad and mlp_grad.  At most
+ *   those ranges.  At most
  *   63 ranges; ranges whose pointers are not 16-byte aligned take a scalar
  *   path.  Errors: FH_E_ARG. */
 int       fh_train_bwd_launches(fh_trainer tr);

@@ -1023,8 +1023,8 @@ int bwd_launch_ranges(fh_encoder e, int i, int64_t *r, int max) {
     return 1;
 }
 fh_status encode_bwd_events(fh_encoder e, const float *coords, int64_t N, const float *dout, float *dtable,
-                            fh_stream stream, cudaEvent_t *ev, int n_ev) {
-    return encode_bwd_impl(e, coords, N, nullptr, dout, dtable, stream, ev, n_ev);
+                            fh_stream stream, cudaEvent_t *ev, int n_ev, bool overwrite) {
+    return encode_bwd_impl(e, coords, N, nullptr, dout, dtable, stream, ev, n_ev, overwrite);
 }
 }  // namespace fh
 

@@ -581,7 +581,8 @@ __global__ void __launch_bounds__(256, 1) mlp_infer_kernel(const InferArgs a) {
 // Bias-corrected Adam (R12), fp32 master/m/v, dense over every parameter:
 //   m = b1 m + (1-b1) g;  v = b2 v + (1-b2) g^2
 //   p -= lr * (m * c1) / (sqrt(v * c2) + eps),  c1 = 1/(1-b1^t), c2 = 1/(1-b2^t)
-// then writes the low-precision shadow (fp16 table / bf16 MLP) and zeroes g.
+// then writes the low-precision shadow (fp16 table / bf16 MLP).  The grads are
+// left as they are: every fh_train_fwd_bwd overwrites them.
 struct AdamSeg {
     float *p, *g, *m, *v;
     void *shadow;        // __half* (kind 1), __nv_bfloat16* (kind 2), unused (kind 0)
@@ -607,7 +608,7 @@ __device__ __forceinline__ void adam_one(const AdamArgs &A, const AdamSeg &s, in
     const float m = fmaf(A.b1, s.m[i], A.omb1 * g);
     const float v = fmaf(A.b2, s.v[i], A.omb2 * g * g);
     const float p = s.p[i] - A.lr * (m * A.c1) / (sqrtf(v * A.c2) + A.eps);
-    s.m[i] = m; s.v[i] = v; s.p[i] = p; s.g[i] = 0.f;
+    s.m[i] = m; s.v[i] = v; s.p[i] = p;
     if (s.kind == 1) reinterpret_cast<__half *>(s.shadow)[i] = __float2half_rn(p);
     else if (s.kind == 2) reinterpret_cast<__nv_bfloat16 *>(s.shadow)[i] = __float2bfloat16_rn(p);
     // kind 0: fp32 master only (FH_F32 tables are read directly), no shadow
@@ -641,7 +642,6 @@ __global__ void __launch_bounds__(256) adam_kernel(const __grid_constant__ AdamA
         reinterpret_cast<float4 *>(s.m)[q] = make_float4(mm[0], mm[1], mm[2], mm[3]);
         reinterpret_cast<float4 *>(s.v)[q] = make_float4(vv[0], vv[1], vv[2], vv[3]);
         reinterpret_cast<float4 *>(s.p)[q] = make_float4(pp[0], pp[1], pp[2], pp[3]);
-        reinterpret_cast<float4 *>(s.g)[q] = make_float4(0.f, 0.f, 0.f, 0.f);
         if (s.kind == 1) {
             __half2 h0 = __floats2half2_rn(pp[0], pp[1]), h1 = __floats2half2_rn(pp[2], pp[3]);
             uint2 u;

@@ -161,7 +161,16 @@ fh_status fh_train_fwd_bwd(fh_trainer tr, const float *coords, const float *targ
     cudaStream_t s = reinterpret_cast<cudaStream_t>(stream);
     float *loss = loss_dev ? loss_dev : tr->loss_scratch;
     fh_status st = cuda_check(cudaMemsetAsync(loss, 0, sizeof(float), s), "zero loss");
-    if (st != FH_OK || N == 0) return st;
+    if (st != FH_OK) return st;
+    // the step's gradients OVERWRITE the grad buffers: the MLP kernel adds
+    // into zeroed MLP grads; the encode backward zeroes each table level
+    // group right before reducing into it (FH_BWD_OVERWRITE)
+    st = cuda_check(cudaMemsetAsync(tr->b.mlp_grad, 0, (size_t)fh::mlp::param_count(tr->K0) * sizeof(float), s),
+                    "zero mlp_grad");
+    if (st != FH_OK) return st;
+    if (N == 0)
+        return cuda_check(cudaMemsetAsync(tr->b.table_grad, 0, (size_t)tr->enc->entries * tr->enc->F * sizeof(float), s),
+                          "zero table_grad");
     const void *table = tr->b.table_shadow ? tr->b.table_shadow : tr->b.table_master;
     if ((st = fh_encode_fwd(tr->enc, coords, N, table, tr->enc_out, FH_BF16, stream)) != FH_OK) return st;
     switch (tr->K0) {
@@ -171,7 +180,8 @@ fh_status fh_train_fwd_bwd(fh_trainer tr, const float *coords, const float *targ
         default: st = launch_mlp<64>(tr, target, N, N_global, loss, s); break;
     }
     if (st != FH_OK) return st;
-    return fh::encode_bwd_events(tr->enc, coords, N, tr->dx, tr->b.table_grad, stream, tr->bwd_ev, tr->n_bwd_ev);
+    return fh::encode_bwd_events(tr->enc, coords, N, tr->dx, tr->b.table_grad, stream, tr->bwd_ev, tr->n_bwd_ev,
+                                 /*overwrite=*/true);
 }
 
 int fh_train_bwd_launches(fh_trainer tr) { return tr ? fh::bwd_launch_count(tr->enc) : -1; }
@@ -296,13 +306,7 @@ fh_status fh_train_apply_ranges(fh_trainer tr, int n, const int64_t *begin, cons
                 return fail(FH_E_ARG, "fh_train_apply_ranges: ranges %d and %d overlap", j, i);
     }
     cudaStream_t s = reinterpret_cast<cudaStream_t>(stream);
-    fh_status st = apply_ranges_impl(tr, n, begin, end, const_cast<float *const *>(grad), s);
-    if (st != FH_OK) return st;
-    // the local (pre-reduction) grads must start the next step at zero
-    st = cuda_check(cudaMemsetAsync(tr->b.table_grad, 0, (size_t)nt * sizeof(float), s), "zero table_grad");
-    if (st != FH_OK) return st;
-    return cuda_check(cudaMemsetAsync(tr->b.mlp_grad, 0, (size_t)fh::mlp::param_count(tr->K0) * sizeof(float), s),
-                      "zero mlp_grad");
+    return apply_ranges_impl(tr, n, begin, end, const_cast<float *const *>(grad), s);
 }
 
 fh_status fh_train_apply_peers(fh_trainer tr, int W, const float *const *peer_table_grad,
@@ -401,10 +405,7 @@ fh_status fh_train_apply_sharded(fh_trainer tr, int64_t begin, int64_t end, cons
     if (end > begin && (!grad_shard || !aligned(grad_shard, 16)))
         return fail(FH_E_ARG, "fh_train_apply_sharded: NULL or misaligned grad_shard");
     cudaStream_t s = reinterpret_cast<cudaStream_t>(stream);
-    fh_status st = apply_impl(tr, begin, end, const_cast<float *>(grad_shard), s);
-    if (st != FH_OK) return st;
-    // the local (pre-reduction) table grads must start the next step at zero
-    return cuda_check(cudaMemsetAsync(tr->b.table_grad, 0, (size_t)n * sizeof(float), s), "zero table_grad");
+    return apply_impl(tr, begin, end, const_cast<float *>(grad_shard), s);
 }
 
 fh_status fh_train_step(fh_trainer tr, const float *coords, const float *target, int64_t N, int64_t N_global,

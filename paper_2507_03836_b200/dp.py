@@ -253,7 +253,8 @@ class PeerShardedDP:
     rank's shadow buffer -- reduce-scatter, Adam and all-gather in one pass,
     overlapped with the later groups' backward.  The tails of overlap_plan
     and the MLP are summed and updated redundantly on every rank at the end;
-    a last barrier precedes zeroing the local gradients.  The trainer must
+    a last barrier precedes the next step's fwd_bwd, which overwrites the
+    local gradients.  The trainer must
     be built with alloc=dp.symm_alloc."""
 
     def __init__(self, trainer, group=None):
@@ -308,8 +309,8 @@ class PeerShardedDP:
             self.hg.barrier(channel=0)
             tr.apply_peers(self.pg, self.ps, self.pm, self.tails, [0] * len(self.tails), True, first,
                            stream=self.comm)
-            self.hg.barrier(channel=0)                  # every rank done reading gradients
-            tr.grads.zero_()
+            self.hg.barrier(channel=0)                  # every rank done reading gradients: the next
+                                                        # fwd_bwd (queued behind it) may overwrite them
         cur.wait_stream(self.comm)
 
 

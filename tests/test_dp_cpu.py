@@ -68,9 +68,10 @@ def _worker(rank, world, port, out):
 
 
 class _MockTrainer:
-    """CPU stand-in with the attributes dp.ShardedDP uses; fwd_bwd adds a
-    deterministic per-(rank, step) gradient, apply_sharded runs the oracle's
-    Adam on the given range (the GPU kernels are tested in test_train_gpu)."""
+    """CPU stand-in with the attributes dp.ShardedDP uses; fwd_bwd writes a
+    deterministic per-(rank, step) gradient (overwriting, as
+    fh_train_fwd_bwd does), apply_sharded runs the oracle's Adam on the given
+    range (the GPU kernels are tested in test_train_gpu)."""
 
     def __init__(self, n_table, n_mlp, world, rank):
         from oracle import train as T
@@ -96,8 +97,8 @@ class _MockTrainer:
     def fwd_bwd(self, coords, target, n_global, stream=None):
         nm = self.mlp_grad.numel()
         g = torch.from_numpy(self.local_grad(self.rank, self.step_no, self.n_table + nm))
-        self.grads[:self.n_table] += g[:self.n_table]
-        self.mlp_grad += g[self.n_table:]
+        self.grads[:self.n_table] = g[:self.n_table]
+        self.mlp_grad.copy_(g[self.n_table:])
 
     def apply_sharded(self, begin, end, shard, stream=None):
         self.step_no += 1
@@ -108,7 +109,6 @@ class _MockTrainer:
         self.pm, self.mm, self.mv = self.T.adam_step(self.pm, self.mlp_grad.numpy().astype(np.float64),
                                                      self.mm, self.mv, s)
         self.shadow_flat[begin:end] = torch.from_numpy(self.p[begin:end]).half()
-        self.grads.zero_()
 
 
 def _sharded_worker(rank, world, port, out):
@@ -220,7 +220,6 @@ class _MockOverlapTrainer(_MockTrainer):
             self.shadow_flat[b:e] = torch.from_numpy(self.p[b:e]).half()
         self.pm, self.mm, self.mv = self.T.adam_step(self.pm, self.mlp_grad.numpy().astype(np.float64),
                                                      self.mm, self.mv, s)
-        self.grads.zero_()
 
 
 def _overlap_worker(rank, world, port, out):
