@@ -799,6 +799,131 @@ static fh_status encode_fwd_impl(fh_encoder e, const float *coords, int64_t N, c
     return cuda_check(cudaGetLastError(), "fh_encode_fwd launch");
 }
 
+// ------------------------------------------------------------- backward
+// One backward call's arguments, shared by the launch helpers below.
+struct BwdCall {
+    fh_encoder e;
+    const float4 *c4;
+    int64_t N;
+    const float *dout;
+    float *dtable;
+    cudaStream_t s;
+};
+
+// bwd_kernel<F, RANGED> for the encoder's F (gsh only for F <= 2).
+static void launch_bwd_kernel(const BwdCall &b, dim3 g, const fh::LevelList &ll, float *dt, float *gsh, bool ranged,
+                              uint32_t lo = 0, uint32_t span = 0, uint32_t rep_n = 0, int64_t rep_stride = 0) {
+    const fh_encoder e = b.e;
+#define FH_BWD(FF, RR, GG)                                                                                     \
+    { fh::bwd_kernel<FF, RR><<<g, 256, 0, b.s>>>(e->params, b.c4, b.N, b.dout, dt, GG, e->flag, ll, nullptr, lo, span, \
+                                                 rep_n, rep_stride); fh::count_launch(); }
+    switch (e->F) {
+        case 1: if (ranged) FH_BWD(1, true, gsh) else FH_BWD(1, false, gsh) break;
+        case 2: if (ranged) FH_BWD(2, true, gsh) else FH_BWD(2, false, gsh) break;
+        case 4: if (ranged) FH_BWD(4, true, nullptr) else FH_BWD(4, false, nullptr) break;
+        default: if (ranged) FH_BWD(8, true, nullptr) else FH_BWD(8, false, nullptr) break;
+    }
+#undef FH_BWD
+}
+
+// The few-cell levels (bwd_small_kernel): one launch with CTA (or per-warp)
+// copies for the non-tiny ones, one lane-private launch per tiny level.
+static fh_status bwd_small_levels(const BwdCall &b, const uint32_t *perm) {
+    const fh_encoder e = b.e;
+    const int optin = e->smem_optin > 0 ? e->smem_optin : 232448;
+    for (int part = 0; part <= e->n_tiny; part++) {
+        const fh::SmallSet &S = part == 0 ? e->small_cta : e->small_tiny[part - 1];
+        if (S.n == 0) continue;
+        int threads = 256, smem = S.total * 4;
+        int64_t cap;
+        fh::SmallSet Sx = S;
+        if (part == 0) {   // one copy per warp when 8 fit in 64 KB (fewer CAS retries between warps:
+                           // Combustion's 728-entry level 161 -> 144 us), else one per CTA
+            const bool pw = e->small_warp_copies && 8 * S.total * 4 <= 64 * 1024;
+            Sx.copies = pw ? 8 : 1;
+            smem = Sx.copies * S.total * 4;
+            const int per_sm = 232448 / (smem + 2048);
+            const int mx = pw ? 4 : 2;
+            cap = (int64_t)e->n_sm * (per_sm < 1 ? 1 : per_sm > mx ? mx : per_sm);
+        } else {           // lane-private copies: whole warps per CTA, as many CTAs per SM as fit
+            const int w = (optin - 4096 - smem) / (S.ttotal * 4 * 32);
+            threads = (w > 8 ? 8 : w < 1 ? 1 : w) * 32;
+            smem += threads * S.ttotal * 4;
+            const int per_sm = 232448 / (smem + 2048);   // the SM's shared memory, not the per-CTA opt-in
+            cap = (int64_t)e->n_sm * (per_sm < 1 ? 1 : per_sm > 8 ? 8 : per_sm);
+        }
+        int64_t blocks = (b.N * S.n + threads - 1) / threads;
+        if (blocks > cap) blocks = cap;
+        const dim3 g((unsigned)blocks);
+        fh_status q = FH_OK;
+        switch (e->F) {
+#define FH_SMALL(FF)                                                                                          \
+    q = cuda_check(cudaFuncSetAttribute(fh::bwd_small_kernel<FF>, cudaFuncAttributeMaxDynamicSharedMemorySize, \
+                                        smem), "cudaFuncSetAttribute(bwd_small)");                           \
+    if (q != FH_OK) return q;                                                                                 \
+    { fh::bwd_small_kernel<FF><<<g, threads, smem, b.s>>>(e->params, Sx, b.c4, b.N, b.dout, b.dtable, e->flag, perm); \
+      fh::count_launch(); }                                                                                   \
+    break;
+            case 1: FH_SMALL(1)
+            case 2: FH_SMALL(2)
+            case 4: FH_SMALL(4)
+            default: FH_SMALL(8)
+#undef FH_SMALL
+        }
+    }
+    return FH_OK;
+}
+
+// The shifted gradient scratch of the calling stream:
+// spans the shiftable levels and holds 64 replicated copies of any
+// replicated level.  nullptr when no level needs it or no slot is free.
+static float *bwd_scratch(fh_encoder e, cudaStream_t s, size_t *bytes) {
+    bool any = false;
+    for (int l = 0; l < e->L; l++) any |= e->shiftable[l] || e->rep[l];
+    if (!any) return nullptr;
+    uint64_t end = 0;
+    size_t need = 64;
+    for (int l = 0; l < e->L; l++) {
+        if (e->shiftable[l] && e->info[l].offset + e->info[l].table_size > end)
+            end = e->info[l].offset + e->info[l].table_size;
+        if (e->rep[l]) {
+            const size_t stride = (size_t)((e->info[l].table_size + 2) * e->F + 3) / 4 * 4;
+            if (64 * stride * 4 > need) need = 64 * stride * 4;
+        }
+    }
+    if ((size_t)end * e->F * 4 + 64 > need) need = (size_t)end * e->F * 4 + 64;
+    fh_encoder_s::Scratch *sc = get_scratch(e, s, 0, need);
+    if (!sc) return nullptr;
+    *bytes = sc->gsh_bytes;
+    return sc->gsh;
+}
+
+// A contended mid-size level (e->rep) in a pass of its own into R
+// replicated copies in the scratch (CTA b -> copy b % R), so same-address
+// reductions spread over R addresses, then one summing kernel.  The copies
+// start at the even entry at or below the level's offset, so the pairs keep
+// their 16-byte alignment.  false: not applicable (the caller runs the
+// level as a normal pass).
+static bool bwd_replicated(const BwdCall &b, int l, dim3 g, const fh::LevelList &ll, float *scratch, size_t cap,
+                           fh_status *st) {
+    const fh_encoder e = b.e;
+    const uint64_t T = e->info[l].table_size, off = e->info[l].offset, off_al = off & ~1ull;
+    if (!scratch || (double)b.N * 16.0 < 4096.0 * (double)T) return false;
+    const int64_t stride = (int64_t)((T + (off - off_al) + 1) * e->F + 3) / 4 * 4;   // floats
+    int R = (int)(cap / ((size_t)stride * 4));
+    if (R > 64) R = 64;
+    if (R < 2) return false;
+    if ((*st = cuda_check(cudaMemsetAsync(scratch, 0, (size_t)R * stride * 4, b.s), "zero replicas")) != FH_OK)
+        return true;
+    launch_bwd_kernel(b, g, ll, scratch - (int64_t)off_al * e->F, nullptr, false, 0, 0, (uint32_t)R, stride);
+    const int64_t cnt = (int64_t)T * e->F;
+    int64_t blocks = (cnt + 255) / 256;
+    if (blocks > (int64_t)e->n_sm * 4) blocks = (int64_t)e->n_sm * 4;
+    { fh::rep_reduce_kernel<<<(unsigned)blocks, 256, 0, b.s>>>(b.dtable + off * e->F, scratch + (off - off_al) * e->F,
+                                                               R, stride, cnt); fh::count_launch(); }
+    return true;
+}
+
 static fh_status encode_bwd_impl(fh_encoder e, const float *coords, int64_t N, const uint32_t *perm,
                                  const float *dout, float *dtable, fh_stream stream,
                                  cudaEvent_t *ev = nullptr, int n_ev = 0, bool zero = false) {
@@ -830,79 +955,24 @@ static fh_status encode_bwd_impl(fh_encoder e, const float *coords, int64_t N, c
         }
         return cuda_check(cudaGetLastError(), "fh_encode_bwd_ordered launch");
     }
+    const BwdCall b{e, c4, N, dout, dtable, s};
+    // launch 0 (when present): the few-cell levels in shared memory
     if (e->small.n > 0) {
         if (zero)
             for (int j = 0; j < e->small.n; j++)
                 if ((st = zero_levels(e->small.id[j], e->small.id[j] + 1)) != FH_OK) return st;
-        const int optin = e->smem_optin > 0 ? e->smem_optin : 232448;
-        for (int part = 0; part <= e->n_tiny; part++) {
-            const fh::SmallSet &S = part == 0 ? e->small_cta : e->small_tiny[part - 1];
-            if (S.n == 0) continue;
-            int threads = 256, smem = S.total * 4;
-            int64_t cap;
-            fh::SmallSet Sx = S;
-            if (part == 0) {   // one copy per warp when 8 fit in 64 KB (fewer CAS retries between warps:
-                               // Combustion's 728-entry level 161 -> 144 us), else one per CTA
-                const bool pw = e->small_warp_copies && 8 * S.total * 4 <= 64 * 1024;
-                Sx.copies = pw ? 8 : 1;
-                smem = Sx.copies * S.total * 4;
-                const int per_sm = 232448 / (smem + 2048);
-                const int mx = pw ? 4 : 2;
-                cap = (int64_t)e->n_sm * (per_sm < 1 ? 1 : per_sm > mx ? mx : per_sm);
-            } else {           // lane-private copies: whole warps per CTA, as many CTAs per SM as fit
-                const int w = (optin - 4096 - smem) / (S.ttotal * 4 * 32);
-                threads = (w > 8 ? 8 : w < 1 ? 1 : w) * 32;
-                smem += threads * S.ttotal * 4;
-                const int per_sm = 232448 / (smem + 2048);   // the SM's shared memory, not the per-CTA opt-in
-                cap = (int64_t)e->n_sm * (per_sm < 1 ? 1 : per_sm > 8 ? 8 : per_sm);
-            }
-            int64_t blocks = (N * S.n + threads - 1) / threads;
-            if (blocks > cap) blocks = cap;
-            const dim3 g((unsigned)blocks);
-            fh_status q = FH_OK;
-            switch (e->F) {
-#define FH_SMALL(FF)                                                                                          \
-    q = cuda_check(cudaFuncSetAttribute(fh::bwd_small_kernel<FF>, cudaFuncAttributeMaxDynamicSharedMemorySize, \
-                                        smem), "cudaFuncSetAttribute(bwd_small)");                           \
-    if (q != FH_OK) return q;                                                                                 \
-    { fh::bwd_small_kernel<FF><<<g, threads, smem, s>>>(e->params, Sx, c4, N, dout, dtable, e->flag, perm); fh::count_launch(); }   \
-    break;
-                case 1: FH_SMALL(1)
-                case 2: FH_SMALL(2)
-                case 4: FH_SMALL(4)
-                default: FH_SMALL(8)
-#undef FH_SMALL
-            }
-        }
+        if ((st = bwd_small_levels(b, perm)) != FH_OK) return st;
         if (ev && n_ev > 0) cudaEventRecord(ev[0], s);
     }
     const int ev0 = e->small.n > 0 ? 1 : 0;
-    // shifted gradient scratch: F <= 2, groups of
-    // shiftable levels, passes that reduce at least about as many corners
-    // as the group has entries (else the merge costs more than it saves)
-    float *gsh_buf = nullptr;
-    bool any_shift = false;
-    for (int l = 0; l < e->L; l++) any_shift |= e->shiftable[l] || e->rep[l];
-    if (any_shift) {
-        uint64_t end = 0;   // the scratch only spans up to the last shiftable level
-        size_t need = 64;   // ... and holds 64 replicated copies of any replicated level
-        for (int l = 0; l < e->L; l++) {
-            if (e->shiftable[l] && e->info[l].offset + e->info[l].table_size > end)
-                end = e->info[l].offset + e->info[l].table_size;
-            if (e->rep[l]) {
-                const size_t stride = (size_t)((e->info[l].table_size + 2) * e->F + 3) / 4 * 4;
-                if (64 * stride * 4 > need) need = 64 * stride * 4;
-            }
-        }
-        if ((size_t)end * e->F * 4 + 64 > need) need = (size_t)end * e->F * 4 + 64;
-        fh_encoder_s::Scratch *sc = get_scratch(e, s, 0, need);
-        if (sc) gsh_buf = sc->gsh;
-    }
+    size_t scratch_bytes = 0;
+    float *scratch = bwd_scratch(e, s, &scratch_bytes);
+    // then one launch group per run of levels (e->gb), its event after it
     for (int k = 0; k < e->n_gb; k++) {
         const int l0 = e->gb[2 * k], lc = e->gb[2 * k + 1] - e->gb[2 * k];
         const dim3 g = grid_for(N, lc);
         if (zero && (st = zero_levels(l0, l0 + lc)) != FH_OK) return st;
-        if (e->kind == 1) {
+        if (e->kind == 1) {   // MHE baseline encoder
             switch (e->F) {
                 case 1: { fh::mhe::bwd_kernel<1><<<g, 256, 0, s>>>(e->params, c4, N, dout, dtable, e->flag, l0, lc); fh::count_launch(); } break;
                 case 2: { fh::mhe::bwd_kernel<2><<<g, 256, 0, s>>>(e->params, c4, N, dout, dtable, e->flag, l0, lc); fh::count_launch(); } break;
@@ -913,81 +983,47 @@ static fh_status encode_bwd_impl(fh_encoder e, const float *coords, int64_t N, c
         }
         fh::LevelList ll;
         ll.n = lc;
-        bool shift = gsh_buf != nullptr;
+        bool shift = scratch != nullptr;
         for (int i = 0; i < lc; i++) {
             ll.id[i] = l0 + i;
             shift &= e->shiftable[l0 + i];
         }
         const uint64_t ge = e->info[l0 + lc - 1].offset + e->info[l0 + lc - 1].table_size - e->info[l0].offset;
-        float *gsh = shift && (double)N * lc * 2.0 >= (double)ge ? gsh_buf : nullptr;
-        // a contended mid-size level (e->rep): a pass of its own into R
-        // replicated copies in the shifted scratch (CTA b -> copy b % R), so
-        // same-address reductions spread over R addresses, then one summing
-        // kernel.  The copies start at the even entry at or below the level's
-        // offset, so the pairs keep their 16-byte alignment.
-        if (lc == 1 && e->rep[l0] && gsh_buf && (double)N * 16.0 >= 4096.0 * (double)e->info[l0].table_size) {
-            const uint64_t T = e->info[l0].table_size, off = e->info[l0].offset, off_al = off & ~1ull;
-            const int64_t stride = (int64_t)((T + (off - off_al) + 1) * e->F + 3) / 4 * 4;   // floats
-            size_t cap = 0;
-            for (auto &sc : e->scratch) if (sc.gsh == gsh_buf) cap = sc.gsh_bytes;
-            int R = (int)(cap / ((size_t)stride * 4));
-            if (R > 64) R = 64;
-            if (R >= 2) {
-                if ((st = cuda_check(cudaMemsetAsync(gsh_buf, 0, (size_t)R * stride * 4, s), "zero replicas")) != FH_OK)
-                    return st;
-                float *base = gsh_buf - (int64_t)off_al * e->F;
-                switch (e->F) {
-                    case 1: { fh::bwd_kernel<1><<<g, 256, 0, s>>>(e->params, c4, N, dout, base, nullptr, e->flag, ll, nullptr, 0, 0, (uint32_t)R, stride); fh::count_launch(); } break;
-                    default: { fh::bwd_kernel<2><<<g, 256, 0, s>>>(e->params, c4, N, dout, base, nullptr, e->flag, ll, nullptr, 0, 0, (uint32_t)R, stride); fh::count_launch(); } break;
+        // the shifted pairs only for passes that reduce at least about as many
+        // corners as the group has entries (else the merge costs more than it saves)
+        float *gsh = shift && (double)N * lc * 2.0 >= (double)ge ? scratch : nullptr;
+        if (lc == 1 && e->rep[l0] && bwd_replicated(b, l0, g, ll, scratch, scratch_bytes, &st)) {
+            if (st != FH_OK) return st;
+        } else {
+            // this group's range of the shifted scratch, zeroed right before use
+            int64_t m0 = (int64_t)e->info[l0].offset * e->F - fh::kShiftFloats;
+            const int64_t m1 =
+                (int64_t)(e->info[l0 + lc - 1].offset + e->info[l0 + lc - 1].table_size) * e->F - fh::kShiftFloats;
+            if (m0 < 0) m0 = 0;
+            if (gsh && (st = cuda_check(cudaMemsetAsync(gsh + m0, 0, (size_t)(m1 - m0) * 4, s), "zero gsh")) != FH_OK)
+                return st;
+            // a single level whose gradients exceed the L2 budget: P passes over
+            // entry ranges of it, each L2-resident.  Measured: Combustion fold-2
+            // shape (F = 2, one 95 MB level) bwd 2.24 -> 2.14 ms; cfg4 (F = 4,
+            // 64 MB levels) 6.05 -> 6.34 ms (the repeated index math and dout
+            // reads cost more than the L2 hits gain at 16 B per corner), so F <= 2.
+            const double gbytes = (double)e->info[l0].table_size * e->F * 4.0;
+            if (lc == 1 && !gsh && e->F <= 2 && e->bwd_split && e->bwd_limit > 0.0 && gbytes > e->bwd_limit) {
+                const int P = (int)std::ceil(gbytes / e->bwd_limit);
+                const uint64_t T = e->info[l0].table_size, off = e->info[l0].offset;
+                for (int q = 0; q < P; q++) {
+                    const uint64_t a = off + T * q / P, c = off + T * (q + 1) / P;
+                    launch_bwd_kernel(b, g, ll, dtable, nullptr, true, (uint32_t)a, (uint32_t)(c - a));
                 }
-                const int64_t cnt = (int64_t)T * e->F;
-                int64_t blocks = (cnt + 255) / 256;
-                if (blocks > (int64_t)e->n_sm * 4) blocks = (int64_t)e->n_sm * 4;
-                { fh::rep_reduce_kernel<<<(unsigned)blocks, 256, 0, s>>>(dtable + off * e->F, gsh_buf + (off - off_al) * e->F,
-                                                                         R, stride, cnt); fh::count_launch(); }
-                if (ev && ev0 + k < n_ev) cudaEventRecord(ev[ev0 + k], s);
-                continue;
-            }
-        }
-        // this group's range of the shifted scratch, zeroed right before use
-        int64_t m0 = (int64_t)e->info[l0].offset * e->F - fh::kShiftFloats;
-        const int64_t m1 = (int64_t)(e->info[l0 + lc - 1].offset + e->info[l0 + lc - 1].table_size) * e->F - fh::kShiftFloats;
-        if (m0 < 0) m0 = 0;
-        if (gsh && (st = cuda_check(cudaMemsetAsync(gsh + m0, 0, (size_t)(m1 - m0) * 4, s), "zero gsh")) != FH_OK)
-            return st;
-        // a single level whose gradients exceed the L2 budget: P passes over
-        // entry ranges of it, each L2-resident.  Measured: Combustion fold-2
-        // shape (F = 2, one 95 MB level) bwd 2.24 -> 2.14 ms; cfg4 (F = 4,
-        // 64 MB levels) 6.05 -> 6.34 ms (the repeated index math and dout
-        // reads cost more than the L2 hits gain at 16 B per corner), so F <= 2.
-        const double gbytes = (double)e->info[l0].table_size * e->F * 4.0;
-        if (lc == 1 && !gsh && e->F <= 2 && e->bwd_split && e->bwd_limit > 0.0 && gbytes > e->bwd_limit) {
-            const int P = (int)std::ceil(gbytes / e->bwd_limit);
-            const uint64_t T = e->info[l0].table_size, off = e->info[l0].offset;
-            for (int q = 0; q < P; q++) {
-                const uint64_t a = off + T * q / P, b = off + T * (q + 1) / P;
-                const uint32_t lo = (uint32_t)a, span = (uint32_t)(b - a);
-                switch (e->F) {
-                    case 1: { fh::bwd_kernel<1, true><<<g, 256, 0, s>>>(e->params, c4, N, dout, dtable, nullptr, e->flag, ll, nullptr, lo, span); fh::count_launch(); } break;
-                    case 2: { fh::bwd_kernel<2, true><<<g, 256, 0, s>>>(e->params, c4, N, dout, dtable, nullptr, e->flag, ll, nullptr, lo, span); fh::count_launch(); } break;
-                    case 4: { fh::bwd_kernel<4, true><<<g, 256, 0, s>>>(e->params, c4, N, dout, dtable, nullptr, e->flag, ll, nullptr, lo, span); fh::count_launch(); } break;
-                    default: { fh::bwd_kernel<8, true><<<g, 256, 0, s>>>(e->params, c4, N, dout, dtable, nullptr, e->flag, ll, nullptr, lo, span); fh::count_launch(); } break;
+            } else {
+                launch_bwd_kernel(b, g, ll, dtable, gsh, false);
+                if (gsh) {   // fold this group's shifted partial sums back into dtable
+                    const int64_t q = (m1 - m0 + 1) / 2;
+                    int64_t blocks = (q + 255) / 256;
+                    if (blocks > (int64_t)e->n_sm * 8) blocks = (int64_t)e->n_sm * 8;
+                    if (blocks > 0) { fh::merge_shift_kernel<<<(unsigned)blocks, 256, 0, s>>>(dtable, gsh, m0, m1); fh::count_launch(); }
                 }
             }
-            if (ev && ev0 + k < n_ev) cudaEventRecord(ev[ev0 + k], s);
-            continue;
-        }
-        switch (e->F) {
-            case 1: { fh::bwd_kernel<1><<<g, 256, 0, s>>>(e->params, c4, N, dout, dtable, gsh, e->flag, ll, nullptr); fh::count_launch(); } break;
-            case 2: { fh::bwd_kernel<2><<<g, 256, 0, s>>>(e->params, c4, N, dout, dtable, gsh, e->flag, ll, nullptr); fh::count_launch(); } break;
-            case 4: { fh::bwd_kernel<4><<<g, 256, 0, s>>>(e->params, c4, N, dout, dtable, nullptr, e->flag, ll, nullptr); fh::count_launch(); } break;
-            default: { fh::bwd_kernel<8><<<g, 256, 0, s>>>(e->params, c4, N, dout, dtable, nullptr, e->flag, ll, nullptr); fh::count_launch(); } break;
-        }
-        if (gsh) {   // fold this group's shifted partial sums back into dtable
-            const int64_t q = (m1 - m0 + 1) / 2;
-            int64_t blocks = (q + 255) / 256;
-            if (blocks > (int64_t)e->n_sm * 8) blocks = (int64_t)e->n_sm * 8;
-            if (blocks > 0) { fh::merge_shift_kernel<<<(unsigned)blocks, 256, 0, s>>>(dtable, gsh, m0, m1); fh::count_launch(); }
         }
         if (ev && ev0 + k < n_ev) cudaEventRecord(ev[ev0 + k], s);
     }
