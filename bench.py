@@ -301,6 +301,10 @@ def microbench_roofline(fh, torch, enc, cfg, N, stream, hbm_peak):
         "model": "level-mix microbenchmark (fh_bench_gather_levels / fh_bench_red_levels) + streamed bytes at the "
                  "measured copy bandwidth",
         "t_roof_per_level_sum_fwd_ms": t_fwd_lv * 1e3, "t_roof_per_level_sum_bwd_ms": t_bwd_lv * 1e3,
+        # SURVEY §8(d) "expected counts": each x-pair as two entry-wide accesses (the
+        # naive shape, per-level rates) -- the pair layout of DESIGN.md §8.1 beats it
+        "t_roof_expected_fwd_ms": (sum(N * 16 / g for g in g_split) + stream_fwd / bw_copy) * 1e3,
+        "t_roof_expected_bwd_ms": (sum(N * 16 / r for r in r_split) + stream_bwd / bw_copy) * 1e3,
         "mix_gather_corner_rate_G_per_s": round(N * cfg.L * 16 / tg_mix / 1e9, 2),
         "mix_red_corner_rate_G_per_s": round(N * cfg.L * 16 / tr_mix / 1e9, 2),
         "copy_gbs": bw_copy / 1e9, "hbm_peak_gbs": hbm_peak,
@@ -800,6 +804,7 @@ def run_ours(args, rank, local_rank, world):
         "bound": "l2-gather/red (measured microbenchmark, same access shape, per-level footprint)",
         "t_roof_ms": t_roof, "t_measured_ms": fwd_ms + bwd_ms,
         "frac": t_roof / (fwd_ms + bwd_ms),
+        "frac_expected_counts": (mb["t_roof_expected_fwd_ms"] + mb["t_roof_expected_bwd_ms"]) / (fwd_ms + bwd_ms),
         "fwd_frac": mb["t_roof_fwd_ms"] / fwd_ms, "bwd_frac": mb["t_roof_bwd_ms"] / bwd_ms, **mb,
     }
     cpu = None
