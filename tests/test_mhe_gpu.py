@@ -59,3 +59,19 @@ def test_mhe_paper_sized_encoder_adjoint():
     lhs = torch.sum(g.double() * out.double()).item()
     rhs = torch.sum(dt.double() * t.double()).item()
     assert abs(lhs - rhs) <= 1e-5 * torch.sum(g.double().abs() * out.double().abs()).item()
+
+
+def test_mhe_backward_overwrite():
+    """fh_encode_bwd_ex(FH_BWD_OVERWRITE) on an MHE encoder: the dtable held
+    garbage, the result equals the oracle's gradient."""
+    res, T, n, F = [8, 16, 40], 4096, 4, 2
+    g = W.rng(5)
+    enc = fh.MHEEncoder(res, F, T, n, "f32")
+    ref = oracle.MHELevels(res, n, T)
+    coords = W.draw_coords(g, 3001).astype(np.float32)
+    dout = W.draw_grads(g, 3001, len(res) * F)
+    dt = torch.full((enc.entries, F), 9.0, device="cuda")
+    enc.bwd(dev(coords), dev(dout), dt, overwrite=True)
+    assert enc.status_sync() == fh.FH_OK
+    G, A = ref.backward(coords, dout, F, want_abs=True)
+    check_bwd(dt.cpu().numpy().astype(np.float64), G, A)
