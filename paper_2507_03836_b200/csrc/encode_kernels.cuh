@@ -480,6 +480,34 @@ __device__ __forceinline__ void red_pair(float *dtable, float *gsh, uint32_t i0,
     red_entry<F>(dtable, i1, v1);
 }
 
+// dtable[m + 2] += gsh[m] over float range [m0, m1) of the shifted scratch
+// (m0 even), by threads t0, t0 + nt, ...: the merge of the pair layout
+// (merge_shift_kernel, or the first CTAs of the next group's bwd_kernel).
+__device__ __forceinline__ void merge_shift_range(float *__restrict__ dtable, float *__restrict__ gsh, int64_t m0,
+                                                  int64_t m1, int64_t t0, int64_t nt) {
+    const int64_t q0 = m0 >> 1, q1 = (m1 + 1) >> 1;
+    float2 *g2 = reinterpret_cast<float2 *>(gsh);
+    float2 *d2 = reinterpret_cast<float2 *>(dtable) + 1;
+    for (int64_t q = q0 + t0; q < q1; q += nt) {
+        const float2 v = g2[q];
+        if (v.x != 0.f || v.y != 0.f) {
+            float2 d = d2[q];
+            d.x += v.x;
+            d.y += v.y;
+            d2[q] = d;
+        }
+    }
+}
+
+// A merge carried by the first `ctas` CTAs of a backward launch: the
+// previous level group's shifted partial sums, folded while this group's
+// reductions run (its ranges are disjoint from this group's).
+struct MergeJob {
+    float *gsh;
+    int64_t m0, m1;
+    int ctas;
+};
+
 // RANGED: only corners whose entry lies in [lo, lo + span) are reduced --
 // one of several passes over a level whose gradients exceed the L2 budget,
 // each pass's range staying L2-resident (the index math and dout are
@@ -491,14 +519,21 @@ __global__ void __launch_bounds__(256) bwd_kernel(const __grid_constant__ Params
                                                   float *__restrict__ gsh,
                                                   int *__restrict__ flag, const __grid_constant__ LevelList LL,
                                                   const uint32_t *__restrict__ perm, uint32_t lo = 0,
-                                                  uint32_t span = 0, uint32_t rep_n = 0, int64_t rep_stride = 0) {
+                                                  uint32_t span = 0, uint32_t rep_n = 0, int64_t rep_stride = 0,
+                                                  const MergeJob mj = MergeJob{nullptr, 0, 0, 0}) {
+    if ((int)blockIdx.x < mj.ctas) {   // the previous group's merge (see MergeJob)
+        merge_shift_range(dtable, mj.gsh, mj.m0, mj.m1, (int64_t)blockIdx.x * blockDim.x + threadIdx.x,
+                          (int64_t)mj.ctas * blockDim.x);
+        return;
+    }
     __shared__ LevelSmem slv;
     load_levels(P, slv);
     const int L = P.L;
     const int lc = LL.n;
-    const int64_t gid = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+    const int64_t bid = (int64_t)blockIdx.x - mj.ctas;
+    const int64_t gid = bid * blockDim.x + threadIdx.x;
     // replicated pass (one contended level): CTA b reduces into copy b % rep_n
-    if (rep_n > 1) dtable += (int64_t)(blockIdx.x % rep_n) * rep_stride;
+    if (rep_n > 1) dtable += (int64_t)(bid % rep_n) * rep_stride;
     const int64_t j = gid / lc;
     if (j >= N) return;
     const int li = (int)(gid - j * lc);
@@ -559,18 +594,8 @@ constexpr int kShiftFloats = 2;
 
 __global__ void __launch_bounds__(256) merge_shift_kernel(float *__restrict__ dtable, float *__restrict__ gsh,
                                                           int64_t m0, int64_t m1) {
-    const int64_t q0 = m0 >> 1, q1 = (m1 + 1) >> 1;
-    float2 *g2 = reinterpret_cast<float2 *>(gsh);
-    float2 *d2 = reinterpret_cast<float2 *>(dtable) + 1;
-    for (int64_t q = q0 + (int64_t)blockIdx.x * blockDim.x + threadIdx.x; q < q1; q += (int64_t)gridDim.x * blockDim.x) {
-        const float2 v = g2[q];
-        if (v.x != 0.f || v.y != 0.f) {
-            float2 d = d2[q];
-            d.x += v.x;
-            d.y += v.y;
-            d2[q] = d;
-        }
-    }
+    merge_shift_range(dtable, gsh, m0, m1, (int64_t)blockIdx.x * blockDim.x + threadIdx.x,
+                      (int64_t)gridDim.x * blockDim.x);
 }
 
 // Sum of the replicated copies of one level into dtable (the replicated

@@ -70,6 +70,7 @@ static fh_status ensure_flag(fh_encoder e) {
     if (const char *v = getenv("FH_AGG_MIN_DENSITY")) e->agg_density = atof(v);
     if (const char *v = getenv("FH_PAIR_SHIFT")) e->pair_shift = atoi(v);
     if (const char *v = getenv("FH_BWD_SPLIT")) e->bwd_split = atoi(v) != 0;
+    if (const char *v = getenv("FH_FUSE_MERGE")) e->fuse_merge = atoi(v) != 0;
     if (const char *v = getenv("FH_SMALL_WARP")) e->small_warp_copies = atoi(v) != 0;
     e->fwd_limit = budget("FH_FWD_GROUP_MB", 0.55);
     // backward: 0.45 L2 (measured with the shifted gradient scratch, whose
@@ -812,11 +813,13 @@ struct BwdCall {
 
 // bwd_kernel<F, RANGED> for the encoder's F (gsh only for F <= 2).
 static void launch_bwd_kernel(const BwdCall &b, dim3 g, const fh::LevelList &ll, float *dt, float *gsh, bool ranged,
-                              uint32_t lo = 0, uint32_t span = 0, uint32_t rep_n = 0, int64_t rep_stride = 0) {
+                              uint32_t lo = 0, uint32_t span = 0, uint32_t rep_n = 0, int64_t rep_stride = 0,
+                              fh::MergeJob mj = fh::MergeJob{nullptr, 0, 0, 0}) {
     const fh_encoder e = b.e;
+    g.x += (unsigned)mj.ctas;   // the merge CTAs come first (blockIdx < mj.ctas)
 #define FH_BWD(FF, RR, GG)                                                                                     \
     { fh::bwd_kernel<FF, RR><<<g, 256, 0, b.s>>>(e->params, b.c4, b.N, b.dout, dt, GG, e->flag, ll, nullptr, lo, span, \
-                                                 rep_n, rep_stride); fh::count_launch(); }
+                                                 rep_n, rep_stride, mj); fh::count_launch(); }
     switch (e->F) {
         case 1: if (ranged) FH_BWD(1, true, gsh) else FH_BWD(1, false, gsh) break;
         case 2: if (ranged) FH_BWD(2, true, gsh) else FH_BWD(2, false, gsh) break;
@@ -967,18 +970,40 @@ static fh_status encode_bwd_impl(fh_encoder e, const float *coords, int64_t N, c
     const int ev0 = e->small.n > 0 ? 1 : 0;
     size_t scratch_bytes = 0;
     float *scratch = bwd_scratch(e, s, &scratch_bytes);
-    // then one launch group per run of levels (e->gb), its event after it
+    auto record = [&](int k) {
+        if (ev && ev0 + k < n_ev) cudaEventRecord(ev[ev0 + k], s);
+    };
+    // A group's merge of the shifted scratch is carried by the next group's
+    // backward launch (its first CTAs, while that group's reductions run);
+    // the group's event follows the launch that completes it.  A pending
+    // merge before any other kind of launch, or at the end, runs on its own.
+    struct Pending { bool on; float *gsh; int64_t m0, m1; int k; } pend{false, nullptr, 0, 0, 0};
+    auto merge_blocks = [&](int64_t m0, int64_t m1) {
+        int64_t blocks = ((m1 - m0 + 1) / 2 + 255) / 256;
+        if (blocks > (int64_t)e->n_sm * 8) blocks = (int64_t)e->n_sm * 8;
+        return blocks;
+    };
+    auto flush = [&]() {
+        if (!pend.on) return;
+        const int64_t blocks = merge_blocks(pend.m0, pend.m1);
+        if (blocks > 0) { fh::merge_shift_kernel<<<(unsigned)blocks, 256, 0, s>>>(dtable, pend.gsh, pend.m0, pend.m1); fh::count_launch(); }
+        record(pend.k);
+        pend.on = false;
+    };
+    // then one launch group per run of levels (e->gb)
     for (int k = 0; k < e->n_gb; k++) {
         const int l0 = e->gb[2 * k], lc = e->gb[2 * k + 1] - e->gb[2 * k];
         const dim3 g = grid_for(N, lc);
         if (zero && (st = zero_levels(l0, l0 + lc)) != FH_OK) return st;
         if (e->kind == 1) {   // MHE baseline encoder
+            flush();
             switch (e->F) {
                 case 1: { fh::mhe::bwd_kernel<1><<<g, 256, 0, s>>>(e->params, c4, N, dout, dtable, e->flag, l0, lc); fh::count_launch(); } break;
                 case 2: { fh::mhe::bwd_kernel<2><<<g, 256, 0, s>>>(e->params, c4, N, dout, dtable, e->flag, l0, lc); fh::count_launch(); } break;
                 case 4: { fh::mhe::bwd_kernel<4><<<g, 256, 0, s>>>(e->params, c4, N, dout, dtable, e->flag, l0, lc); fh::count_launch(); } break;
                 default: { fh::mhe::bwd_kernel<8><<<g, 256, 0, s>>>(e->params, c4, N, dout, dtable, e->flag, l0, lc); fh::count_launch(); } break;
             }
+            record(k);
             continue;
         }
         fh::LevelList ll;
@@ -992,41 +1017,54 @@ static fh_status encode_bwd_impl(fh_encoder e, const float *coords, int64_t N, c
         // the shifted pairs only for passes that reduce at least about as many
         // corners as the group has entries (else the merge costs more than it saves)
         float *gsh = shift && (double)N * lc * 2.0 >= (double)ge ? scratch : nullptr;
-        if (lc == 1 && e->rep[l0] && bwd_replicated(b, l0, g, ll, scratch, scratch_bytes, &st)) {
-            if (st != FH_OK) return st;
-        } else {
-            // this group's range of the shifted scratch, zeroed right before use
-            int64_t m0 = (int64_t)e->info[l0].offset * e->F - fh::kShiftFloats;
-            const int64_t m1 =
-                (int64_t)(e->info[l0 + lc - 1].offset + e->info[l0 + lc - 1].table_size) * e->F - fh::kShiftFloats;
-            if (m0 < 0) m0 = 0;
-            if (gsh && (st = cuda_check(cudaMemsetAsync(gsh + m0, 0, (size_t)(m1 - m0) * 4, s), "zero gsh")) != FH_OK)
-                return st;
-            // a single level whose gradients exceed the L2 budget: P passes over
-            // entry ranges of it, each L2-resident.  Measured: Combustion fold-2
-            // shape (F = 2, one 95 MB level) bwd 2.24 -> 2.14 ms; cfg4 (F = 4,
-            // 64 MB levels) 6.05 -> 6.34 ms (the repeated index math and dout
-            // reads cost more than the L2 hits gain at 16 B per corner), so F <= 2.
-            const double gbytes = (double)e->info[l0].table_size * e->F * 4.0;
-            if (lc == 1 && !gsh && e->F <= 2 && e->bwd_split && e->bwd_limit > 0.0 && gbytes > e->bwd_limit) {
-                const int P = (int)std::ceil(gbytes / e->bwd_limit);
-                const uint64_t T = e->info[l0].table_size, off = e->info[l0].offset;
-                for (int q = 0; q < P; q++) {
-                    const uint64_t a = off + T * q / P, c = off + T * (q + 1) / P;
-                    launch_bwd_kernel(b, g, ll, dtable, nullptr, true, (uint32_t)a, (uint32_t)(c - a));
-                }
-            } else {
-                launch_bwd_kernel(b, g, ll, dtable, gsh, false);
-                if (gsh) {   // fold this group's shifted partial sums back into dtable
-                    const int64_t q = (m1 - m0 + 1) / 2;
-                    int64_t blocks = (q + 255) / 256;
-                    if (blocks > (int64_t)e->n_sm * 8) blocks = (int64_t)e->n_sm * 8;
-                    if (blocks > 0) { fh::merge_shift_kernel<<<(unsigned)blocks, 256, 0, s>>>(dtable, gsh, m0, m1); fh::count_launch(); }
-                }
+        if (lc == 1 && e->rep[l0]) {
+            flush();   // the replicated copies live in the same scratch
+            if (bwd_replicated(b, l0, g, ll, scratch, scratch_bytes, &st)) {
+                if (st != FH_OK) return st;
+                record(k);
+                continue;
             }
         }
-        if (ev && ev0 + k < n_ev) cudaEventRecord(ev[ev0 + k], s);
+        // this group's range of the shifted scratch, zeroed right before use
+        int64_t m0 = (int64_t)e->info[l0].offset * e->F - fh::kShiftFloats;
+        const int64_t m1 =
+            (int64_t)(e->info[l0 + lc - 1].offset + e->info[l0 + lc - 1].table_size) * e->F - fh::kShiftFloats;
+        if (m0 < 0) m0 = 0;
+        if (gsh && (st = cuda_check(cudaMemsetAsync(gsh + m0, 0, (size_t)(m1 - m0) * 4, s), "zero gsh")) != FH_OK)
+            return st;
+        // a single level whose gradients exceed the L2 budget: P passes over
+        // entry ranges of it, each L2-resident.  Measured: Combustion fold-2
+        // shape (F = 2, one 95 MB level) bwd 2.24 -> 2.14 ms; cfg4 (F = 4,
+        // 64 MB levels) 6.05 -> 6.34 ms (the repeated index math and dout
+        // reads cost more than the L2 hits gain at 16 B per corner), so F <= 2.
+        const double gbytes = (double)e->info[l0].table_size * e->F * 4.0;
+        if (lc == 1 && !gsh && e->F <= 2 && e->bwd_split && e->bwd_limit > 0.0 && gbytes > e->bwd_limit) {
+            flush();
+            const int P = (int)std::ceil(gbytes / e->bwd_limit);
+            const uint64_t T = e->info[l0].table_size, off = e->info[l0].offset;
+            for (int q = 0; q < P; q++) {
+                const uint64_t a = off + T * q / P, c = off + T * (q + 1) / P;
+                launch_bwd_kernel(b, g, ll, dtable, nullptr, true, (uint32_t)a, (uint32_t)(c - a));
+            }
+            record(k);
+            continue;
+        }
+        fh::MergeJob mj{nullptr, 0, 0, 0};
+        if (pend.on && e->fuse_merge) {
+            const int64_t blocks = merge_blocks(pend.m0, pend.m1);
+            mj = fh::MergeJob{pend.gsh, pend.m0, pend.m1, (int)(blocks < 2 * e->n_sm ? blocks : 2 * e->n_sm)};
+        } else {
+            flush();
+        }
+        launch_bwd_kernel(b, g, ll, dtable, gsh, false, 0, 0, 0, 0, mj);
+        if (mj.ctas > 0) {
+            record(pend.k);
+            pend.on = false;
+        }
+        if (gsh) pend = Pending{true, gsh, m0, m1, k};
+        else record(k);
     }
+    flush();
     return cuda_check(cudaGetLastError(), "fh_encode_bwd launch");
 }
 

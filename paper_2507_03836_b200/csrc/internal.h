@@ -65,6 +65,7 @@ struct fh_encoder_s {
     int n_tiny = 0;
     bool small_warp_copies = true;                   // FH_SMALL_WARP=0: one CTA copy instead of per-warp copies
     bool rep[FH_MAX_LEVELS] = {false};               // backward: level reduced into replicated copies (own pass)
+    bool fuse_merge = true;                          // FH_FUSE_MERGE=0: every group's merge as its own launch
     double fwd_limit = 0.0, bwd_limit = 0.0;         // L2 budgets of one direct pass (bytes; 0 = one pass)
     fh::KeySpec key{};                               // Morton key of fh_spatial_sort (set by the builder)
     int n_sm = 148;                                  // SMs of the device (set with the status word)
