@@ -367,7 +367,9 @@ fh_status fh_train_apply_sharded(fh_trainer tr, int64_t begin, int64_t end, cons
  *   launch i finalises (k < *n_ranges); FH_E_RANGE if more than max_ranges.
  * fh_train_set_bwd_events: from now on fh_train_fwd_bwd records events[i]
  *   (caller-owned cudaEvent_t, created by the caller) on its stream right
- *   after backward launch i; n = fh_train_bwd_launches, or 0 to stop.
+ *   after the launch that completes backward group i (a group's last step,
+ *   the merge of the shifted scratch, may ride in the next group's launch);
+ *   n = fh_train_bwd_launches, or 0 to stop.
  * fh_train_apply_ranges: one Adam step (step counter += 1) over the table
  *   element ranges [begin_i, end_i) (disjoint) reading grad_i[0 .. end_i -
  *   begin_i) (device f32, e.g. this rank's reduce-scattered chunks), plus the
