@@ -11,7 +11,7 @@ grads + deterministic Adam keep the replicas bit-identical.
 """
 from __future__ import annotations
 
-from typing import Optional, Tuple
+from typing import Tuple
 
 
 def shard(n_global: int, rank: int, world: int) -> Tuple[int, int]:

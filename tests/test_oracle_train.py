@@ -1,6 +1,5 @@
 """Pins for Oracle-T (oracle/train.py): MLP, MSE, Adam.  CPU only."""
 import numpy as np
-import pytest
 import torch
 
 from oracle import train as T

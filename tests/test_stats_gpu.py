@@ -3,7 +3,6 @@
 exhaustive Oracle-S (oracle.Levels.level_stats, MHELevels.level_stats):
 distinct buckets, collisions and utilisation must agree EXACTLY (integer
 work).  -m gpu."""
-import numpy as np
 import pytest
 import torch
 
