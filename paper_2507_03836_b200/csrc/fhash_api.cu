@@ -27,6 +27,7 @@ using fh::g_err;
 
 // Make sure the encoder's status word exists on the current device.
 static fh_status ensure_flag(fh_encoder e) {
+    std::lock_guard<std::mutex> lock(e->mu);
     int dev = -1;
     if (cudaGetDevice(&dev) != cudaSuccess) return fail(FH_E_CUDA, "cudaGetDevice failed");
     if (e->flag) {
@@ -199,6 +200,7 @@ static fh_status ensure_flag(fh_encoder e) {
 // gsh), allocated on first use; nullptr when no slot is free or the stream
 // is capturing a graph (the caller then runs without the shifted pairs).
 static fh_encoder_s::Scratch *get_scratch(fh_encoder e, cudaStream_t s, size_t tsh_bytes, size_t gsh_bytes) {
+    std::lock_guard<std::mutex> lock(e->mu);
     fh_encoder_s::Scratch *slot = nullptr;
     for (auto &sc : e->scratch)
         if (sc.stream == (void *)s && (sc.tsh || sc.gsh)) { slot = &sc; break; }
@@ -715,6 +717,7 @@ fh_status fh_encoder_attach_scratch(fh_encoder e, fh_stream stream, void *ptr, s
     if (e->kind != 0) return fail(FH_E_ARG, "fh_encoder_attach_scratch: MHE encoders use no scratch");
     fh_status st = ensure_flag(e);
     if (st != FH_OK) return st;
+    std::lock_guard<std::mutex> lock(e->mu);
     void *s = stream;
     fh_encoder_s::Scratch *slot = nullptr;
     for (auto &sc : e->scratch)

@@ -1,6 +1,7 @@
 // internal.h -- shared host-side internals of libfhash.so (not part of the ABI).
 #pragma once
 #include <atomic>
+#include <mutex>
 #include <cuda_runtime.h>
 
 #include <cstdarg>
@@ -91,6 +92,8 @@ struct fh_encoder_s {
     static constexpr int kScratchSlots = 8;
     Scratch scratch[kScratchSlots];
     int pair_shift = 3;                              // FH_PAIR_SHIFT bits: 1 backward, 2 forward (default both)
+    std::mutex mu;                                   // guards the lazy device state (status word, scratch slots)
+                                                     // against host threads sharing the encoder
     bool shiftable[FH_MAX_LEVELS] = {false};         // backward: level uses the shifted gradient pairs
     bool bwd_split = true;                           // FH_BWD_SPLIT=0: no entry-range passes for big levels
 };

@@ -655,3 +655,42 @@ def test_backward_replicated_pass(rep, monkeypatch):
     assert st == fh.FH_OK
     G, A = ref.backward(case.coords, case.dout, 2, want_abs=True)
     check_bwd(got, G, A)
+
+
+def test_host_threads_share_one_encoder():
+    """Two host threads drive one encoder on their own streams at the same
+    time (ctypes releases the GIL): the lazy per-stream scratch set-up is
+    serialised by the encoder's lock; both results equal the oracle."""
+    import threading
+    cfg = W.CFG1H
+    enc = fh.Encoder(cfg.levels, cfg.F, cfg.table_dtype, cfg.cap)
+    ref = oracle.Levels(cfg.levels, cfg.cap)
+    cases = [W.encode_case(cfg, 30000 + k, seed=60 + k) for k in range(2)]
+    results, errors = [None, None], []
+
+    def run(k):
+        try:
+            st = torch.cuda.Stream()
+            case = cases[k]
+            with torch.cuda.stream(st):
+                c, t, g = dev(case.coords), dev(case.table), dev(case.dout)
+                o = enc.fwd(c, t, stream=st)
+                d = torch.zeros((enc.entries, cfg.F), device="cuda")
+                enc.bwd(c, g, d, stream=st, overwrite=True)
+            st.synchronize()
+            results[k] = (o.cpu().numpy().astype(np.float64), d.cpu().numpy().astype(np.float64))
+        except Exception as ex:   # surfaced below
+            errors.append(ex)
+
+    threads = [threading.Thread(target=run, args=(k,)) for k in range(2)]
+    for th in threads:
+        th.start()
+    for th in threads:
+        th.join()
+    assert not errors, errors
+    assert enc.status_sync() == fh.FH_OK
+    for case, (o, d) in zip(cases, results):
+        r, ab = ref.forward(case.coords, case.table, want_abs=True)
+        check_fwd(o, r, ab)
+        G, A = ref.backward(case.coords, case.dout, cfg.F, want_abs=True)
+        check_bwd(d, G, A)
