@@ -548,14 +548,15 @@ def test_step_host_end_to_end():
     check_bwd(dt_h.numpy().astype(np.float64), G, A)
 
 
+@pytest.mark.parametrize("F", [1, 2])
 @pytest.mark.parametrize("split", ["0", "1"])
-def test_backward_entry_range_passes(split, monkeypatch):
+def test_backward_entry_range_passes(split, F, monkeypatch):
     """A level whose gradients exceed the backward group budget is reduced
     in entry-range passes (FH_BWD_SPLIT, default on for F <= 2): forced with
     a tiny budget (FH_BWD_GROUP_MB) on cfg1h, results equal the oracle."""
     monkeypatch.setenv("FH_BWD_SPLIT", split)
     monkeypatch.setenv("FH_BWD_GROUP_MB", "0.02")   # 20 KB: every level alone, the big ones split
-    cfg = W.CFG1H
+    cfg = W.EncoderConfig("split", W.CFG1H.levels, F=F, cap=W.CFG1H.cap, table_dtype="f32")
     case = W.encode_case(cfg, 6000 + 3, seed=17)
     enc = fh.Encoder(cfg.levels, cfg.F, cfg.table_dtype, cfg.cap)
     ref = oracle.Levels(cfg.levels, cfg.cap)
@@ -639,21 +640,22 @@ def test_caller_owned_scratch():
         mhe.attach_scratch(buf, st)
 
 
+@pytest.mark.parametrize("F", [1, 2])
 @pytest.mark.parametrize("rep", ["0", "8191"])
-def test_backward_replicated_pass(rep, monkeypatch):
+def test_backward_replicated_pass(rep, F, monkeypatch):
     """A contended mid-size level (< 8192 entries, >= 4096 updates per entry)
     is reduced in a pass of its own into 64 replicated copies summed
     afterwards (FH_REP_MAX_T; 0 disables): equal to the oracle, odd level
     offset included (the copies keep the pairs' 16-byte alignment)."""
     monkeypatch.setenv("FH_REP_MAX_T", rep)
     levels = [(3, 3, 3, 3), (9, 8, 5, 3)]           # offset of level 1 = 81 (odd), T = 1080
-    cfg = W.EncoderConfig("rep", tuple(levels), F=2, cap=0, table_dtype="f32")
+    cfg = W.EncoderConfig("rep", tuple(levels), F=F, cap=0, table_dtype="f32")
     case = W.encode_case(cfg, 300000, seed=31)
-    enc = fh.Encoder(levels, 2)
+    enc = fh.Encoder(levels, F)
     ref = oracle.Levels(levels)
     got, st = run_bwd(enc, case)
     assert st == fh.FH_OK
-    G, A = ref.backward(case.coords, case.dout, 2, want_abs=True)
+    G, A = ref.backward(case.coords, case.dout, F, want_abs=True)
     check_bwd(got, G, A)
 
 
