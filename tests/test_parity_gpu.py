@@ -696,3 +696,21 @@ def test_host_threads_share_one_encoder():
         check_fwd(o, r, ab)
         G, A = ref.backward(case.coords, case.dout, cfg.F, want_abs=True)
         check_bwd(d, G, A)
+
+
+@pytest.mark.parametrize("F", [1, 2, 4, 8])
+def test_few_cell_levels_backward(F):
+    """The coarse end of a fold schedule (the Combustion fold-2 tail: 728,
+    112, 32 and 16 entries) in the shared-memory backward paths -- CTA /
+    per-warp copies and one lane-private launch per tiny level -- for every
+    F; equal to the oracle at a batch large enough that every entry takes
+    thousands of contributions."""
+    levels = [(13, 7, 4, 2), (7, 4, 2, 2), (4, 2, 2, 2), (2, 2, 2, 2)]
+    cfg = W.EncoderConfig("tail", tuple(levels), F=F, cap=0, table_dtype="f32")
+    case = W.encode_case(cfg, 200000, seed=44)
+    enc = fh.Encoder(levels, F)
+    ref = oracle.Levels(levels)
+    got, st = run_bwd(enc, case)
+    assert st == fh.FH_OK
+    G, A = ref.backward(case.coords, case.dout, F, want_abs=True)
+    check_bwd(got, G, A)
