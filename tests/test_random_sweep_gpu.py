@@ -57,3 +57,38 @@ def test_random_encoder_parity(seed):
         assert np.all(gb[A == 0] == 0)
         assert np.all(np.abs(gb - G) <= 1e-5 * A)
     assert enc.status_sync() == fh.FH_OK
+
+
+def random_large_case(seed):
+    """Larger batches than random_case, so the N-dependent backward paths
+    (shifted gradient pairs, replicated copies of contended levels, the
+    few-cell shared-memory levels, the fused merges between level groups)
+    all take part; coarse levels included on purpose."""
+    g = np.random.default_rng(5000 + seed)
+    L = int(g.integers(2, 9))
+    lv = [tuple(int(r) for r in g.integers(2, 6, 4)) for _ in range(L // 2)]          # few-cell levels
+    lv += [tuple(int(r) for r in g.integers(6, 41, 4)) for _ in range(L - L // 2)]   # larger / capped levels
+    order = g.permutation(L)
+    levels = tuple(lv[i] for i in order)
+    F = int(g.choice([1, 2, 4]))
+    cap = int(g.choice([0, 1 << 11, 1 << 14]))
+    N = int(g.integers(100000, 300000))
+    return W.EncoderConfig(f"R{seed}", levels, F=F, cap=cap, table_dtype="f32"), N
+
+
+@pytest.mark.parametrize("seed", range(16))
+def test_random_large_batch_backward(seed):
+    cfg, N = random_large_case(seed)
+    case = W.encode_case(cfg, N, seed=seed)
+    enc = fh.Encoder(cfg.levels, cfg.F, cfg.table_dtype, cfg.cap)
+    ref = oracle.Levels(cfg.levels, cfg.cap)
+    c = torch.from_numpy(case.coords).cuda()
+    g = torch.from_numpy(case.dout).cuda()
+    G, A = ref.backward(case.coords, case.dout, cfg.F, want_abs=True)
+    for overwrite in (False, True):
+        dt = torch.full((enc.entries, cfg.F), 0.0 if not overwrite else 7.0, device="cuda")
+        enc.bwd(c, g, dt, overwrite=overwrite)
+        gb = dt.cpu().numpy().astype(np.float64)
+        assert np.all(gb[A == 0] == 0)
+        assert np.all(np.abs(gb - G) <= 1e-5 * A)
+    assert enc.status_sync() == fh.FH_OK
