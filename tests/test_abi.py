@@ -125,6 +125,15 @@ def test_encode_argument_errors_are_host_side():
     assert b"NULL" in L.fh_last_error()
     # N = 0 is a no-op
     assert L.fh_encode_fwd(enc.handle, 16, 0, 16, 16, 0, None) == fh.FH_OK
+    # fh_encode_bwd_ex: unknown flags, misaligned dout
+    assert L.fh_encode_bwd_ex(enc.handle, 16, 10, 16, 16, 0x80, None) == fh.FH_E_ARG
+    assert L.fh_encode_bwd_ex(enc.handle, 16, 10, 4, 16, 1, None) == fh.FH_E_ARG
+    # fh_level_stats: NULL pointers, level out of range, workspace query
+    assert L.fh_level_stats(enc.handle, 0, None, 0, None, None) == fh.FH_E_ARG
+    assert L.fh_level_stats(enc.handle, 99, 256, 1 << 20, 256, None) == fh.FH_E_ARG
+    assert L.fh_level_stats_workspace_size(enc.handle, 0) >= (128 + 31) // 32 * 4
+    assert L.fh_level_stats_workspace_size(enc.handle, 99) == 0
+    assert L.fh_level_stats(enc.handle, 0, 256, 4, 256, None) == fh.FH_E_ARG   # workspace too small
 
 
 def test_build_levels_lin_brick_info_and_errors():
