@@ -669,28 +669,32 @@ __global__ void __launch_bounds__(256) bwd_small_kernel(const __grid_constant__ 
         if (S.toff[li] >= 0) {
             // tiny level: every lane owns a private copy (column `lane` of its
             // warp's block, conflict-free): plain read-add-write, no atomics
-            float *t = lp + (S.toff[li] - (int)lv.offset * F) * 32;
+            // (indices local to the level: entry - offset, no 32-bit overflow
+            // for levels placed near the top of the 2^32 parameter range)
+            float *t = lp + S.toff[li] * 32;
 #pragma unroll
             for (int k = 0; k < 16; k += 2) {
                 const float Wyzt = wy[(k >> 1) & 1] * wz[(k >> 2) & 1] * wt[(k >> 3) & 1];
                 const float W0 = wx[0] * Wyzt, W1 = wx[1] * Wyzt;
+                const uint32_t e0 = c.idx[k] - lv.offset, e1 = c.idx[k + 1] - lv.offset;
 #pragma unroll
                 for (int f = 0; f < F; f++) {
-                    t[(c.idx[k] * F + f) * 32] += W0 * g[f];
-                    t[(c.idx[k + 1] * F + f) * 32] += W1 * g[f];
+                    t[(e0 * F + f) * 32] += W0 * g[f];
+                    t[(e1 * F + f) * 32] += W1 * g[f];
                 }
             }
             continue;
         }
-        float *a = blk + S.soff[li] - (int)lv.offset * F;
+        float *a = blk + S.soff[li];
 #pragma unroll
         for (int k = 0; k < 16; k += 2) {
             const float Wyzt = wy[(k >> 1) & 1] * wz[(k >> 2) & 1] * wt[(k >> 3) & 1];
             const float W0 = wx[0] * Wyzt, W1 = wx[1] * Wyzt;
+            const uint32_t e0 = c.idx[k] - lv.offset, e1 = c.idx[k + 1] - lv.offset;
 #pragma unroll
             for (int f = 0; f < F; f++) {
-                atomicAdd(a + c.idx[k] * F + f, W0 * g[f]);
-                atomicAdd(a + c.idx[k + 1] * F + f, W1 * g[f]);
+                atomicAdd(a + e0 * F + f, W0 * g[f]);
+                atomicAdd(a + e1 * F + f, W1 * g[f]);
             }
         }
     }

@@ -603,6 +603,13 @@ def test_maximum_table_size(levels, cap, F):
         rhs += torch.sum(dt[a:a + step].double() * table[a:a + step].double()).item()
     scale = torch.sum(dout.abs().double()).item()
     assert abs(lhs - rhs) <= 1e-5 * scale, (lhs, rhs, scale)
+    # the small last level, placed at the top of the index range, exactly:
+    # the oracle of that level alone sees the same corners (level-local)
+    last = ref.L - 1
+    off, T = int(ref.offset[last]), int(ref.tsize[last])
+    sub = oracle.Levels([levels[last]], cap)
+    G, A = sub.backward(coords, dout[:, last * F:(last + 1) * F].cpu().numpy(), F, want_abs=True)
+    check_bwd(dt[off:off + T].cpu().numpy().astype(np.float64), G, A)
     del table, dt
     torch.cuda.empty_cache()
 
