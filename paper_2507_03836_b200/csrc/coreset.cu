@@ -149,6 +149,9 @@ __device__ __forceinline__ bool feature_test(float v, const fh_feature_spec &s) 
 }
 
 constexpr int kFeatUnroll = 8;   // words (independent 128-byte loads) in flight per warp
+#ifndef FH_FEAT_UNITS
+#define FH_FEAT_UNITS 8   // 128-vertex units per warp in flight (the X % 128 == 0 fast path)
+#endif
 
 // Warp per vertex ROW (grid-stride over the n Z Y rows): the row's
 // (frame, z, y) is derived once, then lane i tests vertex 32 w + i of each
@@ -159,38 +162,37 @@ __global__ void __launch_bounds__(kThreads) feature_kernel(const float *__restri
     const uint32_t rows = (uint32_t)d.n * d.Z * d.Y;   // < 2^32 (make_dims)
     const int lane = threadIdx.x & 31;
     const uint32_t G = (gridDim.x * kThreads) >> 5;   // warps in the grid
-    if (s.kind != FH_FEAT_ISOSURFACE && (d.X & 127u) == 0 && (reinterpret_cast<uintptr_t>(vol) & 15u) == 0) {
+    if (s.kind != FH_FEAT_ISOSURFACE && (d.X & 127u) == 0) {
         // rows of whole 128-vertex groups: the (row, group) units of the
         // volume flattened, kUnits per warp in flight (memory-level
-        // parallelism: one unit is only 512 B per warp)
-        constexpr int kUnits = 4;
+        // parallelism: one unit is only 512 B per warp).  Lane i loads
+        // vertex 32 j + i of word j (four coalesced 128-byte loads per unit),
+        // so each ballot IS a mask word: no bit spreading (the float4 form
+        // spent ~100 warp instructions per unit spreading ballot bytes and was
+        // issue-bound, 121 us for 8 x 256^3).
+        constexpr int kUnits = FH_FEAT_UNITS;
+        // both kinds here are one interval test, hoisted out of the ballots:
+        // segmentation v >= p0 == p0 <= v <= +inf (NaN fails both forms)
+        const float lo = s.p0, hi = s.kind == FH_FEAT_INTERVAL ? s.p1 : INFINITY;
         const uint32_t groups = d.X / 128;
         const uint64_t units = (uint64_t)rows * groups;
-        const float4 *v4 = reinterpret_cast<const float4 *>(vol);
         const uint64_t warp0 = (blockIdx.x * kThreads + threadIdx.x) >> 5;
         for (uint64_t u0 = warp0 * kUnits; u0 < units; u0 += (uint64_t)G * kUnits) {
-            float4 v[kUnits];
+            float v[kUnits][4];
 #pragma unroll
             for (int u = 0; u < kUnits; u++)
-                v[u] = u0 + u < units ? __ldcs(v4 + (u0 + u) * 32 + lane) : make_float4(0.f, 0.f, 0.f, 0.f);
+#pragma unroll
+                for (int j = 0; j < 4; j++)
+                    v[u][j] = u0 + u < units ? __ldcs(vol + (u0 + u) * 128 + j * 32 + lane) : 0.f;
 #pragma unroll
             for (int u = 0; u < kUnits; u++) {
                 if (u0 + u >= units) break;   // warp-uniform
-                const uint32_t b0 = __ballot_sync(0xffffffffu, feature_test(v[u].x, s));
-                const uint32_t b1 = __ballot_sync(0xffffffffu, feature_test(v[u].y, s));
-                const uint32_t b2 = __ballot_sync(0xffffffffu, feature_test(v[u].z, s));
-                const uint32_t b3 = __ballot_sync(0xffffffffu, feature_test(v[u].w, s));
-                if (lane < 4) {
-                    auto spread = [](uint32_t x) {   // bit i -> bit 4 i (i < 8)
-                        x = (x | (x << 12)) & 0x000F000Fu;
-                        x = (x | (x << 6)) & 0x03030303u;
-                        return (x | (x << 3)) & 0x11111111u;
-                    };
-                    const uint32_t sh = 8u * lane;
-                    // unit (row, q) -> words 4 q .. 4 q + 3 of the row; rows hold Wx = 4 groups words
-                    f[(u0 + u) * 4 + lane] = spread((b0 >> sh) & 0xFFu) | (spread((b1 >> sh) & 0xFFu) << 1) |
-                                             (spread((b2 >> sh) & 0xFFu) << 2) | (spread((b3 >> sh) & 0xFFu) << 3);
-                }
+                const uint32_t b0 = __ballot_sync(0xffffffffu, lo <= v[u][0] && v[u][0] <= hi);
+                const uint32_t b1 = __ballot_sync(0xffffffffu, lo <= v[u][1] && v[u][1] <= hi);
+                const uint32_t b2 = __ballot_sync(0xffffffffu, lo <= v[u][2] && v[u][2] <= hi);
+                const uint32_t b3 = __ballot_sync(0xffffffffu, lo <= v[u][3] && v[u][3] <= hi);
+                // unit (row, q) -> words 4 q .. 4 q + 3 of the row (Wx = 4 groups)
+                if (lane < 4) f[(u0 + u) * 4 + lane] = lane == 0 ? b0 : lane == 1 ? b1 : lane == 2 ? b2 : b3;
             }
         }
         return;
@@ -268,44 +270,81 @@ __global__ void __launch_bounds__(kThreads) feature_kernel(const float *__restri
 
 // ------------------------------------------------------------ dilation
 // d = 26-neighbourhood of f (clamped); per-frame bounding box; per-CTA
-// popcount (the chunk counts of the compaction, CTA = 256 words).
+// chunk popcounts (the counts of the compaction, chunk = 256 words).  A thread
+// owns kDW consecutive words of one row (when Wx % kDW == 0; otherwise one
+// word each, the generic path), so a neighbour row costs kDW + 2 loads for
+// kDW outputs instead of 3 kDW, and the box / count reductions run once per
+// kDW words (was 61 M warp instructions, 73 us for 8 x 256^3).
+constexpr int kDW = 4;
+
+__device__ __forceinline__ void box_add(int bb[6], uint32_t acc, uint32_t w, uint32_t y, uint32_t z) {
+    if (acc) {
+        bb[0] = min(bb[0], (int)(w * 32 + __ffs(acc) - 1));
+        bb[3] = max(bb[3], (int)(w * 32 + 31 - __clz(acc)));
+        bb[1] = min(bb[1], (int)y);
+        bb[4] = max(bb[4], (int)y);
+        bb[2] = min(bb[2], (int)z);
+        bb[5] = max(bb[5], (int)z);
+    }
+}
+
 __global__ void __launch_bounds__(kThreads) dilate_kernel(const uint32_t *__restrict__ f, Dims d,
                                                          uint32_t *__restrict__ dm, int *__restrict__ boxes,
                                                          uint32_t *__restrict__ counts) {
     __shared__ uint32_t wcnt[kThreads / 32];
     const uint32_t total = (uint32_t)d.n * d.Z * d.Y * d.Wx;
-    const uint32_t g = blockIdx.x * kThreads + threadIdx.x;
+    const bool vec = (d.Wx % kDW) == 0;
+    const int per = vec ? kDW : 1;            // words per thread; the CTA covers `per` chunks
     int bb[6] = {INT_MAX, INT_MAX, INT_MAX, -1, -1, -1};
     uint32_t cnt = 0;
     int frame = -1;
-    if (g < total) {
-        const uint32_t row = g / d.Wx;
-        const uint32_t w = g - row * d.Wx;
-        const uint32_t y = row % d.Y, z = (row / d.Y) % d.Z;
-        const uint32_t k = row / (d.Y * d.Z);
-        frame = (int)k;
-        uint32_t acc = 0;
-        for (int dz = -1; dz <= 1; dz++) {
-            const int zz = (int)z + dz;
-            if (zz < 0 || zz >= (int)d.Z) continue;
-            for (int dy = -1; dy <= 1; dy++) {
-                const int yy = (int)y + dy;
-                if (yy < 0 || yy >= (int)d.Y) continue;
-                const uint32_t *r = f + ((k * d.Z + zz) * d.Y + yy) * d.Wx;
-                const uint32_t c = __ldg(r + w);
-                const uint32_t lft = w > 0 ? __ldg(r + w - 1) : 0u;
-                const uint32_t rgt = w + 1 < d.Wx ? __ldg(r + w + 1) : 0u;
-                acc |= c | (c << 1) | (c >> 1) | (lft >> 31) | (rgt << 31);
+    {
+        const uint32_t g0 = (blockIdx.x * kThreads + threadIdx.x) * per;
+        if (g0 < total) {
+            const uint32_t row = g0 / d.Wx;
+            const uint32_t w0 = g0 - row * d.Wx;
+            const uint32_t y = row % d.Y, z = (row / d.Y) % d.Z;
+            const uint32_t k = row / (d.Y * d.Z);
+            frame = (int)k;
+            uint32_t acc[kDW] = {0, 0, 0, 0};
+            for (int dz = -1; dz <= 1; dz++) {
+                const int zz = (int)z + dz;
+                if (zz < 0 || zz >= (int)d.Z) continue;
+                for (int dy = -1; dy <= 1; dy++) {
+                    const int yy = (int)y + dy;
+                    if (yy < 0 || yy >= (int)d.Y) continue;
+                    const uint32_t *r = f + ((k * d.Z + zz) * d.Y + yy) * d.Wx;
+                    const uint32_t lft = w0 > 0 ? __ldg(r + w0 - 1) : 0u;
+                    if (vec) {
+                        const uint4 c4 = __ldg(reinterpret_cast<const uint4 *>(r + w0));
+                        const uint32_t rgt = w0 + kDW < d.Wx ? __ldg(r + w0 + kDW) : 0u;
+                        const uint32_t c[kDW] = {c4.x, c4.y, c4.z, c4.w};
+#pragma unroll
+                        for (int i = 0; i < kDW; i++) {
+                            const uint32_t l = i > 0 ? c[i - 1] : lft, rr = i + 1 < kDW ? c[i + 1] : rgt;
+                            acc[i] |= c[i] | (c[i] << 1) | (c[i] >> 1) | (l >> 31) | (rr << 31);
+                        }
+                    } else {
+                        const uint32_t c = __ldg(r + w0);
+                        const uint32_t rgt = w0 + 1 < d.Wx ? __ldg(r + w0 + 1) : 0u;
+                        acc[0] |= c | (c << 1) | (c >> 1) | (lft >> 31) | (rgt << 31);
+                    }
+                }
             }
-        }
-        acc &= last_word_mask(d.X, w, d.Wx);
-        dm[g] = acc;
-        cnt = __popc(acc);
-        if (acc) {
-            bb[0] = (int)(w * 32 + __ffs(acc) - 1);
-            bb[3] = (int)(w * 32 + 31 - __clz(acc));
-            bb[1] = bb[4] = (int)y;
-            bb[2] = bb[5] = (int)z;
+            if (vec) {
+#pragma unroll
+                for (int i = 0; i < kDW; i++) {
+                    acc[i] &= last_word_mask(d.X, w0 + i, d.Wx);
+                    cnt += __popc(acc[i]);
+                    box_add(bb, acc[i], w0 + i, y, z);
+                }
+                *reinterpret_cast<uint4 *>(dm + g0) = make_uint4(acc[0], acc[1], acc[2], acc[3]);
+            } else {
+                acc[0] &= last_word_mask(d.X, w0, d.Wx);
+                cnt = __popc(acc[0]);
+                box_add(bb, acc[0], w0, y, z);
+                dm[g0] = acc[0];
+            }
         }
     }
     // boxes are per frame: reduce over the warp when its lanes share the frame
@@ -337,10 +376,12 @@ __global__ void __launch_bounds__(kThreads) dilate_kernel(const uint32_t *__rest
     }
     if ((threadIdx.x & 31) == 0) wcnt[threadIdx.x >> 5] = cnt;
     __syncthreads();
-    if (threadIdx.x == 0) {
+    if ((int)threadIdx.x < per) {   // chunk c of this CTA = its warps [c w, (c + 1) w), w = 8 / per
+        const int wpc = (kThreads / 32) / per;
+        const uint64_t c = (uint64_t)blockIdx.x * per + threadIdx.x;
         uint32_t s = 0;
-        for (int i = 0; i < kThreads / 32; i++) s += wcnt[i];
-        counts[blockIdx.x] = s;
+        for (int i = 0; i < wpc; i++) s += wcnt[threadIdx.x * wpc + i];
+        if (c * kThreads < total) counts[c] = s;
     }
 }
 
@@ -371,70 +412,104 @@ __global__ void __launch_bounds__(kThreads) cellrow_kernel(const uint32_t *__res
     }
 }
 
-// Thread per 32-bit word of the Morton-ordered bitmap: decode the word's
-// base cell once; its 32 cells are fixed offsets (lo_off) from it that lie in
-// m.nrows distinct cell rows (<= 8 on a cube: a 4x4x2 block), each read once
-// -- the x offsets stay inside one 32-bit word because the base x is a
-// multiple of the x extent of the pattern.
+// kOW consecutive 32-bit words of the Morton-ordered bitmap per thread: the
+// base cell of the first word is decoded once (the code bits above the
+// thread's block); the kOW - 1 others differ from it only in code bits
+// 5 .. 5 + log2(kOW) - 1.  Each word's 32 cells are fixed offsets (lo_off)
+// from its base that lie in m.nrows distinct cell rows (<= 8 on a cube: a
+// 4x4x2 block), each read once -- the x offsets stay inside one 32-bit word
+// because the base x is a multiple of the x extent of the pattern.  (One
+// word per thread decoded all nbits code bits per word: 80 M warp
+// instructions, 95 us for 8 x 255^3 cells.)
+constexpr int kOW = 8, kOWBits = 3;
+
+__device__ __forceinline__ uint32_t occupancy_word(const uint32_t *__restrict__ fr, const Dims &d, const Morton &m,
+                                                   const uint32_t base[3]) {
+    const int ncodes = 1 << (m.nbits < 5 ? m.nbits : 5);
+    const uint32_t Yc = d.Y - 1, Zc = d.Z - 1, Xc = d.X - 1;
+    uint32_t word = 0;
+    if (base[0] >= Xc) return 0u;
+    if (m.std5) {
+        // low code bits (x0, y0, z0, x1, y1): row (y, z) contributes the 4 x
+        // bits (base x .. base x + 3) at code positions off(y, z) + {0, 1, 8, 9}
+#pragma unroll
+        for (int zz = 0; zz < 2; zz++)
+#pragma unroll
+            for (int yy = 0; yy < 4; yy++) {
+                const uint32_t cy = base[1] + yy, cz = base[2] + zz;
+                if (cy >= Yc || cz >= Zc) continue;
+                const uint32_t rw = __ldg(fr + (cz * Yc + cy) * d.Wc + (base[0] >> 5));
+                const uint32_t nib = (rw >> (base[0] & 31)) & 0xFu;   // bits past the grid are 0
+                const uint32_t spread = (nib & 3u) | ((nib & 12u) << 6);
+                word |= spread << ((yy & 1) * 2 + zz * 4 + (yy >> 1) * 16);
+            }
+    } else if (m.nrows <= 8) {
+        uint32_t rows[8];
+#pragma unroll
+        for (int r = 0; r < 8; r++) {
+            const uint32_t cy = base[1] + m.row_dy[r], cz = base[2] + m.row_dz[r];
+            rows[r] = (r < m.nrows && cy < Yc && cz < Zc) ? __ldg(fr + (cz * Yc + cy) * d.Wc + (base[0] >> 5)) : 0u;
+        }
+#pragma unroll
+        for (int i = 0; i < 32; i++) {
+            if (i >= ncodes) break;
+            const int ri = m.row_of[i];
+            uint32_t rw = rows[0];
+#pragma unroll
+            for (int r = 1; r < 8; r++) rw = ri == r ? rows[r] : rw;   // register select, no local memory
+            // bits past the grid are 0 in the cell-row mask (last_word_mask)
+            word |= ((rw >> ((base[0] + m.lo_off[i][0]) & 31)) & 1u) << i;
+        }
+    } else {   // degenerate shapes (an axis of one cell): one load per code
+        for (int i = 0; i < ncodes; i++) {
+            const uint32_t cx = base[0] + m.lo_off[i][0], cy = base[1] + m.lo_off[i][1], cz = base[2] + m.lo_off[i][2];
+            if (cx >= Xc || cy >= Yc || cz >= Zc) continue;
+            word |= ((__ldg(fr + (cz * Yc + cy) * d.Wc + (cx >> 5)) >> (cx & 31)) & 1u) << i;
+        }
+    }
+    return word;
+}
+
 __global__ void __launch_bounds__(kThreads) occupancy_kernel(const uint32_t *__restrict__ cm, Dims d, Morton m,
                                                             uint64_t words, uint32_t *__restrict__ occ) {
     const uint64_t k = blockIdx.y;   // frame
-    for (uint64_t wi = (uint64_t)blockIdx.x * kThreads + threadIdx.x; wi < words;
-         wi += (uint64_t)gridDim.x * kThreads) {
-        const uint64_t g = k * words + wi;
-        uint32_t base[3] = {0, 0, 0};
-        for (int p = 5; p < m.nbits; p++) {   // selects, not a dynamically indexed array (no local memory)
-            const uint32_t b = (uint32_t)((wi >> (p - 5)) & 1) << m.bit[p];
+    const uint32_t *fr = cm + k * (uint64_t)(d.Z - 1) * (d.Y - 1) * d.Wc;   // a frame's offsets fit 32 bits
+    const bool vec = (words % 4) == 0 && (reinterpret_cast<uintptr_t>(occ) & 15) == 0;
+    for (uint64_t wi0 = ((uint64_t)blockIdx.x * kThreads + threadIdx.x) * kOW; wi0 < words;
+         wi0 += (uint64_t)gridDim.x * kThreads * kOW) {
+        uint32_t base0[3] = {0, 0, 0};
+        for (int p = 5 + kOWBits; p < m.nbits; p++) {   // selects, not a dynamically indexed array
+            const uint32_t b = (uint32_t)((wi0 >> (p - 5)) & 1) << m.bit[p];
             const int a = m.axis[p];
-            base[0] |= a == 0 ? b : 0u;
-            base[1] |= a == 1 ? b : 0u;
-            base[2] |= a == 2 ? b : 0u;
+            base0[0] |= a == 0 ? b : 0u;
+            base0[1] |= a == 1 ? b : 0u;
+            base0[2] |= a == 2 ? b : 0u;
         }
-        const uint32_t *fr = cm + k * (uint64_t)(d.Z - 1) * (d.Y - 1) * d.Wc;
-        const int ncodes = 1 << (m.nbits < 5 ? m.nbits : 5);
-        uint32_t word = 0;
-        if (m.std5) {
-            // low code bits (x0, y0, z0, x1, y1): row (y, z) contributes the 4 x
-            // bits (base x .. base x + 3) at code positions off(y, z) + {0, 1, 8, 9}
+        uint32_t out[kOW];
 #pragma unroll
-            for (int zz = 0; zz < 2; zz++)
+        for (int j = 0; j < kOW; j++) {
+            uint32_t base[3] = {base0[0], base0[1], base0[2]};
 #pragma unroll
-                for (int yy = 0; yy < 4; yy++) {
-                    const uint32_t cy = base[1] + yy, cz = base[2] + zz;
-                    if (cy >= d.Y - 1 || cz >= d.Z - 1 || base[0] >= d.X - 1) continue;
-                    const uint32_t rw = __ldg(fr + ((uint64_t)cz * (d.Y - 1) + cy) * d.Wc + (base[0] >> 5));
-                    const uint32_t nib = (rw >> (base[0] & 31)) & 0xFu;   // bits past the grid are 0
-                    const uint32_t spread = (nib & 3u) | ((nib & 12u) << 6);
-                    word |= spread << ((yy & 1) * 2 + zz * 4 + (yy >> 1) * 16);
-                }
-        } else if (m.nrows <= 8) {
-            uint32_t rows[8];
-#pragma unroll
-            for (int r = 0; r < 8; r++) {
-                const uint32_t cy = base[1] + m.row_dy[r], cz = base[2] + m.row_dz[r];
-                rows[r] = (r < m.nrows && cy < d.Y - 1 && cz < d.Z - 1 && base[0] < d.X - 1)
-                              ? __ldg(fr + ((uint64_t)cz * (d.Y - 1) + cy) * d.Wc + (base[0] >> 5))
-                              : 0u;
+            for (int i = 0; i < kOWBits; i++) {
+                const int p = 5 + i;
+                const uint32_t b = (p < m.nbits) ? (uint32_t)((j >> i) & 1) << m.bit[p] : 0u;
+                const int a = m.axis[p];
+                base[0] |= a == 0 ? b : 0u;
+                base[1] |= a == 1 ? b : 0u;
+                base[2] |= a == 2 ? b : 0u;
             }
-#pragma unroll
-            for (int i = 0; i < 32; i++) {
-                if (i >= ncodes) break;
-                const int ri = m.row_of[i];
-                uint32_t rw = rows[0];
-#pragma unroll
-                for (int r = 1; r < 8; r++) rw = ri == r ? rows[r] : rw;   // register select, no local memory
-                // bits past the grid are 0 in the cell-row mask (last_word_mask)
-                word |= ((rw >> ((base[0] + m.lo_off[i][0]) & 31)) & 1u) << i;
-            }
-        } else {   // degenerate shapes (an axis of one cell): one load per code
-            for (int i = 0; i < ncodes; i++) {
-                const uint32_t cx = base[0] + m.lo_off[i][0], cy = base[1] + m.lo_off[i][1],
-                               cz = base[2] + m.lo_off[i][2];
-                if (cx >= d.X - 1 || cy >= d.Y - 1 || cz >= d.Z - 1) continue;
-                word |= ((__ldg(fr + ((uint64_t)cz * (d.Y - 1) + cy) * d.Wc + (cx >> 5)) >> (cx & 31)) & 1u) << i;
-            }
+            out[j] = wi0 + j < words ? occupancy_word(fr, d, m, base) : 0u;
         }
-        occ[g] = word;
+        uint32_t *o = occ + k * words + wi0;
+        if (vec && wi0 + kOW <= words) {
+#pragma unroll
+            for (int j = 0; j < kOW; j += 4)
+                *reinterpret_cast<uint4 *>(o + j) = make_uint4(out[j], out[j + 1], out[j + 2], out[j + 3]);
+        } else {
+#pragma unroll
+            for (int j = 0; j < kOW; j++)
+                if (wi0 + j < words) o[j] = out[j];
+        }
     }
 }
 
@@ -662,12 +737,16 @@ fh_status fh_coreset_build(const float *vol, const uint32_t dims_xyz[3], int n_f
         { straddle_kernel<<<grid_for(32 * L.swords), kThreads, 0, s>>>(vol, d, spec->p0, sb); fh::count_launch(); }
     { feature_kernel<<<grid_for(32ull * d.n * d.Z * d.Y), kThreads, 0, s>>>(vol, d, *spec, sb, f); fh::count_launch(); }
     { init_boxes_kernel<<<(6 * n_frames + 255) / 256, 256, 0, s>>>(boxes, n_frames); fh::count_launch(); }
-    { dilate_kernel<<<(unsigned)L.nchunks, kThreads, 0, s>>>(f, d, dm, boxes, counts); fh::count_launch(); }
+    {
+        const uint64_t per = d.Wx % kDW == 0 ? kDW : 1;
+        dilate_kernel<<<(unsigned)((L.nchunks + per - 1) / per), kThreads, 0, s>>>(f, d, dm, boxes, counts);
+        fh::count_launch();
+    }
     if (occupancy) {
         // the cell-row mask reuses the straddle bit buffer (same shape)
         { cellrow_kernel<<<grid_for(L.swords), kThreads, 0, s>>>(dm, d, sb); fh::count_launch(); }
         const uint64_t words = fh_occupancy_words(dims_xyz);
-        const dim3 og(grid_for(words), (unsigned)d.n);
+        const dim3 og(grid_for((words + kOW - 1) / kOW), (unsigned)d.n);
         { occupancy_kernel<<<og, kThreads, 0, s>>>(sb, d, make_morton(d.X, d.Y, d.Z), words, occupancy); fh::count_launch(); }
     }
     cudaMemcpyAsync(offs, counts, 4 * L.nchunks, cudaMemcpyDeviceToDevice, s);
