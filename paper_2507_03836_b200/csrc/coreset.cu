@@ -18,7 +18,8 @@
 //                    bitmap: its 32 cells are a fixed pattern of offsets
 //                    from one decoded base, each one cell-row bit
 //   emit_kernel      CTA per 256 mask words: block scan of popcounts, then
-//                    every thread writes its set bits as samples (Eqs. 1-3)
+//                    each warp writes its words' set bits as samples
+//                    (Eqs. 1-3), 32 consecutive samples per store
 // Order of samples = word order then bit order = frame-major row-major (R26).
 #include <cuda_runtime.h>
 
@@ -576,6 +577,27 @@ __global__ void fbb_kernel(const int *__restrict__ boxes, int n, Dims d, const u
     *count = nchunks ? (uint64_t)offs[nchunks - 1] + counts[nchunks - 1] : 0ull;
 }
 
+// Position of the r-th (0-based) set bit of m (r < popc(m)).
+__device__ __forceinline__ uint32_t nth_set_bit(uint32_t m, uint32_t r) {
+    uint32_t pos = 0;
+#pragma unroll
+    for (int s = 16; s > 0; s >>= 1) {
+        const uint32_t low = __popc(m & ((1u << s) - 1u));
+        if (r >= low) {
+            r -= low;
+            m >>= s;
+            pos += s;
+        }
+    }
+    return pos;
+}
+
+// Warp-cooperative: the warp's 32 words own the output slots [base, base +
+// Cw); slot j = j0 + lane finds its word (the last lane whose exclusive
+// count is <= j: a 5-step shuffle binary search) and its bit (the r-th set
+// bit of that word), so every store instruction writes 32 consecutive
+// samples (512 B of coords, 128 B of values).  (A lane per word writing its
+// own samples serially made each store touch 32 lines: 40 us at 2^21 samples.)
 __global__ void __launch_bounds__(kThreads) emit_kernel(const uint32_t *__restrict__ dm, const float *__restrict__ vol,
                                                        Dims d, const uint32_t *__restrict__ offs,
                                                        const int *__restrict__ fbb, float4 *__restrict__ coords,
@@ -594,30 +616,40 @@ __global__ void __launch_bounds__(kThreads) emit_kernel(const uint32_t *__restri
     }
     if (lane == 31) ws[w] = v;
     __syncthreads();
-    if (!bits) return;
-    uint32_t pos = offs[blockIdx.x] + v - c;
-    for (int i = 0; i < w; i++) pos += ws[i];
-    const uint32_t row = g / d.Wx;
-    const uint32_t wx = g - row * d.Wx;
+    const uint32_t Cw = __shfl_sync(0xffffffffu, v, 31);
+    if (Cw == 0) return;   // warp-uniform
+    uint32_t base = offs[blockIdx.x];
+    for (int i = 0; i < w; i++) base += ws[i];
+    const uint32_t excl = v - c;
+    // this lane's word: row, x word, and the (y, z, t) coordinates of its samples
+    const uint32_t gg = g < total ? g : 0u;
+    const uint32_t row = gg / d.Wx;
+    const uint32_t wx = gg - row * d.Wx;
     const uint32_t y = row % d.Y, z = (row / d.Y) % d.Z;
     const uint32_t k = row / (d.Y * d.Z);
-    const int lo[3] = {fbb[0], fbb[1], fbb[2]};
-    const float span[3] = {(float)(fbb[3] - fbb[0]), (float)(fbb[4] - fbb[1]), (float)(fbb[5] - fbb[2])};
+    const int lo0 = fbb[0];
+    const float span0 = (float)(fbb[3] - fbb[0]);
     // Eqs. 1-2 then (q+1)/2 (R2, R25): (i - lo) / (hi - lo), one rounding
-    const float fy = __fdiv_rn((float)((int)y - lo[1]), span[1]);
-    const float fz = __fdiv_rn((float)((int)z - lo[2]), span[2]);
+    const float fy = __fdiv_rn((float)((int)y - fbb[1]), (float)(fbb[4] - fbb[1]));
+    const float fz = __fdiv_rn((float)((int)z - fbb[2]), (float)(fbb[5] - fbb[2]));
     const float ft = d.n > 1 ? __fdiv_rn((float)k, (float)(d.n - 1)) : 0.5f;   // n = 1: t = 0 in [-1,1]
-    const float *r = vol + (uint64_t)row * d.X;
-    uint32_t rem = bits;
-    while (rem) {
-        const uint32_t b = __ffs(rem) - 1;
-        rem &= rem - 1;
-        if (pos < capacity) {
-            const uint32_t x = wx * 32 + b;
-            coords[pos] = make_float4(__fdiv_rn((float)((int)x - lo[0]), span[0]), fy, fz, ft);
-            values[pos] = __ldg(r + x);
+    for (uint32_t j0 = 0; j0 < Cw; j0 += 32) {
+        const uint32_t j = j0 + lane;
+        int L = 0;
+#pragma unroll
+        for (int st = 16; st > 0; st >>= 1)
+            if (__shfl_sync(0xffffffffu, excl, L + st) <= j) L += st;
+        const uint32_t wb = __shfl_sync(0xffffffffu, bits, L);
+        const uint32_t r = j - __shfl_sync(0xffffffffu, excl, L);
+        const uint32_t rowL = __shfl_sync(0xffffffffu, row, L), wxL = __shfl_sync(0xffffffffu, wx, L);
+        const float fyL = __shfl_sync(0xffffffffu, fy, L), fzL = __shfl_sync(0xffffffffu, fz, L),
+                    ftL = __shfl_sync(0xffffffffu, ft, L);
+        const uint64_t pos = (uint64_t)base + j;
+        if (j < Cw && pos < capacity) {
+            const uint32_t x = wxL * 32 + nth_set_bit(wb, r);
+            coords[pos] = make_float4(__fdiv_rn((float)((int)x - lo0), span0), fyL, fzL, ftL);
+            values[pos] = __ldg(vol + (uint64_t)rowL * d.X + x);
         }
-        pos++;
     }
 }
 
