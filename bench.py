@@ -765,11 +765,24 @@ def run_ours(args, rank, local_rank, world):
         del coords_h, dout_h, sets, out, dout, dtable, flush
         torch.cuda.empty_cache()
         kt = max(3, min(K, 10))
+
+        def leg(which):
+            # The headline above is already measured: a failing train leg is
+            # reported in its own key (traceback on stderr) instead of losing
+            # the line.  Every rank runs the same code, so a failure here is
+            # normally raised on all ranks alike.
+            try:
+                return train_step_bench(fh, torch, W, which, rank, world, dist, kt, args.warmup, args.dp)
+            except Exception as ex:  # noqa: BLE001
+                import traceback
+                traceback.print_exc(file=sys.stderr)
+                return {"error": f"{type(ex).__name__}: {ex}"[:400]}
+            finally:
+                torch.cuda.empty_cache()
+
         if world == 1:
-            train["cfg3"] = train_step_bench(fh, torch, W, "cfg3", rank, world, dist, kt, args.warmup, args.dp)
-            torch.cuda.empty_cache()
-        train["cfg5"] = train_step_bench(fh, torch, W, "cfg5", rank, world, dist, kt, args.warmup, args.dp)
-        torch.cuda.empty_cache()
+            train["cfg3"] = leg("cfg3")
+        train["cfg5"] = leg("cfg5")
     encoders = paper_encoder_compare(fh, torch, W, max(3, min(K, 10))) if not args.no_train else None
     torch.cuda.empty_cache()
     hbm_peak, peak_src = load_peaks()
