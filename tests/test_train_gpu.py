@@ -43,6 +43,46 @@ def make(cfg, N, seed=0, max_batch=None):
 def test_mlp_fwd_bwd_parity(F, L, N):
     cfg = small_cfg(F, L)
     enc, tr, coords, target = make(cfg, N, seed=F * 100 + L)
+    check_fwd_bwd(cfg, tr, coords, target, N)
+
+
+def test_train_fwd_bwd_cfg3_full_size():
+    """bench.py's train_step launch configuration (BASELINE.json configs[2]:
+    cfg3 encoder, L=16 F=2 fp16 tables cap 2^19, MLP 32-64-64-1, batch 2^18):
+    2048 tiles, so every TMEM slot accumulates several tiles' weight
+    gradients before its partial row and the reduce kernel -- the small cases
+    above give each slot at most one tile.  Same bars as above."""
+    cfg, N = W.CFG3, W.N_CFG3
+    g = W.rng(33)
+    enc = fh.Encoder(cfg.levels, cfg.F, cfg.table_dtype, cfg.cap)
+    table = W.draw_table(g, enc.entries, cfg.F, "f32")
+    layers = W.draw_mlp(g, W.MLP3)
+    coords = W.draw_coords(g, N)
+    target = g.random(N, dtype=np.float32)
+    tr = fh.Trainer(enc, table, layers, N)
+    assert (N + 127) // 128 > 2 * torch.cuda.get_device_properties(0).multi_processor_count
+    check_fwd_bwd(cfg, tr, coords, target, N)
+
+
+def test_train_fwd_bwd_cfg5_shape_multi_tile():
+    """The K0 = 64 kernel bench.py's cfg5 leg runs (BASELINE.json configs[3]
+    encoder: L=16 F=4 fp16 tables cap 2^22, MLP 64-64-64-1) at 2^20 samples
+    (8192 tiles, ~28 per slot): loss, MLP gradients and dL/d(enc) against the
+    oracle.  The table gradient at this size is pinned by
+    tests/test_parity_gpu.py::test_cfg4_sampled_rows_and_adjoint."""
+    cfg, N = W.CFG4, 1 << 20
+    g = W.rng(44)
+    enc = fh.Encoder(cfg.levels, cfg.F, cfg.table_dtype, cfg.cap)
+    table = W.draw_table(g, enc.entries, cfg.F, "f32")
+    layers = W.draw_mlp(g, W.MLP4)
+    coords = W.draw_coords(g, N)
+    target = g.random(N, dtype=np.float32)
+    tr = fh.Trainer(enc, table, layers, N)
+    del table
+    check_fwd_bwd(cfg, tr, coords, target, N, table_grad=False)
+
+
+def check_fwd_bwd(cfg, tr, coords, target, N, table_grad=True):
     c, t = torch.from_numpy(coords).cuda(), torch.from_numpy(target).cuda()
     n_global = N + 17  # exercise the 1/N_global scaling
     loss = tr.fwd_bwd(c, t, n_global)
@@ -69,6 +109,8 @@ def test_mlp_fwd_bwd_parity(F, L, N):
             assert np.max(np.abs(got - ref)) <= tol, (o, np.max(np.abs(got - ref)), tol)
     dx = tr.dx(N).cpu().numpy().astype(np.float64)
     assert np.max(np.abs(dx - dx0)) <= 1e-2 * np.max(np.abs(dx0))
+    if not table_grad:
+        return
     # encode bwd of the GPU's own dL/d(enc), against Oracle-B (strict)
     ref = oracle.Levels(cfg.levels, cfg.cap)
     G, A = ref.backward(coords, dx, cfg.F, want_abs=True)
