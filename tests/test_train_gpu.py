@@ -224,6 +224,20 @@ def test_infer_forward_parity(F, L, N):
     loss."""
     cfg = small_cfg(F, L)
     enc, tr, coords, target = make(cfg, N, seed=21 + F + L)
+    check_infer(cfg, tr, coords, target, N)
+
+
+def test_infer_cfg3_full_size():
+    """fh_infer at bench.py's cfg3 inference launch (2^18 samples, the cfg3
+    encoder and MLP 32-64-64-1), same bars."""
+    cfg, N = W.CFG3, W.N_CFG3
+    g = W.rng(55)
+    enc = fh.Encoder(cfg.levels, cfg.F, cfg.table_dtype, cfg.cap)
+    tr = fh.Trainer(enc, W.draw_table(g, enc.entries, cfg.F, "f32"), W.draw_mlp(g, W.MLP3), N)
+    check_infer(cfg, tr, W.draw_coords(g, N), g.random(N, dtype=np.float32), N)
+
+
+def check_infer(cfg, tr, coords, target, N):
     c, t = torch.from_numpy(coords).cuda(), torch.from_numpy(target).cuda()
     loss = tr.fwd_bwd(c, t, N).item()
     x0 = tr.enc_out(N).float().cpu().numpy().astype(np.float64)
