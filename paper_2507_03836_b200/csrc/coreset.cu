@@ -393,23 +393,46 @@ __global__ void init_boxes_kernel(int *boxes, int n) {
 
 // ------------------------------------------------------------ occupancy
 // Cell-row mask: cell x of row (cy, cz) is touched iff vertex x or x+1 of
-// one of its 4 corner rows is in d_k.
+// one of its 4 corner rows is in d_k.  kDW words of one cell row per thread
+// when Wc % kDW == 0 (one index decode and 4 (kDW + 1) loads per kDW words),
+// else one word per thread.
 __global__ void __launch_bounds__(kThreads) cellrow_kernel(const uint32_t *__restrict__ dm, Dims d,
                                                           uint32_t *__restrict__ cm) {
     const uint32_t total = (uint32_t)d.n * (d.Z - 1) * (d.Y - 1) * d.Wc;
-    for (uint32_t g = blockIdx.x * kThreads + threadIdx.x; g < total; g += gridDim.x * kThreads) {
+    const bool vec = (d.Wc % kDW) == 0;
+    const uint32_t per = vec ? kDW : 1;
+    for (uint32_t g = (blockIdx.x * kThreads + threadIdx.x) * per; g < total; g += gridDim.x * kThreads * per) {
         const uint32_t row = g / d.Wc;
         const uint32_t w = g - row * d.Wc;
         const uint32_t cy = row % (d.Y - 1), cz = (row / (d.Y - 1)) % (d.Z - 1);
         const uint32_t k = row / ((d.Y - 1) * (d.Z - 1));
-        uint32_t c = 0, nx = 0;
+        if (vec) {
+            uint32_t c[kDW] = {0, 0, 0, 0};
+            uint32_t nx = 0;
 #pragma unroll
-        for (int q = 0; q < 4; q++) {
-            const uint32_t *r = dm + ((k * d.Z + cz + (q >> 1)) * d.Y + cy + (q & 1)) * d.Wx;
-            c |= __ldg(r + w);
-            if (w + 1 < d.Wx) nx |= __ldg(r + w + 1);
+            for (int q = 0; q < 4; q++) {
+                const uint32_t *r = dm + ((k * d.Z + cz + (q >> 1)) * d.Y + cy + (q & 1)) * d.Wx;
+#pragma unroll
+                for (int i = 0; i < kDW; i++) c[i] |= __ldg(r + w + i);   // Wx >= Wc: w + kDW - 1 < Wx
+                if (w + kDW < d.Wx) nx |= __ldg(r + w + kDW);
+            }
+            uint32_t o[kDW];
+#pragma unroll
+            for (int i = 0; i < kDW; i++) {
+                const uint32_t next = i + 1 < kDW ? c[i + 1] : nx;
+                o[i] = (c[i] | (c[i] >> 1) | (next << 31)) & last_word_mask(d.X - 1, w + i, d.Wc);
+            }
+            *reinterpret_cast<uint4 *>(cm + g) = make_uint4(o[0], o[1], o[2], o[3]);
+        } else {
+            uint32_t c = 0, nx = 0;
+#pragma unroll
+            for (int q = 0; q < 4; q++) {
+                const uint32_t *r = dm + ((k * d.Z + cz + (q >> 1)) * d.Y + cy + (q & 1)) * d.Wx;
+                c |= __ldg(r + w);
+                if (w + 1 < d.Wx) nx |= __ldg(r + w + 1);
+            }
+            cm[g] = (c | (c >> 1) | (nx << 31)) & last_word_mask(d.X - 1, w, d.Wc);
         }
-        cm[g] = (c | (c >> 1) | (nx << 31)) & last_word_mask(d.X - 1, w, d.Wc);
     }
 }
 
@@ -776,7 +799,8 @@ fh_status fh_coreset_build(const float *vol, const uint32_t dims_xyz[3], int n_f
     }
     if (occupancy) {
         // the cell-row mask reuses the straddle bit buffer (same shape)
-        { cellrow_kernel<<<grid_for(L.swords), kThreads, 0, s>>>(dm, d, sb); fh::count_launch(); }
+        { cellrow_kernel<<<grid_for(d.Wc % kDW == 0 ? L.swords / kDW : L.swords), kThreads, 0, s>>>(dm, d, sb);
+          fh::count_launch(); }
         const uint64_t words = fh_occupancy_words(dims_xyz);
         const dim3 og(grid_for((words + kOW - 1) / kOW), (unsigned)d.n);
         { occupancy_kernel<<<og, kThreads, 0, s>>>(sb, d, make_morton(d.X, d.Y, d.Z), words, occupancy); fh::count_launch(); }
