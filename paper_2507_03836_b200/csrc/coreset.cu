@@ -56,6 +56,7 @@ struct Morton {
     uint8_t lo_off[32][3];   // cell offsets of the 32 codes of one word (low 5 code bits)
     int nrows;               // distinct (dy, dz) among them
     bool std5;               // low 5 code bits are x0 y0 z0 x1 y1 (every axis has >= 2 bits)
+    bool cube8;              // std5 and code bits 5..7 are z1 x2 y2 (every axis has >= 3 bits)
     uint8_t row_dy[32], row_dz[32], row_of[32];
 };
 
@@ -79,6 +80,8 @@ static Morton make_morton(uint32_t X, uint32_t Y, uint32_t Z) {
             }
     m.nbits = pos;
     m.std5 = m.bits[0] >= 2 && m.bits[1] >= 2 && m.bits[2] >= 2;
+    m.cube8 = m.std5 && m.nbits >= 8 && m.axis[5] == 2 && m.bit[5] == 1 && m.axis[6] == 0 && m.bit[6] == 2 &&
+              m.axis[7] == 1 && m.bit[7] == 2;
     m.nrows = 0;
     for (int i = 0; i < 32; i++) {
         m.lo_off[i][0] = m.lo_off[i][1] = m.lo_off[i][2] = 0;
@@ -510,6 +513,36 @@ __global__ void __launch_bounds__(kThreads) occupancy_kernel(const uint32_t *__r
             base0[2] |= a == 2 ? b : 0u;
         }
         uint32_t out[kOW];
+        if (m.cube8) {
+            // the kOW = 8 words (code bits 5..7 = z1 x2 y2) cover cells
+            // x0 .. x0+7 (one cell-row word: x0 % 8 == 0), y0 .. y0+7,
+            // z0 .. z0+3: each of those 32 rows is loaded once (was 8 per word)
+            const uint32_t Yc = d.Y - 1, Zc = d.Z - 1, x0 = base0[0];
+            uint32_t rw[4][8];
+#pragma unroll
+            for (int zz = 0; zz < 4; zz++)
+#pragma unroll
+                for (int yy = 0; yy < 8; yy++) {
+                    const uint32_t cy = base0[1] + yy, cz = base0[2] + zz;
+                    rw[zz][yy] = (x0 < d.X - 1 && cy < Yc && cz < Zc)
+                                     ? __ldg(fr + (cz * Yc + cy) * d.Wc + (x0 >> 5)) : 0u;
+                }
+#pragma unroll
+            for (int j = 0; j < kOW; j++) {
+                const int zo = (j & 1) * 2, xo = ((j >> 1) & 1) * 4, yo = ((j >> 2) & 1) * 4;
+                uint32_t word = 0;
+#pragma unroll
+                for (int zz = 0; zz < 2; zz++)
+#pragma unroll
+                    for (int yy = 0; yy < 4; yy++) {
+                        // bits past the grid are 0 in the cell-row mask (last_word_mask)
+                        const uint32_t nib = (rw[zo + zz][yo + yy] >> ((x0 + xo) & 31)) & 0xFu;
+                        const uint32_t spread = (nib & 3u) | ((nib & 12u) << 6);
+                        word |= spread << ((yy & 1) * 2 + zz * 4 + (yy >> 1) * 16);
+                    }
+                out[j] = wi0 + j < words ? word : 0u;
+            }
+        } else
 #pragma unroll
         for (int j = 0; j < kOW; j++) {
             uint32_t base[3] = {base0[0], base0[1], base0[2]};
