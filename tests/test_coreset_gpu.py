@@ -58,7 +58,9 @@ def rand_vol(seed, n=3, shape=(6, 7, 9)):
                                    # (one word per thread); 9x9x100 / 5x5x5: std5 occupancy with 8 words per
                                    # thread / a 2-word bitmap (ragged tail); 3x4x128: non-std5 rows path
                                    # 3x3x129: Wc = 4 cell words, Wx = 5 vertex words (the carry word)
-                                   (9, 9, 100), (4, 5, 130), (3, 4, 128), (5, 5, 5), (3, 3, 129)])
+                                   # Y % 4 == 0 with Wx in {4, 8} (3x8x256, 2x12x100)
+                                   (9, 9, 100), (4, 5, 130), (3, 4, 128), (5, 5, 5), (3, 3, 129),
+                                   (3, 8, 256), (2, 12, 100)])
 def test_coreset_parity(kind, p0, p1, shape):
     check_against_oracle(rand_vol(kind * 7 + shape[0], 3, shape), kind, p0, p1)
 
