@@ -656,9 +656,13 @@ __device__ __forceinline__ uint32_t nth_set_bit(uint32_t m, uint32_t r) {
 // own samples serially made each store touch 32 lines: 40 us at 2^21 samples.)
 __global__ void __launch_bounds__(kThreads) emit_kernel(const uint32_t *__restrict__ dm, const float *__restrict__ vol,
                                                        Dims d, const uint32_t *__restrict__ offs,
+                                                       const uint32_t *__restrict__ counts,
                                                        const int *__restrict__ fbb, float4 *__restrict__ coords,
                                                        float *__restrict__ values, uint64_t capacity) {
     __shared__ uint32_t ws[kThreads / 32];
+    // empty chunk (most of a sparse coreset's volume): its count is known
+    // from the dilation, so skip the mask read and the scan (CTA-uniform)
+    if (counts[blockIdx.x] == 0) return;
     const uint32_t total = (uint32_t)d.n * d.Z * d.Y * d.Wx;
     const uint32_t g = blockIdx.x * kThreads + threadIdx.x;
     const int lane = threadIdx.x & 31, w = threadIdx.x >> 5;
@@ -861,7 +865,7 @@ fh_status fh_coreset_emit(const float *vol, const uint32_t dims_xyz[3], int n_fr
     const char *w = reinterpret_cast<const char *>(workspace);
     { emit_kernel<<<(unsigned)L.nchunks, kThreads, 0, s>>>(
         reinterpret_cast<const uint32_t *>(w + L.dm), vol, d, reinterpret_cast<const uint32_t *>(w + L.offs),
-        reinterpret_cast<const int *>(w + L.fbb), reinterpret_cast<float4 *>(coords), values, capacity); fh::count_launch(); }
+        reinterpret_cast<const uint32_t *>(w + L.counts), reinterpret_cast<const int *>(w + L.fbb), reinterpret_cast<float4 *>(coords), values, capacity); fh::count_launch(); }
     return cuda_check(cudaGetLastError(), "fh_coreset_emit launch");
 }
 
