@@ -131,7 +131,7 @@ fh_status fh_build_levels_lin(const fh_level_res *res, int L, int F, fh_dtype ta
  * trilinear blend of the 8 corners of its (x,y,z) cell.  Table: level l,
  * frame k at entries offset_l + k T + [0, T); params = L n_frames T F.
  * The fh_encode_* calls accept the returned handle (fh_encode_indices then
- * writes [N][L][8]); the ordered variants and the trainer do not.
+ * writes [N][L][8]); the trainer does not.
  * Errors: FH_E_ARG, FH_E_RANGE. */
 fh_status fh_build_mhe(const uint32_t *res, int L, int F, fh_dtype table_dtype, uint64_t T,
                        uint32_t n_frames, fh_encoder *out);
@@ -196,47 +196,6 @@ fh_status fh_encode_bwd_ex(fh_encoder enc, const float *coords, int64_t N, const
  * corner order R3; w [N][L][16] f32 corner weights (may be NULL). */
 fh_status fh_encode_indices(fh_encoder enc, const float *coords, int64_t N, uint32_t *idx,
                             float *w, fh_stream stream);
-
-/* ------------------------------------------------- execution order ---
- * fh_spatial_sort -- an ORDER in which to process a batch so that nearby
- * samples run together (an execution-order optimisation, not part of the
- * method: the encode results are unchanged up to fp summation order).
- * Counting sort of the samples by a 16-bit Morton code of their bin on a
- * grid of 2^bits[a] bins per axis over [0,1]^4 (NaN -> 0, out-of-domain
- * clamped): the encoder shares the 16 bits greedily among the axes so that
- * bins are about cubic in cells of its finest level, and interleaves them
- * from the least significant end (key bit k = bit j of axis a for the j-th
- * round over the axes that still have bits; fh_spatial_sort_bits reports
- * bits[4] and the axis of every key bit).  order [N] uint32 (device)
- * receives a permutation of 0..N-1, sorted by key (order inside a bin
- * unspecified).  workspace (device, 16-byte aligned) of
- * fh_spatial_sort_workspace_size(N) bytes.  N < 2^32.
- * Errors: FH_E_ARG, FH_E_CUDA. */
-size_t    fh_spatial_sort_workspace_size(int64_t N);
-fh_status fh_spatial_sort(fh_encoder enc, const float *coords, int64_t N, uint32_t *order, void *workspace,
-                          size_t workspace_bytes, fh_stream stream);
-fh_status fh_spatial_sort_bits(fh_encoder enc, uint32_t bits[4], uint8_t axis_of_key_bit[16]);
-
-/* fh_encode_fwd_ordered / fh_encode_bwd_ordered -- as fh_encode_fwd /
- * fh_encode_bwd (same inputs, same outputs in the same [N][L*F] row order),
- * but the kernels visit the samples in `order` (device [N] uint32, a
- * permutation of 0..N-1, normally from fh_spatial_sort with this encoder).
- * Forward: the batch is cut into tiles of consecutive `order` positions
- * (<= 2048 samples, one CTA each); on the coarse / mid levels whose per-tile
- * box of vertices is small (planner: about <= 4 vertices per sample, and
- * half the shared memory), the box's table entries are copied into shared
- * memory once (cp.async, double-buffered across levels) and the 16 corners
- * of every sample are read there; other levels (and any tile whose box does
- * not fit) take the direct path.  Bit-identical to fh_encode_fwd for any
- * permutation.  Backward: on the most contended levels (>= 128 F samples
- * per cell) a warp of 32 consecutive samples groups lanes by cell and
- * issues one reduction per (group, corner); other levels take the direct
- * path.  Differs from fh_encode_bwd only in fp32 summation order.
- * MHE encoders: FH_E_ARG. */
-fh_status fh_encode_fwd_ordered(fh_encoder enc, const float *coords, int64_t N, const uint32_t *order,
-                                const void *table, void *out, fh_dtype out_dtype, fh_stream stream);
-fh_status fh_encode_bwd_ordered(fh_encoder enc, const float *coords, int64_t N, const uint32_t *order,
-                                const float *dout, float *dtable, fh_stream stream);
 
 /* fh_zero_grad -- dtable [sum T][F] f32 (device) := 0, stream-ordered
  * (cudaMemsetAsync).  Errors: FH_E_ARG (NULL), FH_E_CUDA. */

@@ -72,6 +72,15 @@ __device__ __forceinline__ uint32_t brick_index(const Level &lv, uint32_t X, uin
            (((T & 1u) * ez + (Z & 1u)) * ey + (Y & 1u)) * ex + (X & 1u);
 }
 
+// Entry of lattice vertex (X, Y, Z, T) of a level: Eq. 9, the brick order
+// (R21) or the R5 hash -- the per-vertex form of cell_of's corner indices
+// (used by encoding_stats, stats.cuh).
+__device__ __forceinline__ uint32_t vertex_entry(const Level &lv, uint32_t X, uint32_t Y, uint32_t Z, uint32_t Tt) {
+    if (lv.hashed == 0) return lv.offset + X + Y * lv.sy + Z * lv.sz + Tt * lv.st;
+    if (lv.hashed == 2) return lv.offset + brick_index(lv, X, Y, Z, Tt);
+    return lv.offset + (hash_x(X, (Y * kPy) ^ (Z * kPz) ^ (Tt * kPt)) & lv.mask);
+}
+
 // Cell of one (sample, level): base indices and fractions.
 struct Cell {
     uint32_t idx[16];
@@ -383,10 +392,8 @@ __global__ void __launch_bounds__(256, FwdMinBlocks<F>::value) fwd_kernel(const 
                                                   const float4 *__restrict__ coords, int64_t N,
                                                   const T *__restrict__ table, const T *__restrict__ tsh,
                                                   O *__restrict__ out, int *__restrict__ flag,
-                                                  const __grid_constant__ LevelList LL,
-                                                  const uint32_t *__restrict__ perm) {
-    // the levels LL.id[0..LL.n) of every sample (a level group: see DESIGN.md §8);
-    // perm (optional): process samples in this (spatially sorted) order
+                                                  const __grid_constant__ LevelList LL) {
+    // the levels LL.id[0..LL.n) of every sample (a level group: see DESIGN.md §8)
     __shared__ LevelSmem slv;
     load_levels(P, slv);
     const int L = P.L;
@@ -396,7 +403,7 @@ __global__ void __launch_bounds__(256, FwdMinBlocks<F>::value) fwd_kernel(const 
     if (j >= N) return;
     const int li = (int)(gid - j * lc);
     const int l = LL.id[li];
-    const int64_t n = perm ? (int64_t)__ldg(perm + j) : j;
+    const int64_t n = j;
     const Level lv = slv.get(l);
     const float4 p = __ldcs(coords + n);
     Cell c;
@@ -518,7 +525,7 @@ __global__ void __launch_bounds__(256) bwd_kernel(const __grid_constant__ Params
                                                   const float *__restrict__ dout, float *__restrict__ dtable,
                                                   float *__restrict__ gsh,
                                                   int *__restrict__ flag, const __grid_constant__ LevelList LL,
-                                                  const uint32_t *__restrict__ perm, uint32_t lo = 0,
+                                                  uint32_t lo = 0,
                                                   uint32_t span = 0, uint32_t rep_n = 0, int64_t rep_stride = 0,
                                                   const MergeJob mj = MergeJob{nullptr, 0, 0, 0}) {
     if ((int)blockIdx.x < mj.ctas) {   // the previous group's merge (see MergeJob)
@@ -538,7 +545,7 @@ __global__ void __launch_bounds__(256) bwd_kernel(const __grid_constant__ Params
     if (j >= N) return;
     const int li = (int)(gid - j * lc);
     const int l = LL.id[li];
-    const int64_t n = perm ? (int64_t)__ldg(perm + j) : j;
+    const int64_t n = j;
     const Level lv = slv.get(l);
     const float4 p = __ldcs(coords + n);
     Cell c;
@@ -622,7 +629,7 @@ __global__ void __launch_bounds__(256) bwd_small_kernel(const __grid_constant__ 
                                                         const __grid_constant__ SmallSet S,
                                                         const float4 *__restrict__ coords, int64_t N,
                                                         const float *__restrict__ dout, float *__restrict__ dtable,
-                                                        int *__restrict__ flag, const uint32_t *__restrict__ perm) {
+                                                        int *__restrict__ flag) {
     extern __shared__ float acc[];
     __shared__ LevelSmem slv;
     load_levels(P, slv);
@@ -643,7 +650,7 @@ __global__ void __launch_bounds__(256) bwd_small_kernel(const __grid_constant__ 
     auto fetch = [&](int64_t gid, float4 &pc, float (&gg)[F]) {
         const int64_t j = gid / S.n;
         const int li = (int)(gid - j * S.n);
-        const int64_t n = perm ? (int64_t)__ldg(perm + j) : j;
+        const int64_t n = j;
         pc = __ldg(coords + n);
 #pragma unroll
         for (int f = 0; f < F; f++) gg[f] = __ldg(dout + n * (int64_t)(L * F) + S.id[li] * F + f);

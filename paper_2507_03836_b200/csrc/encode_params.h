@@ -49,14 +49,4 @@ struct LevelList {
     int id[kMaxLevels];
 };
 
-// Morton key of the spatial sort (fh_spatial_sort): 16 bits; key bit k
-// (LSB first) is bit bit[k] of axis axis[k]'s bin index, bins per axis
-// 2^bits[a] (see fhash_api.cu make_key_spec).
-struct KeySpec {
-    uint8_t axis[16];
-    uint8_t bit[16];
-    uint8_t pos[4][16];   // key position of bit j of axis a
-    uint32_t bits[4];
-};
-
 }  // namespace fh

@@ -11,8 +11,6 @@
 
 #include "internal.h"
 #include "encode_kernels.cuh"
-#include "sort_kernels.cuh"
-#include "tiled_kernels.cuh"
 #include "mhe_kernels.cuh"
 
 namespace fh {
@@ -65,10 +63,6 @@ static fh_status ensure_flag(fh_encoder e) {
     };
     // Measured on B200 (cfg4, 305 MiB fp16 tables / 609 MiB grads): one pass
     // 6.06 / 19.95 ms fwd / bwd; groups of <= 0.55 L2: 2.98 / 6.34 ms.
-    if (const char *v = getenv("FH_TILE_S")) e->tile_s = atoi(v);
-    if (const char *v = getenv("FH_TILE_MARGIN")) e->tile_margin = atof(v);
-    if (const char *v = getenv("FH_FINE_ORDER")) e->fine_order = atoi(v) == 1;
-    if (const char *v = getenv("FH_AGG_MIN_DENSITY")) e->agg_density = atof(v);
     if (const char *v = getenv("FH_PAIR_SHIFT")) e->pair_shift = atoi(v);
     if (const char *v = getenv("FH_BWD_SPLIT")) e->bwd_split = atoi(v) != 0;
     if (const char *v = getenv("FH_FUSE_MERGE")) e->fuse_merge = atoi(v) != 0;
@@ -284,55 +278,9 @@ static int split_lists(fh_encoder e, const bool *include, double bytes_per_entry
     return n;
 }
 
-// ---------------------------------------------------------------- tiling
-// Tile plan of an ordered (spatially sorted) pass: samples per tile and the
-// levels whose per-tile vertex box is expected to fit box_bytes at
-// bytes_per_vertex (tiled_kernels.cuh).  The estimate follows the Morton key:
-// a tile of S of N sorted samples spans about S/N of the 2^16 key bins, i.e.
-// the lowest log2(2^16 S/N) key bits; counting those bits per axis gives its
-// extent in bins, hence in cells of level l.  A margin (default 1.5) covers
-// tiles that straddle two key blocks.  The kernel re-checks every (tile,
-// level) box and falls back to the direct global path when one does not fit.
-static void plan_tiles(fh_encoder e, int64_t N, double max_vertices, double per_sample, int box_bytes,
-                       fh::tiled::TileSet &ts, bool *tiled) {
-    using namespace fh::tiled;
-    const int64_t per_wave = (int64_t)e->n_sm * kMaxTile;
-    const int64_t waves = (N + per_wave - 1) / per_wave;
-    int64_t S = (N + (int64_t)e->n_sm * waves - 1) / ((int64_t)e->n_sm * waves);
-    if (S < 256) S = 256;
-    if (S > kMaxTile) S = kMaxTile;
-    if (e->tile_s > 0 && e->tile_s <= kMaxTile) S = e->tile_s;
-    ts.S = (int)S;
-    ts.box_bytes = box_bytes;
-    ts.n = 0;
-    double kbits = 16.0 + std::log2((double)S / (double)(N > 0 ? N : 1));
-    if (kbits > 16.0) kbits = 16.0;
-    if (kbits < 0.0) kbits = 0.0;
-    int low[4] = {0, 0, 0, 0};
-    const int kb = (int)std::ceil(kbits);
-    for (int k = 0; k < kb && k < 16; k++) low[e->key.axis[k]]++;
-    const double margin = e->tile_margin;
-    // staged boxes pay off up to per_sample vertices per sample (the kernels
-    // allow a larger bound for tiles that straddle key blocks)
-    const double cap = std::min(max_vertices, per_sample * (double)S);
-    for (int l = 0; l < e->L; l++) {
-        double V = 1.0;
-        for (int a = 0; a < 4; a++) {
-            const double frac = std::ldexp(1.0, low[a] - (int)e->key.bits[a]);
-            const double cells = (double)(e->info[l].res[a] - 1) * (frac < 1.0 ? frac : 1.0);
-            double verts = std::ceil(cells) + 2.0;
-            if (verts > e->info[l].res[a]) verts = e->info[l].res[a];
-            V *= verts;
-        }
-        tiled[l] = V * margin <= cap;
-        if (tiled[l]) ts.id[ts.n++] = l;
-    }
-}
-
 template <int F, typename T, typename O>
 static void launch_fwd(fh_encoder e, const float *coords, int64_t N, const void *table, void *out,
-                       cudaStream_t s, const uint32_t *perm) {
-    const uint32_t full_blocks = (uint32_t)((e->entries * (uint64_t)F * sizeof(T)) / 32);
+                       cudaStream_t s) {
     constexpr int kEb = F * (int)sizeof(T);
     // The shifted copy of the table: slot j holds entry j+1,
     // so an x-pair at (i, i+1), i odd, is ONE aligned load.  Per level: only
@@ -342,7 +290,7 @@ static void launch_fwd(fh_encoder e, const float *coords, int64_t N, const void 
     const T *tsh = nullptr;
     bool sh[FH_MAX_LEVELS] = {false};
     fh::Params prm = e->params;
-    if ((kEb == 4 || kEb == 8 || kEb == 16) && (e->pair_shift & 2) && e->kind == 0 && !perm && N >= (1 << 15)) {
+    if ((kEb == 4 || kEb == 8 || kEb == 16) && (e->pair_shift & 2) && e->kind == 0 && N >= (1 << 15)) {
         bool any = false;
         for (int l = 0; l < e->L; l++) {
             const double t = (double)e->info[l].table_size;
@@ -377,23 +325,6 @@ static void launch_fwd(fh_encoder e, const float *coords, int64_t N, const void 
     const float4 *c4 = reinterpret_cast<const float4 *>(coords);
     bool include[FH_MAX_LEVELS];
     for (int l = 0; l < e->L; l++) include[l] = true;
-    const uint32_t *dperm = perm;
-    if (perm) {
-        // ordered pass: coarse / mid levels tiled through shared memory
-        fh::tiled::TileSet ts;
-        const int box_bytes = e->smem_optin - 4096;
-        plan_tiles(e, N, (double)box_bytes / 2.0 / (F * sizeof(T)), 4.0, box_bytes, ts, include);  // two box buffers
-        for (int l = 0; l < e->L; l++) include[l] = !include[l];
-        if (ts.n > 0) {
-            cudaFuncSetAttribute(fh::tiled::fwd_tiled_kernel<F, T, O>, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                                 box_bytes);
-            const unsigned grid = (unsigned)((N + ts.S - 1) / ts.S);
-            { fh::tiled::fwd_tiled_kernel<F, T, O><<<grid, fh::tiled::kThreads, box_bytes, s>>>(
-                e->params, ts, c4, N, perm, reinterpret_cast<const T *>(table), full_blocks,
-                reinterpret_cast<O *>(out), e->flag); fh::count_launch(); }
-        }
-        if (!e->fine_order) dperm = nullptr;  // direct levels: natural order (coalesced rows)
-    }
     fh::LevelList lists[FH_MAX_LEVELS];
     // small batches (e.g. the renderer's ray batches) touch few entries: one
     // pass, fewer launches; large batches: L2-sized level groups
@@ -403,61 +334,18 @@ static void launch_fwd(fh_encoder e, const float *coords, int64_t N, const void 
     for (int g = 0; g < n; g++)
         { fh::fwd_kernel<F, T, O><<<grid_for(N, lists[g].n), 256, 0, s>>>(
             prm, c4, N, reinterpret_cast<const T *>(table), tsh, reinterpret_cast<O *>(out), e->flag,
-            lists[g], dperm); fh::count_launch(); }
+            lists[g]); fh::count_launch(); }
 }
 
 template <typename T, typename O>
 static void dispatch_fwd_F(fh_encoder e, const float *coords, int64_t N, const void *table, void *out,
-                           cudaStream_t s, const uint32_t *perm) {
+                           cudaStream_t s) {
     switch (e->F) {
-        case 1: launch_fwd<1, T, O>(e, coords, N, table, out, s, perm); break;
-        case 2: launch_fwd<2, T, O>(e, coords, N, table, out, s, perm); break;
-        case 4: launch_fwd<4, T, O>(e, coords, N, table, out, s, perm); break;
-        default: launch_fwd<8, T, O>(e, coords, N, table, out, s, perm); break;
+        case 1: launch_fwd<1, T, O>(e, coords, N, table, out, s); break;
+        case 2: launch_fwd<2, T, O>(e, coords, N, table, out, s); break;
+        case 4: launch_fwd<4, T, O>(e, coords, N, table, out, s); break;
+        default: launch_fwd<8, T, O>(e, coords, N, table, out, s); break;
     }
-}
-
-template <int F>
-static void launch_bwd_direct(fh_encoder e, const float4 *c4, int64_t N, const float *dout, float *dtable,
-                              cudaStream_t s, const uint32_t *perm, const bool *include) {
-    fh::LevelList lists[FH_MAX_LEVELS];
-    const int n = split_lists(e, include, (double)F * 4.0, e->bwd_limit, lists);
-    for (int g = 0; g < n; g++)
-        { fh::bwd_kernel<F><<<grid_for(N, lists[g].n), 256, 0, s>>>(e->params, c4, N, dout, dtable, nullptr, e->flag,
-                                                                   lists[g], perm); fh::count_launch(); }
-}
-
-// Ordered backward: levels where a sorted warp's samples nearly always share
-// a cell -- expected samples per cell >= FH_AGG_MIN_DENSITY, default 128 F --
-// run the warp-aggregated kernel in `order`; the others run the direct
-// kernel in natural order (FH_FINE_ORDER=1: in `order`).  Measured on B200
-// (tools/time_levels.py): aggregation wins only on the most contended
-// levels (cfg2 level 0: 163 -> 76 us, cfg4 level 0: 697 -> 496 us); at
-// lower densities its extra instructions cost more than the reductions it
-// saves.
-template <int F>
-static void launch_bwd_ordered(fh_encoder e, const float4 *c4, int64_t N, const float *dout, float *dtable,
-                               cudaStream_t s, const uint32_t *perm) {
-    const double dmin = e->agg_density >= 0.0 ? e->agg_density : 128.0 * F;
-    bool agg[FH_MAX_LEVELS], rest[FH_MAX_LEVELS];
-    for (int l = 0; l < e->L; l++) {
-        double cells = 1.0;
-        for (int a = 0; a < 4; a++) cells *= (double)(e->info[l].res[a] - 1);
-        agg[l] = (double)N / cells >= dmin;
-        rest[l] = !agg[l];
-    }
-    fh::LevelList lists[FH_MAX_LEVELS];
-    const int n = split_lists(e, agg, (double)F * 4.0, e->bwd_limit, lists);
-    const int smem = fh::tiled::kAggWarps * fh::tiled::AggLayout<F>::kWarpFloats * 4;
-    if (n > 0 && smem > 48 * 1024)
-        cudaFuncSetAttribute(fh::tiled::bwd_agg_kernel<F>, cudaFuncAttributeMaxDynamicSharedMemorySize, smem);
-    for (int g = 0; g < n; g++) {
-        const int64_t warps = (N + 31) / 32 * lists[g].n;
-        const unsigned grid = (unsigned)((warps + fh::tiled::kAggWarps - 1) / fh::tiled::kAggWarps);
-        { fh::tiled::bwd_agg_kernel<F><<<grid, fh::tiled::kAggThreads, smem, s>>>(e->params, lists[g], c4, N, perm, dout,
-                                                                           dtable, e->flag); fh::count_launch(); }
-    }
-    launch_bwd_direct<F>(e, c4, N, dout, dtable, s, e->fine_order ? perm : nullptr, rest);
 }
 
 static fh_status check_common(fh_encoder e, const float *coords, int64_t N, const char *who) {
@@ -467,39 +355,6 @@ static fh_status check_common(fh_encoder e, const float *coords, int64_t N, cons
     if (!aligned(coords, 16)) return fail(FH_E_ARG, "%s: coords not 16-byte aligned", who);
     if (N > (int64_t)1 << 40) return fail(FH_E_RANGE, "%s: N too large", who);
     return FH_OK;
-}
-
-// Morton key of fh_spatial_sort for this encoder (sort_kernels.cuh): 16
-// bits shared greedily among the axes, each next bit to the axis whose bins
-// are widest in cells of the finest level (most corners), so bins are about
-// cubic in cells; bits are interleaved from the least significant end
-// (position j of every axis that has more than j bits), so an aligned block
-// of 2^k consecutive keys is also about cubic in cells.
-static void make_key_spec(fh_encoder e) {
-    int fin = 0;
-    for (int l = 1; l < e->L; l++)
-        if (e->info[l].corners > e->info[fin].corners) fin = l;
-    double ext[4];
-    for (int a = 0; a < 4; a++) {
-        ext[a] = (double)(e->info[fin].res[a] - 1);
-        e->key.bits[a] = 0;
-    }
-    for (int k = 0; k < 16; k++) {
-        int best = 0;
-        for (int a = 1; a < 4; a++)
-            if (ext[a] > ext[best]) best = a;
-        e->key.bits[best]++;
-        ext[best] *= 0.5;
-    }
-    int pos = 0;
-    for (uint32_t j = 0; pos < 16; j++)
-        for (int a = 0; a < 4 && pos < 16; a++)
-            if (e->key.bits[a] > j) {
-                e->key.axis[pos] = (uint8_t)a;
-                e->key.bit[pos] = (uint8_t)j;
-                e->key.pos[a][j] = (uint8_t)pos;
-                pos++;
-            }
 }
 
 extern "C" {
@@ -602,7 +457,6 @@ fh_status fh_build_levels_lin(const fh_level_res *res, int L, int F, fh_dtype ta
         K.offset = (uint32_t)I.offset;
     }
     e->entries = off;
-    make_key_spec(e);
     *out = e;
     return FH_OK;
 }
@@ -769,7 +623,7 @@ static void dispatch_mhe_fwd(fh_encoder e, const float *coords, int64_t N, const
     }
 }
 
-static fh_status encode_fwd_impl(fh_encoder e, const float *coords, int64_t N, const uint32_t *perm,
+static fh_status encode_fwd_impl(fh_encoder e, const float *coords, int64_t N,
                                  const void *table, void *out, fh_dtype out_dtype, fh_stream stream) {
     g_err[0] = 0;
     fh_status st = check_common(e, coords, N, "fh_encode_fwd");
@@ -783,7 +637,6 @@ static fh_status encode_fwd_impl(fh_encoder e, const float *coords, int64_t N, c
     if ((st = ensure_flag(e)) != FH_OK) return st;
     cudaStream_t s = reinterpret_cast<cudaStream_t>(stream);
     if (e->kind == 1) {
-        if (perm) return fail(FH_E_ARG, "fh_encode_fwd_ordered: not supported for MHE encoders");
         if (e->table_dtype == FH_F32) {
             if (out_dtype == FH_F32) dispatch_mhe_fwd<float, float>(e, coords, N, table, out, s);
             else dispatch_mhe_fwd<float, __nv_bfloat16>(e, coords, N, table, out, s);
@@ -794,11 +647,11 @@ static fh_status encode_fwd_impl(fh_encoder e, const float *coords, int64_t N, c
         return cuda_check(cudaGetLastError(), "fh_encode_fwd (MHE) launch");
     }
     if (e->table_dtype == FH_F32) {
-        if (out_dtype == FH_F32) dispatch_fwd_F<float, float>(e, coords, N, table, out, s, perm);
-        else dispatch_fwd_F<float, __nv_bfloat16>(e, coords, N, table, out, s, perm);
+        if (out_dtype == FH_F32) dispatch_fwd_F<float, float>(e, coords, N, table, out, s);
+        else dispatch_fwd_F<float, __nv_bfloat16>(e, coords, N, table, out, s);
     } else {
-        if (out_dtype == FH_F32) dispatch_fwd_F<__half, float>(e, coords, N, table, out, s, perm);
-        else dispatch_fwd_F<__half, __nv_bfloat16>(e, coords, N, table, out, s, perm);
+        if (out_dtype == FH_F32) dispatch_fwd_F<__half, float>(e, coords, N, table, out, s);
+        else dispatch_fwd_F<__half, __nv_bfloat16>(e, coords, N, table, out, s);
     }
     return cuda_check(cudaGetLastError(), "fh_encode_fwd launch");
 }
@@ -821,7 +674,7 @@ static void launch_bwd_kernel(const BwdCall &b, dim3 g, const fh::LevelList &ll,
     const fh_encoder e = b.e;
     g.x += (unsigned)mj.ctas;   // the merge CTAs come first (blockIdx < mj.ctas)
 #define FH_BWD(FF, RR, GG)                                                                                     \
-    { fh::bwd_kernel<FF, RR><<<g, 256, 0, b.s>>>(e->params, b.c4, b.N, b.dout, dt, GG, e->flag, ll, nullptr, lo, span, \
+    { fh::bwd_kernel<FF, RR><<<g, 256, 0, b.s>>>(e->params, b.c4, b.N, b.dout, dt, GG, e->flag, ll, lo, span, \
                                                  rep_n, rep_stride, mj); fh::count_launch(); }
     switch (e->F) {
         case 1: if (ranged) FH_BWD(1, true, gsh) else FH_BWD(1, false, gsh) break;
@@ -834,7 +687,7 @@ static void launch_bwd_kernel(const BwdCall &b, dim3 g, const fh::LevelList &ll,
 
 // The few-cell levels (bwd_small_kernel): one launch with CTA (or per-warp)
 // copies for the non-tiny ones, one lane-private launch per tiny level.
-static fh_status bwd_small_levels(const BwdCall &b, const uint32_t *perm) {
+static fh_status bwd_small_levels(const BwdCall &b) {
     const fh_encoder e = b.e;
     const int optin = e->smem_optin > 0 ? e->smem_optin : 232448;
     for (int part = 0; part <= e->n_tiny; part++) {
@@ -867,7 +720,7 @@ static fh_status bwd_small_levels(const BwdCall &b, const uint32_t *perm) {
     q = cuda_check(cudaFuncSetAttribute(fh::bwd_small_kernel<FF>, cudaFuncAttributeMaxDynamicSharedMemorySize, \
                                         smem), "cudaFuncSetAttribute(bwd_small)");                           \
     if (q != FH_OK) return q;                                                                                 \
-    { fh::bwd_small_kernel<FF><<<g, threads, smem, b.s>>>(e->params, Sx, b.c4, b.N, b.dout, b.dtable, e->flag, perm); \
+    { fh::bwd_small_kernel<FF><<<g, threads, smem, b.s>>>(e->params, Sx, b.c4, b.N, b.dout, b.dtable, e->flag); \
       fh::count_launch(); }                                                                                   \
     break;
             case 1: FH_SMALL(1)
@@ -930,7 +783,7 @@ static bool bwd_replicated(const BwdCall &b, int l, dim3 g, const fh::LevelList 
     return true;
 }
 
-static fh_status encode_bwd_impl(fh_encoder e, const float *coords, int64_t N, const uint32_t *perm,
+static fh_status encode_bwd_impl(fh_encoder e, const float *coords, int64_t N,
                                  const float *dout, float *dtable, fh_stream stream,
                                  cudaEvent_t *ev = nullptr, int n_ev = 0, bool zero = false) {
     g_err[0] = 0;
@@ -950,24 +803,13 @@ static fh_status encode_bwd_impl(fh_encoder e, const float *coords, int64_t N, c
     if (!dout || !aligned(dout, vec > 16 ? 16 : vec)) return fail(FH_E_ARG, "fh_encode_bwd: NULL/misaligned dout");
     if ((st = ensure_flag(e)) != FH_OK) return st;
     const float4 *c4 = reinterpret_cast<const float4 *>(coords);
-    if (e->kind == 1 && perm) return fail(FH_E_ARG, "fh_encode_bwd_ordered: not supported for MHE encoders");
-    if (perm && zero && (st = zero_levels(0, e->L)) != FH_OK) return st;
-    if (perm) {
-        switch (e->F) {
-            case 1: launch_bwd_ordered<1>(e, c4, N, dout, dtable, s, perm); break;
-            case 2: launch_bwd_ordered<2>(e, c4, N, dout, dtable, s, perm); break;
-            case 4: launch_bwd_ordered<4>(e, c4, N, dout, dtable, s, perm); break;
-            default: launch_bwd_ordered<8>(e, c4, N, dout, dtable, s, perm); break;
-        }
-        return cuda_check(cudaGetLastError(), "fh_encode_bwd_ordered launch");
-    }
     const BwdCall b{e, c4, N, dout, dtable, s};
     // launch 0 (when present): the few-cell levels in shared memory
     if (e->small.n > 0) {
         if (zero)
             for (int j = 0; j < e->small.n; j++)
                 if ((st = zero_levels(e->small.id[j], e->small.id[j] + 1)) != FH_OK) return st;
-        if ((st = bwd_small_levels(b, perm)) != FH_OK) return st;
+        if ((st = bwd_small_levels(b)) != FH_OK) return st;
         if (ev && n_ev > 0) cudaEventRecord(ev[0], s);
     }
     const int ev0 = e->small.n > 0 ? 1 : 0;
@@ -1101,7 +943,7 @@ int bwd_launch_ranges(fh_encoder e, int i, int64_t *r, int max) {
 }
 fh_status encode_bwd_events(fh_encoder e, const float *coords, int64_t N, const float *dout, float *dtable,
                             fh_stream stream, cudaEvent_t *ev, int n_ev, bool overwrite) {
-    return encode_bwd_impl(e, coords, N, nullptr, dout, dtable, stream, ev, n_ev, overwrite);
+    return encode_bwd_impl(e, coords, N, dout, dtable, stream, ev, n_ev, overwrite);
 }
 }  // namespace fh
 
@@ -1109,66 +951,18 @@ extern "C" {
 
 fh_status fh_encode_fwd(fh_encoder e, const float *coords, int64_t N, const void *table, void *out,
                         fh_dtype out_dtype, fh_stream stream) {
-    return encode_fwd_impl(e, coords, N, nullptr, table, out, out_dtype, stream);
+    return encode_fwd_impl(e, coords, N, table, out, out_dtype, stream);
 }
 
 fh_status fh_encode_bwd_ex(fh_encoder e, const float *coords, int64_t N, const float *dout, float *dtable,
                            unsigned flags, fh_stream stream) {
     if (flags & ~(unsigned)FH_BWD_OVERWRITE) return fail(FH_E_ARG, "fh_encode_bwd_ex: unknown flags 0x%x", flags);
-    return encode_bwd_impl(e, coords, N, nullptr, dout, dtable, stream, nullptr, 0, (flags & FH_BWD_OVERWRITE) != 0);
+    return encode_bwd_impl(e, coords, N, dout, dtable, stream, nullptr, 0, (flags & FH_BWD_OVERWRITE) != 0);
 }
 
 fh_status fh_encode_bwd(fh_encoder e, const float *coords, int64_t N, const float *dout, float *dtable,
                         fh_stream stream) {
-    return encode_bwd_impl(e, coords, N, nullptr, dout, dtable, stream);
-}
-
-fh_status fh_encode_fwd_ordered(fh_encoder e, const float *coords, int64_t N, const uint32_t *order,
-                                const void *table, void *out, fh_dtype out_dtype, fh_stream stream) {
-    if (!order && N > 0) return fail(FH_E_ARG, "fh_encode_fwd_ordered: NULL order");
-    return encode_fwd_impl(e, coords, N, order, table, out, out_dtype, stream);
-}
-
-fh_status fh_encode_bwd_ordered(fh_encoder e, const float *coords, int64_t N, const uint32_t *order,
-                                const float *dout, float *dtable, fh_stream stream) {
-    if (!order && N > 0) return fail(FH_E_ARG, "fh_encode_bwd_ordered: NULL order");
-    return encode_bwd_impl(e, coords, N, order, dout, dtable, stream);
-}
-
-fh_status fh_spatial_sort_bits(fh_encoder e, uint32_t bits[4], uint8_t axis_of_key_bit[16]) {
-    g_err[0] = 0;
-    if (!e || !bits) return fail(FH_E_ARG, "fh_spatial_sort_bits: NULL pointer");
-    for (int a = 0; a < 4; a++) bits[a] = e->key.bits[a];
-    if (axis_of_key_bit)
-        for (int k = 0; k < 16; k++) axis_of_key_bit[k] = e->key.axis[k];
-    return FH_OK;
-}
-
-size_t fh_spatial_sort_workspace_size(int64_t N) {
-    return (size_t)(fh::sortk::kBins + fh::sortk::kScanBlocks) * 4 + ((size_t)(N < 0 ? 0 : N) * 2 + 255) / 256 * 256;
-}
-
-fh_status fh_spatial_sort(fh_encoder e, const float *coords, int64_t N, uint32_t *order, void *workspace,
-                          size_t ws_bytes, fh_stream stream) {
-    g_err[0] = 0;
-    if (!e) return fail(FH_E_ARG, "fh_spatial_sort: NULL encoder");
-    if (N < 0 || N > 0xFFFFFFFFll) return fail(FH_E_ARG, "fh_spatial_sort: N out of range");
-    if (N == 0) return FH_OK;
-    if (!coords || !aligned(coords, 16) || !order || !workspace || !aligned(workspace, 16))
-        return fail(FH_E_ARG, "fh_spatial_sort: NULL or misaligned pointer");
-    if (ws_bytes < fh_spatial_sort_workspace_size(N)) return fail(FH_E_ARG, "fh_spatial_sort: workspace too small");
-    cudaStream_t s = reinterpret_cast<cudaStream_t>(stream);
-    uint32_t *hist = reinterpret_cast<uint32_t *>(workspace);
-    uint32_t *sums = hist + fh::sortk::kBins;
-    uint16_t *keys = reinterpret_cast<uint16_t *>(sums + fh::sortk::kScanBlocks);
-    fh_status st = cuda_check(cudaMemsetAsync(hist, 0, fh::sortk::kBins * 4, s), "fh_spatial_sort memset");
-    if (st != FH_OK) return st;
-    int64_t g = (N + 255) / 256;
-    if (g > 148 * 16) g = 148 * 16;
-    { fh::sortk::key_hist_kernel<<<(unsigned)g, 256, 0, s>>>(e->key, reinterpret_cast<const float4 *>(coords), N, keys, hist); fh::count_launch(); }
-    { fh::sortk::scan_blocks_kernel<<<fh::sortk::kScanBlocks, 1024, 0, s>>>(hist, sums); fh::count_launch(); }
-    { fh::sortk::scatter_kernel<<<(unsigned)g, 256, 0, s>>>(keys, N, hist, sums, order); fh::count_launch(); }
-    return cuda_check(cudaGetLastError(), "fh_spatial_sort launch");
+    return encode_bwd_impl(e, coords, N, dout, dtable, stream);
 }
 
 fh_status fh_encode_indices(fh_encoder e, const float *coords, int64_t N, uint32_t *idx, float *w,

@@ -68,15 +68,8 @@ struct fh_encoder_s {
     bool rep[FH_MAX_LEVELS] = {false};               // backward: level reduced into replicated copies (own pass)
     bool fuse_merge = true;                          // FH_FUSE_MERGE=0: every group's merge as its own launch
     double fwd_limit = 0.0, bwd_limit = 0.0;         // L2 budgets of one direct pass (bytes; 0 = one pass)
-    fh::KeySpec key{};                               // Morton key of fh_spatial_sort (set by the builder)
     int n_sm = 148;                                  // SMs of the device (set with the status word)
     int smem_optin = 0;                              // max dynamic shared memory per CTA (opt-in)
-    // ordered-path knobs, read once from the environment when the encoder
-    // binds to its device (experiments; defaults in fhash_api.cu)
-    int tile_s = 0;                                  // FH_TILE_S: samples per tile (0 = auto)
-    double tile_margin = 1.25;                       // FH_TILE_MARGIN
-    bool fine_order = false;                         // FH_FINE_ORDER=1: direct levels in `order`
-    double agg_density = -1.0;                       // FH_AGG_MIN_DENSITY (< 0: 128 F)
     // Shifted-pair scratch, one slot per stream that ran a
     // large direct pass: tsh = the table shifted by one entry (forward),
     // gsh = zeroed fp32 gradient scratch shifted by two floats (backward).

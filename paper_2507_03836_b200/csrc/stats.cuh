@@ -30,7 +30,7 @@ __global__ void __launch_bounds__(256) stats_mark_kernel(const fh::Level lv, int
             b = lv.hashed ? (uint64_t)((x ^ (y * fh::kPy) ^ (z * fh::kPz)) & lv.mask)
                           : (uint64_t)x + (uint64_t)y * lv.sy + (uint64_t)z * lv.sz;
         } else {
-            b = (uint64_t)(fh::tiled::vertex_entry(lv, x, y, z, t) - lv.offset);
+            b = (uint64_t)(fh::vertex_entry(lv, x, y, z, t) - lv.offset);
         }
         if (b < T) atomicOr(bits + (b >> 5), 1u << (b & 31));
     }

@@ -27,8 +27,7 @@ EXPORTS = [
     "fh_fold_schedule", "fh_build_levels", "fh_level_info_get", "fh_num_levels", "fh_feature_dim",
     "fh_table_entries", "fh_param_count", "fh_encoder_destroy", "fh_encode_fwd", "fh_encode_bwd", "fh_encode_bwd_ex",
     "fh_encode_indices", "fh_zero_grad", "fh_encode_fwd_bwd", "fh_encode_step_host", "fh_status_sync", "fh_last_error",
-    "fh_version", "fh_spatial_sort_workspace_size", "fh_spatial_sort", "fh_encode_fwd_ordered",
-    "fh_encode_bwd_ordered", "fh_build_mhe", "fh_encoder_kind", "fh_spatial_sort_bits", "fh_build_levels_lin",
+    "fh_version", "fh_build_mhe", "fh_encoder_kind", "fh_build_levels_lin",
     # include/fhash_bench.h (measurement kernels)
     "fh_bench_gather", "fh_bench_red", "fh_bench_copy", "fh_bench_gather_levels", "fh_bench_red_levels",
     # train step
@@ -107,15 +106,6 @@ def lib() -> ctypes.CDLL:
     L.fh_encoder_scratch_size.restype = ctypes.c_size_t
     L.fh_encoder_attach_scratch.argtypes = [vp, vp, vp, ctypes.c_size_t]
     L.fh_encoder_attach_scratch.restype = c_int
-    L.fh_spatial_sort_workspace_size.argtypes = [i64]
-    L.fh_spatial_sort_workspace_size.restype = ctypes.c_size_t
-    L.fh_spatial_sort.argtypes = [vp, vp, i64, vp, vp, ctypes.c_size_t, vp]
-    L.fh_spatial_sort_bits.argtypes = [vp, ctypes.POINTER(ctypes.c_uint32), ctypes.POINTER(ctypes.c_uint8)]
-    L.fh_spatial_sort_bits.restype = c_int
-    L.fh_encode_fwd_ordered.argtypes = [vp, vp, i64, vp, vp, vp, c_int, vp]
-    L.fh_encode_bwd_ordered.argtypes = [vp, vp, i64, vp, vp, vp, vp]
-    for name in ("fh_spatial_sort", "fh_encode_fwd_ordered", "fh_encode_bwd_ordered"):
-        getattr(L, name).restype = c_int
     L.fh_encode_step_host.argtypes = [vp, vp, vp, i64, vp, vp, vp, vp, vp, vp, vp, vp]
     L.fh_status_sync.argtypes = [vp, vp]
     L.fh_bench_gather.argtypes = [vp, u64, c_int, i64, c_int, c_int, ctypes.c_uint32, vp, vp]
@@ -232,16 +222,6 @@ class Encoder:
         _check(lib().fh_encode_indices(self._h, _ptr(coords), N, _ptr(idx), _ptr(w), _stream(stream)))
         return idx, w
 
-    def fwd_ordered(self, coords, order, table, out, out_dtype: str = "f32", stream=None):
-        _check(lib().fh_encode_fwd_ordered(self._h, _ptr(coords), coords.shape[0], _ptr(order), _ptr(table),
-                                           _ptr(out), _DT[out_dtype], _stream(stream)))
-        return out
-
-    def bwd_ordered(self, coords, order, dout, dtable, stream=None):
-        _check(lib().fh_encode_bwd_ordered(self._h, _ptr(coords), coords.shape[0], _ptr(order), _ptr(dout),
-                                           _ptr(dtable), _stream(stream)))
-        return dtable
-
     def level_stats(self, l: int, stream=None):
         """encoding_stats of level l on the GPU (fh_level_stats): (distinct
         buckets, collisions, utilisation) -- same tuple as the oracle's."""
@@ -270,13 +250,6 @@ class Encoder:
         else:
             _check(lib().fh_encoder_attach_scratch(self._h, _stream(stream), _ptr(buf),
                                                    buf.numel() * buf.element_size()))
-
-    def sort_bits(self):
-        """(bits per axis [4], axis of each of the 16 key bits, LSB first)."""
-        b = (ctypes.c_uint32 * 4)()
-        ax = (ctypes.c_uint8 * 16)()
-        _check(lib().fh_spatial_sort_bits(self._h, b, ax))
-        return list(b), list(ax)
 
     def zero_grad(self, dtable, stream=None):
         _check(lib().fh_zero_grad(self._h, _ptr(dtable), _stream(stream)))
@@ -667,27 +640,6 @@ class MHEEncoder(Encoder):
         w = torch.empty((N, self.L, 8), dtype=torch.float32, device=coords.device) if want_w else None
         _check(lib().fh_encode_indices(self._h, _ptr(coords), N, _ptr(idx), _ptr(w), _stream(stream)))
         return idx, w
-
-
-class SpatialOrder:
-    """Reusable device buffers for fh_spatial_sort (execution order of a
-    batch, keyed by the encoder's Morton bit allocation)."""
-
-    def __init__(self, enc: "Encoder", max_n: int, device=None):
-        import torch
-        dev = device or torch.device("cuda", torch.cuda.current_device())
-        self.enc = enc
-        self.max_n = max_n
-        self.order = torch.empty(max_n, dtype=torch.int32, device=dev)
-        nb = int(lib().fh_spatial_sort_workspace_size(max_n))
-        self.ws = torch.empty(nb, dtype=torch.uint8, device=dev)
-
-    def __call__(self, coords, stream=None):
-        N = coords.shape[0]
-        assert N <= self.max_n
-        _check(lib().fh_spatial_sort(self.enc.handle, _ptr(coords), N, _ptr(self.order), _ptr(self.ws), self.ws.numel(),
-                                     _stream(stream)))
-        return self.order[:N]
 
 
 # ------------------------------------------------------------ NEXT-4 coreset

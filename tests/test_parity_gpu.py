@@ -234,91 +234,6 @@ def test_single_level_extremes():
     check_fwd(got, r, ab)
 
 
-def morton_keys(enc, coords):
-    """The documented fh_spatial_sort key (include/fhash.h): per-axis bins
-    2^bits[a], key bit k = bit j of axis axis[k] for its j-th occurrence."""
-    bits, axis = enc.sort_bits()
-    assert sum(bits) == 16
-    c = np.clip(np.nan_to_num(coords, nan=0.0), 0, 1).astype(np.float32)
-    q = [np.minimum(np.floor(c[:, a] * np.float32(2 ** bits[a])).astype(np.int64), 2 ** bits[a] - 1)
-         for a in range(4)]
-    key = np.zeros(len(coords), np.int64)
-    seen = [0, 0, 0, 0]
-    for k, a in enumerate(axis):
-        key |= ((q[a] >> seen[a]) & 1) << k
-        seen[a] += 1
-    assert seen == bits
-    return key
-
-
-def ordered_check(cfg, case, order_kind="sorted", seed=0):
-    """fh_encode_fwd_ordered must be bit-identical to fh_encode_fwd (same
-    per-(sample, level) arithmetic, smem copies are exact); the backward meets
-    the bar against the oracle."""
-    N = len(case.coords)
-    enc = fh.Encoder(cfg.levels, cfg.F, cfg.table_dtype, cfg.cap)
-    c, t, g = dev(case.coords), dev(case.table), dev(case.dout)
-    if order_kind == "sorted":
-        so = fh.SpatialOrder(enc, N)
-        order = so(c)
-        o = order.cpu().numpy().view(np.uint32)
-        assert np.array_equal(np.sort(o), np.arange(N, dtype=np.uint32))
-        assert np.all(np.diff(morton_keys(enc, case.coords)[o]) >= 0)
-    else:
-        order = torch.from_numpy(np.random.default_rng(seed).permutation(N).astype(np.int32)).cuda()
-    a = enc.fwd(c, t)
-    b = enc.fwd_ordered(c, order, t, torch.empty_like(a))
-    assert torch.equal(a, b)
-    dt = torch.zeros((enc.entries, cfg.F), device="cuda")
-    enc.bwd_ordered(c, order, g, dt)
-    st = enc.status_sync()
-    ref = oracle.Levels(cfg.levels, cfg.cap)
-    G, A = ref.backward(case.coords, case.dout, cfg.F, want_abs=True)
-    check_bwd(dt.cpu().numpy().astype(np.float64), G, A)
-    return st
-
-
-@pytest.mark.parametrize("cfg", [W.CFG1, W.CFG1H, W.CFG3], ids=lambda c: c.name)
-@pytest.mark.parametrize("N", [20000 + 3, 4096, 77])
-def test_spatial_order_and_tiled_kernels(cfg, N):
-    """Sorted order (the tiled path): every level whose tile box fits is
-    staged in shared memory; bit-identical forward, backward within the bar."""
-    assert ordered_check(cfg, W.encode_case(cfg, N, seed=6)) == fh.FH_OK
-
-
-@pytest.mark.parametrize("cfg", [W.CFG1H, W.CFG3], ids=lambda c: c.name)
-def test_tiled_kernels_random_order_fallback(cfg):
-    """A random permutation makes every tile span the whole domain: the
-    levels planned as tiled (from the sorted estimate) exceed shared memory
-    in the kernel and fall back to the direct global path tile by tile."""
-    assert ordered_check(cfg, W.encode_case(cfg, 30011, seed=7), order_kind="random") == fh.FH_OK
-
-
-@pytest.mark.parametrize("F", [1, 2, 4, 8])
-@pytest.mark.parametrize("tdt", ["f32", "f16"])
-def test_tiled_feature_widths(F, tdt):
-    """Every F (the backward warp reduce-scatter of 16 F values has a
-    different shape per F) and both table dtypes through the tiled path."""
-    cfg = W.EncoderConfig("f", W.cfg1_levels(), F=F, cap=1 << 11, table_dtype=tdt)
-    assert ordered_check(cfg, W.encode_case(cfg, 9001, seed=F)) == fh.FH_OK
-
-
-@pytest.mark.parametrize("S", [256, 300, 2048])
-def test_tiled_tile_sizes(S, monkeypatch):
-    """Tile sizes: the minimum, a ragged one, the maximum (FH_TILE_S)."""
-    monkeypatch.setenv("FH_TILE_S", str(S))
-    cfg = W.CFG3
-    assert ordered_check(cfg, W.encode_case(cfg, 10007, seed=S)) == fh.FH_OK
-
-
-def test_tiled_out_of_domain_flagged():
-    cfg = W.CFG1
-    bad = W.bad_coords()
-    coords = np.concatenate([bad, W.draw_coords(W.rng(3), 3000)])
-    case = W.encode_case(cfg, len(coords), seed=2, coords=coords)
-    assert ordered_check(cfg, case) == fh.FH_E_DOMAIN
-
-
 # ------------------------------------------ NEXT-2: brick linearization (R21)
 BRICK_LEVELS = [W.cfg1_levels(), ((5, 7, 9, 3), (13, 3, 6, 7), (2, 2, 2, 2), (17, 2, 11, 5)),
                 tuple(oracle.fold_schedule((200, 110, 54), 10, 2)[3:])]
@@ -346,9 +261,8 @@ def test_brick_indices_forward_backward(levels, cap):
     check_bwd(gb, G, A)
 
 
-def test_brick_edges_and_ordered_path():
-    """Brick order at the domain edges / lattice points, and through the
-    ordered (tiled forward, aggregated backward) path."""
+def test_brick_edges():
+    """Brick order at the domain edges / lattice points."""
     cfg = W.EncoderConfig("brick", W.cfg1_levels(), F=2, cap=0, table_dtype="f32")
     coords = np.concatenate([W.edge_coords(), W.draw_coords(W.rng(12), 6000)])
     case = W.encode_case(cfg, len(coords), seed=12, coords=coords)
@@ -358,12 +272,10 @@ def test_brick_edges_and_ordered_path():
     assert np.array_equal(idx.cpu().numpy().view(np.uint32), ref.indices(coords)[0])
     c, t, g = dev(case.coords), dev(case.table), dev(case.dout)
     a = enc.fwd(c, t)
-    order = fh.SpatialOrder(enc, len(coords))(c)
-    assert torch.equal(a, enc.fwd_ordered(c, order, t, torch.empty_like(a)))
     r, ab = ref.forward(coords, case.table, want_abs=True)
     check_fwd(a.cpu().numpy().astype(np.float64), r, ab)
     dt = torch.zeros((enc.entries, 2), device="cuda")
-    enc.bwd_ordered(c, order, g, dt)
+    enc.bwd(c, g, dt)
     G, A = ref.backward(coords, case.dout, 2, want_abs=True)
     check_bwd(dt.cpu().numpy().astype(np.float64), G, A)
 
@@ -405,15 +317,6 @@ def test_cfg2_full_size_parity():
     gb, _ = run_bwd(enc, case)
     G, A = ref.backward(case.coords, case.dout, cfg.F, want_abs=True)
     check_bwd(gb, G, A)
-
-
-def test_cfg2_full_size_tiled_parity():
-    """The bench's sorted + tiled launch at full cfg2 size: forward
-    bit-identical to the direct path on every row, backward on every entry
-    against the oracle."""
-    cfg = W.CFG2
-    case = W.encode_case(cfg, W.N_CFG2, seed=0)
-    assert ordered_check(cfg, case) == fh.FH_OK
 
 
 def test_cfg4_sampled_rows_and_adjoint():

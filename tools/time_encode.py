@@ -34,34 +34,23 @@ def main():
     dtab = torch.zeros((enc.entries, cfg.F), device="cuda")
     flush = torch.empty(256 << 20, dtype=torch.uint8, device="cuda")
     e = [torch.cuda.Event(enable_timing=True) for _ in range(4)]
-    sorted_mode = os.environ.get("FH_SORTED", "0") == "1"
-    so = fh.SpatialOrder(enc, N) if sorted_mode else None
-    tf = tb = ts = 0.0
+    tf = tb = 0.0
     overwrite = os.environ.get("FH_OVERWRITE", "0") == "1"   # bwd overwrites dtable (no separate zero_grad)
     for it in range(iters + 3):
         flush.fill_(it & 255)
         if not overwrite:
             enc.zero_grad(dtab)
-        e[0].record()
-        order = so(coords) if so else None
         e[1].record()
-        if so:
-            enc.fwd_ordered(coords, order, table, out)
-        else:
-            enc.fwd(coords, table, out)
+        enc.fwd(coords, table, out)
         e[2].record()
-        if so:
-            enc.bwd_ordered(coords, order, dout, dtab)
-        else:
-            enc.bwd(coords, dout, dtab, overwrite=overwrite)
+        enc.bwd(coords, dout, dtab, overwrite=overwrite)
         e[3].record()
         torch.cuda.synchronize()
         if it >= 3:
-            ts += e[0].elapsed_time(e[1])
             tf += e[1].elapsed_time(e[2])
             tb += e[2].elapsed_time(e[3])
-    tot = (ts + tf + tb) / iters
-    print(f"{os.path.basename(fh.LIB_PATH)} {name}{' sorted' if so else ''} lin={enc.lin}: sort {ts / iters:.4f} ms  "
+    tot = (tf + tb) / iters
+    print(f"{os.path.basename(fh.LIB_PATH)} {name} lin={enc.lin}: "
           f"fwd {tf / iters:.4f} ms  bwd {tb / iters:.4f} ms  ({N / (tot / 1e3) / 1e6:.1f} M samples/s)")
 
 
