@@ -11,7 +11,9 @@
  * Conventions shared by every entry point
  *   - Plain pointers and sizes only.  "device" pointers are CUDA global
  *     memory on the current device, allocated and OWNED BY THE CALLER; the
- *     library owns only the opaque host handles it returns.
+ *     library owns only the opaque host handles it returns and one 16-byte
+ *     status word per encoder (made by fh_build_levels / fh_build_mhe on
+ *     the current device).  No stream-ordered call allocates device memory.
  *   - Every call that takes a stream is stream-ordered on it and does NOT
  *     synchronise (except fh_status_sync).  stream may be NULL (legacy
  *     default stream).
@@ -94,9 +96,15 @@ fh_status fh_fold_schedule(const uint32_t S_xyz[3], uint32_t n_t, uint32_t fold,
  *   of two; a level with C_l > cap becomes a hashed level of T_l = cap
  *   entries (R5; the paper never caps).
  * Errors: FH_E_ARG (L, F, R < 2, cap not a power of two, dtype);
- * FH_E_RANGE if sum_l T_l * F >= 2^32.  On success *out owns a host handle
- * (no device memory until the first encode call, which allocates a 16-byte
- * status word on the current device). */
+ * FH_E_RANGE if sum_l T_l * F >= 2^32; FH_E_CUDA if the status word
+ * cannot be made.  On success *out owns a host handle, bound to the
+ * current device: its launch plan (L2-sized level groups, few-cell and
+ * replicated backward levels) is fixed here from the device's L2 size and
+ * SM count, and a 16-byte status word is allocated there (synchronously:
+ * this is set-up, not a stream-ordered call).  Built with no CUDA device
+ * present, the handle answers the host queries (level info, scratch size)
+ * and every device call returns FH_E_STATE; calls from another device
+ * also return FH_E_STATE. */
 fh_status fh_build_levels(const fh_level_res *res, int L, int F, fh_dtype table_dtype,
                           uint64_t cap, fh_encoder *out);
 
@@ -158,14 +166,15 @@ void      fh_encoder_destroy(fh_encoder enc);
  * (device, 32-byte aligned: x-pairs of corners are fetched as aligned
  * 2-entry chunks); out [N][L*F] of out_dtype FH_F32 or FH_BF16 (device),
  * row n = (level 0 features, level 1 features, ...).
- * Scratch: large passes use encoder-owned scratch of the calling stream
- * (the table shifted by one entry, and in fh_encode_bwd a
- * shifted gradient scratch), allocated on the stream's first large pass
- * (never while the stream is capturing a graph: such a pass runs without
- * it).  Calls of one encoder are therefore safe concurrently on different
- * streams; a graph captured on stream s reuses s's scratch, so do not
- * replay it concurrently with other passes of the same encoder on s.
- * N = 0 is a no-op.  Errors: FH_E_ARG (NULL/misaligned, dtype), FH_E_CUDA. */
+ * Scratch: large passes use the caller-owned scratch attached to the
+ * calling stream (fh_encoder_attach_scratch; the table
+ * shifted by one entry, and in fh_encode_bwd a shifted gradient scratch);
+ * a stream without one runs without the shifted pairs (same results).
+ * Calls of one encoder are safe concurrently on different streams, each
+ * with its own scratch; do not run two passes of one encoder concurrently
+ * on the SAME stream's scratch (e.g. a replayed graph and a live call).
+ * N = 0 is a no-op.  Errors: FH_E_ARG (NULL/misaligned, dtype),
+ * FH_E_STATE (no device state / wrong device), FH_E_CUDA. */
 fh_status fh_encode_fwd(fh_encoder enc, const float *coords, int64_t N, const void *table,
                         void *out, fh_dtype out_dtype, fh_stream stream);
 
@@ -219,8 +228,7 @@ fh_status fh_encode_fwd_bwd(fh_encoder enc, const float *coords, int64_t N, cons
  * without waiting.  Stream-ordered, so a caller pipelines consecutive steps
  * by rotating over several streams with their own device buffers and host
  * outputs: step k+1's H2D then overlaps step k's kernels and step k-1's D2H
- * (bench.py's e2e uses three).  The encoder keeps its shifted-pair scratch
- * per stream, so concurrent steps on different streams do not share it.
+ * (bench.py's e2e uses three), each stream with its own attached scratch.
  * Errors: as the calls it makes. */
 fh_status fh_encode_step_host(fh_encoder enc, const float *coords_h, const float *dout_h,
                               int64_t N, const void *table_d, float *coords_d, float *dout_d,
@@ -408,13 +416,16 @@ size_t    fh_level_stats_workspace_size(fh_encoder enc, int level);
 fh_status fh_level_stats(fh_encoder enc, int level, void *workspace, size_t workspace_bytes, uint64_t *out,
                          fh_stream stream);
 
-/* fh_encoder_scratch_size / fh_encoder_attach_scratch -- caller-owned
- * shifted-pair scratch (see fh_encode_fwd).  By default the encoder
- * allocates it itself per stream on the first large pass; a caller that
- * owns all device memory instead attaches fh_encoder_scratch_size(enc)
- * bytes (device, 256-byte aligned, covers every pass of this encoder) for
- * `stream`.  The library never grows or frees attached memory; ptr = NULL
- * detaches (after synchronising `stream`).  0 / FH_E_ARG for MHE encoders;
+/* fh_encoder_scratch_size / fh_encoder_attach_scratch -- the caller-owned
+ * shifted-pair scratch (see fh_encode_fwd), one per stream:
+ * fh_encoder_scratch_size(enc) bytes (device, 256-byte aligned; covers every
+ * pass of this encoder: the table copy up to the last level the forward may
+ * shift, the fp32 gradient scratch of the shiftable backward levels or the
+ * 64 replicated copies of a replicated level).  No initial contents are
+ * needed: each range is written or zeroed right before use.  The library
+ * never allocates, grows or frees it; ptr = NULL detaches (after
+ * synchronising `stream`: attach is set-up, not stream-ordered).  Size 0 /
+ * FH_E_ARG for MHE encoders; FH_E_ARG if too small or misaligned;
  * FH_E_STATE if all 8 stream slots are taken. */
 size_t    fh_encoder_scratch_size(fh_encoder enc);
 fh_status fh_encoder_attach_scratch(fh_encoder enc, fh_stream stream, void *ptr, size_t bytes);

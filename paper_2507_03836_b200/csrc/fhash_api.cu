@@ -23,25 +23,74 @@ using fh::dtype_size;
 using fh::fail;
 using fh::g_err;
 
-// Make sure the encoder's status word exists on the current device.
-static fh_status ensure_flag(fh_encoder e) {
-    std::lock_guard<std::mutex> lock(e->mu);
-    int dev = -1;
-    if (cudaGetDevice(&dev) != cudaSuccess) return fail(FH_E_CUDA, "cudaGetDevice failed");
-    if (e->flag) {
-        if (dev != e->device) return fail(FH_E_STATE, "encoder used on device %d, flag lives on %d", dev, e->device);
-        return FH_OK;
+// Launch shape of the few-cell backward launches (bwd_small_kernel), fixed
+// per encoder: part 0 = the CTA-copy levels, part p = tiny level p - 1
+// (lane-private copies).  The kernel's dynamic shared-memory limit is raised
+// once here, so the backward makes no attribute calls.
+static fh_status plan_small(fh_encoder e) {
+    const int optin = e->smem_optin > 0 ? e->smem_optin : 232448;
+    int smem_max = 0;
+    for (int part = 0; part <= e->n_tiny; part++) {
+        const fh::SmallSet &S = part == 0 ? e->small_cta : e->small_tiny[part - 1];
+        fh_encoder_s::SmallPlan &pl = e->small_plan[part];
+        pl = fh_encoder_s::SmallPlan{};
+        if (S.n == 0) continue;
+        int threads = 256, smem = S.total * 4, copies = 1;
+        int64_t cap;
+        if (part == 0) {   // one copy per warp when 8 fit in 64 KB (fewer CAS retries between warps:
+                           // Combustion's 728-entry level 161 -> 144 us), else one per CTA
+            const bool pw = e->small_warp_copies && 8 * S.total * 4 <= 64 * 1024;
+            copies = pw ? 8 : 1;
+            smem = copies * S.total * 4;
+            const int per_sm = 232448 / (smem + 2048);
+            const int mx = pw ? 4 : 2;
+            cap = (int64_t)e->n_sm * (per_sm < 1 ? 1 : per_sm > mx ? mx : per_sm);
+        } else {           // lane-private copies: whole warps per CTA, as many CTAs per SM as fit
+            const int w = (optin - 4096 - smem) / (S.ttotal * 4 * 32);
+            threads = (w > 8 ? 8 : w < 1 ? 1 : w) * 32;
+            smem += threads * S.ttotal * 4;
+            const int per_sm = 232448 / (smem + 2048);   // the SM's shared memory, not the per-CTA opt-in
+            cap = (int64_t)e->n_sm * (per_sm < 1 ? 1 : per_sm > 8 ? 8 : per_sm);
+        }
+        pl.threads = threads;
+        pl.smem = smem;
+        pl.copies = copies;
+        pl.cap = cap;
+        smem_max = smem > smem_max ? smem : smem_max;
     }
-    fh_status s = cuda_check(cudaMalloc(&e->flag, 16), "cudaMalloc(status word)");
-    if (s != FH_OK) return s;
-    s = cuda_check(cudaMemset(e->flag, 0, 16), "cudaMemset(status word)");
-    if (s != FH_OK) return s;
-    e->device = dev;
-    // Level groups from the device's L2 size.
-    int l2 = 0;
-    cudaDeviceGetAttribute(&l2, cudaDevAttrL2CacheSize, dev);
-    cudaDeviceGetAttribute(&e->n_sm, cudaDevAttrMultiProcessorCount, dev);
-    cudaDeviceGetAttribute(&e->smem_optin, cudaDevAttrMaxSharedMemoryPerBlockOptin, dev);
+    if (!e->flag || smem_max == 0) return FH_OK;
+    const void *k = e->F == 1 ? (const void *)fh::bwd_small_kernel<1> : e->F == 2 ? (const void *)fh::bwd_small_kernel<2>
+                  : e->F == 4 ? (const void *)fh::bwd_small_kernel<4> : (const void *)fh::bwd_small_kernel<8>;
+    return cuda_check(cudaFuncSetAttribute(k, cudaFuncAttributeMaxDynamicSharedMemorySize, smem_max),
+                      "cudaFuncSetAttribute(bwd_small)");
+}
+
+// Device binding of a new encoder (end of fh_build_levels / fh_build_mhe):
+// the launch plan (level groups from the device's L2 size, the few-cell and
+// replicated backward levels, the shifted-pair levels), the SM count and
+// shared-memory limit, and the 16-byte status word -- the library's ONLY
+// device allocation, made here once so that no encode call allocates or
+// synchronises.  Without a CUDA device (host-only use: level queries,
+// scratch sizing) the plan uses B200 defaults, no status word is made, and
+// every device call returns FH_E_STATE.
+static fh_status bind_device(fh_encoder e) {
+    int ndev = 0, dev = -1;
+    int l2 = 126 * 1048576;   // B200 L2 (cudaDevAttrL2CacheSize) when no device is present
+    if (cudaGetDeviceCount(&ndev) == cudaSuccess && ndev > 0 && cudaGetDevice(&dev) == cudaSuccess) {
+        fh_status s = cuda_check(cudaMalloc(&e->flag, 16), "cudaMalloc(status word)");
+        if (s != FH_OK) return s;
+        if ((s = cuda_check(cudaMemset(e->flag, 0, 16), "cudaMemset(status word)")) != FH_OK) {
+            cudaFree(e->flag);
+            e->flag = nullptr;
+            return s;
+        }
+        e->device = dev;
+        cudaDeviceGetAttribute(&l2, cudaDevAttrL2CacheSize, dev);
+        cudaDeviceGetAttribute(&e->n_sm, cudaDevAttrMultiProcessorCount, dev);
+        cudaDeviceGetAttribute(&e->smem_optin, cudaDevAttrMaxSharedMemoryPerBlockOptin, dev);
+    } else {
+        cudaGetLastError();   // clear "no device"
+    }
     auto budget = [&](const char *env, double frac) -> double {
         const char *v = getenv(env);
         if (v) return atof(v) * 1048576.0;  // MiB; 0 = one group
@@ -151,11 +200,12 @@ static fh_status ensure_flag(fh_encoder e) {
         // reductions it saves (measured: Combustion fold-2 shape).
         for (int q = 0; q < e->L; q++) {
             const double g = (double)e->info[q].table_size * e->F * 4.0;
-            e->shiftable[q] = (e->pair_shift & 1) && e->kind == 0 && e->F <= 2 && (lim <= 0.0 || 2.0 * g <= lim);
+            e->shiftable[q] = (e->pair_shift & 1) && e->kind == 0 && e->F == 2 && (lim <= 0.0 || 2.0 * g <= lim);
         }
         // contended mid-size levels (not small, at most FH_REP_MAX_T entries):
         // a pass of their own into replicated gradient copies (see the
-        // backward launch loop), F <= 2 (the copies live in the shifted scratch)
+        // backward launch loop), F == 2 (the copies live in the shifted scratch;
+        // F == 1 would need 4-entry alignment of the copies and the merge)
         // Measured: the Combustion fold-2 shape's 4900-entry level 223 ->
         // ~150 us replicated; cfg2's 8192-entry level slower in a pass of its
         // own than mixed with the other levels (bwd 0.713 -> 0.758 ms), so
@@ -163,7 +213,7 @@ static fh_status ensure_flag(fh_encoder e) {
         const char *rv = getenv("FH_REP_MAX_T");
         const uint64_t rep_max = rv ? (uint64_t)atoll(rv) : 8191;
         for (int q = 0; q < e->L; q++)
-            e->rep[q] = e->kind == 0 && e->F <= 2 && (e->pair_shift & 1) && !small[q] &&
+            e->rep[q] = e->kind == 0 && e->F == 2 && (e->pair_shift & 1) && !small[q] &&
                         e->info[q].table_size <= rep_max;
         e->n_gb = 0;
         int l = 0;
@@ -183,48 +233,29 @@ static fh_status ensure_flag(fh_encoder e) {
             e->n_gb++;
         }
     }
-    return FH_OK;
+    return plan_small(e);
 }
 
 // ------------------------------------------------------- shifted-pair scratch
-// Whether a direct pass of N samples uses the shifted pairs:
-// the copy / merge it costs streams the table once, so it pays when the
-// pass gathers at least about as many corners as the table has entries.
-// The scratch slot of `stream` with at least tsh_bytes / gsh_bytes (a zeroed
-// gsh), allocated on first use; nullptr when no slot is free or the stream
-// is capturing a graph (the caller then runs without the shifted pairs).
+// The shifted-pair scratch is caller-owned: attached per
+// stream with fh_encoder_attach_scratch.  A pass on a stream without one
+// (or with one too small) runs without the shifted pairs -- same results,
+// fewer aligned pair accesses.  Lookup only: never allocates.
 static fh_encoder_s::Scratch *get_scratch(fh_encoder e, cudaStream_t s, size_t tsh_bytes, size_t gsh_bytes) {
     std::lock_guard<std::mutex> lock(e->mu);
-    fh_encoder_s::Scratch *slot = nullptr;
     for (auto &sc : e->scratch)
-        if (sc.stream == (void *)s && (sc.tsh || sc.gsh)) { slot = &sc; break; }
-    if (!slot)
-        for (auto &sc : e->scratch)
-            if (!sc.tsh && !sc.gsh) { slot = &sc; break; }
-    if (!slot) return nullptr;
-    const bool need_t = tsh_bytes > slot->tsh_bytes, need_g = gsh_bytes > slot->gsh_bytes;
-    if ((need_t || need_g) && slot->caller) return nullptr;   // caller-owned scratch is never grown
-    if (need_t || need_g) {
-        cudaStreamCaptureStatus cs = cudaStreamCaptureStatusNone;
-        if (cudaStreamIsCapturing(s, &cs) != cudaSuccess || cs != cudaStreamCaptureStatusNone) return nullptr;
-        if (need_t) {
-            void *p = nullptr;
-            if (cudaMalloc(&p, tsh_bytes) != cudaSuccess) { cudaGetLastError(); return nullptr; }
-            if (slot->tsh) cudaFree(slot->tsh);
-            slot->tsh = p;
-            slot->tsh_bytes = tsh_bytes;
-        }
-        if (need_g) {
-            void *p = nullptr;
-            if (cudaMalloc(&p, gsh_bytes) != cudaSuccess) { cudaGetLastError(); return nullptr; }
-            if (cudaMemsetAsync(p, 0, gsh_bytes, s) != cudaSuccess) { cudaFree(p); cudaGetLastError(); return nullptr; }
-            if (slot->gsh) { cudaStreamSynchronize(s); cudaFree(slot->gsh); }
-            slot->gsh = reinterpret_cast<float *>(p);
-            slot->gsh_bytes = gsh_bytes;
-        }
-    }
-    slot->stream = (void *)s;
-    return slot;
+        if (sc.stream == (void *)s && (sc.tsh || sc.gsh))
+            return (tsh_bytes <= sc.tsh_bytes && gsh_bytes <= sc.gsh_bytes) ? &sc : nullptr;
+    return nullptr;
+}
+
+// Encode calls need the device state bind_device made, on its device.
+static fh_status device_ready(fh_encoder e) {
+    if (!e->flag) return fail(FH_E_STATE, "encoder was built without a CUDA device");
+    int dev = -1;
+    if (cudaGetDevice(&dev) != cudaSuccess) return fail(FH_E_CUDA, "cudaGetDevice failed");
+    if (dev != e->device) return fail(FH_E_STATE, "encoder bound to device %d used on device %d", e->device, dev);
+    return FH_OK;
 }
 
 // ------------------------------------------------------------------ launches
@@ -304,15 +335,20 @@ static void launch_fwd(fh_encoder e, const float *coords, int64_t N, const void 
             if (sh[l] && e->info[l].offset + e->info[l].table_size > end) end = e->info[l].offset + e->info[l].table_size;
         fh_encoder_s::Scratch *sc = any ? get_scratch(e, s, (size_t)end * kEb, 0) : nullptr;
         if (sc) {
-            // one copy per run of consecutive shifted levels
+            // one copy per run of consecutive shifted levels: slot j = entry
+            // j + 1 for the run's entries [b, en).  An odd pair (i, i + 1)
+            // reads slots (i - 1, i), so a run starting at an odd b also
+            // needs slot b - 1 (= entry b); slot b - 1 then lies in the
+            // unshifted level before the run, which never reads tsh.
             for (int l = 0; l < e->L;) {
                 if (!sh[l]) { l++; continue; }
                 int r = l;
                 while (r + 1 < e->L && sh[r + 1]) r++;
                 const uint64_t b = e->info[l].offset, en = e->info[r].offset + e->info[r].table_size;
-                if (en - b > 1)
-                    cudaMemcpyAsync(reinterpret_cast<char *>(sc->tsh) + b * kEb,
-                                    reinterpret_cast<const char *>(table) + (b + 1) * kEb, (en - b - 1) * kEb,
+                const uint64_t s0 = b - (b & 1);
+                if (en - s0 > 1)
+                    cudaMemcpyAsync(reinterpret_cast<char *>(sc->tsh) + s0 * kEb,
+                                    reinterpret_cast<const char *>(table) + (s0 + 1) * kEb, (en - s0 - 1) * kEb,
                                     cudaMemcpyDeviceToDevice, s);
                 l = r + 1;
             }
@@ -457,6 +493,8 @@ fh_status fh_build_levels_lin(const fh_level_res *res, int L, int F, fh_dtype ta
         K.offset = (uint32_t)I.offset;
     }
     e->entries = off;
+    const fh_status st = bind_device(e);
+    if (st != FH_OK) { delete e; return st; }
     *out = e;
     return FH_OK;
 }
@@ -481,11 +519,6 @@ void fh_encoder_destroy(fh_encoder e) {
         cudaGetDevice(&cur);
         if (cur != e->device) cudaSetDevice(e->device);
         cudaFree(e->flag);
-        for (auto &sc : e->scratch) {
-            if (sc.caller) continue;
-            if (sc.tsh) cudaFree(sc.tsh);
-            if (sc.gsh) cudaFree(sc.gsh);
-        }
         if (cur != e->device && cur >= 0) cudaSetDevice(cur);
     }
     delete e;
@@ -538,6 +571,8 @@ fh_status fh_build_mhe(const uint32_t *res, int L, int F, fh_dtype table_dtype, 
         K.offset = (uint32_t)I.offset;
     }
     e->entries = off;
+    const fh_status st = bind_device(e);
+    if (st != FH_OK) { delete e; return st; }
     *out = e;
     return FH_OK;
 }
@@ -546,22 +581,34 @@ int fh_encoder_kind(fh_encoder e) { return e ? e->kind : -1; }
 
 unsigned long long fh_kernel_launches(void) { return fh::g_launches.load(std::memory_order_relaxed); }
 
+// Scratch bytes of one stream slot: tsh up to the end of the last level the
+// forward may shift (table + copy within half the forward group budget),
+// then gsh up to the end of the last shiftable backward level, or the 64
+// replicated copies of a replicated level if larger.
 static size_t scratch_parts(fh_encoder e, size_t *tsh_bytes, size_t *gsh_bytes) {
-    const size_t t = (size_t)e->entries * e->F * dtype_size(e->table_dtype);
-    size_t g = e->F <= 2 ? (size_t)e->entries * e->F * 4 + 64 : 0;
-    for (int l = 0; l < e->L; l++)   // 64 replicated copies of a replicated level (set by ensure_flag)
+    const size_t kEb = (size_t)e->F * dtype_size(e->table_dtype);
+    uint64_t tend = 0, gend = 0;
+    size_t g = 0;
+    for (int l = 0; l < e->L; l++) {
+        const fh_level_info &I = e->info[l];
+        if ((kEb == 4 || kEb == 8 || kEb == 16) && (e->pair_shift & 2) &&
+            (e->fwd_limit <= 0.0 || 4.0 * (double)I.table_size * kEb <= e->fwd_limit))
+            tend = I.offset + I.table_size;
+        if (e->shiftable[l]) gend = I.offset + I.table_size;
         if (e->rep[l]) {
-            const size_t stride = (size_t)((e->info[l].table_size + 2) * e->F + 3) / 4 * 4;
+            const size_t stride = (size_t)((I.table_size + 2) * e->F + 3) / 4 * 4;
             if (64 * stride * 4 > g) g = 64 * stride * 4;
         }
-    const size_t ta = (t + 255) / 256 * 256;
+    }
+    if (gend > 0 && (size_t)gend * e->F * 4 + 64 > g) g = (size_t)gend * e->F * 4 + 64;
+    const size_t ta = ((size_t)tend * kEb + 255) / 256 * 256;
     if (tsh_bytes) *tsh_bytes = ta;
     if (gsh_bytes) *gsh_bytes = g;
     return ta + g;
 }
 
 size_t fh_encoder_scratch_size(fh_encoder e) {
-    if (!e || e->kind != 0 || ensure_flag(e) != FH_OK) return 0;
+    if (!e || e->kind != 0) return 0;
     return scratch_parts(e, nullptr, nullptr);
 }
 
@@ -569,38 +616,31 @@ fh_status fh_encoder_attach_scratch(fh_encoder e, fh_stream stream, void *ptr, s
     g_err[0] = 0;
     if (!e) return fail(FH_E_ARG, "fh_encoder_attach_scratch: NULL encoder");
     if (e->kind != 0) return fail(FH_E_ARG, "fh_encoder_attach_scratch: MHE encoders use no scratch");
-    fh_status st = ensure_flag(e);
-    if (st != FH_OK) return st;
+    size_t tb, gb;
+    const size_t need = scratch_parts(e, &tb, &gb);
+    if (ptr && (bytes < need || !aligned(ptr, 256)))
+        return fail(FH_E_ARG, "fh_encoder_attach_scratch: need %zu bytes, 256-byte aligned", need);
     std::lock_guard<std::mutex> lock(e->mu);
     void *s = stream;
     fh_encoder_s::Scratch *slot = nullptr;
     for (auto &sc : e->scratch)
         if (sc.stream == s && (sc.tsh || sc.gsh)) { slot = &sc; break; }
     if (slot) {   // detach / replace: stream-ordered with earlier passes on this stream
-        if ((st = cuda_check(cudaStreamSynchronize(reinterpret_cast<cudaStream_t>(stream)), "attach_scratch sync")) != FH_OK)
-            return st;
-        if (!slot->caller) {
-            if (slot->tsh) cudaFree(slot->tsh);
-            if (slot->gsh) cudaFree(slot->gsh);
-        }
+        fh_status st = cuda_check(cudaStreamSynchronize(reinterpret_cast<cudaStream_t>(stream)), "attach_scratch sync");
+        if (st != FH_OK) return st;
         *slot = fh_encoder_s::Scratch{};
     }
-    if (!ptr) return FH_OK;   // detached: the library allocates again on demand
-    size_t tb, gb;
-    const size_t need = scratch_parts(e, &tb, &gb);
-    if (bytes < need || !aligned(ptr, 256))
-        return fail(FH_E_ARG, "fh_encoder_attach_scratch: need %zu bytes, 256-byte aligned", need);
+    if (!ptr || need == 0) return FH_OK;   // detached (or nothing to shift): passes run without the shifted pairs
     if (!slot)
         for (auto &sc : e->scratch)
             if (!sc.tsh && !sc.gsh) { slot = &sc; break; }
     if (!slot) return fail(FH_E_STATE, "fh_encoder_attach_scratch: all %d stream slots in use", fh_encoder_s::kScratchSlots);
     slot->stream = s;
-    slot->caller = true;
-    slot->tsh = ptr;
+    slot->tsh = tb ? ptr : nullptr;
     slot->tsh_bytes = tb;
     slot->gsh = gb ? reinterpret_cast<float *>(reinterpret_cast<char *>(ptr) + tb) : nullptr;
     slot->gsh_bytes = gb;
-    if (!slot->gsh) slot->gsh_bytes = 0;
+    if (!slot->tsh && !slot->gsh) *slot = fh_encoder_s::Scratch{};
     return FH_OK;
 }
 
@@ -634,7 +674,7 @@ static fh_status encode_fwd_impl(fh_encoder e, const float *coords, int64_t N,
     if (!table || !aligned(table, 32)) return fail(FH_E_ARG, "fh_encode_fwd: NULL or not 32-byte aligned table");
     const size_t ovec = (size_t)e->F * dtype_size(out_dtype);
     if (!out || !aligned(out, ovec > 16 ? 16 : ovec)) return fail(FH_E_ARG, "fh_encode_fwd: NULL/misaligned out");
-    if ((st = ensure_flag(e)) != FH_OK) return st;
+    if ((st = device_ready(e)) != FH_OK) return st;
     cudaStream_t s = reinterpret_cast<cudaStream_t>(stream);
     if (e->kind == 1) {
         if (e->table_dtype == FH_F32) {
@@ -689,39 +729,19 @@ static void launch_bwd_kernel(const BwdCall &b, dim3 g, const fh::LevelList &ll,
 // copies for the non-tiny ones, one lane-private launch per tiny level.
 static fh_status bwd_small_levels(const BwdCall &b) {
     const fh_encoder e = b.e;
-    const int optin = e->smem_optin > 0 ? e->smem_optin : 232448;
     for (int part = 0; part <= e->n_tiny; part++) {
         const fh::SmallSet &S = part == 0 ? e->small_cta : e->small_tiny[part - 1];
         if (S.n == 0) continue;
-        int threads = 256, smem = S.total * 4;
-        int64_t cap;
+        const fh_encoder_s::SmallPlan &pl = e->small_plan[part];
         fh::SmallSet Sx = S;
-        if (part == 0) {   // one copy per warp when 8 fit in 64 KB (fewer CAS retries between warps:
-                           // Combustion's 728-entry level 161 -> 144 us), else one per CTA
-            const bool pw = e->small_warp_copies && 8 * S.total * 4 <= 64 * 1024;
-            Sx.copies = pw ? 8 : 1;
-            smem = Sx.copies * S.total * 4;
-            const int per_sm = 232448 / (smem + 2048);
-            const int mx = pw ? 4 : 2;
-            cap = (int64_t)e->n_sm * (per_sm < 1 ? 1 : per_sm > mx ? mx : per_sm);
-        } else {           // lane-private copies: whole warps per CTA, as many CTAs per SM as fit
-            const int w = (optin - 4096 - smem) / (S.ttotal * 4 * 32);
-            threads = (w > 8 ? 8 : w < 1 ? 1 : w) * 32;
-            smem += threads * S.ttotal * 4;
-            const int per_sm = 232448 / (smem + 2048);   // the SM's shared memory, not the per-CTA opt-in
-            cap = (int64_t)e->n_sm * (per_sm < 1 ? 1 : per_sm > 8 ? 8 : per_sm);
-        }
-        int64_t blocks = (b.N * S.n + threads - 1) / threads;
-        if (blocks > cap) blocks = cap;
+        Sx.copies = pl.copies;
+        int64_t blocks = (b.N * S.n + pl.threads - 1) / pl.threads;
+        if (blocks > pl.cap) blocks = pl.cap;
         const dim3 g((unsigned)blocks);
-        fh_status q = FH_OK;
         switch (e->F) {
-#define FH_SMALL(FF)                                                                                          \
-    q = cuda_check(cudaFuncSetAttribute(fh::bwd_small_kernel<FF>, cudaFuncAttributeMaxDynamicSharedMemorySize, \
-                                        smem), "cudaFuncSetAttribute(bwd_small)");                           \
-    if (q != FH_OK) return q;                                                                                 \
-    { fh::bwd_small_kernel<FF><<<g, threads, smem, b.s>>>(e->params, Sx, b.c4, b.N, b.dout, b.dtable, e->flag); \
-      fh::count_launch(); }                                                                                   \
+#define FH_SMALL(FF)                                                                                                 \
+    { fh::bwd_small_kernel<FF><<<g, pl.threads, pl.smem, b.s>>>(e->params, Sx, b.c4, b.N, b.dout, b.dtable, e->flag); \
+      fh::count_launch(); }                                                                                          \
     break;
             case 1: FH_SMALL(1)
             case 2: FH_SMALL(2)
@@ -801,7 +821,7 @@ static fh_status encode_bwd_impl(fh_encoder e, const float *coords, int64_t N,
     };
     if (N == 0) return zero ? zero_levels(0, e->L) : FH_OK;
     if (!dout || !aligned(dout, vec > 16 ? 16 : vec)) return fail(FH_E_ARG, "fh_encode_bwd: NULL/misaligned dout");
-    if ((st = ensure_flag(e)) != FH_OK) return st;
+    if ((st = device_ready(e)) != FH_OK) return st;
     const float4 *c4 = reinterpret_cast<const float4 *>(coords);
     const BwdCall b{e, c4, N, dout, dtable, s};
     // launch 0 (when present): the few-cell levels in shared memory
@@ -918,7 +938,7 @@ namespace fh {
 // ranges each one finalises -- for callers that overlap the gradient
 // reduction with the rest of the backward (train_api.cu).
 int bwd_launch_count(fh_encoder e) {
-    if (!e || ensure_flag(e) != FH_OK) return -1;
+    if (!e) return -1;
     return (e->small.n > 0 ? 1 : 0) + e->n_gb;
 }
 int bwd_launch_ranges(fh_encoder e, int i, int64_t *r, int max) {
@@ -972,7 +992,7 @@ fh_status fh_encode_indices(fh_encoder e, const float *coords, int64_t N, uint32
     if (st != FH_OK) return st;
     if (N == 0) return FH_OK;
     if (!idx || !aligned(idx, 16) || !aligned(w, 16)) return fail(FH_E_ARG, "fh_encode_indices: NULL/misaligned output");
-    if ((st = ensure_flag(e)) != FH_OK) return st;
+    if ((st = device_ready(e)) != FH_OK) return st;
     cudaStream_t s = reinterpret_cast<cudaStream_t>(stream);
     if (e->kind == 1)
         { fh::mhe::indices_kernel<<<grid_for(N, e->L), 256, 0, s>>>(

@@ -53,7 +53,7 @@ struct fh_encoder_s {
     fh_level_info info[FH_MAX_LEVELS];
     uint64_t entries = 0;
     fh::Params params;
-    int *flag = nullptr;  // sticky domain flag (device), allocated lazily
+    int *flag = nullptr;  // sticky domain flag (device), allocated by fh_build_levels (bind_device)
     int device = -1;
     // Level groups: consecutive levels whose table (fwd) or
     // fp32 grad (bwd) footprint fits an L2 budget run as one pass, so the
@@ -64,29 +64,30 @@ struct fh_encoder_s {
     fh::SmallSet small_cta{};                        // ... launch with CTA copies (non-tiny levels)
     fh::SmallSet small_tiny[FH_MAX_LEVELS];          // ... one launch per tiny level (lane-private copies)
     int n_tiny = 0;
+    struct SmallPlan { int threads = 0, smem = 0, copies = 1; int64_t cap = 0; };
+    SmallPlan small_plan[FH_MAX_LEVELS + 1];         // launch shape of each few-cell launch (plan_small)
     bool small_warp_copies = true;                   // FH_SMALL_WARP=0: one CTA copy instead of per-warp copies
     bool rep[FH_MAX_LEVELS] = {false};               // backward: level reduced into replicated copies (own pass)
     bool fuse_merge = true;                          // FH_FUSE_MERGE=0: every group's merge as its own launch
     double fwd_limit = 0.0, bwd_limit = 0.0;         // L2 budgets of one direct pass (bytes; 0 = one pass)
     int n_sm = 148;                                  // SMs of the device (set with the status word)
     int smem_optin = 0;                              // max dynamic shared memory per CTA (opt-in)
-    // Shifted-pair scratch, one slot per stream that ran a
-    // large direct pass: tsh = the table shifted by one entry (forward),
-    // gsh = zeroed fp32 gradient scratch shifted by two floats (backward).
-    // Allocated on first use; freed with the encoder.
+    bool mlp_attrs_set[4] = {false, false, false, false};   // fh_infer: MLP kernel smem limits raised (n_in/16 - 1)
+    // Shifted-pair scratch, one caller-owned slot per
+    // stream (fh_encoder_attach_scratch): tsh = the table shifted by one
+    // entry (forward), gsh = fp32 gradient scratch shifted by two floats
+    // (backward; each range is zeroed right before the launch that uses it).
     struct Scratch {
         void *stream = nullptr;
         void *tsh = nullptr;
         size_t tsh_bytes = 0;
         float *gsh = nullptr;
         size_t gsh_bytes = 0;
-        bool caller = false;   // attached by fh_encoder_attach_scratch: caller-owned, never grown or freed
     };
     static constexpr int kScratchSlots = 8;
     Scratch scratch[kScratchSlots];
     int pair_shift = 3;                              // FH_PAIR_SHIFT bits: 1 backward, 2 forward (default both)
-    std::mutex mu;                                   // guards the lazy device state (status word, scratch slots)
-                                                     // against host threads sharing the encoder
+    std::mutex mu;                                   // guards the scratch slots against host threads sharing the encoder
     bool shiftable[FH_MAX_LEVELS] = {false};         // backward: level uses the shifted gradient pairs
     bool bwd_split = true;                           // FH_BWD_SPLIT=0: no entry-range passes for big levels
 };

@@ -30,6 +30,7 @@ struct fh_trainer_s {
     float *loss_scratch = nullptr;
     cudaEvent_t bwd_ev[FH_MAX_LEVELS + 1] = {};  // caller's events, recorded after each backward launch
     int n_bwd_ev = 0;
+    bool flags_cleared = false;        // the workspace flags are zeroed on the first step's stream
 };
 
 namespace {
@@ -37,14 +38,40 @@ namespace {
 size_t align_up(size_t v, size_t a) { return (v + a - 1) / a * a; }
 
 // The MLP kernel's per-slot gradient partials: 2 slots x (at most) one CTA
-// per SM of the current device.
-int device_sms() {
-    int dev = 0, n = 148;
-    if (cudaGetDevice(&dev) == cudaSuccess) cudaDeviceGetAttribute(&n, cudaDevAttrMultiProcessorCount, dev);
-    return n > 0 ? n : 148;
+// per SM of the encoder's device.
+size_t partial_bytes(fh_encoder enc, int K0) {
+    return align_up((size_t)2 * enc->n_sm * ((fh::mlp::param_count(K0) + 3) / 4 * 4) * 4, 256);
 }
-size_t partial_bytes(int K0) {
-    return align_up((size_t)2 * device_sms() * ((fh::mlp::param_count(K0) + 3) / 4 * 4) * 4, 256);
+
+template <int K0>
+int mlp_smem() {
+    using Lo = fh::mlp::Layout<K0>;
+    // enough dynamic smem to keep ONE CTA per SM (the kernel owns all 512
+    // TMEM columns of its SM)
+    return (int)(Lo::SMEM > 120 * 1024 ? Lo::SMEM : 120 * 1024);
+}
+
+// Raise the MLP kernels' dynamic shared-memory limits once (trainer
+// creation / first inference), never on the step path.
+fh_status set_mlp_attrs(int K0) {
+    auto set = [](const void *k, int smem) {
+        return cuda_check(cudaFuncSetAttribute(k, cudaFuncAttributeMaxDynamicSharedMemorySize, smem),
+                          "cudaFuncSetAttribute(mlp)");
+    };
+    fh_status st = FH_OK;
+    switch (K0) {
+        case 16: st = set((const void *)fh::mlp::mlp_train_kernel<16>, mlp_smem<16>()); break;
+        case 32: st = set((const void *)fh::mlp::mlp_train_kernel<32>, mlp_smem<32>()); break;
+        case 48: st = set((const void *)fh::mlp::mlp_train_kernel<48>, mlp_smem<48>()); break;
+        default: st = set((const void *)fh::mlp::mlp_train_kernel<64>, mlp_smem<64>()); break;
+    }
+    if (st != FH_OK) return st;
+    switch (K0) {
+        case 16: return set((const void *)fh::mlp::mlp_infer_kernel<16>, (int)fh::mlp::InferLayout<16>::SMEM);
+        case 32: return set((const void *)fh::mlp::mlp_infer_kernel<32>, (int)fh::mlp::InferLayout<32>::SMEM);
+        case 48: return set((const void *)fh::mlp::mlp_infer_kernel<48>, (int)fh::mlp::InferLayout<48>::SMEM);
+        default: return set((const void *)fh::mlp::mlp_infer_kernel<64>, (int)fh::mlp::InferLayout<64>::SMEM);
+    }
 }
 
 fh_status check_mlp(fh_encoder enc, const fh_mlp_desc *m) {
@@ -60,14 +87,7 @@ fh_status check_mlp(fh_encoder enc, const fh_mlp_desc *m) {
 template <int K0>
 fh_status launch_mlp(fh_trainer tr, const float *target, int64_t N, int64_t N_global, float *loss,
                      cudaStream_t s) {
-    using Lo = fh::mlp::Layout<K0>;
-    // Request enough dynamic smem to keep ONE CTA per SM (the kernel owns all
-    // 512 TMEM columns of its SM).
-    const int smem = (int)(Lo::SMEM > 120 * 1024 ? Lo::SMEM : 120 * 1024);
-    fh_status st = cuda_check(cudaFuncSetAttribute(fh::mlp::mlp_train_kernel<K0>,
-                                                   cudaFuncAttributeMaxDynamicSharedMemorySize, smem),
-                              "cudaFuncSetAttribute(mlp)");
-    if (st != FH_OK) return st;
+    const int smem = mlp_smem<K0>();
     fh::mlp::TrainArgs a;
     a.x = tr->enc_out;
     a.target = target;
@@ -104,7 +124,7 @@ size_t fh_train_workspace_size(fh_encoder enc, const fh_mlp_desc *m, int64_t max
     if (!enc || !m || max_batch < 0) return 0;
     const size_t K0 = (size_t)m->n_in;
     return align_up((size_t)max_batch * K0 * 2, 256) + align_up((size_t)max_batch * K0 * 4, 256) + 256 +
-           partial_bytes(m->n_in);
+           partial_bytes(enc, m->n_in);
 }
 
 fh_status fh_trainer_create(fh_encoder enc, const fh_mlp_desc *m, const fh_train_buffers *b, const fh_adam *adam,
@@ -115,6 +135,7 @@ fh_status fh_trainer_create(fh_encoder enc, const fh_mlp_desc *m, const fh_train
     fh_status st = check_mlp(enc, m);
     if (st != FH_OK) return st;
     if (max_batch < 1) return fail(FH_E_ARG, "fh_trainer_create: max_batch < 1");
+    if (!enc->flag) return fail(FH_E_STATE, "fh_trainer_create: encoder was built without a CUDA device");
     const void *need16[] = {b->table_master, b->table_grad, b->table_m, b->table_v, b->mlp_master,
                             b->mlp_grad, b->mlp_m, b->mlp_v, b->mlp_shadow, b->workspace};
     for (const void *p : need16)
@@ -134,9 +155,7 @@ fh_status fh_trainer_create(fh_encoder enc, const fh_mlp_desc *m, const fh_train
     tr->b = *b;
     tr->adam = *adam;
     tr->max_batch = max_batch;
-    int dev = 0;
-    cudaGetDevice(&dev);
-    cudaDeviceGetAttribute(&tr->n_sm, cudaDevAttrMultiProcessorCount, dev);
+    tr->n_sm = enc->n_sm;
     char *w = reinterpret_cast<char *>(b->workspace);
     tr->enc_out = reinterpret_cast<__nv_bfloat16 *>(w);
     w += align_up((size_t)max_batch * tr->K0 * 2, 256);
@@ -145,8 +164,8 @@ fh_status fh_trainer_create(fh_encoder enc, const fh_mlp_desc *m, const fh_train
     tr->flag = reinterpret_cast<int *>(w);
     tr->loss_scratch = reinterpret_cast<float *>(w + 16);
     tr->partial = reinterpret_cast<float *>(w + 256);
-    st = cuda_check(cudaMemset(tr->flag, 0, 32), "fh_trainer_create: clear flags");
-    if (st != FH_OK) { delete tr; return st; }
+    // no device work here: the flags are cleared on the first step's stream
+    if ((st = set_mlp_attrs(tr->K0)) != FH_OK) { delete tr; return st; }
     *out = tr;
     return FH_OK;
 }
@@ -160,7 +179,12 @@ fh_status fh_train_fwd_bwd(fh_trainer tr, const float *coords, const float *targ
     if (N > 0 && (!coords || !target)) return fail(FH_E_ARG, "fh_train_fwd_bwd: NULL coords/target");
     cudaStream_t s = reinterpret_cast<cudaStream_t>(stream);
     float *loss = loss_dev ? loss_dev : tr->loss_scratch;
-    fh_status st = cuda_check(cudaMemsetAsync(loss, 0, sizeof(float), s), "zero loss");
+    fh_status st;
+    if (!tr->flags_cleared) {
+        if ((st = cuda_check(cudaMemsetAsync(tr->flag, 0, 32, s), "clear trainer flags")) != FH_OK) return st;
+        tr->flags_cleared = true;
+    }
+    st = cuda_check(cudaMemsetAsync(loss, 0, sizeof(float), s), "zero loss");
     if (st != FH_OK) return st;
     // the step's gradients OVERWRITE the grad buffers: the MLP kernel adds
     // into zeroed MLP grads; the encode backward zeroes each table level
@@ -168,9 +192,15 @@ fh_status fh_train_fwd_bwd(fh_trainer tr, const float *coords, const float *targ
     st = cuda_check(cudaMemsetAsync(tr->b.mlp_grad, 0, (size_t)fh::mlp::param_count(tr->K0) * sizeof(float), s),
                     "zero mlp_grad");
     if (st != FH_OK) return st;
-    if (N == 0)
-        return cuda_check(cudaMemsetAsync(tr->b.table_grad, 0, (size_t)tr->enc->entries * tr->enc->F * sizeof(float), s),
-                          "zero table_grad");
+    if (N == 0) {   // no samples on this rank: zero gradients, and the caller's
+                    // per-launch events still mark them final (DP overlap)
+        st = cuda_check(cudaMemsetAsync(tr->b.table_grad, 0, (size_t)tr->enc->entries * tr->enc->F * sizeof(float), s),
+                        "zero table_grad");
+        if (st != FH_OK) return st;
+        for (int i = 0; i < tr->n_bwd_ev; i++)
+            if ((st = cuda_check(cudaEventRecord(tr->bwd_ev[i], s), "record bwd event")) != FH_OK) return st;
+        return FH_OK;
+    }
     const void *table = tr->b.table_shadow ? tr->b.table_shadow : tr->b.table_master;
     if ((st = fh_encode_fwd(tr->enc, coords, N, table, tr->enc_out, FH_BF16, stream)) != FH_OK) return st;
     switch (tr->K0) {
@@ -421,6 +451,7 @@ fh_status fh_trainer_status(fh_trainer tr, fh_stream stream) {
     fh_status st = fh_status_sync(tr->enc, stream);
     if (st != FH_OK && st != FH_E_DOMAIN) return st;
     int h = 0;
+    if (!tr->flags_cleared) return st == FH_E_DOMAIN ? fail(FH_E_DOMAIN, "out-of-domain coordinates") : FH_OK;
     fh_status st2 = cuda_check(cudaMemcpy(&h, tr->flag, sizeof(int), cudaMemcpyDeviceToHost), "read trainer flag");
     if (st2 != FH_OK) return st2;
     if (h & 2) {
@@ -453,15 +484,14 @@ fh_status fh_infer(fh_encoder enc, const fh_mlp_desc *m, const void *table, cons
     if ((st = fh_encode_fwd(enc, coords, N, table, x, FH_BF16, stream)) != FH_OK) return st;
     cudaStream_t s = reinterpret_cast<cudaStream_t>(stream);
     fh::mlp::InferArgs a{x, reinterpret_cast<const __nv_bfloat16 *>(mlp_shadow), mlp_master, y, N};
-    int n_sm = 148, dev = 0;
-    cudaGetDevice(&dev);
-    cudaDeviceGetAttribute(&n_sm, cudaDevAttrMultiProcessorCount, dev);
+    const int n_sm = enc->n_sm;
     const int64_t pairs = ((N + fh::mlp::TILE - 1) / fh::mlp::TILE + 1) / 2;
     const int grid = (int)(pairs < 2 * n_sm ? pairs : 2 * n_sm);
+    if (!enc->mlp_attrs_set[m->n_in / 16 - 1]) {
+        if ((st = set_mlp_attrs(m->n_in)) != FH_OK) return st;
+        enc->mlp_attrs_set[m->n_in / 16 - 1] = true;
+    }
     auto go = [&](auto kern, int smem) -> fh_status {
-        fh_status q = cuda_check(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, smem),
-                                 "cudaFuncSetAttribute(mlp_infer)");
-        if (q != FH_OK) return q;
         { kern<<<grid, 256, smem, s>>>(a); fh::count_launch(); }
         return cuda_check(cudaGetLastError(), "mlp_infer_kernel launch");
     };

@@ -161,7 +161,12 @@ class Encoder:
     FH_LIN_BRICK (NEXT-2 brick order of the bijective levels, R21)."""
 
     def __init__(self, levels: Sequence[Sequence[int]], F: int, table_dtype: str = "f32", cap: int = 0,
-                 lin: int = FH_LIN_EQ9):
+                 lin: int = FH_LIN_EQ9, auto_scratch: bool = True):
+        # auto_scratch: the binding allocates (torch) and attaches the
+        # caller-owned shifted-pair scratch of each stream on that stream's
+        # first pass (fh_encoder_attach_scratch); the library never allocates
+        self._scratch = {}
+        self.auto_scratch = auto_scratch
         L = len(levels)
         arr = (LevelRes * max(L, 1))()
         for i, r in enumerate(levels):
@@ -191,10 +196,24 @@ class Encoder:
         return dict(res=tuple(I.res), corners=I.corners, table_size=I.table_size, hashed=bool(I.hashed),
                     offset=I.offset, lin=int(I.lin))
 
+    def _auto_scratch(self, stream, device=None):
+        """Attach torch-allocated scratch to `stream` once (see __init__)."""
+        sid = _stream(stream)
+        if not self.auto_scratch or sid in self._scratch:
+            return
+        import torch
+        n = self.scratch_size()
+        buf = None
+        if n > 0:
+            buf = torch.empty(n, dtype=torch.uint8, device=device or torch.device("cuda", torch.cuda.current_device()))
+            _check(lib().fh_encoder_attach_scratch(self._h, sid, _ptr(buf), n))
+        self._scratch[sid] = buf
+
     # -------------------------------------------------------------- kernels
     def fwd(self, coords, table, out=None, out_dtype: str = "f32", stream=None):
         import torch
         N = coords.shape[0]
+        self._auto_scratch(stream, coords.device)
         if out is None:
             dt = torch.float32 if out_dtype == "f32" else torch.bfloat16
             out = torch.empty((N, self.L * self.F), dtype=dt, device=coords.device)
@@ -206,6 +225,7 @@ class Encoder:
         """dtable += gradient (fh_encode_bwd), or dtable = gradient with
         overwrite=True (fh_encode_bwd_ex FH_BWD_OVERWRITE: zeroed per level
         group right before its reductions)."""
+        self._auto_scratch(stream, coords.device)
         if overwrite:
             _check(lib().fh_encode_bwd_ex(self._h, _ptr(coords), coords.shape[0], _ptr(dout), _ptr(dtable), 1,
                                           _stream(stream)))
@@ -244,24 +264,28 @@ class Encoder:
 
     def attach_scratch(self, buf, stream=None):
         """Use caller-owned device memory (>= scratch_size() bytes) as the
-        shifted-pair scratch of `stream`; buf=None detaches."""
+        shifted-pair scratch of `stream`; buf=None detaches (the stream then
+        runs without the shifted pairs; no automatic re-attach)."""
+        sid = _stream(stream)
         if buf is None:
-            _check(lib().fh_encoder_attach_scratch(self._h, _stream(stream), None, 0))
+            _check(lib().fh_encoder_attach_scratch(self._h, sid, None, 0))
         else:
-            _check(lib().fh_encoder_attach_scratch(self._h, _stream(stream), _ptr(buf),
-                                                   buf.numel() * buf.element_size()))
+            _check(lib().fh_encoder_attach_scratch(self._h, sid, _ptr(buf), buf.numel() * buf.element_size()))
+        self._scratch[sid] = buf
 
     def zero_grad(self, dtable, stream=None):
         _check(lib().fh_zero_grad(self._h, _ptr(dtable), _stream(stream)))
 
     def fwd_bwd(self, coords, table, out, dout, dtable, out_dtype: str = "f32", zero_dtable: bool = True,
                 stream=None):
+        self._auto_scratch(stream, coords.device)
         _check(lib().fh_encode_fwd_bwd(self._h, _ptr(coords), coords.shape[0], _ptr(table), _ptr(out),
                                        _DT[out_dtype], _ptr(dout), _ptr(dtable), int(zero_dtable),
                                        _stream(stream)))
 
     def step_host(self, coords_h, dout_h, table_d, coords_d, dout_d, out_d, dtable_d, out_h, dtable_h,
                   stream=None):
+        self._auto_scratch(stream, coords_d.device)
         _check(lib().fh_encode_step_host(self._h, _ptr(coords_h), _ptr(dout_h), coords_h.shape[0], _ptr(table_d),
                                          _ptr(coords_d), _ptr(dout_d), _ptr(out_d), _ptr(dtable_d), _ptr(out_h),
                                          _ptr(dtable_h), _stream(stream)))
@@ -470,6 +494,7 @@ class Trainer:
 
     def fwd_bwd(self, coords, target, n_global=None, stream=None):
         N = coords.shape[0]
+        self.enc._auto_scratch(stream, coords.device)
         _check(_train_lib().fh_train_fwd_bwd(self._h, _ptr(coords), _ptr(target), N, n_global or N,
                                              self.loss.data_ptr(), _stream(stream)))
         return self.loss
@@ -483,6 +508,7 @@ class Trainer:
         if y is None:
             y = torch.empty(N, dtype=torch.float32, device=coords.device)
         table = self.table_shadow if self.table_shadow is not None else self.table_master
+        self.enc._auto_scratch(stream, coords.device)
         L = _train_lib()
         ws = int(L.fh_infer_workspace_size(self.enc.handle, ctypes.byref(self.desc), N))
         _check(L.fh_infer(self.enc.handle, ctypes.byref(self.desc), _ptr(table), _ptr(self.mlp_shadow),
@@ -541,6 +567,7 @@ class Trainer:
 
     def step(self, coords, target, n_global=None, stream=None):
         N = coords.shape[0]
+        self.enc._auto_scratch(stream, coords.device)
         _check(_train_lib().fh_train_step(self._h, _ptr(coords), _ptr(target), N, n_global or N,
                                           self.loss.data_ptr(), _stream(stream)))
         return self.loss
@@ -622,6 +649,8 @@ class MHEEncoder(Encoder):
     fwd / bwd / indices calls.  res: vertices per spatial axis per level."""
 
     def __init__(self, res: Sequence[int], F: int, T: int, n_frames: int, table_dtype: str = "f32"):
+        self._scratch = {}
+        self.auto_scratch = False   # MHE encoders use no scratch
         L = len(res)
         arr = (ctypes.c_uint32 * max(L, 1))(*[int(r) for r in res])
         h = ctypes.c_void_p()

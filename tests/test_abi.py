@@ -136,6 +136,21 @@ def test_encode_argument_errors_are_host_side():
     assert L.fh_level_stats(enc.handle, 0, 256, 4, 256, None) == fh.FH_E_ARG   # workspace too small
 
 
+def test_host_only_encoder_reports_state_error():
+    """Without a CUDA device (this CPU container) fh_build_levels still
+    builds the host plan (level queries, scratch sizing) but makes no device
+    state, and a valid encode call returns FH_E_STATE rather than faulting."""
+    import torch
+    if torch.cuda.is_available():
+        pytest.skip("host-only behaviour")
+    enc = fh.Encoder(W.CFG2.levels, 2, cap=W.CFG2.cap)
+    assert enc.scratch_size() > 0
+    L = fh.lib()
+    assert L.fh_encode_fwd(enc.handle, 16, 10, 256, 256, 0, None) == fh.FH_E_STATE
+    assert b"without a CUDA device" in L.fh_last_error()
+    assert L.fh_encode_bwd(enc.handle, 16, 10, 256, 256, None) == fh.FH_E_STATE
+
+
 def test_build_levels_lin_brick_info_and_errors():
     """NEXT-2 through the ABI: the brick linearization keeps the table sizes
     and packing of Eq. 9 (a bijection onto [0, C_l)), is reported per level,

@@ -38,6 +38,17 @@ def run_bwd(enc, case):
     return dtable.cpu().numpy().astype(np.float64), st
 
 
+def kernel_names(fn):
+    """Names of the CUDA kernels fn() launches (CUPTI through torch.profiler):
+    proves which launch path a test exercised."""
+    from torch.profiler import ProfilerActivity, profile
+    torch.cuda.synchronize()
+    with profile(activities=[ProfilerActivity.CUDA]) as prof:
+        fn()
+        torch.cuda.synchronize()
+    return [e.name for e in prof.events() if e.device_type.name == "CUDA"]
+
+
 def check_fwd(got, ref, absref, rel=1e-6):
     err = np.abs(got - ref)
     bound = rel * absref + 1e-30
@@ -517,6 +528,37 @@ def test_maximum_table_size(levels, cap, F):
     torch.cuda.empty_cache()
 
 
+def test_encode_makes_no_device_allocations():
+    """SURVEY.md §8(b) ownership: after fh_build_levels (which makes the
+    16-byte status word) no encode call allocates device memory -- large
+    fwd / bwd passes without scratch (no shifted pairs) and with caller
+    scratch leave the device's free memory unchanged."""
+    cfg = W.CFG2
+    N = 1 << 18
+    g = torch.Generator("cuda").manual_seed(1)
+    c = torch.rand((N, 4), device="cuda", generator=g)
+    warm = fh.Encoder(cfg.levels, cfg.F, cfg.table_dtype, cfg.cap)
+    t = torch.zeros((warm.entries, cfg.F), device="cuda")
+    out = torch.empty((N, cfg.L * cfg.F), device="cuda")
+    dout = torch.randn((N, cfg.L * cfg.F), device="cuda", generator=g)
+    dt = torch.empty_like(t)
+    warm.fwd(c, t, out)
+    warm.bwd(c, dout, dt, overwrite=True)             # loads every kernel module
+    enc = fh.Encoder(cfg.levels, cfg.F, cfg.table_dtype, cfg.cap, auto_scratch=False)
+    buf = torch.empty(enc.scratch_size(), dtype=torch.uint8, device="cuda")
+    s2 = torch.cuda.Stream()
+    torch.cuda.synchronize()
+    free0 = torch.cuda.mem_get_info()[0]
+    enc.fwd(c, t, out)
+    enc.bwd(c, dout, dt, overwrite=True)
+    enc.attach_scratch(buf, s2)
+    enc.fwd(c, t, out, stream=s2)
+    enc.bwd(c, dout, dt, stream=s2, overwrite=True)
+    torch.cuda.synchronize()
+    assert torch.cuda.mem_get_info()[0] == free0
+    assert enc.status_sync() == fh.FH_OK
+
+
 def test_caller_owned_scratch():
     """fh_encoder_attach_scratch: the shifted-pair scratch in caller-owned
     memory (the caller owns every device buffer); results
@@ -550,28 +592,78 @@ def test_caller_owned_scratch():
         mhe.attach_scratch(buf, st)
 
 
-@pytest.mark.parametrize("F", [1, 2])
 @pytest.mark.parametrize("rep", ["0", "8191"])
-def test_backward_replicated_pass(rep, F, monkeypatch):
-    """A contended mid-size level (< 8192 entries, >= 4096 updates per entry)
-    is reduced in a pass of its own into 64 replicated copies summed
-    afterwards (FH_REP_MAX_T; 0 disables): equal to the oracle, odd level
-    offset included (the copies keep the pairs' 16-byte alignment)."""
+def test_backward_replicated_pass(rep, monkeypatch):
+    """A contended mid-size level (2048 < T < 8192 entries, >= 4096 updates
+    per entry) is reduced in a pass of its own into 64 replicated copies
+    summed afterwards (FH_REP_MAX_T; 0 disables): equal to the oracle, at an
+    ODD level offset (81: the copies start at the even entry below it so the
+    pairs keep their 16-byte alignment).  The launch list proves which path
+    ran (rep_reduce_kernel)."""
     monkeypatch.setenv("FH_REP_MAX_T", rep)
-    levels = [(3, 3, 3, 3), (9, 8, 5, 3)]           # offset of level 1 = 81 (odd), T = 1080
-    cfg = W.EncoderConfig("rep", tuple(levels), F=F, cap=0, table_dtype="f32")
-    case = W.encode_case(cfg, 300000, seed=31)
-    enc = fh.Encoder(levels, F)
+    levels = [(3, 3, 3, 3), (9, 9, 9, 9)]           # offset of level 1 = 81 (odd), T = 6561
+    cfg = W.EncoderConfig("rep", tuple(levels), F=2, cap=0, table_dtype="f32")
+    N = 1 << 21                                     # 16 N / T = 5114 updates per entry
+    case = W.encode_case(cfg, N, seed=31)
+    enc = fh.Encoder(levels, 2)
     ref = oracle.Levels(levels)
-    got, st = run_bwd(enc, case)
-    assert st == fh.FH_OK
-    G, A = ref.backward(case.coords, case.dout, F, want_abs=True)
-    check_bwd(got, G, A)
+    c, g = dev(case.coords), dev(case.dout)
+    dt = torch.zeros((enc.entries, 2), device="cuda")
+    enc.bwd(c, g, dt)                               # attaches the scratch (first pass on the stream)
+    dt.zero_()
+    names = kernel_names(lambda: enc.bwd(c, g, dt))
+    assert any("rep_reduce_kernel" in n for n in names) == (rep != "0"), names
+    assert enc.status_sync() == fh.FH_OK
+    G, A = ref.backward(case.coords, case.dout, 2, want_abs=True)
+    check_bwd(dt.cpu().numpy().astype(np.float64), G, A)
+
+
+def test_backward_f1_adjacent_odd_levels():
+    """F = 1 with two adjacent mid-size levels at an odd boundary (6561):
+    no shifted scratch or replicated copies for F = 1 (their merge works in
+    16-byte float pairs that would straddle the boundary); equal to the
+    oracle, a second pass accumulates exactly."""
+    levels = [(9, 9, 9, 9), (16, 16, 16, 16)]
+    cfg = W.EncoderConfig("f1", tuple(levels), F=1, cap=0, table_dtype="f32")
+    case = W.encode_case(cfg, 100000, seed=32)
+    enc = fh.Encoder(levels, 1)
+    ref = oracle.Levels(levels)
+    c, g = dev(case.coords), dev(case.dout)
+    dt = torch.zeros((enc.entries, 1), device="cuda")
+    enc.bwd(c, g, dt)
+    enc.bwd(c, g, dt)
+    assert enc.status_sync() == fh.FH_OK
+    G, A = ref.backward(case.coords, case.dout, 1, want_abs=True)
+    check_bwd(dt.cpu().numpy().astype(np.float64), 2 * G, 2 * A)
+
+
+@pytest.mark.parametrize("tdt", ["f32", "f16"])
+def test_forward_shifted_copy_odd_run_start(tdt):
+    """The forward's shifted table copy when a run of shifted levels starts
+    at an ODD offset: a large unshifted level (129^3 x 5, 10.7 M entries,
+    beyond the copy budget) followed by a small one at offset 10,733,445.
+    The scratch is filled with NaN first, so a slot the copy misses shows
+    up; samples at the first cells of level 1 read the pair (b, b + 1)."""
+    levels = [(129, 129, 129, 5), (65, 65, 65, 3)]
+    cfg = W.EncoderConfig("oddrun", tuple(levels), F=2, cap=0, table_dtype=tdt)
+    enc = fh.Encoder(levels, 2, tdt, 0, auto_scratch=False)
+    assert enc.level_info(1)["offset"] % 2 == 1
+    g = W.rng(33)
+    corner = np.array([[0.0, 0.0, 0.0, 0.0], [1e-3, 1e-3, 1e-3, 1e-3], [0.01, 0.0, 0.0, 0.2]], np.float32)
+    coords = np.concatenate([np.repeat(corner, 50, axis=0), W.draw_coords(g, 1 << 17)]).astype(np.float32)
+    case = W.encode_case(cfg, len(coords), seed=33, coords=coords)
+    buf = torch.full((enc.scratch_size() // 4,), float("nan"), device="cuda").view(torch.uint8)
+    enc.attach_scratch(buf)
+    c, t = dev(case.coords), dev(case.table)
+    out = enc.fwd(c, t)
+    assert enc.status_sync() == fh.FH_OK
+    r, ab = oracle.Levels(levels).forward(case.coords, case.table, want_abs=True)
+    check_fwd(out.cpu().numpy().astype(np.float64), r, ab)
 
 
 def test_host_threads_share_one_encoder():
     """Two host threads drive one encoder on their own streams at the same
-    time (ctypes releases the GIL): the lazy per-stream scratch set-up is
+    time (ctypes releases the GIL): the per-stream scratch attach is
     serialised by the encoder's lock; both results equal the oracle."""
     import threading
     cfg = W.CFG1H
