@@ -21,7 +21,15 @@ Readings:
 Pins (tests/test_oracle_train.py): central finite differences of the fp64
 (unrounded) MLP, targets = forward -> zero loss and zero grads, zero
 weights -> bias-only output, Adam first-step closed form
--lr * g / (|g| + eps), lr = 0 -> unchanged.
+-lr * g / (|g| + eps), lr = 0 -> unchanged, and the bf16-emulating
+oracle within bf16 distance (the mlp_backward_bounds bar) of the unrounded
+fp64 one -- the emulated rounding points are a precision reading (R13), not
+a change of the mathematics.
+
+Tolerance companion (mlp_backward_bounds): for every gradient element the
+sum of the absolute values of its contributions (like Oracle-B's A), and an
+extra term for ReLU units whose pre-activation is within rounding distance
+of 0 (their derivative, 0 or 1, is decided by rounding order).
 """
 from __future__ import annotations
 
@@ -95,6 +103,56 @@ def mlp_backward(dy: np.ndarray, layers, cache, emulate_bf16: bool = True):
         else:
             dx0 = da
     return grads, dx0
+
+
+def mlp_backward_bounds(layers, cache, target: np.ndarray, n_global: int, tau: float = 2.0 ** -8):
+    """Per-element tolerance companions of mse_loss + mlp_backward, by plain
+    propagation of absolute values through the same formulas:
+      A  -- running sum of |contributions|: forward abs scales
+            S_0 = |a_0|, S_k = (S_{k-1} |W_k|^T + |b_k|) masked by the ReLU,
+            S_y = S_{last} |W|^T + |b|; dL/dy's companion 2 (S_y + |t|) / N;
+            backward A_dz -> A_dW = A_dz^T S_{k-1}, A_db = sum A_dz,
+            A_da = A_dz |W_k|, masked by ReLU'.  A rounding error relative to
+            each summed term (bf16 operands, fp32 order) stays within c * A.
+      U  -- ambiguity of the ReLU derivative: a unit with
+            |z| <= tau * S (pre-activation within tau of its own abs scale;
+            tau = one bf16 ulp covers an operand flip upstream) may take
+            either derivative, so its dz is known only to within A_da; that
+            uncertainty propagates like A.
+    Returns ([(A_dW, A_db, U_dW, U_db) per layer], A_dx0, U_dx0); a GPU value
+    passes where |got - ref| <= c * A + U."""
+    acts, zs = cache
+    n_layers = len(layers)
+    S = [np.abs(acts[0])]
+    live = []
+    for k in range(n_layers):
+        W, b = layers[k]
+        sc = S[-1] @ np.abs(_id(W)).T + np.abs(_id(b))[None, :]
+        if k < n_layers - 1:
+            z = zs[k]
+            amb = np.abs(z) <= tau * sc
+            lv = (z > 0.0) | amb
+            live.append((lv, amb))
+            S.append(sc * lv)
+        else:
+            S_y = sc[:, 0]
+    A_dz = (2.0 * (S_y + np.abs(_id(target))) / n_global)[:, None]
+    U_dz = np.zeros_like(A_dz)
+    out = [None] * n_layers
+    A_dx0 = U_dx0 = None
+    for k in range(n_layers - 1, -1, -1):
+        aW = np.abs(_id(layers[k][0]))
+        out[k] = (A_dz.T @ S[k], A_dz.sum(axis=0), U_dz.T @ S[k], U_dz.sum(axis=0))
+        A_da = A_dz @ aW
+        U_da = U_dz @ aW
+        if k > 0:
+            lv, amb = live[k - 1]
+            A_dz = A_da * lv
+            # the derivative of an ambiguous unit is 0 or 1: its dz is unknown up to A_da
+            U_dz = U_da * lv + amb * A_da
+        else:
+            A_dx0, U_dx0 = A_da, U_da
+    return out, A_dx0, U_dx0
 
 
 def adam_step(p: np.ndarray, g: np.ndarray, m: np.ndarray, v: np.ndarray, step: int,

@@ -177,6 +177,28 @@ def test_hash_reduces_to_x_when_yzt_zero():
     assert oracle.spatial_hash(0, 3, 0, 0, 1 << 32) == (3 * 2654435761) % (1 << 32)
 
 
+def test_hash_hand_computed_golden():
+    """R5 against values worked out by hand (tests/golden/r5_hash.json, the
+    arithmetic written beside each): every term non-zero, Z/T swapped (a
+    swapped or mistyped z or t prime fails), each prime alone, and the
+    uint32 wrap of X + (...)."""
+    g = gold("r5_hash.json")
+    for c in g["cases"]:
+        assert oracle.spatial_hash(c["X"], c["Y"], c["Z"], c["T"], c["tsize"]) == c["bucket"], c["what"]
+
+
+def test_hash_pipeline_golden():
+    """Steps 1-3 end to end on a capped cfg1h level: cell location (R2),
+    corner order (R3) and R5 plus the level offset, against the hand-worked
+    indices in tests/golden/r5_hash.json."""
+    p = gold("r5_hash.json")["pipeline"]
+    lv = oracle.Levels([tuple(r) for r in p["levels"]], p["cap"])
+    idx, _, bad = lv.indices(np.array([p["coord"]], np.float32), want_w=False)
+    assert bad == 0
+    for c in p["corners"]:
+        assert int(idx[0, p["level"], c["c"]]) == c["index"], c
+
+
 def test_hash_x_neighbours_adjacent():
     """R5 (x additive): the x-neighbour of a capped-level vertex is the next
     bucket (mod T_l) -- the property the pair layout relies on (DESIGN.md

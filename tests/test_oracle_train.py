@@ -100,3 +100,60 @@ def test_mlp_init_shapes():
     layers = W.draw_mlp(W.rng(0), W.MLP3)
     assert [l[0].shape for l in layers] == [(64, 32), (64, 64), (1, 64)]
     assert sum(l[0].size + l[1].size for l in layers) == 6337
+
+
+def _mlp_case(seed, N=512, widths=(32, 64, 64, 1)):
+    g = np.random.default_rng(seed)
+    layers = W.draw_mlp(g, W.MLPConfig(widths))
+    x = g.uniform(-1e-2, 1e-2, (N, widths[0]))           # encoder outputs are small
+    t = g.random(N)
+    return layers, x, t
+
+
+def test_bf16_oracle_within_bf16_distance_of_fp64():
+    """The bf16-emulating Oracle-T (R13 rounding points) against the
+    unrounded fp64 MLP -- whose formulas the finite-difference pin fixes:
+    every gradient element within 2^-5 (about four bf16 roundings of 2^-8
+    in a chain) of its sum of |contributions| plus the ReLU-ambiguity term,
+    and the loss within 1e-2 relative.  So the emulation is a precision
+    reading, not a different computation."""
+    for seed in range(4):
+        layers, x, t = _mlp_case(seed)
+        y64, c64 = T.mlp_forward(x, layers, emulate_bf16=False)
+        yb, cb = T.mlp_forward(x, layers, emulate_bf16=True)
+        l64, dy64 = T.mse_loss(y64, t, 1000)
+        lb, dyb = T.mse_loss(yb, t, 1000)
+        assert abs(lb - l64) <= 1e-2 * l64
+        g64, dx64 = T.mlp_backward(dy64, layers, c64, emulate_bf16=False)
+        gb, dxb = T.mlp_backward(dyb, layers, cb, emulate_bf16=True)
+        bounds, A_dx, U_dx = T.mlp_backward_bounds(layers, c64, t, 1000)
+        for (dW, db), (dWb, dbb), (AW, Ab, UW, Ub) in zip(g64, gb, bounds):
+            assert np.all(np.abs(dWb - dW) <= 2 ** -5 * AW + UW + 1e-300)
+            assert np.all(np.abs(dbb - db) <= 2 ** -5 * Ab + Ub + 1e-300)
+        assert np.all(np.abs(dxb - dx64) <= 2 ** -5 * A_dx + U_dx + 1e-300)
+
+
+def test_backward_bounds_are_sums_of_abs_contributions():
+    """mlp_backward_bounds on a one-hidden-layer net with no ambiguous units:
+    A equals the textbook sums of |contributions| written out by loops."""
+    g = np.random.default_rng(9)
+    W1, b1 = g.standard_normal((3, 2)), np.abs(g.standard_normal(3)) + 5.0   # z1 > 0 everywhere
+    W2, b2 = g.standard_normal((1, 3)), g.standard_normal(1)
+    x = g.uniform(0, 0.1, (4, 2))
+    layers = [(W1, b1), (W2, b2)]
+    t = g.random(4)
+    y, cache = T.mlp_forward(x, layers, emulate_bf16=False)
+    bounds, A_dx, U_dx = T.mlp_backward_bounds(layers, cache, t, 4)
+    # forward abs scales written out: S1[n,i] = sum_j |W1 x| + |b1|, Sy = sum_i |W2 S1| + |b2|
+    S1 = [[sum(abs(W1[i, j] * x[n, j]) for j in range(2)) + abs(b1[i]) for i in range(3)] for n in range(4)]
+    Sy = [sum(abs(W2[0, i]) * S1[n][i] for i in range(3)) + abs(b2[0]) for n in range(4)]
+    Ady = [2.0 * (Sy[n] + abs(t[n])) / 4 for n in range(4)]
+    for i in range(3):
+        assert np.isclose(bounds[1][0][0, i], sum(Ady[n] * S1[n][i] for n in range(4)))
+        for j in range(2):
+            want = sum(Ady[n] * abs(W2[0, i]) * abs(x[n, j]) for n in range(4))
+            assert np.isclose(bounds[0][0][i, j], want)
+    for n in range(4):
+        for j in range(2):
+            assert np.isclose(A_dx[n, j], sum(Ady[n] * abs(W2[0, i]) * abs(W1[i, j]) for i in range(3)))
+    assert not np.any(U_dx) and not np.any(bounds[0][2])

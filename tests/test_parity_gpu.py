@@ -82,6 +82,20 @@ def test_indices_bit_exact(cfg, N):
     assert np.all(np.abs(wg - rW) <= 1e-6 * rW + 1e-12)
 
 
+def test_indices_hand_computed_golden():
+    """The kernels' corner indices on the hand-worked R5 case
+    (tests/golden/r5_hash.json "pipeline"): not only equal to the oracle,
+    equal to the arithmetic written out in the golden file."""
+    import json
+    import os
+    p = json.load(open(os.path.join(os.path.dirname(__file__), "golden", "r5_hash.json")))["pipeline"]
+    enc = fh.Encoder([tuple(r) for r in p["levels"]], 2, "f32", p["cap"])
+    idx, _ = enc.indices(dev(np.array([p["coord"]], np.float32)))
+    got = idx.cpu().numpy().view(np.uint32)
+    for c in p["corners"]:
+        assert int(got[0, p["level"], c["c"]]) == c["index"], c
+
+
 @pytest.mark.parametrize("cfg", CFGS, ids=lambda c: c.name)
 @pytest.mark.parametrize("N", [4096, 4096 + 37, 1])
 def test_forward_parity(cfg, N):
