@@ -13,7 +13,13 @@ outside the per-step events.
 
 Multi-GPU: the path shards by samples with no data-path collective (each
 rank runs its own 2^20 points, seed = rank): "scaling": "weak", value = all
-ranks' samples / max-over-ranks device time.
+ranks' samples / max-over-ranks device time.  `--gpus N` without a torchrun
+environment re-launches this script under torch.distributed.run with N
+ranks (one per GPU, 127.0.0.1 rendezvous, NCCL init lines logged); under
+torchrun, --gpus must equal WORLD_SIZE.  The line carries every rank's
+device, PCI bus id and device time, and the communicator's size.
+`--launch-check` runs only the launcher, rendezvous and max-over-ranks
+reduction (gloo, no GPU work) -- the CPU test of the N > 1 plumbing.
 
 The reference arm (--impl reference) times the CPU oracle (oracle/, plain
 C, fp64, 1 thread) on a bounded sample of the same workload -- the only
@@ -216,6 +222,162 @@ def cpu_baseline_all_cores(cfg, case_coords, case_table, case_dout, max_procs=16
 def W_table_sizes(cfg):
     import workloads as W
     return W.table_sizes(cfg.levels, cfg.cap)
+
+
+def _par_encode_worker(args):
+    """One process of an all-cores oracle encode: forward of its sample range
+    (output kept in shared memory when asked) and backward of its range
+    into a private shared-memory gradient table."""
+    from multiprocessing import shared_memory
+    import numpy as np
+    import oracle
+    k, a, b, shm_name, total, F, want_out, out_name, LF = args
+    d = _PAR
+    lv = oracle.Levels(d["levels"], d["cap"])
+    out = lv.forward(d["coords"][a:b], d["t64"])
+    if want_out:
+        sh = shared_memory.SharedMemory(name=out_name)
+        np.ndarray((len(d["coords"]), LF), dtype=np.float64, buffer=sh.buf)[a:b] = out
+        sh.close()
+    if d.get("dout") is not None:
+        G = lv.backward(d["coords"][a:b], d["dout"][a:b], F)
+        shm = shared_memory.SharedMemory(name=shm_name)
+        np.ndarray((total, F), dtype=np.float64, buffer=shm.buf)[:] = G
+        shm.close()
+    return k
+
+
+def _par_sum_worker(args):
+    """Sum rows [a, b) of the P private gradient tables, in process order,
+    into the result table (the all-cores merge, split over entries)."""
+    from multiprocessing import shared_memory
+    import numpy as np
+    a, b, names, out_name, total, F = args
+    sh = shared_memory.SharedMemory(name=out_name)
+    dst = np.ndarray((total, F), dtype=np.float64, buffer=sh.buf)
+    for nm in names:
+        s = shared_memory.SharedMemory(name=nm)
+        dst[a:b] += np.ndarray((total, F), dtype=np.float64, buffer=s.buf)[a:b]
+        s.close()
+    del dst
+    sh.close()
+    return a
+
+
+def _oracle_encode_par(levels, cap, coords, t64, dout, F, P, want_out=False):
+    """Oracle fwd (+ bwd when dout is given) with the samples split over P
+    forked processes; private gradient tables summed in process order (the
+    sum itself split over entry ranges across the same processes)."""
+    import multiprocessing as mp
+    from multiprocessing import shared_memory
+    import numpy as np
+    total, n, LF = t64.shape[0], len(coords), len(levels) * F
+    _PAR.clear()
+    _PAR.update(levels=levels, cap=cap, coords=coords, t64=t64, dout=dout)
+    shms = [shared_memory.SharedMemory(create=True, size=total * F * 8) for _ in range(P)] if dout is not None else []
+    osh = shared_memory.SharedMemory(create=True, size=max(8, n * LF * 8)) if want_out else None
+    try:
+        bounds = [(i * n // P, (i + 1) * n // P) for i in range(P)]
+        G = None
+        with mp.get_context("fork").Pool(P) as pool:
+            pool.map(_par_encode_worker, [(i, a, b, shms[i].name if shms else "", total, F, want_out,
+                                           osh.name if osh else "", LF) for i, (a, b) in enumerate(bounds)])
+            if shms:
+                gsh = shared_memory.SharedMemory(create=True, size=total * F * 8)
+                shms.append(gsh)
+                eb = [(i * total // P, (i + 1) * total // P) for i in range(P)]
+                pool.map(_par_sum_worker, [(a, b, [x.name for x in shms[:-1]], gsh.name, total, F) for a, b in eb])
+                G = np.ndarray((total, F), dtype=np.float64, buffer=gsh.buf).copy()
+        out = np.ndarray((n, LF), dtype=np.float64, buffer=osh.buf).copy() if want_out else None
+        return out, G
+    finally:
+        for sh in shms + ([osh] if osh else []):
+            sh.close()
+            sh.unlink()
+
+
+def _oracle_train_step(levels, cap, F, coords, target, t16, layers, adam_state, n_global, P):
+    """Oracle-T, one train step as the tests compose it (oracle/train.py;
+    SURVEY §8(c)): encode fwd over the fp16 table values (Oracle-F), bf16
+    rounding of the encoding (R13), MLP fwd, MSE, analytic bwd, Oracle-B of
+    dL/d(enc), dense Adam over every table and MLP parameter (R12)."""
+    import numpy as np
+    import oracle
+    from oracle import train as T
+    t64 = t16.astype(np.float64)
+    if P > 1:
+        x0, _ = _oracle_encode_par(levels, cap, coords, t64, None, F, P, want_out=True)
+    else:
+        x0 = oracle.Levels(levels, cap).forward(coords, t64)
+    y, cache = T.mlp_forward(T.bf16_round(x0), layers)
+    loss, dy = T.mse_loss(y, target.astype(np.float64), n_global)
+    grads, dx0 = T.mlp_backward(dy, layers, cache)
+    if P > 1:
+        _, G = _oracle_encode_par(levels, cap, coords, t64, dx0, F, P)
+    else:
+        G = oracle.Levels(levels, cap).backward(coords, dx0, F)
+    p, m, v = adam_state["table"]
+    adam_state["table"] = T.adam_step(p, G, m, v, 1)
+    for k, ((dW, db), (W_, b_)) in enumerate(zip(grads, layers)):
+        T.adam_step(W_, dW, np.zeros_like(dW), np.zeros_like(dW), 1)
+        T.adam_step(b_, db, np.zeros_like(db), np.zeros_like(db), 1)
+    return loss
+
+
+def cpu_oracle_baselines(W, max_procs=8):
+    """SURVEY §8(d) "Oracle timing beside the GPU": the oracle, as it stands,
+    on 2^18-point subsets of the HBM-regime encoder (cfg4 = cfg5's encoder:
+    L=16, F=4, 160 M parameters) -- encode fwd+bwd, and the whole Oracle-T
+    train step with dense Adam over every parameter -- plus Oracle-T on
+    cfg3's full 2^18 batch; each on 1 core (BLAS limited to one thread) and
+    on up to max_procs cores (encode split over forked processes, private
+    gradient tables summed in process order; each table is 1.3 GB at cfg4)."""
+    import numpy as np
+    from threadpoolctl import threadpool_limits
+    import oracle
+    out = {"cpu_model": cpu_model(), "host_cores": len(os.sched_getaffinity(0))}
+    P = max(1, min(len(os.sched_getaffinity(0)), max_procs))
+    n = 1 << 18
+    g = W.rng(123)
+    for name, cfg, mlp in (("cfg4_cfg5", W.CFG4, W.MLP4), ("cfg3", W.CFG3, W.MLP3)):
+        total = int(sum(W.table_sizes(cfg.levels, cfg.cap)))
+        t16 = W.draw_table(g, total, cfg.F, "f16")
+        coords = W.draw_coords(g, n)
+        dout = g.standard_normal((n, cfg.L * cfg.F), dtype=np.float32)
+        target = g.random(n, dtype=np.float32)
+        layers = W.draw_mlp(g, mlp)
+        res = {}
+        if name == "cfg4_cfg5":
+            t64 = t16.astype(np.float64)
+            with threadpool_limits(1):
+                t0 = time.perf_counter()
+                lv = oracle.Levels(cfg.levels, cfg.cap)
+                lv.forward(coords, t64)
+                lv.backward(coords, dout, cfg.F)
+                d1 = time.perf_counter() - t0
+            t0 = time.perf_counter()
+            _oracle_encode_par(cfg.levels, cfg.cap, coords, t64, dout, cfg.F, P)
+            dP = time.perf_counter() - t0
+            res["encode_fwd_bwd"] = {"unit": UNIT, "sample": f"{n} of cfg4's 2^22 points, fwd+bwd over the full "
+                                                            f"40 M-entry F=4 table, fp64 C oracle",
+                                     "one_core": {"value": n / d1, "cores": 1, "seconds": d1},
+                                     "all_cores": {"value": n / dP, "cores": P, "seconds": dP}}
+            del t64
+        for label, procs in (("one_core", 1), ("all_cores", P)):
+            state = {"table": (t16.astype(np.float64).reshape(-1, cfg.F), np.zeros((total, cfg.F)),
+                               np.zeros((total, cfg.F)))}
+            with threadpool_limits(1 if procs == 1 else None):
+                t0 = time.perf_counter()
+                _oracle_train_step(cfg.levels, cfg.cap, cfg.F, coords, target, t16, layers, state, n, procs)
+                dt = time.perf_counter() - t0
+            res.setdefault("train_step", {"unit": UNIT, "sample": f"{n} samples of the {name} train step "
+                                          f"(Oracle-T: encode fwd, bf16 rounding, MLP {mlp.widths}, MSE, bwd, "
+                                          f"encode bwd, dense Adam over {total * cfg.F + sum(W_.size + b_.size for W_, b_ in layers)} "
+                                          f"parameters), fp64"})[label] = {"value": n / dt, "cores": procs,
+                                                                           "seconds": dt}
+            del state
+        out[name] = res
+    return out
 
 
 # ------------------------------------------------------------------ ours
@@ -706,6 +868,17 @@ def run_ours(args, rank, local_rank, world):
     if status != fh.FH_OK:
         raise RuntimeError("domain flag set during timed region")
     value = N * world * K / total_s
+    props = torch.cuda.get_device_properties(local_rank)
+    me = {"rank": rank, "local_rank": local_rank, "device": props.name,
+          "pci_bus_id": getattr(props, "pci_bus_id", None), "uuid": str(getattr(props, "uuid", "")),
+          "device_ms_per_step": step_ms}
+    ranks = [me]
+    comm = {"backend": None, "world_size": 1}
+    if dist:
+        ranks = [None] * world
+        dist.all_gather_object(ranks, me)
+        comm = {"backend": dist.get_backend(), "world_size": dist.get_world_size(),
+                "nccl_version": ".".join(str(v) for v in torch.cuda.nccl.version())}
 
     # e2e: the same step through the C ABI from pinned HOST buffers, copies
     # inside the timed region (fh_encode_step_host: H2D of the step's coords and
@@ -821,19 +994,26 @@ def run_ours(args, rank, local_rank, world):
     }
     cpu = None
     cpu_all = None
+    cpu_more = None
     if world == 1 and not args.no_cpu_baseline:
         cpu = cpu_baseline(cfg, case.coords, case.table, case.dout)
         try:
             cpu_all = cpu_baseline_all_cores(cfg, case.coords, case.table, case.dout)
         except Exception as ex:   # the all-cores run is context; never fail the bench on it
             cpu_all = {"unavailable": f"{type(ex).__name__}: {ex}"}
+        if not args.no_train:
+            try:
+                cpu_more = cpu_oracle_baselines(W)
+            except Exception as ex:   # context; never fail the bench on it
+                cpu_more = {"unavailable": f"{type(ex).__name__}: {ex}"}
     line = {
         "metric": METRIC, "value": value, "unit": UNIT, "n_gpus": world, "steps": K, "warmup": max(args.warmup, 3),
         "ms_per_step": total_s * 1e3 / K, "higher_is_better": True, "scaling": "weak", "vs_baseline": None,
         "dtype": "f32", "data": "synthetic", "config": config_block(cfg, N, world),
         "kernels_ms": {"zero_grad": "inside encode_bwd (FH_BWD_OVERWRITE)", "encode_fwd": fwd_ms, "encode_bwd": bwd_ms, "step": step_ms},
-        "roofline": roofline, "gather_roofline": gather_roofline, "cpu_baseline": cpu, "cpu_baseline_all_cores": cpu_all, "e2e": e2e,
-        "gpu_launches": launches, "clocks": clk.summary(), "train_step": train,
+        "roofline": roofline, "gather_roofline": gather_roofline, "cpu_baseline": cpu, "cpu_baseline_all_cores": cpu_all,
+        "cpu_oracle_baselines": cpu_more, "e2e": e2e,
+        "gpu_launches": launches, "clocks": clk.summary(), "ranks": ranks, "comm": comm, "train_step": train,
         "paper_encoders": encoders, "coreset": coreset, "hbm_regime": hbm_regime,
     }
     print(json.dumps(line), flush=True)
@@ -841,9 +1021,56 @@ def run_ours(args, rank, local_rank, world):
         dist.destroy_process_group()
 
 
+def free_port() -> int:
+    import socket
+    with socket.socket(socket.AF_INET, socket.SOCK_STREAM) as so:
+        so.bind(("127.0.0.1", 0))
+        return so.getsockname()[1]
+
+
+def spawn_ranks(n: int, argv) -> int:
+    """Re-launch this script with n ranks under torch.distributed.run (one
+    process per GPU, rendezvous on 127.0.0.1).  NCCL's INIT lines (which
+    report nranks and the rank -> device mapping) go to stderr."""
+    env = dict(os.environ)
+    env.setdefault("NCCL_DEBUG", "INFO")
+    env.setdefault("NCCL_DEBUG_SUBSYS", "INIT")
+    cmd = [sys.executable, "-m", "torch.distributed.run", "--nnodes=1", f"--nproc-per-node={n}",
+           "--master-addr", "127.0.0.1", "--master-port", str(free_port()), os.path.abspath(__file__), *argv]
+    return subprocess.call(cmd, env=env)
+
+
+def launch_check(args, rank, world):
+    """The N > 1 plumbing without GPU work: gloo rendezvous, a barrier, the
+    max-over-ranks reduction of a per-rank time, and the per-rank record."""
+    import socket
+    import torch
+    import torch.distributed as dist
+    if world > 1:
+        dist.init_process_group("gloo")
+    t = 0.001 * (rank + 1)   # a rank-dependent "device time": the max must be the last rank's
+    info = {"rank": rank, "local_rank": env_int("LOCAL_RANK", 0), "host": socket.gethostname(), "pid": os.getpid(),
+            "device_ms": t * 1e3}
+    ranks = [info]
+    if world > 1:
+        dist.barrier()
+        tt = torch.tensor([t], dtype=torch.float64)
+        dist.all_reduce(tt, op=dist.ReduceOp.MAX)
+        t = float(tt.item())
+        ranks = [None] * world
+        dist.all_gather_object(ranks, info)
+    if rank == 0:
+        print(json.dumps({"launch_check": True, "metric": METRIC, "unit": UNIT, "n_gpus": world,
+                          "max_rank_ms": t * 1e3, "ranks": ranks,
+                          "comm": {"backend": "gloo" if world > 1 else None, "world_size": world}}), flush=True)
+    if world > 1:
+        dist.destroy_process_group()
+
+
 def main():
     ap = argparse.ArgumentParser()
-    ap.add_argument("--gpus", type=int, default=1)
+    ap.add_argument("--gpus", type=int, default=None, help="ranks (GPUs); default WORLD_SIZE or 1")
+    ap.add_argument("--launch-check", action="store_true", help="launcher / rendezvous / reduction only (CPU, gloo)")
     ap.add_argument("--steps", type=int, default=20)
     ap.add_argument("--warmup", type=int, default=5)
     ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
@@ -853,10 +1080,16 @@ def main():
                     help="N>1 gradient path: NCCL reduce-scatter overlapped with the backward (default), or the "
                          "fused peer-memory reduce + Adam + all-gather kernel (torch symmetric memory)")
     args = ap.parse_args()
+    if "WORLD_SIZE" not in os.environ and (args.gpus or 1) > 1:
+        sys.exit(spawn_ranks(args.gpus, sys.argv[1:]))
     rank = env_int("RANK", 0)
     local_rank = env_int("LOCAL_RANK", 0)
     world = env_int("WORLD_SIZE", 1)
-    if args.impl == "reference":
+    if args.gpus is not None and args.gpus != world:
+        sys.exit(f"bench.py: --gpus {args.gpus} but WORLD_SIZE={world}")
+    if args.launch_check:
+        launch_check(args, rank, world)
+    elif args.impl == "reference":
         run_reference(args, rank, world)
     else:
         run_ours(args, rank, local_rank, world)

@@ -146,7 +146,7 @@ class Levels:
     def forward(self, coords: np.ndarray, table: np.ndarray, want_abs: bool = False):
         """Oracle-F: out [N][L*F] fp64 (and sum_c W_c|E_c| when want_abs)."""
         c = _c(coords, np.float32).reshape(-1, 4)
-        t = _c(np.asarray(table).astype(np.float64), np.float64)
+        t = _c(table, np.float64)
         F = t.shape[1]
         assert t.shape[0] == self.total
         N = c.shape[0]
@@ -159,7 +159,7 @@ class Levels:
     def backward(self, coords: np.ndarray, dout: np.ndarray, F: int, want_abs: bool = False):
         """Oracle-B: G [sum T][F] fp64 (and A = sum |W g| when want_abs)."""
         c = _c(coords, np.float32).reshape(-1, 4)
-        g = _c(np.asarray(dout).astype(np.float64), np.float64)
+        g = _c(dout, np.float64)
         N = c.shape[0]
         assert g.shape == (N, self.L * F)
         G = np.zeros((self.total, F), np.float64)
@@ -207,7 +207,7 @@ class MHELevels:
 
     def forward(self, coords, table, want_abs=False):
         c = _c(coords, np.float32).reshape(-1, 4)
-        t = _c(np.asarray(table).astype(np.float64), np.float64)
+        t = _c(table, np.float64)
         F = t.shape[1]
         assert t.shape[0] == self.total
         N = c.shape[0]
@@ -219,7 +219,7 @@ class MHELevels:
 
     def backward(self, coords, dout, F, want_abs=False):
         c = _c(coords, np.float32).reshape(-1, 4)
-        g = _c(np.asarray(dout).astype(np.float64), np.float64)
+        g = _c(dout, np.float64)
         N = c.shape[0]
         G = np.zeros((self.total, F))
         A = np.zeros_like(G) if want_abs else None

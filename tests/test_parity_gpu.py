@@ -369,6 +369,62 @@ def test_cfg4_sampled_rows_and_adjoint():
     assert abs(lhs - rhs) <= 1e-5 * scale
 
 
+def test_cfg4_full_size_backward_every_entry():
+    """BASELINE.json configs[3] (2^22 points, L=16, F=4, fp16 tables capped
+    at 2^22: 40 M entries, 609 MiB of fp32 gradients, the HBM regime) in the
+    launch configuration bench.py times (FH_BWD_OVERWRITE into a NaN-filled
+    buffer, L2-sized level groups): the backward on EVERY entry against
+    Oracle-B -- the dominant kernel of the train step."""
+    cfg = W.CFG4
+    g = W.rng(40)
+    enc = fh.Encoder(cfg.levels, cfg.F, cfg.table_dtype, cfg.cap)
+    coords = W.draw_coords(g, W.N_CFG4)
+    dout = g.standard_normal((W.N_CFG4, cfg.L * cfg.F), dtype=np.float32)
+    c_d, g_d = dev(coords), dev(dout)
+    dt = torch.full((enc.entries, cfg.F), float("nan"), device="cuda")
+    enc.bwd(c_d, g_d, dt, overwrite=True)
+    assert enc.status_sync() == fh.FH_OK
+    got = dt.cpu().numpy()
+    del dt, c_d, g_d
+    G, A = oracle.Levels(cfg.levels, cfg.cap).backward(coords, dout, cfg.F, want_abs=True)
+    del dout
+    check_bwd(got.astype(np.float64), G, A)
+
+
+def test_combustion_fold2_full_size_every_entry():
+    """The paper's own encoder: Combustion-Seg, pure MPHF (Eq. 9; no
+    cap), fold 2 (Eqs. 4-8; 24.2 Mi parameters), F = 2 fp32, at
+    the paper's batch of 2^21 -- forward on every row and backward on
+    every entry against the oracle.  This one launch sequence runs the
+    entry-range passes of the 95 MB finest level, the 64-copy replicated pass
+    of the 4900-entry level and the shared-memory few-cell launches
+    (CTA copies and lane-private tiny levels) together; the launch list
+    proves each ran."""
+    levels = tuple(oracle.fold_schedule((200, 110, 54), 10, 2))
+    cfg = W.EncoderConfig("pc", levels, F=2, cap=0, table_dtype="f32")
+    N = 1 << 21
+    case = W.encode_case(cfg, N, seed=41)
+    enc = fh.Encoder(levels, 2)
+    assert enc.param_count == 25374176
+    ref = oracle.Levels(levels)
+    c, t, g = dev(case.coords), dev(case.table), dev(case.dout)
+    out = enc.fwd(c, t)
+    dt = torch.full((enc.entries, 2), float("nan"), device="cuda")
+    enc.bwd(c, g, dt, overwrite=True)               # first pass on the stream: scratch attached
+    dt.fill_(float("nan"))
+    names = kernel_names(lambda: enc.bwd(c, g, dt, overwrite=True))
+    assert any("bwd_kernel<2, true>" in n for n in names), "entry-range passes"
+    assert any("rep_reduce_kernel" in n for n in names), "replicated pass"
+    assert sum("bwd_small_kernel" in n for n in names) >= 2, "CTA-copy and lane-private launches"
+    assert enc.status_sync() == fh.FH_OK
+    got = out.cpu().numpy().astype(np.float64)
+    r, ab = ref.forward(case.coords, case.table, want_abs=True)
+    check_fwd(got, r, ab)
+    del r, ab, got
+    G, A = ref.backward(case.coords, case.dout, 2, want_abs=True)
+    check_bwd(dt.cpu().numpy().astype(np.float64), G, A)
+
+
 # ------------------------------------------------------ closed forms on GPU
 def test_constant_table_and_multilinear_on_gpu():
     """Closed forms, no oracle: constant table -> constant output;
