@@ -449,134 +449,6 @@ __global__ void __launch_bounds__(256) mlp_grad_reduce_kernel(float *__restrict_
     atomicAdd(grad + p, v);
 }
 
-// ------------------------------------------------------------ inference
-// Forward only (the renderer's "V = model(S)" of Alg. 1):
-// MMA1 -> epilogue 1 -> MMA2 -> epilogue 2 -> y, same numerics as the train
-// kernel's forward.  Two tile slots per CTA, 64 TMEM columns per slot.
-struct InferArgs {
-    const __nv_bfloat16 *x;      // [N][K0]
-    const __nv_bfloat16 *wsh;    // bf16 shadow
-    const float *wmaster;        // fp32 master (biases)
-    float *y;                    // [N]
-    int64_t N;
-};
-
-template <int K0>
-struct InferLayout {
-    static constexpr uint32_t SBO_X = (K0 / 8) * 128;
-    static constexpr uint32_t SBO_H = (H / 8) * 128;
-    static constexpr uint32_t BYTES_X = TILE * K0 * 2;
-    static constexpr uint32_t BYTES_H = TILE * H * 2;
-    static constexpr uint32_t BYTES_SLOT = BYTES_X + BYTES_H;
-    static constexpr uint32_t SMEM = 2 * BYTES_SLOT + H * K0 * 2 + H * H * 2;
-};
-
-template <int K0>
-__global__ void __launch_bounds__(256, 1) mlp_infer_kernel(const InferArgs a) {
-    using Lo = InferLayout<K0>;
-    extern __shared__ __align__(1024) uint8_t smem[];
-    uint8_t *sW1 = smem;
-    uint8_t *sW2 = sW1 + H * K0 * 2;
-    __shared__ uint64_t bar[2];
-    __shared__ uint32_t tbase;
-    __shared__ float b1[H], b2[H], w3[H];
-    const int tid = threadIdx.x, warp = tid >> 5;
-    const int slot = warp >> 2, t = tid & 127;
-    uint8_t *sX = sW2 + H * H * 2 + slot * Lo::BYTES_SLOT;
-    uint8_t *sH = sX + Lo::BYTES_X;
-    const int64_t n_tiles = (a.N + TILE - 1) / TILE;
-    for (int i = tid; i < H * K0; i += blockDim.x)
-        *reinterpret_cast<__nv_bfloat16 *>(sW1 + tc::core_off(i / K0, i % K0, Lo::SBO_X)) = a.wsh[off_W1() + i];
-    for (int i = tid; i < H * H; i += blockDim.x)
-        *reinterpret_cast<__nv_bfloat16 *>(sW2 + tc::core_off(i / H, i % H, Lo::SBO_H)) = a.wsh[off_W2(K0) + i];
-    if (tid < H) {
-        b1[tid] = a.wmaster[off_b1(K0) + tid];
-        b2[tid] = a.wmaster[off_b2(K0) + tid];
-        w3[tid] = __bfloat162float(a.wsh[off_w3(K0) + tid]);
-    }
-    const float b3 = a.wmaster[off_b3(K0)];
-    if (warp == 0) tc::tmem_alloc(&tbase, 128);
-    if (tid == 0) { tc::mbar_init(&bar[0], 1); tc::mbar_init(&bar[1], 1); tc::fence_mbar_init(); }
-    tc::fence_smem_to_async();
-    tc::fence_before_sync();
-    __syncthreads();
-    tc::fence_after_sync();
-    const uint32_t tm = tbase + (uint32_t)slot * 64u;
-    const uint32_t lane_off = (uint32_t)((warp & 3) * 32) << 16;
-    uint64_t *mbar = &bar[slot];
-    const uint32_t aX = tc::smem_u32(sX), aH = tc::smem_u32(sH);
-    const uint32_t aW1 = tc::smem_u32(sW1), aW2 = tc::smem_u32(sW2);
-    constexpr uint32_t id_h = tc::idesc_bf16_f32(128, H, false, false);
-    uint32_t phase = 0;
-    for (int64_t tile = 2 * (int64_t)blockIdx.x + slot; tile < n_tiles; tile += 2 * (int64_t)gridDim.x) {
-        const int64_t row = tile * TILE + t;
-        const bool valid = row < a.N;
-        {
-            const uint4 *src = reinterpret_cast<const uint4 *>(a.x + row * K0);
-            uint4 xv[K0 / 8];
-#pragma unroll
-            for (int q = 0; q < K0 / 8; q++) xv[q] = valid ? __ldg(src + q) : make_uint4(0u, 0u, 0u, 0u);
-#pragma unroll
-            for (int q = 0; q < K0 / 8; q++) st16(sX, tc::core_off(t, 8 * q, Lo::SBO_X), xv[q]);
-        }
-        tc::fence_smem_to_async();
-        tc::fence_before_sync();
-        slot_sync(slot);
-        tc::fence_after_sync();
-        if (t == 0) {
-#pragma unroll
-            for (int s = 0; s < K0 / 16; s++)
-                tc::mma_bf16(tm, tc::sdesc(aX + s * 256, 128, Lo::SBO_X), tc::sdesc(aW1 + s * 256, 128, Lo::SBO_X),
-                             id_h, s > 0);
-            tc::commit(mbar);
-        }
-        tc::mbar_wait(mbar, phase); phase ^= 1;
-        tc::fence_after_sync();
-#pragma unroll
-        for (int c = 0; c < H; c += 16) {
-            float v[16];
-            tc::tmem_ld16(tm + lane_off + c, v);
-            tc::tmem_wait_ld();
-            uint32_t p[8];
-#pragma unroll
-            for (int j = 0; j < 16; j += 2)
-                p[j / 2] = pack_bf16(fmaxf(v[j] + b1[c + j], 0.f), fmaxf(v[j + 1] + b1[c + j + 1], 0.f));
-            st16(sH, tc::core_off(t, c, Lo::SBO_H), make_uint4(p[0], p[1], p[2], p[3]));
-            st16(sH, tc::core_off(t, c + 8, Lo::SBO_H), make_uint4(p[4], p[5], p[6], p[7]));
-        }
-        tc::fence_smem_to_async();
-        tc::fence_before_sync();
-        slot_sync(slot);
-        tc::fence_after_sync();
-        if (t == 0) {
-#pragma unroll
-            for (int s = 0; s < H / 16; s++)
-                tc::mma_bf16(tm, tc::sdesc(aH + s * 256, 128, Lo::SBO_H), tc::sdesc(aW2 + s * 256, 128, Lo::SBO_H),
-                             id_h, s > 0);
-            tc::commit(mbar);
-        }
-        tc::mbar_wait(mbar, phase); phase ^= 1;
-        tc::fence_after_sync();
-        float ya[4] = {0.f, 0.f, 0.f, 0.f};
-#pragma unroll
-        for (int c = 0; c < H; c += 16) {
-            float v[16];
-            tc::tmem_ld16(tm + lane_off + c, v);
-            tc::tmem_wait_ld();
-#pragma unroll
-            for (int j = 0; j < 16; j++)
-                ya[j & 3] = fmaf(bf16r(fmaxf(v[j] + b2[c + j], 0.f)), w3[c + j], ya[j & 3]);
-        }
-        if (valid) a.y[row] = ((ya[0] + ya[1]) + (ya[2] + ya[3])) + b3;
-        tc::fence_before_sync();
-        slot_sync(slot);
-        tc::fence_after_sync();
-    }
-    tc::fence_before_sync();
-    __syncthreads();
-    if (warp == 0) tc::tmem_dealloc(tbase, 128);
-}
-
 // ------------------------------------------------------------------ Adam
 // Bias-corrected Adam (R12), fp32 master/m/v, dense over every parameter:
 //   m = b1 m + (1-b1) g;  v = b2 v + (1-b2) g^2

@@ -8,6 +8,7 @@
 
 #include "internal.h"
 #include "mlp_kernels.cuh"
+#include "infer_kernels.cuh"
 
 using fh::aligned;
 using fh::cuda_check;
@@ -51,8 +52,8 @@ int mlp_smem() {
     return (int)(Lo::SMEM > 120 * 1024 ? Lo::SMEM : 120 * 1024);
 }
 
-// Raise the MLP kernels' dynamic shared-memory limits once (trainer
-// creation / first inference), never on the step path.
+// Raise the MLP train kernel's dynamic shared-memory limit once (trainer
+// creation), never on the step path.
 fh_status set_mlp_attrs(int K0) {
     auto set = [](const void *k, int smem) {
         return cuda_check(cudaFuncSetAttribute(k, cudaFuncAttributeMaxDynamicSharedMemorySize, smem),
@@ -65,13 +66,7 @@ fh_status set_mlp_attrs(int K0) {
         case 48: st = set((const void *)fh::mlp::mlp_train_kernel<48>, mlp_smem<48>()); break;
         default: st = set((const void *)fh::mlp::mlp_train_kernel<64>, mlp_smem<64>()); break;
     }
-    if (st != FH_OK) return st;
-    switch (K0) {
-        case 16: return set((const void *)fh::mlp::mlp_infer_kernel<16>, (int)fh::mlp::InferLayout<16>::SMEM);
-        case 32: return set((const void *)fh::mlp::mlp_infer_kernel<32>, (int)fh::mlp::InferLayout<32>::SMEM);
-        case 48: return set((const void *)fh::mlp::mlp_infer_kernel<48>, (int)fh::mlp::InferLayout<48>::SMEM);
-        default: return set((const void *)fh::mlp::mlp_infer_kernel<64>, (int)fh::mlp::InferLayout<64>::SMEM);
-    }
+    return st;
 }
 
 fh_status check_mlp(fh_encoder enc, const fh_mlp_desc *m) {
@@ -465,42 +460,112 @@ fh_status fh_trainer_status(fh_trainer tr, fh_stream stream) {
 int64_t fh_trainer_step_count(fh_trainer tr) { return tr ? tr->step : -1; }
 
 size_t fh_infer_workspace_size(fh_encoder enc, const fh_mlp_desc *m, int64_t max_batch) {
-    if (!enc || !m || max_batch < 0) return 0;
-    return align_up((size_t)max_batch * (size_t)m->n_in * 2, 256);
+    (void)enc; (void)m; (void)max_batch;
+    return 0;   // the fused kernel keeps the encoding on chip
 }
+
+}  // extern "C"
+
+namespace {
+
+// One fused inference launch (infer_kernels.cuh) for the encoder's F and
+// table dtype and the MLP's K0.  The kernel's shared-memory limit and its
+// CTAs per SM are fixed once per encoder (first call), never per call.
+template <int F, typename T, int K0>
+fh_status launch_infer(fh_encoder enc, const fh::infer::FusedArgs &a, cudaStream_t s) {
+    using Lo = fh::infer::FusedLayout<K0>;
+    auto kern = fh::infer::infer_fused_kernel<F, T, K0>;
+    cudaLaunchConfig_t cfg = {};
+    cudaLaunchAttribute attr[1];
+    attr[0].id = cudaLaunchAttributeClusterDimension;
+    attr[0].val.clusterDim.x = 1;   // set below
+    attr[0].val.clusterDim.y = 1;
+    attr[0].val.clusterDim.z = 1;
+    cfg.blockDim = dim3(fh::infer::Threads<F>::value);
+    cfg.dynamicSmemBytes = Lo::SMEM;
+    cfg.stream = s;
+    cfg.attrs = attr;
+    cfg.numAttrs = 1;
+    // Set up once per encoder: the number of resident clusters for each
+    // cluster size C in {8, 4, 2, 1}.
+    int *max_clusters = enc->infer_clusters[K0 / 16 - 1];
+    if (max_clusters[0] == 0) {
+        fh_status st = cuda_check(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)Lo::SMEM),
+                                  "cudaFuncSetAttribute(infer_fused)");
+        if (st != FH_OK) return st;
+        for (int k = 0; k < 4; k++) {
+            const int c = 8 >> k;
+            attr[0].val.clusterDim.x = (unsigned)c;
+            cfg.gridDim = dim3((unsigned)(c * enc->n_sm));
+            int o = 0;
+            if (cudaOccupancyMaxActiveClusters(&o, kern, &cfg) != cudaSuccess) { cudaGetLastError(); o = 0; }
+            max_clusters[k] = o > 0 ? o : -1;
+        }
+        if (max_clusters[3] <= 0) return fail(FH_E_CUDA, "infer_fused_kernel: does not fit the device");
+    }
+    // Each SM issues about one L2 request per cycle, so the gathers of a
+    // 128-sample tile (8 x 128 L pair requests) are spread over a cluster of
+    // C SMs: the largest C in {8, 4, 2, 1} whose one wave of resident
+    // clusters holds every tile (small batches: 8 SMs per tile; from about
+    // one tile per SM on: C = 1, every CTA gathers and evaluates its own
+    // tiles, CTA-scope hand-offs only).  (64-sample tiles, i.e. twice the SMs
+    // per batch, measured slower: 8.98 -> 10.3 us at 1024 samples.)
+    const int64_t tiles = (a.N + fh::mlp::TILE - 1) / fh::mlp::TILE;
+    int k = 3;
+    for (int q = 0; q < 3; q++)
+        if (max_clusters[q] > 0 && tiles <= max_clusters[q]) { k = q; break; }
+    const int cs = 8 >> k;
+    attr[0].val.clusterDim.x = (unsigned)cs;
+    const int64_t ncl = tiles < max_clusters[k] ? tiles : max_clusters[k];
+    cfg.gridDim = dim3((unsigned)(ncl * cs));
+    fh_status st = cuda_check(cudaLaunchKernelEx(&cfg, kern, enc->params, a), "infer_fused_kernel launch");
+    fh::count_launch();
+    return st;
+}
+
+template <int F, typename T>
+fh_status dispatch_infer_k0(fh_encoder enc, int K0, const fh::infer::FusedArgs &a, cudaStream_t s) {
+    switch (K0) {
+        case 16: return launch_infer<F, T, 16>(enc, a, s);
+        case 32: return launch_infer<F, T, 32>(enc, a, s);
+        case 48: return launch_infer<F, T, 48>(enc, a, s);
+        default: return launch_infer<F, T, 64>(enc, a, s);
+    }
+}
+
+template <typename T>
+fh_status dispatch_infer(fh_encoder enc, int K0, const fh::infer::FusedArgs &a, cudaStream_t s) {
+    switch (enc->F) {
+        case 1: return dispatch_infer_k0<1, T>(enc, K0, a, s);
+        case 2: return dispatch_infer_k0<2, T>(enc, K0, a, s);
+        case 4: return dispatch_infer_k0<4, T>(enc, K0, a, s);
+        default: return dispatch_infer_k0<8, T>(enc, K0, a, s);
+    }
+}
+
+}  // namespace
+
+extern "C" {
 
 fh_status fh_infer(fh_encoder enc, const fh_mlp_desc *m, const void *table, const void *mlp_shadow,
                    const float *mlp_master, const float *coords, int64_t N, float *y, void *workspace,
                    size_t workspace_bytes, fh_stream stream) {
+    (void)workspace; (void)workspace_bytes;
     g_err[0] = 0;
     fh_status st = check_mlp(enc, m);
     if (st != FH_OK) return st;
+    if (enc->kind != 0) return fail(FH_E_ARG, "fh_infer: F-Hash encoders only");
     if (N < 0) return fail(FH_E_ARG, "fh_infer: N < 0");
     if (N == 0) return FH_OK;
-    if (!mlp_shadow || !mlp_master || !y || !workspace || !aligned(workspace, 16))
+    if (!coords || !aligned(coords, 16) || !table || !aligned(table, 32) || !mlp_shadow ||
+        !aligned(mlp_shadow, 16) || !mlp_master || !y)
         return fail(FH_E_ARG, "fh_infer: NULL or misaligned pointer");
-    if (workspace_bytes < fh_infer_workspace_size(enc, m, N)) return fail(FH_E_ARG, "fh_infer: workspace too small");
-    __nv_bfloat16 *x = reinterpret_cast<__nv_bfloat16 *>(workspace);
-    if ((st = fh_encode_fwd(enc, coords, N, table, x, FH_BF16, stream)) != FH_OK) return st;
+    if (!enc->flag) return fail(FH_E_STATE, "fh_infer: encoder was built without a CUDA device");
+    const fh::infer::FusedArgs a{reinterpret_cast<const float4 *>(coords), table,
+                                 reinterpret_cast<const __nv_bfloat16 *>(mlp_shadow), mlp_master, y, N, enc->flag};
     cudaStream_t s = reinterpret_cast<cudaStream_t>(stream);
-    fh::mlp::InferArgs a{x, reinterpret_cast<const __nv_bfloat16 *>(mlp_shadow), mlp_master, y, N};
-    const int n_sm = enc->n_sm;
-    const int64_t pairs = ((N + fh::mlp::TILE - 1) / fh::mlp::TILE + 1) / 2;
-    const int grid = (int)(pairs < 2 * n_sm ? pairs : 2 * n_sm);
-    if (!enc->mlp_attrs_set[m->n_in / 16 - 1]) {
-        if ((st = set_mlp_attrs(m->n_in)) != FH_OK) return st;
-        enc->mlp_attrs_set[m->n_in / 16 - 1] = true;
-    }
-    auto go = [&](auto kern, int smem) -> fh_status {
-        { kern<<<grid, 256, smem, s>>>(a); fh::count_launch(); }
-        return cuda_check(cudaGetLastError(), "mlp_infer_kernel launch");
-    };
-    switch (m->n_in) {
-        case 16: return go(fh::mlp::mlp_infer_kernel<16>, (int)fh::mlp::InferLayout<16>::SMEM);
-        case 32: return go(fh::mlp::mlp_infer_kernel<32>, (int)fh::mlp::InferLayout<32>::SMEM);
-        case 48: return go(fh::mlp::mlp_infer_kernel<48>, (int)fh::mlp::InferLayout<48>::SMEM);
-        default: return go(fh::mlp::mlp_infer_kernel<64>, (int)fh::mlp::InferLayout<64>::SMEM);
-    }
+    return enc->table_dtype == FH_F32 ? dispatch_infer<float>(enc, m->n_in, a, s)
+                                      : dispatch_infer<__half>(enc, m->n_in, a, s);
 }
 
 int64_t fh_arm_pace(int64_t n_rays, int64_t n_alive) {

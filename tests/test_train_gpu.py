@@ -222,12 +222,15 @@ def test_sharded_apply_matches_full_apply():
     assert not torch.equal(after[lo:hi], before[lo:hi])
 
 
-@pytest.mark.parametrize("F,L,N", [(2, 16, 1000), (4, 16, 3001), (4, 4, 130)])
-def test_infer_forward_parity(F, L, N):
-    """NEXT-1: fh_infer (encode fwd + tcgen05 MLP forward) equals Oracle-T's
-    forward on the GPU's own bf16 encoding, and reproduces the train step's
-    loss."""
-    cfg = small_cfg(F, L)
+@pytest.mark.parametrize("F,L,N,tdt", [(2, 16, 1000, "f16"), (4, 16, 3001, "f16"), (4, 4, 130, "f16"),
+                                        (1, 16, 200, "f16"), (8, 8, 500, "f32"), (2, 24, 700, "f32"),
+                                        (2, 16, 1, "f16")])
+def test_infer_forward_parity(F, L, N, tdt):
+    """NEXT-1: fh_infer (ONE fused launch: encode fwd into the shared-memory
+    X tile + tcgen05 MLP forward) equals Oracle-T's forward on the GPU's own
+    bf16 encoding (which the fused kernel recomputes bit-identically), and
+    reproduces the train step's loss."""
+    cfg = small_cfg(F, L, tdt)
     enc, tr, coords, target = make(cfg, N, seed=21 + F + L)
     check_infer(cfg, tr, coords, target, N)
 
@@ -246,7 +249,11 @@ def check_infer(cfg, tr, coords, target, N):
     c, t = torch.from_numpy(coords).cuda(), torch.from_numpy(target).cuda()
     loss = tr.fwd_bwd(c, t, N).item()
     x0 = tr.enc_out(N).float().cpu().numpy().astype(np.float64)
+    torch.cuda.synchronize()
+    l0 = fh.kernel_launches()
     y = tr.infer(c).cpu().numpy().astype(np.float64)
+    assert fh.kernel_launches() - l0 == 1          # NEXT-1 fused: encode + MLP in one launch
+    assert tr.status() == fh.FH_OK
     master = tr.mlp_master.cpu().numpy().astype(np.float64)
     K0, o, layers = cfg.L * cfg.F, 0, []
     for fi, fo in ((K0, 64), (64, 64), (64, 1)):
