@@ -57,13 +57,13 @@ def load_peaks():
     return 6650.0, "fallback (B200_PROFILING.md 6.65 TB/s)"
 
 
-def load_ncu_traffic():
-    """Per-launch DRAM bytes of our kernels from the committed ncu summary."""
+def load_ncu_summary():
+    """The committed ncu summary of the headline kernels (profiles/)."""
     p = os.path.join(ROOT, "profiles", "ncu_summary.json")
     if not os.path.exists(p):
         return {}
     with open(p) as f:
-        return json.load(f).get("dram_bytes_per_launch", {})
+        return json.load(f)
 
 
 class ClockSampler:
@@ -397,7 +397,8 @@ def cpu_baseline(cfg, case_coords, case_table, case_dout):
 
 
 def microbench_roofline(fh, torch, enc, cfg, N, stream, hbm_peak):
-    """§8(d): the measured ceiling of the encode's access shape.  Per level
+    """§8(d): microbenchmarks of the encode's access shape (context: the
+    kernel is not bounded by them).  Per level
     l, random x-pair gathers / vector reds over a T_l-entry buffer (same
     entry width, 8 pairs per thread) give a corner rate; streaming bytes go
     at the measured copy bandwidth.  t_roof = N * sum_l 16/rate_l + stream/BW."""
@@ -439,6 +440,14 @@ def microbench_roofline(fh, torch, enc, cfg, N, stream, hbm_peak):
                                                                    stream=stream)))
         r_split.append(16 * n_thr / timeit(lambda: fh.bench_red(buf, T, eb, n_thr, mode=0, seed=l, stream=stream)))
         del buf
+    # the L2's random-reduction op rate: one 16-byte red.v4 per x-pair at
+    # uniform positions in an L2-resident 48 MiB buffer (8-byte entries,
+    # mode 1) -- the unit the encode backward is bound by
+    rb = torch.zeros((48 << 20) // 4, device="cuda")
+    fh.bench_red(rb, (48 << 20) // 8, 8, n_thr, mode=1, seed=99, stream=stream)
+    t_red = timeit(lambda: fh.bench_red(rb, (48 << 20) // 8, 8, n_thr, mode=1, seed=99, stream=stream))
+    red_ops_per_s = 8 * n_thr / t_red
+    del rb
     stream_fwd = N * (16 + cfg.L * F * 4)
     stream_bwd = N * (16 + cfg.L * F * 4)
     t_fwd_lv = sum(N * 16 / g for g in g_rate) + stream_fwd / bw_copy
@@ -461,14 +470,15 @@ def microbench_roofline(fh, torch, enc, cfg, N, stream, hbm_peak):
         "t_roof_fwd_ms": t_fwd * 1e3, "t_roof_bwd_ms": t_bwd * 1e3,
         "model": "level-mix microbenchmark (fh_bench_gather_levels / fh_bench_red_levels) + streamed bytes at the "
                  "measured copy bandwidth",
-        "t_roof_per_level_sum_fwd_ms": t_fwd_lv * 1e3, "t_roof_per_level_sum_bwd_ms": t_bwd_lv * 1e3,
+        "t_per_level_sum_fwd_ms": t_fwd_lv * 1e3, "t_per_level_sum_bwd_ms": t_bwd_lv * 1e3,
         # SURVEY §8(d) "expected counts": each x-pair as two entry-wide accesses (the
         # naive shape, per-level rates) -- the pair layout of DESIGN.md §8.1 beats it
-        "t_roof_expected_fwd_ms": (sum(N * 16 / g for g in g_split) + stream_fwd / bw_copy) * 1e3,
-        "t_roof_expected_bwd_ms": (sum(N * 16 / r for r in r_split) + stream_bwd / bw_copy) * 1e3,
+        "t_split_pairs_fwd_ms": (sum(N * 16 / g for g in g_split) + stream_fwd / bw_copy) * 1e3,
+        "t_split_pairs_bwd_ms": (sum(N * 16 / r for r in r_split) + stream_bwd / bw_copy) * 1e3,
         "mix_gather_corner_rate_G_per_s": round(N * cfg.L * 16 / tg_mix / 1e9, 2),
         "mix_red_corner_rate_G_per_s": round(N * cfg.L * 16 / tr_mix / 1e9, 2),
         "copy_gbs": bw_copy / 1e9, "hbm_peak_gbs": hbm_peak,
+        "l2_red_op_ceiling_G_per_s": red_ops_per_s / 1e9,
         "gather_corner_rate_G_per_s": [round(g / 1e9, 2) for g in g_rate],
         "red_corner_rate_G_per_s": [round(r / 1e9, 2) for r in r_rate],
         "split_gather_corner_rate_G_per_s": [round(g / 1e9, 2) for g in g_split],
@@ -476,7 +486,7 @@ def microbench_roofline(fh, torch, enc, cfg, N, stream, hbm_peak):
     }
 
 
-def hbm_regime_bench(fh, torch, W, steps, copy_gbs):
+def hbm_regime_bench(fh, torch, W, steps, hbm_peak):
     """The metric's HBM regime: BASELINE.json configs[3] encoder (L=16, F=4
     fp16 tables capped at 2^22: 305 MiB of tables, 609 MiB of fp32 grads),
     2^22 uniform points, encode fwd (bf16 out, as in the train step) + bwd,
@@ -485,8 +495,7 @@ def hbm_regime_bench(fh, torch, W, steps, copy_gbs):
     and entry width (8 B fp16x4 rows; 16 B fp32x4 grads, no pair merge) bounds
     the corner traffic, and the compulsory HBM bytes -- tables read once,
     grads read + written once, coordinates, encodings and upstream grads
-    streamed -- go at the measured copy bandwidth:
-        t_roof = N sum_l 16 / rate_l + HBM bytes / BW_copy."""
+    streamed -- go at the measured copy bandwidth."""
     cfg, N = W.CFG4, W.N_CFG4
     enc = fh.Encoder(cfg.levels, cfg.F, cfg.table_dtype, cfg.cap)
     g = torch.Generator("cuda").manual_seed(4)
@@ -511,44 +520,24 @@ def hbm_regime_bench(fh, torch, W, steps, copy_gbs):
             tb += e[1].elapsed_time(e[2])
     fwd_ms, bwd_ms = tf / steps, tb / steps
     del out, dout, flush
-    n_thr = 1 << 20
-    sink = torch.empty(n_thr, device="cuda")
-    ev0, ev1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
-
-    def timeit(fn, reps=3):
-        best = 1e9
-        for _ in range(reps):
-            ev0.record()
-            fn()
-            ev1.record()
-            ev1.synchronize()
-            best = min(best, ev0.elapsed_time(ev1) / 1e3)
-        return best
-
-    t_g = t_r = 0.0
-    for l in range(cfg.L):
-        T = enc.level_info(l)["table_size"]
-        gb = torch.zeros((T, 2), device="cuda")                 # 8-byte rows (fp16 x 4)
-        rb = torch.zeros((T, 4), device="cuda")                 # 16-byte rows (fp32 x 4)
-        fh.bench_gather(gb, T, 8, n_thr, sink, mode=1, seed=l)
-        rg = 16 * n_thr / timeit(lambda: fh.bench_gather(gb, T, 8, n_thr, sink, mode=1, seed=l))
-        rr = 16 * n_thr / timeit(lambda: fh.bench_red(rb, T, 16, n_thr, mode=1, seed=l))
-        t_g += N * 16 / rg
-        t_r += N * 16 / rr
-        del gb, rb
     LF = cfg.L * cfg.F
-    hbm_fwd = enc.entries * cfg.F * 2 + N * (16 + LF * 2)           # tables + coords + bf16 out
+    # compulsory HBM bytes of one pass: the table (fwd) or the fp32 grads
+    # (bwd: read + written) once, plus the streamed coordinates and encodings /
+    # upstream grads -- a lower bound on the DRAM traffic, so frac <= 1
+    hbm_fwd = enc.entries * cfg.F * 2 + N * (16 + LF * 2)           # fp16 tables + coords + bf16 out
     hbm_bwd = enc.entries * cfg.F * 4 * 2 + N * (16 + LF * 4)       # grads RMW + coords + fp32 dout
-    bw = copy_gbs * 1e9
-    roof_f = t_g + hbm_fwd / bw
-    roof_b = t_r + hbm_bwd / bw
-    return {"workload": "cfg4 encoder (BASELINE.json configs[3]): 2^22 points, L=16, F=4 fp16 tables cap 2^22 "
-                        "(305 MiB) + fp32 grads (609 MiB); fwd (bf16 out) + bwd, L2 flushed",
-            "fwd_ms": fwd_ms, "bwd_ms": bwd_ms, "samples_per_s": N / ((fwd_ms + bwd_ms) / 1e3),
-            "t_roof_fwd_ms": roof_f * 1e3, "t_roof_bwd_ms": roof_b * 1e3,
-            "fwd_frac": roof_f * 1e3 / fwd_ms, "bwd_frac": roof_b * 1e3 / bwd_ms,
-            "frac": (roof_f + roof_b) * 1e3 / (fwd_ms + bwd_ms),
-            "hbm_bytes_per_step": hbm_fwd + hbm_bwd}
+    bw = hbm_peak * 1e9
+    ncu = load_ncu_summary().get("cfg4", {})
+    out = {"workload": "cfg4 encoder (BASELINE.json configs[3]): 2^22 points, L=16, F=4 fp16 tables cap 2^22 "
+                       "(305 MiB) + fp32 grads (609 MiB); fwd (bf16 out) + bwd, L2 flushed",
+           "fwd_ms": fwd_ms, "bwd_ms": bwd_ms, "samples_per_s": N / ((fwd_ms + bwd_ms) / 1e3),
+           "compulsory_hbm_bytes": {"fwd": hbm_fwd, "bwd": hbm_bwd},
+           "hbm_frac_fwd": hbm_fwd / bw / (fwd_ms / 1e3), "hbm_frac_bwd": hbm_bwd / bw / (bwd_ms / 1e3),
+           "note": "compulsory bytes / time / measured HBM peak: the lower bound of the DRAM traffic, so <= 1; the "
+                   "passes are bound by L2 request / atomic throughput (see ncu)"}
+    if ncu:
+        out["ncu"] = ncu
+    return out
 
 
 def train_step_bench(fh, torch, W, which, rank, world, dist, steps, warmup, dp_mode="nccl"):
@@ -969,28 +958,43 @@ def run_ours(args, rank, local_rank, world):
         return
 
     mb = microbench_roofline(fh, torch, enc, cfg, N, stream, hbm_peak)
-    hbm_regime = hbm_regime_bench(fh, torch, W, max(3, min(K, 10)), mb["copy_gbs"]) if not args.no_train else None
+    hbm_regime = hbm_regime_bench(fh, torch, W, max(3, min(K, 10)), hbm_peak) if not args.no_train else None
     # Contract roofline of the dominant kernel: algorithmic bytes / launch time.
     LF4 = cfg.L * cfg.F * 4
     alg = {"fwd": N * (16 * cfg.L * cfg.F * 4 + 16 + LF4), "bwd": N * (16 * cfg.L * cfg.F * 4 + 16 + LF4)}
     dom = "bwd" if bwd_ms >= fwd_ms else "fwd"
     dom_ms = bwd_ms if dom == "bwd" else fwd_ms
     achieved = alg[dom] / (dom_ms / 1e3) / 1e9
-    traffic = load_ncu_traffic().get(dom)
+    ncu = load_ncu_summary().get("cfg2", {})
+    traffic = ncu.get("dram_bytes_per_pass", {}).get(dom)
     roofline = {"bound": "hbm", "kernel": f"encode {dom} pass (fh::{dom}_kernel<2> level groups"
                 + (" + merge_shift_kernel)" if dom == "bwd" else ")"), "achieved": achieved, "peak": hbm_peak,
                 "unit": "GB/s", "frac": achieved / hbm_peak, "traffic": traffic,
                 "peak_source": peak_src,
                 "algorithmic_bytes_per_launch": alg[dom], "launch_unit": "one encode pass (all its launches)",
-                "note": "useful gather (or red) payload 16*L*F*4 B + coords 16 B + out/dout L*F*4 B per sample; "
-                        "the tables are L2-resident, so the gather roofline below is the binding ceiling"}
-    t_roof = mb["t_roof_fwd_ms"] + mb["t_roof_bwd_ms"]
-    gather_roofline = {
-        "bound": "l2-gather/red (measured microbenchmark, same access shape, per-level footprint)",
-        "t_roof_ms": t_roof, "t_measured_ms": fwd_ms + bwd_ms,
-        "frac": t_roof / (fwd_ms + bwd_ms),
-        "frac_expected_counts": (mb["t_roof_expected_fwd_ms"] + mb["t_roof_expected_bwd_ms"]) / (fwd_ms + bwd_ms),
-        "fwd_frac": mb["t_roof_fwd_ms"] / fwd_ms, "bwd_frac": mb["t_roof_bwd_ms"] / bwd_ms, **mb,
+                "note": "useful gather (or red) payload 16*L*F*4 B + coords 16 B + out/dout L*F*4 B per sample over the "
+                        "measured HBM copy peak; the cfg2 tables are L2-resident, so the binding unit is the L2 "
+                        "(l2_frac: ncu lts__throughput of the same launches, profiles/)"}
+    # the backward issues one 16-byte reduction per x-pair of every (sample,
+    # level) (F = 2 with the shifted pairs): 8 per cell
+    red_ops = N * cfg.L * 8
+    roofline["l2_red"] = {"what": "encode bwd: L2 reduction ops issued per second vs the measured random red.v4 op "
+                                  "rate of an L2-resident buffer (the unit the backward is bound by)",
+                          "ops_per_pass": red_ops, "achieved_G_per_s": red_ops / (bwd_ms / 1e3) / 1e9,
+                          "ceiling_G_per_s": mb["l2_red_op_ceiling_G_per_s"],
+                          "frac": red_ops / (bwd_ms / 1e3) / 1e9 / mb["l2_red_op_ceiling_G_per_s"]}
+    if ncu:
+        roofline["l2_frac"] = ncu.get("lts_throughput_frac", {}).get(dom)
+        roofline["l2_evidence"] = {k: ncu[k] for k in ("source", "lts_throughput_frac", "l1tex2xbar_req_frac",
+                                                        "l2_red_sectors_per_pass", "l2_hit_frac") if k in ncu}
+    t_micro = mb["t_roof_fwd_ms"] + mb["t_roof_bwd_ms"]
+    gather_microbench = {
+        "what": "the encode's access shape without its index math (fh_bench_gather_levels / fh_bench_red_levels: "
+                "one aligned x-pair access per corner pair, same level mix) + streamed bytes at the copy bandwidth; "
+                "context, NOT a ceiling (the kernel may beat it)",
+        "t_ms": t_micro, "t_measured_ms": fwd_ms + bwd_ms, "measured_over_microbench": (fwd_ms + bwd_ms) / t_micro,
+        **{k: v for k, v in mb.items() if k not in ("t_roof_fwd_ms", "t_roof_bwd_ms")},
+        "t_fwd_ms": mb["t_roof_fwd_ms"], "t_bwd_ms": mb["t_roof_bwd_ms"],
     }
     cpu = None
     cpu_all = None
@@ -1011,7 +1015,7 @@ def run_ours(args, rank, local_rank, world):
         "ms_per_step": total_s * 1e3 / K, "higher_is_better": True, "scaling": "weak", "vs_baseline": None,
         "dtype": "f32", "data": "synthetic", "config": config_block(cfg, N, world),
         "kernels_ms": {"zero_grad": "inside encode_bwd (FH_BWD_OVERWRITE)", "encode_fwd": fwd_ms, "encode_bwd": bwd_ms, "step": step_ms},
-        "roofline": roofline, "gather_roofline": gather_roofline, "cpu_baseline": cpu, "cpu_baseline_all_cores": cpu_all,
+        "roofline": roofline, "gather_microbench": gather_microbench, "cpu_baseline": cpu, "cpu_baseline_all_cores": cpu_all,
         "cpu_oracle_baselines": cpu_more, "e2e": e2e,
         "gpu_launches": launches, "clocks": clk.summary(), "ranks": ranks, "comm": comm, "train_step": train,
         "paper_encoders": encoders, "coreset": coreset, "hbm_regime": hbm_regime,

@@ -1,0 +1,20 @@
+# round-2 evidence: launch list of the bench and --set full of one encode
+# step (cfg2 headline, cfg4 HBM regime), L2 flushed between steps.
+mkdir -p gpurun_out
+FH_OVERWRITE=1 timeout 300 python tools/time_encode.py cfg2 1 > gpurun_out/r02_enc_cfg2_plain.log 2>&1 && \
+FH_OVERWRITE=1 timeout 900 ncu --set full --clock-control none --import-source on -k "regex:fwd_kernel|bwd_kernel|merge_shift" -o gpurun_out/r02_encode_cfg2 -f python tools/time_encode.py cfg2 1 > gpurun_out/r02_ncu_cfg2.log 2>&1
+echo cfg2 rc=$?
+FH_OVERWRITE=1 timeout 300 python tools/time_encode.py cfg4 1 > gpurun_out/r02_enc_cfg4_plain.log 2>&1 && \
+FH_OVERWRITE=1 timeout 1500 ncu --set full --clock-control none -k "regex:fwd_kernel|bwd_kernel|merge_shift" -s 30 -o gpurun_out/r02_encode_cfg4 -f python tools/time_encode.py cfg4 1 > gpurun_out/r02_ncu_cfg4.log 2>&1
+echo cfg4 rc=$?
+timeout 600 python bench.py --steps 2 --warmup 3 --no-cpu-baseline > gpurun_out/r02_bench_plain.log 2>&1 && \
+timeout 1500 ncu --metrics gpu__time_duration.sum --clock-control none -c 400 --csv --log-file gpurun_out/r02_bench_launches.csv python bench.py --steps 2 --warmup 3 --no-cpu-baseline > gpurun_out/r02_ncu_launch.log 2>&1
+echo launches rc=$?
+# summaries on the box (the reports themselves can exceed gpurun's 64 MiB copy-back)
+for r in r02_encode_cfg2 r02_encode_cfg4; do
+  python tools/ncu_summary.py gpurun_out/$r.ncu-rep > gpurun_out/${r}_summary.txt 2>&1
+  ncu -i gpurun_out/$r.ncu-rep --page raw --csv > gpurun_out/${r}_raw.csv 2>/dev/null
+done
+ls -la gpurun_out; du -sh gpurun_out
+rm -f gpurun_out/r02_encode_cfg4.ncu-rep
+du -sh gpurun_out

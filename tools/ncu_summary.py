@@ -20,6 +20,9 @@ KEYS = [
     ("lts__t_requests.sum", "l2_req"),
     ("lts__t_sector_hit_rate.pct", "l2hit%"),
     ("lts__t_sectors_srcunit_ltcfabric.sum", "fabric"),
+    ("lts__t_sectors_op_red.sum", "l2_red_sect"),
+    ("lts__t_sectors_op_atom.sum", "l2_atom_sect"),
+    ("l1tex__m_l1tex2xbar_req_cycles_active.avg.pct_of_peak_sustained_elapsed", "xbar_req%"),
     ("l1tex__t_sectors_pipe_lsu_mem_global_op_red.sum", "red_sect"),
     ("smsp__inst_executed_op_global_red.sum", "red_inst"),
     ("dram__bytes_read.sum", "dram_rd"),
