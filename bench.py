@@ -561,6 +561,7 @@ def train_step_bench(fh, torch, W, which, rank, world, dist, steps, warmup, dp_m
     gen = torch.Generator("cuda").manual_seed(0)           # identical init on every rank
     table0 = (torch.rand((enc.entries, cfg.F), device="cuda", generator=gen) * 2 - 1) * 1e-4
     peer = world > 1 and dp_mode == "peer"
+    fused = world > 1 and dp_mode == "fused"
     tr = fh.Trainer(enc, table0, W.draw_mlp(W.rng(0), mlp), n_local, world=world,
                     alloc=dp.symm_alloc if peer else None)
     del table0
@@ -574,7 +575,13 @@ def train_step_bench(fh, torch, W, which, rank, world, dist, steps, warmup, dp_m
     # table shadow.  Falls back to dp.ShardedDP (no overlap) if the plan
     # needs more than 63 Adam ranges.
     sdp = None
-    if peer:
+    comm = None
+    if fused:   # the library's own NCCL exchange (fh_trainer_set_comm), communicator from torch's libnccl
+        uid = [fh.nccl_unique_id() if rank == 0 else None]
+        dist.broadcast_object_list(uid, src=0)
+        comm = fh.NcclComm(uid[0], world, rank)
+        tr.set_comm(comm)
+    elif peer:
         sdp = dp.PeerShardedDP(tr)     # --dp peer: fused reduce + Adam + all-gather over NVLink peer memory
     elif world > 1:
         try:
@@ -586,6 +593,11 @@ def train_step_bench(fh, torch, W, which, rank, world, dist, steps, warmup, dp_m
         if ev: ev[0].record(stream)
         fh.sample_voxels(field, n_local, seed=1234, subsequence=rank, offset=k, coords=coords, target=target)
         if ev: ev[1].record(stream)
+        if comm is not None:   # fused: fwd_bwd + exchange + Adam + all-gather in one library call
+            loss = tr.step(coords, target, n_global)
+            if ev:
+                for i in (2, 3, 4): ev[i].record(stream)
+            return loss
         loss = tr.fwd_bwd(coords, target, n_global)
         if ev: ev[2].record(stream)
         if isinstance(sdp, (dp.OverlappedShardedDP, dp.PeerShardedDP)):
@@ -661,6 +673,10 @@ def train_step_bench(fh, torch, W, which, rank, world, dist, steps, warmup, dp_m
         del graph
     # DP correctness: after the timed steps the replicas must be bit-identical
     same = dp.replicas_identical(tr.shadow_flat) and dp.replicas_identical(tr.mlp_master)
+    if comm is not None:
+        torch.cuda.synchronize()
+        tr.set_comm(None)
+        comm.destroy()
     last = tr.loss.clone()
     if dist:
         dist.all_reduce(last)
@@ -675,7 +691,9 @@ def train_step_bench(fh, torch, W, which, rank, world, dist, steps, warmup, dp_m
         "scaling": "strong" if which == "cfg5" else "weak",
         "phase_ms": {"sample": phase[0], "fwd_bwd": phase[1], "grad_reduce": phase[2],
                      "adam_and_gather": phase[3]},
-        "dp": ("per-level-group fused reduce + Adam + shadow broadcast over NVLink peer memory (fh_train_apply_peers)"
+        "dp": ("fused in the library (fh_trainer_set_comm): per-level-group ncclReduceScatter overlapped with the "
+               "backward + sharded Adam + in-place fp16 ncclAllGather" if comm is not None else
+               "per-level-group fused reduce + Adam + shadow broadcast over NVLink peer memory (fh_train_apply_peers)"
                if isinstance(sdp, dp.PeerShardedDP) else
                "per-backward-launch reduce-scatter overlapped with the backward + sharded Adam + all-gather (NCCL)"
                if isinstance(sdp, dp.OverlappedShardedDP) else
@@ -1080,9 +1098,10 @@ def main():
     ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--no-train", action="store_true", help="skip the train_step (cfg3 / cfg5) sub-benchmarks")
-    ap.add_argument("--dp", default="nccl", choices=["nccl", "peer"],
-                    help="N>1 gradient path: NCCL reduce-scatter overlapped with the backward (default), or the "
-                         "fused peer-memory reduce + Adam + all-gather kernel (torch symmetric memory)")
+    ap.add_argument("--dp", default="nccl", choices=["nccl", "fused", "peer"],
+                    help="N>1 gradient path: NCCL reduce-scatter overlapped with the backward from Python (default), "
+                         "the same exchange driven inside the library (fused, fh_trainer_set_comm), or the fused "
+                         "peer-memory reduce + Adam + all-gather kernel (torch symmetric memory)")
     args = ap.parse_args()
     if "WORLD_SIZE" not in os.environ and (args.gpus or 1) > 1:
         sys.exit(spawn_ranks(args.gpus, sys.argv[1:]))

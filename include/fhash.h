@@ -372,7 +372,39 @@ fh_status fh_train_apply_peers(fh_trainer tr, int W, const float *const *peer_ta
                                const int64_t *begin, const int64_t *end, const int *broadcast, int with_mlp,
                                int new_step, fh_stream stream);
 
-/* fh_train_fwd_bwd + fh_train_apply (single GPU). */
+/* ---- the fused data-parallel form (SURVEY.md §8(b) "nccl_comm", §8(e))
+ * The library drives the gradient exchange itself with NCCL: the
+ * libnccl.so.2 the process already loaded (torch's; resolved with dlopen
+ * RTLD_NOLOAD, else a plain dlopen), so the library shares torch's NCCL.
+ * fh_nccl_unique_id: 128 bytes of ncclUniqueId into id (rank 0 calls it;
+ *   the caller broadcasts them, e.g. over torch.distributed).
+ * fh_nccl_comm_create: ncclCommInitRank(nranks, id, rank) on the current
+ *   device -> *comm (opaque; the caller destroys it after its trainers).
+ * fh_trainer_dp_workspace_size / fh_trainer_set_comm: attach a communicator
+ *   (comm NULL detaches) and caller-owned device workspace (shards of the
+ *   reduce-scattered gradients and the small replicated tail + MLP buffer).
+ *   From then on fh_train_step runs the whole data-parallel step: the encode
+ *   backward's level groups (fh_train_bwd_ranges) are reduce-scattered
+ *   (ncclReduceScatter, SUM) on an internal stream as soon as each group's
+ *   gradients are final, overlapping the later groups; the < 4W + 4
+ *   unaligned tail elements of every group and the MLP gradients are
+ *   all-reduced; ONE Adam launch updates this rank's chunks and the tails;
+ *   the fp16 shadow chunks are all-gathered (ncclAllGather, in place).  The
+ *   caller's stream is ordered after all of it.  Same mathematics as
+ *   fh_train_fwd_bwd + all-reduce + fh_train_apply.  Needs an FH_F16 table
+ *   (the fp16 shadow is the replicated state: the fp32 masters and moments
+ *   of a rank are current only inside its own chunks).
+ * Errors: FH_E_STATE (NCCL not loadable, no fp16 shadow), FH_E_ARG,
+ * FH_E_CUDA (NCCL failures, with NCCL's message). */
+fh_status fh_nccl_unique_id(void *id128);
+fh_status fh_nccl_comm_create(const void *id128, int nranks, int rank, void **comm);
+fh_status fh_nccl_comm_destroy(void *comm);
+size_t    fh_trainer_dp_workspace_size(fh_trainer tr, int nranks);
+fh_status fh_trainer_set_comm(fh_trainer tr, void *comm, int nranks, int rank, void *workspace,
+                              size_t workspace_bytes);
+
+/* fh_train_fwd_bwd + fh_train_apply (single GPU); with a communicator
+ * attached (fh_trainer_set_comm) the fused data-parallel step. */
 fh_status fh_train_step(fh_trainer tr, const float *coords, const float *target, int64_t N_local,
                         int64_t N_global, float *loss_dev, fh_stream stream);
 
@@ -384,12 +416,16 @@ int64_t   fh_trainer_step_count(fh_trainer tr);
 void      fh_trainer_destroy(fh_trainer tr);
 
 /* ============================================================ inference
- * The renderer's model evaluation "V = model(S)" (Alg. 1):
- * encode fwd (bf16 encoding into workspace) + the MLP forward on tcgen05,
- * with exactly the forward numerics of the train step (R13).  table: the
- * encoder's table dtype (fp16 shadow or fp32); mlp_shadow bf16 and
- * mlp_master fp32 in the flat MLP layout; y [N] f32 (device).  workspace of
- * fh_infer_workspace_size(enc, mlp, N) bytes.  Errors as fh_train_fwd_bwd. */
+ * The renderer's model evaluation "V = model(S)" (Alg. 1) as ONE
+ * fused kernel (NEXT-1): the encode forward of each 128-sample tile goes as
+ * bf16 straight into the shared-memory X operand of the tcgen05 MLP forward
+ * (a thread-block cluster of up to 8 SMs shares a tile's gathers for small
+ * batches), with exactly the forward numerics of the train step (R13).
+ * table: the encoder's table dtype (fp16 shadow or fp32, 32-byte aligned);
+ * mlp_shadow bf16 (16-byte aligned) and mlp_master fp32 in the flat MLP
+ * layout; y [N] f32 (device).  No workspace (fh_infer_workspace_size
+ * returns 0; workspace may be NULL).  F-Hash encoders only.  Errors as
+ * fh_train_fwd_bwd. */
 size_t    fh_infer_workspace_size(fh_encoder enc, const fh_mlp_desc *mlp, int64_t max_batch);
 fh_status fh_infer(fh_encoder enc, const fh_mlp_desc *mlp, const void *table, const void *mlp_shadow,
                    const float *mlp_master, const float *coords, int64_t N, float *y, void *workspace,

@@ -2,9 +2,12 @@
 // step" section): trainer object, launch sequence, Adam bookkeeping.
 #include <cuda_runtime.h>
 
+#include <dlfcn.h>
+
 #include <cmath>
 #include <cstring>
 #include <new>
+#include <vector>
 
 #include "internal.h"
 #include "mlp_kernels.cuh"
@@ -32,6 +35,19 @@ struct fh_trainer_s {
     cudaEvent_t bwd_ev[FH_MAX_LEVELS + 1] = {};  // caller's events, recorded after each backward launch
     int n_bwd_ev = 0;
     bool flags_cleared = false;        // the workspace flags are zeroed on the first step's stream
+    // fused data-parallel form (fh_trainer_set_comm)
+    struct DP {
+        void *comm = nullptr;
+        int W = 1, rank = 0;
+        cudaStream_t cs = nullptr;                 // communication stream
+        cudaEvent_t ev[FH_MAX_LEVELS + 1] = {};    // after each backward launch
+        cudaEvent_t ev_step = nullptr, ev_red = nullptr;
+        struct Main { int launch; int64_t a, m; };
+        std::vector<Main> mains;                   // reduce-scattered parts (overlap plan)
+        std::vector<int64_t> tb, te;               // tails (replicated)
+        float *shard = nullptr, *tail = nullptr;   // workspace views
+        int64_t n_tail = 0;
+    } dp;
 };
 
 namespace {
@@ -300,6 +316,167 @@ static fh_status apply_ranges_impl(fh_trainer tr, int n, const int64_t *begin, c
     return cuda_check(cudaGetLastError(), "adam_kernel launch");
 }
 
+// ------------------------------------------------------------ fused DP (NCCL)
+// NCCL through the libnccl.so.2 torch already loaded (no link-time
+// dependency; the C ABI of ncclUniqueId / enums is stable).
+namespace nccl {
+struct UniqueId { char internal[128]; };
+typedef int (*GetUniqueId_t)(UniqueId *);
+typedef int (*CommInitRank_t)(void **, int, UniqueId, int);
+typedef int (*CommDestroy_t)(void *);
+typedef int (*ReduceScatter_t)(const void *, void *, size_t, int, int, void *, cudaStream_t);
+typedef int (*AllReduce_t)(const void *, void *, size_t, int, int, void *, cudaStream_t);
+typedef int (*AllGather_t)(const void *, void *, size_t, int, void *, cudaStream_t);
+typedef int (*Group_t)();
+typedef const char *(*ErrStr_t)(int);
+constexpr int kFloat16 = 6, kFloat32 = 7, kSum = 0;
+struct Api {
+    bool ok = false;
+    GetUniqueId_t get_id; CommInitRank_t init; CommDestroy_t destroy;
+    ReduceScatter_t reduce_scatter; AllReduce_t all_reduce; AllGather_t all_gather;
+    Group_t group_start, group_end; ErrStr_t err;
+};
+static Api &api() {
+    static Api a;
+    static bool tried = false;
+    if (tried) return a;
+    tried = true;
+    void *h = dlopen("libnccl.so.2", RTLD_NOW | RTLD_NOLOAD);
+    if (!h) h = dlopen("libnccl.so.2", RTLD_NOW | RTLD_GLOBAL);
+    if (!h) return a;
+    a.get_id = (GetUniqueId_t)dlsym(h, "ncclGetUniqueId");
+    a.init = (CommInitRank_t)dlsym(h, "ncclCommInitRank");
+    a.destroy = (CommDestroy_t)dlsym(h, "ncclCommDestroy");
+    a.reduce_scatter = (ReduceScatter_t)dlsym(h, "ncclReduceScatter");
+    a.all_reduce = (AllReduce_t)dlsym(h, "ncclAllReduce");
+    a.all_gather = (AllGather_t)dlsym(h, "ncclAllGather");
+    a.group_start = (Group_t)dlsym(h, "ncclGroupStart");
+    a.group_end = (Group_t)dlsym(h, "ncclGroupEnd");
+    a.err = (ErrStr_t)dlsym(h, "ncclGetErrorString");
+    a.ok = a.get_id && a.init && a.destroy && a.reduce_scatter && a.all_reduce && a.all_gather && a.group_start &&
+           a.group_end && a.err;
+    return a;
+}
+static fh_status check(int r, const char *what) {
+    if (r == 0) return FH_OK;
+    return fail(FH_E_CUDA, "%s: NCCL error %d (%s)", what, r, api().err ? api().err(r) : "?");
+}
+}  // namespace nccl
+
+// The partition of the table gradient (dp.overlap_plan): every range a
+// backward launch finalises splits into a MAIN part [a, a + m) -- a = the
+// range start rounded up to 4, m the largest multiple of 4 W that fits --
+// reduce-scattered in W chunks of m / W (16-byte aligned for the vectorised
+// Adam), and < 4 W + 4 TAIL elements all-reduced and updated on every rank.
+static void dp_plan(fh_trainer tr, int W) {
+    auto &d = tr->dp;
+    d.mains.clear(); d.tb.clear(); d.te.clear();
+    const int q = 4 * W;
+    const int n = fh::bwd_launch_count(tr->enc);
+    int64_t r[2 * 64];
+    for (int li = 0; li < n; li++) {
+        const int k = fh::bwd_launch_ranges(tr->enc, li, r, 64);
+        for (int j = 0; j < k && j < 64; j++) {
+            const int64_t b = r[2 * j], e = r[2 * j + 1];
+            int64_t a = (b + 3) / 4 * 4;
+            if (a > e) a = e;
+            const int64_t m = (e - a) / q * q;
+            if (a > b) { d.tb.push_back(b); d.te.push_back(a); }
+            if (m > 0) d.mains.push_back({li, a, m});
+            if (a + m < e) { d.tb.push_back(a + m); d.te.push_back(e); }
+        }
+    }
+    d.n_tail = 0;
+    for (size_t i = 0; i < d.tb.size(); i++) d.n_tail += d.te[i] - d.tb[i];
+}
+
+static size_t dp_bytes(fh_trainer tr, int W, size_t *shard_floats) {
+    dp_plan(tr, W);
+    size_t sf = 0;
+    for (auto &m : tr->dp.mains) sf += (size_t)(m.m / W);
+    if (shard_floats) *shard_floats = sf;
+    const size_t P = (size_t)fh::mlp::param_count(tr->K0);
+    return align_up(sf * 4, 256) + align_up(((size_t)tr->dp.n_tail + P) * 4, 256);
+}
+
+// One fused data-parallel step (fh_train_step with a communicator).
+static fh_status dp_step(fh_trainer tr, const float *coords, const float *target, int64_t N, int64_t N_global,
+                         float *loss_dev, fh_stream stream) {
+    auto &d = tr->dp;
+    auto &A = nccl::api();
+    cudaStream_t s = reinterpret_cast<cudaStream_t>(stream);
+    fh_status st = fh_train_fwd_bwd(tr, coords, target, N, N_global, loss_dev, stream);
+    if (st != FH_OK) return st;
+    if ((st = cuda_check(cudaEventRecord(d.ev_step, s), "dp: record step")) != FH_OK) return st;
+    float *g = tr->b.table_grad;
+    const int W = d.W;
+    // per backward launch: reduce-scatter its main parts once its gradients are final
+    const int n_launch = fh::bwd_launch_count(tr->enc);
+    size_t k = 0;
+    float *sh = d.shard;
+    for (int li = 0; li < n_launch; li++) {
+        if ((st = cuda_check(cudaStreamWaitEvent(d.cs, d.ev[li], 0), "dp: wait bwd event")) != FH_OK) return st;
+        if (k < d.mains.size() && d.mains[k].launch == li) {
+            A.group_start();
+            for (; k < d.mains.size() && d.mains[k].launch == li; k++) {
+                const auto &m = d.mains[k];
+                if ((st = nccl::check(A.reduce_scatter(g + m.a, sh, (size_t)(m.m / W), nccl::kFloat32, nccl::kSum,
+                                                       d.comm, d.cs), "ncclReduceScatter")) != FH_OK) {
+                    A.group_end();
+                    return st;
+                }
+                sh += m.m / W;
+            }
+            if ((st = nccl::check(A.group_end(), "ncclGroupEnd")) != FH_OK) return st;
+        }
+    }
+    // tails + MLP grads (the whole local step is done): all-reduce, MLP grads back
+    if ((st = cuda_check(cudaStreamWaitEvent(d.cs, d.ev_step, 0), "dp: wait step")) != FH_OK) return st;
+    float *t = d.tail;
+    for (size_t i = 0; i < d.tb.size(); i++) {
+        const int64_t n = d.te[i] - d.tb[i];
+        if ((st = cuda_check(cudaMemcpyAsync(t, g + d.tb[i], (size_t)n * 4, cudaMemcpyDeviceToDevice, d.cs),
+                             "dp: gather tails")) != FH_OK) return st;
+        t += n;
+    }
+    const int64_t P = fh::mlp::param_count(tr->K0);
+    if ((st = cuda_check(cudaMemcpyAsync(t, tr->b.mlp_grad, (size_t)P * 4, cudaMemcpyDeviceToDevice, d.cs),
+                         "dp: mlp grads")) != FH_OK) return st;
+    if ((st = nccl::check(A.all_reduce(d.tail, d.tail, (size_t)(d.n_tail + P), nccl::kFloat32, nccl::kSum, d.comm,
+                                       d.cs), "ncclAllReduce")) != FH_OK) return st;
+    if ((st = cuda_check(cudaMemcpyAsync(tr->b.mlp_grad, t, (size_t)P * 4, cudaMemcpyDeviceToDevice, d.cs),
+                         "dp: mlp grads back")) != FH_OK) return st;
+    if ((st = cuda_check(cudaEventRecord(d.ev_red, d.cs), "dp: record reduced")) != FH_OK) return st;
+    if ((st = cuda_check(cudaStreamWaitEvent(s, d.ev_red, 0), "dp: wait reduced")) != FH_OK) return st;
+    // ONE Adam over this rank's chunks + the tails (+ the MLP)
+    std::vector<int64_t> b, e;
+    std::vector<float *> gp;
+    sh = d.shard;
+    for (auto &m : d.mains) {
+        const int64_t c = m.m / W;
+        b.push_back(m.a + d.rank * c); e.push_back(m.a + (d.rank + 1) * c); gp.push_back(sh);
+        sh += c;
+    }
+    t = d.tail;
+    for (size_t i = 0; i < d.tb.size(); i++) {
+        b.push_back(d.tb[i]); e.push_back(d.te[i]); gp.push_back(t);
+        t += d.te[i] - d.tb[i];
+    }
+    if ((st = apply_ranges_impl(tr, (int)b.size(), b.data(), e.data(), gp.data(), s)) != FH_OK) return st;
+    // all-gather the fp16 shadow chunks (in place), on the caller's stream
+    __half *shadow = reinterpret_cast<__half *>(tr->b.table_shadow);
+    A.group_start();
+    for (auto &m : d.mains) {
+        const int64_t c = m.m / W;
+        if ((st = nccl::check(A.all_gather(shadow + m.a + d.rank * c, shadow + m.a, (size_t)c, nccl::kFloat16, d.comm,
+                                           s), "ncclAllGather")) != FH_OK) {
+            A.group_end();
+            return st;
+        }
+    }
+    return nccl::check(A.group_end(), "ncclGroupEnd");
+}
+
 static fh_status apply_impl(fh_trainer tr, int64_t begin, int64_t end, float *tgrad, cudaStream_t s) {
     float *g[1] = {tgrad};
     return apply_ranges_impl(tr, end > begin ? 1 : 0, &begin, &end, g, s);
@@ -435,6 +612,7 @@ fh_status fh_train_apply_sharded(fh_trainer tr, int64_t begin, int64_t end, cons
 
 fh_status fh_train_step(fh_trainer tr, const float *coords, const float *target, int64_t N, int64_t N_global,
                         float *loss_dev, fh_stream stream) {
+    if (tr && tr->dp.comm) return dp_step(tr, coords, target, N, N_global, loss_dev, stream);
     fh_status st = fh_train_fwd_bwd(tr, coords, target, N, N_global, loss_dev, stream);
     if (st != FH_OK) return st;
     return fh_train_apply(tr, stream);
@@ -575,6 +753,90 @@ int64_t fh_arm_pace(int64_t n_rays, int64_t n_alive) {
     return p < 1 ? 1 : p;
 }
 
-void fh_trainer_destroy(fh_trainer tr) { delete tr; }
+fh_status fh_nccl_unique_id(void *id128) {
+    g_err[0] = 0;
+    if (!id128) return fail(FH_E_ARG, "fh_nccl_unique_id: NULL id");
+    auto &A = nccl::api();
+    if (!A.ok) return fail(FH_E_STATE, "fh_nccl_unique_id: libnccl.so.2 not loadable");
+    nccl::UniqueId id;
+    fh_status st = nccl::check(A.get_id(&id), "ncclGetUniqueId");
+    if (st == FH_OK) memcpy(id128, &id, sizeof(id));
+    return st;
+}
+
+fh_status fh_nccl_comm_create(const void *id128, int nranks, int rank, void **comm) {
+    g_err[0] = 0;
+    if (!id128 || !comm) return fail(FH_E_ARG, "fh_nccl_comm_create: NULL pointer");
+    if (nranks < 1 || rank < 0 || rank >= nranks) return fail(FH_E_ARG, "fh_nccl_comm_create: bad rank / nranks");
+    auto &A = nccl::api();
+    if (!A.ok) return fail(FH_E_STATE, "fh_nccl_comm_create: libnccl.so.2 not loadable");
+    nccl::UniqueId id;
+    memcpy(&id, id128, sizeof(id));
+    *comm = nullptr;
+    return nccl::check(A.init(comm, nranks, id, rank), "ncclCommInitRank");
+}
+
+fh_status fh_nccl_comm_destroy(void *comm) {
+    g_err[0] = 0;
+    if (!comm) return FH_OK;
+    auto &A = nccl::api();
+    if (!A.ok) return fail(FH_E_STATE, "fh_nccl_comm_destroy: libnccl.so.2 not loadable");
+    return nccl::check(A.destroy(comm), "ncclCommDestroy");
+}
+
+size_t fh_trainer_dp_workspace_size(fh_trainer tr, int nranks) {
+    if (!tr || nranks < 1) return 0;
+    return dp_bytes(tr, nranks, nullptr);
+}
+
+fh_status fh_trainer_set_comm(fh_trainer tr, void *comm, int nranks, int rank, void *workspace, size_t bytes) {
+    g_err[0] = 0;
+    if (!tr) return fail(FH_E_ARG, "fh_trainer_set_comm: NULL trainer");
+    auto &d = tr->dp;
+    // detach (also before re-attaching): stream-ordered teardown of the old state
+    if (d.cs) {
+        cudaStreamSynchronize(d.cs);
+        for (auto &e : d.ev) if (e) { cudaEventDestroy(e); e = nullptr; }
+        if (d.ev_step) cudaEventDestroy(d.ev_step);
+        if (d.ev_red) cudaEventDestroy(d.ev_red);
+        cudaStreamDestroy(d.cs);
+        tr->n_bwd_ev = 0;
+    }
+    tr->dp = fh_trainer_s::DP{};
+    if (!comm) return FH_OK;
+    if (nranks < 1 || rank < 0 || rank >= nranks) return fail(FH_E_ARG, "fh_trainer_set_comm: bad rank / nranks");
+    if (!tr->b.table_shadow || tr->enc->table_dtype != FH_F16)
+        return fail(FH_E_STATE, "fh_trainer_set_comm: the fused DP form needs an FH_F16 table (fp16 shadow)");
+    size_t sf = 0;
+    const size_t need = dp_bytes(tr, nranks, &sf);
+    if (!workspace || bytes < need || !aligned(workspace, 256))
+        return fail(FH_E_ARG, "fh_trainer_set_comm: need %zu bytes of 256-byte aligned workspace", need);
+    if (d.mains.size() + d.tb.size() + 1 > (size_t)fh::mlp::kMaxAdamSeg)
+        return fail(FH_E_RANGE, "fh_trainer_set_comm: %zu Adam ranges (max %d)", d.mains.size() + d.tb.size(),
+                    fh::mlp::kMaxAdamSeg - 1);
+    if (!nccl::api().ok) return fail(FH_E_STATE, "fh_trainer_set_comm: libnccl.so.2 not loadable");
+    fh_status st = cuda_check(cudaStreamCreateWithFlags(&d.cs, cudaStreamNonBlocking), "dp: comm stream");
+    if (st != FH_OK) return st;
+    const int n = fh::bwd_launch_count(tr->enc);
+    for (int i = 0; i < n && st == FH_OK; i++)
+        st = cuda_check(cudaEventCreateWithFlags(&d.ev[i], cudaEventDisableTiming), "dp: events");
+    if (st == FH_OK) st = cuda_check(cudaEventCreateWithFlags(&d.ev_step, cudaEventDisableTiming), "dp: events");
+    if (st == FH_OK) st = cuda_check(cudaEventCreateWithFlags(&d.ev_red, cudaEventDisableTiming), "dp: events");
+    if (st != FH_OK) return st;
+    d.comm = comm;
+    d.W = nranks;
+    d.rank = rank;
+    d.shard = reinterpret_cast<float *>(workspace);
+    d.tail = reinterpret_cast<float *>(reinterpret_cast<char *>(workspace) + align_up(sf * 4, 256));
+    for (int i = 0; i < n; i++) tr->bwd_ev[i] = d.ev[i];   // fh_train_fwd_bwd records them
+    tr->n_bwd_ev = n;
+    return FH_OK;
+}
+
+void fh_trainer_destroy(fh_trainer tr) {
+    if (!tr) return;
+    fh_trainer_set_comm(tr, nullptr, 1, 0, nullptr, 0);
+    delete tr;
+}
 
 }  // extern "C"

@@ -34,7 +34,8 @@ EXPORTS = [
     "fh_mlp_param_count", "fh_train_workspace_size", "fh_trainer_create", "fh_train_fwd_bwd", "fh_train_apply",
     "fh_train_step", "fh_trainer_status", "fh_trainer_step_count", "fh_trainer_destroy", "fh_train_apply_sharded",
     "fh_train_bwd_launches", "fh_train_bwd_ranges", "fh_train_set_bwd_events", "fh_train_apply_ranges",
-    "fh_train_apply_peers", "fh_level_stats_workspace_size", "fh_level_stats", "fh_kernel_launches", "fh_encoder_scratch_size", "fh_encoder_attach_scratch",
+    "fh_train_apply_peers", "fh_nccl_unique_id", "fh_nccl_comm_create", "fh_nccl_comm_destroy",
+    "fh_trainer_dp_workspace_size", "fh_trainer_set_comm", "fh_level_stats_workspace_size", "fh_level_stats", "fh_kernel_launches", "fh_encoder_scratch_size", "fh_encoder_attach_scratch",
     # inference (renderer's model evaluation) and the ARM pace rule
     "fh_infer_workspace_size", "fh_infer", "fh_arm_pace",
     # include/fhash_coreset.h (NEXT-4 coreset selection)
@@ -385,6 +386,14 @@ def _train_lib():
                                        ctypes.c_int, ctypes.POINTER(i64), ctypes.POINTER(i64),
                                        ctypes.POINTER(ctypes.c_int), ctypes.c_int, ctypes.c_int, vp]
     L.fh_train_apply_peers.restype = ctypes.c_int
+    L.fh_nccl_unique_id.argtypes = [vp]
+    L.fh_nccl_comm_create.argtypes = [vp, ctypes.c_int, ctypes.c_int, ctypes.POINTER(vp)]
+    L.fh_nccl_comm_destroy.argtypes = [vp]
+    L.fh_trainer_dp_workspace_size.argtypes = [vp, ctypes.c_int]
+    L.fh_trainer_dp_workspace_size.restype = ctypes.c_size_t
+    L.fh_trainer_set_comm.argtypes = [vp, vp, ctypes.c_int, ctypes.c_int, vp, ctypes.c_size_t]
+    for n in ("fh_nccl_unique_id", "fh_nccl_comm_create", "fh_nccl_comm_destroy", "fh_trainer_set_comm"):
+        getattr(L, n).restype = ctypes.c_int
     L.fh_infer_workspace_size.argtypes = [vp, ctypes.POINTER(MLPDesc), i64]
     L.fh_infer_workspace_size.restype = ctypes.c_size_t
     L.fh_infer.argtypes = [vp, ctypes.POINTER(MLPDesc), vp, vp, vp, vp, i64, vp, vp, ctypes.c_size_t, vp]
@@ -572,6 +581,22 @@ class Trainer:
                                           self.loss.data_ptr(), _stream(stream)))
         return self.loss
 
+    def set_comm(self, comm: "NcclComm"):
+        """The fused data-parallel form (fh_trainer_set_comm): from now on
+        step() reduce-scatters / all-reduces / all-gathers through `comm`
+        inside the library.  comm=None detaches."""
+        import torch
+        L = _train_lib()
+        if comm is None:
+            _check(L.fh_trainer_set_comm(self._h, None, 1, 0, None, 0))
+            self._dp_ws = None
+            return
+        n = int(L.fh_trainer_dp_workspace_size(self._h, comm.nranks))
+        self._dp_ws = torch.empty(max(n, 256), dtype=torch.uint8, device=self.grads.device)
+        self._comm = comm   # keep alive
+        _check(L.fh_trainer_set_comm(self._h, comm.handle, comm.nranks, comm.rank, _ptr(self._dp_ws),
+                                     self._dp_ws.numel()))
+
     def status(self, stream=None) -> int:
         s = _train_lib().fh_trainer_status(self._h, _stream(stream))
         if s not in (FH_OK, FH_E_DOMAIN, FH_E_DIVERGED):
@@ -581,6 +606,29 @@ class Trainer:
     @property
     def step_count(self) -> int:
         return int(_train_lib().fh_trainer_step_count(self._h))
+
+
+def nccl_unique_id() -> bytes:
+    """128-byte ncclUniqueId (fh_nccl_unique_id) for NcclComm; rank 0 makes
+    it, the caller broadcasts it (e.g. torch.distributed.broadcast_object_list)."""
+    buf = ctypes.create_string_buffer(128)
+    _check(_train_lib().fh_nccl_unique_id(buf))
+    return buf.raw
+
+
+class NcclComm:
+    """An NCCL communicator made by the library (fh_nccl_comm_create) from
+    torch's libnccl, for Trainer.set_comm (the fused data-parallel form)."""
+
+    def __init__(self, uid: bytes, nranks: int, rank: int):
+        h = ctypes.c_void_p()
+        _check(_train_lib().fh_nccl_comm_create(ctypes.create_string_buffer(uid, 128), nranks, rank, ctypes.byref(h)))
+        self.handle, self.nranks, self.rank = h, nranks, rank
+
+    def destroy(self):
+        if self.handle is not None and self.handle.value:
+            _check(_train_lib().fh_nccl_comm_destroy(self.handle))
+        self.handle = None
 
 
 def arm_pace(n_rays: int, n_alive: int) -> int:

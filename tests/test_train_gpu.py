@@ -495,3 +495,55 @@ def test_fwd_bwd_overwrites_gradients():
     torch.cuda.synchronize()
     assert torch.count_nonzero(ta.grads[:ta.n_table]).item() == 0
     assert torch.count_nonzero(ta.mlp_grad).item() == 0
+
+
+def test_fused_nccl_dp_step_equals_plain_step():
+    """The fused data-parallel form (fh_trainer_set_comm, SURVEY.md §8(b)
+    nccl_comm): the library's own NCCL reduce-scatter of every backward
+    level group (overlapped through per-group events), the tails + MLP
+    all-reduce, ONE Adam over the rank's chunks + tails, and the in-place
+    fp16 all-gather.  On a 1-rank communicator it must be exactly Adam on
+    the step's gradient: a twin trainer fed the same gradients (copied from
+    the DP trainer, whose grad buffers still hold them) and stepped with the
+    plain fh_train_apply ends bit-identical after every step (the atomics of
+    two independent fwd_bwd runs would differ in the last bits)."""
+    cfg = small_cfg(4, 12)
+    g = W.rng(70)
+    enc = fh.Encoder(cfg.levels, cfg.F, cfg.table_dtype, cfg.cap)
+    table = W.draw_table(g, enc.entries, cfg.F, "f32")
+    layers = W.draw_mlp(g, W.MLPConfig((cfg.L * cfg.F, 64, 64, 1)))
+    N = 3000
+    a = fh.Trainer(enc, table, layers, N)
+    b = fh.Trainer(enc, table, layers, N)
+    comm = fh.NcclComm(fh.nccl_unique_id(), 1, 0)
+    b.set_comm(comm)
+    for k in range(3):
+        c = torch.from_numpy(W.draw_coords(g, N)).cuda()
+        t = torch.from_numpy(g.random(N, dtype=np.float32)).cuda()
+        b.step(c, t)
+        a.grads.copy_(b.grads)
+        a.apply()
+        torch.cuda.synchronize()
+        assert torch.equal(a.table_shadow, b.table_shadow), k
+        assert torch.equal(a.table_master, b.table_master), k
+        assert torch.equal(a.mlp_master, b.mlp_master) and torch.equal(a.mlp_shadow, b.mlp_shadow), k
+    assert b.status() == fh.FH_OK and a.step_count == b.step_count == 3
+    b.set_comm(None)
+    comm.destroy()
+
+
+@pytest.mark.parametrize("world", [1, 2, 3, 8])
+def test_fused_dp_plan_matches_overlap_plan(world):
+    """The library's gradient partition for the fused DP form is the one
+    dp.overlap_plan defines (tested on CPU with gloo at world 2): its
+    workspace = this rank's shards (sum m / W) + tails + MLP, 256-aligned."""
+    from paper_2507_03836_b200 import dp
+    cfg = W.CFG3
+    g = W.rng(71)
+    enc = fh.Encoder(cfg.levels, cfg.F, cfg.table_dtype, cfg.cap)
+    tr = fh.Trainer(enc, W.draw_table(g, enc.entries, cfg.F, "f32"), W.draw_mlp(g, W.MLP3), 1024)
+    mains, tails = dp.overlap_plan(tr.bwd_launch_ranges(), world, 0)
+    shard = sum(m // world for (_, _, m) in mains)
+    tail = sum(e - b for b, e in tails) + tr.n_mlp
+    up = lambda v: (v + 255) // 256 * 256
+    assert int(fh._train_lib().fh_trainer_dp_workspace_size(tr._h, world)) == up(4 * shard) + up(4 * tail)
