@@ -11,9 +11,10 @@ CUDA path (`paper_2507_03836_b200/`) and never imports it.
                        1-3): extraction, dilation, occupancy bits, FBB,
                        Eqs. 1-2 coordinates, the Eq. 3 union.
 
-Parity-pin status of each function is listed in DESIGN.md §4; the capped
-(hashed) level index is "parity unpinned" by the paper (pinned only by its
-integer definition and brute-force statistics).
+Parity-pin status of each function is listed in DESIGN.md §4.  The capped
+(hashed) level index (reading R5: the paper never caps) is pinned by values
+worked out by hand from its definition (tests/golden/r5_hash.json), the
+x-adjacency property and brute-force statistics.
 """
 from __future__ import annotations
 
