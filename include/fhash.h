@@ -419,8 +419,8 @@ void      fh_trainer_destroy(fh_trainer tr);
  * The renderer's model evaluation "V = model(S)" (Alg. 1) as ONE
  * fused kernel (NEXT-1): the encode forward of each 128-sample tile goes as
  * bf16 straight into the shared-memory X operand of the tcgen05 MLP forward
- * (a thread-block cluster of up to 8 SMs shares a tile's gathers for small
- * batches), with exactly the forward numerics of the train step (R13).
+ * (small batches are cut into short tiles so they spread over the SMs), with
+ * exactly the forward numerics of the train step (R13).
  * table: the encoder's table dtype (fp16 shadow or fp32, 32-byte aligned);
  * mlp_shadow bf16 (16-byte aligned) and mlp_master fp32 in the flat MLP
  * layout; y [N] f32 (device).  No workspace (fh_infer_workspace_size

@@ -6,27 +6,23 @@
 // bias + ReLU -> MMA2 -> bias + ReLU -> 64 -> 1 output): no encoder-output
 // round trip through global memory, one launch.
 //
-// Why a cluster.  A 128-sample tile is 128 L corner-cell gathers, i.e.
-// 8 x 128 L pair requests (16 K at L = 16): one SM issues about one L2
-// request per cycle, so a tile gathered by one CTA costs >= 8 us however the
-// loads are scheduled (measured: 22.7 us for a single tile).  Here a
-// cluster of C = 8 CTAs (8 SMs) shares every tile: CTA r gathers the items
-// i = r, r + C, ... of the tile and stores their bf16 features into the X
-// tile of the tile's LEADER CTA through distributed shared memory; tiles
-// rotate over the cluster's CTAs as leaders, so the MLP work is spread too.
+// Short tiles for small batches.  A 128-sample tile is 128 L corner-cell
+// gathers, i.e. 8 x 128 L pair requests (16 K at L = 16), and one SM issues
+// about one L2 request per cycle: a full tile gathered by one CTA costs
+// >= 8 us (measured 22.7 us for one tile).  So a batch that does not fill
+// the GPU is cut into tiles of R = 8 .. 128 samples (the smallest power of
+// two that keeps one wave of CTAs), each CTA gathering and evaluating its
+// own: the MMA still runs M = 128 rows, those past R are never read back.
+// (Thread-block clusters sharing a tile's gathers through distributed
+// shared memory were measured too -- never faster than short tiles, and
+// slower at 4096 samples: 12.3 vs 10.7 us.)
 //
-// Large batches need no spreading: there the cluster size is 1 (every CTA
-// gathers and evaluates its own tiles, CTA-scope fences only).
-//
-// Roles per CTA: warps 0-3 run the MLP of the tiles this CTA leads
-// (thread t = TMEM lane = sample row t); the other warps gather, as 2-3
-// groups of 8 warps working on different tiles (more loads in flight).  Per
-// leader NB = 4 X buffers; mbarriers (no cluster-wide barrier in the loop):
-//   full[b]     (in the leader)  C x 8 gather-warp arrivals: X[b] complete;
-//   xfree[L][b] (in every CTA)   1 arrival from leader L's MLP thread once
-//                                MMA1 has consumed L's X[b].
-// Cluster-local tile u (global tile c + n_clusters u of cluster c) is led by
-// rank u % C in buffer (u / C) % NB.
+// Roles per CTA: warps 0-3 run the MLP (thread t = TMEM lane = sample row
+// t); the other warps gather, as G groups of 8 warps working on different
+// tiles (more loads in flight per SM).  X buffers: NB = 4; mbarriers
+//   full[b]   8 arrivals (the gather warps of the group that filled X[b]);
+//   xfree[b]  1 arrival from the MLP thread once MMA1 has consumed X[b].
+// The CTA's tile u (global tile blockIdx.x + gridDim.x u) uses X[u % NB].
 //
 // Numerics = fh_encode_fwd(FH_BF16) followed by the forward half of
 // mlp_train_kernel: the same gather / lerp tree / RNE bf16 rounding of the
@@ -42,14 +38,13 @@ namespace infer {
 using mlp::H;
 using mlp::TILE;
 
-constexpr int kMaxCluster = 8;              // CTAs per cluster (portable maximum; 16 measured slower: fewer
-                                            // resident clusters, longer waits for the slowest CTA)
 constexpr int kMlpWarps = 4, kGatherWarps = 8;   // gather warps per group
-// groups of gather warps work on different tiles concurrently (more loads in
-// flight per SM); the register file bounds them: 3 groups (896 threads, 72
-// registers) for F <= 2, 2 groups (640 threads, 96 registers) for wider entries
+// Short-tile launches (small batches) use one gather group (384 threads: a
+// smaller CTA launches faster); full tiles as many as the register file
+// allows: 3 groups (896 threads, 72 registers) for F <= 2, 2 (640 threads,
+// 96 registers) for wider entries.
 template <int F> struct Groups { static constexpr int value = F <= 2 ? 3 : 2; };
-template <int F> struct Threads { static constexpr int value = 32 * (kMlpWarps + Groups<F>::value * kGatherWarps); };
+template <int G> struct Threads { static constexpr int value = 32 * (kMlpWarps + G * kGatherWarps); };
 
 template <int K0>
 struct FusedLayout {
@@ -71,107 +66,56 @@ struct FusedArgs {
     float *y;                      // [N]
     int64_t N;
     int *flag;                     // encoder status word (out-of-domain coordinates)
+    int rows;                      // samples per tile R (8 .. 128, a power of two)
 };
 
-// ---- cluster / DSMEM / mbarrier primitives (PTX ISA: mapa, st.shared::cluster,
-// mbarrier.arrive.release.cluster, barrier.cluster)
-__device__ __forceinline__ uint32_t cluster_rank() {
-    uint32_t r;
-    asm volatile("mov.u32 %0, %%cluster_ctarank;" : "=r"(r));
-    return r;
-}
-__device__ __forceinline__ uint32_t cluster_size() {
-    uint32_t r;
-    asm volatile("mov.u32 %0, %%cluster_nctarank;" : "=r"(r));
-    return r;
-}
-__device__ __forceinline__ uint32_t cluster_id() {
-    uint32_t r;
-    asm volatile("mov.u32 %0, %%clusterid.x;" : "=r"(r));
-    return r;
-}
-__device__ __forceinline__ uint32_t n_clusters() {
-    uint32_t r;
-    asm volatile("mov.u32 %0, %%nclusterid.x;" : "=r"(r));
-    return r;
-}
-__device__ __forceinline__ uint32_t mapa(uint32_t saddr, uint32_t rank) {
-    uint32_t r;
-    asm volatile("mapa.shared::cluster.u32 %0, %1, %2;" : "=r"(r) : "r"(saddr), "r"(rank));
-    return r;
-}
-__device__ __forceinline__ void cluster_sync_all() {
-    asm volatile("barrier.cluster.arrive.release.aligned;\n\tbarrier.cluster.wait.acquire.aligned;" ::: "memory");
-}
-__device__ __forceinline__ void arrive_remote(uint32_t cluster_addr) {
-    asm volatile("mbarrier.arrive.release.cluster.shared::cluster.b64 _, [%0];" ::"r"(cluster_addr) : "memory");
-}
-__device__ __forceinline__ void wait_cluster(uint64_t *mbar, uint32_t parity) {
-    const uint32_t a = tc::smem_u32(mbar);
-    asm volatile(
-        "{\n\t.reg .pred p;\n\t"
-        "W_%=:\n\t"
-        "mbarrier.try_wait.parity.acquire.cluster.shared::cta.b64 p, [%0], %1;\n\t"
-        "@!p bra W_%=;\n\t}\n" ::"r"(a),
-        "r"(parity)
-        : "memory");
-}
-
-// bf16 of the F blended features into X at a shared::cluster address.
+// bf16 of the F blended features into the X tile at p.
 template <int F>
-__device__ __forceinline__ void st_x_remote(uint32_t addr, const float (&v)[F]) {
+__device__ __forceinline__ void st_x(uint8_t *p, const float (&v)[F]) {
     if constexpr (F == 1) {
-        const __nv_bfloat16 h = __float2bfloat16_rn(v[0]);
-        asm volatile("st.shared::cluster.b16 [%0], %1;" ::"r"(addr), "h"(*reinterpret_cast<const unsigned short *>(&h))
-                     : "memory");
+        *reinterpret_cast<__nv_bfloat16 *>(p) = __float2bfloat16_rn(v[0]);
     } else if constexpr (F == 2) {
-        asm volatile("st.shared::cluster.b32 [%0], %1;" ::"r"(addr), "r"(mlp::pack_bf16(v[0], v[1])) : "memory");
+        *reinterpret_cast<uint32_t *>(p) = mlp::pack_bf16(v[0], v[1]);
     } else if constexpr (F == 4) {
-        asm volatile("st.shared::cluster.v2.b32 [%0], {%1, %2};" ::"r"(addr), "r"(mlp::pack_bf16(v[0], v[1])),
-                     "r"(mlp::pack_bf16(v[2], v[3]))
-                     : "memory");
+        *reinterpret_cast<uint2 *>(p) = make_uint2(mlp::pack_bf16(v[0], v[1]), mlp::pack_bf16(v[2], v[3]));
     } else {
-        asm volatile("st.shared::cluster.v4.b32 [%0], {%1, %2, %3, %4};" ::"r"(addr), "r"(mlp::pack_bf16(v[0], v[1])),
-                     "r"(mlp::pack_bf16(v[2], v[3])), "r"(mlp::pack_bf16(v[4], v[5])), "r"(mlp::pack_bf16(v[6], v[7]))
-                     : "memory");
+        *reinterpret_cast<uint4 *>(p) = make_uint4(mlp::pack_bf16(v[0], v[1]), mlp::pack_bf16(v[2], v[3]),
+                                                   mlp::pack_bf16(v[4], v[5]), mlp::pack_bf16(v[6], v[7]));
     }
 }
 
+__device__ __forceinline__ void mbar_arrive(uint64_t *mbar) {
+    asm volatile("mbarrier.arrive.shared::cta.b64 _, [%0];" ::"r"(tc::smem_u32(mbar)) : "memory");
+}
 
-template <int F, typename T, int K0>
-__global__ void __launch_bounds__(Threads<F>::value, 1) infer_fused_kernel(const __grid_constant__ Params P, const FusedArgs a) {
+template <int F, typename T, int K0, int G>
+__global__ void __launch_bounds__(Threads<G>::value, 1) infer_fused_kernel(const __grid_constant__ Params P, const FusedArgs a) {
     using Lo = FusedLayout<K0>;
+    constexpr int NB = Lo::NB;
     extern __shared__ __align__(1024) uint8_t smem[];
     uint8_t *sW1 = smem;
     uint8_t *sW2 = sW1 + Lo::BYTES_W1;
     uint8_t *sX0 = sW2 + Lo::BYTES_W2;       // X[0 .. NB)
-    uint8_t *sH = sX0 + Lo::NB * Lo::BYTES_X;
-    constexpr int NB = Lo::NB;
+    uint8_t *sH = sX0 + NB * Lo::BYTES_X;
     __shared__ LevelSmem slv;
-    __shared__ uint64_t full[Lo::NB], xfree[kMaxCluster][Lo::NB], mma_bar;
+    __shared__ uint64_t full[NB], xfree[NB], mma_bar;
     __shared__ uint32_t tbase;
     __shared__ float b1[H], b2[H], w3[H];
 
     const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
-    const uint32_t rank = cluster_rank(), cid = cluster_id(), ncl = n_clusters();
-    const int C = (int)cluster_size();
     if (tid == 0) {
         for (int b = 0; b < NB; b++) {
-            tc::mbar_init(&full[b], C * kGatherWarps);
-            for (int l = 0; l < C; l++) tc::mbar_init(&xfree[l][b], 1);
+            tc::mbar_init(&full[b], kGatherWarps);
+            tc::mbar_init(&xfree[b], 1);
         }
         tc::mbar_init(&mma_bar, 1);
         tc::fence_mbar_init();
     }
-    tc::fence_smem_to_async();
-    load_levels(P, slv);
-    tc::fence_before_sync();
-    cluster_sync_all();   // every CTA's barriers initialised before any remote arrive
-    tc::fence_after_sync();
+    load_levels(P, slv);   // ends with __syncthreads: barriers and level table ready
 
-    constexpr int R = TILE;
+    const int R = a.rows;
     const int64_t n_tiles = (a.N + R - 1) / R;
-    const int64_t n_u = (int64_t)cid < n_tiles ? (n_tiles - cid + ncl - 1) / ncl : 0;   // this cluster's tiles
+    const int64_t n_u = (int64_t)blockIdx.x < n_tiles ? (n_tiles - blockIdx.x + gridDim.x - 1) / gridDim.x : 0;
     const int L = P.L;
 
     if (warp >= kMlpWarps) {
@@ -181,19 +125,16 @@ __global__ void __launch_bounds__(Threads<F>::value, 1) infer_fused_kernel(const
         const int gt = gq % (32 * kGatherWarps);      // 0 .. 255 within the group
         const T *table = reinterpret_cast<const T *>(a.table);
         const int items = R * L;
-        const uint32_t x0 = tc::smem_u32(sX0);
-        const uint32_t full0 = tc::smem_u32(&full[0]);
-        // tiles u = grp, grp + G, ...: tiles u and u + NB C (the next use of a
-        // leader's buffer) may belong to different groups, so the xfree wait
-        // orders them
-        for (int64_t u = grp; u < n_u; u += Groups<F>::value) {
-            const uint32_t ld = (uint32_t)(u % C), b = (uint32_t)((u / C) % NB);
-            const int64_t m = u / (NB * C);           // use index of (leader, buffer)
-            if (m > 0) wait_cluster(&xfree[ld][b], (uint32_t)((m - 1) & 1));
-            const int64_t tile = (int64_t)cid + (int64_t)ncl * u;
-            const uint32_t xr = mapa(x0 + b * Lo::BYTES_X, ld);
+        // tiles u = grp, grp + G, ...: tile u + NB (the next use of buffer
+        // u % NB) may belong to another group, so the xfree wait orders them
+        for (int64_t u = grp; u < n_u; u += G) {
+            const int b = (int)(u % NB);
+            const int64_t m = u / NB;                 // use index of the buffer
+            if (m > 0) tc::mbar_wait(&xfree[b], (uint32_t)((m - 1) & 1));
+            const int64_t tile = (int64_t)blockIdx.x + (int64_t)gridDim.x * u;
+            uint8_t *sX = sX0 + b * Lo::BYTES_X;
 #pragma unroll 1
-            for (int i = (int)rank + C * gt; i < items; i += C * 32 * kGatherWarps) {
+            for (int i = gt; i < items; i += 32 * kGatherWarps) {
                 const int s = i / L, l = i - s * L;
                 const int64_t n = tile * R + s;
                 float v[F];
@@ -207,32 +148,25 @@ __global__ void __launch_bounds__(Threads<F>::value, 1) infer_fused_kernel(const
 #pragma unroll
                     for (int f = 0; f < F; f++) v[f] = 0.f;
                 }
-                st_x_remote<F>(xr + tc::core_off(s, l * F, Lo::SBO_X), v);
+                st_x<F>(sX + tc::core_off(s, l * F, Lo::SBO_X), v);
             }
-            // the stores (generic proxy) must be visible to the leader's tensor core
-            if (C > 1) {   // stores into a peer's X: cluster-scope proxy fence + release
-                asm volatile("fence.proxy.async;" ::: "memory");
-                __syncwarp();
-                if (lane == 0) arrive_remote(mapa(full0 + b * 8, ld));
-            } else {       // own X: CTA scope is enough
-                tc::fence_smem_to_async();
-                __syncwarp();
-                if (lane == 0) asm volatile("mbarrier.arrive.shared::cta.b64 _, [%0];" ::"r"(full0 + b * 8) : "memory");
-            }
+            // the stores (generic proxy) must be visible to the tensor core
+            tc::fence_smem_to_async();
+            __syncwarp();
+            if (lane == 0) mbar_arrive(&full[b]);
         }
     } else {
-        // ------------------------------------------------ MLP warps (this CTA's tiles)
+        // ------------------------------------------------ MLP warps
         // TMEM and the weights are set up here, while the gather warps already gather
         if (warp == 0) tc::tmem_alloc(&tbase, 64);
-        // weights -> shared memory (core-matrix layout, one 16-byte row segment per store)
-        {
+        {   // weights -> shared memory (core-matrix layout, one 16-byte row segment per store)
             const uint4 *w = reinterpret_cast<const uint4 *>(a.wsh);
-            for (int q = tid; q < H * K0 / 8; q += (32 * kMlpWarps)) {
+            for (int q = tid; q < H * K0 / 8; q += 32 * kMlpWarps) {
                 const int r = q / (K0 / 8), c = (q % (K0 / 8)) * 8;
                 mlp::st16(sW1, tc::core_off(r, c, Lo::SBO_X), __ldg(w + (mlp::off_W1() / 8) + q));
             }
             const uint4 *w2 = reinterpret_cast<const uint4 *>(a.wsh + mlp::off_W2(K0));
-            for (int q = tid; q < H * H / 8; q += (32 * kMlpWarps)) {
+            for (int q = tid; q < H * H / 8; q += 32 * kMlpWarps) {
                 const int r = q / (H / 8), c = (q % (H / 8)) * 8;
                 mlp::st16(sW2, tc::core_off(r, c, Lo::SBO_H), __ldg(w2 + q));
             }
@@ -252,12 +186,10 @@ __global__ void __launch_bounds__(Threads<F>::value, 1) infer_fused_kernel(const
         const uint32_t aH = tc::smem_u32(sH), aW1 = tc::smem_u32(sW1), aW2 = tc::smem_u32(sW2);
         constexpr uint32_t id_h = tc::idesc_bf16_f32(128, H, false, false);
         const float b3 = a.wmaster[mlp::off_b3(K0)];
-        const uint32_t xfree0 = tc::smem_u32(&xfree[rank][0]);
         uint32_t phase = 0;
-        for (int64_t u = rank; u < n_u; u += C) {
-            const uint32_t b = (uint32_t)((u / C) % NB);
-            const int64_t m = u / (NB * C);
-            wait_cluster(&full[b], (uint32_t)(m & 1));
+        for (int64_t u = 0; u < n_u; u++) {
+            const int b = (int)(u % NB);
+            tc::mbar_wait(&full[b], (uint32_t)((u / NB) & 1));
             tc::fence_after_sync();
             const uint32_t aX = tc::smem_u32(sX0 + b * Lo::BYTES_X);
             // ---- MMA1: Z1 = X . W1^T
@@ -270,13 +202,8 @@ __global__ void __launch_bounds__(Threads<F>::value, 1) infer_fused_kernel(const
             }
             tc::mbar_wait(&mma_bar, phase); phase ^= 1;
             tc::fence_after_sync();
-            // X[b] consumed: free it in every CTA of the cluster (lane j -> CTA j, in
-            // parallel) -- only if the gather warps will refill it (tile u + NB C),
-            // so every remote arrival targets a CTA that is still waiting for it
-            if (tid < C && u + NB * C < n_u) {
-                if (C > 1) arrive_remote(mapa(xfree0 + b * 8, (uint32_t)tid));
-                else asm volatile("mbarrier.arrive.shared::cta.b64 _, [%0];" ::"r"(xfree0 + b * 8) : "memory");
-            }
+            // X[b] consumed: free it (only if a gather group will refill it)
+            if (tid == 0 && u + NB < n_u) mbar_arrive(&xfree[b]);
             // ---- H1 = bf16(relu(Z1 + b1))
 #pragma unroll
             for (int c = 0; c < H; c += 16) {
@@ -292,7 +219,7 @@ __global__ void __launch_bounds__(Threads<F>::value, 1) infer_fused_kernel(const
             }
             tc::fence_smem_to_async();
             tc::fence_before_sync();
-            mlp::slot_sync(0);                            // named barrier 1 over the 128 MLP threads
+            mlp::slot_sync(0);
             tc::fence_after_sync();
             // ---- MMA2: Z2 = H1 . W2^T
             if (tid == 0) {
@@ -315,17 +242,13 @@ __global__ void __launch_bounds__(Threads<F>::value, 1) infer_fused_kernel(const
                 for (int j = 0; j < 16; j++)
                     ya[j & 3] = fmaf(mlp::bf16r(fmaxf(v[j] + b2[c + j], 0.f)), w3[c + j], ya[j & 3]);
             }
-            const int64_t n = ((int64_t)cid + (int64_t)ncl * u) * R + row;
-            if (n < a.N) a.y[n] = ((ya[0] + ya[1]) + (ya[2] + ya[3])) + b3;
+            const int64_t n = ((int64_t)blockIdx.x + (int64_t)gridDim.x * u) * R + row;
+            if (row < R && n < a.N) a.y[n] = ((ya[0] + ya[1]) + (ya[2] + ya[3])) + b3;
             tc::fence_before_sync();
             mlp::slot_sync(0);                            // TMEM and H reused by the next tile
             tc::fence_after_sync();
         }
     }
-    // No closing cluster barrier: a CTA's X buffers and barriers are only
-    // written by peers while it still waits for them (full[] before each of
-    // its MLP tiles, xfree[] before each refill), so every CTA may exit as
-    // soon as its own work is done.
     tc::fence_before_sync();
     __syncthreads();
     if (warp == 0) tc::tmem_dealloc(tbase, 64);

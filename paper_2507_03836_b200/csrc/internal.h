@@ -72,7 +72,7 @@ struct fh_encoder_s {
     double fwd_limit = 0.0, bwd_limit = 0.0;         // L2 budgets of one direct pass (bytes; 0 = one pass)
     int n_sm = 148;                                  // SMs of the device (set with the status word)
     int smem_optin = 0;                              // max dynamic shared memory per CTA (opt-in)
-    int infer_clusters[4][4] = {};                   // fh_infer: resident clusters of size 8, 4, 2, 1, per n_in/16 - 1
+    bool infer_ready[4] = {false, false, false, false};   // fh_infer: kernels set up, per n_in/16 - 1
     // Shifted-pair scratch, one caller-owned slot per
     // stream (fh_encoder_attach_scratch): tsh = the table shifted by one
     // entry (forward), gsh = fp32 gradient scratch shifted by two floats

@@ -647,58 +647,39 @@ size_t fh_infer_workspace_size(fh_encoder enc, const fh_mlp_desc *m, int64_t max
 namespace {
 
 // One fused inference launch (infer_kernels.cuh) for the encoder's F and
-// table dtype and the MLP's K0.  The kernel's shared-memory limit and its
-// CTAs per SM are fixed once per encoder (first call), never per call.
+// table dtype and the MLP's K0.  The kernels' shared-memory limits are
+// raised once per encoder (first call), never per call.
 template <int F, typename T, int K0>
 fh_status launch_infer(fh_encoder enc, const fh::infer::FusedArgs &a, cudaStream_t s) {
     using Lo = fh::infer::FusedLayout<K0>;
-    auto kern = fh::infer::infer_fused_kernel<F, T, K0>;
-    cudaLaunchConfig_t cfg = {};
-    cudaLaunchAttribute attr[1];
-    attr[0].id = cudaLaunchAttributeClusterDimension;
-    attr[0].val.clusterDim.x = 1;   // set below
-    attr[0].val.clusterDim.y = 1;
-    attr[0].val.clusterDim.z = 1;
-    cfg.blockDim = dim3(fh::infer::Threads<F>::value);
-    cfg.dynamicSmemBytes = Lo::SMEM;
-    cfg.stream = s;
-    cfg.attrs = attr;
-    cfg.numAttrs = 1;
-    // Set up once per encoder: the number of resident clusters for each
-    // cluster size C in {8, 4, 2, 1}.
-    int *max_clusters = enc->infer_clusters[K0 / 16 - 1];
-    if (max_clusters[0] == 0) {
-        fh_status st = cuda_check(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)Lo::SMEM),
+    constexpr int Gbig = fh::infer::Groups<F>::value;
+    auto k1 = fh::infer::infer_fused_kernel<F, T, K0, 1>;      // short tiles: one gather group
+    auto kG = fh::infer::infer_fused_kernel<F, T, K0, Gbig>;   // full tiles
+    if (!enc->infer_ready[K0 / 16 - 1]) {
+        fh_status st = cuda_check(cudaFuncSetAttribute(k1, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)Lo::SMEM),
                                   "cudaFuncSetAttribute(infer_fused)");
+        if (st == FH_OK)
+            st = cuda_check(cudaFuncSetAttribute(kG, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)Lo::SMEM),
+                            "cudaFuncSetAttribute(infer_fused)");
         if (st != FH_OK) return st;
-        for (int k = 0; k < 4; k++) {
-            const int c = 8 >> k;
-            attr[0].val.clusterDim.x = (unsigned)c;
-            cfg.gridDim = dim3((unsigned)(c * enc->n_sm));
-            int o = 0;
-            if (cudaOccupancyMaxActiveClusters(&o, kern, &cfg) != cudaSuccess) { cudaGetLastError(); o = 0; }
-            max_clusters[k] = o > 0 ? o : -1;
-        }
-        if (max_clusters[3] <= 0) return fail(FH_E_CUDA, "infer_fused_kernel: does not fit the device");
+        enc->infer_ready[K0 / 16 - 1] = true;
     }
-    // Each SM issues about one L2 request per cycle, so the gathers of a
-    // 128-sample tile (8 x 128 L pair requests) are spread over a cluster of
-    // C SMs: the largest C in {8, 4, 2, 1} whose one wave of resident
-    // clusters holds every tile (small batches: 8 SMs per tile; from about
-    // one tile per SM on: C = 1, every CTA gathers and evaluates its own
-    // tiles, CTA-scope hand-offs only).  (64-sample tiles, i.e. twice the SMs
-    // per batch, measured slower: 8.98 -> 10.3 us at 1024 samples.)
-    const int64_t tiles = (a.N + fh::mlp::TILE - 1) / fh::mlp::TILE;
-    int k = 3;
-    for (int q = 0; q < 3; q++)
-        if (max_clusters[q] > 0 && tiles <= max_clusters[q]) { k = q; break; }
-    const int cs = 8 >> k;
-    attr[0].val.clusterDim.x = (unsigned)cs;
-    const int64_t ncl = tiles < max_clusters[k] ? tiles : max_clusters[k];
-    cfg.gridDim = dim3((unsigned)(ncl * cs));
-    fh_status st = cuda_check(cudaLaunchKernelEx(&cfg, kern, enc->params, a), "infer_fused_kernel launch");
+    // Tiles of R samples, one CTA per SM: the smallest power-of-two R in
+    // [8, 128] that keeps every tile in one wave (each SM issues about one L2
+    // request per cycle, so a small batch is spread over as many SMs as it
+    // can use); large batches: R = 128 and every CTA loops over its tiles.
+    // (R = 8 vs 16 vs 32 at 1024 samples: 8.25 / 8.88 / 10.3 us.)
+    fh::infer::FusedArgs b = a;
+    b.rows = fh::mlp::TILE;
+    while (b.rows > 8 && (a.N + b.rows / 2 - 1) / (b.rows / 2) <= enc->n_sm) b.rows /= 2;
+    const int64_t tiles = (a.N + b.rows - 1) / b.rows;
+    const unsigned grid = (unsigned)(tiles < enc->n_sm ? tiles : enc->n_sm);
+    if (b.rows < fh::mlp::TILE)
+        k1<<<grid, fh::infer::Threads<1>::value, Lo::SMEM, s>>>(enc->params, b);
+    else
+        kG<<<grid, fh::infer::Threads<Gbig>::value, Lo::SMEM, s>>>(enc->params, b);
     fh::count_launch();
-    return st;
+    return cuda_check(cudaGetLastError(), "infer_fused_kernel launch");
 }
 
 template <int F, typename T>
@@ -740,7 +721,8 @@ fh_status fh_infer(fh_encoder enc, const fh_mlp_desc *m, const void *table, cons
         return fail(FH_E_ARG, "fh_infer: NULL or misaligned pointer");
     if (!enc->flag) return fail(FH_E_STATE, "fh_infer: encoder was built without a CUDA device");
     const fh::infer::FusedArgs a{reinterpret_cast<const float4 *>(coords), table,
-                                 reinterpret_cast<const __nv_bfloat16 *>(mlp_shadow), mlp_master, y, N, enc->flag};
+                                 reinterpret_cast<const __nv_bfloat16 *>(mlp_shadow), mlp_master, y, N, enc->flag,
+                                 fh::mlp::TILE};
     cudaStream_t s = reinterpret_cast<cudaStream_t>(stream);
     return enc->table_dtype == FH_F32 ? dispatch_infer<float>(enc, m->n_in, a, s)
                                       : dispatch_infer<__half>(enc, m->n_in, a, s);

@@ -245,6 +245,17 @@ def test_infer_cfg3_full_size():
     check_infer(cfg, tr, W.draw_coords(g, N), g.random(N, dtype=np.float32), N)
 
 
+def test_infer_cfg4_shape_many_tiles():
+    """fh_infer with the cfg4 encoder (F = 4 fp16, K0 = 64: the two-group
+    full-tile kernel) at 2^17 samples -- every CTA loops over several tiles
+    and all four X buffers rotate -- same bars."""
+    cfg, N = W.CFG4, 1 << 17
+    g = W.rng(56)
+    enc = fh.Encoder(cfg.levels, cfg.F, cfg.table_dtype, cfg.cap)
+    tr = fh.Trainer(enc, W.draw_table(g, enc.entries, cfg.F, "f32"), W.draw_mlp(g, W.MLP4), N)
+    check_infer(cfg, tr, W.draw_coords(g, N), g.random(N, dtype=np.float32), N)
+
+
 def check_infer(cfg, tr, coords, target, N):
     c, t = torch.from_numpy(coords).cuda(), torch.from_numpy(target).cuda()
     loss = tr.fwd_bwd(c, t, N).item()
