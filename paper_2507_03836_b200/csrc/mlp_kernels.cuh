@@ -134,7 +134,7 @@ __global__ void __launch_bounds__(256, 1) mlp_train_kernel(const TrainArgs a) {
     extern __shared__ __align__(1024) uint8_t smem[];
     uint8_t *sW1 = smem;
     uint8_t *sW2 = sW1 + Lo::BYTES_W1;
-    __shared__ uint64_t bar[2];
+    __shared__ uint64_t bar[2], xbar[2];
     __shared__ uint32_t tbase;
     __shared__ float b1[H], b2[H], w3[H];
     __shared__ float s_db3[8], s_loss[8];
@@ -170,11 +170,34 @@ __global__ void __launch_bounds__(256, 1) mlp_train_kernel(const TrainArgs a) {
     const float b3 = a.wmaster[off_b3(K0)];
 
     if (warp == 0) tc::tmem_alloc(&tbase, Lo::TMEM_COLS);
-    if (tid == 0) { tc::mbar_init(&bar[0], 1); tc::mbar_init(&bar[1], 1); tc::fence_mbar_init(); }
+    if (tid == 0) {
+        for (int q = 0; q < 2; q++) { tc::mbar_init(&bar[q], 1); tc::mbar_init(&xbar[q], 1); }
+        tc::fence_mbar_init();
+    }
     tc::fence_smem_to_async();
     tc::fence_before_sync();
     __syncthreads();
     tc::fence_after_sync();
+    // X tiles arrive by ONE bulk async copy each (a tile's rows are one
+    // contiguous block of x), issued a tile ahead into the slot's h2 tile --
+    // free from the completion of MMA3/6 (its last reader) to the next
+    // epilogue 2 -- and unpacked into the core-matrix layout at the tile's
+    // start: the HBM latency of X (~1.5 us per tile when each thread loaded
+    // its own row) overlaps the previous tile's epilogues.
+    uint64_t *xb = &xbar[slot];
+    uint32_t xphase = 0;
+    auto issue_x = [&](int64_t tl) {
+        if (t != 0 || tl >= n_tiles) return;
+        const int64_t rows = a.N - tl * TILE < TILE ? a.N - tl * TILE : TILE;
+        const uint32_t bytes = (uint32_t)(rows * K0 * 2);
+        asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
+        asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;" ::"r"(tc::smem_u32(xb)), "r"(bytes)
+                     : "memory");
+        asm volatile("cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1], %2, [%3];"
+                     ::"r"(tc::smem_u32(sH2)), "l"(a.x + tl * TILE * K0), "r"(bytes), "r"(tc::smem_u32(xb))
+                     : "memory");
+    };
+    issue_x(2 * (int64_t)blockIdx.x + slot);
     const uint32_t tm = tbase + (uint32_t)slot * 256u;
     const uint32_t lane_off = (uint32_t)((warp & 3) * 32) << 16;
     uint64_t *mbar = &bar[slot];
@@ -197,14 +220,18 @@ __global__ void __launch_bounds__(256, 1) mlp_train_kernel(const TrainArgs a) {
     for (int64_t tile = 2 * (int64_t)blockIdx.x + slot; tile < n_tiles; tile += 2 * (int64_t)gridDim.x, my_tiles++) {
         const int64_t row = tile * TILE + t;
         const bool valid = row < a.N;
-        // ---- stage X row (bf16) into [H1 | X | 1] columns H .. H+K0
+        // ---- X row (bf16, landed in the h2 tile by the bulk copy) -> [H1 | X | 1]
+        // columns H .. H+K0 (16-byte chunks read in a per-row rotated order:
+        // rows are K0 * 2 bytes apart, so the same chunk of 8 rows would share banks)
+        tc::mbar_wait(xb, xphase); xphase ^= 1;
         {
-            const uint4 *src = reinterpret_cast<const uint4 *>(a.x + row * K0);
-            uint4 xv[K0 / 8];
+            const uint4 *src = reinterpret_cast<const uint4 *>(sH2) + t * (K0 / 8);
 #pragma unroll
-            for (int q = 0; q < K0 / 8; q++) xv[q] = valid ? __ldg(src + q) : make_uint4(0u, 0u, 0u, 0u);
-#pragma unroll
-            for (int q = 0; q < K0 / 8; q++) st16(sHX, tc::core_off(t, H + 8 * q, Lo::SBO_HX), xv[q]);
+            for (int q0 = 0; q0 < K0 / 8; q0++) {
+                const int q = (q0 + t) % (K0 / 8);
+                const uint4 v = valid ? src[q] : make_uint4(0u, 0u, 0u, 0u);
+                st16(sHX, tc::core_off(t, H + 8 * q, Lo::SBO_HX), v);
+            }
         }
         const float tgt = valid ? __ldg(a.target + row) : 0.f;
         tc::fence_smem_to_async();
@@ -322,6 +349,7 @@ __global__ void __launch_bounds__(256, 1) mlp_train_kernel(const TrainArgs a) {
             tc::commit(mbar);
         }
         tc::mbar_wait(mbar, phase); phase ^= 1;
+        issue_x(tile + 2 * (int64_t)gridDim.x);   // the h2 tile is free: prefetch the next X
         tc::fence_after_sync();
         // ---- epilogue 3: dZ1 = bf16(dH1 * mask1), mask1 = (h1 > 0) from the H1 tile
 #pragma unroll
@@ -360,16 +388,35 @@ __global__ void __launch_bounds__(256, 1) mlp_train_kernel(const TrainArgs a) {
         }
         tc::mbar_wait(mbar, phase); phase ^= 1;
         tc::fence_after_sync();
-        // ---- epilogue 4: dX row -> global (fp32)
+        // ---- epilogue 4: dX (fp32) -> shared staging -> coalesced global stores.
+        // The [dZ2 | dZ1] tile is free (MMA4/5 have completed) and holds the
+        // 128 x K0 fp32 tile exactly (K0 <= 64); 16-byte chunk q of row t sits
+        // at chunk q ^ (t & m) of its row (conflict-free writes), then the
+        // slot's 128 threads store the tile -- ONE contiguous block of dX -- in
+        // consecutive 16-byte chunks (each warp store 512 contiguous bytes;
+        // per-row stores left half of every sector empty and stalled on
+        // lg_throttle).
+        {
+            constexpr int CH = K0 / 4;                            // 16-byte chunks per row
+            constexpr int SW = (CH % 8 == 0) ? 7 : 3;             // swizzle mask within aligned chunk groups
+            float4 *stg = reinterpret_cast<float4 *>(sDZ);
 #pragma unroll
-        for (int c = 0; c < K0; c += 16) {
-            float v[16];
-            tc::tmem_ld16(tm + lane_off + Lo::T_ACC + c, v);
-            tc::tmem_wait_ld();
-            if (valid) {
-                float4 *dst = reinterpret_cast<float4 *>(a.dx + row * K0 + c);
+            for (int c = 0; c < K0; c += 16) {
+                float v[16];
+                tc::tmem_ld16(tm + lane_off + Lo::T_ACC + c, v);
+                tc::tmem_wait_ld();
 #pragma unroll
-                for (int j = 0; j < 16; j += 4) dst[j / 4] = make_float4(v[j], v[j + 1], v[j + 2], v[j + 3]);
+                for (int j = 0; j < 16; j += 4)
+                    stg[t * CH + (((c + j) / 4) ^ (t & SW))] = make_float4(v[j], v[j + 1], v[j + 2], v[j + 3]);
+            }
+            tc::fence_before_sync();
+            slot_sync(slot);
+            const int64_t rows_left = a.N - tile * TILE;          // valid rows of this tile
+            float4 *dst = reinterpret_cast<float4 *>(a.dx) + tile * TILE * CH;
+#pragma unroll 4
+            for (int k = t; k < TILE * CH; k += TILE) {
+                const int r = k / CH, q = k - r * CH;
+                if (r < rows_left) dst[k] = stg[r * CH + (q ^ (r & SW))];
             }
         }
         tc::fence_before_sync();
