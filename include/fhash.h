@@ -423,9 +423,14 @@ void      fh_trainer_destroy(fh_trainer tr);
  * exactly the forward numerics of the train step (R13).
  * table: the encoder's table dtype (fp16 shadow or fp32, 32-byte aligned);
  * mlp_shadow bf16 (16-byte aligned) and mlp_master fp32 in the flat MLP
- * layout; y [N] f32 (device).  No workspace (fh_infer_workspace_size
- * returns 0; workspace may be NULL).  F-Hash encoders only.  Errors as
- * fh_train_fwd_bwd. */
+ * layout; y [N] f32 (device).  Workspace: none for the fused form
+ * (fh_infer_workspace_size returns 0; workspace may be NULL); a LARGE batch
+ * (>= 8 tiles per SM) over tables bigger than the forward's L2 budget is
+ * faster in two launches -- fh_encode_fwd's L2-sized level groups into
+ * max_batch * n_in bf16 of workspace, then the kernel's MLP-only mode --
+ * and fh_infer_workspace_size(enc, mlp, max_batch) returns that size.
+ * F-Hash encoders only.  Errors as fh_train_fwd_bwd (FH_E_ARG when a
+ * two-launch batch gets too little workspace). */
 size_t    fh_infer_workspace_size(fh_encoder enc, const fh_mlp_desc *mlp, int64_t max_batch);
 fh_status fh_infer(fh_encoder enc, const fh_mlp_desc *mlp, const void *table, const void *mlp_shadow,
                    const float *mlp_master, const float *coords, int64_t N, float *y, void *workspace,

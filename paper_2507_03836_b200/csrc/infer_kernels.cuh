@@ -67,6 +67,9 @@ struct FusedArgs {
     int64_t N;
     int *flag;                     // encoder status word (out-of-domain coordinates)
     int rows;                      // samples per tile R (8 .. 128, a power of two)
+    const __nv_bfloat16 *xin;      // NULL: gather; else the encoding [N][K0] bf16 already in global memory
+                                   // (large batches over HBM-sized tables: fh_encode_fwd's L2-sized level
+                                   // groups first, then this kernel as the MLP forward only)
 };
 
 // bf16 of the F blended features into the X tile at p.
@@ -133,6 +136,15 @@ __global__ void __launch_bounds__(Threads<G>::value, 1) infer_fused_kernel(const
             if (m > 0) tc::mbar_wait(&xfree[b], (uint32_t)((m - 1) & 1));
             const int64_t tile = (int64_t)blockIdx.x + (int64_t)gridDim.x * u;
             uint8_t *sX = sX0 + b * Lo::BYTES_X;
+            if (a.xin) {   // copy the tile's encoding rows (coalesced 16-byte chunks) into the X tile
+                constexpr int CH = K0 / 8;
+                const uint4 *src = reinterpret_cast<const uint4 *>(a.xin + tile * R * K0);
+                for (int k = gt; k < R * CH; k += 32 * kGatherWarps) {
+                    const int r = k / CH, q = k - r * CH;
+                    const uint4 v = tile * R + r < a.N ? __ldg(src + k) : make_uint4(0u, 0u, 0u, 0u);
+                    mlp::st16(sX, tc::core_off(r, 8 * q, Lo::SBO_X), v);
+                }
+            } else
 #pragma unroll 1
             for (int i = gt; i < items; i += 32 * kGatherWarps) {
                 const int s = i / L, l = i - s * L;

@@ -637,9 +637,18 @@ fh_status fh_trainer_status(fh_trainer tr, fh_stream stream) {
 
 int64_t fh_trainer_step_count(fh_trainer tr) { return tr ? tr->step : -1; }
 
+// Large batches over tables beyond the forward's L2 budget (the encode
+// forward then runs as several L2-sized level groups, which one fused pass
+// cannot: measured cfg5 shape 21.9 vs 12.6 ms at 2^24) take two launches:
+// fh_encode_fwd into the workspace, then the kernel's MLP-only mode.
+static bool infer_two_phase(fh_encoder enc, int64_t N) {
+    const double table_bytes = (double)enc->entries * enc->F * fh::dtype_size(enc->table_dtype);
+    return enc->fwd_limit > 0.0 && table_bytes > enc->fwd_limit && N >= (int64_t)enc->n_sm * fh::mlp::TILE * 8;
+}
+
 size_t fh_infer_workspace_size(fh_encoder enc, const fh_mlp_desc *m, int64_t max_batch) {
-    (void)enc; (void)m; (void)max_batch;
-    return 0;   // the fused kernel keeps the encoding on chip
+    if (!enc || !m || max_batch < 0 || !infer_two_phase(enc, max_batch)) return 0;   // fused: on chip
+    return align_up((size_t)max_batch * (size_t)m->n_in * 2, 256);
 }
 
 }  // extern "C"
@@ -709,7 +718,6 @@ extern "C" {
 fh_status fh_infer(fh_encoder enc, const fh_mlp_desc *m, const void *table, const void *mlp_shadow,
                    const float *mlp_master, const float *coords, int64_t N, float *y, void *workspace,
                    size_t workspace_bytes, fh_stream stream) {
-    (void)workspace; (void)workspace_bytes;
     g_err[0] = 0;
     fh_status st = check_mlp(enc, m);
     if (st != FH_OK) return st;
@@ -720,9 +728,15 @@ fh_status fh_infer(fh_encoder enc, const fh_mlp_desc *m, const void *table, cons
         !aligned(mlp_shadow, 16) || !mlp_master || !y)
         return fail(FH_E_ARG, "fh_infer: NULL or misaligned pointer");
     if (!enc->flag) return fail(FH_E_STATE, "fh_infer: encoder was built without a CUDA device");
-    const fh::infer::FusedArgs a{reinterpret_cast<const float4 *>(coords), table,
-                                 reinterpret_cast<const __nv_bfloat16 *>(mlp_shadow), mlp_master, y, N, enc->flag,
-                                 fh::mlp::TILE};
+    fh::infer::FusedArgs a{reinterpret_cast<const float4 *>(coords), table,
+                           reinterpret_cast<const __nv_bfloat16 *>(mlp_shadow), mlp_master, y, N, enc->flag,
+                           fh::mlp::TILE, nullptr};
+    if (infer_two_phase(enc, N)) {   // see fh_infer_workspace_size
+        if (!workspace || !aligned(workspace, 16) || workspace_bytes < (size_t)N * m->n_in * 2)
+            return fail(FH_E_ARG, "fh_infer: this batch needs fh_infer_workspace_size bytes of workspace");
+        if ((st = fh_encode_fwd(enc, coords, N, table, workspace, FH_BF16, stream)) != FH_OK) return st;
+        a.xin = reinterpret_cast<const __nv_bfloat16 *>(workspace);
+    }
     cudaStream_t s = reinterpret_cast<cudaStream_t>(stream);
     return enc->table_dtype == FH_F32 ? dispatch_infer<float>(enc, m->n_in, a, s)
                                       : dispatch_infer<__half>(enc, m->n_in, a, s);

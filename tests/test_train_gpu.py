@@ -256,14 +256,30 @@ def test_infer_cfg4_shape_many_tiles():
     check_infer(cfg, tr, W.draw_coords(g, N), g.random(N, dtype=np.float32), N)
 
 
-def check_infer(cfg, tr, coords, target, N):
+def test_infer_two_phase_large_batch_hbm_tables():
+    """A large batch over tables beyond the forward's L2 budget (cfg4: 305
+    MiB fp16) takes fh_encode_fwd's L2-sized level groups into the workspace
+    and then the fused kernel's MLP-only mode (fh_infer_workspace_size > 0):
+    same bars against Oracle-T."""
+    import ctypes
+    cfg, N = W.CFG4, 1 << 18
+    g = W.rng(57)
+    enc = fh.Encoder(cfg.levels, cfg.F, cfg.table_dtype, cfg.cap)
+    tr = fh.Trainer(enc, W.draw_table(g, enc.entries, cfg.F, "f32"), W.draw_mlp(g, W.MLP4), N)
+    L = fh._train_lib()
+    assert int(L.fh_infer_workspace_size(enc.handle, ctypes.byref(tr.desc), N)) >= N * 64 * 2
+    check_infer(cfg, tr, W.draw_coords(g, N), g.random(N, dtype=np.float32), N, one_launch=False)
+
+
+def check_infer(cfg, tr, coords, target, N, one_launch=True):
     c, t = torch.from_numpy(coords).cuda(), torch.from_numpy(target).cuda()
     loss = tr.fwd_bwd(c, t, N).item()
     x0 = tr.enc_out(N).float().cpu().numpy().astype(np.float64)
     torch.cuda.synchronize()
     l0 = fh.kernel_launches()
     y = tr.infer(c).cpu().numpy().astype(np.float64)
-    assert fh.kernel_launches() - l0 == 1          # NEXT-1 fused: encode + MLP in one launch
+    if one_launch:
+        assert fh.kernel_launches() - l0 == 1      # NEXT-1 fused: encode + MLP in one launch
     assert tr.status() == fh.FH_OK
     master = tr.mlp_master.cpu().numpy().astype(np.float64)
     K0, o, layers = cfg.L * cfg.F, 0, []
