@@ -463,18 +463,24 @@ static fh_status dp_step(fh_trainer tr, const float *coords, const float *target
         t += d.te[i] - d.tb[i];
     }
     if ((st = apply_ranges_impl(tr, (int)b.size(), b.data(), e.data(), gp.data(), s)) != FH_OK) return st;
-    // all-gather the fp16 shadow chunks (in place), on the caller's stream
+    // all-gather the fp16 shadow chunks (in place) -- on the communication
+    // stream too, so every NCCL call of the communicator is issued to ONE
+    // stream in one order; the caller's stream waits for it
+    if ((st = cuda_check(cudaEventRecord(d.ev_step, s), "dp: record adam")) != FH_OK) return st;
+    if ((st = cuda_check(cudaStreamWaitEvent(d.cs, d.ev_step, 0), "dp: wait adam")) != FH_OK) return st;
     __half *shadow = reinterpret_cast<__half *>(tr->b.table_shadow);
     A.group_start();
     for (auto &m : d.mains) {
         const int64_t c = m.m / W;
         if ((st = nccl::check(A.all_gather(shadow + m.a + d.rank * c, shadow + m.a, (size_t)c, nccl::kFloat16, d.comm,
-                                           s), "ncclAllGather")) != FH_OK) {
+                                           d.cs), "ncclAllGather")) != FH_OK) {
             A.group_end();
             return st;
         }
     }
-    return nccl::check(A.group_end(), "ncclGroupEnd");
+    if ((st = nccl::check(A.group_end(), "ncclGroupEnd")) != FH_OK) return st;
+    if ((st = cuda_check(cudaEventRecord(d.ev_red, d.cs), "dp: record gathered")) != FH_OK) return st;
+    return cuda_check(cudaStreamWaitEvent(s, d.ev_red, 0), "dp: wait gathered");
 }
 
 static fh_status apply_impl(fh_trainer tr, int64_t begin, int64_t end, float *tgrad, cudaStream_t s) {
