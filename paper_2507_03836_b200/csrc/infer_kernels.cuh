@@ -87,6 +87,9 @@ __device__ __forceinline__ void st_x(uint8_t *p, const float (&v)[F]) {
     }
 }
 
+// Barrier over the 128 MLP threads (named barrier 1).
+__device__ __forceinline__ void mlp_sync() { asm volatile("bar.sync 1, 128;" ::: "memory"); }
+
 __device__ __forceinline__ void mbar_arrive(uint64_t *mbar) {
     asm volatile("mbarrier.arrive.shared::cta.b64 _, [%0];" ::"r"(tc::smem_u32(mbar)) : "memory");
 }
@@ -103,7 +106,7 @@ __global__ void __launch_bounds__(Threads<G>::value, 1) infer_fused_kernel(const
     __shared__ LevelSmem slv;
     __shared__ uint64_t full[NB], xfree[NB], mma_bar;
     __shared__ uint32_t tbase;
-    __shared__ float b1[H], b2[H], w3[H];
+    __shared__ __align__(16) float b1[H], b2[H], w3[H];   // read as float4
 
     const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
     if (tid == 0) {
@@ -190,7 +193,7 @@ __global__ void __launch_bounds__(Threads<G>::value, 1) infer_fused_kernel(const
         }
         tc::fence_smem_to_async();
         tc::fence_before_sync();
-        mlp::slot_sync(0);                                // named barrier 1 over the 128 MLP threads
+        mlp_sync();                                       // named barrier 1 over the 128 MLP threads
         tc::fence_after_sync();
         const uint32_t tm = tbase;
         const int row = tid;                              // TMEM lane = sample row
@@ -231,7 +234,7 @@ __global__ void __launch_bounds__(Threads<G>::value, 1) infer_fused_kernel(const
             }
             tc::fence_smem_to_async();
             tc::fence_before_sync();
-            mlp::slot_sync(0);
+            mlp_sync();
             tc::fence_after_sync();
             // ---- MMA2: Z2 = H1 . W2^T
             if (tid == 0) {
@@ -257,7 +260,7 @@ __global__ void __launch_bounds__(Threads<G>::value, 1) infer_fused_kernel(const
             const int64_t n = ((int64_t)blockIdx.x + (int64_t)gridDim.x * u) * R + row;
             if (row < R && n < a.N) a.y[n] = ((ya[0] + ya[1]) + (ya[2] + ya[3])) + b3;
             tc::fence_before_sync();
-            mlp::slot_sync(0);                            // TMEM and H reused by the next tile
+            mlp_sync();                            // TMEM and H reused by the next tile
             tc::fence_after_sync();
         }
     }

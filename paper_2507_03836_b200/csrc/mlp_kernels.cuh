@@ -8,7 +8,8 @@
 // MSE over the global batch), R13 (bf16 operand rounding points), R15
 // (ReLU hidden layers, identity output, biases) -- DESIGN.md §3.
 //
-// One persistent CTA per SM, 128 threads; each 128-sample tile is one
+// One persistent CTA per SM, 512 threads (two tile slots of 8 warps); each
+// 128-sample tile is one
 // M = 128 tcgen05 GEMM chain with the accumulators in TMEM:
 //   MMA1  Z1  = X  . W1^T          (N = 64, K = K0)
 //   MMA2  Z2  = H1 . W2^T          (N = 64, K = 64)
@@ -18,10 +19,12 @@
 // MMA5 accumulates dW2 (top-left), dW1 (bottom, X columns) and, through the
 // constant-one column, db2 / db1, in TMEM across all tiles of the CTA; the
 // transposed operands are the SAME shared-memory tiles read through
-// MN-major descriptors.  Thread t owns sample row t of every tile (TMEM
-// lane t), so every epilogue (bias, ReLU, bf16 rounding, the 64 -> 1 output
-// layer, the loss) runs in registers of one thread.
+// MN-major descriptors.  Two threads own sample row t of every tile (TMEM
+// lane t), one per half of the columns, so every epilogue (bias, ReLU, bf16
+// rounding, the 64 -> 1 output layer, the loss) runs in registers of those
+// two threads; the output layer's two partial sums meet in shared memory.
 #pragma once
+#include <cuda.h>   // CUtensorMap
 #include <cuda_bf16.h>
 #include <stdint.h>
 
@@ -102,51 +105,73 @@ __device__ __forceinline__ void st16(uint8_t *base, uint32_t off, uint4 v) {
     *reinterpret_cast<uint4 *>(base + off) = v;
 }
 
-// Barrier over the 128 threads of one slot (named barrier 1 + slot).
+// Threads of the train kernel: two tile slots x 8 warps.  Warp ws (0..7) of
+// a slot reads TMEM lane quarter ws & 3 (sample rows 32 (ws & 3) .. +31)
+// and owns column half ws >> 2 of every epilogue, so each sample row's
+// epilogue work is split over two threads.  (Round 1 / early round 2: 4
+// warps per slot, one thread per row: the per-row epilogues were most of
+// the per-tile chain -- 4.0 of 5.8 us at cfg4.)
+constexpr int SLOT_THREADS = 256;
+constexpr int TRAIN_THREADS = 2 * SLOT_THREADS;
+
+// Barrier over the 256 threads of one slot (named barrier 1 + slot).
 __device__ __forceinline__ void slot_sync(int slot) {
-    asm volatile("bar.sync %0, 128;" ::"r"(1 + slot) : "memory");
+    asm volatile("bar.sync %0, 256;" ::"r"(1 + slot) : "memory");
 }
 
-// Sum v[0..63] over the 32 lanes of a warp by recursive halving: 62
-// shuffles; afterwards lane holds the totals of columns col, col + 1 with
-// col = 32 b4 + 16 b3 + 8 b2 + 4 b1 + 2 b0 (b_k = bit k of the lane).
-__device__ __forceinline__ void warp_reduce64(float (&v)[64], int lane) {
+// TMEM -> registers, N consecutive columns (N = 8, 16, 24 or 32), one wait.
+template <int N>
+__device__ __forceinline__ void tmem_ld_cols(uint32_t taddr, float (&v)[N]) {
+    static_assert(N == 8 || N == 16 || N == 24 || N == 32, "column count");
+    if constexpr (N == 32) {
+        tc::tmem_ld32(taddr, v);
+    } else if constexpr (N == 16) {
+        tc::tmem_ld16(taddr, v);
+    } else if constexpr (N == 8) {
+        tc::tmem_ld8(taddr, v);
+    } else {
+        float a[16];
+        tc::tmem_ld16(taddr, a);
+        tc::tmem_ld8(taddr + 16, v + 16);
 #pragma unroll
-    for (int st = 0; st < 5; st++) {
-        const int off = 16 >> st, half = 32 >> st;
-        const bool upper = (lane & off) != 0;
-#pragma unroll
-        for (int i = 0; i < half; i++) {
-            const float send = upper ? v[i] : v[i + half];
-            const float keep = upper ? v[i + half] : v[i];
-            v[i] = keep + __shfl_xor_sync(0xffffffffu, send, off);
-        }
+        for (int i = 0; i < 16; i++) v[i] = a[i];
     }
-}
-__device__ __forceinline__ int reduce64_col(int lane) {
-    return 32 * ((lane >> 4) & 1) + 16 * ((lane >> 3) & 1) + 8 * ((lane >> 2) & 1) + 4 * ((lane >> 1) & 1) +
-           2 * (lane & 1);
+    tc::tmem_wait_ld();
 }
 
 template <int K0>
-__global__ void __launch_bounds__(256, 1) mlp_train_kernel(const TrainArgs a) {
+// tm_dx: 2-D tensor map of dX ([max_batch][K0] fp32), box 128 rows x 16
+// columns, 64-byte swizzle (created once per trainer).
+__global__ void __launch_bounds__(TRAIN_THREADS, 1) mlp_train_kernel(const TrainArgs a,
+                                                                     const __grid_constant__ CUtensorMap tm_dx) {
     using Lo = Layout<K0>;
+    constexpr int HC = H / 2;            // hidden columns per thread
+    constexpr int XC = K0 / 2;           // X / dX columns per thread
+    constexpr int XQ = K0 / 8;           // 16-byte chunks of an X row
     extern __shared__ __align__(1024) uint8_t smem[];
     uint8_t *sW1 = smem;
     uint8_t *sW2 = sW1 + Lo::BYTES_W1;
     __shared__ uint64_t bar[2], xbar[2];
     __shared__ uint32_t tbase;
-    __shared__ float b1[H], b2[H], w3[H];
-    __shared__ float s_db3[8], s_loss[8];
+    __shared__ __align__(16) float b1[H];   // read as float4
+    __shared__ __align__(16) float b2[H];
+    __shared__ __align__(16) float w3[H];
+    __shared__ float s_y[2][2][TILE];    // [slot][column half][row]: partial output-layer sums
+    __shared__ float s_db3[16], s_loss[16];
 
     const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
-    const int slot = warp >> 2;          // 0: warps 0-3, 1: warps 4-7
-    const int t = tid & 127;             // sample row within the slot's tile = TMEM lane
+    const int slot = warp >> 3;          // 0: warps 0-7, 1: warps 8-15
+    const int ws = warp & 7;
+    const int hf = ws >> 2;              // column half
+    const int t = ((ws & 3) << 5) | lane;   // sample row within the slot's tile = TMEM lane
+    const int ts = tid & (SLOT_THREADS - 1);
     uint8_t *sHX = smem + Lo::BYTES_W1 + Lo::BYTES_W2 + slot * Lo::BYTES_SLOT;
     uint8_t *sDZ = sHX + Lo::BYTES_HX;
     uint8_t *sH2 = sDZ + Lo::BYTES_DZ;
     uint8_t *sDY = sH2 + Lo::BYTES_H2;
     const int64_t n_tiles = (a.N + TILE - 1) / TILE;
+    // the dX staging relies on the TMA swizzle's address pattern (512-byte atoms)
+    if (tid == 0 && (tc::smem_u32(smem) & 1023u) != 0u) __trap();
 
     // ---- weights -> shared memory (bf16 shadow), once per CTA
     for (int i = tid; i < H * K0; i += blockDim.x) {
@@ -159,8 +184,7 @@ __global__ void __launch_bounds__(256, 1) mlp_train_kernel(const TrainArgs a) {
     }
     {   // constant columns [H + K0, H + K0 + 16) of each slot's HX tile: 1, 0, ..., 0
         const uint4 ones = make_uint4(pack_bf16(1.f, 0.f), 0u, 0u, 0u), zero = make_uint4(0u, 0u, 0u, 0u);
-        st16(sHX, tc::core_off(t, H + K0, Lo::SBO_HX), ones);
-        st16(sHX, tc::core_off(t, H + K0 + 8, Lo::SBO_HX), zero);
+        st16(sHX, tc::core_off(t, H + K0 + 8 * hf, Lo::SBO_HX), hf ? zero : ones);
     }
     if (tid < H) {
         b1[tid] = a.wmaster[off_b1(K0) + tid];
@@ -182,12 +206,11 @@ __global__ void __launch_bounds__(256, 1) mlp_train_kernel(const TrainArgs a) {
     // contiguous block of x), issued a tile ahead into the slot's h2 tile --
     // free from the completion of MMA3/6 (its last reader) to the next
     // epilogue 2 -- and unpacked into the core-matrix layout at the tile's
-    // start: the HBM latency of X (~1.5 us per tile when each thread loaded
-    // its own row) overlaps the previous tile's epilogues.
+    // start: the HBM latency of X overlaps the previous tile's epilogues.
     uint64_t *xb = &xbar[slot];
     uint32_t xphase = 0;
     auto issue_x = [&](int64_t tl) {
-        if (t != 0 || tl >= n_tiles) return;
+        if (ts != 0 || tl >= n_tiles) return;
         const int64_t rows = a.N - tl * TILE < TILE ? a.N - tl * TILE : TILE;
         const uint32_t bytes = (uint32_t)(rows * K0 * 2);
         asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
@@ -199,9 +222,10 @@ __global__ void __launch_bounds__(256, 1) mlp_train_kernel(const TrainArgs a) {
     };
     issue_x(2 * (int64_t)blockIdx.x + slot);
     const uint32_t tm = tbase + (uint32_t)slot * 256u;
-    const uint32_t lane_off = (uint32_t)((warp & 3) * 32) << 16;
+    const uint32_t lane_off = (uint32_t)((ws & 3) * 32) << 16;
     uint64_t *mbar = &bar[slot];
-    const bool issuer = (t == 0);
+    const bool issuer = (ts == 0);
+    const int hc0 = hf * HC;             // this thread's first hidden column
 
     const uint32_t aHX = tc::smem_u32(sHX), aDZ = tc::smem_u32(sDZ);
     const uint32_t aH2 = tc::smem_u32(sH2), aDY = tc::smem_u32(sDY);
@@ -221,14 +245,15 @@ __global__ void __launch_bounds__(256, 1) mlp_train_kernel(const TrainArgs a) {
         const int64_t row = tile * TILE + t;
         const bool valid = row < a.N;
         // ---- X row (bf16, landed in the h2 tile by the bulk copy) -> [H1 | X | 1]
-        // columns H .. H+K0 (16-byte chunks read in a per-row rotated order:
-        // rows are K0 * 2 bytes apart, so the same chunk of 8 rows would share banks)
+        // columns H .. H+K0.  Half hf takes the chunks of its parity; chunk
+        // order rotated by the row (rows are K0 * 2 bytes apart: the same
+        // chunk of 8 rows would share banks).
         tc::mbar_wait(xb, xphase); xphase ^= 1;
         {
-            const uint4 *src = reinterpret_cast<const uint4 *>(sH2) + t * (K0 / 8);
+            const uint4 *src = reinterpret_cast<const uint4 *>(sH2) + t * XQ;
 #pragma unroll
-            for (int q0 = 0; q0 < K0 / 8; q0++) {
-                const int q = (q0 + t) % (K0 / 8);
+            for (int q0 = 0; q0 < XQ / 2; q0++) {
+                const int q = (2 * q0 + hf + t) % XQ;
                 const uint4 v = valid ? src[q] : make_uint4(0u, 0u, 0u, 0u);
                 st16(sHX, tc::core_off(t, H + 8 * q, Lo::SBO_HX), v);
             }
@@ -249,21 +274,19 @@ __global__ void __launch_bounds__(256, 1) mlp_train_kernel(const TrainArgs a) {
         tc::mbar_wait(mbar, phase); phase ^= 1;
         tc::fence_after_sync();
         // ---- epilogue 1: H1 = bf16(relu(Z1 + b1)) (its sign is the ReLU mask later)
+        {
+            float v[HC];
+            tmem_ld_cols<HC>(tm + lane_off + Lo::T_ACC + hc0, v);
 #pragma unroll
-        for (int c = 0; c < H; c += 16) {
-            float v[16];
-            tc::tmem_ld16(tm + lane_off + Lo::T_ACC + c, v);
-            tc::tmem_wait_ld();
-            uint32_t p[8];
-            const float4 *bb = reinterpret_cast<const float4 *>(b1 + c);
-#pragma unroll
-            for (int j = 0; j < 16; j += 4) {
-                const float4 b = bb[j / 4];
-                p[j / 2] = pack_bf16(fmaxf(v[j] + b.x, 0.f), fmaxf(v[j + 1] + b.y, 0.f));
-                p[j / 2 + 1] = pack_bf16(fmaxf(v[j + 2] + b.z, 0.f), fmaxf(v[j + 3] + b.w, 0.f));
+            for (int c = 0; c < HC; c += 8) {
+                const float4 ba = *reinterpret_cast<const float4 *>(b1 + hc0 + c);
+                const float4 bb = *reinterpret_cast<const float4 *>(b1 + hc0 + c + 4);
+                st16(sHX, tc::core_off(t, hc0 + c, Lo::SBO_HX),
+                     make_uint4(pack_bf16(fmaxf(v[c] + ba.x, 0.f), fmaxf(v[c + 1] + ba.y, 0.f)),
+                                pack_bf16(fmaxf(v[c + 2] + ba.z, 0.f), fmaxf(v[c + 3] + ba.w, 0.f)),
+                                pack_bf16(fmaxf(v[c + 4] + bb.x, 0.f), fmaxf(v[c + 5] + bb.y, 0.f)),
+                                pack_bf16(fmaxf(v[c + 6] + bb.z, 0.f), fmaxf(v[c + 7] + bb.w, 0.f))));
             }
-            st16(sHX, tc::core_off(t, c, Lo::SBO_HX), make_uint4(p[0], p[1], p[2], p[3]));
-            st16(sHX, tc::core_off(t, c + 8, Lo::SBO_HX), make_uint4(p[4], p[5], p[6], p[7]));
         }
         tc::fence_smem_to_async();
         tc::fence_before_sync();
@@ -279,57 +302,60 @@ __global__ void __launch_bounds__(256, 1) mlp_train_kernel(const TrainArgs a) {
         }
         tc::mbar_wait(mbar, phase); phase ^= 1;
         tc::fence_after_sync();
-        // ---- epilogue 2: H2 = bf16(relu(Z2 + b2)); y = H2 . w3 + b3; MSE; dZ2
-        // ReLU masks are read back as (h > 0): h = bf16(relu(z)) is > 0 iff z > 0.
-        float ya[4] = {0.f, 0.f, 0.f, 0.f};
+        // ---- epilogue 2: H2 = bf16(relu(Z2 + b2)); y = H2 . w3 + b3 (the two
+        // halves' partial sums meet in shared memory); MSE; dZ2.  ReLU masks
+        // are read as (h > 0): h = bf16(relu(z)) is > 0 iff z > 0.
+        {
+            float v[HC];
+            tmem_ld_cols<HC>(tm + lane_off + Lo::T_ACC + hc0, v);
+            float ya[4] = {0.f, 0.f, 0.f, 0.f};
+            uint32_t hp[HC / 2];
 #pragma unroll
-        for (int c = 0; c < H; c += 16) {
-            float v[16];
-            tc::tmem_ld16(tm + lane_off + Lo::T_ACC + c, v);
-            tc::tmem_wait_ld();
-            uint32_t p[8];
-            const float4 *bb = reinterpret_cast<const float4 *>(b2 + c);
-            const float4 *ww = reinterpret_cast<const float4 *>(w3 + c);
-#pragma unroll
-            for (int j = 0; j < 16; j += 4) {
-                const float4 b = bb[j / 4], w = ww[j / 4];
-                const float h0 = bf16r(fmaxf(v[j] + b.x, 0.f)), h1 = bf16r(fmaxf(v[j + 1] + b.y, 0.f));
-                const float h2_ = bf16r(fmaxf(v[j + 2] + b.z, 0.f)), h3 = bf16r(fmaxf(v[j + 3] + b.w, 0.f));
-                ya[0] = fmaf(h0, w.x, ya[0]);
-                ya[1] = fmaf(h1, w.y, ya[1]);
-                ya[2] = fmaf(h2_, w.z, ya[2]);
-                ya[3] = fmaf(h3, w.w, ya[3]);
-                p[j / 2] = pack_bf16(h0, h1);
-                p[j / 2 + 1] = pack_bf16(h2_, h3);
+            for (int j = 0; j < HC; j += 4) {
+                const float4 b = *reinterpret_cast<const float4 *>(b2 + hc0 + j);
+                const float4 w = *reinterpret_cast<const float4 *>(w3 + hc0 + j);
+                // bf16 rounding by the packing conversion (one F2FP per two
+                // values), unpacked by shifts: the scalar F2F round trip runs
+                // on the MIO pipe and stalled the epilogue
+                hp[j / 2] = pack_bf16(fmaxf(v[j] + b.x, 0.f), fmaxf(v[j + 1] + b.y, 0.f));
+                hp[j / 2 + 1] = pack_bf16(fmaxf(v[j + 2] + b.z, 0.f), fmaxf(v[j + 3] + b.w, 0.f));
+                const float2 h01 = unpack_bf16(hp[j / 2]), h23 = unpack_bf16(hp[j / 2 + 1]);
+                ya[0] = fmaf(h01.x, w.x, ya[0]);
+                ya[1] = fmaf(h01.y, w.y, ya[1]);
+                ya[2] = fmaf(h23.x, w.z, ya[2]);
+                ya[3] = fmaf(h23.y, w.w, ya[3]);
             }
-            st16(sH2, tc::core_off(t, c, 1024), make_uint4(p[0], p[1], p[2], p[3]));
-            st16(sH2, tc::core_off(t, c + 8, 1024), make_uint4(p[4], p[5], p[6], p[7]));
-        }
-        const float y = ((ya[0] + ya[1]) + (ya[2] + ya[3])) + b3;
-        const float diff = valid ? (y - tgt) : 0.f;
-        if (!isfinite(diff)) bad = true;
-        loss_acc = fmaf(diff, diff, loss_acc);
-        const float dy = 2.f * diff * a.inv_n_global;
-        db3_acc += dy;
-        {   // dy as two bf16 (hi + lo: ~16 mantissa bits) for the dw3 GEMM below
-            const float hi = bf16r(dy);
-            st16(sDY, tc::core_off(t, 0, 256), make_uint4(pack_bf16(hi, dy - hi), 0u, 0u, 0u));
-            st16(sDY, tc::core_off(t, 8, 256), make_uint4(0u, 0u, 0u, 0u));
-        }
 #pragma unroll
-        for (int c = 0; c < H; c += 8) {
-            const uint4 u = *reinterpret_cast<const uint4 *>(sH2 + tc::core_off(t, c, 1024));
-            const uint32_t hw[4] = {u.x, u.y, u.z, u.w};
-            const float4 w0 = reinterpret_cast<const float4 *>(w3 + c)[0];
-            const float4 w1 = reinterpret_cast<const float4 *>(w3 + c)[1];
-            const float ww[8] = {w0.x, w0.y, w0.z, w0.w, w1.x, w1.y, w1.z, w1.w};
-            uint32_t p[4];
-#pragma unroll
-            for (int k = 0; k < 4; k++) {
-                const float2 h = unpack_bf16(hw[k]);
-                p[k] = pack_bf16(h.x > 0.f ? dy * ww[2 * k] : 0.f, h.y > 0.f ? dy * ww[2 * k + 1] : 0.f);
+            for (int c = 0; c < HC; c += 8)
+                st16(sH2, tc::core_off(t, hc0 + c, 1024), make_uint4(hp[c / 2], hp[c / 2 + 1], hp[c / 2 + 2], hp[c / 2 + 3]));
+            s_y[slot][hf][t] = (ya[0] + ya[1]) + (ya[2] + ya[3]);
+            // the previous tile's dX stores have read the [dZ2 | dZ1] tile before it is rewritten below
+            if (issuer) asm volatile("cp.async.bulk.wait_group.read 0;" ::: "memory");
+            slot_sync(slot);
+            const float y = (s_y[slot][0][t] + s_y[slot][1][t]) + b3;
+            const float diff = valid ? (y - tgt) : 0.f;
+            const float dy = 2.f * diff * a.inv_n_global;
+            if (hf == 0) {
+                if (!isfinite(diff)) bad = true;
+                loss_acc = fmaf(diff, diff, loss_acc);
+                db3_acc += dy;
+                // dy as two bf16 (hi + lo: ~16 mantissa bits) for the dw3 GEMM below
+                const float hi = bf16r(dy);
+                st16(sDY, tc::core_off(t, 0, 256), make_uint4(pack_bf16(hi, dy - hi), 0u, 0u, 0u));
+            } else {
+                st16(sDY, tc::core_off(t, 8, 256), make_uint4(0u, 0u, 0u, 0u));
             }
-            st16(sDZ, tc::core_off(t, c, Lo::SBO_DZ), make_uint4(p[0], p[1], p[2], p[3]));
+#pragma unroll
+            for (int c = 0; c < HC; c += 8) {
+                uint32_t p[4];
+#pragma unroll
+                for (int k = 0; k < 4; k++) {
+                    const float2 h = unpack_bf16(hp[c / 2 + k]);
+                    const int col = hc0 + c + 2 * k;
+                    p[k] = pack_bf16(h.x > 0.f ? dy * w3[col] : 0.f, h.y > 0.f ? dy * w3[col + 1] : 0.f);
+                }
+                st16(sDZ, tc::core_off(t, hc0 + c, Lo::SBO_DZ), make_uint4(p[0], p[1], p[2], p[3]));
+            }
         }
         tc::fence_smem_to_async();
         tc::fence_before_sync();
@@ -352,22 +378,21 @@ __global__ void __launch_bounds__(256, 1) mlp_train_kernel(const TrainArgs a) {
         issue_x(tile + 2 * (int64_t)gridDim.x);   // the h2 tile is free: prefetch the next X
         tc::fence_after_sync();
         // ---- epilogue 3: dZ1 = bf16(dH1 * mask1), mask1 = (h1 > 0) from the H1 tile
+        {
+            float v[HC];
+            tmem_ld_cols<HC>(tm + lane_off + Lo::T_ACC + hc0, v);
 #pragma unroll
-        for (int c = 0; c < H; c += 16) {
-            float v[16];
-            tc::tmem_ld16(tm + lane_off + Lo::T_ACC + c, v);
-            tc::tmem_wait_ld();
-            const uint4 ha = *reinterpret_cast<const uint4 *>(sHX + tc::core_off(t, c, Lo::SBO_HX));
-            const uint4 hb = *reinterpret_cast<const uint4 *>(sHX + tc::core_off(t, c + 8, Lo::SBO_HX));
-            const uint32_t hw[8] = {ha.x, ha.y, ha.z, ha.w, hb.x, hb.y, hb.z, hb.w};
-            uint32_t p[8];
+            for (int c = 0; c < HC; c += 8) {
+                const uint4 ha = *reinterpret_cast<const uint4 *>(sHX + tc::core_off(t, hc0 + c, Lo::SBO_HX));
+                const uint32_t hw[4] = {ha.x, ha.y, ha.z, ha.w};
+                uint32_t p[4];
 #pragma unroll
-            for (int k = 0; k < 8; k++) {
-                const float2 h = unpack_bf16(hw[k]);
-                p[k] = pack_bf16(h.x > 0.f ? v[2 * k] : 0.f, h.y > 0.f ? v[2 * k + 1] : 0.f);
+                for (int k = 0; k < 4; k++) {
+                    const float2 h = unpack_bf16(hw[k]);
+                    p[k] = pack_bf16(h.x > 0.f ? v[c + 2 * k] : 0.f, h.y > 0.f ? v[c + 2 * k + 1] : 0.f);
+                }
+                st16(sDZ, tc::core_off(t, H + hc0 + c, Lo::SBO_DZ), make_uint4(p[0], p[1], p[2], p[3]));
             }
-            st16(sDZ, tc::core_off(t, H + c, Lo::SBO_DZ), make_uint4(p[0], p[1], p[2], p[3]));
-            st16(sDZ, tc::core_off(t, H + c + 8, Lo::SBO_DZ), make_uint4(p[4], p[5], p[6], p[7]));
         }
         tc::fence_smem_to_async();
         tc::fence_before_sync();
@@ -388,35 +413,42 @@ __global__ void __launch_bounds__(256, 1) mlp_train_kernel(const TrainArgs a) {
         }
         tc::mbar_wait(mbar, phase); phase ^= 1;
         tc::fence_after_sync();
-        // ---- epilogue 4: dX (fp32) -> shared staging -> coalesced global stores.
-        // The [dZ2 | dZ1] tile is free (MMA4/5 have completed) and holds the
-        // 128 x K0 fp32 tile exactly (K0 <= 64); 16-byte chunk q of row t sits
-        // at chunk q ^ (t & m) of its row (conflict-free writes), then the
-        // slot's 128 threads store the tile -- ONE contiguous block of dX -- in
-        // consecutive 16-byte chunks (each warp store 512 contiguous bytes;
-        // per-row stores left half of every sector empty and stalled on
-        // lg_throttle).
+        // ---- epilogue 4: dX (fp32) -> shared staging -> TMA tensor stores.
+        // The [dZ2 | dZ1] tile is free (MMA4/5 have completed); it takes the
+        // 128 x K0 fp32 tile as K0 / 16 boxes of 128 rows x 16 columns in the
+        // TMA's 64-byte swizzle (row t at 64 t, 16-byte chunk c at
+        // c ^ ((t >> 1) & 3): conflict-free writes).  One thread issues the
+        // stores; the copy engine writes dX while the slot goes on, and that
+        // thread waits for the engine's reads before the tile is rewritten
+        // (epilogue 2 of the next tile).  Earlier forms: 16-byte per-row
+        // stores (half sectors, lg_throttle); a shared staging tile stored by
+        // the threads with coalesced STGs (~1.2 us of the per-tile chain);
+        // 32-byte st.global.v8 per row segment (slower).  A ragged last tile
+        // is stored by the threads.
         {
-            constexpr int CH = K0 / 4;                            // 16-byte chunks per row
-            constexpr int SW = (CH % 8 == 0) ? 7 : 3;             // swizzle mask within aligned chunk groups
-            float4 *stg = reinterpret_cast<float4 *>(sDZ);
+            float v[XC];
+            tmem_ld_cols<XC>(tm + lane_off + Lo::T_ACC + hf * XC, v);
+            if (a.N - tile * TILE >= TILE) {   // full tile (slot-uniform)
 #pragma unroll
-            for (int c = 0; c < K0; c += 16) {
-                float v[16];
-                tc::tmem_ld16(tm + lane_off + Lo::T_ACC + c, v);
-                tc::tmem_wait_ld();
+                for (int j = 0; j < XC; j += 4) {
+                    const int col = hf * XC + j, bx = col >> 4, c = (col >> 2) & 3;
+                    *reinterpret_cast<float4 *>(sDZ + bx * 8192 + t * 64 + 16 * (c ^ ((t >> 1) & 3))) =
+                        make_float4(v[j], v[j + 1], v[j + 2], v[j + 3]);
+                }
+                tc::fence_smem_to_async();
+                slot_sync(slot);
+                if (issuer) {
 #pragma unroll
-                for (int j = 0; j < 16; j += 4)
-                    stg[t * CH + (((c + j) / 4) ^ (t & SW))] = make_float4(v[j], v[j + 1], v[j + 2], v[j + 3]);
-            }
-            tc::fence_before_sync();
-            slot_sync(slot);
-            const int64_t rows_left = a.N - tile * TILE;          // valid rows of this tile
-            float4 *dst = reinterpret_cast<float4 *>(a.dx) + tile * TILE * CH;
-#pragma unroll 4
-            for (int k = t; k < TILE * CH; k += TILE) {
-                const int r = k / CH, q = k - r * CH;
-                if (r < rows_left) dst[k] = stg[r * CH + (q ^ (r & SW))];
+                    for (int bx = 0; bx < K0 / 16; bx++)
+                        asm volatile("cp.async.bulk.tensor.2d.global.shared::cta.bulk_group [%0, {%1, %2}], [%3];"
+                                     ::"l"(reinterpret_cast<uint64_t>(&tm_dx)), "r"(16 * bx), "r"((int)(tile * TILE)),
+                                     "r"(aDZ + 8192u * bx) : "memory");
+                    asm volatile("cp.async.bulk.commit_group;" ::: "memory");
+                }
+            } else if (valid) {
+                float4 *dst = reinterpret_cast<float4 *>(a.dx + row * K0 + hf * XC);
+#pragma unroll
+                for (int j = 0; j < XC; j += 4) dst[j / 4] = make_float4(v[j], v[j + 1], v[j + 2], v[j + 3]);
             }
         }
         tc::fence_before_sync();
@@ -424,15 +456,18 @@ __global__ void __launch_bounds__(256, 1) mlp_train_kernel(const TrainArgs a) {
         tc::fence_after_sync();
     }
 
+    if (issuer) asm volatile("cp.async.bulk.wait_group 0;" ::: "memory");   // the last dX stores are done
+
     // ---- weight gradients out of TMEM: rows 0..63 -> dW2, db2; 64..127 -> dW1, db1,
     // written (not atomically added) into this slot's row of the partial
     // buffer; mlp_grad_reduce_kernel sums the rows.  (Per-slot atomics on
     // the same 6-8 k addresses from ~300 slots cost ~38 us per call at cfg3.)
+    // The two column halves take alternate 16-column chunks.
     {
         const int r = t;  // TMEM lane = row of DW
         float *g = a.partial + (int64_t)(2 * blockIdx.x + slot) * a.P;
 #pragma unroll 1
-        for (int c = 0; c < Lo::WHX; c += 16) {
+        for (int c = 16 * hf; c < Lo::WHX; c += 32) {
             float v[16];
             if (my_tiles > 0) {   // slot-uniform
                 tc::tmem_ld16(tm + lane_off + Lo::T_DW + c, v);
@@ -455,14 +490,16 @@ __global__ void __launch_bounds__(256, 1) mlp_train_kernel(const TrainArgs a) {
             }
         }
         // dw3[r] = hi + lo columns of the D3 accumulator, rows 0..63
-        float d3[16] = {0.f};
-        if (my_tiles > 0) {
-            tc::tmem_ld16(tm + lane_off + Lo::T_D3, d3);
-            tc::tmem_wait_ld();
+        if (hf == 0) {
+            float d3[16] = {0.f};
+            if (my_tiles > 0) {
+                tc::tmem_ld16(tm + lane_off + Lo::T_D3, d3);
+                tc::tmem_wait_ld();
+            }
+            if (r < H) g[off_w3(K0) + r] = d3[0] + d3[1];
         }
-        if (r < H) g[off_w3(K0) + r] = d3[0] + d3[1];
     }
-    // db3 and loss: warp reduce, then one atomic per CTA
+    // db3 and loss (column half 0 holds them): warp reduce, then one atomic per CTA
 #pragma unroll
     for (int o = 16; o > 0; o >>= 1) {
         db3_acc += __shfl_xor_sync(0xffffffffu, db3_acc, o);
@@ -474,7 +511,7 @@ __global__ void __launch_bounds__(256, 1) mlp_train_kernel(const TrainArgs a) {
     __syncthreads();
     if (tid == 0) {
         float d = 0.f, l = 0.f;
-        for (int w = 0; w < 8; w++) { d += s_db3[w]; l += s_loss[w]; }
+        for (int w = 0; w < 16; w++) { d += s_db3[w]; l += s_loss[w]; }
         a.partial[(int64_t)(2 * blockIdx.x) * a.P + off_b3(K0)] = d;
         a.partial[(int64_t)(2 * blockIdx.x + 1) * a.P + off_b3(K0)] = 0.f;
         if (2 * (int64_t)blockIdx.x < n_tiles) atomicAdd(a.loss, l * a.inv_n_global);

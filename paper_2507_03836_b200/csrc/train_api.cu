@@ -1,5 +1,7 @@
 // train_api.cu -- host side of the train step (include/fhash.h "train
 // step" section): trainer object, launch sequence, Adam bookkeeping.
+#include <cuda.h>
+#include <cudaTypedefs.h>
 #include <cuda_runtime.h>
 
 #include <dlfcn.h>
@@ -29,6 +31,7 @@ struct fh_trainer_s {
     // workspace carve-up
     __nv_bfloat16 *enc_out = nullptr;  // [max_batch][K0]
     float *dx = nullptr;               // [max_batch][K0]
+    CUtensorMap tm_dx;                 // TMA map of dx for the MLP kernel's dX stores
     int *flag = nullptr;               // bit 1: non-finite loss
     float *partial = nullptr;          // [2 n_sm][P] per-slot MLP gradient partials
     float *loss_scratch = nullptr;
@@ -95,6 +98,31 @@ fh_status check_mlp(fh_encoder enc, const fh_mlp_desc *m) {
     return FH_OK;
 }
 
+// 2-D tensor map of dx ([max_batch][K0] fp32): box 128 rows x 16 columns,
+// 64-byte swizzle -- the MLP kernel's dX staging layout.  The encode
+// function comes from the driver through the runtime (no libcuda link).
+fh_status make_dx_map(fh_trainer tr) {
+    static PFN_cuTensorMapEncodeTiled_v12000 encode = nullptr;
+    if (!encode) {
+        void *fn = nullptr;
+        cudaDriverEntryPointQueryResult q;
+        if (cudaGetDriverEntryPoint("cuTensorMapEncodeTiled", &fn, cudaEnableDefault, &q) != cudaSuccess ||
+            q != cudaDriverEntryPointSuccess || !fn)
+            return fail(FH_E_CUDA, "cuTensorMapEncodeTiled not available from the driver");
+        encode = reinterpret_cast<PFN_cuTensorMapEncodeTiled_v12000>(fn);
+    }
+    if (tr->max_batch >= (int64_t)1 << 31) return fail(FH_E_ARG, "fh_trainer_create: max_batch >= 2^31");
+    cuuint64_t dims[2] = {(cuuint64_t)tr->K0, (cuuint64_t)tr->max_batch};
+    cuuint64_t strides[1] = {(cuuint64_t)tr->K0 * 4};
+    cuuint32_t box[2] = {16, 128};
+    cuuint32_t es[2] = {1, 1};
+    const CUresult r = encode(&tr->tm_dx, CU_TENSOR_MAP_DATA_TYPE_FLOAT32, 2, tr->dx, dims, strides, box, es,
+                              CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_64B, CU_TENSOR_MAP_L2_PROMOTION_NONE,
+                              CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
+    if (r != CUDA_SUCCESS) return fail(FH_E_CUDA, "cuTensorMapEncodeTiled(dx) failed (%d)", (int)r);
+    return FH_OK;
+}
+
 template <int K0>
 fh_status launch_mlp(fh_trainer tr, const float *target, int64_t N, int64_t N_global, float *loss,
                      cudaStream_t s) {
@@ -115,7 +143,7 @@ fh_status launch_mlp(fh_trainer tr, const float *target, int64_t N, int64_t N_gl
     const int64_t tiles = (N + fh::mlp::TILE - 1) / fh::mlp::TILE;
     const int64_t pairs = (tiles + 1) / 2;  // two tile slots per CTA
     const int grid = (int)(pairs < tr->n_sm ? pairs : tr->n_sm);
-    { fh::mlp::mlp_train_kernel<K0><<<grid, 256, smem, s>>>(a); fh::count_launch(); }
+    { fh::mlp::mlp_train_kernel<K0><<<grid, fh::mlp::TRAIN_THREADS, smem, s>>>(a, tr->tm_dx); fh::count_launch(); }
     const int rows = 2 * grid;
     const dim3 rg((unsigned)((a.P + 255) / 256), (unsigned)((rows + 15) / 16));
     { fh::mlp::mlp_grad_reduce_kernel<<<rg, 256, 0, s>>>(tr->b.mlp_grad, tr->partial, rows, a.P,
@@ -177,6 +205,7 @@ fh_status fh_trainer_create(fh_encoder enc, const fh_mlp_desc *m, const fh_train
     tr->partial = reinterpret_cast<float *>(w + 256);
     // no device work here: the flags are cleared on the first step's stream
     if ((st = set_mlp_attrs(tr->K0)) != FH_OK) { delete tr; return st; }
+    if ((st = make_dx_map(tr)) != FH_OK) { delete tr; return st; }
     *out = tr;
     return FH_OK;
 }
