@@ -46,26 +46,36 @@ __host__ __device__ constexpr int off_w3(int K0) { return H * K0 + 2 * H + H * H
 __host__ __device__ constexpr int off_b3(int K0) { return H * K0 + 3 * H + H * H; }
 __host__ __device__ constexpr int param_count(int K0) { return H * K0 + 3 * H + H * H + 1; }
 
-// Two independent tile "slots" per CTA (warps 0-3 and 4-7), each with its
-// own shared-memory tiles, TMEM columns, mbarrier and MMA-issuing thread, so
-// one slot's epilogue math overlaps the other slot's MMAs and loads.  Within
-// a slot the four per-tile accumulators Z1, Z2, dH1, dX share ONE 64-column
-// TMEM region (each is consumed before the next MMA of the chain is issued);
-// each slot accumulates its own DW block across all its tiles.
+// Two independent tile "slots" per CTA (warps 0-7 and 8-15), each with its
+// own shared-memory tiles, TMEM columns, mbarriers and MMA-issuing thread,
+// so one slot's epilogue math overlaps the other slot's MMAs and loads.
+// Within a slot the four per-tile accumulators Z1, Z2, dH1, dX share ONE
+// 64-column TMEM region (each is consumed before the next MMA of the chain
+// is issued); each slot accumulates its own DW block across all its tiles.
+//
+// Per slot: the [H1 | 1 0..0] tile; two 16 KB buffers that alternate
+// between the tile's X operand (landed by TMA in the core-matrix layout, a
+// tile ahead) and its h2 tile (the next tile's X lands in this tile's h2
+// buffer once MMA6 has read it; this tile's X buffer takes the next tile's
+// h2 once MMA5 has read it); the [dZ2 | dZ1] tile (also the dX staging);
+// the [dy_hi dy_lo] tile.
 template <int K0>
 struct Layout {
-    static constexpr int WHX = H + K0 + 16;               // columns of the [H1 | X | 1..] tile
-    static constexpr uint32_t SBO_HX = (WHX / 8) * 128;   // bytes per 8-sample row group
+    static constexpr int WH1 = H + 16;                    // columns of the [H1 | 1 0..0] tile
+    static constexpr int WHX = WH1 + K0;                  // DW accumulator columns: [dW2 | db | dW1]
+    static constexpr uint32_t SBO_H1 = (WH1 / 8) * 128;   // bytes per 8-sample row group: 1280
+    static constexpr uint32_t SBO_X = (K0 / 8) * 128;
     static constexpr uint32_t SBO_DZ = (2 * H / 8) * 128; // [dZ2 | dZ1] tile: 2048
     static constexpr uint32_t SBO_W1 = (K0 / 8) * 128;
     static constexpr uint32_t SBO_W2 = (H / 8) * 128;
-    static constexpr uint32_t BYTES_HX = TILE * WHX * 2;
+    static constexpr uint32_t BYTES_H1 = TILE * WH1 * 2;
+    static constexpr uint32_t BYTES_X = TILE * K0 * 2;    // X tile (TMA transaction bytes)
+    static constexpr uint32_t BYTES_XB = TILE * H * 2;    // one X / h2 buffer (h2: SBO 1024; K0 <= H)
     static constexpr uint32_t BYTES_DZ = TILE * 2 * H * 2;
-    static constexpr uint32_t BYTES_H2 = TILE * H * 2;    // bf16 h2 tile (core-matrix layout, SBO 1024)
     static constexpr uint32_t BYTES_DY = TILE * 16 * 2;   // [dy_hi, dy_lo, 0 x 14] per sample (SBO 256)
     // the dw3 MMA reads A rows 64..127 past the h2 tile (results discarded):
-    // keep 1 KB of slack inside the slot so those reads stay in bounds
-    static constexpr uint32_t BYTES_SLOT = BYTES_HX + BYTES_DZ + BYTES_H2 + BYTES_DY + 1024;
+    // 1 KB past the second buffer is the DZ tile, keep 1 KB of slack after DY
+    static constexpr uint32_t BYTES_SLOT = BYTES_H1 + 2 * BYTES_XB + BYTES_DZ + BYTES_DY + 1024;
     static constexpr uint32_t BYTES_W1 = H * K0 * 2;
     static constexpr uint32_t BYTES_W2 = H * H * 2;
     static constexpr int SLOTS = 2;
@@ -74,6 +84,8 @@ struct Layout {
     static constexpr uint32_t T_ACC = 0, T_DW = 64, T_D3 = 64 + WHX;  // T_D3: [dw3_hi, dw3_lo] accumulators
     static constexpr uint32_t TMEM_COLS = 512;
     static_assert(T_D3 + 16 <= 256, "slot TMEM region overflow");
+    static_assert(K0 <= H && BYTES_X <= BYTES_XB, "X tile must fit an h2 buffer");
+    static_assert(BYTES_H1 % 1024 == 0 && BYTES_XB % 1024 == 0 && BYTES_SLOT % 1024 == 0, "1 KB aligned tiles");
 };
 
 __device__ __forceinline__ uint32_t pack_bf16(float a, float b) {
@@ -140,9 +152,13 @@ __device__ __forceinline__ void tmem_ld_cols(uint32_t taddr, float (&v)[N]) {
 }
 
 template <int K0>
-// tm_dx: 2-D tensor map of dX ([max_batch][K0] fp32), box 128 rows x 16
-// columns, 64-byte swizzle (created once per trainer).
+// tm_x: 4-D tensor map of x ([N][K0] bf16) as (8 elements, row % 8, 16-byte
+// chunk, row / 8): a box of 128 rows lands in the core-matrix layout
+// (SWIZZLE_NONE, SBO = K0 * 16); rows past N read as zero.  tm_dx: 2-D map
+// of dX ([N][K0] fp32), box 128 rows x 16 columns, 64-byte swizzle; rows
+// past N are not written.  Both encoded per launch (train_api.cu).
 __global__ void __launch_bounds__(TRAIN_THREADS, 1) mlp_train_kernel(const TrainArgs a,
+                                                                     const __grid_constant__ CUtensorMap tm_x,
                                                                      const __grid_constant__ CUtensorMap tm_dx) {
     using Lo = Layout<K0>;
     constexpr int HC = H / 2;            // hidden columns per thread
@@ -165,10 +181,10 @@ __global__ void __launch_bounds__(TRAIN_THREADS, 1) mlp_train_kernel(const Train
     const int hf = ws >> 2;              // column half
     const int t = ((ws & 3) << 5) | lane;   // sample row within the slot's tile = TMEM lane
     const int ts = tid & (SLOT_THREADS - 1);
-    uint8_t *sHX = smem + Lo::BYTES_W1 + Lo::BYTES_W2 + slot * Lo::BYTES_SLOT;
-    uint8_t *sDZ = sHX + Lo::BYTES_HX;
-    uint8_t *sH2 = sDZ + Lo::BYTES_DZ;
-    uint8_t *sDY = sH2 + Lo::BYTES_H2;
+    uint8_t *sH1 = smem + Lo::BYTES_W1 + Lo::BYTES_W2 + slot * Lo::BYTES_SLOT;
+    uint8_t *sXB = sH1 + Lo::BYTES_H1;   // the two X / h2 buffers
+    uint8_t *sDZ = sXB + 2 * Lo::BYTES_XB;
+    uint8_t *sDY = sDZ + Lo::BYTES_DZ;
     const int64_t n_tiles = (a.N + TILE - 1) / TILE;
     // the dX staging relies on the TMA swizzle's address pattern (512-byte atoms)
     if (tid == 0 && (tc::smem_u32(smem) & 1023u) != 0u) __trap();
@@ -182,9 +198,9 @@ __global__ void __launch_bounds__(TRAIN_THREADS, 1) mlp_train_kernel(const Train
         const int r = i / H, c = i % H;
         *reinterpret_cast<__nv_bfloat16 *>(sW2 + tc::core_off(r, c, Lo::SBO_W2)) = a.wsh[off_W2(K0) + i];
     }
-    {   // constant columns [H + K0, H + K0 + 16) of each slot's HX tile: 1, 0, ..., 0
+    {   // constant columns [H, H + 16) of each slot's H1 tile: 1, 0, ..., 0
         const uint4 ones = make_uint4(pack_bf16(1.f, 0.f), 0u, 0u, 0u), zero = make_uint4(0u, 0u, 0u, 0u);
-        st16(sHX, tc::core_off(t, H + K0 + 8 * hf, Lo::SBO_HX), hf ? zero : ones);
+        st16(sH1, tc::core_off(t, H + 8 * hf, Lo::SBO_H1), hf ? zero : ones);
     }
     if (tid < H) {
         b1[tid] = a.wmaster[off_b1(K0) + tid];
@@ -202,38 +218,34 @@ __global__ void __launch_bounds__(TRAIN_THREADS, 1) mlp_train_kernel(const Train
     tc::fence_before_sync();
     __syncthreads();
     tc::fence_after_sync();
-    // X tiles arrive by ONE bulk async copy each (a tile's rows are one
-    // contiguous block of x), issued a tile ahead into the slot's h2 tile --
-    // free from the completion of MMA3/6 (its last reader) to the next
-    // epilogue 2 -- and unpacked into the core-matrix layout at the tile's
-    // start: the HBM latency of X overlaps the previous tile's epilogues.
+    // X tiles arrive by TMA (tm_x), a tile ahead, into the buffer the
+    // previous tile's h2 used (see Layout): the HBM latency of X overlaps the
+    // previous tile's epilogues, and no thread touches X.
     uint64_t *xb = &xbar[slot];
     uint32_t xphase = 0;
-    auto issue_x = [&](int64_t tl) {
+    auto issue_x = [&](int64_t tl, uint32_t dst) {
         if (ts != 0 || tl >= n_tiles) return;
-        const int64_t rows = a.N - tl * TILE < TILE ? a.N - tl * TILE : TILE;
-        const uint32_t bytes = (uint32_t)(rows * K0 * 2);
         asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
-        asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;" ::"r"(tc::smem_u32(xb)), "r"(bytes)
+        asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;" ::"r"(tc::smem_u32(xb)), "r"(Lo::BYTES_X)
                      : "memory");
-        asm volatile("cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1], %2, [%3];"
-                     ::"r"(tc::smem_u32(sH2)), "l"(a.x + tl * TILE * K0), "r"(bytes), "r"(tc::smem_u32(xb))
-                     : "memory");
+        asm volatile("cp.async.bulk.tensor.4d.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1, {%2, %3, %4, %5}], [%6];"
+                     ::"r"(dst), "l"(reinterpret_cast<uint64_t>(&tm_x)), "r"(0), "r"(0), "r"(0), "r"((int)(tl * (TILE / 8))),
+                     "r"(tc::smem_u32(xb)) : "memory");
     };
-    issue_x(2 * (int64_t)blockIdx.x + slot);
+    issue_x(2 * (int64_t)blockIdx.x + slot, tc::smem_u32(sXB));
     const uint32_t tm = tbase + (uint32_t)slot * 256u;
     const uint32_t lane_off = (uint32_t)((ws & 3) * 32) << 16;
     uint64_t *mbar = &bar[slot];
     const bool issuer = (ts == 0);
     const int hc0 = hf * HC;             // this thread's first hidden column
 
-    const uint32_t aHX = tc::smem_u32(sHX), aDZ = tc::smem_u32(sDZ);
-    const uint32_t aH2 = tc::smem_u32(sH2), aDY = tc::smem_u32(sDY);
+    const uint32_t aH1 = tc::smem_u32(sH1), aDZ = tc::smem_u32(sDZ), aDY = tc::smem_u32(sDY);
     const uint32_t aW1 = tc::smem_u32(sW1), aW2 = tc::smem_u32(sW2);
     constexpr uint32_t id_h = tc::idesc_bf16_f32(128, H, false, false);      // N = 64, K-major A,B
     constexpr uint32_t id_dh = tc::idesc_bf16_f32(128, H, false, true);      // B = W2 MN-major
     constexpr uint32_t id_dx = tc::idesc_bf16_f32(128, K0, false, true);     // B = W1 MN-major
-    constexpr uint32_t id_dw = tc::idesc_bf16_f32(128, Lo::WHX, true, true); // both MN-major
+    constexpr uint32_t id_dw = tc::idesc_bf16_f32(128, Lo::WH1, true, true); // both MN-major: [H1 | 1] block
+    constexpr uint32_t id_dwx = tc::idesc_bf16_f32(128, K0, true, true);     // X block
     constexpr uint32_t id_d3 = tc::idesc_bf16_f32(128, 16, true, true);      // dw3: H2^T . [dy_hi dy_lo]
 
     uint32_t phase = 0;
@@ -244,30 +256,32 @@ __global__ void __launch_bounds__(TRAIN_THREADS, 1) mlp_train_kernel(const Train
     for (int64_t tile = 2 * (int64_t)blockIdx.x + slot; tile < n_tiles; tile += 2 * (int64_t)gridDim.x, my_tiles++) {
         const int64_t row = tile * TILE + t;
         const bool valid = row < a.N;
-        // ---- X row (bf16, landed in the h2 tile by the bulk copy) -> [H1 | X | 1]
-        // columns H .. H+K0.  Half hf takes the chunks of its parity; chunk
-        // order rotated by the row (rows are K0 * 2 bytes apart: the same
-        // chunk of 8 rows would share banks).
-        tc::mbar_wait(xb, xphase); xphase ^= 1;
-        {
-            const uint4 *src = reinterpret_cast<const uint4 *>(sH2) + t * XQ;
-#pragma unroll
-            for (int q0 = 0; q0 < XQ / 2; q0++) {
-                const int q = (2 * q0 + hf + t) % XQ;
-                const uint4 v = valid ? src[q] : make_uint4(0u, 0u, 0u, 0u);
-                st16(sHX, tc::core_off(t, H + 8 * q, Lo::SBO_HX), v);
-            }
-        }
+        // this tile's X buffer and h2 buffer (they swap every tile)
+        const int xi = my_tiles & 1;
+        uint8_t *sX = sXB + xi * Lo::BYTES_XB, *sH2 = sXB + (xi ^ 1) * Lo::BYTES_XB;
+        const uint32_t aX = tc::smem_u32(sX), aH2 = tc::smem_u32(sH2);
         const float tgt = valid ? __ldg(a.target + row) : 0.f;
-        tc::fence_smem_to_async();
-        tc::fence_before_sync();
-        slot_sync(slot);
-        tc::fence_after_sync();
+        if (a.N - tile * TILE < TILE) {
+            // ragged last tile: the TMA zero-fills whole 8-row groups past N;
+            // rows past N inside the last group are zeroed here
+            tc::mbar_wait(xb, xphase);
+            if (!valid) {
+#pragma unroll
+                for (int q = hf; q < K0 / 8; q += 2) st16(sX, tc::core_off(t, 8 * q, Lo::SBO_X), make_uint4(0u, 0u, 0u, 0u));
+            }
+            tc::fence_smem_to_async();
+            tc::fence_before_sync();
+            slot_sync(slot);
+            tc::fence_after_sync();
+        } else if (issuer) {
+            tc::mbar_wait(xb, xphase);   // only the MMA issuer needs X
+        }
+        xphase ^= 1;
         // ---- MMA1: Z1 = X . W1^T
         if (issuer) {
 #pragma unroll
             for (int s = 0; s < K0 / 16; s++)
-                tc::mma_bf16(tm + Lo::T_ACC, tc::sdesc(aHX + (H / 8) * 128 + s * 256, 128, Lo::SBO_HX),
+                tc::mma_bf16(tm + Lo::T_ACC, tc::sdesc(aX + s * 256, 128, Lo::SBO_X),
                              tc::sdesc(aW1 + s * 256, 128, Lo::SBO_W1), id_h, s > 0);
             tc::commit(mbar);
         }
@@ -281,7 +295,7 @@ __global__ void __launch_bounds__(TRAIN_THREADS, 1) mlp_train_kernel(const Train
             for (int c = 0; c < HC; c += 8) {
                 const float4 ba = *reinterpret_cast<const float4 *>(b1 + hc0 + c);
                 const float4 bb = *reinterpret_cast<const float4 *>(b1 + hc0 + c + 4);
-                st16(sHX, tc::core_off(t, hc0 + c, Lo::SBO_HX),
+                st16(sH1, tc::core_off(t, hc0 + c, Lo::SBO_H1),
                      make_uint4(pack_bf16(fmaxf(v[c] + ba.x, 0.f), fmaxf(v[c + 1] + ba.y, 0.f)),
                                 pack_bf16(fmaxf(v[c + 2] + ba.z, 0.f), fmaxf(v[c + 3] + ba.w, 0.f)),
                                 pack_bf16(fmaxf(v[c + 4] + bb.x, 0.f), fmaxf(v[c + 5] + bb.y, 0.f)),
@@ -296,7 +310,7 @@ __global__ void __launch_bounds__(TRAIN_THREADS, 1) mlp_train_kernel(const Train
         if (issuer) {
 #pragma unroll
             for (int s = 0; s < H / 16; s++)
-                tc::mma_bf16(tm + Lo::T_ACC, tc::sdesc(aHX + s * 256, 128, Lo::SBO_HX),
+                tc::mma_bf16(tm + Lo::T_ACC, tc::sdesc(aH1 + s * 256, 128, Lo::SBO_H1),
                              tc::sdesc(aW2 + s * 256, 128, Lo::SBO_W2), id_h, s > 0);
             tc::commit(mbar);
         }
@@ -375,7 +389,7 @@ __global__ void __launch_bounds__(TRAIN_THREADS, 1) mlp_train_kernel(const Train
             tc::commit(mbar);
         }
         tc::mbar_wait(mbar, phase); phase ^= 1;
-        issue_x(tile + 2 * (int64_t)gridDim.x);   // the h2 tile is free: prefetch the next X
+        issue_x(tile + 2 * (int64_t)gridDim.x, aH2);   // the h2 buffer is free: the next tile's X
         tc::fence_after_sync();
         // ---- epilogue 3: dZ1 = bf16(dH1 * mask1), mask1 = (h1 > 0) from the H1 tile
         {
@@ -383,7 +397,7 @@ __global__ void __launch_bounds__(TRAIN_THREADS, 1) mlp_train_kernel(const Train
             tmem_ld_cols<HC>(tm + lane_off + Lo::T_ACC + hc0, v);
 #pragma unroll
             for (int c = 0; c < HC; c += 8) {
-                const uint4 ha = *reinterpret_cast<const uint4 *>(sHX + tc::core_off(t, hc0 + c, Lo::SBO_HX));
+                const uint4 ha = *reinterpret_cast<const uint4 *>(sH1 + tc::core_off(t, hc0 + c, Lo::SBO_H1));
                 const uint32_t hw[4] = {ha.x, ha.y, ha.z, ha.w};
                 uint32_t p[4];
 #pragma unroll
@@ -398,7 +412,8 @@ __global__ void __launch_bounds__(TRAIN_THREADS, 1) mlp_train_kernel(const Train
         tc::fence_before_sync();
         slot_sync(slot);
         tc::fence_after_sync();
-        // ---- MMA4: dX = dZ1 . W1 ; MMA5: DW += [dZ2^T; dZ1^T] . [H1 | X | 1]
+        // ---- MMA4: dX = dZ1 . W1 ; MMA5: DW += [dZ2^T; dZ1^T] . [H1 | 1 | X]
+        // (two N blocks: the [H1 | 1] tile and the X buffer)
         if (issuer) {
 #pragma unroll
             for (int s = 0; s < H / 16; s++)
@@ -406,9 +421,12 @@ __global__ void __launch_bounds__(TRAIN_THREADS, 1) mlp_train_kernel(const Train
                              tc::sdesc(aW1 + s * 2 * Lo::SBO_W1, Lo::SBO_W1, 128), id_dx, s > 0);
 #pragma unroll
             for (int s = 0; s < TILE / 16; s++)
-                tc::mma_bf16(tm + Lo::T_DW, tc::sdesc(aDZ + s * 2 * Lo::SBO_DZ, Lo::SBO_DZ, 128),
-                             tc::sdesc(aHX + s * 2 * Lo::SBO_HX, Lo::SBO_HX, 128), id_dw,
-                             (my_tiles > 0 || s > 0) ? 1u : 0u);
+            {
+                const uint64_t ad = tc::sdesc(aDZ + s * 2 * Lo::SBO_DZ, Lo::SBO_DZ, 128);
+                const uint32_t acc = (my_tiles > 0 || s > 0) ? 1u : 0u;
+                tc::mma_bf16(tm + Lo::T_DW, ad, tc::sdesc(aH1 + s * 2 * Lo::SBO_H1, Lo::SBO_H1, 128), id_dw, acc);
+                tc::mma_bf16(tm + Lo::T_DW + Lo::WH1, ad, tc::sdesc(aX + s * 2 * Lo::SBO_X, Lo::SBO_X, 128), id_dwx, acc);
+            }
             tc::commit(mbar);
         }
         tc::mbar_wait(mbar, phase); phase ^= 1;
@@ -423,12 +441,11 @@ __global__ void __launch_bounds__(TRAIN_THREADS, 1) mlp_train_kernel(const Train
         // (epilogue 2 of the next tile).  Earlier forms: 16-byte per-row
         // stores (half sectors, lg_throttle); a shared staging tile stored by
         // the threads with coalesced STGs (~1.2 us of the per-tile chain);
-        // 32-byte st.global.v8 per row segment (slower).  A ragged last tile
-        // is stored by the threads.
+        // 32-byte st.global.v8 per row segment (slower).
         {
             float v[XC];
             tmem_ld_cols<XC>(tm + lane_off + Lo::T_ACC + hf * XC, v);
-            if (a.N - tile * TILE >= TILE) {   // full tile (slot-uniform)
+            {   // rows past N (ragged last tile) are clipped by the TMA
 #pragma unroll
                 for (int j = 0; j < XC; j += 4) {
                     const int col = hf * XC + j, bx = col >> 4, c = (col >> 2) & 3;
@@ -445,10 +462,6 @@ __global__ void __launch_bounds__(TRAIN_THREADS, 1) mlp_train_kernel(const Train
                                      "r"(aDZ + 8192u * bx) : "memory");
                     asm volatile("cp.async.bulk.commit_group;" ::: "memory");
                 }
-            } else if (valid) {
-                float4 *dst = reinterpret_cast<float4 *>(a.dx + row * K0 + hf * XC);
-#pragma unroll
-                for (int j = 0; j < XC; j += 4) dst[j / 4] = make_float4(v[j], v[j + 1], v[j + 2], v[j + 3]);
             }
         }
         tc::fence_before_sync();
@@ -476,15 +489,15 @@ __global__ void __launch_bounds__(TRAIN_THREADS, 1) mlp_train_kernel(const Train
 #pragma unroll
                 for (int j = 0; j < 16; j++) v[j] = 0.f;
             }
-            // 16-column chunks lie entirely in one block: W2 (c < H), W1 (H <= c < H + K0) or the
-            // bias chunk (c = H + K0); the two weight blocks as float4 stores (rows padded to 4)
+            // 16-column chunks lie entirely in one block: W2 (c < H), the bias chunk (c = H) or
+            // W1 (c >= H + 16); the two weight blocks as float4 stores (rows padded to 4)
             float4 *dst = nullptr;
             if (r < H && c < H) dst = reinterpret_cast<float4 *>(g + off_W2(K0) + r * H + c);
-            else if (r >= H && c >= H && c < H + K0) dst = reinterpret_cast<float4 *>(g + off_W1() + (r - H) * K0 + (c - H));
+            else if (r >= H && c >= Lo::WH1) dst = reinterpret_cast<float4 *>(g + off_W1() + (r - H) * K0 + (c - Lo::WH1));
             if (dst) {
 #pragma unroll
                 for (int j = 0; j < 16; j += 4) dst[j / 4] = make_float4(v[j], v[j + 1], v[j + 2], v[j + 3]);
-            } else if (c == H + K0) {
+            } else if (c == H) {
                 if (r < H) g[off_b2(K0) + r] = v[0];
                 else g[off_b1(K0) + (r - H)] = v[0];
             }

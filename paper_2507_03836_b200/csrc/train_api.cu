@@ -31,7 +31,6 @@ struct fh_trainer_s {
     // workspace carve-up
     __nv_bfloat16 *enc_out = nullptr;  // [max_batch][K0]
     float *dx = nullptr;               // [max_batch][K0]
-    CUtensorMap tm_dx;                 // TMA map of dx for the MLP kernel's dX stores
     int *flag = nullptr;               // bit 1: non-finite loss
     float *partial = nullptr;          // [2 n_sm][P] per-slot MLP gradient partials
     float *loss_scratch = nullptr;
@@ -98,28 +97,50 @@ fh_status check_mlp(fh_encoder enc, const fh_mlp_desc *m) {
     return FH_OK;
 }
 
-// 2-D tensor map of dx ([max_batch][K0] fp32): box 128 rows x 16 columns,
-// 64-byte swizzle -- the MLP kernel's dX staging layout.  The encode
-// function comes from the driver through the runtime (no libcuda link).
-fh_status make_dx_map(fh_trainer tr) {
+// The MLP kernel's tensor maps for an N-sample launch (host-side encoding,
+// no device work; the encode function comes from the driver through the
+// runtime, no libcuda link):
+//   x  [N][K0] bf16 as 4-D (8 elements, row % 8, 16-byte chunk, row / 8),
+//      box (8, 8, K0 / 8, 16): a 128-row tile lands in the core-matrix
+//      layout (SWIZZLE_NONE, SBO = K0 * 16); row groups past N read as zero;
+//   dx [N][K0] fp32, box 128 rows x 16 columns, 64-byte swizzle (the
+//      kernel's dX staging layout); rows past N are not written.
+PFN_cuTensorMapEncodeTiled_v12000 tmap_encoder() {
     static PFN_cuTensorMapEncodeTiled_v12000 encode = nullptr;
     if (!encode) {
         void *fn = nullptr;
         cudaDriverEntryPointQueryResult q;
-        if (cudaGetDriverEntryPoint("cuTensorMapEncodeTiled", &fn, cudaEnableDefault, &q) != cudaSuccess ||
-            q != cudaDriverEntryPointSuccess || !fn)
-            return fail(FH_E_CUDA, "cuTensorMapEncodeTiled not available from the driver");
-        encode = reinterpret_cast<PFN_cuTensorMapEncodeTiled_v12000>(fn);
+        if (cudaGetDriverEntryPoint("cuTensorMapEncodeTiled", &fn, cudaEnableDefault, &q) == cudaSuccess &&
+            q == cudaDriverEntryPointSuccess)
+            encode = reinterpret_cast<PFN_cuTensorMapEncodeTiled_v12000>(fn);
     }
-    if (tr->max_batch >= (int64_t)1 << 31) return fail(FH_E_ARG, "fh_trainer_create: max_batch >= 2^31");
-    cuuint64_t dims[2] = {(cuuint64_t)tr->K0, (cuuint64_t)tr->max_batch};
-    cuuint64_t strides[1] = {(cuuint64_t)tr->K0 * 4};
-    cuuint32_t box[2] = {16, 128};
-    cuuint32_t es[2] = {1, 1};
-    const CUresult r = encode(&tr->tm_dx, CU_TENSOR_MAP_DATA_TYPE_FLOAT32, 2, tr->dx, dims, strides, box, es,
-                              CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_64B, CU_TENSOR_MAP_L2_PROMOTION_NONE,
-                              CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
-    if (r != CUDA_SUCCESS) return fail(FH_E_CUDA, "cuTensorMapEncodeTiled(dx) failed (%d)", (int)r);
+    return encode;
+}
+
+fh_status make_mlp_maps(fh_trainer tr, int64_t N, CUtensorMap *tm_x, CUtensorMap *tm_dx) {
+    PFN_cuTensorMapEncodeTiled_v12000 encode = tmap_encoder();
+    if (!encode) return fail(FH_E_CUDA, "cuTensorMapEncodeTiled not available from the driver");
+    const cuuint64_t K0 = (cuuint64_t)tr->K0;
+    {
+        cuuint64_t dims[4] = {8, 8, K0 / 8, (cuuint64_t)((N + 7) / 8)};
+        cuuint64_t strides[3] = {K0 * 2, 16, K0 * 16};
+        cuuint32_t box[4] = {8, 8, (cuuint32_t)(K0 / 8), 16};
+        cuuint32_t es[4] = {1, 1, 1, 1};
+        const CUresult r = encode(tm_x, CU_TENSOR_MAP_DATA_TYPE_BFLOAT16, 4, tr->enc_out, dims, strides, box, es,
+                                  CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_NONE,
+                                  CU_TENSOR_MAP_L2_PROMOTION_NONE, CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
+        if (r != CUDA_SUCCESS) return fail(FH_E_CUDA, "cuTensorMapEncodeTiled(x) failed (%d)", (int)r);
+    }
+    {
+        cuuint64_t dims[2] = {K0, (cuuint64_t)N};
+        cuuint64_t strides[1] = {K0 * 4};
+        cuuint32_t box[2] = {16, 128};
+        cuuint32_t es[2] = {1, 1};
+        const CUresult r = encode(tm_dx, CU_TENSOR_MAP_DATA_TYPE_FLOAT32, 2, tr->dx, dims, strides, box, es,
+                                  CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_64B,
+                                  CU_TENSOR_MAP_L2_PROMOTION_NONE, CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
+        if (r != CUDA_SUCCESS) return fail(FH_E_CUDA, "cuTensorMapEncodeTiled(dx) failed (%d)", (int)r);
+    }
     return FH_OK;
 }
 
@@ -127,6 +148,9 @@ template <int K0>
 fh_status launch_mlp(fh_trainer tr, const float *target, int64_t N, int64_t N_global, float *loss,
                      cudaStream_t s) {
     const int smem = mlp_smem<K0>();
+    CUtensorMap tm_x, tm_dx;
+    fh_status st = make_mlp_maps(tr, N, &tm_x, &tm_dx);
+    if (st != FH_OK) return st;
     fh::mlp::TrainArgs a;
     a.x = tr->enc_out;
     a.target = target;
@@ -143,7 +167,7 @@ fh_status launch_mlp(fh_trainer tr, const float *target, int64_t N, int64_t N_gl
     const int64_t tiles = (N + fh::mlp::TILE - 1) / fh::mlp::TILE;
     const int64_t pairs = (tiles + 1) / 2;  // two tile slots per CTA
     const int grid = (int)(pairs < tr->n_sm ? pairs : tr->n_sm);
-    { fh::mlp::mlp_train_kernel<K0><<<grid, fh::mlp::TRAIN_THREADS, smem, s>>>(a, tr->tm_dx); fh::count_launch(); }
+    { fh::mlp::mlp_train_kernel<K0><<<grid, fh::mlp::TRAIN_THREADS, smem, s>>>(a, tm_x, tm_dx); fh::count_launch(); }
     const int rows = 2 * grid;
     const dim3 rg((unsigned)((a.P + 255) / 256), (unsigned)((rows + 15) / 16));
     { fh::mlp::mlp_grad_reduce_kernel<<<rg, 256, 0, s>>>(tr->b.mlp_grad, tr->partial, rows, a.P,
@@ -205,7 +229,8 @@ fh_status fh_trainer_create(fh_encoder enc, const fh_mlp_desc *m, const fh_train
     tr->partial = reinterpret_cast<float *>(w + 256);
     // no device work here: the flags are cleared on the first step's stream
     if ((st = set_mlp_attrs(tr->K0)) != FH_OK) { delete tr; return st; }
-    if ((st = make_dx_map(tr)) != FH_OK) { delete tr; return st; }
+    if (max_batch >= (int64_t)1 << 31) { delete tr; return fail(FH_E_ARG, "fh_trainer_create: max_batch >= 2^31"); }
+    if (!tmap_encoder()) { delete tr; return fail(FH_E_CUDA, "cuTensorMapEncodeTiled not available from the driver"); }
     *out = tr;
     return FH_OK;
 }
