@@ -97,6 +97,20 @@ __device__ __forceinline__ float2 unpack_bf16(uint32_t u) {
     return __bfloat1622float2(*reinterpret_cast<const __nv_bfloat162 *>(&u));
 }
 
+// Packed-pair epilogue arithmetic (sm_100 fp32x2 / bf16x2 instructions;
+// element-wise identical to the scalar forms, half the instructions):
+// bf16(relu(z + b)) of a pair (rounding is monotonic, so relu after the
+// rounding gives the same value), and "p where h > 0, else +0" on bf16 pairs.
+__device__ __forceinline__ uint32_t bf2_bits(__nv_bfloat162 h) { return *reinterpret_cast<uint32_t *>(&h); }
+__device__ __forceinline__ __nv_bfloat162 bits_bf2(uint32_t u) { return *reinterpret_cast<__nv_bfloat162 *>(&u); }
+__device__ __forceinline__ uint32_t bias_relu_bf16x2(float z0, float z1, float b0, float b1) {
+    const float2 zb = __fadd2_rn(make_float2(z0, z1), make_float2(b0, b1));
+    return bf2_bits(__hmax2(__float22bfloat162_rn(zb), __float2bfloat162_rn(0.f)));
+}
+__device__ __forceinline__ uint32_t where_pos(uint32_t p, uint32_t h) {
+    return p & __hgt2_mask(bits_bf2(h), __float2bfloat162_rn(0.f));
+}
+
 struct TrainArgs {
     const __nv_bfloat16 *x;      // [N][K0] encoder output
     const float *target;         // [N]
@@ -296,10 +310,10 @@ __global__ void __launch_bounds__(TRAIN_THREADS, 1) mlp_train_kernel(const Train
                 const float4 ba = *reinterpret_cast<const float4 *>(b1 + hc0 + c);
                 const float4 bb = *reinterpret_cast<const float4 *>(b1 + hc0 + c + 4);
                 st16(sH1, tc::core_off(t, hc0 + c, Lo::SBO_H1),
-                     make_uint4(pack_bf16(fmaxf(v[c] + ba.x, 0.f), fmaxf(v[c + 1] + ba.y, 0.f)),
-                                pack_bf16(fmaxf(v[c + 2] + ba.z, 0.f), fmaxf(v[c + 3] + ba.w, 0.f)),
-                                pack_bf16(fmaxf(v[c + 4] + bb.x, 0.f), fmaxf(v[c + 5] + bb.y, 0.f)),
-                                pack_bf16(fmaxf(v[c + 6] + bb.z, 0.f), fmaxf(v[c + 7] + bb.w, 0.f))));
+                     make_uint4(bias_relu_bf16x2(v[c], v[c + 1], ba.x, ba.y),
+                                bias_relu_bf16x2(v[c + 2], v[c + 3], ba.z, ba.w),
+                                bias_relu_bf16x2(v[c + 4], v[c + 5], bb.x, bb.y),
+                                bias_relu_bf16x2(v[c + 6], v[c + 7], bb.z, bb.w)));
             }
         }
         tc::fence_smem_to_async();
@@ -322,27 +336,21 @@ __global__ void __launch_bounds__(TRAIN_THREADS, 1) mlp_train_kernel(const Train
         {
             float v[HC];
             tmem_ld_cols<HC>(tm + lane_off + Lo::T_ACC + hc0, v);
-            float ya[4] = {0.f, 0.f, 0.f, 0.f};
+            float2 ya01 = make_float2(0.f, 0.f), ya23 = make_float2(0.f, 0.f);   // columns = 0, 1, 2, 3 mod 4
             uint32_t hp[HC / 2];
 #pragma unroll
             for (int j = 0; j < HC; j += 4) {
                 const float4 b = *reinterpret_cast<const float4 *>(b2 + hc0 + j);
                 const float4 w = *reinterpret_cast<const float4 *>(w3 + hc0 + j);
-                // bf16 rounding by the packing conversion (one F2FP per two
-                // values), unpacked by shifts: the scalar F2F round trip runs
-                // on the MIO pipe and stalled the epilogue
-                hp[j / 2] = pack_bf16(fmaxf(v[j] + b.x, 0.f), fmaxf(v[j + 1] + b.y, 0.f));
-                hp[j / 2 + 1] = pack_bf16(fmaxf(v[j + 2] + b.z, 0.f), fmaxf(v[j + 3] + b.w, 0.f));
-                const float2 h01 = unpack_bf16(hp[j / 2]), h23 = unpack_bf16(hp[j / 2 + 1]);
-                ya[0] = fmaf(h01.x, w.x, ya[0]);
-                ya[1] = fmaf(h01.y, w.y, ya[1]);
-                ya[2] = fmaf(h23.x, w.z, ya[2]);
-                ya[3] = fmaf(h23.y, w.w, ya[3]);
+                hp[j / 2] = bias_relu_bf16x2(v[j], v[j + 1], b.x, b.y);
+                hp[j / 2 + 1] = bias_relu_bf16x2(v[j + 2], v[j + 3], b.z, b.w);
+                ya01 = __ffma2_rn(unpack_bf16(hp[j / 2]), make_float2(w.x, w.y), ya01);
+                ya23 = __ffma2_rn(unpack_bf16(hp[j / 2 + 1]), make_float2(w.z, w.w), ya23);
             }
 #pragma unroll
             for (int c = 0; c < HC; c += 8)
                 st16(sH2, tc::core_off(t, hc0 + c, 1024), make_uint4(hp[c / 2], hp[c / 2 + 1], hp[c / 2 + 2], hp[c / 2 + 3]));
-            s_y[slot][hf][t] = (ya[0] + ya[1]) + (ya[2] + ya[3]);
+            s_y[slot][hf][t] = (ya01.x + ya01.y) + (ya23.x + ya23.y);
             // the previous tile's dX stores have read the [dZ2 | dZ1] tile before it is rewritten below
             if (issuer) asm volatile("cp.async.bulk.wait_group.read 0;" ::: "memory");
             slot_sync(slot);
@@ -361,14 +369,16 @@ __global__ void __launch_bounds__(TRAIN_THREADS, 1) mlp_train_kernel(const Train
             }
 #pragma unroll
             for (int c = 0; c < HC; c += 8) {
-                uint32_t p[4];
-#pragma unroll
-                for (int k = 0; k < 4; k++) {
-                    const float2 h = unpack_bf16(hp[c / 2 + k]);
-                    const int col = hc0 + c + 2 * k;
-                    p[k] = pack_bf16(h.x > 0.f ? dy * w3[col] : 0.f, h.y > 0.f ? dy * w3[col + 1] : 0.f);
-                }
-                st16(sDZ, tc::core_off(t, hc0 + c, Lo::SBO_DZ), make_uint4(p[0], p[1], p[2], p[3]));
+                const float4 wa = *reinterpret_cast<const float4 *>(w3 + hc0 + c);
+                const float4 wb = *reinterpret_cast<const float4 *>(w3 + hc0 + c + 4);
+                const float2 d2 = make_float2(dy, dy);
+                const uint32_t p0 = bf2_bits(__float22bfloat162_rn(__fmul2_rn(d2, make_float2(wa.x, wa.y))));
+                const uint32_t p1 = bf2_bits(__float22bfloat162_rn(__fmul2_rn(d2, make_float2(wa.z, wa.w))));
+                const uint32_t p2 = bf2_bits(__float22bfloat162_rn(__fmul2_rn(d2, make_float2(wb.x, wb.y))));
+                const uint32_t p3 = bf2_bits(__float22bfloat162_rn(__fmul2_rn(d2, make_float2(wb.z, wb.w))));
+                st16(sDZ, tc::core_off(t, hc0 + c, Lo::SBO_DZ),
+                     make_uint4(where_pos(p0, hp[c / 2]), where_pos(p1, hp[c / 2 + 1]), where_pos(p2, hp[c / 2 + 2]),
+                                where_pos(p3, hp[c / 2 + 3])));
             }
         }
         tc::fence_smem_to_async();
@@ -398,14 +408,9 @@ __global__ void __launch_bounds__(TRAIN_THREADS, 1) mlp_train_kernel(const Train
 #pragma unroll
             for (int c = 0; c < HC; c += 8) {
                 const uint4 ha = *reinterpret_cast<const uint4 *>(sH1 + tc::core_off(t, hc0 + c, Lo::SBO_H1));
-                const uint32_t hw[4] = {ha.x, ha.y, ha.z, ha.w};
-                uint32_t p[4];
-#pragma unroll
-                for (int k = 0; k < 4; k++) {
-                    const float2 h = unpack_bf16(hw[k]);
-                    p[k] = pack_bf16(h.x > 0.f ? v[c + 2 * k] : 0.f, h.y > 0.f ? v[c + 2 * k + 1] : 0.f);
-                }
-                st16(sDZ, tc::core_off(t, H + hc0 + c, Lo::SBO_DZ), make_uint4(p[0], p[1], p[2], p[3]));
+                st16(sDZ, tc::core_off(t, H + hc0 + c, Lo::SBO_DZ),
+                     make_uint4(where_pos(pack_bf16(v[c], v[c + 1]), ha.x), where_pos(pack_bf16(v[c + 2], v[c + 3]), ha.y),
+                                where_pos(pack_bf16(v[c + 4], v[c + 5]), ha.z), where_pos(pack_bf16(v[c + 6], v[c + 7]), ha.w)));
             }
         }
         tc::fence_smem_to_async();
