@@ -316,6 +316,9 @@ __global__ void __launch_bounds__(TRAIN_THREADS, 1) mlp_train_kernel(const Train
                                 bias_relu_bf16x2(v[c + 6], v[c + 7], bb.z, bb.w)));
             }
         }
+        // the previous tile's dX stores have read the [dZ2 | dZ1] tile before
+        // epilogue 2 rewrites it (this slot barrier orders the writes behind the wait)
+        if (issuer) asm volatile("cp.async.bulk.wait_group.read 0;" ::: "memory");
         tc::fence_smem_to_async();
         tc::fence_before_sync();
         slot_sync(slot);
@@ -351,9 +354,8 @@ __global__ void __launch_bounds__(TRAIN_THREADS, 1) mlp_train_kernel(const Train
             for (int c = 0; c < HC; c += 8)
                 st16(sH2, tc::core_off(t, hc0 + c, 1024), make_uint4(hp[c / 2], hp[c / 2 + 1], hp[c / 2 + 2], hp[c / 2 + 3]));
             s_y[slot][hf][t] = (ya01.x + ya01.y) + (ya23.x + ya23.y);
-            // the previous tile's dX stores have read the [dZ2 | dZ1] tile before it is rewritten below
-            if (issuer) asm volatile("cp.async.bulk.wait_group.read 0;" ::: "memory");
-            slot_sync(slot);
+            // only the two warps of this lane quarter exchange partial sums
+            asm volatile("bar.sync %0, 64;" ::"r"(3 + 4 * slot + (ws & 3)) : "memory");
             const float y = (s_y[slot][0][t] + s_y[slot][1][t]) + b3;
             const float diff = valid ? (y - tgt) : 0.f;
             const float dy = 2.f * diff * a.inv_n_global;
