@@ -82,8 +82,13 @@ struct Layout {
     static constexpr uint32_t SMEM = SLOTS * BYTES_SLOT + BYTES_W1 + BYTES_W2;
     // TMEM columns (per slot, base = slot * 256)
     static constexpr uint32_t T_ACC = 0, T_DW = 64, T_D3 = 64 + WHX;  // T_D3: [dw3_hi, dw3_lo] accumulators
+    // T_A: the A operand of MMA2 / MMA3 / MMA4 (H1, dZ2, dZ1 in turn: 128 x 64
+    // bf16, two per column) written by the epilogues straight into TMEM, so
+    // those MMAs read only B from shared memory (SS-mode MMAs with N = 64 are
+    // bound by the shared-memory operand reads, A being two thirds of them)
+    static constexpr uint32_t T_A = T_D3 + 16;
     static constexpr uint32_t TMEM_COLS = 512;
-    static_assert(T_D3 + 16 <= 256, "slot TMEM region overflow");
+    static_assert(T_A + H / 2 <= 256, "slot TMEM region overflow");
     static_assert(K0 <= H && BYTES_X <= BYTES_XB, "X tile must fit an h2 buffer");
     static_assert(BYTES_H1 % 1024 == 0 && BYTES_XB % 1024 == 0 && BYTES_SLOT % 1024 == 0, "1 KB aligned tiles");
 };
@@ -165,12 +170,26 @@ __device__ __forceinline__ void tmem_ld_cols(uint32_t taddr, float (&v)[N]) {
     tc::tmem_wait_ld();
 }
 
-template <int K0>
+// A thread's N bf16 of its row of an MMA A operand (N / 2 packed columns)
+// into TMEM, then wait for the writes (the slot barrier follows).
+template <int N>
+__device__ __forceinline__ void store_a_tmem(uint32_t taddr, const uint32_t (&pk)[N / 2]) {
+#pragma unroll
+    for (int c = 0; c < N / 2; c += 8) {
+        uint32_t r[8];
+#pragma unroll
+        for (int j = 0; j < 8; j++) r[j] = pk[c + j];
+        tc::tmem_st8(taddr + c, r);
+    }
+    tc::tmem_wait_st();
+}
+
 // tm_x: 4-D tensor map of x ([N][K0] bf16) as (8 elements, row % 8, 16-byte
 // chunk, row / 8): a box of 128 rows lands in the core-matrix layout
 // (SWIZZLE_NONE, SBO = K0 * 16); rows past N read as zero.  tm_dx: 2-D map
 // of dX ([N][K0] fp32), box 128 rows x 16 columns, 64-byte swizzle; rows
 // past N are not written.  Both encoded per launch (train_api.cu).
+template <int K0>
 __global__ void __launch_bounds__(TRAIN_THREADS, 1) mlp_train_kernel(const TrainArgs a,
                                                                      const __grid_constant__ CUtensorMap tm_x,
                                                                      const __grid_constant__ CUtensorMap tm_dx) {
@@ -306,15 +325,18 @@ __global__ void __launch_bounds__(TRAIN_THREADS, 1) mlp_train_kernel(const Train
             float v[HC];
             tmem_ld_cols<HC>(tm + lane_off + Lo::T_ACC + hc0, v);
 #pragma unroll
+            uint32_t pk[HC / 2];
+#pragma unroll
             for (int c = 0; c < HC; c += 8) {
                 const float4 ba = *reinterpret_cast<const float4 *>(b1 + hc0 + c);
                 const float4 bb = *reinterpret_cast<const float4 *>(b1 + hc0 + c + 4);
-                st16(sH1, tc::core_off(t, hc0 + c, Lo::SBO_H1),
-                     make_uint4(bias_relu_bf16x2(v[c], v[c + 1], ba.x, ba.y),
-                                bias_relu_bf16x2(v[c + 2], v[c + 3], ba.z, ba.w),
-                                bias_relu_bf16x2(v[c + 4], v[c + 5], bb.x, bb.y),
-                                bias_relu_bf16x2(v[c + 6], v[c + 7], bb.z, bb.w)));
+                pk[c / 2] = bias_relu_bf16x2(v[c], v[c + 1], ba.x, ba.y);
+                pk[c / 2 + 1] = bias_relu_bf16x2(v[c + 2], v[c + 3], ba.z, ba.w);
+                pk[c / 2 + 2] = bias_relu_bf16x2(v[c + 4], v[c + 5], bb.x, bb.y);
+                pk[c / 2 + 3] = bias_relu_bf16x2(v[c + 6], v[c + 7], bb.z, bb.w);
+                st16(sH1, tc::core_off(t, hc0 + c, Lo::SBO_H1), make_uint4(pk[c / 2], pk[c / 2 + 1], pk[c / 2 + 2], pk[c / 2 + 3]));
             }
+            store_a_tmem<HC>(tm + lane_off + Lo::T_A + hc0 / 2, pk);
         }
         // the previous tile's dX stores have read the [dZ2 | dZ1] tile before
         // epilogue 2 rewrites it (this slot barrier orders the writes behind the wait)
@@ -327,8 +349,8 @@ __global__ void __launch_bounds__(TRAIN_THREADS, 1) mlp_train_kernel(const Train
         if (issuer) {
 #pragma unroll
             for (int s = 0; s < H / 16; s++)
-                tc::mma_bf16(tm + Lo::T_ACC, tc::sdesc(aH1 + s * 256, 128, Lo::SBO_H1),
-                             tc::sdesc(aW2 + s * 256, 128, Lo::SBO_W2), id_h, s > 0);
+                tc::mma_bf16_ta(tm + Lo::T_ACC, tm + Lo::T_A + 8 * s, tc::sdesc(aW2 + s * 256, 128, Lo::SBO_W2), id_h,
+                                s > 0);
             tc::commit(mbar);
         }
         tc::mbar_wait(mbar, phase); phase ^= 1;
@@ -378,10 +400,13 @@ __global__ void __launch_bounds__(TRAIN_THREADS, 1) mlp_train_kernel(const Train
                 const uint32_t p1 = bf2_bits(__float22bfloat162_rn(__fmul2_rn(d2, make_float2(wa.z, wa.w))));
                 const uint32_t p2 = bf2_bits(__float22bfloat162_rn(__fmul2_rn(d2, make_float2(wb.x, wb.y))));
                 const uint32_t p3 = bf2_bits(__float22bfloat162_rn(__fmul2_rn(d2, make_float2(wb.z, wb.w))));
-                st16(sDZ, tc::core_off(t, hc0 + c, Lo::SBO_DZ),
-                     make_uint4(where_pos(p0, hp[c / 2]), where_pos(p1, hp[c / 2 + 1]), where_pos(p2, hp[c / 2 + 2]),
-                                where_pos(p3, hp[c / 2 + 3])));
+                hp[c / 2] = where_pos(p0, hp[c / 2]);          // h2 is no longer needed: hp takes dZ2
+                hp[c / 2 + 1] = where_pos(p1, hp[c / 2 + 1]);
+                hp[c / 2 + 2] = where_pos(p2, hp[c / 2 + 2]);
+                hp[c / 2 + 3] = where_pos(p3, hp[c / 2 + 3]);
+                st16(sDZ, tc::core_off(t, hc0 + c, Lo::SBO_DZ), make_uint4(hp[c / 2], hp[c / 2 + 1], hp[c / 2 + 2], hp[c / 2 + 3]));
             }
+            store_a_tmem<HC>(tm + lane_off + Lo::T_A + hc0 / 2, hp);
         }
         tc::fence_smem_to_async();
         tc::fence_before_sync();
@@ -392,8 +417,8 @@ __global__ void __launch_bounds__(TRAIN_THREADS, 1) mlp_train_kernel(const Train
         if (issuer) {
 #pragma unroll
             for (int s = 0; s < H / 16; s++)
-                tc::mma_bf16(tm + Lo::T_ACC, tc::sdesc(aDZ + s * 256, 128, Lo::SBO_DZ),
-                             tc::sdesc(aW2 + s * 2 * Lo::SBO_W2, Lo::SBO_W2, 128), id_dh, s > 0);
+                tc::mma_bf16_ta(tm + Lo::T_ACC, tm + Lo::T_A + 8 * s, tc::sdesc(aW2 + s * 2 * Lo::SBO_W2, Lo::SBO_W2, 128),
+                                id_dh, s > 0);
 #pragma unroll
             for (int s = 0; s < TILE / 16; s++)
                 tc::mma_bf16(tm + Lo::T_D3, tc::sdesc(aH2 + s * 2 * 1024, 1024, 128),
@@ -406,14 +431,18 @@ __global__ void __launch_bounds__(TRAIN_THREADS, 1) mlp_train_kernel(const Train
         // ---- epilogue 3: dZ1 = bf16(dH1 * mask1), mask1 = (h1 > 0) from the H1 tile
         {
             float v[HC];
+            uint32_t pk[HC / 2];
             tmem_ld_cols<HC>(tm + lane_off + Lo::T_ACC + hc0, v);
 #pragma unroll
             for (int c = 0; c < HC; c += 8) {
                 const uint4 ha = *reinterpret_cast<const uint4 *>(sH1 + tc::core_off(t, hc0 + c, Lo::SBO_H1));
-                st16(sDZ, tc::core_off(t, H + hc0 + c, Lo::SBO_DZ),
-                     make_uint4(where_pos(pack_bf16(v[c], v[c + 1]), ha.x), where_pos(pack_bf16(v[c + 2], v[c + 3]), ha.y),
-                                where_pos(pack_bf16(v[c + 4], v[c + 5]), ha.z), where_pos(pack_bf16(v[c + 6], v[c + 7]), ha.w)));
+                pk[c / 2] = where_pos(pack_bf16(v[c], v[c + 1]), ha.x);
+                pk[c / 2 + 1] = where_pos(pack_bf16(v[c + 2], v[c + 3]), ha.y);
+                pk[c / 2 + 2] = where_pos(pack_bf16(v[c + 4], v[c + 5]), ha.z);
+                pk[c / 2 + 3] = where_pos(pack_bf16(v[c + 6], v[c + 7]), ha.w);
+                st16(sDZ, tc::core_off(t, H + hc0 + c, Lo::SBO_DZ), make_uint4(pk[c / 2], pk[c / 2 + 1], pk[c / 2 + 2], pk[c / 2 + 3]));
             }
+            store_a_tmem<HC>(tm + lane_off + Lo::T_A + hc0 / 2, pk);
         }
         tc::fence_smem_to_async();
         tc::fence_before_sync();
@@ -424,8 +453,8 @@ __global__ void __launch_bounds__(TRAIN_THREADS, 1) mlp_train_kernel(const Train
         if (issuer) {
 #pragma unroll
             for (int s = 0; s < H / 16; s++)
-                tc::mma_bf16(tm + Lo::T_ACC, tc::sdesc(aDZ + (H / 8) * 128 + s * 256, 128, Lo::SBO_DZ),
-                             tc::sdesc(aW1 + s * 2 * Lo::SBO_W1, Lo::SBO_W1, 128), id_dx, s > 0);
+                tc::mma_bf16_ta(tm + Lo::T_ACC, tm + Lo::T_A + 8 * s, tc::sdesc(aW1 + s * 2 * Lo::SBO_W1, Lo::SBO_W1, 128),
+                                id_dx, s > 0);
 #pragma unroll
             for (int s = 0; s < TILE / 16; s++)
             {

@@ -22,7 +22,8 @@ __global__ void __launch_bounds__(128) probe(const __nv_bfloat16 *A, const __nv_
     uint8_t *sB = smem + M * K * 2;     // N*K*2 bytes
     const int t = threadIdx.x, warp = t >> 5;
     // ---- stage operands into core-matrix layouts
-    for (int i = t; i < M * K; i += blockDim.x) {
+    // a_mn == 2: A[128][K] goes to TMEM (lane = row, two bf16 per column)
+    for (int i = t; i < M * K && a_mn != 2; i += blockDim.x) {
         int m, k;
         uint32_t off;
         if (!a_mn) { m = i / K; k = i % K; off = core_off(m, k, (K / 8) * 128); }
@@ -43,15 +44,34 @@ __global__ void __launch_bounds__(128) probe(const __nv_bfloat16 *A, const __nv_
     __syncthreads();
     fence_after_sync();
     const uint32_t d = tbase;
+    const uint32_t a_col = 160;        // A in TMEM (a_mn == 2): columns [160, 160 + K/2)
+    if (a_mn == 2) {
+        for (int c0 = 0; c0 < K / 2; c0 += 8) {
+            uint32_t r[8];
+            for (int j = 0; j < 8; j++) {
+                const int k = 2 * (c0 + j);
+                __nv_bfloat162 v;
+                v.x = A[t * K + k];
+                v.y = A[t * K + k + 1];
+                r[j] = *reinterpret_cast<uint32_t *>(&v);
+            }
+            tmem_st8(d + ((uint32_t)(warp * 32) << 16) + a_col + c0, r);
+        }
+        tmem_wait_st();
+        fence_before_sync();
+        __syncthreads();
+        fence_after_sync();
+    }
     if (t == 0) {
-        const uint32_t idesc = idesc_bf16_f32(M, N, a_mn, b_mn);
+        const uint32_t idesc = idesc_bf16_f32(M, N, a_mn == 1, b_mn);
         for (int s = 0; s < K / 16; s++) {
             uint64_t ad, bd;
             if (!a_mn) ad = sdesc(smem_u32(sA) + s * 256, 128, (K / 8) * 128);
             else ad = sdesc(smem_u32(sA) + s * 2 * (M / 8) * 128, (M / 8) * 128, 128);
             if (!b_mn) bd = sdesc(smem_u32(sB) + s * 256, 128, (K / 8) * 128);
             else bd = sdesc(smem_u32(sB) + s * 2 * (N / 8) * 128, (N / 8) * 128, 128);
-            mma_bf16(d, ad, bd, idesc, s > 0);
+            if (a_mn == 2) mma_bf16_ta(d, d + a_col + 8 * s, bd, idesc, s > 0);
+            else mma_bf16(d, ad, bd, idesc, s > 0);
         }
         commit(&bar);
     }

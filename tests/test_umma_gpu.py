@@ -26,13 +26,14 @@ def probe_lib():
 
 
 @pytest.mark.parametrize("N,K,a_mn,b_mn", [(64, 64, 0, 0), (64, 32, 0, 0), (32, 64, 0, 0), (144, 128, 1, 1),
-                                           (112, 128, 1, 1), (64, 64, 0, 1), (64, 64, 1, 0)])
+                                           (112, 128, 1, 1), (64, 64, 0, 1), (64, 64, 1, 0),
+                                           (64, 64, 2, 0), (64, 64, 2, 1), (32, 64, 2, 1), (64, 16, 2, 0)])
 def test_umma_gemm(N, K, a_mn, b_mn):
     L = probe_lib()
     g = torch.Generator("cuda").manual_seed(N * 1000 + K)
     A = torch.randn(128, K, device="cuda", generator=g).bfloat16()
     B = torch.randn(N, K, device="cuda", generator=g).bfloat16()
-    Ain = A.t().contiguous() if a_mn else A
+    Ain = A.t().contiguous() if a_mn == 1 else A   # a_mn == 2: A read from TMEM
     Bin = B.t().contiguous() if b_mn else B
     D = torch.empty(128, N, device="cuda")
     assert L.umma_probe(Ain.data_ptr(), Bin.data_ptr(), D.data_ptr(), N, K, a_mn, b_mn) == 0
