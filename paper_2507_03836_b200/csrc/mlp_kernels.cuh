@@ -73,9 +73,7 @@ struct Layout {
     static constexpr uint32_t BYTES_XB = TILE * H * 2;    // one X / h2 buffer (h2: SBO 1024; K0 <= H)
     static constexpr uint32_t BYTES_DZ = TILE * 2 * H * 2;
     static constexpr uint32_t BYTES_DY = TILE * 16 * 2;   // [dy_hi, dy_lo, 0 x 14] per sample (SBO 256)
-    // the dw3 MMA reads A rows 64..127 past the h2 tile (results discarded):
-    // 1 KB past the second buffer is the DZ tile, keep 1 KB of slack after DY
-    static constexpr uint32_t BYTES_SLOT = BYTES_H1 + 2 * BYTES_XB + BYTES_DZ + BYTES_DY + 1024;
+    static constexpr uint32_t BYTES_SLOT = BYTES_H1 + 2 * BYTES_XB + BYTES_DZ + BYTES_DY;
     static constexpr uint32_t BYTES_W1 = H * K0 * 2;
     static constexpr uint32_t BYTES_W2 = H * H * 2;
     static constexpr int SLOTS = 2;
@@ -279,7 +277,7 @@ __global__ void __launch_bounds__(TRAIN_THREADS, 1) mlp_train_kernel(const Train
     constexpr uint32_t id_dx = tc::idesc_bf16_f32(128, K0, false, true);     // B = W1 MN-major
     constexpr uint32_t id_dw = tc::idesc_bf16_f32(128, Lo::WH1, true, true); // both MN-major: [H1 | 1] block
     constexpr uint32_t id_dwx = tc::idesc_bf16_f32(128, K0, true, true);     // X block
-    constexpr uint32_t id_d3 = tc::idesc_bf16_f32(128, 16, true, true);      // dw3: H2^T . [dy_hi dy_lo]
+    constexpr uint32_t id_d3 = tc::idesc_bf16_f32(64, 16, true, true);       // dw3: H2^T . [dy_hi dy_lo], M = 64
 
     uint32_t phase = 0;
     float db3_acc = 0.f, loss_acc = 0.f;
@@ -413,7 +411,8 @@ __global__ void __launch_bounds__(TRAIN_THREADS, 1) mlp_train_kernel(const Train
         slot_sync(slot);
         tc::fence_after_sync();
         // ---- MMA3: dH1 = dZ2 . W2 ; MMA6: [dw3_hi dw3_lo] += H2^T . [dy_hi dy_lo]
-        // (MMA6: M = 128 with A rows 64..127 reading past the h2 tile -- discarded)
+        // (MMA6: M = 64, hidden unit j in TMEM lane 32 (j / 16) + j % 16; was
+        // M = 128 with A rows 64..127 read past the h2 tile and discarded)
         if (issuer) {
 #pragma unroll
             for (int s = 0; s < H / 16; s++)
@@ -538,14 +537,15 @@ __global__ void __launch_bounds__(TRAIN_THREADS, 1) mlp_train_kernel(const Train
                 else g[off_b1(K0) + (r - H)] = v[0];
             }
         }
-        // dw3[r] = hi + lo columns of the D3 accumulator, rows 0..63
+        // dw3[j] = hi + lo columns of the D3 accumulator (M = 64 layout: j in
+        // lane 32 (j / 16) + j % 16)
         if (hf == 0) {
             float d3[16] = {0.f};
             if (my_tiles > 0) {
                 tc::tmem_ld16(tm + lane_off + Lo::T_D3, d3);
                 tc::tmem_wait_ld();
             }
-            if (r < H) g[off_w3(K0) + r] = d3[0] + d3[1];
+            if ((r & 31) < 16) g[off_w3(K0) + (r >> 5) * 16 + (r & 15)] = d3[0] + d3[1];
         }
     }
     // db3 and loss (column half 0 holds them): warp reduce, then one atomic per CTA
