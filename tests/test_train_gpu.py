@@ -84,6 +84,38 @@ def test_train_fwd_bwd_cfg5_shape_multi_tile():
     check_fwd_bwd(cfg, tr, coords, target, N)
 
 
+@pytest.mark.parametrize("F,L,N", [(2, 16, 1), (4, 16, 129), (2, 8, 255), (4, 4, 7)])
+def test_mlp_fwd_bwd_ragged_tiles(F, L, N):
+    """Tile edges of the TMA paths: one sample, one full tile + one row, a
+    tile short of one row, fewer rows than one 8-row group (the X tensor map
+    zero-fills row groups past N; rows past N inside the last group are
+    zeroed by the kernel; the dX tensor map clips rows past N)."""
+    cfg = small_cfg(F, L)
+    enc, tr, coords, target = make(cfg, N, seed=F * 10 + N)
+    check_fwd_bwd(cfg, tr, coords, target, N)
+
+
+def test_mlp_fwd_bwd_after_a_larger_batch():
+    """A trainer's workspace keeps the previous call's encoder output and dX
+    rows past the current N: a small batch after a large one must not read
+    them (per-launch tensor maps sized to N), and its dX rows past N are
+    left alone."""
+    cfg = small_cfg(2, 16)
+    g = W.rng(77)
+    enc = fh.Encoder(cfg.levels, cfg.F, cfg.table_dtype, cfg.cap)
+    tr = fh.Trainer(enc, W.draw_table(g, enc.entries, cfg.F, "f32"), W.draw_mlp(g, W.MLPConfig((32, 64, 64, 1))), 5000)
+    big = W.draw_coords(g, 5000)
+    tr.fwd_bwd(torch.from_numpy(big).cuda(), torch.from_numpy(g.random(5000, dtype=np.float32)).cuda())
+    torch.cuda.synchronize()
+    dx_big = tr.dx(5000).clone()
+    N = 301
+    coords = W.draw_coords(g, N)
+    target = g.random(N, dtype=np.float32)
+    check_fwd_bwd(cfg, tr, coords, target, N)
+    # rows past N (also those inside the last 128-row tile) are clipped by the dX store
+    assert torch.equal(tr.dx(5000)[N:], dx_big[N:])
+
+
 def check_fwd_bwd(cfg, tr, coords, target, N, table_grad=True):
     c, t = torch.from_numpy(coords).cuda(), torch.from_numpy(target).cuda()
     n_global = N + 17  # exercise the 1/N_global scaling
