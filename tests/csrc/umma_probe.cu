@@ -101,7 +101,7 @@ extern "C" int umma_probe(const void *A, const void *B, float *D, int N, int K, 
 // (b_mn: [K][N]); D read back from all 128 TMEM lanes x N columns into
 // Dall[128][N] (lanes the MMA does not write keep the 0 they were set to).
 __global__ void __launch_bounds__(128) probe64(const __nv_bfloat16 *A, const __nv_bfloat16 *B, float *Dall, int N,
-                                               int K, int a_mn, int b_mn) {
+                                               int K, int a_mn, int b_mn, int lane0) {
     extern __shared__ __align__(1024) uint8_t smem[];
     __shared__ uint64_t bar;
     __shared__ uint32_t tbase;
@@ -146,7 +146,7 @@ __global__ void __launch_bounds__(128) probe64(const __nv_bfloat16 *A, const __n
             else ad = sdesc(smem_u32(sA) + s * 2 * (M / 8) * 128, (M / 8) * 128, 128);
             if (!b_mn) bd = sdesc(smem_u32(sB) + s * 256, 128, (K / 8) * 128);
             else bd = sdesc(smem_u32(sB) + s * 2 * (N / 8) * 128, (N / 8) * 128, 128);
-            mma_bf16(d, ad, bd, idesc, 1);
+            mma_bf16(d + ((uint32_t)lane0 << 16), ad, bd, idesc, 1);
         }
         commit(&bar);
     }
@@ -164,10 +164,12 @@ __global__ void __launch_bounds__(128) probe64(const __nv_bfloat16 *A, const __n
     if (warp == 0) tmem_dealloc(d, 256);
 }
 
-extern "C" int umma_probe64(const void *A, const void *B, float *Dall, int N, int K, int a_mn, int b_mn) {
+// lane0: lane field of the D address (0, or 16 for the other half of the
+// lanes when the M = 64 layout allows it)
+extern "C" int umma_probe64(const void *A, const void *B, float *Dall, int N, int K, int a_mn, int b_mn, int lane0) {
     const int smem = (64 * K + N * K) * 2;
     if (cudaFuncSetAttribute(probe64, cudaFuncAttributeMaxDynamicSharedMemorySize, smem) != cudaSuccess) return -1;
-    probe64<<<1, 128, smem>>>((const __nv_bfloat16 *)A, (const __nv_bfloat16 *)B, Dall, N, K, a_mn, b_mn);
+    probe64<<<1, 128, smem>>>((const __nv_bfloat16 *)A, (const __nv_bfloat16 *)B, Dall, N, K, a_mn, b_mn, lane0);
     if (cudaGetLastError() != cudaSuccess) return -2;
     return cudaDeviceSynchronize() == cudaSuccess ? 0 : -3;
 }

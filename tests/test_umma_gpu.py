@@ -43,21 +43,24 @@ def test_umma_gemm(N, K, a_mn, b_mn):
 
 
 @pytest.mark.parametrize("N,K,a_mn,b_mn", [(16, 128, 1, 1), (64, 64, 0, 0)])
-def test_umma_m64_lane_layout(N, K, a_mn, b_mn):
-    """M = 64 (cta_group::1): D row i lands in TMEM lane 32 (i // 16) + i % 16
-    (the layout mlp_train_kernel's dw3 MMA relies on); the other lanes are
+@pytest.mark.parametrize("lane0", [0, 16])
+def test_umma_m64_lane_layout(N, K, a_mn, b_mn, lane0):
+    """M = 64 (cta_group::1): D row i lands in TMEM lane lane0 + 32 (i // 16)
+    + i % 16, lane0 = the lane field of the D address (0 or 16): two M = 64
+    MMAs share TMEM columns in the two lane halves (mlp_train_kernel's
+    weight-gradient and dw3 accumulators rely on it); the other lanes are
     not written."""
     L = probe_lib()
-    L.umma_probe64.argtypes = [ctypes.c_void_p] * 3 + [ctypes.c_int] * 4
+    L.umma_probe64.argtypes = [ctypes.c_void_p] * 3 + [ctypes.c_int] * 5
     g = torch.Generator("cuda").manual_seed(N + K)
     A = torch.randn(64, K, device="cuda", generator=g).bfloat16()
     B = torch.randn(N, K, device="cuda", generator=g).bfloat16()
     Ain = A.t().contiguous() if a_mn else A
     Bin = B.t().contiguous() if b_mn else B
     D = torch.full((128, N), 7.0, device="cuda")
-    assert L.umma_probe64(Ain.data_ptr(), Bin.data_ptr(), D.data_ptr(), N, K, a_mn, b_mn) == 0
+    assert L.umma_probe64(Ain.data_ptr(), Bin.data_ptr(), D.data_ptr(), N, K, a_mn, b_mn, lane0) == 0
     ref = A.float() @ B.float().t()
-    lanes = torch.tensor([32 * (i // 16) + i % 16 for i in range(64)], device="cuda")
+    lanes = torch.tensor([lane0 + 32 * (i // 16) + i % 16 for i in range(64)], device="cuda")
     err = (D[lanes] - ref).abs().max().item()
     assert err <= 1e-4 * ref.abs().max().item() + 1e-5, err
     other = torch.ones(128, dtype=torch.bool, device="cuda")
