@@ -186,7 +186,9 @@ uint64_t fh_mlp_param_count(const fh_mlp_desc *m) {
 size_t fh_train_workspace_size(fh_encoder enc, const fh_mlp_desc *m, int64_t max_batch) {
     if (!enc || !m || max_batch < 0) return 0;
     const size_t K0 = (size_t)m->n_in;
-    return align_up((size_t)max_batch * K0 * 2, 256) + align_up((size_t)max_batch * K0 * 4, 256) + 256 +
+    // the encoder-output rows are sized to whole 8-row groups: the MLP
+    // kernel's X tensor map reads the last group whole (rows past N zeroed)
+    return align_up(align_up((size_t)max_batch, 8) * K0 * 2, 256) + align_up((size_t)max_batch * K0 * 4, 256) + 256 +
            partial_bytes(enc, m->n_in);
 }
 
@@ -221,7 +223,7 @@ fh_status fh_trainer_create(fh_encoder enc, const fh_mlp_desc *m, const fh_train
     tr->n_sm = enc->n_sm;
     char *w = reinterpret_cast<char *>(b->workspace);
     tr->enc_out = reinterpret_cast<__nv_bfloat16 *>(w);
-    w += align_up((size_t)max_batch * tr->K0 * 2, 256);
+    w += align_up(align_up((size_t)max_batch, 8) * tr->K0 * 2, 256);
     tr->dx = reinterpret_cast<float *>(w);
     w += align_up((size_t)max_batch * tr->K0 * 4, 256);
     tr->flag = reinterpret_cast<int *>(w);

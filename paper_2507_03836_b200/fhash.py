@@ -498,7 +498,7 @@ class Trainer:
 
     def dx(self, N):
         import torch
-        off = (self.max_batch * self.K0 * 2 + 255) // 256 * 256
+        off = ((self.max_batch + 7) // 8 * 8 * self.K0 * 2 + 255) // 256 * 256   # encoder rows in whole 8-row groups
         return self.workspace[off: off + N * self.K0 * 4].view(torch.float32).view(N, self.K0)
 
     def fwd_bwd(self, coords, target, n_global=None, stream=None):
