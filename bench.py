@@ -560,7 +560,7 @@ def train_step_bench(fh, torch, W, which, rank, world, dist, steps, warmup, dp_m
     enc = fh.Encoder(cfg.levels, cfg.F, cfg.table_dtype, cfg.cap)
     gen = torch.Generator("cuda").manual_seed(0)           # identical init on every rank
     table0 = (torch.rand((enc.entries, cfg.F), device="cuda", generator=gen) * 2 - 1) * 1e-4
-    peer = world > 1 and dp_mode == "peer"
+    peer = world > 1 and dp_mode in ("peer", "multicast")
     fused = world > 1 and dp_mode == "fused"
     tr = fh.Trainer(enc, table0, W.draw_mlp(W.rng(0), mlp), n_local, world=world,
                     alloc=dp.symm_alloc if peer else None)
@@ -581,6 +581,13 @@ def train_step_bench(fh, torch, W, which, rank, world, dist, steps, warmup, dp_m
         dist.broadcast_object_list(uid, src=0)
         comm = fh.NcclComm(uid[0], world, rank)
         tr.set_comm(comm)
+    elif peer and dp_mode == "multicast":
+        # --dp multicast: the same through an NVLS multicast object (multimem.ld_reduce / multimem.st);
+        # falls back to the peer-pointer form when the system gives torch no multicast object
+        try:
+            sdp = dp.MulticastShardedDP(tr)
+        except ValueError:
+            sdp = dp.PeerShardedDP(tr)
     elif peer:
         sdp = dp.PeerShardedDP(tr)     # --dp peer: fused reduce + Adam + all-gather over NVLink peer memory
     elif world > 1:
@@ -693,6 +700,8 @@ def train_step_bench(fh, torch, W, which, rank, world, dist, steps, warmup, dp_m
                      "adam_and_gather": phase[3]},
         "dp": ("fused in the library (fh_trainer_set_comm): per-level-group ncclReduceScatter overlapped with the "
                "backward + sharded Adam + in-place fp16 ncclAllGather" if comm is not None else
+               "per-level-group NVLS multimem.ld_reduce + Adam + multimem.st of the fp16 shadow "
+               "(fh_train_apply_multicast)" if isinstance(sdp, dp.MulticastShardedDP) else
                "per-level-group fused reduce + Adam + shadow broadcast over NVLink peer memory (fh_train_apply_peers)"
                if isinstance(sdp, dp.PeerShardedDP) else
                "per-backward-launch reduce-scatter overlapped with the backward + sharded Adam + all-gather (NCCL)"
@@ -1098,10 +1107,11 @@ def main():
     ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--no-train", action="store_true", help="skip the train_step (cfg3 / cfg5) sub-benchmarks")
-    ap.add_argument("--dp", default="nccl", choices=["nccl", "fused", "peer"],
+    ap.add_argument("--dp", default="nccl", choices=["nccl", "fused", "peer", "multicast"],
                     help="N>1 gradient path: NCCL reduce-scatter overlapped with the backward from Python (default), "
                          "the same exchange driven inside the library (fused, fh_trainer_set_comm), or the fused "
-                         "peer-memory reduce + Adam + all-gather kernel (torch symmetric memory)")
+                         "peer-memory reduce + Adam + all-gather kernel (torch symmetric memory), or that step through "
+                         "an NVLS multicast object (multimem.ld_reduce / multimem.st; falls back to peer without one)")
     args = ap.parse_args()
     if "WORLD_SIZE" not in os.environ and (args.gpus or 1) > 1:
         sys.exit(spawn_ranks(args.gpus, sys.argv[1:]))

@@ -372,6 +372,29 @@ fh_status fh_train_apply_peers(fh_trainer tr, int W, const float *const *peer_ta
                                const int64_t *begin, const int64_t *end, const int *broadcast, int with_mlp,
                                int new_step, fh_stream stream);
 
+/* fh_train_apply_multicast: the same step through an NVLS multicast object
+ * ("multimem.ld_reduce of a shard from an NVLS
+ * multicast buffer, Adam in registers, then multimem.st of the fp16 shard
+ * to all peers").  mc_table_grad, mc_table_shadow, mc_mlp_grad are the
+ * MULTICAST addresses of the group's flat table grad buffer [entries*F]
+ * f32, fp16 table shadow and MLP grad buffer (a multicast object bound to
+ * the same buffer on every rank: torch symmetric memory's multicast
+ * pointer, or cuMulticastCreate + cuMulticastBindMem; 16-byte aligned
+ * grads, 8-byte aligned shadow).  Each element's gradient is ONE
+ * multimem.ld_reduce (.add.f32: the sum over the ranks, formed by the
+ * NVSwitch); broadcast ranges store the fp16 shadow with ONE multimem.st
+ * into every rank's shadow (in f16x2 pairs: broadcast ranges have even
+ * begin and end), replicated ranges (and the MLP) store locally
+ * -- replicas stay identical when every rank receives the same reduced
+ * value.  Same range / broadcast / with_mlp / new_step / ordering contract
+ * as fh_train_apply_peers (the caller orders the call after every rank's
+ * backward and zeroes nothing).  Errors: FH_E_ARG (NULL / misaligned
+ * address, bad ranges), FH_E_STATE (no fp16 shadow, first call without
+ * new_step). */
+fh_status fh_train_apply_multicast(fh_trainer tr, const float *mc_table_grad, void *mc_table_shadow,
+                                   const float *mc_mlp_grad, int n, const int64_t *begin, const int64_t *end,
+                                   const int *broadcast, int with_mlp, int new_step, fh_stream stream);
+
 /* ---- the fused data-parallel form (SURVEY.md §8(b) "nccl_comm", §8(e))
  * The library drives the gradient exchange itself with NCCL: the
  * libnccl.so.2 the process already loaded (torch's; resolved with dlopen

@@ -194,7 +194,6 @@ __global__ void __launch_bounds__(TRAIN_THREADS, 1) mlp_train_kernel(const Train
     using Lo = Layout<K0>;
     constexpr int HC = H / 2;            // hidden columns per thread
     constexpr int XC = K0 / 2;           // X / dX columns per thread
-    constexpr int XQ = K0 / 8;           // 16-byte chunks of an X row
     extern __shared__ __align__(1024) uint8_t smem[];
     uint8_t *sW1 = smem;
     uint8_t *sW2 = sW1 + Lo::BYTES_W1;
@@ -322,7 +321,6 @@ __global__ void __launch_bounds__(TRAIN_THREADS, 1) mlp_train_kernel(const Train
         {
             float v[HC];
             tmem_ld_cols<HC>(tm + lane_off + Lo::T_ACC + hc0, v);
-#pragma unroll
             uint32_t pk[HC / 2];
 #pragma unroll
             for (int c = 0; c < HC; c += 8) {
@@ -718,6 +716,107 @@ __global__ void __launch_bounds__(256) adam_peers_kernel(const __grid_constant__
         float g = 0.f;
         for (int r = 0; r < P.W; r++) g += G[r][off + i];   // ranks in order: same sum on every rank
         update(i, g);
+    }
+}
+
+// ------------------------------------------------ fused DP step over NVLS
+// The same reduce-scatter + Adam + all-gather through an NVLS multicast
+// object (SURVEY.md §8(e) item 3 as written): the gradient of an element is
+// ONE multimem.ld_reduce of its multicast address (the sum over every
+// rank's buffer, formed by the NVSwitch), and the fp16 shadow of a
+// broadcast range is ONE multimem.st to the multicast address (written into
+// every rank's shadow).  Replicated ranges (every rank updates them) store
+// the local shadow only.
+struct McArgs {
+    const float *g;                // multicast address of the flat table grad buffer
+    __half *sh;                    // multicast address of the fp16 table shadow
+    const float *mg;               // multicast address of the MLP grads
+    int64_t off[kMaxAdamSeg];      // element offset of segment i in the multicast buffers
+    int src[kMaxAdamSeg];          // 0: table grads, 1: MLP grads
+    int bcast[kMaxAdamSeg];        // 1: multimem.st the fp16 shadow to every rank
+};
+
+__device__ __forceinline__ float4 mc_ld_reduce4(const float *p) {
+    float4 v;
+    asm volatile("multimem.ld_reduce.relaxed.sys.global.add.v4.f32 {%0, %1, %2, %3}, [%4];"
+                 : "=f"(v.x), "=f"(v.y), "=f"(v.z), "=f"(v.w)
+                 : "l"(p)
+                 : "memory");
+    return v;
+}
+__device__ __forceinline__ float mc_ld_reduce(const float *p) {
+    float v;
+    asm volatile("multimem.ld_reduce.relaxed.sys.global.add.f32 %0, [%1];" : "=f"(v) : "l"(p) : "memory");
+    return v;
+}
+// (multimem.st has no 16-bit form: the fp16 shadow goes out as f16x2 pairs)
+__device__ __forceinline__ void mc_st8(void *p, uint32_t a, uint32_t b) {   // 4 fp16 to every rank
+    asm volatile("multimem.st.relaxed.sys.global.v2.f16x2 [%0], {%1, %2};" ::"l"(p), "r"(a), "r"(b) : "memory");
+}
+__device__ __forceinline__ void mc_st4(void *p, uint32_t a) {               // 2 fp16 to every rank
+    asm volatile("multimem.st.relaxed.sys.global.f16x2 [%0], %1;" ::"l"(p), "r"(a) : "memory");
+}
+
+__global__ void __launch_bounds__(256) adam_multicast_kernel(const __grid_constant__ AdamArgs A,
+                                                             const __grid_constant__ McArgs M) {
+    int si = 0;
+    while (si + 1 < A.nseg && (int64_t)blockIdx.x >= A.block0[si + 1]) si++;
+    const AdamSeg &s = A.seg[si];
+    const int64_t b = (int64_t)blockIdx.x - A.block0[si];
+    const int64_t nb = A.block0[si + 1] - A.block0[si];
+    const float *G = (M.src[si] ? M.mg : M.g) + M.off[si];
+    const bool bc = M.bcast[si] != 0 && s.kind == 1;
+    __half *msh = M.sh + M.off[si];
+    auto one = [&](int64_t i, float g) -> float {   // the new master; stores the local shadow unless broadcast
+        const float m = fmaf(A.b1, s.m[i], A.omb1 * g);
+        const float v = fmaf(A.b2, s.v[i], A.omb2 * g * g);
+        const float p = s.p[i] - A.lr * (m * A.c1) / (sqrtf(v * A.c2) + A.eps);
+        s.m[i] = m; s.v[i] = v; s.p[i] = p;
+        if (s.kind == 2) reinterpret_cast<__nv_bfloat16 *>(s.shadow)[i] = __float2bfloat16_rn(p);
+        else if (s.kind == 1 && !bc) reinterpret_cast<__half *>(s.shadow)[i] = __float2half_rn(p);
+        return p;
+    };
+    // 4 elements per thread when the segment and its multicast offset allow
+    // 16-byte (grads) / 8-byte (shadow) accesses; else one at a time
+    const bool vec = s.vec && (M.off[si] % 4) == 0;
+    const int64_t n4 = vec ? s.n / 4 : 0;
+    for (int64_t q = b * blockDim.x + threadIdx.x; q < n4; q += nb * blockDim.x) {
+        const float4 g = mc_ld_reduce4(G + 4 * q);
+        float4 m = reinterpret_cast<const float4 *>(s.m)[q];
+        float4 v = reinterpret_cast<const float4 *>(s.v)[q];
+        float4 p = reinterpret_cast<const float4 *>(s.p)[q];
+        float gg[4] = {g.x, g.y, g.z, g.w}, mm[4] = {m.x, m.y, m.z, m.w};
+        float vv[4] = {v.x, v.y, v.z, v.w}, pp[4] = {p.x, p.y, p.z, p.w};
+#pragma unroll
+        for (int k = 0; k < 4; k++) {
+            mm[k] = fmaf(A.b1, mm[k], A.omb1 * gg[k]);
+            vv[k] = fmaf(A.b2, vv[k], A.omb2 * gg[k] * gg[k]);
+            pp[k] = pp[k] - A.lr * (mm[k] * A.c1) / (sqrtf(vv[k] * A.c2) + A.eps);
+        }
+        reinterpret_cast<float4 *>(s.m)[q] = make_float4(mm[0], mm[1], mm[2], mm[3]);
+        reinterpret_cast<float4 *>(s.v)[q] = make_float4(vv[0], vv[1], vv[2], vv[3]);
+        reinterpret_cast<float4 *>(s.p)[q] = make_float4(pp[0], pp[1], pp[2], pp[3]);
+        if (s.kind == 1) {
+            __half2 h0 = __floats2half2_rn(pp[0], pp[1]), h1 = __floats2half2_rn(pp[2], pp[3]);
+            const uint32_t u0 = *reinterpret_cast<uint32_t *>(&h0), u1 = *reinterpret_cast<uint32_t *>(&h1);
+            if (bc) mc_st8(msh + 4 * q, u0, u1);
+            else reinterpret_cast<uint2 *>(s.shadow)[q] = make_uint2(u0, u1);
+        } else if (s.kind == 2) {
+            __nv_bfloat162 h0 = __floats2bfloat162_rn(pp[0], pp[1]), h1 = __floats2bfloat162_rn(pp[2], pp[3]);
+            uint2 u;
+            u.x = *reinterpret_cast<uint32_t *>(&h0);
+            u.y = *reinterpret_cast<uint32_t *>(&h1);
+            reinterpret_cast<uint2 *>(s.shadow)[q] = u;
+        }
+    }
+    if (bc) {   // broadcast scalar path: element pairs (even offsets and lengths, checked by the host)
+        for (int64_t i = 4 * n4 + 2 * (b * blockDim.x + threadIdx.x); i < s.n; i += 2 * nb * blockDim.x) {
+            const float p0 = one(i, mc_ld_reduce(G + i)), p1 = one(i + 1, mc_ld_reduce(G + i + 1));
+            __half2 h = __floats2half2_rn(p0, p1);
+            mc_st4(msh + i, *reinterpret_cast<uint32_t *>(&h));
+        }
+    } else {
+        for (int64_t i = 4 * n4 + b * blockDim.x + threadIdx.x; i < s.n; i += nb * blockDim.x) one(i, mc_ld_reduce(G + i));
     }
 }
 

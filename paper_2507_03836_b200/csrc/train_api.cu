@@ -659,6 +659,90 @@ fh_status fh_train_apply_peers(fh_trainer tr, int W, const float *const *peer_ta
     return cuda_check(cudaGetLastError(), "adam_peers_kernel launch");
 }
 
+fh_status fh_train_apply_multicast(fh_trainer tr, const float *mc_table_grad, void *mc_table_shadow,
+                                   const float *mc_mlp_grad, int n, const int64_t *begin, const int64_t *end,
+                                   const int *broadcast, int with_mlp, int new_step, fh_stream stream) {
+    using fh::mlp::AdamArgs;
+    using fh::mlp::AdamSeg;
+    using fh::mlp::McArgs;
+    g_err[0] = 0;
+    if (!tr) return fail(FH_E_ARG, "fh_train_apply_multicast: NULL trainer");
+    if (!tr->b.table_shadow) return fail(FH_E_STATE, "fh_train_apply_multicast: needs an fp16 table shadow");
+    if (n < 0 || n + (with_mlp ? 1 : 0) > fh::mlp::kMaxAdamSeg || (n > 0 && (!begin || !end || !broadcast)))
+        return fail(FH_E_ARG, "fh_train_apply_multicast: bad range list (n = %d)", n);
+    if (!mc_table_grad || !mc_table_shadow || (with_mlp && !mc_mlp_grad))
+        return fail(FH_E_ARG, "fh_train_apply_multicast: NULL multicast address");
+    if (!aligned(mc_table_grad, 16) || !aligned(mc_table_shadow, 8) || (with_mlp && !aligned(mc_mlp_grad, 16)))
+        return fail(FH_E_ARG, "fh_train_apply_multicast: misaligned multicast address");
+    const int64_t nt = (int64_t)(tr->enc->entries * (uint64_t)tr->enc->F);
+    for (int i = 0; i < n; i++)
+        if (begin[i] < 0 || end[i] < begin[i] || end[i] > nt)
+            return fail(FH_E_ARG, "fh_train_apply_multicast: range %d outside the table", i);
+        else if (broadcast[i] && ((begin[i] | end[i]) & 1))
+            return fail(FH_E_ARG, "fh_train_apply_multicast: broadcast range %d not in whole fp16 pairs", i);
+    if (new_step) tr->step += 1;
+    if (tr->step < 1) return fail(FH_E_STATE, "fh_train_apply_multicast: first call of a step must set new_step");
+    const double t = (double)tr->step;
+    AdamArgs A;
+    McArgs M;
+    memset(&A, 0, sizeof(A));
+    memset(&M, 0, sizeof(M));
+    A.lr = tr->adam.lr;
+    A.b1 = tr->adam.beta1;
+    A.b2 = tr->adam.beta2;
+    A.eps = tr->adam.eps;
+    A.omb1 = (float)(1.0 - (double)tr->adam.beta1);
+    A.omb2 = (float)(1.0 - (double)tr->adam.beta2);
+    A.c1 = (float)(1.0 / (1.0 - std::pow((double)tr->adam.beta1, t)));
+    A.c2 = (float)(1.0 / (1.0 - std::pow((double)tr->adam.beta2, t)));
+    M.g = mc_table_grad;
+    M.sh = reinterpret_cast<__half *>(mc_table_shadow);
+    M.mg = with_mlp ? mc_mlp_grad : nullptr;
+    const int64_t cap = (int64_t)tr->n_sm * 16;
+    int64_t blocks = 0;
+    int k = 0;
+    auto add = [&](AdamSeg g, int64_t off, int src, int bc) {
+        if (g.n <= 0) return;
+        int64_t want = (g.n + 256 * 4 - 1) / (256 * 4);
+        if (want > cap) want = cap;
+        if (want < 1) want = 1;
+        A.seg[k] = g;
+        M.off[k] = off;
+        M.src[k] = src;
+        M.bcast[k] = bc;
+        A.block0[k] = blocks;
+        blocks += want;
+        k++;
+    };
+    for (int i = 0; i < n; i++) {
+        AdamSeg T{};
+        T.p = tr->b.table_master + begin[i];
+        T.m = tr->b.table_m + begin[i];
+        T.v = tr->b.table_v + begin[i];
+        T.shadow = reinterpret_cast<__half *>(tr->b.table_shadow) + begin[i];
+        T.n = end[i] - begin[i];
+        T.kind = 1;
+        T.vec = aligned(T.p, 16) && aligned(T.m, 16) && aligned(T.v, 16) && aligned(T.shadow, 8);
+        add(T, begin[i], 0, broadcast[i] ? 1 : 0);
+    }
+    if (with_mlp) {
+        AdamSeg Mg{};
+        Mg.p = tr->b.mlp_master;
+        Mg.m = tr->b.mlp_m;
+        Mg.v = tr->b.mlp_v;
+        Mg.shadow = tr->b.mlp_shadow;
+        Mg.n = fh::mlp::param_count(tr->K0);
+        Mg.kind = 2;
+        Mg.vec = aligned(Mg.p, 16) && aligned(Mg.m, 16) && aligned(Mg.v, 16) && aligned(Mg.shadow, 8);
+        add(Mg, 0, 1, 0);
+    }
+    if (k == 0) return FH_OK;
+    A.nseg = k;
+    A.block0[k] = blocks;
+    { fh::mlp::adam_multicast_kernel<<<(unsigned)blocks, 256, 0, reinterpret_cast<cudaStream_t>(stream)>>>(A, M); fh::count_launch(); }
+    return cuda_check(cudaGetLastError(), "adam_multicast_kernel launch");
+}
+
 fh_status fh_train_apply_sharded(fh_trainer tr, int64_t begin, int64_t end, const float *grad_shard,
                                  fh_stream stream) {
     g_err[0] = 0;

@@ -314,6 +314,75 @@ class PeerShardedDP:
         cur.wait_stream(self.comm)
 
 
+class MulticastShardedDP(PeerShardedDP):
+    """SURVEY.md §8(e) item 3 as written: the same schedule as PeerShardedDP,
+    with the gradient sum and the shadow broadcast done by the NVSwitch
+    through an NVLS multicast object bound to every rank's grad and shadow
+    buffers (fh_train_apply_multicast: multimem.ld_reduce, Adam in
+    registers, multimem.st).  By default the multicast addresses and the
+    cross-rank barrier come from torch symmetric memory (Trainer built with
+    alloc=dp.symm_alloc, on a system with multicast support); `mc` =
+    (grad, shadow) multicast addresses and `barrier` override them (tests:
+    a one-device multicast object, no peers)."""
+
+    def __init__(self, trainer, group=None, mc=None, barrier=None):
+        import torch
+        self.tr = trainer
+        if trainer.shadow_flat is None:
+            raise ValueError("MulticastShardedDP needs an fp16 table shadow")
+        if mc is None:
+            import torch.distributed as dist
+            import torch.distributed._symmetric_memory as sm
+            grp = group or dist.group.WORLD
+            self.hg = sm.rendezvous(trainer.grads, grp.group_name)
+            self.hs = sm.rendezvous(trainer.shadow_flat, grp.group_name)
+            mg, ms = int(self.hg.multicast_ptr), int(self.hs.multicast_ptr)
+            if not mg or not ms:
+                raise ValueError("torch symmetric memory has no multicast object on this system")
+            mc = (mg + int(getattr(self.hg, "offset", 0)), ms + int(getattr(self.hs, "offset", 0)))
+            self.world, self.rank = self.hg.world_size, self.hg.rank
+            self._barrier = barrier or (lambda: self.hg.barrier(channel=0))
+        else:
+            import torch.distributed as dist
+            self.world = dist.get_world_size(group) if dist.is_initialized() else 1
+            self.rank = dist.get_rank(group) if dist.is_initialized() else 0
+            self._barrier = barrier or (lambda: None)
+        self.mg, self.ms = mc
+        self.mm = self.mg + trainer.nt_pad * 4
+        self.launches = trainer.bwd_launch_ranges()
+        self.mains, self.tails = overlap_plan(self.launches, self.world, self.rank)
+        self.by_launch = [[] for _ in self.launches]
+        for (li, a, m) in self.mains:
+            c = m // self.world
+            self.by_launch[li].append((a + self.rank * c, a + (self.rank + 1) * c))
+        self.comm = torch.cuda.Stream(device=trainer.grads.device)
+        self.events = [torch.cuda.Event() for _ in self.launches]
+        for ev in self.events:
+            ev.record()
+        trainer.set_bwd_events(self.events)
+
+    def reduce_and_apply(self, stream=None):
+        import torch
+        tr = self.tr
+        cur = torch.cuda.current_stream() if stream is None else stream
+        first = True
+        with torch.cuda.stream(self.comm):
+            for li, ranges in enumerate(self.by_launch):
+                self.comm.wait_event(self.events[li])   # this rank's group li is final
+                self._barrier()                         # ... and every other rank's
+                if ranges:
+                    tr.apply_multicast(self.mg, self.ms, self.mm, ranges, [1] * len(ranges), False, first,
+                                       stream=self.comm)
+                    first = False
+            self.comm.wait_stream(cur)
+            self._barrier()
+            tr.apply_multicast(self.mg, self.ms, self.mm, self.tails, [0] * len(self.tails), True, first,
+                               stream=self.comm)
+            self._barrier()                             # gradients read by every rank: the next
+                                                        # fwd_bwd may overwrite them
+        cur.wait_stream(self.comm)
+
+
 def replicas_identical(tensor, group=None) -> bool:
     """True when `tensor` is bit-identical on every rank (compares a 64-bit
     checksum of its bytes gathered from all ranks)."""

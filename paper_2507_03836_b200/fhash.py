@@ -34,7 +34,7 @@ EXPORTS = [
     "fh_mlp_param_count", "fh_train_workspace_size", "fh_trainer_create", "fh_train_fwd_bwd", "fh_train_apply",
     "fh_train_step", "fh_trainer_status", "fh_trainer_step_count", "fh_trainer_destroy", "fh_train_apply_sharded",
     "fh_train_bwd_launches", "fh_train_bwd_ranges", "fh_train_set_bwd_events", "fh_train_apply_ranges",
-    "fh_train_apply_peers", "fh_nccl_unique_id", "fh_nccl_comm_create", "fh_nccl_comm_destroy",
+    "fh_train_apply_peers", "fh_train_apply_multicast", "fh_nccl_unique_id", "fh_nccl_comm_create", "fh_nccl_comm_destroy",
     "fh_trainer_dp_workspace_size", "fh_trainer_set_comm", "fh_level_stats_workspace_size", "fh_level_stats", "fh_kernel_launches", "fh_encoder_scratch_size", "fh_encoder_attach_scratch",
     # inference (renderer's model evaluation) and the ARM pace rule
     "fh_infer_workspace_size", "fh_infer", "fh_arm_pace",
@@ -386,6 +386,9 @@ def _train_lib():
                                        ctypes.c_int, ctypes.POINTER(i64), ctypes.POINTER(i64),
                                        ctypes.POINTER(ctypes.c_int), ctypes.c_int, ctypes.c_int, vp]
     L.fh_train_apply_peers.restype = ctypes.c_int
+    L.fh_train_apply_multicast.argtypes = [vp, vp, vp, vp, ctypes.c_int, ctypes.POINTER(i64), ctypes.POINTER(i64),
+                                           ctypes.POINTER(ctypes.c_int), ctypes.c_int, ctypes.c_int, vp]
+    L.fh_train_apply_multicast.restype = ctypes.c_int
     L.fh_nccl_unique_id.argtypes = [vp]
     L.fh_nccl_comm_create.argtypes = [vp, ctypes.c_int, ctypes.c_int, ctypes.POINTER(vp)]
     L.fh_nccl_comm_destroy.argtypes = [vp]
@@ -564,6 +567,16 @@ class Trainer:
         bc = (ctypes.c_int * max(1, n))(*[int(x) for x in broadcast])
         _check(_train_lib().fh_train_apply_peers(self._h, W, pg, ps, pm, n, b, e, bc, int(with_mlp), int(new_step),
                                                  _stream(stream)))
+
+    def apply_multicast(self, mc_grads, mc_shadow, mc_mlp_grads, ranges, broadcast, with_mlp, new_step,
+                        stream=None):
+        """fh_train_apply_multicast: mc_* are NVLS multicast device addresses (int)."""
+        n = len(ranges)
+        b = (ctypes.c_int64 * max(1, n))(*[r[0] for r in ranges])
+        e = (ctypes.c_int64 * max(1, n))(*[r[1] for r in ranges])
+        bc = (ctypes.c_int * max(1, n))(*[int(x) for x in broadcast])
+        _check(_train_lib().fh_train_apply_multicast(self._h, mc_grads, mc_shadow, mc_mlp_grads, n, b, e, bc,
+                                                     int(with_mlp), int(new_step), _stream(stream)))
 
     def apply_ranges(self, ranges, grads, stream=None):
         """One Adam step over table element ranges [(b, e)] with grads (f32

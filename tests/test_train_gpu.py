@@ -453,6 +453,119 @@ def test_apply_peers_sums_ranks_and_broadcasts():
     assert ta.step_count == 1
 
 
+def test_apply_multicast_nvls_single_gpu():
+    """fh_train_apply_multicast (multimem.ld_reduce +
+    Adam + multimem.st) on a real NVLS multicast object spanning this one
+    GPU (tests/mc_alloc.py: cuMemCreate memory bound to a one-device
+    multicast object): the reduction over one rank is the buffer itself, so
+    the update must equal plain Adam bit for bit; broadcast ranges reach the
+    shadow through the multicast address (f16x2 multimem.st), replicated
+    ranges through the local one; vector and pair (unaligned) paths."""
+    import mc_alloc
+    ok, why = mc_alloc.multicast_supported()
+    if not ok:
+        pytest.skip(why)
+    cfg = small_cfg(2, 16, cap=1 << 10)
+    mca = mc_alloc.McAllocator()
+    g = W.rng(61)
+    enc = fh.Encoder(cfg.levels, cfg.F, cfg.table_dtype, cfg.cap)
+    table = W.draw_table(g, enc.entries, cfg.F, "f32")
+    layers = W.draw_mlp(g, W.MLPConfig((32, 64, 64, 1)))
+    ta = fh.Trainer(enc, table, layers, 1500, alloc=mca)
+    tb = fh.Trainer(enc, table, layers, 1500)
+    coords = torch.from_numpy(W.draw_coords(g, 1500)).cuda()
+    target = torch.from_numpy(g.random(1500, dtype=np.float32)).cuda()
+    for step in range(2):
+        ta.fwd_bwd(coords, target)
+        tb.grads.copy_(ta.grads)
+        nt = ta.n_table
+        half = (nt // 2) // 4 * 4
+        odd = half + 6            # a broadcast range off the 4-element grid: pair path
+        rngs = [(0, half), (half, odd), (odd, nt)]
+        ta.apply_multicast(mca.mc(ta.grads), mca.mc(ta.shadow_flat), mca.mc(ta.grads) + ta.nt_pad * 4,
+                           rngs, [1, 1, 0], True, True)
+        tb.apply()
+        torch.cuda.synchronize()
+        assert torch.equal(ta.table_master, tb.table_master)
+        assert torch.equal(ta.mlp_master, tb.mlp_master)
+        assert torch.equal(ta.table_shadow, tb.table_shadow)
+    assert ta.step_count == 2
+    # broadcast ranges must be whole fp16 pairs
+    with pytest.raises(fh.FHashError):
+        ta.apply_multicast(mca.mc(ta.grads), mca.mc(ta.shadow_flat), mca.mc(ta.grads) + ta.nt_pad * 4,
+                           [(1, 5)], [1], False, True)
+
+
+def test_apply_multicast_argument_checks():
+    """fh_train_apply_multicast's host-side checks (run without a multicast
+    object: every call here fails before any launch)."""
+    cfg = small_cfg(2, 16, cap=1 << 10)
+    enc, tr, _, _ = make(cfg, 300, seed=63)
+    g = tr.grads.data_ptr()
+    sh = tr.shadow_flat.data_ptr()
+    nt = tr.n_table
+    bad = [
+        (0, sh, g, [(0, 4)], [1], False),                 # NULL grad address
+        (g, 0, g, [(0, 4)], [1], False),                  # NULL shadow address
+        (g + 4, sh, g, [(0, 4)], [1], False),             # grad not 16-byte aligned
+        (g, sh + 2, g, [(0, 4)], [1], False),             # shadow not 8-byte aligned
+        (g, sh, g, [(1, 5)], [1], False),                 # broadcast range not in fp16 pairs
+        (g, sh, g, [(0, nt + 2)], [1], False),            # range outside the table
+        (g, sh, 0, [(0, 4)], [1], True),                  # with_mlp and a NULL MLP address
+    ]
+    for (mg, ms, mm, rngs, bc, with_mlp) in bad:
+        with pytest.raises(fh.FHashError):
+            tr.apply_multicast(mg, ms, mm, rngs, bc, with_mlp, True)
+    assert tr.step_count == 0
+    # an fp32-table trainer has no fp16 shadow to broadcast
+    cfg32 = small_cfg(2, 16, tdt="f32", cap=1 << 10)
+    _, tr32, _, _ = make(cfg32, 300, seed=64)
+    with pytest.raises(fh.FHashError):
+        tr32.apply_multicast(tr32.grads.data_ptr(), tr32.grads.data_ptr(), tr32.grads.data_ptr(), [(0, 4)], [1],
+                             False, True)
+
+
+def test_multicast_sharded_dp_single_rank():
+    """dp.MulticastShardedDP (per backward launch: this rank's chunk through
+    fh_train_apply_multicast, tails + MLP at the end) on a 1-rank NCCL group
+    with a one-device multicast object: equal to the plain step, bit for bit."""
+    import mc_alloc
+    import torch.distributed as dist
+    from paper_2507_03836_b200 import dp
+    ok, why = mc_alloc.multicast_supported()
+    if not ok:
+        pytest.skip(why)
+    import os
+    os.environ.setdefault("MASTER_ADDR", "127.0.0.1")
+    os.environ.setdefault("MASTER_PORT", "29581")
+    created = not dist.is_initialized()
+    if created:
+        dist.init_process_group("nccl", rank=0, world_size=1, device_id=torch.device("cuda", 0))
+    try:
+        cfg = small_cfg(2, 16, cap=1 << 10)
+        mca = mc_alloc.McAllocator()
+        g = W.rng(62)
+        enc = fh.Encoder(cfg.levels, cfg.F, cfg.table_dtype, cfg.cap)
+        table = W.draw_table(g, enc.entries, cfg.F, "f32")
+        layers = W.draw_mlp(g, W.MLPConfig((32, 64, 64, 1)))
+        ta = fh.Trainer(enc, table, layers, 3000, alloc=mca)
+        tb = fh.Trainer(enc, table, layers, 3000)
+        sdp = dp.MulticastShardedDP(ta, mc=(mca.mc(ta.grads), mca.mc(ta.shadow_flat)), barrier=lambda: None)
+        for k in range(3):
+            coords = torch.from_numpy(W.draw_coords(W.rng(100 + k), 3000)).cuda()
+            target = torch.from_numpy(W.rng(200 + k).random(3000, dtype=np.float32)).cuda()
+            sdp.step(coords, target, 3000)
+            tb.fwd_bwd(coords, target)
+            tb.apply()
+        torch.cuda.synchronize()
+        assert torch.equal(ta.table_master, tb.table_master)
+        assert torch.equal(ta.mlp_master, tb.mlp_master)
+        assert torch.equal(ta.table_shadow, tb.table_shadow)
+    finally:
+        if created:
+            dist.destroy_process_group()
+
+
 def test_peer_sharded_dp_single_rank():
     """dp.PeerShardedDP on a 1-rank NCCL group with torch symmetric memory:
     the fused kernel path equals the plain step (same gradients)."""
