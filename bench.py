@@ -443,10 +443,13 @@ def microbench_roofline(fh, torch, enc, cfg, N, stream, hbm_peak):
     # the L2's random-reduction op rate: one 16-byte red.v4 per x-pair at
     # uniform positions in an L2-resident 48 MiB buffer (8-byte entries,
     # mode 1) -- the unit the encode backward is bound by
+    # (67 M reductions per launch, best of 5: a launch as long as the
+    # backward pass itself, so ramp-up and tail do not understate the rate)
+    n_red = 1 << 23
     rb = torch.zeros((48 << 20) // 4, device="cuda")
-    fh.bench_red(rb, (48 << 20) // 8, 8, n_thr, mode=1, seed=99, stream=stream)
-    t_red = timeit(lambda: fh.bench_red(rb, (48 << 20) // 8, 8, n_thr, mode=1, seed=99, stream=stream))
-    red_ops_per_s = 8 * n_thr / t_red
+    fh.bench_red(rb, (48 << 20) // 8, 8, n_red, mode=1, seed=99, stream=stream)
+    t_red = timeit(lambda: fh.bench_red(rb, (48 << 20) // 8, 8, n_red, mode=1, seed=99, stream=stream), reps=5)
+    red_ops_per_s = 8 * n_red / t_red
     del rb
     stream_fwd = N * (16 + cfg.L * F * 4)
     stream_bwd = N * (16 + cfg.L * F * 4)
