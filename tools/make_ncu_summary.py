@@ -65,7 +65,7 @@ def summarise(ls):
 
 def main():
     out = {"_source": "ncu --set full --clock-control none of tools/time_encode.py <cfg> 1 (FH_OVERWRITE=1) on one "
-                      "B200, round 2 (tools/gpu_prof_r02.sh); per encode PASS = all launches of fh_encode_fwd / "
+                      "B200, round 2 (tools/gpu_prof_r02c_encode.sh); per encode PASS = all launches of fh_encode_fwd / "
                       "fh_encode_bwd_ex of the last captured step.  *_frac = time-weighted fraction of the unit's "
                       "peak (lts__throughput, l1tex2xbar request port, L2 red-sector rate, atomic input).  Cold "
                       "cache, serialised launches: shares, not absolute times, match the bench."}
