@@ -422,6 +422,39 @@ def test_overlapped_dp_single_rank_equals_plain_step():
     assert ta.status() == fh.FH_OK and torch.isfinite(loss).all()
 
 
+def test_fwd_bwd_zero_samples_records_events_after_zeroing():
+    """A rank with no samples (N_local = 0, n_global > 0): fh_train_fwd_bwd
+    zeroes the gradients and records the caller's per-launch events AFTER
+    the zeroing, so a communication stream that waits on them reads zeros
+    (not the previous step's gradients)."""
+    cfg = small_cfg(2, 16, cap=1 << 10)
+    enc, tr, coords, target = make(cfg, 500, seed=37)
+    launches = tr.bwd_launch_ranges()
+    evs = [torch.cuda.Event() for _ in launches]
+    for ev in evs:
+        ev.record()
+    tr.set_bwd_events(evs)
+    tr.fwd_bwd(torch.from_numpy(coords).cuda(), torch.from_numpy(target).cuda())
+    torch.cuda.synchronize()
+    tr.grads[:tr.n_table].fill_(float("nan"))            # stale: must be overwritten before the events
+    torch.cuda.synchronize()
+    main = torch.cuda.Stream()
+    comm = torch.cuda.Stream()
+    empty = torch.empty((0, 4), device="cuda")
+    with torch.cuda.stream(main):
+        torch.cuda._sleep(2_000_000)                      # keep the zeroing late on its stream
+        tr.fwd_bwd(empty, torch.empty((0,), device="cuda"), 1000, stream=main)
+    seen = []
+    with torch.cuda.stream(comm):
+        for ev in evs:
+            comm.wait_event(ev)
+        seen.append(tr.grads[:tr.n_table].clone())
+    torch.cuda.synchronize()
+    assert torch.all(seen[0] == 0)
+    assert torch.all(tr.table_grad == 0)
+    tr.set_bwd_events([])
+
+
 def test_apply_peers_sums_ranks_and_broadcasts():
     """fh_train_apply_peers with W = 3 'ranks' simulated by local buffers:
     the update uses the rank-ordered SUM of the three gradient buffers
