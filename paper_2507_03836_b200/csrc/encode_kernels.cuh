@@ -165,7 +165,9 @@ __global__ void __launch_bounds__(256) bwd_kernel(const __grid_constant__ Params
     const int64_t n = j;
     const Level lv = slv.get(l);
     const float4 p = __ldcs(coords + n);
-    // dout is loaded before the cell arithmetic: both HBM loads in flight at once
+    Cell c;
+    const bool bad = cell_of(lv, p, c);
+    if (bad && li == 0) atomicOr(flag, 1);
     float g[F];
     const float *gp = dout + n * (int64_t)(L * F) + l * F;
     if constexpr (F == 2) {
@@ -181,9 +183,6 @@ __global__ void __launch_bounds__(256) bwd_kernel(const __grid_constant__ Params
 #pragma unroll
         for (int f = 0; f < F; f++) g[f] = __ldcs(gp + f);
     }
-    Cell c;
-    const bool bad = cell_of(lv, p, c);
-    if (bad && li == 0) atomicOr(flag, 1);
     const float wx[2] = {__fsub_rn(1.0f, c.w[0]), c.w[0]}, wy[2] = {__fsub_rn(1.0f, c.w[1]), c.w[1]};
     const float wz[2] = {__fsub_rn(1.0f, c.w[2]), c.w[2]}, wt[2] = {__fsub_rn(1.0f, c.w[3]), c.w[3]};
 #pragma unroll
