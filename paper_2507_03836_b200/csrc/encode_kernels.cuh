@@ -30,22 +30,29 @@ __global__ void __launch_bounds__(256, FwdMinBlocks<F>::value) fwd_kernel(const 
     load_levels(P, slv);
     const int L = P.L;
     const int lc = LL.n;
-    const int64_t gid = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
-    const int64_t j = gid / lc;
-    if (j >= N) return;
-    const int li = (int)(gid - j * lc);
-    const int l = LL.id[li];
-    const int64_t n = j;
-    const Level lv = slv.get(l);
-    const float4 p = __ldcs(coords + n);
-    Cell c;
-    const bool bad = cell_of(lv, p, c);
-    if (bad && li == 0) atomicOr(flag, 1);
-    float e[16][F];
-    gather16<T, F>(table, lv.tshift ? tsh : nullptr, c.idx, e);
-    float v[F];
-    blend16<F>(e, c.w, v);
-    Store<F, O>::store(out + n * (int64_t)(L * F) + l * F, v);
+    // F >= 4: a capped, grid-stride grid (FwdGrid) -- each CTA sets up its
+    // level table once and works through many (sample, level) items; F <= 2
+    // keeps one item per thread (its 64-register budget would spill the loop)
+    constexpr bool kLoop = F >= 4;
+    const int64_t total = N * lc, stride = kLoop ? (int64_t)gridDim.x * blockDim.x : total;
+#pragma unroll 1
+    for (int64_t gid = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; gid < total; gid += stride) {
+        const int64_t j = gid / lc;
+        const int li = (int)(gid - j * lc);
+        const int l = LL.id[li];
+        const int64_t n = j;
+        const Level lv = slv.get(l);
+        const float4 p = __ldcs(coords + n);
+        Cell c;
+        const bool bad = cell_of(lv, p, c);
+        if (bad && li == 0) atomicOr(flag, 1);
+        float e[16][F];
+        gather16<T, F>(table, lv.tshift ? tsh : nullptr, c.idx, e);
+        float v[F];
+        blend16<F>(e, c.w, v);
+        Store<F, O>::store(out + n * (int64_t)(L * F) + l * F, v);
+        if constexpr (!kLoop) break;
+    }
 }
 
 // ------------------------------------------------------------ backward

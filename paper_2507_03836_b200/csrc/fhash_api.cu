@@ -368,7 +368,12 @@ static void launch_fwd(fh_encoder e, const float *coords, int64_t N, const void 
     const int n = split_lists(e, include, (double)F * sizeof(T), limit, lists, sh,
                               (int)(32 / (F * sizeof(O))) > 1 ? (int)(32 / (F * sizeof(O))) : 1);
     for (int g = 0; g < n; g++)
-        { fh::fwd_kernel<F, T, O><<<grid_for(N, lists[g].n), 256, 0, s>>>(
+        { dim3 gg = grid_for(N, lists[g].n);
+          if (F >= 4) {   // grid-stride kernel: a capped grid (FH_FWD_GRID CTAs per SM, default 8)
+              static const int cap = getenv("FH_FWD_GRID") ? atoi(getenv("FH_FWD_GRID")) : 8;
+              if (cap > 0 && gg.x > (unsigned)(cap * e->n_sm)) gg.x = (unsigned)(cap * e->n_sm);
+          }
+          fh::fwd_kernel<F, T, O><<<gg, 256, 0, s>>>(
             prm, c4, N, reinterpret_cast<const T *>(table), tsh, reinterpret_cast<O *>(out), e->flag,
             lists[g]); fh::count_launch(); }
 }
