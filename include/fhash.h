@@ -196,6 +196,13 @@ fh_status fh_encode_bwd(fh_encoder enc, const float *coords, int64_t N, const fl
  * the reductions arrive; a separate fh_zero_grad before the forward has
  * them evicted by the forward's traffic).  Unknown flags: FH_E_ARG. */
 #define FH_BWD_OVERWRITE 1u
+/* FH_BWD_DOUT_LEVEL_MAJOR: dout is level-major, [L][N][F] f32 (level l's
+ * gradient rows at dout + l N F), instead of the row-major [N][L F] of
+ * fh_encode_bwd; same values, same result.  A level pass then reads
+ * contiguous F-float rows (cfg4, F = 4: bwd 6.11 -> 5.51 ms; F = 2:
+ * neutral).  The trainer's dL/d(enc) for F >= 4 is in this layout.
+ * F-Hash encoders only (MHE: FH_E_ARG). */
+#define FH_BWD_DOUT_LEVEL_MAJOR 2u
 fh_status fh_encode_bwd_ex(fh_encoder enc, const float *coords, int64_t N, const float *dout,
                            float *dtable, unsigned flags, fh_stream stream);
 
@@ -310,6 +317,13 @@ fh_status fh_trainer_create(fh_encoder enc, const fh_mlp_desc *mlp, const fh_tra
  * N_local. */
 fh_status fh_train_fwd_bwd(fh_trainer tr, const float *coords, const float *target, int64_t N_local,
                            int64_t N_global, float *loss_dev, fh_stream stream);
+
+/* fh_train_dx_layout -- the layout of the trainer's dL/d(enc) workspace
+ * (the MLP kernel's dX, the encode backward's dout): 0 = row-major
+ * [N][L F]; F (>= 4) = level-major [L][N][F] (FH_BWD_DOUT_LEVEL_MAJOR),
+ * chosen at fh_trainer_create for F >= 4 unless FH_DX_ROW_MAJOR is set in
+ * the environment.  -1: NULL trainer.  Host only. */
+int       fh_train_dx_layout(fh_trainer tr);
 
 /* One Adam step on all parameters (step counter += 1). */
 fh_status fh_train_apply(fh_trainer tr, fh_stream stream);

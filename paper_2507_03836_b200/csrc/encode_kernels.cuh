@@ -146,8 +146,8 @@ struct MergeJob {
 template <int F, bool RANGED = false>
 __global__ void __launch_bounds__(256) bwd_kernel(const __grid_constant__ Params P,
                                                   const float4 *__restrict__ coords, int64_t N,
-                                                  const float *__restrict__ dout, float *__restrict__ dtable,
-                                                  float *__restrict__ gsh,
+                                                  const float *__restrict__ dout, const DoutLayout dl,
+                                                  float *__restrict__ dtable, float *__restrict__ gsh,
                                                   int *__restrict__ flag, const __grid_constant__ LevelList LL,
                                                   uint32_t lo = 0,
                                                   uint32_t span = 0, uint32_t rep_n = 0, int64_t rep_stride = 0,
@@ -159,7 +159,6 @@ __global__ void __launch_bounds__(256) bwd_kernel(const __grid_constant__ Params
     }
     __shared__ LevelSmem slv;
     load_levels(P, slv);
-    const int L = P.L;
     const int lc = LL.n;
     const int64_t bid = (int64_t)blockIdx.x - mj.ctas;
     const int64_t gid = bid * blockDim.x + threadIdx.x;
@@ -176,7 +175,7 @@ __global__ void __launch_bounds__(256) bwd_kernel(const __grid_constant__ Params
     const bool bad = cell_of(lv, p, c);
     if (bad && li == 0) atomicOr(flag, 1);
     float g[F];
-    const float *gp = dout + n * (int64_t)(L * F) + l * F;
+    const float *gp = dout + n * dl.ns + l * dl.ls;
     if constexpr (F == 2) {
         const float2 q = __ldcs(reinterpret_cast<const float2 *>(gp));
         g[0] = q.x; g[1] = q.y;
@@ -252,8 +251,8 @@ template <int F>
 __global__ void __launch_bounds__(256) bwd_small_kernel(const __grid_constant__ Params P,
                                                         const __grid_constant__ SmallSet S,
                                                         const float4 *__restrict__ coords, int64_t N,
-                                                        const float *__restrict__ dout, float *__restrict__ dtable,
-                                                        int *__restrict__ flag) {
+                                                        const float *__restrict__ dout, const DoutLayout dl,
+                                                        float *__restrict__ dtable, int *__restrict__ flag) {
     extern __shared__ float acc[];
     __shared__ LevelSmem slv;
     load_levels(P, slv);
@@ -265,7 +264,6 @@ __global__ void __launch_bounds__(256) bwd_small_kernel(const __grid_constant__ 
     float *lp = acc + ncopy * S.total + warp * S.ttotal * 32 + lane;
     for (int i = threadIdx.x; i < ncopy * S.total + (int)(blockDim.x >> 5) * S.ttotal * 32; i += blockDim.x) acc[i] = 0.f;
     __syncthreads();
-    const int L = P.L;
     const int64_t items = N * S.n;
     const int64_t stride = (int64_t)gridDim.x * blockDim.x;
     // one item ahead: the next item's coordinates and upstream gradient are
@@ -277,7 +275,7 @@ __global__ void __launch_bounds__(256) bwd_small_kernel(const __grid_constant__ 
         const int64_t n = j;
         pc = __ldg(coords + n);
 #pragma unroll
-        for (int f = 0; f < F; f++) gg[f] = __ldg(dout + n * (int64_t)(L * F) + S.id[li] * F + f);
+        for (int f = 0; f < F; f++) gg[f] = __ldg(dout + n * dl.ns + S.id[li] * dl.ls + f);
     };
     float4 p_nxt = make_float4(0.f, 0.f, 0.f, 0.f);
     float g_nxt[F];

@@ -49,4 +49,13 @@ struct LevelList {
     int id[kMaxLevels];
 };
 
+// Layout of the backward's upstream gradient: level l of sample n starts at
+// dout + n * ns + l * ls (floats).  Row-major [N][L][F] (the ABI default):
+// ns = L F, ls = F.  Level-major [L][N][F] (FH_BWD_DOUT_LEVEL_MAJOR, the
+// trainer's dL/d(enc) for F >= 4): ns = F, ls = N F -- a level pass then
+// reads contiguous F-float rows instead of F of every L F floats.
+struct DoutLayout {
+    int64_t ns, ls;
+};
+
 }  // namespace fh

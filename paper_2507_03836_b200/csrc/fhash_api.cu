@@ -718,6 +718,7 @@ struct BwdCall {
     const float4 *c4;
     int64_t N;
     const float *dout;
+    fh::DoutLayout dl;
     float *dtable;
     cudaStream_t s;
 };
@@ -729,7 +730,7 @@ static void launch_bwd_kernel(const BwdCall &b, dim3 g, const fh::LevelList &ll,
     const fh_encoder e = b.e;
     g.x += (unsigned)mj.ctas;   // the merge CTAs come first (blockIdx < mj.ctas)
 #define FH_BWD(FF, RR, GG)                                                                                     \
-    { fh::bwd_kernel<FF, RR><<<g, 256, 0, b.s>>>(e->params, b.c4, b.N, b.dout, dt, GG, e->flag, ll, lo, span, \
+    { fh::bwd_kernel<FF, RR><<<g, 256, 0, b.s>>>(e->params, b.c4, b.N, b.dout, b.dl, dt, GG, e->flag, ll, lo, span, \
                                                  rep_n, rep_stride, mj); fh::count_launch(); }
     switch (e->F) {
         case 1: if (ranged) FH_BWD(1, true, gsh) else FH_BWD(1, false, gsh) break;
@@ -755,7 +756,7 @@ static fh_status bwd_small_levels(const BwdCall &b) {
         const dim3 g((unsigned)blocks);
         switch (e->F) {
 #define FH_SMALL(FF)                                                                                                 \
-    { fh::bwd_small_kernel<FF><<<g, pl.threads, pl.smem, b.s>>>(e->params, Sx, b.c4, b.N, b.dout, b.dtable, e->flag); \
+    { fh::bwd_small_kernel<FF><<<g, pl.threads, pl.smem, b.s>>>(e->params, Sx, b.c4, b.N, b.dout, b.dl, b.dtable, e->flag); \
       fh::count_launch(); }                                                                                          \
     break;
             case 1: FH_SMALL(1)
@@ -825,7 +826,8 @@ static bool bwd_replicated(const BwdCall &b, int l, dim3 g, const fh::LevelList 
 
 static fh_status encode_bwd_impl(fh_encoder e, const float *coords, int64_t N,
                                  const float *dout, float *dtable, fh_stream stream,
-                                 cudaEvent_t *ev = nullptr, int n_ev = 0, bool zero = false) {
+                                 cudaEvent_t *ev = nullptr, int n_ev = 0, bool zero = false,
+                                 bool level_major = false) {
     g_err[0] = 0;
     fh_status st = check_common(e, coords, N, "fh_encode_bwd");
     if (st != FH_OK) return st;
@@ -843,7 +845,11 @@ static fh_status encode_bwd_impl(fh_encoder e, const float *coords, int64_t N,
     if (!dout || !aligned(dout, vec > 16 ? 16 : vec)) return fail(FH_E_ARG, "fh_encode_bwd: NULL/misaligned dout");
     if ((st = device_ready(e)) != FH_OK) return st;
     const float4 *c4 = reinterpret_cast<const float4 *>(coords);
-    const BwdCall b{e, c4, N, dout, dtable, s};
+    if (level_major && e->kind == 1)
+        return fail(FH_E_ARG, "fh_encode_bwd: level-major dout is not supported by the MHE encoder");
+    const int64_t LF = (int64_t)e->L * e->F;
+    const fh::DoutLayout dl = level_major ? fh::DoutLayout{e->F, N * e->F} : fh::DoutLayout{LF, e->F};
+    const BwdCall b{e, c4, N, dout, dl, dtable, s};
     // launch 0 (when present): the few-cell levels in shared memory
     if (e->small.n > 0) {
         if (zero)
@@ -982,8 +988,8 @@ int bwd_launch_ranges(fh_encoder e, int i, int64_t *r, int max) {
     return 1;
 }
 fh_status encode_bwd_events(fh_encoder e, const float *coords, int64_t N, const float *dout, float *dtable,
-                            fh_stream stream, cudaEvent_t *ev, int n_ev, bool overwrite) {
-    return encode_bwd_impl(e, coords, N, dout, dtable, stream, ev, n_ev, overwrite);
+                            fh_stream stream, cudaEvent_t *ev, int n_ev, bool overwrite, bool level_major) {
+    return encode_bwd_impl(e, coords, N, dout, dtable, stream, ev, n_ev, overwrite, level_major);
 }
 }  // namespace fh
 
@@ -996,8 +1002,10 @@ fh_status fh_encode_fwd(fh_encoder e, const float *coords, int64_t N, const void
 
 fh_status fh_encode_bwd_ex(fh_encoder e, const float *coords, int64_t N, const float *dout, float *dtable,
                            unsigned flags, fh_stream stream) {
-    if (flags & ~(unsigned)FH_BWD_OVERWRITE) return fail(FH_E_ARG, "fh_encode_bwd_ex: unknown flags 0x%x", flags);
-    return encode_bwd_impl(e, coords, N, dout, dtable, stream, nullptr, 0, (flags & FH_BWD_OVERWRITE) != 0);
+    if (flags & ~(unsigned)(FH_BWD_OVERWRITE | FH_BWD_DOUT_LEVEL_MAJOR))
+        return fail(FH_E_ARG, "fh_encode_bwd_ex: unknown flags 0x%x", flags);
+    return encode_bwd_impl(e, coords, N, dout, dtable, stream, nullptr, 0, (flags & FH_BWD_OVERWRITE) != 0,
+                           (flags & FH_BWD_DOUT_LEVEL_MAJOR) != 0);
 }
 
 fh_status fh_encode_bwd(fh_encoder e, const float *coords, int64_t N, const float *dout, float *dtable,

@@ -41,7 +41,8 @@ inline void count_launch() { g_launches.fetch_add(1, std::memory_order_relaxed);
 int bwd_launch_count(fh_encoder e);
 int bwd_launch_ranges(fh_encoder e, int launch, int64_t *ranges, int max);
 fh_status encode_bwd_events(fh_encoder e, const float *coords, int64_t N, const float *dout, float *dtable,
-                            fh_stream stream, cudaEvent_t *ev, int n_ev, bool overwrite = false);
+                            fh_stream stream, cudaEvent_t *ev, int n_ev, bool overwrite = false,
+                            bool level_major = false);
 
 }  // namespace fh
 

@@ -127,6 +127,7 @@ struct TrainArgs {
     int *flag;                   // bit 1: non-finite loss
     int64_t N;
     float inv_n_global;
+    int dx_lm_log2;              // 0: dx row-major [N][K0]; 2 / 3: level-major [L][N][F], F = 4 / 8
 };
 
 // Write 8 bf16 (16 B) = one core-matrix row segment.
@@ -479,20 +480,34 @@ __global__ void __launch_bounds__(TRAIN_THREADS, 1) mlp_train_kernel(const Train
             float v[XC];
             tmem_ld_cols<XC>(tm + lane_off + Lo::T_ACC + hf * XC, v);
             {   // rows past N (ragged last tile) are clipped by the TMA
+                // level-major dX (F = 2^fl >= 4): a box is 16 / F levels of
+                // 128 rows x F floats, row t of level-in-box lv at
+                // lv * 512 F + t * 4 F bytes (F = 4: a warp's 32 rows are
+                // 512 contiguous bytes, conflict-free)
+                const int fl = a.dx_lm_log2;
 #pragma unroll
                 for (int j = 0; j < XC; j += 4) {
-                    const int col = hf * XC + j, bx = col >> 4, c = (col >> 2) & 3;
-                    *reinterpret_cast<float4 *>(sDZ + bx * 8192 + t * 64 + 16 * (c ^ ((t >> 1) & 3))) =
-                        make_float4(v[j], v[j + 1], v[j + 2], v[j + 3]);
+                    const int col = hf * XC + j, bx = col >> 4, c = (col >> 2) & 3, cc = col & 15;
+                    const int off = fl ? bx * 8192 + ((cc >> fl) << (fl + 9)) + (t << (fl + 2)) + ((cc & ((1 << fl) - 1)) << 2)
+                                       : bx * 8192 + t * 64 + 16 * (c ^ ((t >> 1) & 3));
+                    *reinterpret_cast<float4 *>(sDZ + off) = make_float4(v[j], v[j + 1], v[j + 2], v[j + 3]);
                 }
                 tc::fence_smem_to_async();
                 slot_sync(slot);
                 if (issuer) {
+                    if (fl) {
 #pragma unroll
-                    for (int bx = 0; bx < K0 / 16; bx++)
-                        asm volatile("cp.async.bulk.tensor.2d.global.shared::cta.bulk_group [%0, {%1, %2}], [%3];"
-                                     ::"l"(reinterpret_cast<uint64_t>(&tm_dx)), "r"(16 * bx), "r"((int)(tile * TILE)),
-                                     "r"(aDZ + 8192u * bx) : "memory");
+                        for (int bx = 0; bx < K0 / 16; bx++)
+                            asm volatile("cp.async.bulk.tensor.3d.global.shared::cta.bulk_group [%0, {%1, %2, %3}], [%4];"
+                                         ::"l"(reinterpret_cast<uint64_t>(&tm_dx)), "r"(0), "r"((int)(tile * TILE)),
+                                         "r"((16 * bx) >> fl), "r"(aDZ + 8192u * bx) : "memory");
+                    } else {
+#pragma unroll
+                        for (int bx = 0; bx < K0 / 16; bx++)
+                            asm volatile("cp.async.bulk.tensor.2d.global.shared::cta.bulk_group [%0, {%1, %2}], [%3];"
+                                         ::"l"(reinterpret_cast<uint64_t>(&tm_dx)), "r"(16 * bx), "r"((int)(tile * TILE)),
+                                         "r"(aDZ + 8192u * bx) : "memory");
+                    }
                     asm volatile("cp.async.bulk.commit_group;" ::: "memory");
                 }
             }

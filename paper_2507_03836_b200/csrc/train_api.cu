@@ -30,7 +30,8 @@ struct fh_trainer_s {
     int n_sm = 148;
     // workspace carve-up
     __nv_bfloat16 *enc_out = nullptr;  // [max_batch][K0]
-    float *dx = nullptr;               // [max_batch][K0]
+    float *dx = nullptr;               // [max_batch][K0], or [L][N][F] when dx_lm
+    int dx_lm = 0;                     // F when dX is level-major (F >= 4; see make_mlp_maps), else 0
     int *flag = nullptr;               // bit 1: non-finite loss
     float *partial = nullptr;          // [2 n_sm][P] per-slot MLP gradient partials
     float *loss_scratch = nullptr;
@@ -105,6 +106,10 @@ fh_status check_mlp(fh_encoder enc, const fh_mlp_desc *m) {
 //      layout (SWIZZLE_NONE, SBO = K0 * 16); row groups past N read as zero;
 //   dx [N][K0] fp32, box 128 rows x 16 columns, 64-byte swizzle (the
 //      kernel's dX staging layout); rows past N are not written.
+//      Level-major (tr->dx_lm = F >= 4): dX is [L][N][F], a 3-D map
+//      (F, N, L), box (F, 128, 16 / F) = 8 KB, no swizzle -- the encode
+//      backward's level passes then read contiguous 16-byte rows
+//      (FH_BWD_DOUT_LEVEL_MAJOR; cfg4 bwd 6.11 -> 5.51 ms).
 PFN_cuTensorMapEncodeTiled_v12000 tmap_encoder() {
     static PFN_cuTensorMapEncodeTiled_v12000 encode = nullptr;
     if (!encode) {
@@ -131,7 +136,17 @@ fh_status make_mlp_maps(fh_trainer tr, int64_t N, CUtensorMap *tm_x, CUtensorMap
                                   CU_TENSOR_MAP_L2_PROMOTION_NONE, CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
         if (r != CUDA_SUCCESS) return fail(FH_E_CUDA, "cuTensorMapEncodeTiled(x) failed (%d)", (int)r);
     }
-    {
+    if (tr->dx_lm) {
+        const cuuint64_t F = (cuuint64_t)tr->dx_lm;
+        cuuint64_t dims[3] = {F, (cuuint64_t)N, K0 / F};
+        cuuint64_t strides[2] = {F * 4, (cuuint64_t)N * F * 4};
+        cuuint32_t box[3] = {(cuuint32_t)F, 128, (cuuint32_t)(16 / F)};
+        cuuint32_t es[3] = {1, 1, 1};
+        const CUresult r = encode(tm_dx, CU_TENSOR_MAP_DATA_TYPE_FLOAT32, 3, tr->dx, dims, strides, box, es,
+                                  CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_NONE,
+                                  CU_TENSOR_MAP_L2_PROMOTION_NONE, CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
+        if (r != CUDA_SUCCESS) return fail(FH_E_CUDA, "cuTensorMapEncodeTiled(dx, level-major) failed (%d)", (int)r);
+    } else {
         cuuint64_t dims[2] = {K0, (cuuint64_t)N};
         cuuint64_t strides[1] = {K0 * 4};
         cuuint32_t box[2] = {16, 128};
@@ -164,6 +179,7 @@ fh_status launch_mlp(fh_trainer tr, const float *target, int64_t N, int64_t N_gl
     a.flag = tr->flag;
     a.N = N;
     a.inv_n_global = (float)(1.0 / (double)N_global);
+    a.dx_lm_log2 = tr->dx_lm == 8 ? 3 : tr->dx_lm == 4 ? 2 : 0;
     const int64_t tiles = (N + fh::mlp::TILE - 1) / fh::mlp::TILE;
     const int64_t pairs = (tiles + 1) / 2;  // two tile slots per CTA
     const int grid = (int)(pairs < tr->n_sm ? pairs : tr->n_sm);
@@ -221,6 +237,8 @@ fh_status fh_trainer_create(fh_encoder enc, const fh_mlp_desc *m, const fh_train
     tr->adam = *adam;
     tr->max_batch = max_batch;
     tr->n_sm = enc->n_sm;
+    // dL/d(enc) level-major for F >= 4 (FH_DX_ROW_MAJOR=1: the row-major form, for A/B)
+    tr->dx_lm = (enc->F >= 4 && !getenv("FH_DX_ROW_MAJOR")) ? enc->F : 0;
     char *w = reinterpret_cast<char *>(b->workspace);
     tr->enc_out = reinterpret_cast<__nv_bfloat16 *>(w);
     w += align_up(align_up((size_t)max_batch, 8) * tr->K0 * 2, 256);
@@ -278,8 +296,10 @@ fh_status fh_train_fwd_bwd(fh_trainer tr, const float *coords, const float *targ
     }
     if (st != FH_OK) return st;
     return fh::encode_bwd_events(tr->enc, coords, N, tr->dx, tr->b.table_grad, stream, tr->bwd_ev, tr->n_bwd_ev,
-                                 /*overwrite=*/true);
+                                 /*overwrite=*/true, /*level_major=*/tr->dx_lm != 0);
 }
+
+int fh_train_dx_layout(fh_trainer tr) { return tr ? tr->dx_lm : -1; }
 
 int fh_train_bwd_launches(fh_trainer tr) { return tr ? fh::bwd_launch_count(tr->enc) : -1; }
 

@@ -33,7 +33,7 @@ EXPORTS = [
     # train step
     "fh_mlp_param_count", "fh_train_workspace_size", "fh_trainer_create", "fh_train_fwd_bwd", "fh_train_apply",
     "fh_train_step", "fh_trainer_status", "fh_trainer_step_count", "fh_trainer_destroy", "fh_train_apply_sharded",
-    "fh_train_bwd_launches", "fh_train_bwd_ranges", "fh_train_set_bwd_events", "fh_train_apply_ranges",
+    "fh_train_dx_layout", "fh_train_bwd_launches", "fh_train_bwd_ranges", "fh_train_set_bwd_events", "fh_train_apply_ranges",
     "fh_train_apply_peers", "fh_train_apply_multicast", "fh_nccl_unique_id", "fh_nccl_comm_create", "fh_nccl_comm_destroy",
     "fh_trainer_dp_workspace_size", "fh_trainer_set_comm", "fh_level_stats_workspace_size", "fh_level_stats", "fh_kernel_launches", "fh_encoder_scratch_size", "fh_encoder_attach_scratch",
     # inference (renderer's model evaluation) and the ARM pace rule
@@ -222,13 +222,15 @@ class Encoder:
                                    _stream(stream)))
         return out
 
-    def bwd(self, coords, dout, dtable, stream=None, overwrite: bool = False):
+    def bwd(self, coords, dout, dtable, stream=None, overwrite: bool = False, level_major: bool = False):
         """dtable += gradient (fh_encode_bwd), or dtable = gradient with
         overwrite=True (fh_encode_bwd_ex FH_BWD_OVERWRITE: zeroed per level
-        group right before its reductions)."""
+        group right before its reductions).  level_major=True: dout is
+        [L][N][F] (FH_BWD_DOUT_LEVEL_MAJOR) instead of [N][L*F]."""
         self._auto_scratch(stream, coords.device)
-        if overwrite:
-            _check(lib().fh_encode_bwd_ex(self._h, _ptr(coords), coords.shape[0], _ptr(dout), _ptr(dtable), 1,
+        if overwrite or level_major:
+            flags = (1 if overwrite else 0) | (2 if level_major else 0)
+            _check(lib().fh_encode_bwd_ex(self._h, _ptr(coords), coords.shape[0], _ptr(dout), _ptr(dtable), flags,
                                           _stream(stream)))
         else:
             _check(lib().fh_encode_bwd(self._h, _ptr(coords), coords.shape[0], _ptr(dout), _ptr(dtable),
@@ -373,6 +375,8 @@ def _train_lib():
     L.fh_train_apply.argtypes = [vp, vp]
     L.fh_train_apply_sharded.argtypes = [vp, i64, i64, vp, vp]
     L.fh_train_apply_sharded.restype = ctypes.c_int
+    L.fh_train_dx_layout.argtypes = [vp]
+    L.fh_train_dx_layout.restype = ctypes.c_int
     L.fh_train_bwd_launches.argtypes = [vp]
     L.fh_train_bwd_launches.restype = ctypes.c_int
     L.fh_train_bwd_ranges.argtypes = [vp, ctypes.c_int, ctypes.POINTER(i64), ctypes.c_int, ctypes.POINTER(ctypes.c_int)]
@@ -499,10 +503,23 @@ class Trainer:
         import torch
         return self.workspace[: N * self.K0 * 2].view(torch.bfloat16).view(N, self.K0)
 
-    def dx(self, N):
+    def dx_layout(self):
+        """0: dL/d(enc) row-major [N][K0]; F: level-major [L][N][F] (fh_train_dx_layout)."""
+        return int(_train_lib().fh_train_dx_layout(self._h))
+
+    def dx_raw(self, N):
+        """The dL/d(enc) workspace of an N-sample step as stored (flat f32)."""
         import torch
         off = ((self.max_batch + 7) // 8 * 8 * self.K0 * 2 + 255) // 256 * 256   # encoder rows in whole 8-row groups
-        return self.workspace[off: off + N * self.K0 * 4].view(torch.float32).view(N, self.K0)
+        return self.workspace[off: off + N * self.K0 * 4].view(torch.float32)
+
+    def dx(self, N):
+        """dL/d(enc) as [N][K0] (a permuted copy when stored level-major)."""
+        F = self.dx_layout()
+        raw = self.dx_raw(N)
+        if F > 0:
+            return raw.view(self.K0 // F, N, F).permute(1, 0, 2).reshape(N, self.K0)
+        return raw.view(N, self.K0)
 
     def fwd_bwd(self, coords, target, n_global=None, stream=None):
         N = coords.shape[0]

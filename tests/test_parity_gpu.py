@@ -385,10 +385,19 @@ def test_cfg4_full_size_backward_every_entry():
     enc.bwd(c_d, g_d, dt, overwrite=True)
     assert enc.status_sync() == fh.FH_OK
     got = dt.cpu().numpy()
-    del dt, c_d, g_d
+    # the same gradient from a level-major dout (FH_BWD_DOUT_LEVEL_MAJOR, the
+    # trainer's dL/d(enc) layout for F >= 4)
+    g_lm = g_d.view(W.N_CFG4, cfg.L, cfg.F).permute(1, 0, 2).contiguous()
+    del g_d
+    dt.fill_(float("nan"))
+    enc.bwd(c_d, g_lm, dt, overwrite=True, level_major=True)
+    assert enc.status_sync() == fh.FH_OK
+    got_lm = dt.cpu().numpy()
+    del dt, c_d, g_lm
     G, A = oracle.Levels(cfg.levels, cfg.cap).backward(coords, dout, cfg.F, want_abs=True)
     del dout
     check_bwd(got.astype(np.float64), G, A)
+    check_bwd(got_lm.astype(np.float64), G, A)
 
 
 def test_combustion_fold2_full_size_every_entry():
@@ -786,3 +795,25 @@ def test_few_cell_levels_backward(F):
     assert st == fh.FH_OK
     G, A = ref.backward(case.coords, case.dout, F, want_abs=True)
     check_bwd(got, G, A)
+
+
+@pytest.mark.parametrize("F", [1, 2, 4, 8])
+def test_backward_level_major_dout(F):
+    """FH_BWD_DOUT_LEVEL_MAJOR: dout as [L][N][F] gives the oracle's
+    gradient through every backward path -- the few-cell levels in shared
+    memory, an L2 level group, a capped (hashed) level -- and accumulates
+    (+=) like the row-major form; the overwrite flag combines with it."""
+    levels = [(2, 2, 2, 2), (13, 7, 4, 2), (33, 33, 33, 5), (64, 64, 64, 8)]
+    cfg = W.EncoderConfig("lm", tuple(levels), F=F, cap=1 << 16, table_dtype="f32")
+    N = 60000 + 37
+    case = W.encode_case(cfg, N, seed=45)
+    enc = fh.Encoder(levels, F, "f32", 1 << 16)
+    ref = oracle.Levels(levels, 1 << 16)
+    c = dev(case.coords)
+    g_lm = dev(case.dout).view(N, cfg.L, F).permute(1, 0, 2).contiguous()
+    dt = torch.full((enc.entries, F), float("nan"), device="cuda")
+    enc.bwd(c, g_lm, dt, overwrite=True, level_major=True)
+    enc.bwd(c, g_lm, dt, level_major=True)
+    assert enc.status_sync() == fh.FH_OK
+    G, A = ref.backward(case.coords, case.dout, F, want_abs=True)
+    check_bwd(dt.cpu().numpy().astype(np.float64), 2 * G, 2 * A)

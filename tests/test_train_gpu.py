@@ -95,29 +95,33 @@ def test_mlp_fwd_bwd_ragged_tiles(F, L, N):
     check_fwd_bwd(cfg, tr, coords, target, N)
 
 
-def test_mlp_fwd_bwd_after_a_larger_batch():
+@pytest.mark.parametrize("F,L", [(2, 16), (4, 8)])
+def test_mlp_fwd_bwd_after_a_larger_batch(F, L):
     """A trainer's workspace keeps the previous call's encoder output and dX
     rows past the current N: a small batch after a large one must not read
     them (per-launch tensor maps sized to N), and its dX rows past N are
-    left alone."""
-    cfg = small_cfg(2, 16)
+    left alone (F = 4: the level-major dX, [L][N][F] packed for this N, ends
+    at N K0 floats; nothing past it is written)."""
+    cfg = small_cfg(F, L)
     g = W.rng(77)
     enc = fh.Encoder(cfg.levels, cfg.F, cfg.table_dtype, cfg.cap)
-    tr = fh.Trainer(enc, W.draw_table(g, enc.entries, cfg.F, "f32"), W.draw_mlp(g, W.MLPConfig((32, 64, 64, 1))), 5000)
+    tr = fh.Trainer(enc, W.draw_table(g, enc.entries, cfg.F, "f32"), W.draw_mlp(g, W.MLPConfig((L * F, 64, 64, 1))), 5000)
     big = W.draw_coords(g, 5000)
     tr.fwd_bwd(torch.from_numpy(big).cuda(), torch.from_numpy(g.random(5000, dtype=np.float32)).cuda())
     torch.cuda.synchronize()
-    dx_big = tr.dx(5000).clone()
+    raw_big = tr.dx_raw(5000).clone()
     N = 301
     coords = W.draw_coords(g, N)
     target = g.random(N, dtype=np.float32)
     check_fwd_bwd(cfg, tr, coords, target, N)
     # rows past N (also those inside the last 128-row tile) are clipped by the dX store
-    assert torch.equal(tr.dx(5000)[N:], dx_big[N:])
+    K0 = L * F
+    assert torch.equal(tr.dx_raw(5000)[N * K0:], raw_big[N * K0:])
 
 
 def check_fwd_bwd(cfg, tr, coords, target, N, table_grad=True):
     c, t = torch.from_numpy(coords).cuda(), torch.from_numpy(target).cuda()
+    assert tr.dx_layout() == (cfg.F if cfg.F >= 4 else 0)   # level-major dL/d(enc) for F >= 4
     n_global = N + 17  # exercise the 1/N_global scaling
     loss = tr.fwd_bwd(c, t, n_global)
     assert tr.status() == fh.FH_OK
