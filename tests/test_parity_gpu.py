@@ -8,6 +8,8 @@ Bars (from BASELINE.json north_star and SURVEY.md §8(c)):
   backward    |gpu - oracle| <= 1e-5 * sum |W_c g|; untouched entries exactly 0
   bf16 out    within half a bf16 ulp of the oracle + the forward bound
 """
+import re
+
 import numpy as np
 import pytest
 import torch
@@ -541,19 +543,31 @@ def test_step_host_end_to_end():
     check_bwd(dt_h.numpy().astype(np.float64), G, A)
 
 
-@pytest.mark.parametrize("F", [1, 2])
+@pytest.mark.parametrize("F,lm", [(1, False), (2, False), (2, True), (4, True)])
 @pytest.mark.parametrize("split", ["0", "1"])
-def test_backward_entry_range_passes(split, F, monkeypatch):
+def test_backward_entry_range_passes(split, F, lm, monkeypatch):
     """A level whose gradients exceed the backward group budget is reduced
-    in entry-range passes (FH_BWD_SPLIT, default on for F <= 2): forced with
-    a tiny budget (FH_BWD_GROUP_MB) on cfg1h, results equal the oracle."""
+    in entry-range passes (FH_BWD_SPLIT, default on for F <= 2; F = 4 keeps
+    one pass: cfg4 with a level-major dout and FH_BWD_OVERWRITE, the train
+    step's form, 5.36 ms in one pass vs 5.47 in two): forced with a tiny
+    budget (FH_BWD_GROUP_MB) on cfg1h, results equal the oracle."""
     monkeypatch.setenv("FH_BWD_SPLIT", split)
-    monkeypatch.setenv("FH_BWD_GROUP_MB", "0.02")   # 20 KB: every level alone, the big ones split
+    monkeypatch.setenv("FH_BWD_GROUP_MB", "0.002")   # 2 KB: every level alone, all but level 0 split
+    monkeypatch.setenv("FH_SMALL_MAX_T", "0")        # no level in the shared-memory pass
     cfg = W.EncoderConfig("split", W.CFG1H.levels, F=F, cap=W.CFG1H.cap, table_dtype="f32")
-    case = W.encode_case(cfg, 6000 + 3, seed=17)
+    N = 6000 + 3
+    case = W.encode_case(cfg, N, seed=17)
     enc = fh.Encoder(cfg.levels, cfg.F, cfg.table_dtype, cfg.cap)
     ref = oracle.Levels(cfg.levels, cfg.cap)
-    got, st = run_bwd(enc, case)
+    c, g = dev(case.coords), dev(case.dout)
+    if lm:
+        g = g.view(N, cfg.L, F).permute(1, 0, 2).contiguous()
+    dt = torch.zeros((enc.entries, F), device="cuda")
+    names = kernel_names(lambda: enc.bwd(c, g, dt, level_major=lm))
+    st = enc.status_sync()
+    got = dt.cpu().numpy().astype(np.float64)
+    ranged = any(re.search(r"bwd_kernel<\d+, (true|1)>", n) for n in names)
+    assert ranged == (split == "1" and F <= 2), names
     assert st == fh.FH_OK
     G, A = ref.backward(case.coords, case.dout, cfg.F, want_abs=True)
     check_bwd(got, G, A)

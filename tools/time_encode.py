@@ -36,6 +36,9 @@ def main():
     e = [torch.cuda.Event(enable_timing=True) for _ in range(4)]
     tf = tb = 0.0
     overwrite = os.environ.get("FH_OVERWRITE", "0") == "1"   # bwd overwrites dtable (no separate zero_grad)
+    lm = os.environ.get("FH_LM", "0") == "1"                 # level-major dout (FH_BWD_DOUT_LEVEL_MAJOR)
+    if lm:
+        dout = dout.view(N, cfg.L, cfg.F).permute(1, 0, 2).contiguous()
     for it in range(iters + 3):
         flush.fill_(it & 255)
         if not overwrite:
@@ -43,14 +46,14 @@ def main():
         e[1].record()
         enc.fwd(coords, table, out)
         e[2].record()
-        enc.bwd(coords, dout, dtab, overwrite=overwrite)
+        enc.bwd(coords, dout, dtab, overwrite=overwrite, level_major=lm)
         e[3].record()
         torch.cuda.synchronize()
         if it >= 3:
             tf += e[1].elapsed_time(e[2])
             tb += e[2].elapsed_time(e[3])
     tot = (tf + tb) / iters
-    print(f"{os.path.basename(fh.LIB_PATH)} {name} lin={enc.lin}: "
+    print(f"{os.path.basename(fh.LIB_PATH)} {name} lin={enc.lin} lm={int(lm)}: "
           f"fwd {tf / iters:.4f} ms  bwd {tb / iters:.4f} ms  ({N / (tot / 1e3) / 1e6:.1f} M samples/s)")
 
 
