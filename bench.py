@@ -522,7 +522,21 @@ def hbm_regime_bench(fh, torch, W, steps, hbm_peak):
             tf += e[0].elapsed_time(e[1])
             tb += e[1].elapsed_time(e[2])
     fwd_ms, bwd_ms = tf / steps, tb / steps
-    del out, dout, flush
+    # the same backward from a level-major dout ([L][N][F], FH_BWD_DOUT_LEVEL_MAJOR:
+    # the train step's dL/d(enc) layout for F >= 4)
+    dout_lm = dout.view(N, cfg.L, cfg.F).permute(1, 0, 2).contiguous()
+    del dout
+    tl = 0.0
+    for it in range(steps + 2):
+        flush.fill_(it & 255)
+        e[1].record()
+        enc.bwd(coords, dout_lm, dt, overwrite=True, level_major=True)
+        e[2].record()
+        torch.cuda.synchronize()
+        if it >= 2:
+            tl += e[1].elapsed_time(e[2])
+    bwd_lm_ms = tl / steps
+    del out, dout_lm, flush
     LF = cfg.L * cfg.F
     # compulsory HBM bytes of one pass: the table (fwd) or the fp32 grads
     # (bwd: read + written) once, plus the streamed coordinates and encodings /
@@ -534,6 +548,7 @@ def hbm_regime_bench(fh, torch, W, steps, hbm_peak):
     out = {"workload": "cfg4 encoder (BASELINE.json configs[3]): 2^22 points, L=16, F=4 fp16 tables cap 2^22 "
                        "(305 MiB) + fp32 grads (609 MiB); fwd (bf16 out) + bwd, L2 flushed",
            "fwd_ms": fwd_ms, "bwd_ms": bwd_ms, "samples_per_s": N / ((fwd_ms + bwd_ms) / 1e3),
+           "bwd_ms_level_major_dout": bwd_lm_ms,
            "compulsory_hbm_bytes": {"fwd": hbm_fwd, "bwd": hbm_bwd},
            "hbm_frac_fwd": hbm_fwd / bw / (fwd_ms / 1e3), "hbm_frac_bwd": hbm_bwd / bw / (bwd_ms / 1e3),
            "note": "compulsory bytes / time / measured HBM peak: the lower bound of the DRAM traffic, so <= 1; the "
