@@ -555,6 +555,9 @@ def hbm_regime_bench(fh, torch, W, steps, hbm_peak):
                    "passes are bound by L2 request / atomic throughput (see ncu)"}
     if ncu:
         out["ncu"] = ncu
+    ncu_lm = load_ncu_summary().get("cfg4_lm", {})
+    if ncu_lm:
+        out["ncu_level_major_dout"] = ncu_lm
     return out
 
 

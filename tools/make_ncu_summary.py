@@ -69,8 +69,14 @@ def main():
                       "fh_encode_bwd_ex of the last captured step.  *_frac = time-weighted fraction of the unit's "
                       "peak (lts__throughput, l1tex2xbar request port, L2 red-sector rate, atomic input).  Cold "
                       "cache, serialised launches: shares, not absolute times, match the bench."}
+    path = os.path.join(ROOT, "profiles", "ncu_summary.json")
+    if os.path.exists(path):   # merge: entries of earlier captures stay unless re-captured
+        prev = json.load(open(path))
+        prev.update({k: v for k, v in out.items()})
+        out = prev
     for p in sys.argv[1:]:
-        name = "cfg4" if "cfg4" in p else "cfg2"
+        # cfg4lm: the cfg4 step in the train step's form (level-major dout, tools/gpu_prof_r02d.sh)
+        name = "cfg4_lm" if "cfg4lm" in p else "cfg4" if "cfg4" in p else "cfg2"
         fwd, bwd = last_step(launches(p))
         f, b = summarise(fwd), summarise(bwd)
         out[name] = {"source": "profiles/" + os.path.basename(p).replace("_raw.csv", ".txt"), "fwd": f, "bwd": b,
@@ -79,7 +85,7 @@ def main():
                      "l1tex2xbar_req_frac": {"fwd": f["l1tex2xbar_req_frac"], "bwd": b["l1tex2xbar_req_frac"]},
                      "l2_red_sectors_per_pass": b["l2_red_sectors"],
                      "l2_hit_frac": {"fwd": f["l2_hit_frac"], "bwd": b["l2_hit_frac"]}}
-    with open(os.path.join(ROOT, "profiles", "ncu_summary.json"), "w") as fo:
+    with open(path, "w") as fo:
         json.dump(out, fo, indent=1)
     print(json.dumps(out, indent=1))
 
