@@ -833,6 +833,8 @@ static fh_status encode_bwd_impl(fh_encoder e, const float *coords, int64_t N,
     if (st != FH_OK) return st;
     const size_t vec = (size_t)e->F * 4;
     if (!dtable || !aligned(dtable, vec > 16 ? 16 : vec)) return fail(FH_E_ARG, "fh_encode_bwd: NULL/misaligned dtable");
+    if (level_major && e->kind == 1)
+        return fail(FH_E_ARG, "fh_encode_bwd: level-major dout is not supported by the MHE encoder");
     cudaStream_t s = reinterpret_cast<cudaStream_t>(stream);
     // zero: dtable is overwritten -- zeroed range by range right before the
     // launch that reduces into it, so the zero lines are still in L2 when the
@@ -845,8 +847,6 @@ static fh_status encode_bwd_impl(fh_encoder e, const float *coords, int64_t N,
     if (!dout || !aligned(dout, vec > 16 ? 16 : vec)) return fail(FH_E_ARG, "fh_encode_bwd: NULL/misaligned dout");
     if ((st = device_ready(e)) != FH_OK) return st;
     const float4 *c4 = reinterpret_cast<const float4 *>(coords);
-    if (level_major && e->kind == 1)
-        return fail(FH_E_ARG, "fh_encode_bwd: level-major dout is not supported by the MHE encoder");
     const int64_t LF = (int64_t)e->L * e->F;
     const fh::DoutLayout dl = level_major ? fh::DoutLayout{e->F, N * e->F} : fh::DoutLayout{LF, e->F};
     const BwdCall b{e, c4, N, dout, dl, dtable, s};

@@ -128,6 +128,15 @@ def test_encode_argument_errors_are_host_side():
     # fh_encode_bwd_ex: unknown flags, misaligned dout
     assert L.fh_encode_bwd_ex(enc.handle, 16, 10, 16, 16, 0x80, None) == fh.FH_E_ARG
     assert L.fh_encode_bwd_ex(enc.handle, 16, 10, 4, 16, 1, None) == fh.FH_E_ARG
+    # FH_BWD_DOUT_LEVEL_MAJOR: accepted by F-Hash encoders (the call then fails
+    # only on the missing device here), rejected host-side by the MHE baseline
+    lm = 2
+    assert L.fh_encode_bwd_ex(enc.handle, 16, 10, 16, 16, lm | 1, None) != fh.FH_E_ARG
+    mhe = fh.MHEEncoder([4, 8, 12, 16], 2, 1 << 10, 5)
+    assert L.fh_encode_bwd_ex(mhe.handle, 16, 10, 16, 16, lm, None) == fh.FH_E_ARG
+    assert b"MHE" in L.fh_last_error()
+    # the trainer's dL/d(enc) layout query: NULL trainer -> -1
+    assert fh._train_lib().fh_train_dx_layout(None) == -1
     # fh_level_stats: NULL pointers, level out of range, workspace query
     assert L.fh_level_stats(enc.handle, 0, None, 0, None, None) == fh.FH_E_ARG
     assert L.fh_level_stats(enc.handle, 99, 256, 1 << 20, 256, None) == fh.FH_E_ARG
