@@ -84,7 +84,7 @@ def test_train_fwd_bwd_cfg5_shape_multi_tile():
     check_fwd_bwd(cfg, tr, coords, target, N)
 
 
-@pytest.mark.parametrize("F,L,N", [(2, 16, 1), (4, 16, 129), (2, 8, 255), (4, 4, 7)])
+@pytest.mark.parametrize("F,L,N", [(2, 16, 1), (4, 16, 129), (2, 8, 255), (4, 4, 7), (4, 16, 1), (4, 8, 8)])
 def test_mlp_fwd_bwd_ragged_tiles(F, L, N):
     """Tile edges of the TMA paths: one sample, one full tile + one row, a
     tile short of one row, fewer rows than one 8-row group (the X tensor map
