@@ -151,7 +151,8 @@ __global__ void __launch_bounds__(256) bwd_kernel(const __grid_constant__ Params
                                                   int *__restrict__ flag, const __grid_constant__ LevelList LL,
                                                   uint32_t lo = 0,
                                                   uint32_t span = 0, uint32_t rep_n = 0, int64_t rep_stride = 0,
-                                                  const MergeJob mj = MergeJob{nullptr, 0, 0, 0}) {
+                                                  const MergeJob mj = MergeJob{nullptr, 0, 0, 0},
+                                                  const RepSpec rs = RepSpec{0, {}, {}, {}, {}}) {
     if ((int)blockIdx.x < mj.ctas) {   // the previous group's merge (see MergeJob)
         merge_shift_range(dtable, mj.gsh, mj.m0, mj.m1, (int64_t)blockIdx.x * blockDim.x + threadIdx.x,
                           (int64_t)mj.ctas * blockDim.x);
@@ -191,6 +192,10 @@ __global__ void __launch_bounds__(256) bwd_kernel(const __grid_constant__ Params
     }
     const float wx[2] = {__fsub_rn(1.0f, c.w[0]), c.w[0]}, wy[2] = {__fsub_rn(1.0f, c.w[1]), c.w[1]};
     const float wz[2] = {__fsub_rn(1.0f, c.w[2]), c.w[2]}, wt[2] = {__fsub_rn(1.0f, c.w[3]), c.w[3]};
+    float *dt = dtable;   // or this CTA's replicated copy of a contended level (RepSpec)
+#pragma unroll
+    for (int q = 0; q < kMaxInRep; q++)   // constant indices: the spec stays in parameter space
+        if (q < rs.n && l == rs.lvl[q]) dt = rs.base[q] + (int64_t)((uint32_t)bid % (uint32_t)rs.R[q]) * rs.stride[q];
 #pragma unroll
     for (int k = 0; k < 16; k += 2) {
         const float Wyzt = wy[(k >> 1) & 1] * wz[(k >> 2) & 1] * wt[(k >> 3) & 1];
@@ -201,13 +206,13 @@ __global__ void __launch_bounds__(256) bwd_kernel(const __grid_constant__ Params
         if constexpr (RANGED) {
             const bool in0 = c.idx[k] - lo < span, in1 = c.idx[k + 1] - lo < span;
             if (in0 && in1) {
-                red_pair<F>(dtable, gsh, c.idx[k], c.idx[k + 1], v0, v1);
+                red_pair<F>(dt, gsh, c.idx[k], c.idx[k + 1], v0, v1);
             } else {
-                if (in0) red_entry<F>(dtable, c.idx[k], v0);
-                if (in1) red_entry<F>(dtable, c.idx[k + 1], v1);
+                if (in0) red_entry<F>(dt, c.idx[k], v0);
+                if (in1) red_entry<F>(dt, c.idx[k + 1], v1);
             }
         } else {
-            red_pair<F>(dtable, gsh, c.idx[k], c.idx[k + 1], v0, v1);
+            red_pair<F>(dt, gsh, c.idx[k], c.idx[k + 1], v0, v1);
         }
     }
 }

@@ -58,4 +58,19 @@ struct DoutLayout {
     int64_t ns, ls;
 };
 
+// In-pass replicated copies (F >= 4): the contended coarse levels of a
+// level-group launch reduce into R copies in the scratch (CTA b -> copy
+// b % R) instead of dtable, so same-address reductions, which serialise in
+// the L2, spread over R addresses; rep_reduce_kernel adds the copies into
+// dtable after the launch.  base[q] is the copies' start minus the level's
+// entry offset times F, so base[q] + idx * F addresses copy 0 directly.
+constexpr int kMaxInRep = 4;
+struct RepSpec {
+    int n;
+    int lvl[kMaxInRep];
+    int R[kMaxInRep];
+    float *base[kMaxInRep];
+    int64_t stride[kMaxInRep];   // floats between copies
+};
+
 }  // namespace fh

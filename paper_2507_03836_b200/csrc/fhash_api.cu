@@ -215,6 +215,16 @@ static fh_status bind_device(fh_encoder e) {
         for (int q = 0; q < e->L; q++)
             e->rep[q] = e->kind == 0 && e->F == 2 && (e->pair_shift & 1) && !small[q] &&
                         e->info[q].table_size <= rep_max;
+        // F >= 4: the contended coarse levels (at most FH_INREP_MAX_T
+        // entries) reduce into in-pass replicated copies (RepSpec; the number
+        // of copies is decided per call from the updates per entry).
+        // Measured on cfg4 (2^22 samples; levels 0-2: 8192 / 21660 / 41262
+        // entries, 8192 / 3098 / 1626 updates each, 8 / 4 / 2 copies): bwd
+        // 5.37 -> 5.10 ms in the train step's form.
+        const char *iv = getenv("FH_INREP_MAX_T");
+        const uint64_t inrep_max = iv ? (uint64_t)atoll(iv) : (uint64_t)1 << 18;
+        for (int q = 0; q < e->L; q++)
+            e->inrep[q] = e->kind == 0 && e->F >= 4 && !small[q] && e->info[q].table_size <= inrep_max;
         e->n_gb = 0;
         int l = 0;
         while (l < e->L) {
@@ -599,6 +609,18 @@ unsigned long long fh_kernel_launches(void) { return fh::g_launches.load(std::me
 static constexpr size_t kGshSlack = (size_t)32 << 20;
 static constexpr size_t kGshRel = (size_t)2 << 20;
 
+// In-pass replicated copies (RepSpec): each copy the level's T F floats
+// rounded up to 64 floats (256-byte aligned copies); at most kInRepMax
+// copies and at most 2^20 entries over all copies of a level.
+static constexpr int kInRepMax = 32;
+static size_t inrep_stride(fh_encoder e, int l) {
+    return ((size_t)e->info[l].table_size * e->F + 63) / 64 * 64;
+}
+static int inrep_rmax(fh_encoder e, int l) {
+    const uint64_t r = ((uint64_t)1 << 20) / (e->info[l].table_size ? e->info[l].table_size : 1);
+    return r >= (uint64_t)kInRepMax ? kInRepMax : r < 2 ? 2 : (int)r;
+}
+
 static size_t scratch_parts(fh_encoder e, size_t *tsh_bytes, size_t *gsh_bytes) {
     const size_t kEb = (size_t)e->F * dtype_size(e->table_dtype);
     uint64_t tend = 0, gend = 0;
@@ -613,6 +635,12 @@ static size_t scratch_parts(fh_encoder e, size_t *tsh_bytes, size_t *gsh_bytes) 
             const size_t stride = (size_t)((I.table_size + 2) * e->F + 3) / 4 * 4;
             if (64 * stride * 4 > g) g = 64 * stride * 4;
         }
+    }
+    {   // in-pass replicated copies (F >= 4): kInRepMax copies of every such level
+        size_t ib = 0;
+        for (int l = 0; l < e->L; l++)
+            if (e->inrep[l]) ib += inrep_rmax(e, l) * inrep_stride(e, l) * 4;
+        if (ib > g) g = ib;
     }
     if (gend > 0 && (size_t)gend * e->F * 4 + 64 > g) g = (size_t)gend * e->F * 4 + 64;
     if (g) g += kGshSlack;   // room to place the scratch at a chosen offset from dtable (place_gsh)
@@ -726,12 +754,13 @@ struct BwdCall {
 // bwd_kernel<F, RANGED> for the encoder's F (gsh only for F <= 2).
 static void launch_bwd_kernel(const BwdCall &b, dim3 g, const fh::LevelList &ll, float *dt, float *gsh, bool ranged,
                               uint32_t lo = 0, uint32_t span = 0, uint32_t rep_n = 0, int64_t rep_stride = 0,
-                              fh::MergeJob mj = fh::MergeJob{nullptr, 0, 0, 0}) {
+                              fh::MergeJob mj = fh::MergeJob{nullptr, 0, 0, 0},
+                              const fh::RepSpec &rs = fh::RepSpec{0, {}, {}, {}, {}}) {
     const fh_encoder e = b.e;
     g.x += (unsigned)mj.ctas;   // the merge CTAs come first (blockIdx < mj.ctas)
 #define FH_BWD(FF, RR, GG)                                                                                     \
     { fh::bwd_kernel<FF, RR><<<g, 256, 0, b.s>>>(e->params, b.c4, b.N, b.dout, b.dl, dt, GG, e->flag, ll, lo, span, \
-                                                 rep_n, rep_stride, mj); fh::count_launch(); }
+                                                 rep_n, rep_stride, mj, rs); fh::count_launch(); }
     switch (e->F) {
         case 1: if (ranged) FH_BWD(1, true, gsh) else FH_BWD(1, false, gsh) break;
         case 2: if (ranged) FH_BWD(2, true, gsh) else FH_BWD(2, false, gsh) break;
@@ -774,7 +803,7 @@ static fh_status bwd_small_levels(const BwdCall &b) {
 // replicated level.  nullptr when no level needs it or no slot is free.
 static float *bwd_scratch(fh_encoder e, cudaStream_t s, const float *dtable, size_t *bytes) {
     bool any = false;
-    for (int l = 0; l < e->L; l++) any |= e->shiftable[l] || e->rep[l];
+    for (int l = 0; l < e->L; l++) any |= e->shiftable[l] || e->rep[l] || e->inrep[l];
     if (!any) return nullptr;
     uint64_t end = 0;
     size_t need = 64;
@@ -787,6 +816,12 @@ static float *bwd_scratch(fh_encoder e, cudaStream_t s, const float *dtable, siz
         }
     }
     if ((size_t)end * e->F * 4 + 64 > need) need = (size_t)end * e->F * 4 + 64;
+    {
+        size_t ib = 0;
+        for (int l = 0; l < e->L; l++)
+            if (e->inrep[l]) ib += inrep_rmax(e, l) * inrep_stride(e, l) * 4;
+        if (ib > need) need = ib;
+    }
     fh_encoder_s::Scratch *sc = get_scratch(e, s, 0, need + kGshSlack);
     if (!sc) return nullptr;
     // place_gsh: (scratch - dtable) mod kGshSlack = the chosen offset
@@ -940,6 +975,35 @@ static fh_status encode_bwd_impl(fh_encoder e, const float *coords, int64_t N,
             record(k);
             continue;
         }
+        // contended levels of this group into in-pass replicated copies
+        // (F >= 4; for u updates per entry, R = u / FH_INREP_UPDATES (1024)
+        // rounded up to a power of two, 2 <= R <= inrep_rmax; measured on
+        // cfg4: 512 / 1024 / 2048 updates per copy 5.10 / 5.10 / 5.17 ms)
+        fh::RepSpec rs{0, {}, {}, {}, {}};
+        if (scratch && !gsh) {
+            static const double per_copy = getenv("FH_INREP_UPDATES") ? atof(getenv("FH_INREP_UPDATES")) : 1024.0;
+            size_t used = 0;
+            for (int i = 0; i < lc && rs.n < fh::kMaxInRep; i++) {
+                const int l = l0 + i;
+                if (!e->inrep[l]) continue;
+                const double u = (double)N * 16.0 / (double)e->info[l].table_size;
+                int R = 1;
+                while (R < kInRepMax && R * per_copy < u) R *= 2;
+                if (R > inrep_rmax(e, l)) R = inrep_rmax(e, l);
+                if (R < 2) continue;
+                const size_t stride = inrep_stride(e, l);
+                if ((used + R * stride) * 4 > scratch_bytes) break;
+                float *copies = scratch + used;
+                if ((st = cuda_check(cudaMemsetAsync(copies, 0, R * stride * 4, s), "zero replicas")) != FH_OK)
+                    return st;
+                rs.lvl[rs.n] = l;
+                rs.R[rs.n] = R;
+                rs.base[rs.n] = copies - (int64_t)e->info[l].offset * e->F;
+                rs.stride[rs.n] = (int64_t)stride;
+                rs.n++;
+                used += R * stride;
+            }
+        }
         fh::MergeJob mj{nullptr, 0, 0, 0};
         if (pend.on && e->fuse_merge) {
             const int64_t blocks = merge_blocks(pend.m0, pend.m1);
@@ -947,7 +1011,16 @@ static fh_status encode_bwd_impl(fh_encoder e, const float *coords, int64_t N,
         } else {
             flush();
         }
-        launch_bwd_kernel(b, g, ll, dtable, gsh, false, 0, 0, 0, 0, mj);
+        launch_bwd_kernel(b, g, ll, dtable, gsh, false, 0, 0, 0, 0, mj, rs);
+        for (int q = 0; q < rs.n; q++) {   // dtable += the sum of the level's copies
+            const int l = rs.lvl[q];
+            const int64_t cnt = (int64_t)e->info[l].table_size * e->F;
+            int64_t blocks = (cnt + 255) / 256;
+            if (blocks > (int64_t)e->n_sm * 4) blocks = (int64_t)e->n_sm * 4;
+            { fh::rep_reduce_kernel<<<(unsigned)blocks, 256, 0, s>>>(dtable + (int64_t)e->info[l].offset * e->F,
+                                                                     rs.base[q] + (int64_t)e->info[l].offset * e->F,
+                                                                     rs.R[q], rs.stride[q], cnt); fh::count_launch(); }
+        }
         if (mj.ctas > 0) {
             record(pend.k);
             pend.on = false;

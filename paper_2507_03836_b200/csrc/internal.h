@@ -69,6 +69,7 @@ struct fh_encoder_s {
     SmallPlan small_plan[FH_MAX_LEVELS + 1];         // launch shape of each few-cell launch (plan_small)
     bool small_warp_copies = true;                   // FH_SMALL_WARP=0: one CTA copy instead of per-warp copies
     bool rep[FH_MAX_LEVELS] = {false};               // backward: level reduced into replicated copies (own pass)
+    bool inrep[FH_MAX_LEVELS] = {false};             // backward, F >= 4: contended level into in-pass replicated copies
     bool fuse_merge = true;                          // FH_FUSE_MERGE=0: every group's merge as its own launch
     double fwd_limit = 0.0, bwd_limit = 0.0;         // L2 budgets of one direct pass (bytes; 0 = one pass)
     int n_sm = 148;                                  // SMs of the device (set with the status word)

@@ -831,3 +831,28 @@ def test_backward_level_major_dout(F):
     assert enc.status_sync() == fh.FH_OK
     G, A = ref.backward(case.coords, case.dout, F, want_abs=True)
     check_bwd(dt.cpu().numpy().astype(np.float64), 2 * G, 2 * A)
+
+
+@pytest.mark.parametrize("F", [4, 8])
+@pytest.mark.parametrize("attach", [True, False])
+def test_backward_inpass_replicas(F, attach):
+    """F >= 4: a contended level (6561 entries, ~2560 updates each at 2^20
+    samples) reduces into in-pass replicated copies of the scratch (CTA b ->
+    copy b % R, then rep_reduce_kernel adds them into dtable); equal to the
+    oracle on every entry, accumulating (+=) like the direct form.  Without
+    a scratch attached the same call runs without copies, same result."""
+    levels = [(9, 9, 9, 9), (16, 16, 16, 16), (33, 33, 33, 5)]
+    cfg = W.EncoderConfig("inrep", tuple(levels), F=F, cap=0, table_dtype="f32")
+    N = (1 << 20) + 5
+    case = W.encode_case(cfg, N, seed=46)
+    enc = fh.Encoder(levels, F, "f32", 0, auto_scratch=attach)
+    ref = oracle.Levels(levels)
+    c, g = dev(case.coords), dev(case.dout)
+    g_lm = g.view(N, cfg.L, F).permute(1, 0, 2).contiguous()
+    dt = torch.full((enc.entries, F), float("nan"), device="cuda")
+    names = kernel_names(lambda: enc.bwd(c, g_lm, dt, overwrite=True, level_major=True))
+    assert any("rep_reduce_kernel" in n for n in names) == attach, names
+    enc.bwd(c, g, dt)
+    assert enc.status_sync() == fh.FH_OK
+    G, A = ref.backward(case.coords, case.dout, F, want_abs=True)
+    check_bwd(dt.cpu().numpy().astype(np.float64), 2 * G, 2 * A)
