@@ -499,7 +499,10 @@ fh_status fh_level_stats(fh_encoder enc, int level, void *workspace, size_t work
  * fh_encoder_scratch_size(enc) bytes (device, 256-byte aligned; covers every
  * pass of this encoder: the table copy up to the last level the forward may
  * shift, the fp32 gradient scratch of the shiftable backward levels or the
- * 64 replicated copies of a replicated level).  No initial contents are
+ * 64 replicated copies of a replicated level, and for F >= 4 the in-pass
+ * replicated copies of the contended coarse levels -- up to 32 copies, at
+ * most 2^20 entries, per level of at most 2^18 entries; a backward on a
+ * stream without scratch runs without them, same result).  No initial contents are
  * needed: each range is written or zeroed right before use.  The library
  * never allocates, grows or frees it; ptr = NULL detaches (after
  * synchronising `stream`: attach is set-up, not stream-ordered).  Size 0 /
