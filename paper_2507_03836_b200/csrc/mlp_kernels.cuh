@@ -128,6 +128,7 @@ struct TrainArgs {
     int64_t N;
     float inv_n_global;
     int dx_lm_log2;              // 0: dx row-major [N][K0]; 2 / 3: level-major [L][N][F], F = 4 / 8
+    int dx_direct;               // level-major only: dX stored from registers (no staging), MMA5 overlapping
 };
 
 // Write 8 bf16 (16 B) = one core-matrix row segment.
@@ -268,6 +269,7 @@ __global__ void __launch_bounds__(TRAIN_THREADS, 1) mlp_train_kernel(const Train
     const uint32_t lane_off = (uint32_t)((ws & 3) * 32) << 16;
     uint64_t *mbar = &bar[slot];
     const bool issuer = (ts == 0);
+    const bool direct = a.dx_direct != 0 && a.dx_lm_log2 != 0;
     const int hc0 = hf * HC;             // this thread's first hidden column
 
     const uint32_t aH1 = tc::smem_u32(sH1), aDZ = tc::smem_u32(sDZ), aDY = tc::smem_u32(sDY);
@@ -453,6 +455,10 @@ __global__ void __launch_bounds__(TRAIN_THREADS, 1) mlp_train_kernel(const Train
             for (int s = 0; s < H / 16; s++)
                 tc::mma_bf16_ta(tm + Lo::T_ACC, tm + Lo::T_A + 8 * s, tc::sdesc(aW1 + s * 2 * Lo::SBO_W1, Lo::SBO_W1, 128),
                                 id_dx, s > 0);
+            // direct dX (level-major): epilogue 4 needs only MMA4; MMA5 runs
+            // under it, its completion covered by the next commit (the next
+            // tile's MMA1, or the one after the loop)
+            if (direct) tc::commit(mbar);
 #pragma unroll
             for (int s = 0; s < TILE / 16; s++)
             {
@@ -461,7 +467,7 @@ __global__ void __launch_bounds__(TRAIN_THREADS, 1) mlp_train_kernel(const Train
                 tc::mma_bf16(tm + Lo::T_DW, ad, tc::sdesc(aH1 + s * 2 * Lo::SBO_H1, Lo::SBO_H1, 128), id_dw, acc);
                 tc::mma_bf16(tm + Lo::T_DW + Lo::WH1, ad, tc::sdesc(aX + s * 2 * Lo::SBO_X, Lo::SBO_X, 128), id_dwx, acc);
             }
-            tc::commit(mbar);
+            if (!direct) tc::commit(mbar);
         }
         tc::mbar_wait(mbar, phase); phase ^= 1;
         tc::fence_after_sync();
@@ -476,7 +482,23 @@ __global__ void __launch_bounds__(TRAIN_THREADS, 1) mlp_train_kernel(const Train
         // stores (half sectors, lg_throttle); a shared staging tile stored by
         // the threads with coalesced STGs (~1.2 us of the per-tile chain);
         // 32-byte st.global.v8 per row segment (slower).
-        {
+        if (direct) {
+            // level-major dX (F = 2^fl >= 4) straight from registers: a warp's
+            // store of one level covers 32 consecutive rows = 32 x 4 F
+            // contiguous bytes (whole lines); the [dZ2 | dZ1] tile stays
+            // untouched for MMA5, which runs meanwhile
+            float v[XC];
+            tmem_ld_cols<XC>(tm + lane_off + Lo::T_ACC + hf * XC, v);
+            const int fl = a.dx_lm_log2;
+            if (valid) {
+#pragma unroll
+                for (int j = 0; j < XC; j += 4) {
+                    const int col = hf * XC + j;
+                    float *p = a.dx + ((((int64_t)(col >> fl) * a.N + row) << fl) + (col & ((1 << fl) - 1)));
+                    __stcs(reinterpret_cast<float4 *>(p), make_float4(v[j], v[j + 1], v[j + 2], v[j + 3]));
+                }
+            }
+        } else {
             float v[XC];
             tmem_ld_cols<XC>(tm + lane_off + Lo::T_ACC + hf * XC, v);
             {   // rows past N (ragged last tile) are clipped by the TMA
@@ -518,6 +540,11 @@ __global__ void __launch_bounds__(TRAIN_THREADS, 1) mlp_train_kernel(const Train
     }
 
     if (issuer) asm volatile("cp.async.bulk.wait_group 0;" ::: "memory");   // the last dX stores are done
+    if (direct && my_tiles > 0) {   // the last tile's MMA5 (slot-uniform)
+        if (issuer) tc::commit(mbar);
+        tc::mbar_wait(mbar, phase); phase ^= 1;
+        tc::fence_after_sync();
+    }
 
     // ---- weight gradients out of TMEM: rows 0..63 -> dW2, db2; 64..127 -> dW1, db1,
     // written (not atomically added) into this slot's row of the partial

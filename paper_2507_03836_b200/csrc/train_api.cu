@@ -180,6 +180,11 @@ fh_status launch_mlp(fh_trainer tr, const float *target, int64_t N, int64_t N_gl
     a.N = N;
     a.inv_n_global = (float)(1.0 / (double)N_global);
     a.dx_lm_log2 = tr->dx_lm == 8 ? 3 : tr->dx_lm == 4 ? 2 : 0;
+    // level-major dX straight from registers, MMA5 overlapping that epilogue
+    // (ncu, cfg4 2^22: 527 us per launch vs 585 through the staging tile and
+    // 3-D TMA stores; FH_DX_STAGE=1 keeps the staged form, for A/B)
+    static const bool stage = getenv("FH_DX_STAGE") != nullptr;
+    a.dx_direct = stage ? 0 : 1;
     const int64_t tiles = (N + fh::mlp::TILE - 1) / fh::mlp::TILE;
     const int64_t pairs = (tiles + 1) / 2;  // two tile slots per CTA
     const int grid = (int)(pairs < tr->n_sm ? pairs : tr->n_sm);
