@@ -636,7 +636,7 @@ static size_t scratch_parts(fh_encoder e, size_t *tsh_bytes, size_t *gsh_bytes) 
             if (64 * stride * 4 > g) g = 64 * stride * 4;
         }
     }
-    {   // in-pass replicated copies (F >= 4): kInRepMax copies of every such level
+    {   // in-pass replicated copies (F >= 4): up to inrep_rmax copies of every such level
         size_t ib = 0;
         for (int l = 0; l < e->L; l++)
             if (e->inrep[l]) ib += inrep_rmax(e, l) * inrep_stride(e, l) * 4;
